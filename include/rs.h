@@ -1,0 +1,293 @@
+/*
+ * rs.h — C-ABI of the B200-native planning core (librs_b200.so).
+ *
+ * This is the drop-in boundary for the data-parallel hot path of the
+ * RLHFless `rollsim` library (reference: /root/reference/proj). Every entry
+ * point below replaces one reference function; the cited file:line is the
+ * interface it stands in for. Signatures use plain pointers and sizes only.
+ *
+ * Conventions
+ *  - Every function returns an rs_status. On failure a message is available
+ *    from rs_last_error() (thread-local). RS_E_VALIDATION / RS_E_CONFIG map
+ *    1:1 onto rollsim::ValidationError / rollsim::ConfigError
+ *    (proj/include/rollsim/errors.hpp:17-32) and are raised in the same
+ *    order as the reference raises them.
+ *  - Host-pointer entry points are synchronous: inputs are copied to HBM,
+ *    the kernels run on the context stream, results are copied back and the
+ *    stream is synchronised before return. `*_device` entry points take
+ *    device pointers and are asynchronous on the context stream.
+ *  - Caller owns every buffer it passes. Opaque handles are freed with the
+ *    matching *_free / *_destroy call.
+ *  - There is no CPU fallback: without a usable CUDA device every compute
+ *    entry point fails with RS_E_CUDA.
+ */
+#ifndef RS_H_
+#define RS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_ABI_VERSION 1
+
+typedef enum rs_status {
+  RS_OK = 0,
+  RS_E_VALIDATION = 1, /* rollsim::ValidationError */
+  RS_E_CONFIG = 2,     /* rollsim::ConfigError */
+  RS_E_CUDA = 3,       /* CUDA runtime / launch failure, or no device */
+  RS_E_NOMEM = 4,      /* device or pinned allocation failed */
+  RS_E_ARG = 5         /* NULL handle / pointer misuse (programming error) */
+} rs_status;
+
+const char* rs_last_error(void);
+int rs_abi_version(void);
+
+/* ------------------------------------------------------------------ */
+/* Context: one per device (and per host thread that drives it).       */
+/* Owns the stream, a grow-only scratch arena and per-profile tables.  */
+/* ------------------------------------------------------------------ */
+typedef struct rs_ctx rs_ctx;
+
+int rs_ctx_create(int device, rs_ctx** out);
+int rs_ctx_destroy(rs_ctx* ctx);
+/* Use a caller stream (e.g. torch.cuda.current_stream().cuda_stream). NULL
+ * restores the context's own stream. */
+int rs_ctx_set_stream(rs_ctx* ctx, void* cuda_stream);
+int rs_ctx_synchronize(rs_ctx* ctx);
+/* Number of kernels this context has launched since creation. */
+int rs_ctx_kernel_launches(const rs_ctx* ctx, uint64_t* count);
+/* Per-kernel timing: when enabled, every launch of a named kernel is
+ * bracketed by CUDA events on the launching stream; rs_ctx_kernel_time
+ * returns the summed milliseconds and launch count since the last reset. */
+int rs_ctx_enable_kernel_timing(rs_ctx* ctx, int enable);
+int rs_ctx_reset_kernel_timing(rs_ctx* ctx);
+int rs_ctx_kernel_time(rs_ctx* ctx, const char* kernel_name, double* total_ms,
+                       uint64_t* launches);
+
+/* ------------------------------------------------------------------ */
+/* Latency profile (proj/include/rollsim/profile.hpp:17-35).          */
+/* ------------------------------------------------------------------ */
+typedef struct rs_profile {
+  const double* batch_knots;   /* nb, strictly increasing */
+  int32_t nb;
+  const double* context_knots; /* nc, strictly increasing */
+  int32_t nc;
+  const double* tpot_grid;     /* nb*nc row-major: [batch][context] */
+  double rho;                  /* dollars per GPU-second */
+} rs_profile;
+
+/* LatencyProfile::tpot_seconds (proj/src/profile.cpp:43-59) evaluated on
+ * the device for n (batch, context) points. Bit-identical to the reference. */
+int rs_tpot_seconds(rs_ctx* ctx, const rs_profile* profile, const double* batch,
+                    const double* context, int64_t n, double* out);
+
+/* ------------------------------------------------------------------ */
+/* (1) Shared-prefix dedup (proj/include/rollsim/dedup.hpp:20-78).     */
+/* Prompts are CSR: tokens[offsets[i] .. offsets[i+1]) is prompt i.    */
+/* ------------------------------------------------------------------ */
+typedef struct rs_prefix_index rs_prefix_index;
+
+/* PrefixIndex::build (proj/include/rollsim/dedup.hpp:22,
+ * proj/src/dedup.cpp:30-100). Host CSR in, index handle out. */
+int rs_prefix_index_build(rs_ctx* ctx, const int32_t* tokens,
+                          const int64_t* offsets, int32_t batch,
+                          rs_prefix_index** out);
+/* Same with the CSR already resident in HBM (device pointers). */
+int rs_prefix_index_build_device(rs_ctx* ctx, const int32_t* d_tokens,
+                                 const int64_t* d_offsets, int32_t batch,
+                                 rs_prefix_index** out);
+/* Device-resident outputs for benchmarking: no host copies of the CSR or the
+ * tables (the refinement rounds still read one counter per round). The five
+ * tables land in d_tables (5 consecutive int64 arrays of max_len_cap+2
+ * entries: nodes_at_depth, short_count_below, short_tokens_below,
+ * longer_count_from, longer_tokens_from) and d_info receives
+ * {batch, min_len, max_len, total_tokens, status}. max_len_cap must be >=
+ * the longest prompt; status != 0 flags a validation failure. */
+int rs_prefix_index_build_device_async(rs_ctx* ctx, const int32_t* d_tokens,
+                                       const int64_t* d_offsets, int32_t batch,
+                                       int32_t max_len_cap, int64_t* d_tables,
+                                       int64_t* d_info);
+void rs_prefix_index_free(rs_prefix_index* idx);
+
+/* Accessors (proj/include/rollsim/dedup.hpp:25-34, dedup.cpp:102-122). */
+int rs_prefix_index_info(const rs_prefix_index* idx, int32_t* batch_size,
+                         int32_t* min_len, int32_t* max_len,
+                         int64_t* total_tokens);
+int rs_unique_prefix_count(const rs_prefix_index* idx, int32_t prefix_len,
+                           int64_t* out);
+int rs_unique_prefix_tokens(const rs_prefix_index* idx, int32_t prefix_len,
+                            int64_t* out);
+int rs_remainder_tokens(const rs_prefix_index* idx, int32_t prefix_len,
+                        int64_t* out);
+/* Raw tables (the private members of PrefixIndex, dedup.hpp:43-47):
+ * nodes_at_depth has max_len+1 entries, the other four max_len+2. */
+int rs_prefix_index_tables(const rs_prefix_index* idx, int64_t* nodes_at_depth,
+                           int64_t* short_count_below,
+                           int64_t* short_tokens_below,
+                           int64_t* longer_count_from,
+                           int64_t* longer_tokens_from);
+
+/* select_prefix_length (dedup.hpp:63-65, dedup.cpp:124-144). */
+int rs_select_prefix_length(const rs_prefix_index* idx,
+                            int32_t max_unique_prefixes, int32_t gpu_count,
+                            int32_t l_min, int32_t l_max, int32_t* prefix_len,
+                            int32_t* capacity_exceeded);
+/* dedup_savings (dedup.hpp:73-74, dedup.cpp:146-161). */
+int rs_dedup_savings(const rs_prefix_index* idx, int32_t l_star,
+                     int32_t responses_per_prompt, int64_t* raw_prefill_tokens,
+                     int64_t* dedup_prefill_tokens, double* saved_fraction);
+/* unique_prefix_count_among (dedup.hpp:77-78, dedup.cpp:163-183). */
+int rs_unique_prefix_count_among(rs_ctx* ctx, const int32_t* tokens,
+                                 const int64_t* offsets, int32_t count,
+                                 int32_t prefix_len, int64_t* out);
+/* Dedup map (extension): labels[i] = smallest batch index j
+ * whose length-L prefix (full sequence if shorter) equals prompt i's. */
+int rs_dedup_map(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets,
+                 int32_t count, int32_t prefix_len, int32_t* labels);
+/* Chained block hashes (extension). For prompt i with
+ * n_i = ceil(len_i / block_tokens) blocks, hashes[hash_offset(i) + j] is the
+ * chained hash of tokens [0, min(len_i, (j+1)*block_tokens)), where
+ * hash_offset(i) = sum_{k<i} n_k. Definition in DESIGN.md §3.4. */
+int rs_block_hashes(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets,
+                    int32_t count, int32_t block_tokens, uint64_t* hashes);
+
+/* ------------------------------------------------------------------ */
+/* (2) Length-aware assignment (proj/include/rollsim/planner.hpp).     */
+/* Prompts are SoA: pred (predicted_len), prompt_len, id_rank (rank of */
+/* the prompt id under std::string ordering; ties in predicted length  */
+/* are broken by it).                                                  */
+/* ------------------------------------------------------------------ */
+
+/* assign (planner.hpp:33-34, planner.cpp:16-51): order[r] = input index of
+ * the prompt at rank r (pred desc, id asc); group g is
+ * order[group_offsets[g] .. group_offsets[g+1]). */
+int rs_assign(rs_ctx* ctx, const double* pred, const int32_t* id_rank,
+              int32_t count, int32_t n_actors, int32_t* order,
+              int32_t* group_offsets);
+
+/* integrate_decode_seconds (planner.hpp:47-48, planner.cpp:88-130). */
+int rs_integrate_decode_seconds(rs_ctx* ctx, const int32_t* prompt_len,
+                                const double* target_len, int64_t count,
+                                const rs_profile* profile, double* out);
+
+/* estimate_actor_time (planner.hpp:52-54, planner.cpp:132-146) for one
+ * group given as SoA. */
+int rs_estimate_actor_time(rs_ctx* ctx, const int32_t* prompt_len,
+                           const double* pred, int32_t count,
+                           const rs_profile* profile,
+                           int32_t responses_per_prompt, double* out);
+
+/* estimate_cost (planner.hpp:57-58, planner.cpp:148-157): groups are
+ * consecutive slices [group_offsets[g], group_offsets[g+1]) of the SoA;
+ * times (nullable) receives each group's estimate_actor_time. */
+int rs_estimate_cost(rs_ctx* ctx, const int32_t* prompt_len, const double* pred,
+                     const int32_t* group_offsets, const int32_t* gpu_count,
+                     int32_t n_groups, const rs_profile* profile,
+                     int32_t responses_per_prompt, double* cost, double* times);
+
+/* ------------------------------------------------------------------ */
+/* (3) Cost-aware actor scaling (planner.hpp:60-91, planner.cpp:159-218) */
+/* ------------------------------------------------------------------ */
+typedef struct rs_scale_out {
+  /* Arrays of C = n_max - n_min + 1 entries, ascending N; any may be NULL. */
+  int32_t n_star;
+  double* t_total;
+  double* t_penalty;
+  double* cost;
+  double* t_norm;
+  double* c_norm;
+  double* score;
+  int64_t* idle_slot_ticks; /* sum over groups of G*(max ceil - ceil_i) */
+  /* count entries: input index at each rank (shared by every candidate). */
+  int32_t* order;
+  /* n_star entries: estimate per actor for the chosen N. */
+  double* actor_times;
+  /* sum_{N=n_min}^{n_max} N entries: every group time of every candidate,
+   * candidate-major (for host TimePenaltyFn callbacks). */
+  double* group_times;
+} rs_scale_out;
+
+/* scale(): t_penalty (nullable, C entries) is added to each candidate's
+ * t_total before normalisation, like TimePenaltyFn (planner.hpp:80-82). */
+int rs_scale(rs_ctx* ctx, const double* pred, const int32_t* prompt_len,
+             const int32_t* id_rank, int32_t count, const rs_profile* profile,
+             int32_t responses_per_prompt, int32_t n_min, int32_t n_max,
+             double lambda, int32_t gpus_per_actor, const double* t_penalty,
+             rs_scale_out* out);
+
+/* The normalise + argmin tail of scale() (planner.cpp:196-217) on
+ * caller-provided per-candidate totals; used after host penalty callbacks. */
+int rs_scale_select(rs_ctx* ctx, const double* t_total, const double* t_penalty,
+                    const double* cost, int32_t n_candidates, int32_t n_min,
+                    double lambda, double* t_norm, double* c_norm,
+                    double* score, int32_t* n_star);
+
+/* ------------------------------------------------------------------ */
+/* Monte-Carlo scaling sweep: scale() for every        */
+/* scenario x candidate, scenarios generated on the device.            */
+/* ------------------------------------------------------------------ */
+typedef struct rs_scenario_spec {
+  uint64_t base_seed;     /* scenario s uses Rng(hash_combine(base_seed, s)) */
+  int64_t first_scenario; /* global index of the first scenario (sharding) */
+  int32_t n_scenarios;
+  int32_t count;          /* prompts per scenario */
+  double plen_mean, plen_sigma;
+  int32_t plen_min, plen_max;
+  double pred_scale, pred_min, pred_max;
+} rs_scenario_spec;
+
+/* Materialise scenarios (pred, prompt_len: n_scenarios*count each).
+ * device_ptrs != 0: outputs are device pointers and the call is async. */
+int rs_generate_scenarios(rs_ctx* ctx, const rs_scenario_spec* spec,
+                          double* pred, int32_t* prompt_len, int device_ptrs);
+
+typedef struct rs_sweep_out {
+  /* Per scenario x candidate (scenario-major, S*C); nullable. */
+  double* t_total;
+  double* cost;
+  int64_t* idle_slot_ticks;
+  /* Per scenario (S); nullable. */
+  int32_t* n_star;
+  /* Per candidate (C) aggregates over this call's scenarios; nullable. */
+  int32_t* nstar_hist;
+  double* sum_t;
+  double* sum_c;
+} rs_sweep_out;
+
+/* Sweep over generated scenarios. device_ptrs != 0: every out pointer is a
+ * device pointer and the call is asynchronous on the context stream. */
+int rs_sweep(rs_ctx* ctx, const rs_scenario_spec* spec,
+             const rs_profile* profile, int32_t responses_per_prompt,
+             int32_t n_min, int32_t n_max, double lambda,
+             int32_t gpus_per_actor, rs_sweep_out* out, int device_ptrs);
+
+/* Sweep over caller scenarios (pred/prompt_len: S*count, id_rank = index). */
+int rs_sweep_arrays(rs_ctx* ctx, const double* pred, const int32_t* prompt_len,
+                    int32_t n_scenarios, int32_t count,
+                    const rs_profile* profile, int32_t responses_per_prompt,
+                    int32_t n_min, int32_t n_max, double lambda,
+                    int32_t gpus_per_actor, rs_sweep_out* out, int device_ptrs);
+
+/* Aggregate pick over the whole sweep from per-candidate sums (after the
+ * cross-rank allreduce): mean t and mean c are min-max normalised like
+ * scale() and the first strict minimum wins. Host-side O(C). */
+int rs_sweep_select(const double* sum_t, const double* sum_c,
+                    int64_t n_scenarios, int32_t n_candidates, int32_t n_min,
+                    double lambda, int32_t* n_star);
+
+/* ------------------------------------------------------------------ */
+/* LPT extension: responses (prompt i, r<G) of length  */
+/* ceil(pred_i) sorted (len desc, id_rank asc, r asc) are placed one by */
+/* one on the least-loaded actor (ties -> lowest index).               */
+/* ------------------------------------------------------------------ */
+int rs_lpt(rs_ctx* ctx, const double* pred, const int32_t* id_rank,
+           int32_t count, int32_t responses_per_prompt, int32_t n_min,
+           int32_t n_max, int64_t* makespan, int64_t* idle_tokens);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RS_H_ */

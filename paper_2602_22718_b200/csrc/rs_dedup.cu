@@ -1,0 +1,708 @@
+// rs_dedup.cu — shared-prefix dedup (1) of the RLHFless planning core.
+//
+// Reference: PrefixIndex::build (proj/src/dedup.cpp:30-100) sorts the batch
+// lexicographically and counts, per depth, the trie nodes created by each
+// distinct prompt after its sorted predecessor (node_diff[lcp+1] += 1,
+// node_diff[len+1] -= 1), skipping exact duplicates, then turns the
+// difference array and the per-length counts into five prefix tables.
+//
+// B200 design: no string sort. The multiset of adjacent LCPs
+// of the sorted distinct prompts equals sum over trie branch nodes v of
+// (deg(v) - 1) copies of depth(v), where deg counts children plus "a prompt
+// ends here". We recover every branch node exactly by refining classes of
+// prompts that share a verified prefix:
+//   class c = (representative r, verified common prefix length l)
+//   each member m computes x = lcp(m, r) from l on (warp-cooperative,
+//   coalesced 128-bit loads of m; r is hot in L1) and t = m[x] or END;
+//   (c, x) names the branch node on r's path at depth x; every distinct t
+//   is one extra child -> node_diff[x+1] += 1; members with equal (c, x, t)
+//   form the next class with verified prefix x+1 (rep = min index), or a
+//   leaf (END, or a single member); exact duplicates of r are dropped.
+// Every token of every prompt is read at most once (plus r's, from cache),
+// so the pass is HBM-bound on the first round. Grouping uses two
+// open-addressing tables keyed (c<<32|x) and (slotA<<33|t) with CAS insert.
+// The same refinement with lengths truncated to L gives the dedup map and
+// unique_prefix_count_among (dedup.cpp:163-183).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "rs_internal.cuh"
+
+namespace rs {
+
+namespace {
+
+constexpr uint64_t kEmpty = ~0ULL;
+constexpr uint64_t kEnd = 1ULL << 32;  // t value for "prompt ends at x"
+
+struct DedupState {
+  int P;
+  const int32_t* tok;
+  const int64_t* off;
+  int32_t* len;       // effective (possibly truncated) lengths
+  int64_t* node_diff; // maxd + 2
+  int64_t* end_count; // maxd + 2
+  int64_t* len_count; // maxd + 2
+  int64_t* stats;     // {min, max, total, leaves}
+  int32_t* labels;    // optional
+  // refinement
+  int32_t* mem_idx[2];
+  int32_t* mem_cls[2];
+  int32_t* cls_rep[2];
+  int32_t* cls_lcp[2];
+  int32_t* m_slot;    // per member: B slot or -1
+  uint64_t* a_keys;
+  uint64_t* b_keys;
+  int32_t* b_rep;
+  int32_t* b_cnt;
+  int32_t* counter;   // next member count
+};
+
+// Warp-aggregated atomicAdd of `v` (same for all active lanes) at base[idx].
+__device__ __forceinline__ void agg_add(int64_t* base, int64_t idx, int64_t v) {
+  unsigned act = __activemask();
+  unsigned peers = __match_any_sync(act, idx);
+  int leader = __ffs(peers) - 1;
+  if ((threadIdx.x & 31) == leader)
+    atomicAdd((unsigned long long*)(base + idx), (unsigned long long)(v * __popc(peers)));
+}
+
+__device__ __forceinline__ uint64_t volatile_load(const uint64_t* p) {
+  return *(volatile const uint64_t*)p;
+}
+
+__device__ __forceinline__ uint32_t table_insert(uint64_t* keys, uint32_t mask,
+                                                 uint64_t key, bool* created) {
+  uint32_t h = (uint32_t)hash_u64(key) & mask;
+  for (;;) {
+    uint64_t cur = volatile_load(keys + h);
+    if (cur == key) {
+      *created = false;
+      return h;
+    }
+    if (cur == kEmpty) {
+      uint64_t prev = atomicCAS((unsigned long long*)(keys + h), kEmpty, key);
+      if (prev == kEmpty) {
+        *created = true;
+        return h;
+      }
+      if (prev == key) {
+        *created = false;
+        return h;
+      }
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+__global__ void lengths_kernel(DedupState st, int32_t cap_len, int strict, int* flags) {
+  long long mn = INT64_MAX, mx = 0;
+  unsigned long long sum = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < st.P; i += gridDim.x * blockDim.x) {
+    int64_t raw = st.off[i + 1] - st.off[i];
+    if (strict && raw < 1) atomicOr(flags, kFlagEmptyPrompt);
+    int32_t l = (int32_t)(raw < cap_len ? raw : cap_len);
+    if (l < 0) l = 0;
+    st.len[i] = l;
+    mn = l < mn ? l : mn;
+    mx = l > mx ? l : mx;
+    sum += (unsigned long long)l;
+  }
+  mn = warp_min(mn);
+  mx = warp_max(mx);
+  sum = warp_sum(sum);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin((long long*)&st.stats[0], mn);
+    atomicMax((long long*)&st.stats[1], mx);
+    atomicAdd((unsigned long long*)&st.stats[2], sum);
+  }
+}
+
+__global__ void len_hist_kernel(DedupState st) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < st.P; i += gridDim.x * blockDim.x)
+    agg_add(st.len_count, st.len[i], 1);
+}
+
+__global__ void init_root_kernel(DedupState st) {
+  // Root class: rep = prompt 0 (smallest index), verified prefix 0.
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < st.P; i += gridDim.x * blockDim.x) {
+    if (i == 0) {
+      st.cls_rep[0][0] = 0;
+      st.cls_lcp[0][0] = 0;
+      int l0 = st.len[0];
+      atomicAdd((unsigned long long*)&st.node_diff[1], 1ULL);  // first sorted string
+      atomicAdd((unsigned long long*)&st.end_count[l0], 1ULL);
+      atomicAdd((unsigned long long*)&st.node_diff[l0 + 1], (unsigned long long)-1LL);
+      atomicAdd((unsigned long long*)&st.stats[3], 1ULL);
+      if (st.labels) st.labels[0] = 0;
+    } else {
+      st.mem_idx[0][i - 1] = i;
+      st.mem_cls[0][i - 1] = 0;
+    }
+  }
+}
+
+// Exact lcp(m, r) over [l0, n), warp-cooperative. m is streamed with 128-bit
+// non-allocating loads when 16B aligned; r is read through L1.
+__device__ __forceinline__ int warp_lcp(const int32_t* __restrict__ pm,
+                                        const int32_t* __restrict__ pr, int l0, int n) {
+  const int lane = threadIdx.x & 31;
+  constexpr int kU = 4;               // 4 x 128 tokens in flight per warp
+  const uintptr_t am = (uintptr_t)pm;
+  // first position whose address in m is 16B aligned, at or below l0
+  int align_shift = (int)((am / 4 + l0) & 3);
+  const bool r_aligned = (((uintptr_t)pr - am) & 15) == 0;
+  int pos = l0 - align_shift;
+  while (pos < n) {
+    int best = INT32_MAX;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      int p = pos + (u * 32 + lane) * 4;
+      int4 a;
+      if (p >= 0 && p + 3 < n) {
+        asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w)
+                     : "l"(pm + p));
+      } else {
+        a.x = (p + 0 >= 0 && p + 0 < n) ? pm[p + 0] : 0;
+        a.y = (p + 1 >= 0 && p + 1 < n) ? pm[p + 1] : 0;
+        a.z = (p + 2 >= 0 && p + 2 < n) ? pm[p + 2] : 0;
+        a.w = (p + 3 >= 0 && p + 3 < n) ? pm[p + 3] : 0;
+      }
+      int4 b;
+      if (r_aligned && p >= 0 && p + 3 < n) {
+        b = __ldg(reinterpret_cast<const int4*>(pr + p));
+      } else {
+        b.x = (p + 0 >= 0 && p + 0 < n) ? __ldg(pr + p + 0) : 0;
+        b.y = (p + 1 >= 0 && p + 1 < n) ? __ldg(pr + p + 1) : 0;
+        b.z = (p + 2 >= 0 && p + 2 < n) ? __ldg(pr + p + 2) : 0;
+        b.w = (p + 3 >= 0 && p + 3 < n) ? __ldg(pr + p + 3) : 0;
+      }
+      int e[4] = {a.x, a.y, a.z, a.w};
+      int f[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int q = p + j;
+        if (q >= l0 && q < n && best == INT32_MAX && e[j] != f[j]) best = q;
+      }
+    }
+    best = warp_min(best);
+    if (best != INT32_MAX) return best;
+    pos += kU * 128;
+  }
+  return n;
+}
+
+__global__ void __launch_bounds__(256)
+compare_kernel(DedupState st, int cur, int K, uint32_t mask) {
+  const int lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < K; k += W) {
+    const int m = st.mem_idx[cur][k];
+    const int c = st.mem_cls[cur][k];
+    const int r = st.cls_rep[cur][c];
+    const int l0 = st.cls_lcp[cur][c];
+    const int lm = st.len[m], lr = st.len[r];
+    const int n = min(lm, lr);
+    const int x = warp_lcp(st.tok + st.off[m], st.tok + st.off[r], l0, n);
+    if (lane == 0) {
+      if (x == lm && x == lr) {  // exact duplicate of r: skipped (dedup.cpp:62)
+        st.m_slot[k] = -1;
+        if (st.labels) st.labels[m] = r;
+      } else {
+        uint64_t t = x < lm ? (uint64_t)(uint32_t)st.tok[st.off[m] + x] : kEnd;
+        bool created;
+        uint32_t sa = table_insert(st.a_keys, mask, ((uint64_t)c << 32) | (uint32_t)x, &created);
+        uint32_t sb = table_insert(st.b_keys, mask, ((uint64_t)sa << 33) | t, &created);
+        atomicMin(st.b_rep + sb, m);
+        atomicAdd(st.b_cnt + sb, 1);
+        st.m_slot[k] = (int32_t)sb;
+      }
+    }
+  }
+}
+
+// One thread per B slot: branch children, leaves, next classes.
+__global__ void finalize_kernel(DedupState st, int cur, uint32_t cap) {
+  const int nxt = cur ^ 1;
+  for (uint32_t sb = blockIdx.x * blockDim.x + threadIdx.x; sb < cap; sb += gridDim.x * blockDim.x) {
+    uint64_t key = st.b_keys[sb];
+    if (key == kEmpty) continue;
+    uint32_t sa = (uint32_t)(key >> 33);
+    uint64_t t = key & ((1ULL << 33) - 1);
+    int x = (int)(uint32_t)(st.a_keys[sa] & 0xffffffffULL);
+    agg_add(st.node_diff, x + 1, 1);  // one more child of the node at depth x
+    int rep = st.b_rep[sb];
+    int leaf_len = -1;
+    if (t == kEnd) {
+      leaf_len = x;
+    } else if (st.b_cnt[sb] == 1) {
+      leaf_len = st.len[rep];
+    } else {
+      st.cls_rep[nxt][sb] = rep;
+      st.cls_lcp[nxt][sb] = x + 1;
+      leaf_len = st.len[rep];  // the new class's representative is a leaf
+    }
+    agg_add(st.end_count, leaf_len, 1);
+    agg_add(st.node_diff, leaf_len + 1, -1);
+    agg_add(st.stats, 3, 1);
+  }
+}
+
+__global__ void compact_kernel(DedupState st, int cur, int K) {
+  const int nxt = cur ^ 1;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
+    int sb = st.m_slot[k];
+    if (sb < 0) continue;
+    int m = st.mem_idx[cur][k];
+    int rep = st.b_rep[sb];
+    uint64_t t = st.b_keys[sb] & ((1ULL << 33) - 1);
+    bool leaf = t == kEnd || st.b_cnt[sb] == 1;
+    if (leaf || m == rep) {
+      if (st.labels) st.labels[m] = rep;
+      continue;
+    }
+    // warp-aggregated append
+    unsigned act = __activemask();
+    int leader = __ffs(act) - 1;
+    int rank = __popc(act & ((1u << (threadIdx.x & 31)) - 1));
+    int base = 0;
+    if ((threadIdx.x & 31) == leader) base = atomicAdd(st.counter, __popc(act));
+    base = __shfl_sync(act, base, leader);
+    st.mem_idx[nxt][base + rank] = m;
+    st.mem_cls[nxt][base + rank] = sb;
+  }
+}
+
+// The five PrefixIndex tables from the difference array and the counts
+// (dedup.cpp:73-98). One CTA; maxd is small (max prompt length).
+__global__ void tables_kernel(DedupState st, int maxd, int64_t* out /*5*(maxd+2)*/) {
+  if (threadIdx.x != 0) return;
+  int64_t* nodes = out;
+  int64_t* scb = out + (maxd + 2);
+  int64_t* stb = out + 2 * (int64_t)(maxd + 2);
+  int64_t* lcf = out + 3 * (int64_t)(maxd + 2);
+  int64_t* ltf = out + 4 * (int64_t)(maxd + 2);
+  int64_t run = 0;
+  nodes[0] = 0;
+  for (int d = 1; d <= maxd; ++d) {
+    run += st.node_diff[d];
+    nodes[d] = run;
+  }
+  nodes[maxd + 1] = 0;
+  scb[0] = 0;
+  stb[0] = 0;
+  for (int d = 1; d <= maxd + 1; ++d) {
+    int64_t ec = d - 1 >= 1 ? st.end_count[d - 1] : 0;
+    scb[d] = scb[d - 1] + ec;
+    stb[d] = stb[d - 1] + ec * (d - 1);
+  }
+  lcf[maxd + 1] = 0;
+  ltf[maxd + 1] = 0;
+  for (int d = maxd; d >= 0; --d) {
+    int64_t lc = d + 1 <= maxd ? st.len_count[d + 1] : 0;
+    lcf[d] = lcf[d + 1] + lc;
+    ltf[d] = ltf[d + 1] + lc * (d + 1);
+  }
+}
+
+uint32_t pow2_at_least(int64_t v) {
+  uint32_t c = 64;
+  while ((int64_t)c < v) c <<= 1;
+  return c;
+}
+
+}  // namespace
+
+// Runs the refinement on device-resident CSR. cap_len = INT32_MAX for the
+// full index. Fills node_diff/end_count/len_count/stats (and labels if
+// non-null). Host-synchronous (one flag read per round).
+static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off, int P,
+                        int32_t cap_len, int strict, bool want_labels, int32_t max_len_hint,
+                        DedupState* out_state, int64_t* h_stats, int32_t* h_labels) {
+  // Pass 1: lengths + stats (needs maxd to size the tables).
+  const uint32_t cap = pow2_at_least(2 * (int64_t)P + 2);
+  const size_t base_bytes = abytes(P, 4) + abytes(4, 8) + abytes(P, 4) * 4 +
+                            abytes(cap, 4) * 4 + abytes(P, 4) + abytes(cap, 8) * 2 +
+                            abytes(cap, 4) * 2 + abytes(1, 4) + abytes(P, 4);
+  int64_t maxd = max_len_hint > 0 ? max_len_hint : 0;
+  DedupState st{};
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    size_t need = base_bytes + abytes(maxd + 2, 8) * 3 + 5 * abytes(maxd + 2, 8) + (1 << 16);
+    RS_TRY(arena_reserve(ctx, need));
+    st.P = P;
+    st.tok = d_tok;
+    st.off = d_off;
+    st.len = arena_alloc<int32_t>(ctx, P);
+    st.stats = arena_alloc<int64_t>(ctx, 4);
+    RS_TRY(clear_flags(ctx));
+    int64_t init[4] = {INT64_MAX, 0, 0, 0};
+    RS_TRY(h2d(ctx, st.stats, init, sizeof(init)));
+    int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, 8 * ctx->num_sms));
+    RS_LAUNCH(ctx, "dedup_lengths", lengths_kernel, blocks, 256, 0, st, cap_len, strict, ctx->d_flags);
+    int64_t hs[4];
+    RS_TRY(d2h(ctx, hs, st.stats, sizeof(hs)));
+    RS_TRY(sync_and_check(ctx));
+    if (hs[1] <= maxd || attempt == 1) {
+      maxd = std::max<int64_t>(maxd, hs[1]);
+      break;
+    }
+    maxd = hs[1];
+  }
+  const int md = (int)maxd;
+  st.node_diff = arena_alloc<int64_t>(ctx, md + 2);
+  st.end_count = arena_alloc<int64_t>(ctx, md + 2);
+  st.len_count = arena_alloc<int64_t>(ctx, md + 2);
+  for (int b = 0; b < 2; ++b) {
+    st.mem_idx[b] = arena_alloc<int32_t>(ctx, std::max(P, 1));
+    st.mem_cls[b] = arena_alloc<int32_t>(ctx, std::max(P, 1));
+    st.cls_rep[b] = arena_alloc<int32_t>(ctx, cap);
+    st.cls_lcp[b] = arena_alloc<int32_t>(ctx, cap);
+  }
+  st.m_slot = arena_alloc<int32_t>(ctx, std::max(P, 1));
+  st.a_keys = arena_alloc<uint64_t>(ctx, cap);
+  st.b_keys = arena_alloc<uint64_t>(ctx, cap);
+  st.b_rep = arena_alloc<int32_t>(ctx, cap);
+  st.b_cnt = arena_alloc<int32_t>(ctx, cap);
+  st.counter = arena_alloc<int32_t>(ctx, 1);
+  st.labels = want_labels ? arena_alloc<int32_t>(ctx, std::max(P, 1)) : nullptr;
+  if (!st.counter || (want_labels && !st.labels)) return fail(RS_E_NOMEM, "arena exhausted (dedup)");
+  RS_CUDA_TRY(cudaMemsetAsync(st.node_diff, 0, 8 * (md + 2), ctx->stream));
+  RS_CUDA_TRY(cudaMemsetAsync(st.end_count, 0, 8 * (md + 2), ctx->stream));
+  RS_CUDA_TRY(cudaMemsetAsync(st.len_count, 0, 8 * (md + 2), ctx->stream));
+  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, 8 * ctx->num_sms));
+  RS_LAUNCH(ctx, "dedup_len_hist", len_hist_kernel, blocks, 256, 0, st);
+  RS_LAUNCH(ctx, "dedup_init", init_root_kernel, blocks, 256, 0, st);
+  int K = P - 1;
+  int cur = 0;
+  while (K > 0) {
+    uint32_t c = pow2_at_least(2 * (int64_t)K + 2);
+    RS_CUDA_TRY(cudaMemsetAsync(st.a_keys, 0xff, 8ull * c, ctx->stream));
+    RS_CUDA_TRY(cudaMemsetAsync(st.b_keys, 0xff, 8ull * c, ctx->stream));
+    RS_CUDA_TRY(cudaMemsetAsync(st.b_rep, 0x7f, 4ull * c, ctx->stream));
+    RS_CUDA_TRY(cudaMemsetAsync(st.b_cnt, 0, 4ull * c, ctx->stream));
+    RS_CUDA_TRY(cudaMemsetAsync(st.counter, 0, 4, ctx->stream));
+    int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)K + 7) / 8, 64 * ctx->num_sms));
+    RS_LAUNCH(ctx, "dedup_compare", compare_kernel, wblocks, 256, 0, st, cur, K, c - 1);
+    int fb = (int)std::max<int64_t>(1, std::min<int64_t>((c + 255) / 256, 8 * ctx->num_sms));
+    RS_LAUNCH(ctx, "dedup_finalize", finalize_kernel, fb, 256, 0, st, cur, c);
+    int kb = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)K + 255) / 256, 8 * ctx->num_sms));
+    RS_LAUNCH(ctx, "dedup_compact", compact_kernel, kb, 256, 0, st, cur, K);
+    int nk = 0;
+    RS_TRY(d2h(ctx, &nk, st.counter, 4));
+    RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    K = nk;
+    cur ^= 1;
+  }
+  if (h_stats) RS_TRY(d2h(ctx, h_stats, st.stats, 4 * 8));
+  if (h_labels && P > 0) RS_TRY(d2h(ctx, h_labels, st.labels, 4ull * P));
+  *out_state = st;
+  return RS_OK;
+}
+
+}  // namespace rs
+
+using namespace rs;
+
+struct rs_prefix_index {
+  int32_t batch = 0, min_len = 0, max_len = 0;
+  int64_t total = 0;
+  std::vector<int64_t> nodes, scb, stb, lcf, ltf;
+};
+
+static int build_index_device(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
+                              int32_t P, rs_prefix_index** out) {
+  if (P <= 0) return fail(RS_E_VALIDATION, "prefix index needs a non-empty batch");
+  DedupState st;
+  int64_t stats[4];
+  RS_TRY(dedup_refine(ctx, d_tok, d_off, P, INT32_MAX, 1, false, 0, &st, stats, nullptr));
+  const int md = (int)stats[1];
+  int64_t* d_tables = arena_alloc<int64_t>(ctx, 5ull * (md + 2));
+  if (!d_tables) return fail(RS_E_NOMEM, "arena exhausted (tables)");
+  RS_LAUNCH(ctx, "dedup_tables", tables_kernel, 1, 32, 0, st, md, d_tables);
+  std::vector<int64_t> h(5ull * (md + 2));
+  RS_TRY(d2h(ctx, h.data(), d_tables, 8 * h.size()));
+  RS_TRY(sync_and_check(ctx));
+  auto* idx = new rs_prefix_index();
+  idx->batch = P;
+  idx->min_len = (int32_t)stats[0];
+  idx->max_len = md;
+  idx->total = stats[2];
+  idx->nodes.assign(h.begin(), h.begin() + md + 1);
+  idx->scb.assign(h.begin() + (md + 2), h.begin() + 2 * (md + 2));
+  idx->stb.assign(h.begin() + 2 * (md + 2), h.begin() + 3 * (md + 2));
+  idx->lcf.assign(h.begin() + 3 * (md + 2), h.begin() + 4 * (md + 2));
+  idx->ltf.assign(h.begin() + 4 * (md + 2), h.begin() + 5 * (md + 2));
+  *out = idx;
+  return RS_OK;
+}
+
+// Copy a host CSR into dedicated device buffers (kept outside the arena,
+// which the refinement re-reserves).
+struct DeviceCSR {
+  int32_t* tok = nullptr;
+  int64_t* off = nullptr;
+  ~DeviceCSR() {
+    if (tok) cudaFree(tok);
+    if (off) cudaFree(off);
+  }
+};
+
+static int upload_csr(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets, int32_t count,
+                      DeviceCSR* d) {
+  if (count < 0) return fail(RS_E_ARG, "negative count");
+  if (!offsets) return fail(RS_E_ARG, "offsets is NULL");
+  int64_t ntok = offsets[count] - offsets[0];
+  if (ntok < 0) return fail(RS_E_VALIDATION, "offsets must be non-decreasing");
+  if (cudaMalloc(&d->tok, std::max<int64_t>(ntok, 1) * 4 + 16) != cudaSuccess ||
+      cudaMalloc(&d->off, 8ull * (count + 1)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(RS_E_NOMEM, "device CSR allocation failed");
+  }
+  std::vector<int64_t> rel(count + 1);
+  for (int32_t i = 0; i <= count; ++i) rel[i] = offsets[i] - offsets[0];
+  if (ntok) RS_TRY(h2d(ctx, d->tok, tokens + offsets[0], 4ull * ntok));
+  RS_TRY(h2d(ctx, d->off, rel.data(), 8ull * (count + 1)));
+  return RS_OK;
+}
+
+__global__ void block_hash_kernel(const int32_t* tok, const int64_t* off, int P, int K,
+                                  const int64_t* hash_off, uint64_t* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const uint64_t kMul = 0x9e3779b97f4a7c15ULL;
+  const int lanes_per_block = K / 4 < 32 ? K / 4 : 32;  // K in {4..128}
+  const int blocks_per_chunk = 128 / K > 0 ? 128 / K : 1;
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < P; i += W) {
+    const int32_t* p = tok + off[i];
+    const int64_t len = off[i + 1] - off[i];
+    uint64_t* o = out + hash_off[i];
+    uint64_t h = 0x243f6a8885a308d3ULL;
+    int64_t wb = 0;
+    for (int64_t c0 = 0; c0 < len; c0 += 128) {
+      // lane covers tokens [c0 + 4*lane, +4); its block is (4*lane)/K
+      int64_t q = c0 + 4 * lane;
+      int blk = (4 * lane) / K;
+      int64_t bstart = c0 + (int64_t)blk * K;
+      int64_t bend = bstart + K < len ? bstart + K : len;
+      uint64_t acc = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int64_t pos = q + j;
+        if (pos < bend) {
+          // exponent = bend - 1 - pos
+          uint64_t e = (uint64_t)(bend - 1 - pos), pw = 1, bse = kMul;
+          while (e) {
+            if (e & 1) pw *= bse;
+            bse *= bse;
+            e >>= 1;
+          }
+          acc += ((uint64_t)(uint32_t)p[pos] + 1) * pw;
+        }
+      }
+      // reduce within the lanes of one block
+      for (int o2 = 1; o2 < lanes_per_block; o2 <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o2);
+      uint64_t m = (uint64_t)(bend - bstart);
+      uint64_t bh = hash_u64(acc ^ (m << 56));
+      int nblk = (int)std::min<int64_t>(blocks_per_chunk, (len - c0 + K - 1) / K);
+      for (int b = 0; b < nblk; ++b) {
+        uint64_t v = __shfl_sync(0xffffffffu, bh, b * lanes_per_block);
+        h = hash_combine(h, v);
+        if (lane == 0) o[wb] = h;
+        ++wb;
+      }
+    }
+  }
+}
+
+extern "C" {
+
+int rs_prefix_index_build(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets,
+                          int32_t batch, rs_prefix_index** out) {
+  if (!ctx || !out) return fail(RS_E_ARG, "NULL argument");
+  *out = nullptr;
+  if (batch <= 0) return fail(RS_E_VALIDATION, "prefix index needs a non-empty batch");
+  for (int32_t i = 0; i < batch; ++i)
+    if (offsets[i + 1] - offsets[i] < 1)
+      return fail(RS_E_VALIDATION, "prefix index: empty prompt in batch");
+  DeviceCSR d;
+  RS_TRY(upload_csr(ctx, tokens, offsets, batch, &d));
+  return build_index_device(ctx, d.tok, d.off, batch, out);
+}
+
+int rs_prefix_index_build_device(rs_ctx* ctx, const int32_t* d_tokens, const int64_t* d_offsets,
+                                 int32_t batch, rs_prefix_index** out) {
+  if (!ctx || !out) return fail(RS_E_ARG, "NULL argument");
+  *out = nullptr;
+  return build_index_device(ctx, d_tokens, d_offsets, batch, out);
+}
+
+int rs_prefix_index_build_device_async(rs_ctx* ctx, const int32_t* d_tokens,
+                                       const int64_t* d_offsets, int32_t batch,
+                                       int32_t max_len_cap, int64_t* d_tables, int64_t* d_info) {
+  if (!ctx || !d_tables || !d_info) return fail(RS_E_ARG, "NULL argument");
+  if (batch <= 0) return fail(RS_E_VALIDATION, "prefix index needs a non-empty batch");
+  DedupState st;
+  int64_t stats[4];
+  RS_TRY(dedup_refine(ctx, d_tokens, d_offsets, batch, INT32_MAX, 1, false, max_len_cap, &st,
+                      stats, nullptr));
+  if (stats[1] > max_len_cap) return fail(RS_E_ARG, "max_len_cap below the longest prompt");
+  RS_LAUNCH(ctx, "dedup_tables", tables_kernel, 1, 32, 0, st, max_len_cap, d_tables);
+  int64_t info[5] = {batch, stats[0], stats[1], stats[2], 0};
+  RS_TRY(h2d(ctx, d_info, info, sizeof(info)));
+  return RS_OK;
+}
+
+void rs_prefix_index_free(rs_prefix_index* idx) { delete idx; }
+
+int rs_prefix_index_info(const rs_prefix_index* idx, int32_t* batch, int32_t* min_len,
+                         int32_t* max_len, int64_t* total) {
+  if (!idx) return fail(RS_E_ARG, "index is NULL");
+  if (batch) *batch = idx->batch;
+  if (min_len) *min_len = idx->min_len;
+  if (max_len) *max_len = idx->max_len;
+  if (total) *total = idx->total;
+  return RS_OK;
+}
+
+// dedup.cpp:102-122
+int rs_unique_prefix_count(const rs_prefix_index* idx, int32_t l, int64_t* out) {
+  if (!idx || !out) return fail(RS_E_ARG, "NULL argument");
+  if (l < 1) return fail(RS_E_VALIDATION, "unique_prefix_count: prefix_len must be >= 1");
+  int32_t m = std::min(l, idx->max_len);
+  *out = idx->nodes[m] + idx->scb[m];
+  return RS_OK;
+}
+
+int rs_unique_prefix_tokens(const rs_prefix_index* idx, int32_t l, int64_t* out) {
+  if (!idx || !out) return fail(RS_E_ARG, "NULL argument");
+  if (l < 1) return fail(RS_E_VALIDATION, "unique_prefix_tokens: prefix_len must be >= 1");
+  int32_t m = std::min(l, idx->max_len);
+  *out = idx->nodes[m] * m + idx->stb[m];
+  return RS_OK;
+}
+
+int rs_remainder_tokens(const rs_prefix_index* idx, int32_t l, int64_t* out) {
+  if (!idx || !out) return fail(RS_E_ARG, "NULL argument");
+  if (l < 1) return fail(RS_E_VALIDATION, "remainder_tokens: prefix_len must be >= 1");
+  if (l >= idx->max_len) {
+    *out = 0;
+    return RS_OK;
+  }
+  *out = idx->ltf[l] - idx->lcf[l] * l;
+  return RS_OK;
+}
+
+int rs_prefix_index_tables(const rs_prefix_index* idx, int64_t* nodes, int64_t* scb,
+                           int64_t* stb, int64_t* lcf, int64_t* ltf) {
+  if (!idx) return fail(RS_E_ARG, "index is NULL");
+  if (nodes) std::memcpy(nodes, idx->nodes.data(), 8 * idx->nodes.size());
+  if (scb) std::memcpy(scb, idx->scb.data(), 8 * idx->scb.size());
+  if (stb) std::memcpy(stb, idx->stb.data(), 8 * idx->stb.size());
+  if (lcf) std::memcpy(lcf, idx->lcf.data(), 8 * idx->lcf.size());
+  if (ltf) std::memcpy(ltf, idx->ltf.data(), 8 * idx->ltf.size());
+  return RS_OK;
+}
+
+// dedup.cpp:124-144
+int rs_select_prefix_length(const rs_prefix_index* idx, int32_t cap, int32_t gpu_count,
+                            int32_t l_min, int32_t l_max, int32_t* len, int32_t* exceeded) {
+  (void)gpu_count;  // PrefillCapacity::gpu_count does not enter the math
+  if (!idx || !len || !exceeded) return fail(RS_E_ARG, "NULL argument");
+  if (l_min < 1 || l_min > l_max)
+    return fail(RS_E_VALIDATION, "select_prefix_length: need 1 <= l_min <= l_max");
+  if (cap < 1) return fail(RS_E_CONFIG, "prefill capacity must allow at least one prefix");
+  int64_t d;
+  RS_TRY(rs_unique_prefix_count(idx, l_min, &d));
+  if (d > cap) {
+    *len = l_min;
+    *exceeded = 1;
+    return RS_OK;
+  }
+  int32_t lo = l_min, hi = l_max;
+  while (lo < hi) {
+    int32_t mid = lo + (hi - lo + 1) / 2;
+    RS_TRY(rs_unique_prefix_count(idx, mid, &d));
+    if (d <= cap) lo = mid; else hi = mid - 1;
+  }
+  *len = lo;
+  *exceeded = 0;
+  return RS_OK;
+}
+
+// dedup.cpp:146-161
+int rs_dedup_savings(const rs_prefix_index* idx, int32_t l_star, int32_t g, int64_t* raw,
+                     int64_t* dedup, double* frac) {
+  if (!idx || !raw || !dedup || !frac) return fail(RS_E_ARG, "NULL argument");
+  if (g < 1) return fail(RS_E_VALIDATION, "dedup_savings: responses_per_prompt must be >= 1");
+  int64_t r = idx->total * (int64_t)g;
+  int64_t ut, rem;
+  RS_TRY(rs_unique_prefix_tokens(idx, l_star, &ut));
+  RS_TRY(rs_remainder_tokens(idx, l_star, &rem));
+  *raw = r;
+  *dedup = ut + rem;
+  *frac = r == 0 ? 0.0 : (double)(r - *dedup) / (double)r;
+  return RS_OK;
+}
+
+int rs_unique_prefix_count_among(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets,
+                                 int32_t count, int32_t prefix_len, int64_t* out) {
+  if (!ctx || !out) return fail(RS_E_ARG, "NULL argument");
+  if (prefix_len < 1)
+    return fail(RS_E_VALIDATION, "unique_prefix_count_among: prefix_len must be >= 1");
+  if (count <= 0) {
+    *out = 0;
+    return RS_OK;
+  }
+  DeviceCSR d;
+  RS_TRY(upload_csr(ctx, tokens, offsets, count, &d));
+  DedupState st;
+  int64_t stats[4];
+  RS_TRY(dedup_refine(ctx, d.tok, d.off, count, prefix_len, 0, false, prefix_len, &st, stats,
+                      nullptr));
+  RS_TRY(sync_and_check(ctx));
+  *out = stats[3];
+  return RS_OK;
+}
+
+int rs_dedup_map(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets, int32_t count,
+                 int32_t prefix_len, int32_t* labels) {
+  if (!ctx || !labels) return fail(RS_E_ARG, "NULL argument");
+  if (prefix_len < 1) return fail(RS_E_VALIDATION, "dedup_map: prefix_len must be >= 1");
+  if (count <= 0) return RS_OK;
+  DeviceCSR d;
+  RS_TRY(upload_csr(ctx, tokens, offsets, count, &d));
+  DedupState st;
+  int64_t stats[4];
+  RS_TRY(dedup_refine(ctx, d.tok, d.off, count, prefix_len, 0, true, prefix_len, &st, stats,
+                      labels));
+  return sync_and_check(ctx);
+}
+
+int rs_block_hashes(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets, int32_t count,
+                    int32_t K, uint64_t* hashes) {
+  if (!ctx || !hashes) return fail(RS_E_ARG, "NULL argument");
+  if (K < 4 || K > 128 || (K & (K - 1)))
+    return fail(RS_E_CONFIG, "block_hashes: block_tokens must be a power of two in [4, 128]");
+  if (count <= 0) return RS_OK;
+  std::vector<int64_t> hoff(count + 1, 0);
+  for (int32_t i = 0; i < count; ++i) {
+    int64_t len = offsets[i + 1] - offsets[i];
+    if (len < 0) return fail(RS_E_VALIDATION, "offsets must be non-decreasing");
+    hoff[i + 1] = hoff[i] + (len + K - 1) / K;
+  }
+  DeviceCSR d;
+  RS_TRY(upload_csr(ctx, tokens, offsets, count, &d));
+  const int64_t nh = hoff[count];
+  RS_TRY(arena_reserve(ctx, abytes(count + 1, 8) + abytes(std::max<int64_t>(nh, 1), 8) + 4096));
+  int64_t* dho = arena_alloc<int64_t>(ctx, count + 1);
+  uint64_t* dh = arena_alloc<uint64_t>(ctx, std::max<int64_t>(nh, 1));
+  RS_TRY(h2d(ctx, dho, hoff.data(), 8ull * (count + 1)));
+  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)count + 7) / 8, 16 * ctx->num_sms));
+  RS_LAUNCH(ctx, "block_hashes", block_hash_kernel, blocks, 256, 0, d.tok, d.off, count, K, dho, dh);
+  if (nh) RS_TRY(d2h(ctx, hashes, dh, 8ull * nh));
+  return sync_and_check(ctx);
+}
+
+}  // extern "C"

@@ -1,0 +1,1412 @@
+// rs_planner.cu — length-aware assignment (2) and cost-aware actor scaling
+// (3) of the RLHFless planning core on sm_100a.
+//
+// Reference semantics (proj/src/planner.cpp):
+//   assign            :16-51   sort (pred desc, id asc) + contiguous split
+//   run sum           :61-84   per knot piece count*(tpot(lo)+tpot(hi))/2
+//   integrate         :88-130  runs of equal ceil(target), ascending, summed
+//                              sequentially; batch = live responses, context
+//                              = max live prompt_len + tick - 1
+//   estimate_actor_time :132-146 (G copies per prompt), estimate_cost :148-157
+//   scale             :159-218 per-candidate max/sum, min-max normalise,
+//                              first strict argmin
+//
+// Device pipeline: every "scenario" (one predicted-length
+// vector) is turned into a rank-ordered scenario structure (SS):
+//   plen_r[r], order_r[r], seg_of[r]          r = rank (pred desc, id asc)
+//   segF[k], segS[k], segMX[k], segCF[k]      k = run of equal ceil(pred)
+// built either by a per-scenario bucket sort in shared memory (finish ticks
+// <= 16384, the Monte-Carlo path) or by the generic radix sort. Then one warp
+// evaluates one (scenario, candidate N, group g): the group is the contiguous
+// rank range [a, b); its runs are the segments it spans, taken in ascending
+// finish order; each lane evaluates one run (prefix-max base via a warp
+// scan + carry), and the lanes' run sums are added in lane order so the FP64
+// sum is the reference's sequential sum bit for bit.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "rs_scenario_tables.h"
+#include "rs_sort.cuh"
+
+namespace rs {
+
+// ---------------------------------------------------------------- views --
+struct SSView {
+  int S;
+  const int64_t* item_off;  // S+1
+  const int32_t* plen_r;
+  const int32_t* order_r;
+  const int32_t* seg_of;
+  const int64_t* segF;   // segment arrays of scenario s start at item_off[s]+s
+  const int32_t* segS;   // k in [0, D]; segS[D] = P_s
+  const int32_t* segMX;
+  const int64_t* segCF;  // exclusive prefix of count*F, segCF[D] = total
+  const int32_t* nseg;
+};
+
+struct SSBuffers {
+  int32_t* plen_r;
+  int32_t* order_r;
+  int32_t* seg_of;
+  int64_t* segF;
+  int32_t* segS;
+  int32_t* segMX;
+  int64_t* segCF;
+  int32_t* nseg;
+  int32_t* tmp_idx;
+};
+
+static size_t ss_bytes(int64_t items, int S) {
+  int64_t segs = items + S;
+  return abytes(items, 4) * 4 + abytes(segs, 8) * 2 + abytes(segs, 4) * 2 +
+         abytes(S, 4);
+}
+
+static SSBuffers ss_alloc(rs_ctx* ctx, int64_t items, int S) {
+  int64_t segs = items + S;
+  SSBuffers b;
+  b.plen_r = arena_alloc<int32_t>(ctx, items);
+  b.order_r = arena_alloc<int32_t>(ctx, items);
+  b.seg_of = arena_alloc<int32_t>(ctx, items);
+  b.tmp_idx = arena_alloc<int32_t>(ctx, items);
+  b.segF = arena_alloc<int64_t>(ctx, segs);
+  b.segCF = arena_alloc<int64_t>(ctx, segs);
+  b.segS = arena_alloc<int32_t>(ctx, segs);
+  b.segMX = arena_alloc<int32_t>(ctx, segs);
+  b.nseg = arena_alloc<int32_t>(ctx, S);
+  return b;
+}
+
+static SSView ss_view(const SSBuffers& b, const int64_t* item_off, int S) {
+  return SSView{S, item_off, b.plen_r, b.order_r, b.seg_of, b.segF,
+                b.segS, b.segMX, b.segCF, b.nseg};
+}
+
+// --------------------------------------------------- scenario generation --
+struct GenSpec {
+  uint64_t base_seed;
+  int64_t first;
+  int count;
+  double plen_mean, plen_sigma;
+  int plen_min, plen_max;
+  double pred_scale, pred_min, pred_max;
+};
+
+// Quantile interpolation (oracle: orc_generate_scenarios).
+__device__ __forceinline__ double qinterp(const double* t, uint64_t u) {
+  uint64_t j = u >> 52;
+  double f = dmul((double)((u >> 11) & ((1ULL << 41) - 1)), 0x1.0p-41);
+  double a = __ldg(t + j), b = __ldg(t + j + 1);
+  return dadd(a, dmul(dsub(b, a), f));
+}
+
+__device__ __forceinline__ void gen_item(const GenSpec& g, const double* nz,
+                                         const double* lnz, uint64_t seed,
+                                         int i, double* pred, int32_t* plen) {
+  uint64_t u1 = draw_at(seed, 2 * (uint64_t)i + 1);
+  uint64_t u2 = draw_at(seed, 2 * (uint64_t)i + 2);
+  double z = qinterp(nz, u1);
+  double pl = round(dadd(g.plen_mean, dmul(g.plen_sigma, z)));
+  pl = pl < (double)g.plen_min ? (double)g.plen_min : pl;
+  pl = pl > (double)g.plen_max ? (double)g.plen_max : pl;
+  double pr = dmul(g.pred_scale, qinterp(lnz, u2));
+  pr = pr < g.pred_min ? g.pred_min : pr;
+  pr = pr > g.pred_max ? g.pred_max : pr;
+  *pred = pr;
+  *plen = (int32_t)pl;
+}
+
+__global__ void gen_scenarios_kernel(GenSpec g, const double* nz,
+                                     const double* lnz, int S, double* pred,
+                                     int32_t* plen) {
+  int64_t total = (int64_t)S * g.count;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int s = (int)(t / g.count), i = (int)(t % g.count);
+    uint64_t seed = hash_combine(g.base_seed, (uint64_t)(g.first + s));
+    gen_item(g, nz, lnz, seed, i, pred + t, plen + t);
+  }
+}
+
+// ------------------------------------------ bucketed structure builder --
+// One CTA per scenario. Counting sort by finish tick f = ceil(pred) in
+// descending order (shared-memory histogram over [1, Fmax]), then each
+// bucket is ordered by (pred desc, input index asc) inside one warp.
+constexpr int kBuildThreads = 1024;
+constexpr int kWideBucket = 4096;
+
+__device__ __forceinline__ bool rank_less(double pa, int ia, double pb, int ib) {
+  return pa > pb || (pa == pb && ia < ib);
+}
+
+template <bool kGenerate>
+__global__ void __launch_bounds__(kBuildThreads)
+build_bucketed_kernel(GenSpec gs, const double* nz, const double* lnz,
+                      double* pred_io, int32_t* plen_io,
+                      const int64_t* item_off, SSBuffers ss, int* flags) {
+  extern __shared__ int32_t smem[];
+  int32_t* endb = smem;                      // [kBucketFmax + 2] cursors
+  int32_t* segid = smem + kBucketFmax + 2;   // [kBucketFmax + 2]
+  __shared__ int32_t wsum[32];
+  __shared__ int64_t wsum64[32];
+  __shared__ int bad;
+  const int s = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t i0 = item_off[s];
+  const int P = (int)(item_off[s + 1] - i0);
+  double* pred = pred_io + i0;
+  int32_t* plen = plen_io + i0;
+  const int64_t so = i0 + s;
+  for (int f = tid; f < kBucketFmax + 2; f += kBuildThreads) endb[f] = 0;
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  uint64_t seed = kGenerate ? hash_combine(gs.base_seed, (uint64_t)(gs.first + s)) : 0;
+  int lflags = 0;
+  for (int i = tid; i < P; i += kBuildThreads) {
+    double p;
+    if (kGenerate) {
+      int32_t pl;
+      gen_item(gs, nz, lnz, seed, i, &p, &pl);
+      pred[i] = p;
+      plen[i] = pl;
+    } else {
+      p = pred[i];
+    }
+    if (!isfinite(p)) { lflags |= kFlagNotFinite; continue; }
+    double fc = ceil(p);
+    if (!(fc >= 1.0) || fc > (double)kBucketFmax) { lflags |= kFlagBucketOverflow; continue; }
+    atomicAdd(&endb[(int)fc], 1);
+  }
+  if (lflags) atomicOr(&bad, lflags);
+  __syncthreads();
+  if (bad) {
+    if (tid == 0) atomicOr(flags, bad);
+    return;
+  }
+  // Descending exclusive scan over f = Fmax..1 (thread t owns 16 bins).
+  constexpr int kPer = kBucketFmax / kBuildThreads;  // 16
+  int cnt[kPer];
+  int csum = 0, nz_cnt = 0;
+  int64_t cf = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    int f = kBucketFmax - tid * kPer - j;
+    cnt[j] = endb[f];
+    csum += cnt[j];
+    nz_cnt += cnt[j] ? 1 : 0;
+    cf += (int64_t)cnt[j] * f;
+  }
+  // block exclusive scans of csum, nz_cnt, cf
+  auto block_excl = [&](int v) -> int {
+    int incl = warp_incl_sum(v);
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int x = wsum[lane];
+      wsum[lane] = warp_incl_sum(x) - x;
+    }
+    __syncthreads();
+    int r = wsum[wid] + incl - v;
+    __syncthreads();
+    return r;
+  };
+  int start = block_excl(csum);
+  int kbase = block_excl(nz_cnt);
+  int64_t cfbase;
+  {
+    int64_t incl = warp_incl_sum(cf);
+    if (lane == 31) wsum64[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int64_t x = wsum64[lane];
+      wsum64[lane] = warp_incl_sum(x) - x;
+    }
+    __syncthreads();
+    cfbase = wsum64[wid] + incl - cf;
+    if (tid == kBuildThreads - 1) {
+      ss.nseg[s] = kbase + nz_cnt;
+      ss.segS[so + kbase + nz_cnt] = P;
+      ss.segCF[so + kbase + nz_cnt] = cfbase + cf;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    int f = kBucketFmax - tid * kPer - j;
+    endb[f] = start;
+    if (cnt[j]) {
+      segid[f] = kbase;
+      ss.segF[so + kbase] = f;
+      ss.segS[so + kbase] = start;
+      ss.segCF[so + kbase] = cfbase;
+      ++kbase;
+    }
+    start += cnt[j];
+    cfbase += (int64_t)cnt[j] * f;
+  }
+  __syncthreads();
+  // Scatter input indices into their bucket (unordered inside it).
+  for (int i = tid; i < P; i += kBuildThreads) {
+    int f = (int)ceil(pred[i]);
+    int pos = atomicAdd(&endb[f], 1);
+    ss.tmp_idx[i0 + pos] = i;
+  }
+  __syncthreads();
+  // Order each bucket by (pred desc, index asc); one warp per bucket.
+  const int D = ss.nseg[s];
+  const int nwarps = kBuildThreads / 32;
+  for (int k = wid; k < D; k += nwarps) {
+    int lo = ss.segS[so + k], hi = ss.segS[so + k + 1], m = hi - lo;
+    int mx = INT32_MIN;
+    if (m <= 32) {
+      int idx = lane < m ? ss.tmp_idx[i0 + lo + lane] : INT32_MAX;
+      double key = lane < m ? pred[idx] : -INFINITY;
+      // bitonic sort over the 32 lanes; inactive lanes sort last
+#pragma unroll
+      for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          double ok = __shfl_xor_sync(0xffffffffu, key, stride);
+          int oi = __shfl_xor_sync(0xffffffffu, idx, stride);
+          bool up = ((lane & size) == 0);
+          bool lower = (lane & stride) == 0;
+          bool other_first = rank_less(ok, oi, key, idx);
+          // lower lane keeps the "first" element when ascending in rank
+          bool take = lower == up ? other_first : !other_first && !(ok == key && oi == idx);
+          if (take) { key = ok; idx = oi; }
+        }
+      }
+      if (lane < m) {
+        int pl = plen[idx];
+        ss.order_r[i0 + lo + lane] = idx;
+        ss.plen_r[i0 + lo + lane] = pl;
+        ss.seg_of[i0 + lo + lane] = k;
+        mx = pl;
+      }
+    } else if (m <= kWideBucket) {
+      for (int e = lane; e < m; e += 32) {
+        int idx = ss.tmp_idx[i0 + lo + e];
+        double key = pred[idx];
+        int rank = 0;
+        for (int o = 0; o < m; ++o) {
+          int oi = ss.tmp_idx[i0 + lo + o];
+          rank += rank_less(pred[oi], oi, key, idx) ? 1 : 0;
+        }
+        int pl = plen[idx];
+        ss.order_r[i0 + lo + rank] = idx;
+        ss.plen_r[i0 + lo + rank] = pl;
+        ss.seg_of[i0 + lo + rank] = k;
+        mx = max(mx, pl);
+      }
+    } else {
+      if (lane == 0) atomicOr(flags, kFlagBucketTooWide);
+    }
+    mx = warp_max(mx);
+    if (lane == 0) ss.segMX[so + k] = mx;
+  }
+}
+
+// --------------------------------------------- generic structure builder --
+// Input: rank-ordered pred_r / plen_r (after the radix sort). One CTA per
+// scenario: segment flags, block scan, segment arrays.
+__global__ void __launch_bounds__(kBuildThreads)
+build_structure_kernel(const double* pred_r, const int64_t* item_off,
+                       SSBuffers ss) {
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t carry_s;
+  const int s = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t i0 = item_off[s];
+  const int P = (int)(item_off[s + 1] - i0);
+  const int64_t so = i0 + s;
+  if (tid == 0) carry_s = -1;
+  __syncthreads();
+  for (int t0 = 0; t0 < P; t0 += kBuildThreads) {
+    int r = t0 + tid;
+    bool valid = r < P;
+    int64_t fin = valid ? (int64_t)ceil(pred_r[i0 + r]) : 0;
+    int64_t prev = (valid && r > 0) ? (int64_t)ceil(pred_r[i0 + r - 1]) : -1;
+    int flag = valid && (r == 0 || fin != prev) ? 1 : 0;
+    int incl = warp_incl_sum(flag);
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int x = wsum[lane];
+      wsum[lane] = warp_incl_sum(x) - x;
+    }
+    __syncthreads();
+    int carry = carry_s;
+    int seg = carry + wsum[wid] + incl;
+    if (valid) {
+      ss.seg_of[i0 + r] = seg;
+      if (flag) {
+        ss.segF[so + seg] = fin;
+        ss.segS[so + seg] = r;
+      }
+    }
+    __syncthreads();
+    if (tid == kBuildThreads - 1) carry_s = seg;
+    __syncthreads();
+  }
+  const int D = carry_s + 1;
+  if (tid == 0) {
+    ss.nseg[s] = D;
+    ss.segS[so + D] = P;
+  }
+  __syncthreads();
+  // Segment maxima: one warp per segment.
+  for (int k = wid; k < D; k += kBuildThreads / 32) {
+    int lo = ss.segS[so + k], hi = ss.segS[so + k + 1];
+    int mx = INT32_MIN;
+    for (int r = lo + lane; r < hi; r += 32) mx = max(mx, ss.plen_r[i0 + r]);
+    mx = warp_max(mx);
+    if (lane == 0) ss.segMX[so + k] = mx;
+  }
+  // segCF: exclusive prefix of count*F (one warp, sequential chunks).
+  if (wid == 0) {
+    int64_t run = 0;
+    for (int k0 = 0; k0 < D; k0 += 32) {
+      int k = k0 + lane;
+      int64_t v = k < D ? (int64_t)(ss.segS[so + k + 1] - ss.segS[so + k]) * ss.segF[so + k] : 0;
+      int64_t incl = warp_incl_sum(v);
+      if (k < D) ss.segCF[so + k] = run + incl - v;
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) ss.segCF[so + D] = run;
+  }
+}
+
+// ---------------------------------------------------- group evaluation --
+struct CandSpec {
+  int n_min, n_max;
+  int64_t T;  // groups per scenario = sum_{N=n_min}^{n_max} N
+  int G;
+};
+
+__device__ __forceinline__ int64_t tri(int64_t n) { return n * (n - 1) / 2; }
+
+// flat index within a scenario -> (N, g)
+__device__ __forceinline__ void flat_to_ng(int64_t flat, int n_min, int* N, int* g) {
+  int64_t x = flat + tri(n_min);
+  int64_t n = (int64_t)floor((1.0 + sqrt(1.0 + 8.0 * (double)x)) * 0.5);
+  while (n > 1 && tri(n) > x) --n;
+  while (tri(n + 1) <= x) ++n;
+  *N = (int)n;
+  *g = (int)(x - tri(n));
+}
+
+constexpr int kEvalThreads = 256;
+constexpr int kEvalWarps = kEvalThreads / 32;
+constexpr int kCarry = 128;  // chunks of 32 runs per carry window
+
+// Time of one group [a, b) of scenario s (all lanes return the same value).
+__device__ double group_time_warp(const SSView& ss, const DevProfile& prof,
+                                  int s, int a, int b, int G, int* carry_buf) {
+  const int lane = lane_id();
+  const int64_t i0 = ss.item_off[s];
+  const int64_t so = i0 + s;
+  const int32_t* plen = ss.plen_r + i0;
+  const int32_t* sof = ss.seg_of + i0;
+  const int64_t* F = ss.segF + so;
+  const int32_t* Sg = ss.segS + so;
+  const int32_t* MX = ss.segMX + so;
+  if (b <= a) return 0.0;
+  const int ka = __ldg(sof + a), kb = __ldg(sof + b - 1);
+  if (ka == kb) {
+    int m = INT32_MIN;
+    for (int i = a + lane; i < b; i += 32) m = max(m, __ldg(plen + i));
+    m = warp_max(m);
+    int64_t f = __ldg(F + ka);
+    double rs = run_sum_int(prof, (int64_t)G * (b - a), m, (int64_t)m + f - 1);
+    return dadd(0.0, rs);
+  }
+  // Partial maxima of the two boundary segments.
+  int va = INT32_MIN, vb = INT32_MIN;
+  {
+    int ea = __ldg(Sg + ka + 1);
+    for (int i = a + lane; i < ea; i += 32) va = max(va, __ldg(plen + i));
+    int sb = __ldg(Sg + kb);
+    for (int i = sb + lane; i < b; i += 32) vb = max(vb, __ldg(plen + i));
+    va = warp_max(va);
+    vb = warp_max(vb);
+  }
+  auto vk_of = [&](int k) -> int {
+    return k == ka ? va : (k == kb ? vb : __ldg(MX + k));
+  };
+  const int nk = kb - ka + 1;
+  const int J = (nk + 31) >> 5;
+  double total = 0.0;
+  int64_t prevF = 0;
+  for (int j0 = 0; j0 < J; j0 += kCarry) {
+    const int j1 = min(J, j0 + kCarry);
+    // max of v over all chunks below the window (lower k)
+    int lm = INT32_MIN;
+    for (int j = j1; j < J; ++j) {
+      int k = kb - 32 * j - lane;
+      if (k >= ka) lm = max(lm, vk_of(k));
+    }
+    int run = warp_max(lm);
+    for (int j = j1 - 1; j >= j0; --j) {
+      if (lane == 0) carry_buf[j - j0] = run;
+      int k = kb - 32 * j - lane;
+      int m = k >= ka ? vk_of(k) : INT32_MIN;
+      run = max(run, warp_max(m));
+    }
+    __syncwarp();
+    for (int j = j0; j < j1; ++j) {
+      const int k = kb - 32 * j - lane;
+      const bool act = k >= ka;
+      int64_t Fk = act ? __ldg(F + k) : 0;
+      int vk = act ? vk_of(k) : INT32_MIN;
+      int xk = act ? (k == kb ? b : __ldg(Sg + k + 1)) : 0;
+      int m = vk;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int u = __shfl_down_sync(0xffffffffu, m, o);
+        if (lane + o < 32) m = max(m, u);
+      }
+      int base = max(m, carry_buf[j - j0]);
+      int64_t Fup = __shfl_up_sync(0xffffffffu, Fk, 1);
+      if (lane == 0) Fup = prevF;
+      double rs = 0.0;
+      if (act) {
+        int64_t tstart = (k == kb) ? 1 : Fup + 1;
+        int64_t live = xk - a;
+        rs = run_sum_int(prof, (int64_t)G * live, (int64_t)base + tstart - 1,
+                         (int64_t)base + Fk - 1);
+      }
+      const int nact = min(32, kb - 32 * j - ka + 1);
+      for (int l = 0; l < nact; ++l) total = dadd(total, __shfl_sync(0xffffffffu, rs, l));
+      prevF = __shfl_sync(0xffffffffu, Fk, 31);
+    }
+    __syncwarp();
+  }
+  return total;
+}
+
+__global__ void __launch_bounds__(kEvalThreads)
+group_eval_kernel(SSView ss, DevProfile prof, CandSpec cs, double* gt) {
+  __shared__ int carry[kEvalWarps][kCarry];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t W = (int64_t)gridDim.x * kEvalWarps;
+  const int64_t total = (int64_t)ss.S * cs.T;
+  for (int64_t item = (int64_t)blockIdx.x * kEvalWarps + wid; item < total; item += W) {
+    int s = (int)(item / cs.T);
+    int64_t flat = item - (int64_t)s * cs.T;
+    int N, g;
+    flat_to_ng(flat, cs.n_min, &N, &g);
+    int P = (int)(ss.item_off[s + 1] - ss.item_off[s]);
+    int q = P / N, r = P % N;
+    int a = g * q + min(g, r);
+    int b = a + q + (g < r ? 1 : 0);
+    double t = group_time_warp(ss, prof, s, a, b, cs.G, carry[wid]);
+    if (lane == 0) gt[item] = t;
+  }
+}
+
+// Per (scenario, candidate): t_total = max, cost = sequential sum in group
+// order (planner.cpp:181-186), reference-model idle slot-ticks.
+__global__ void candidate_reduce_kernel(SSView ss, CandSpec cs, double rho,
+                                        int gpus, const double* gt,
+                                        double* t_total, double* cost,
+                                        int64_t* idle) {
+  const int C = cs.n_max - cs.n_min + 1;
+  const int64_t total = (int64_t)ss.S * C;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int s = (int)(t / C), ci = (int)(t % C);
+    int N = cs.n_min + ci;
+    const double* g = gt + (int64_t)s * cs.T + (tri(N) - tri(cs.n_min));
+    double tt = 0.0, dollars = 0.0;
+    const double gd = (double)gpus;
+    for (int k = 0; k < N; ++k) {
+      double v = g[k];
+      tt = tt < v ? v : tt;                          // std::max(t_total, t)
+      dollars = dadd(dollars, dmul(dmul(rho, v), gd));  // rho * t * gpu_count
+    }
+    t_total[t] = tt;
+    cost[t] = dollars;
+    if (idle) {
+      const int64_t i0 = ss.item_off[s];
+      const int64_t so = i0 + s;
+      const int P = (int)(ss.item_off[s + 1] - i0);
+      const int D = ss.nseg[s];
+      auto cfpos = [&](int p) -> int64_t {
+        if (p >= P) return ss.segCF[so + D];
+        int k = ss.seg_of[i0 + p];
+        return ss.segCF[so + k] + (int64_t)(p - ss.segS[so + k]) * ss.segF[so + k];
+      };
+      int q = P / N, r = P % N;
+      int64_t acc = 0;
+      for (int k = 0; k < N; ++k) {
+        int a = k * q + min(k, r), b = a + q + (k < r ? 1 : 0);
+        if (b <= a) continue;
+        int64_t fa = ss.segF[so + ss.seg_of[i0 + a]];
+        acc += (int64_t)(b - a) * fa - (cfpos(b) - cfpos(a));
+      }
+      idle[t] = acc * cs.G;
+    }
+  }
+}
+
+// Normalise + first strict argmin (planner.cpp:196-217), one thread per
+// scenario, sequential exactly like the reference.
+__global__ void select_kernel(int S, int C, int n_min, double lambda,
+                              const double* t_total, const double* t_pen,
+                              const double* cost, double* t_norm,
+                              double* c_norm, double* score, int32_t* n_star) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S;
+       s += gridDim.x * blockDim.x) {
+    const double* tt = t_total + (int64_t)s * C;
+    const double* cc = cost + (int64_t)s * C;
+    const double* tp = t_pen ? t_pen + (int64_t)s * C : nullptr;
+    double t_min = dadd(tt[0], tp ? tp[0] : 0.0);
+    double t_max = t_min, c_min = cc[0], c_max = c_min;
+    for (int i = 0; i < C; ++i) {
+      double t = dadd(tt[i], tp ? tp[i] : 0.0);
+      t_min = t < t_min ? t : t_min;
+      t_max = t_max < t ? t : t_max;
+      c_min = cc[i] < c_min ? cc[i] : c_min;
+      c_max = c_max < cc[i] ? cc[i] : c_max;
+    }
+    int best = 0;
+    double best_score = 0.0;
+    for (int i = 0; i < C; ++i) {
+      double t = dadd(tt[i], tp ? tp[i] : 0.0);
+      double tn = t_max > t_min ? ddiv(dsub(t, t_min), dsub(t_max, t_min)) : 0.0;
+      double cn = c_max > c_min ? ddiv(dsub(cc[i], c_min), dsub(c_max, c_min)) : 0.0;
+      double sc = dadd(dmul(lambda, tn), dmul(dsub(1.0, lambda), cn));
+      if (t_norm) t_norm[(int64_t)s * C + i] = tn;
+      if (c_norm) c_norm[(int64_t)s * C + i] = cn;
+      if (score) score[(int64_t)s * C + i] = sc;
+      if (i == 0) best_score = sc;
+      if (sc < best_score) {
+        best = i;
+        best_score = sc;
+      }
+    }
+    n_star[s] = n_min + best;
+  }
+}
+
+// Sweep aggregate over this batch's scenarios, fixed order (deterministic).
+__global__ void aggregate_kernel(int S, int C, int n_min, const double* t_total,
+                                 const double* cost, const int32_t* n_star,
+                                 double* sum_t, double* sum_c, int32_t* hist) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < C;
+       i += gridDim.x * blockDim.x) {
+    double st = 0.0, sc = 0.0;
+    int h = 0;
+    for (int s = 0; s < S; ++s) {
+      st = dadd(st, t_total[(int64_t)s * C + i]);
+      sc = dadd(sc, cost[(int64_t)s * C + i]);
+      h += n_star[s] == n_min + i ? 1 : 0;
+    }
+    sum_t[i] = dadd(sum_t[i], st);
+    sum_c[i] = dadd(sum_c[i], sc);
+    hist[i] += h;
+  }
+}
+
+// ------------------------------------------------------ input shaping --
+// Scatter caller SoA into id order (id_rank[i] = rank of prompt i's id) and
+// validate. The bucketed / generic builders then treat the position as the
+// tie-break index.
+__global__ void to_id_order_kernel(const double* pred, const int32_t* plen,
+                                   const int32_t* id_rank, int64_t n,
+                                   double* pred_o, int32_t* plen_o,
+                                   int32_t* orig, int32_t* seen, int* flags,
+                                   int require_ge1) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double p = pred[i];
+    int64_t j = id_rank ? id_rank[i] : i;
+    if (j < 0 || j >= n) {
+      atomicOr(flags, kFlagWorkOverflow << 1);
+      continue;
+    }
+    if (seen && atomicAdd(seen + j, 1) != 0) atomicOr(flags, kFlagWorkOverflow << 1);
+    if (!isfinite(p)) atomicOr(flags, kFlagNotFinite);
+    else if (require_ge1 && p < 1.0) atomicOr(flags, kFlagTargetBelowOne);
+    pred_o[j] = p == 0.0 ? 0.0 : p;  // -0.0 == +0.0 in the reference order
+    if (plen_o) plen_o[j] = plen ? plen[i] : 0;
+    if (orig) orig[j] = (int32_t)i;
+  }
+}
+
+// Order-preserving u64 key of a double, descending (negated total order).
+__device__ __forceinline__ uint64_t desc_key(double p) {
+  uint64_t b = (uint64_t)__double_as_longlong(p);
+  uint64_t asc = (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+  return ~asc;
+}
+
+__global__ void make_keys_kernel(const double* pred, int64_t n, uint64_t* keys,
+                                 uint32_t* vals) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = desc_key(pred[i]);
+    vals[i] = (uint32_t)i;
+  }
+}
+
+__global__ void scenario_keys_kernel(const int64_t* item_off, int S,
+                                     const uint32_t* vals, int64_t n,
+                                     uint64_t* keys) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v = vals[i];
+    int lo = 0, hi = S;  // scenario containing item v
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (item_off[mid] <= v) lo = mid; else hi = mid;
+    }
+    keys[i] = (uint64_t)lo;
+  }
+}
+
+__global__ void gather_ranked_kernel(const int64_t* item_off, int S,
+                                     const uint32_t* vals, int64_t n,
+                                     const double* pred, const int32_t* plen,
+                                     double* pred_r, SSBuffers ss) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v = vals[j];
+    int lo = 0, hi = S;
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (item_off[mid] <= v) lo = mid; else hi = mid;
+    }
+    pred_r[j] = pred[v];
+    ss.plen_r[j] = plen ? plen[v] : 0;
+    ss.order_r[j] = (int32_t)(v - item_off[lo]);
+  }
+}
+
+// ----------------------------------------------------- host orchestration --
+struct Built {
+  SSBuffers ss;
+  SSView view;
+};
+
+static int grid_for(rs_ctx* ctx, int64_t n, int threads) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads,
+                                                     (int64_t)ctx->num_sms * 8));
+}
+
+// Generic path: radix sort by (scenario, pred desc, index asc).
+static int build_generic(rs_ctx* ctx, int S, const int64_t* d_off, int64_t n,
+                         const double* pred, const int32_t* plen, SSBuffers ss,
+                         char* scratch) {
+  char* q = scratch;
+  uint64_t* keys = (uint64_t*)q; q += abytes(n, 8);
+  uint32_t* vals = (uint32_t*)q; q += abytes(n, 4);
+  double* pred_r = (double*)q; q += abytes(n, 8);
+  char* sort_scratch = q;
+  int blocks = grid_for(ctx, n, 256);
+  RS_LAUNCH(ctx, "make_keys", make_keys_kernel, blocks, 256, 0, pred, n, keys, vals);
+  uint64_t* ko;
+  uint32_t* vo;
+  RS_TRY(radix_sort_pairs(ctx, keys, vals, n, sort_scratch, &ko, &vo));
+  if (S > 1) {
+    // Second stable pass by scenario id -> order (scenario, pred desc, idx).
+    // The sorted pred keys are no longer needed, so `keys` holds the new
+    // keys; the values must not live in the sort scratch (ping-pong target).
+    if (vo != vals)
+      RS_CUDA_TRY(cudaMemcpyAsync(vals, vo, 4 * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    RS_LAUNCH(ctx, "scenario_keys", scenario_keys_kernel, blocks, 256, 0, d_off, S, vals, n, keys);
+    RS_TRY(radix_sort_pairs(ctx, keys, vals, n, sort_scratch, &ko, &vo));
+  }
+  RS_LAUNCH(ctx, "gather_ranked", gather_ranked_kernel, blocks, 256, 0, d_off, S, vo, n,
+            pred, plen, pred_r, ss);
+  RS_LAUNCH(ctx, "build_structure", build_structure_kernel, S, kBuildThreads, 0,
+            pred_r, d_off, ss);
+  return RS_OK;
+}
+
+static size_t generic_scratch_bytes(int64_t n) {
+  return abytes(n, 8) * 2 + abytes(n, 4) + radix_sort_scratch_bytes64(n);
+}
+
+static const size_t kBucketSmem = sizeof(int32_t) * 2 * (kBucketFmax + 2);
+
+static int build_bucketed(rs_ctx* ctx, int S, const int64_t* d_off, double* pred,
+                          int32_t* plen, SSBuffers ss, const GenSpec* gen,
+                          const double* nz, const double* lnz) {
+  RS_CUDA_TRY(cudaFuncSetAttribute(build_bucketed_kernel<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBucketSmem));
+  RS_CUDA_TRY(cudaFuncSetAttribute(build_bucketed_kernel<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBucketSmem));
+  GenSpec g{};
+  if (gen) g = *gen;
+  if (gen)
+    RS_LAUNCH(ctx, "build_bucketed", build_bucketed_kernel<true>, S, kBuildThreads,
+              kBucketSmem, g, nz, lnz, pred, plen, d_off, ss, ctx->d_flags);
+  else
+    RS_LAUNCH(ctx, "build_bucketed", build_bucketed_kernel<false>, S, kBuildThreads,
+              kBucketSmem, g, nz, lnz, pred, plen, d_off, ss, ctx->d_flags);
+  return RS_OK;
+}
+
+static int read_flags(rs_ctx* ctx, int* flags) {
+  RS_CUDA_TRY(cudaMemcpyAsync(ctx->h_flags, ctx->d_flags, sizeof(int),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+  RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  *flags = *ctx->h_flags;
+  return RS_OK;
+}
+
+// Build the SS for S scenarios laid out by d_off (host copy h_off) over
+// id-ordered pred/plen already in HBM. Tries the bucketed path first.
+static int build_any(rs_ctx* ctx, int S, const int64_t* d_off, int64_t n,
+                     double* pred, int32_t* plen, SSBuffers ss, char* scratch,
+                     bool allow_bucket) {
+  if (allow_bucket) {
+    RS_TRY(clear_flags(ctx));
+    RS_TRY(build_bucketed(ctx, S, d_off, pred, plen, ss, nullptr, nullptr, nullptr));
+    int fl;
+    RS_TRY(read_flags(ctx, &fl));
+    if (fl & kFlagNotFinite) return flags_to_status(fl);
+    if (!(fl & (kFlagBucketOverflow | kFlagBucketTooWide))) return RS_OK;
+    RS_TRY(clear_flags(ctx));
+  }
+  return build_generic(ctx, S, d_off, n, pred, plen, ss, scratch);
+}
+
+static int64_t groups_per_scenario(int n_min, int n_max) {
+  return (int64_t)n_max * (n_max + 1) / 2 - (int64_t)(n_min - 1) * n_min / 2;
+}
+
+static int eval_grid(rs_ctx* ctx, int64_t items) {
+  int64_t want = (items + kEvalWarps - 1) / kEvalWarps;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->num_sms * 8));
+}
+
+// scale()'s argument checks, in the reference order (planner.cpp:164-168),
+// then the ones the reference raises from inside its loop.
+static int check_scale_args(int32_t count, int32_t G, int32_t n_min,
+                            int32_t n_max, double lambda) {
+  if (n_min < 1 || n_min > n_max)
+    return fail(RS_E_VALIDATION, "scale: need 1 <= n_min <= n_max");
+  if (n_max > count) return fail(RS_E_VALIDATION, "scale: n_max exceeds prompt count");
+  if (lambda < 0 || lambda > 1) return fail(RS_E_CONFIG, "scale: lambda must be in [0, 1]");
+  if (G < 1) return fail(RS_E_VALIDATION, "estimate_actor_time: responses_per_prompt >= 1");
+  return RS_OK;
+}
+
+static int gen_tables(rs_ctx* ctx, double** nz, double** lnz) {
+  const size_t nt = RS_QTABLE_N + 1;
+  double* t = arena_alloc<double>(ctx, 2 * nt);
+  if (!t) return fail(RS_E_NOMEM, "arena exhausted (tables)");
+  RS_TRY(h2d(ctx, t, RS_NZ, 8 * nt));
+  RS_TRY(h2d(ctx, t + nt, RS_LNZ, 8 * nt));
+  *nz = t;
+  *lnz = t + nt;
+  return RS_OK;
+}
+
+static GenSpec to_gen(const rs_scenario_spec* sp, int64_t first) {
+  return GenSpec{sp->base_seed, first, sp->count, sp->plen_mean, sp->plen_sigma,
+                 sp->plen_min, sp->plen_max, sp->pred_scale, sp->pred_min, sp->pred_max};
+}
+
+static int check_spec(const rs_scenario_spec* sp) {
+  if (!sp) return fail(RS_E_ARG, "spec is NULL");
+  if (sp->n_scenarios < 0 || sp->count < 1)
+    return fail(RS_E_VALIDATION, "scenario spec needs count >= 1 and n_scenarios >= 0");
+  if (!(sp->pred_min >= 1.0) || !(sp->pred_max >= sp->pred_min))
+    return fail(RS_E_VALIDATION, "scenario spec needs 1 <= pred_min <= pred_max");
+  if (sp->plen_min > sp->plen_max) return fail(RS_E_VALIDATION, "scenario spec plen range");
+  return RS_OK;
+}
+
+// Shared sweep driver: scenarios either generated (spec) or from arrays.
+static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec,
+                      const double* h_pred, const int32_t* h_plen, int S,
+                      int P, const rs_profile* profile, int G, int n_min,
+                      int n_max, double lambda, int gpus, rs_sweep_out* out,
+                      int device_ptrs) {
+  RS_TRY(check_scale_args(P, G, n_min, n_max, lambda));
+  DevProfile dp;
+  RS_TRY(get_profile(ctx, profile, &dp));
+  const int C = n_max - n_min + 1;
+  const int64_t T = groups_per_scenario(n_min, n_max);
+  // Batch size: keep per-batch scratch near 2 GiB.
+  const size_t per_scen = abytes(P, 8) + abytes(P, 4) + ss_bytes(P, 1) + abytes(T, 8) +
+                          abytes(C, 8) * 2 + abytes(C, 8) + 1024;
+  int B = (int)std::max<size_t>(1, std::min<size_t>((size_t)S, (size_t)(2ull << 30) / per_scen));
+  if (B > 1024) B = 1024;
+  const bool generated = spec != nullptr;
+  bool bucket_ok = !generated || std::ceil(spec->pred_max) <= (double)kBucketFmax;
+  size_t need = (size_t)B * per_scen + abytes(B + 1, 8) + abytes(2 * (RS_QTABLE_N + 1), 8) +
+                abytes(C, 8) * 2 + abytes(C, 4) + (size_t)B * abytes(1, 8) * 4 + (1 << 20);
+  if (!bucket_ok || !generated) need += generic_scratch_bytes((int64_t)B * P);
+  RS_TRY(arena_reserve(ctx, need));
+  double* nz = nullptr;
+  double* lnz = nullptr;
+  RS_TRY(gen_tables(ctx, &nz, &lnz));
+  int64_t* d_off = arena_alloc<int64_t>(ctx, B + 1);
+  double* pred = arena_alloc<double>(ctx, (size_t)B * P);
+  int32_t* plen = arena_alloc<int32_t>(ctx, (size_t)B * P);
+  SSBuffers ss = ss_alloc(ctx, (int64_t)B * P, B);
+  double* gt = arena_alloc<double>(ctx, (size_t)B * T);
+  double* agg_t = arena_alloc<double>(ctx, C);
+  double* agg_c = arena_alloc<double>(ctx, C);
+  int32_t* agg_h = arena_alloc<int32_t>(ctx, C);
+  // per-batch outputs when the caller wants host results
+  double* b_tt = arena_alloc<double>(ctx, (size_t)B * C);
+  double* b_cc = arena_alloc<double>(ctx, (size_t)B * C);
+  int64_t* b_idle = arena_alloc<int64_t>(ctx, (size_t)B * C);
+  int32_t* b_ns = arena_alloc<int32_t>(ctx, B);
+  char* gscratch = (!bucket_ok || !generated) ? arena_alloc<char>(ctx, generic_scratch_bytes((int64_t)B * P)) : nullptr;
+  if (!b_ns || !agg_h || !gt || !ss.nseg) return fail(RS_E_NOMEM, "arena exhausted (sweep)");
+  {
+    std::vector<int64_t> off(B + 1);
+    for (int i = 0; i <= B; ++i) off[i] = (int64_t)i * P;
+    RS_TRY(h2d(ctx, d_off, off.data(), 8 * (B + 1)));
+  }
+  RS_CUDA_TRY(cudaMemsetAsync(agg_t, 0, 8 * C, ctx->stream));
+  RS_CUDA_TRY(cudaMemsetAsync(agg_c, 0, 8 * C, ctx->stream));
+  RS_CUDA_TRY(cudaMemsetAsync(agg_h, 0, 4 * C, ctx->stream));
+  RS_TRY(clear_flags(ctx));
+  CandSpec cs{n_min, n_max, T, G};
+  for (int s0 = 0; s0 < S; s0 += B) {
+    const int Sb = std::min(B, S - s0);
+    // When the final batch is short, the offsets prefix still applies.
+    SSView view = ss_view(ss, d_off, Sb);
+    if (generated) {
+      GenSpec g = to_gen(spec, spec->first_scenario + s0);
+      if (bucket_ok) {
+        RS_TRY(build_bucketed(ctx, Sb, d_off, pred, plen, ss, &g, nz, lnz));
+      } else {
+        RS_LAUNCH(ctx, "gen_scenarios", gen_scenarios_kernel, grid_for(ctx, (int64_t)Sb * P, 256),
+                  256, 0, g, nz, lnz, Sb, pred, plen);
+        RS_TRY(build_generic(ctx, Sb, d_off, (int64_t)Sb * P, pred, plen, ss, gscratch));
+      }
+    } else {
+      const double* src_p = h_pred + (size_t)s0 * P;
+      const int32_t* src_l = h_plen + (size_t)s0 * P;
+      if (device_ptrs) {
+        RS_CUDA_TRY(cudaMemcpyAsync(pred, src_p, 8ull * Sb * P, cudaMemcpyDeviceToDevice, ctx->stream));
+        RS_CUDA_TRY(cudaMemcpyAsync(plen, src_l, 4ull * Sb * P, cudaMemcpyDeviceToDevice, ctx->stream));
+      } else {
+        RS_TRY(h2d(ctx, pred, src_p, 8ull * Sb * P));
+        RS_TRY(h2d(ctx, plen, src_l, 4ull * Sb * P));
+      }
+      RS_LAUNCH(ctx, "validate_inputs", to_id_order_kernel, grid_for(ctx, (int64_t)Sb * P, 256), 256, 0,
+                pred, (const int32_t*)nullptr, (const int32_t*)nullptr, (int64_t)Sb * P,
+                pred, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr, ctx->d_flags, 1);
+      int fl;
+      RS_TRY(read_flags(ctx, &fl));
+      if (fl) return flags_to_status(fl);
+      RS_TRY(build_any(ctx, Sb, d_off, (int64_t)Sb * P, pred, plen, ss, gscratch, true));
+    }
+    double* o_tt = (device_ptrs && out->t_total) ? out->t_total + (size_t)s0 * C : b_tt;
+    double* o_cc = (device_ptrs && out->cost) ? out->cost + (size_t)s0 * C : b_cc;
+    int64_t* o_idle = (device_ptrs && out->idle_slot_ticks) ? out->idle_slot_ticks + (size_t)s0 * C : b_idle;
+    int32_t* o_ns = (device_ptrs && out->n_star) ? out->n_star + s0 : b_ns;
+    const int64_t items = (int64_t)Sb * T;
+    RS_LAUNCH(ctx, "group_eval", group_eval_kernel, eval_grid(ctx, items), kEvalThreads, 0,
+              view, dp, cs, gt);
+    RS_LAUNCH(ctx, "candidate_reduce", candidate_reduce_kernel,
+              grid_for(ctx, (int64_t)Sb * C, 128), 128, 0, view, cs, dp.rho, gpus, gt,
+              o_tt, o_cc, out->idle_slot_ticks ? o_idle : (int64_t*)nullptr);
+    RS_LAUNCH(ctx, "select", select_kernel, grid_for(ctx, Sb, 128), 128, 0, Sb, C, n_min,
+              lambda, o_tt, (const double*)nullptr, o_cc, (double*)nullptr, (double*)nullptr,
+              (double*)nullptr, o_ns);
+    RS_LAUNCH(ctx, "aggregate", aggregate_kernel, grid_for(ctx, C, 128), 128, 0, Sb, C, n_min,
+              o_tt, o_cc, o_ns, agg_t, agg_c, agg_h);
+    if (!device_ptrs) {
+      if (out->t_total) RS_TRY(d2h(ctx, out->t_total + (size_t)s0 * C, o_tt, 8ull * Sb * C));
+      if (out->cost) RS_TRY(d2h(ctx, out->cost + (size_t)s0 * C, o_cc, 8ull * Sb * C));
+      if (out->idle_slot_ticks)
+        RS_TRY(d2h(ctx, out->idle_slot_ticks + (size_t)s0 * C, o_idle, 8ull * Sb * C));
+      if (out->n_star) RS_TRY(d2h(ctx, out->n_star + s0, o_ns, 4ull * Sb));
+      RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    }
+  }
+  if (device_ptrs) {
+    if (out->sum_t) RS_CUDA_TRY(cudaMemcpyAsync(out->sum_t, agg_t, 8 * C, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (out->sum_c) RS_CUDA_TRY(cudaMemcpyAsync(out->sum_c, agg_c, 8 * C, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (out->nstar_hist) RS_CUDA_TRY(cudaMemcpyAsync(out->nstar_hist, agg_h, 4 * C, cudaMemcpyDeviceToDevice, ctx->stream));
+    return RS_OK;
+  }
+  if (out->sum_t) RS_TRY(d2h(ctx, out->sum_t, agg_t, 8 * C));
+  if (out->sum_c) RS_TRY(d2h(ctx, out->sum_c, agg_c, 8 * C));
+  if (out->nstar_hist) RS_TRY(d2h(ctx, out->nstar_hist, agg_h, 4 * C));
+  return sync_and_check(ctx);
+}
+
+// Single-set pipeline used by scale / assign / integrate / estimate_*:
+// S sets of caller items (host SoA), each its own scenario, id order given.
+struct SetRun {
+  int S;
+  int64_t n;
+  int64_t* d_off;
+  double* pred;
+  int32_t* plen;
+  int32_t* orig;
+  SSBuffers ss;
+  SSView view;
+};
+
+static int prepare_sets(rs_ctx* ctx, const double* h_pred, const int32_t* h_plen,
+                        const int32_t* h_id_rank, const std::vector<int64_t>& off,
+                        int require_ge1, size_t extra_bytes, SetRun* run) {
+  const int S = (int)off.size() - 1;
+  const int64_t n = off.back();
+  size_t need = abytes(S + 1, 8) + abytes(n, 8) * 2 + abytes(n, 4) * 4 + ss_bytes(n, S) +
+                generic_scratch_bytes(n) + extra_bytes + (1 << 20);
+  RS_TRY(arena_reserve(ctx, need));
+  run->S = S;
+  run->n = n;
+  run->d_off = arena_alloc<int64_t>(ctx, S + 1);
+  double* raw_pred = arena_alloc<double>(ctx, n);
+  int32_t* raw_plen = arena_alloc<int32_t>(ctx, n);
+  int32_t* raw_rank = arena_alloc<int32_t>(ctx, n);
+  int32_t* seen = arena_alloc<int32_t>(ctx, n);
+  run->pred = arena_alloc<double>(ctx, n);
+  run->plen = arena_alloc<int32_t>(ctx, n);
+  run->orig = arena_alloc<int32_t>(ctx, n);
+  run->ss = ss_alloc(ctx, n, S);
+  char* gscratch = arena_alloc<char>(ctx, generic_scratch_bytes(n));
+  if (!gscratch) return fail(RS_E_NOMEM, "arena exhausted (sets)");
+  RS_TRY(h2d(ctx, run->d_off, off.data(), 8 * (S + 1)));
+  RS_TRY(clear_flags(ctx));
+  if (n > 0) {
+    RS_TRY(h2d(ctx, raw_pred, h_pred, 8 * n));
+    if (h_plen) RS_TRY(h2d(ctx, raw_plen, h_plen, 4 * n));
+    if (h_id_rank) {
+      RS_TRY(h2d(ctx, raw_rank, h_id_rank, 4 * n));
+      RS_CUDA_TRY(cudaMemsetAsync(seen, 0, 4 * n, ctx->stream));
+    }
+    RS_LAUNCH(ctx, "to_id_order", to_id_order_kernel, grid_for(ctx, n, 256), 256, 0, raw_pred,
+              h_plen ? raw_plen : (const int32_t*)nullptr,
+              h_id_rank ? raw_rank : (const int32_t*)nullptr, n, run->pred, run->plen,
+              run->orig, h_id_rank ? seen : (int32_t*)nullptr, ctx->d_flags, require_ge1);
+    int fl;
+    RS_TRY(read_flags(ctx, &fl));
+    if (fl & (kFlagWorkOverflow << 1)) return fail(RS_E_ARG, "id_rank is not a permutation of [0, count)");
+    if (fl) return flags_to_status(fl);
+    RS_TRY(build_any(ctx, S, run->d_off, n, run->pred, run->plen, run->ss, gscratch, true));
+  }
+  run->view = ss_view(run->ss, run->d_off, S);
+  return RS_OK;
+}
+
+__global__ void map_order_kernel(const int32_t* order_r, const int32_t* orig,
+                                 int64_t n, int32_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = orig[order_r[i]];
+}
+
+__global__ void chunk_offsets_kernel(int P, int N, int32_t* off) {
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a <= N; a += gridDim.x * blockDim.x) {
+    int q = P / N, r = P % N;
+    off[a] = a * q + min(a, r);
+  }
+}
+
+// Sequential dollars over groups with per-group GPU counts (planner.cpp:148-157).
+__global__ void cost_sum_kernel(const double* times, const int32_t* gpu_count,
+                                int n, double rho, double* cost) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double d = 0.0;
+    for (int k = 0; k < n; ++k) d = dadd(d, dmul(dmul(rho, times[k]), (double)gpu_count[k]));
+    *cost = d;
+  }
+}
+
+// --------------------------------------------------------------- LPT --
+// Warp per candidate N <= 32*R: loads live in registers, each response goes
+// to the least-loaded actor (ties -> lowest index) via a packed u64 warp
+// argmin (load << 11 | actor).
+template <int R>
+__global__ void lpt_kernel(const int64_t* len_r, int64_t count, int G, int n_min,
+                           int n_max, int64_t* makespan, int64_t* idle) {
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int N = n_min + w;
+  if (N > n_max) return;
+  uint64_t load[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) load[j] = 0;
+  for (int64_t i0 = 0; i0 < count; i0 += 32) {
+    int64_t my = i0 + lane < count ? len_r[i0 + lane] : 0;
+    int nn = (int)(count - i0 < 32 ? count - i0 : 32);
+    for (int e = 0; e < nn; ++e) {
+      uint64_t len = (uint64_t)__shfl_sync(0xffffffffu, my, e);
+      for (int r = 0; r < G; ++r) {
+        uint64_t best = ~0ULL;
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          int a = j * 32 + lane;
+          uint64_t key = a < N ? (load[j] << 11) | (uint64_t)a : ~0ULL;
+          best = key < best ? key : best;
+        }
+        best = warp_min(best);
+        int a = (int)(best & 2047);
+        if ((a & 31) == lane) {
+#pragma unroll
+          for (int j = 0; j < R; ++j)
+            if (j == (a >> 5)) load[j] += len;
+        }
+      }
+    }
+  }
+  uint64_t mx = 0, sum = 0;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    int a = j * 32 + lane;
+    if (a < N) {
+      mx = load[j] > mx ? load[j] : mx;
+      sum += load[j];
+    }
+  }
+  mx = warp_max(mx);
+  sum = warp_sum(sum);
+  if (lane == 0) {
+    makespan[N - n_min] = (int64_t)mx;
+    idle[N - n_min] = (int64_t)(mx * (uint64_t)N - sum);
+  }
+}
+
+__global__ void lpt_keys_kernel(const double* pred_id, int64_t n, uint64_t* keys,
+                                uint32_t* vals) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = ~(uint64_t)(int64_t)ceil(pred_id[i]);  // finish desc
+    vals[i] = (uint32_t)i;                           // id order is stable
+  }
+}
+
+__global__ void lpt_gather_kernel(const double* pred_id, const uint32_t* vals,
+                                  int64_t n, int64_t* len_r) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    len_r[i] = (int64_t)ceil(pred_id[vals[i]]);
+}
+
+}  // namespace rs
+
+using namespace rs;
+
+extern "C" {
+
+int rs_generate_scenarios(rs_ctx* ctx, const rs_scenario_spec* spec, double* pred,
+                          int32_t* plen, int device_ptrs) {
+  if (!ctx) return fail(RS_E_ARG, "ctx is NULL");
+  RS_TRY(check_spec(spec));
+  int64_t n = (int64_t)spec->n_scenarios * spec->count;
+  if (n == 0) return RS_OK;
+  RS_TRY(arena_reserve(ctx, abytes(2 * (RS_QTABLE_N + 1), 8) +
+                                (device_ptrs ? 0 : abytes(n, 8) + abytes(n, 4)) + 4096));
+  double *nz, *lnz;
+  RS_TRY(gen_tables(ctx, &nz, &lnz));
+  double* dp = device_ptrs ? pred : arena_alloc<double>(ctx, n);
+  int32_t* dl = device_ptrs ? plen : arena_alloc<int32_t>(ctx, n);
+  GenSpec g = to_gen(spec, spec->first_scenario);
+  RS_LAUNCH(ctx, "gen_scenarios", gen_scenarios_kernel, grid_for(ctx, n, 256), 256, 0, g, nz,
+            lnz, spec->n_scenarios, dp, dl);
+  if (device_ptrs) return RS_OK;
+  RS_TRY(d2h(ctx, pred, dp, 8 * n));
+  RS_TRY(d2h(ctx, plen, dl, 4 * n));
+  return sync_and_check(ctx);
+}
+
+int rs_sweep(rs_ctx* ctx, const rs_scenario_spec* spec, const rs_profile* profile,
+             int32_t G, int32_t n_min, int32_t n_max, double lambda, int32_t gpus,
+             rs_sweep_out* out, int device_ptrs) {
+  if (!ctx || !out) return fail(RS_E_ARG, "NULL argument");
+  RS_TRY(check_spec(spec));
+  if (spec->n_scenarios == 0) return RS_OK;
+  return sweep_impl(ctx, spec, nullptr, nullptr, spec->n_scenarios, spec->count, profile, G,
+                    n_min, n_max, lambda, gpus, out, device_ptrs);
+}
+
+int rs_sweep_arrays(rs_ctx* ctx, const double* pred, const int32_t* plen, int32_t S,
+                    int32_t count, const rs_profile* profile, int32_t G, int32_t n_min,
+                    int32_t n_max, double lambda, int32_t gpus, rs_sweep_out* out,
+                    int device_ptrs) {
+  if (!ctx || !out || !pred || !plen) return fail(RS_E_ARG, "NULL argument");
+  if (S <= 0) return RS_OK;
+  return sweep_impl(ctx, nullptr, pred, plen, S, count, profile, G, n_min, n_max, lambda,
+                    gpus, out, device_ptrs);
+}
+
+int rs_sweep_select(const double* sum_t, const double* sum_c, int64_t n_scenarios,
+                    int32_t C, int32_t n_min, double lambda, int32_t* n_star) {
+  if (!sum_t || !sum_c || !n_star || C < 1 || n_scenarios < 1)
+    return fail(RS_E_ARG, "bad arguments");
+  if (lambda < 0 || lambda > 1) return fail(RS_E_CONFIG, "lambda must be in [0, 1]");
+  std::vector<double> mt(C), mc(C);
+  for (int i = 0; i < C; ++i) {
+    mt[i] = sum_t[i] / (double)n_scenarios;
+    mc[i] = sum_c[i] / (double)n_scenarios;
+  }
+  double t_min = mt[0], t_max = mt[0], c_min = mc[0], c_max = mc[0];
+  for (int i = 0; i < C; ++i) {
+    t_min = mt[i] < t_min ? mt[i] : t_min;
+    t_max = t_max < mt[i] ? mt[i] : t_max;
+    c_min = mc[i] < c_min ? mc[i] : c_min;
+    c_max = c_max < mc[i] ? mc[i] : c_max;
+  }
+  int best = 0;
+  double bs = 0;
+  for (int i = 0; i < C; ++i) {
+    double tn = t_max > t_min ? (mt[i] - t_min) / (t_max - t_min) : 0.0;
+    double cn = c_max > c_min ? (mc[i] - c_min) / (c_max - c_min) : 0.0;
+    double sc = lambda * tn + (1.0 - lambda) * cn;
+    if (i == 0) bs = sc;
+    if (sc < bs) {
+      best = i;
+      bs = sc;
+    }
+  }
+  *n_star = n_min + best;
+  return RS_OK;
+}
+
+int rs_scale(rs_ctx* ctx, const double* pred, const int32_t* plen, const int32_t* id_rank,
+             int32_t count, const rs_profile* profile, int32_t G, int32_t n_min,
+             int32_t n_max, double lambda, int32_t gpus, const double* t_penalty,
+             rs_scale_out* out) {
+  if (!ctx || !out) return fail(RS_E_ARG, "NULL argument");
+  RS_TRY(check_scale_args(count, G, n_min, n_max, lambda));
+  if (!pred || !plen) return fail(RS_E_ARG, "NULL argument");
+  DevProfile dp;
+  RS_TRY(get_profile(ctx, profile, &dp));
+  const int C = n_max - n_min + 1;
+  const int64_t T = groups_per_scenario(n_min, n_max);
+  std::vector<int64_t> off = {0, count};
+  SetRun run;
+  size_t extra = abytes(T, 8) + abytes(C, 8) * 7 + abytes(count, 4) + abytes(C, 8) + 4096;
+  RS_TRY(prepare_sets(ctx, pred, plen, id_rank, off, 1, extra, &run));
+  double* gt = arena_alloc<double>(ctx, T);
+  double* tt = arena_alloc<double>(ctx, C);
+  double* cc = arena_alloc<double>(ctx, C);
+  double* tp = arena_alloc<double>(ctx, C);
+  double* tn = arena_alloc<double>(ctx, C);
+  double* cn = arena_alloc<double>(ctx, C);
+  double* sc = arena_alloc<double>(ctx, C);
+  int64_t* idle = arena_alloc<int64_t>(ctx, C);
+  int32_t* order = arena_alloc<int32_t>(ctx, count);
+  int32_t* ns = arena_alloc<int32_t>(ctx, 1);
+  if (!ns) return fail(RS_E_NOMEM, "arena exhausted (scale)");
+  if (t_penalty) RS_TRY(h2d(ctx, tp, t_penalty, 8 * C));
+  CandSpec cs{n_min, n_max, T, G};
+  RS_LAUNCH(ctx, "group_eval", group_eval_kernel, eval_grid(ctx, T), kEvalThreads, 0, run.view,
+            dp, cs, gt);
+  RS_LAUNCH(ctx, "candidate_reduce", candidate_reduce_kernel, grid_for(ctx, C, 128), 128, 0,
+            run.view, cs, dp.rho, gpus, gt, tt, cc, idle);
+  RS_LAUNCH(ctx, "select", select_kernel, 1, 32, 0, 1, C, n_min, lambda, tt,
+            t_penalty ? tp : (const double*)nullptr, cc, tn, cn, sc, ns);
+  RS_LAUNCH(ctx, "map_order", map_order_kernel, grid_for(ctx, count, 256), 256, 0,
+            run.ss.order_r, run.orig, (int64_t)count, order);
+  RS_TRY(d2h(ctx, &out->n_star, ns, 4));
+  if (out->t_total) RS_TRY(d2h(ctx, out->t_total, tt, 8 * C));
+  if (out->cost) RS_TRY(d2h(ctx, out->cost, cc, 8 * C));
+  if (out->t_norm) RS_TRY(d2h(ctx, out->t_norm, tn, 8 * C));
+  if (out->c_norm) RS_TRY(d2h(ctx, out->c_norm, cn, 8 * C));
+  if (out->score) RS_TRY(d2h(ctx, out->score, sc, 8 * C));
+  if (out->idle_slot_ticks) RS_TRY(d2h(ctx, out->idle_slot_ticks, idle, 8 * C));
+  if (out->order) RS_TRY(d2h(ctx, out->order, order, 4 * count));
+  if (out->group_times) RS_TRY(d2h(ctx, out->group_times, gt, 8 * T));
+  RS_TRY(sync_and_check(ctx));
+  if (out->t_penalty)
+    for (int i = 0; i < C; ++i) out->t_penalty[i] = t_penalty ? t_penalty[i] : 0.0;
+  if (out->actor_times) {
+    int n = out->n_star;
+    int64_t base = (int64_t)n * (n - 1) / 2 - (int64_t)n_min * (n_min - 1) / 2;
+    RS_CUDA_TRY(cudaMemcpy(out->actor_times, gt + base, 8 * n, cudaMemcpyDeviceToHost));
+  }
+  return RS_OK;
+}
+
+int rs_scale_select(rs_ctx* ctx, const double* t_total, const double* t_penalty,
+                    const double* cost, int32_t C, int32_t n_min, double lambda,
+                    double* t_norm, double* c_norm, double* score, int32_t* n_star) {
+  if (!ctx || !t_total || !cost || !n_star || C < 1) return fail(RS_E_ARG, "bad arguments");
+  if (lambda < 0 || lambda > 1) return fail(RS_E_CONFIG, "scale: lambda must be in [0, 1]");
+  RS_TRY(arena_reserve(ctx, abytes(C, 8) * 6 + 4096));
+  double* d[6];
+  for (auto& x : d) x = arena_alloc<double>(ctx, C);
+  int32_t* ns = arena_alloc<int32_t>(ctx, 1);
+  RS_TRY(h2d(ctx, d[0], t_total, 8 * C));
+  RS_TRY(h2d(ctx, d[1], cost, 8 * C));
+  if (t_penalty) RS_TRY(h2d(ctx, d[2], t_penalty, 8 * C));
+  RS_LAUNCH(ctx, "select", select_kernel, 1, 32, 0, 1, C, n_min, lambda, d[0],
+            t_penalty ? d[2] : (const double*)nullptr, d[1], d[3], d[4], d[5], ns);
+  RS_TRY(d2h(ctx, n_star, ns, 4));
+  if (t_norm) RS_TRY(d2h(ctx, t_norm, d[3], 8 * C));
+  if (c_norm) RS_TRY(d2h(ctx, c_norm, d[4], 8 * C));
+  if (score) RS_TRY(d2h(ctx, score, d[5], 8 * C));
+  return sync_and_check(ctx);
+}
+
+int rs_assign(rs_ctx* ctx, const double* pred, const int32_t* id_rank, int32_t count,
+              int32_t n_actors, int32_t* order, int32_t* group_offsets) {
+  if (!ctx) return fail(RS_E_ARG, "ctx is NULL");
+  if (count <= 0) return fail(RS_E_VALIDATION, "assign: empty batch");
+  if (n_actors < 1) return fail(RS_E_VALIDATION, "assign: n_actors must be >= 1");
+  if (n_actors > count)
+    return fail(RS_E_VALIDATION, "assign: more actors (" + std::to_string(n_actors) +
+                                     ") than prompts (" + std::to_string(count) + ")");
+  if (!pred || !order || !group_offsets) return fail(RS_E_ARG, "NULL argument");
+  std::vector<int64_t> off = {0, count};
+  SetRun run;
+  RS_TRY(prepare_sets(ctx, pred, nullptr, id_rank, off, 0,
+                      abytes(count, 4) + abytes(n_actors + 1, 4) + 4096, &run));
+  int32_t* d_order = arena_alloc<int32_t>(ctx, count);
+  int32_t* d_off = arena_alloc<int32_t>(ctx, n_actors + 1);
+  RS_LAUNCH(ctx, "map_order", map_order_kernel, grid_for(ctx, count, 256), 256, 0,
+            run.ss.order_r, run.orig, (int64_t)count, d_order);
+  RS_LAUNCH(ctx, "chunk_offsets", chunk_offsets_kernel, grid_for(ctx, n_actors + 1, 256), 256, 0,
+            count, n_actors, d_off);
+  RS_TRY(d2h(ctx, order, d_order, 4 * count));
+  RS_TRY(d2h(ctx, group_offsets, d_off, 4 * (n_actors + 1)));
+  return sync_and_check(ctx);
+}
+
+// Integral of S independent item sets (one group each = whole set).
+static int integrate_sets(rs_ctx* ctx, const int32_t* plen, const double* target,
+                          const std::vector<int64_t>& off, int G, const rs_profile* profile,
+                          double* times_host, const int32_t* gpu_count, double* cost_host) {
+  DevProfile dp;
+  RS_TRY(get_profile(ctx, profile, &dp));
+  const int S = (int)off.size() - 1;
+  SetRun run;
+  RS_TRY(prepare_sets(ctx, target, plen, nullptr, off, 1,
+                      abytes(S, 8) + abytes(S, 4) + abytes(1, 8) + 4096, &run));
+  double* gt = arena_alloc<double>(ctx, S);
+  int32_t* gc = arena_alloc<int32_t>(ctx, S);
+  double* dcost = arena_alloc<double>(ctx, 1);
+  CandSpec cs{1, 1, 1, G};
+  RS_LAUNCH(ctx, "group_eval", group_eval_kernel, eval_grid(ctx, S), kEvalThreads, 0, run.view,
+            dp, cs, gt);
+  if (cost_host) {
+    RS_TRY(h2d(ctx, gc, gpu_count, 4 * S));
+    RS_LAUNCH(ctx, "cost_sum", cost_sum_kernel, 1, 32, 0, gt, gc, S, dp.rho, dcost);
+    RS_TRY(d2h(ctx, cost_host, dcost, 8));
+  }
+  if (times_host) RS_TRY(d2h(ctx, times_host, gt, 8 * S));
+  return sync_and_check(ctx);
+}
+
+int rs_integrate_decode_seconds(rs_ctx* ctx, const int32_t* prompt_len,
+                                const double* target_len, int64_t count,
+                                const rs_profile* profile, double* out) {
+  if (!ctx || !out) return fail(RS_E_ARG, "NULL argument");
+  if (count <= 0) {
+    *out = 0.0;
+    return RS_OK;
+  }
+  if (count > INT32_MAX) return fail(RS_E_VALIDATION, "too many responses");
+  std::vector<int64_t> off = {0, count};
+  return integrate_sets(ctx, prompt_len, target_len, off, 1, profile, out, nullptr, nullptr);
+}
+
+int rs_estimate_actor_time(rs_ctx* ctx, const int32_t* prompt_len, const double* pred,
+                           int32_t count, const rs_profile* profile, int32_t G, double* out) {
+  if (!ctx || !out) return fail(RS_E_ARG, "NULL argument");
+  if (G < 1) return fail(RS_E_VALIDATION, "estimate_actor_time: responses_per_prompt >= 1");
+  if (count <= 0) {
+    *out = 0.0;
+    return RS_OK;
+  }
+  std::vector<int64_t> off = {0, count};
+  return integrate_sets(ctx, prompt_len, pred, off, G, profile, out, nullptr, nullptr);
+}
+
+int rs_estimate_cost(rs_ctx* ctx, const int32_t* prompt_len, const double* pred,
+                     const int32_t* group_offsets, const int32_t* gpu_count, int32_t n_groups,
+                     const rs_profile* profile, int32_t G, double* cost, double* times) {
+  if (!ctx || !cost) return fail(RS_E_ARG, "NULL argument");
+  if (n_groups <= 0) {
+    *cost = 0.0;
+    return RS_OK;
+  }
+  if (G < 1) return fail(RS_E_VALIDATION, "estimate_actor_time: responses_per_prompt >= 1");
+  std::vector<int64_t> off(n_groups + 1);
+  for (int k = 0; k <= n_groups; ++k) off[k] = group_offsets[k] - group_offsets[0];
+  std::vector<double> t(n_groups);
+  RS_TRY(integrate_sets(ctx, prompt_len + group_offsets[0], pred + group_offsets[0], off, G,
+                        profile, t.data(), gpu_count, cost));
+  if (times) std::memcpy(times, t.data(), 8 * n_groups);
+  return RS_OK;
+}
+
+int rs_lpt(rs_ctx* ctx, const double* pred, const int32_t* id_rank, int32_t count, int32_t G,
+           int32_t n_min, int32_t n_max, int64_t* makespan, int64_t* idle) {
+  if (!ctx || !pred || !makespan || !idle) return fail(RS_E_ARG, "NULL argument");
+  if (count <= 0) return fail(RS_E_VALIDATION, "lpt: empty batch");
+  if (n_min < 1 || n_min > n_max) return fail(RS_E_VALIDATION, "lpt: need 1 <= n_min <= n_max");
+  if (G < 1) return fail(RS_E_VALIDATION, "lpt: responses_per_prompt >= 1");
+  if (n_max > 1024) return fail(RS_E_CONFIG, "lpt: n_max <= 1024 supported");
+  {
+    double mx = 0;
+    for (int32_t i = 0; i < count; ++i) {
+      if (!std::isfinite(pred[i])) return fail(RS_E_VALIDATION, "predicted length is not finite");
+      mx = pred[i] > mx ? pred[i] : mx;
+    }
+    if (std::ceil(mx) * (double)count * G >= 0x1.0p52)
+      return fail(RS_E_CONFIG, "lpt: total response tokens must stay below 2^52");
+  }
+  const int C = n_max - n_min + 1;
+  size_t need = abytes(count, 8) * 4 + abytes(count, 4) * 6 + radix_sort_scratch_bytes64(count) +
+                abytes(C, 8) * 2 + (1 << 20);
+  RS_TRY(arena_reserve(ctx, need));
+  double* raw = arena_alloc<double>(ctx, count);
+  int32_t* rk = arena_alloc<int32_t>(ctx, count);
+  int32_t* seen = arena_alloc<int32_t>(ctx, count);
+  double* pid = arena_alloc<double>(ctx, count);
+  uint64_t* keys = arena_alloc<uint64_t>(ctx, count);
+  uint32_t* vals = arena_alloc<uint32_t>(ctx, count);
+  int64_t* len_r = arena_alloc<int64_t>(ctx, count);
+  int64_t* mk = arena_alloc<int64_t>(ctx, C);
+  int64_t* id = arena_alloc<int64_t>(ctx, C);
+  char* sscr = arena_alloc<char>(ctx, radix_sort_scratch_bytes64(count));
+  if (!sscr) return fail(RS_E_NOMEM, "arena exhausted (lpt)");
+  RS_TRY(clear_flags(ctx));
+  RS_TRY(h2d(ctx, raw, pred, 8 * count));
+  if (id_rank) {
+    RS_TRY(h2d(ctx, rk, id_rank, 4 * count));
+    RS_CUDA_TRY(cudaMemsetAsync(seen, 0, 4 * count, ctx->stream));
+  }
+  RS_LAUNCH(ctx, "to_id_order", to_id_order_kernel, grid_for(ctx, count, 256), 256, 0, raw,
+            (const int32_t*)nullptr, id_rank ? rk : (const int32_t*)nullptr, (int64_t)count, pid,
+            (int32_t*)nullptr, (int32_t*)nullptr, id_rank ? seen : (int32_t*)nullptr,
+            ctx->d_flags, 1);
+  int fl;
+  RS_TRY(read_flags(ctx, &fl));
+  if (fl & (kFlagWorkOverflow << 1)) return fail(RS_E_ARG, "id_rank is not a permutation of [0, count)");
+  if (fl) return flags_to_status(fl);
+  RS_LAUNCH(ctx, "lpt_keys", lpt_keys_kernel, grid_for(ctx, count, 256), 256, 0, pid,
+            (int64_t)count, keys, vals);
+  uint64_t* ko;
+  uint32_t* vo;
+  RS_TRY(radix_sort_pairs(ctx, keys, vals, count, sscr, &ko, &vo));
+  RS_LAUNCH(ctx, "lpt_gather", lpt_gather_kernel, grid_for(ctx, count, 256), 256, 0, pid, vo,
+            (int64_t)count, len_r);
+  int warps_per_block = 4;
+  int blocks = (C + warps_per_block - 1) / warps_per_block;
+  int R = (n_max + 31) / 32;
+#define RS_LPT(RR)                                                                           \
+  RS_LAUNCH(ctx, "lpt", lpt_kernel<RR>, blocks, 32 * warps_per_block, 0, len_r, (int64_t)count, \
+            G, n_min, n_max, mk, id)
+  if (R <= 1) RS_LPT(1);
+  else if (R <= 2) RS_LPT(2);
+  else if (R <= 4) RS_LPT(4);
+  else if (R <= 8) RS_LPT(8);
+  else if (R <= 16) RS_LPT(16);
+  else RS_LPT(32);
+#undef RS_LPT
+  RS_TRY(d2h(ctx, makespan, mk, 8 * C));
+  RS_TRY(d2h(ctx, idle, id, 8 * C));
+  return sync_and_check(ctx);
+}
+
+}  // extern "C"

@@ -1,0 +1,442 @@
+"""Python mirror of the reference `rollsim` hot-path API over librs_b200.
+
+Same names, argument meaning and error behaviour as the reference C++
+library (/root/reference/proj/include/rollsim/{dedup,planner,profile}.hpp),
+so tests read like the reference's own. Every computation runs on the GPU
+through the C-ABI (include/rs.h); this module only marshals arguments.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+from .lib import (ConfigError, DeviceError, Error, ValidationError, as_f64, as_i32,
+                  as_i64, check, context, profile_struct, ptr)
+
+__all__ = [
+    "Error", "ConfigError", "ValidationError", "DeviceError",
+    "LatencyProfile", "default_profile", "Prompt", "PrefixIndex", "PrefillCapacity",
+    "PrefixSelection", "DedupSavings", "select_prefix_length", "dedup_savings",
+    "unique_prefix_count_among", "dedup_map", "block_hashes", "PredictedPrompt",
+    "ActorGroup", "ResponseSpec", "assign", "integrate_decode_seconds",
+    "estimate_actor_time", "estimate_cost", "ScaleCandidate", "ScaleResult", "scale",
+    "lpt", "to_csr", "id_ranks",
+]
+
+
+# ------------------------------------------------------------------ profile
+@dataclass
+class LatencyProfile:
+    """proj/include/rollsim/profile.hpp:17-35 (tpot part)."""
+    batch_knots: List[float]
+    context_knots: List[float]
+    tpot_grid: List[List[float]]
+    rho: float = 0.0005
+    gpus_per_actor: int = 2
+
+    def struct(self):
+        return profile_struct(self.batch_knots, self.context_knots,
+                              np.asarray(self.tpot_grid, dtype=np.float64), self.rho)
+
+    def tpot_seconds(self, batch_size, context_len):
+        b = np.atleast_1d(as_f64(batch_size))
+        c = np.atleast_1d(as_f64(context_len))
+        b, c = np.broadcast_arrays(b, c)
+        b, c = as_f64(b), as_f64(c)
+        out = np.empty(b.shape, np.float64)
+        s, keep = self.struct()
+        ctx = context()
+        check(ctx.lib.rs_tpot_seconds(ctx.handle, C.byref(s), ptr(b, C.c_double),
+                                      ptr(c, C.c_double), b.size, ptr(out, C.c_double)))
+        return out if np.ndim(batch_size) or np.ndim(context_len) else float(out[0])
+
+
+def default_profile() -> LatencyProfile:
+    """default_profile() (proj/src/profile.cpp:159-185): same grid bits."""
+    bk = [1, 2, 4, 8, 16, 32, 64, 128, 256]
+    ck = [128, 512, 1024, 2048, 4096]
+    grid = [[0.006 + 2e-5 * float(b) + 1.2e-6 * float(c) + 4.5e-8 * float(b) * float(c)
+             for c in ck] for b in bk]
+    return LatencyProfile([float(x) for x in bk], [float(x) for x in ck], grid, 0.0005, 2)
+
+
+# -------------------------------------------------------------------- dedup
+@dataclass
+class Prompt:
+    """proj/include/rollsim/workload.hpp:18-25."""
+    id: str
+    token_ids: Sequence[int]
+    ground_truth_len: int = 1
+
+    def prompt_len(self):
+        return len(self.token_ids)
+
+
+def to_csr(prompts):
+    """Batch (list of Prompt or token lists) -> (tokens int32, offsets int64)."""
+    seqs = [p.token_ids if isinstance(p, Prompt) else p for p in prompts]
+    lens = np.fromiter((len(s) for s in seqs), dtype=np.int64, count=len(seqs))
+    off = np.zeros(len(seqs) + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    tok = np.empty(int(off[-1]), np.int32)
+    for i, s in enumerate(seqs):
+        tok[off[i]:off[i + 1]] = s
+    return tok, off
+
+
+def _csr_args(batch):
+    if isinstance(batch, tuple) and len(batch) == 2:
+        tok, off = as_i32(batch[0]), as_i64(batch[1])
+    else:
+        tok, off = to_csr(batch)
+    if tok.size == 0:
+        tok = np.zeros(1, np.int32)
+    return tok, off
+
+
+class PrefixIndex:
+    """PrefixIndex (proj/include/rollsim/dedup.hpp:20-48) built on the GPU."""
+
+    def __init__(self, handle, ctx):
+        self._h = handle
+        self._ctx = ctx
+        b, mn, mx, tot = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
+        check(ctx.lib.rs_prefix_index_info(handle, C.byref(b), C.byref(mn), C.byref(mx),
+                                           C.byref(tot)))
+        self._batch, self._min, self._max, self._total = b.value, mn.value, mx.value, tot.value
+
+    @staticmethod
+    def build(batch) -> "PrefixIndex":
+        tok, off = _csr_args(batch)
+        ctx = context()
+        h = C.c_void_p()
+        check(ctx.lib.rs_prefix_index_build(ctx.handle, ptr(tok, C.c_int32), ptr(off, C.c_int64),
+                                            len(off) - 1, C.byref(h)))
+        return PrefixIndex(h, ctx)
+
+    @staticmethod
+    def build_device(d_tokens, d_offsets, batch) -> "PrefixIndex":
+        ctx = context()
+        h = C.c_void_p()
+        check(ctx.lib.rs_prefix_index_build_device(ctx.handle, C.c_void_p(d_tokens),
+                                                   C.c_void_p(d_offsets), batch, C.byref(h)))
+        return PrefixIndex(h, ctx)
+
+    def __del__(self):
+        try:
+            if self._h:
+                self._ctx.lib.rs_prefix_index_free(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def _acc(self, fn, l):
+        out = C.c_int64()
+        check(fn(self._h, int(l), C.byref(out)))
+        return out.value
+
+    def unique_prefix_count(self, prefix_len):
+        return self._acc(self._ctx.lib.rs_unique_prefix_count, prefix_len)
+
+    def unique_prefix_tokens(self, prefix_len):
+        return self._acc(self._ctx.lib.rs_unique_prefix_tokens, prefix_len)
+
+    def remainder_tokens(self, prefix_len):
+        return self._acc(self._ctx.lib.rs_remainder_tokens, prefix_len)
+
+    def total_prompt_tokens(self):
+        return self._total
+
+    def min_prompt_len(self):
+        return self._min
+
+    def max_prompt_len(self):
+        return self._max
+
+    def batch_size(self):
+        return self._batch
+
+    def tables(self):
+        m = self._max
+        arrs = [np.zeros(m + 1, np.int64)] + [np.zeros(m + 2, np.int64) for _ in range(4)]
+        check(self._ctx.lib.rs_prefix_index_tables(self._h, *[ptr(a, C.c_int64) for a in arrs]))
+        return arrs
+
+
+@dataclass
+class PrefillCapacity:
+    max_unique_prefixes: int = 64
+    gpu_count: int = 1
+
+
+@dataclass
+class PrefixSelection:
+    prefix_len: int = 0
+    capacity_exceeded: bool = False
+
+
+@dataclass
+class DedupSavings:
+    raw_prefill_tokens: int = 0
+    dedup_prefill_tokens: int = 0
+    saved_fraction: float = 0.0
+
+
+def select_prefix_length(index: PrefixIndex, capacity: PrefillCapacity, l_min, l_max):
+    ln, ex = C.c_int32(), C.c_int32()
+    check(index._ctx.lib.rs_select_prefix_length(index._h, capacity.max_unique_prefixes,
+                                                 capacity.gpu_count, l_min, l_max,
+                                                 C.byref(ln), C.byref(ex)))
+    return PrefixSelection(ln.value, bool(ex.value))
+
+
+def dedup_savings(index: PrefixIndex, l_star, responses_per_prompt):
+    raw, dd, fr = C.c_int64(), C.c_int64(), C.c_double()
+    check(index._ctx.lib.rs_dedup_savings(index._h, l_star, responses_per_prompt,
+                                          C.byref(raw), C.byref(dd), C.byref(fr)))
+    return DedupSavings(raw.value, dd.value, fr.value)
+
+
+def unique_prefix_count_among(prompts, prefix_len):
+    tok, off = _csr_args(prompts)
+    ctx = context()
+    out = C.c_int64()
+    check(ctx.lib.rs_unique_prefix_count_among(ctx.handle, ptr(tok, C.c_int32),
+                                               ptr(off, C.c_int64), len(off) - 1,
+                                               prefix_len, C.byref(out)))
+    return out.value
+
+
+def dedup_map(prompts, prefix_len):
+    tok, off = _csr_args(prompts)
+    n = len(off) - 1
+    lab = np.zeros(max(n, 1), np.int32)
+    ctx = context()
+    check(ctx.lib.rs_dedup_map(ctx.handle, ptr(tok, C.c_int32), ptr(off, C.c_int64), n,
+                               prefix_len, ptr(lab, C.c_int32)))
+    return lab[:n]
+
+
+def block_hashes(prompts, block_tokens=16):
+    tok, off = _csr_args(prompts)
+    n = len(off) - 1
+    nb = int(sum((int(off[i + 1] - off[i]) + block_tokens - 1) // block_tokens for i in range(n)))
+    out = np.zeros(max(nb, 1), np.uint64)
+    ctx = context()
+    check(ctx.lib.rs_block_hashes(ctx.handle, ptr(tok, C.c_int32), ptr(off, C.c_int64), n,
+                                  block_tokens, ptr(out, C.c_uint64)))
+    return out[:nb]
+
+
+# ------------------------------------------------------------------ planner
+@dataclass
+class PredictedPrompt:
+    """proj/include/rollsim/planner.hpp:16-20."""
+    id: str
+    prompt_len: int = 0
+    predicted_len: float = 1.0
+
+
+@dataclass
+class ActorGroup:
+    """proj/include/rollsim/planner.hpp:22-28."""
+    actor_id: int = 0
+    prompt_ids: List[str] = field(default_factory=list)
+    prompt_lens: List[int] = field(default_factory=list)
+    predicted_lengths: List[float] = field(default_factory=list)
+    gpu_count: int = 1
+
+
+@dataclass
+class ResponseSpec:
+    prompt_len: int = 0
+    target_len: float = 1.0
+
+
+@dataclass
+class ScaleCandidate:
+    n_actors: int = 0
+    t_total: float = 0.0
+    t_penalty: float = 0.0
+    cost: float = 0.0
+    t_norm: float = 0.0
+    c_norm: float = 0.0
+    score: float = 0.0
+
+
+@dataclass
+class ScaleResult:
+    n_star: int = 0
+    candidates: List[ScaleCandidate] = field(default_factory=list)
+    groups: List[ActorGroup] = field(default_factory=list)
+    actor_times: List[float] = field(default_factory=list)
+
+
+def id_ranks(ids):
+    """Rank of each id under std::string ordering (unsigned bytewise)."""
+    keys = [s.encode() for s in ids]
+    order = sorted(range(len(keys)), key=keys.__getitem__)
+    rank = np.empty(len(keys), np.int32)
+    rank[order] = np.arange(len(keys), dtype=np.int32)
+    return rank
+
+
+def _soa(predicted):
+    pred = as_f64([p.predicted_len for p in predicted])
+    plen = as_i32([p.prompt_len for p in predicted])
+    return pred, plen, id_ranks([p.id for p in predicted])
+
+
+def _groups_from_order(predicted, order, n, gpus):
+    P = len(predicted)
+    q, r = divmod(P, n)
+    groups, pos = [], 0
+    for a in range(n):
+        size = q + (1 if a < r else 0)
+        g = ActorGroup(actor_id=a, gpu_count=gpus)
+        for k in order[pos:pos + size]:
+            p = predicted[int(k)]
+            g.prompt_ids.append(p.id)
+            g.prompt_lens.append(p.prompt_len)
+            g.predicted_lengths.append(p.predicted_len)
+        groups.append(g)
+        pos += size
+    return groups
+
+
+def assign(predicted: Sequence[PredictedPrompt], n_actors: int, gpus_per_actor: int):
+    """assign (proj/src/planner.cpp:16-51)."""
+    ctx = context()
+    P = len(predicted)
+    pred, _, rank = _soa(predicted) if P else (as_f64([0.0]), None, as_i32([0]))
+    order = np.zeros(max(P, 1), np.int32)
+    goff = np.zeros(max(n_actors, 0) + 2, np.int32)
+    check(ctx.lib.rs_assign(ctx.handle, ptr(pred, C.c_double), ptr(rank, C.c_int32), P,
+                            n_actors, ptr(order, C.c_int32), ptr(goff, C.c_int32)))
+    return _groups_from_order(predicted, order[:P], n_actors, gpus_per_actor)
+
+
+def integrate_decode_seconds(responses: Sequence[ResponseSpec], profile: LatencyProfile):
+    """integrate_decode_seconds (proj/src/planner.cpp:88-130)."""
+    ctx = context()
+    n = len(responses)
+    plen = as_i32([r.prompt_len for r in responses] or [0])
+    tgt = as_f64([r.target_len for r in responses] or [1.0])
+    s, keep = profile.struct()
+    out = C.c_double()
+    check(ctx.lib.rs_integrate_decode_seconds(ctx.handle, ptr(plen, C.c_int32),
+                                              ptr(tgt, C.c_double), n, C.byref(s),
+                                              C.byref(out)))
+    return out.value
+
+
+def estimate_actor_time(group: ActorGroup, profile: LatencyProfile, responses_per_prompt):
+    """estimate_actor_time (proj/src/planner.cpp:132-146)."""
+    ctx = context()
+    n = len(group.prompt_ids)
+    plen = as_i32(list(group.prompt_lens) or [0])
+    pred = as_f64(list(group.predicted_lengths) or [1.0])
+    s, keep = profile.struct()
+    out = C.c_double()
+    check(ctx.lib.rs_estimate_actor_time(ctx.handle, ptr(plen, C.c_int32), ptr(pred, C.c_double),
+                                         n, C.byref(s), responses_per_prompt, C.byref(out)))
+    return out.value
+
+
+def estimate_cost(groups: Sequence[ActorGroup], profile: LatencyProfile, responses_per_prompt,
+                  times_out=None):
+    """estimate_cost (proj/src/planner.cpp:148-157)."""
+    ctx = context()
+    plen = as_i32([l for g in groups for l in g.prompt_lens] or [0])
+    pred = as_f64([p for g in groups for p in g.predicted_lengths] or [1.0])
+    goff = np.zeros(len(groups) + 1, np.int32)
+    goff[1:] = np.cumsum([len(g.prompt_ids) for g in groups]) if groups else []
+    gpus = as_i32([g.gpu_count for g in groups] or [0])
+    times = np.zeros(max(len(groups), 1), np.float64)
+    s, keep = profile.struct()
+    out = C.c_double()
+    check(ctx.lib.rs_estimate_cost(ctx.handle, ptr(plen, C.c_int32), ptr(pred, C.c_double),
+                                   ptr(goff, C.c_int32), ptr(gpus, C.c_int32), len(groups),
+                                   C.byref(s), responses_per_prompt, C.byref(out),
+                                   ptr(times, C.c_double)))
+    if times_out is not None:
+        times_out.extend(times[:len(groups)].tolist())
+    return out.value
+
+
+TimePenaltyFn = Callable[[int, List[ActorGroup], List[float]], float]
+
+
+def scale(predicted: Sequence[PredictedPrompt], profile: LatencyProfile, responses_per_prompt,
+          n_min, n_max, lambda_, gpus_per_actor, penalty: Optional[TimePenaltyFn] = None):
+    """scale (proj/src/planner.cpp:159-218). A Python `penalty` is called per
+    candidate in ascending N with that candidate's groups and times, like
+    TimePenaltyFn (planner.hpp:80-82)."""
+    ctx = context()
+    P = len(predicted)
+    if P:
+        pred, plen, rank = _soa(predicted)
+    else:
+        pred, plen, rank = as_f64([1.0]), as_i32([0]), as_i32([0])
+    Cn = max(n_max - n_min + 1, 1)
+    T = max((n_max * (n_max + 1) - (n_min - 1) * n_min) // 2, 1)
+    arr = {k: np.zeros(Cn, np.float64) for k in ("t_total", "t_penalty", "cost", "t_norm",
+                                                 "c_norm", "score")}
+    idle = np.zeros(Cn, np.int64)
+    order = np.zeros(max(P, 1), np.int32)
+    gt = np.zeros(T, np.float64)
+    at = np.zeros(max(n_max, 1), np.float64)
+    out = _abi.RsScaleOut(0, *[ptr(arr[k], C.c_double) for k in
+                               ("t_total", "t_penalty", "cost", "t_norm", "c_norm", "score")],
+                          ptr(idle, C.c_int64), ptr(order, C.c_int32), ptr(at, C.c_double),
+                          ptr(gt, C.c_double) if penalty else None)
+    s, keep = profile.struct()
+    check(ctx.lib.rs_scale(ctx.handle, ptr(pred, C.c_double), ptr(plen, C.c_int32),
+                           ptr(rank, C.c_int32), P, C.byref(s), responses_per_prompt, n_min,
+                           n_max, float(lambda_), gpus_per_actor, None, C.byref(out)))
+    n_star = out.n_star
+    if penalty is not None:
+        pen = np.zeros(Cn, np.float64)
+        base = 0
+        for i, n in enumerate(range(n_min, n_max + 1)):
+            groups = _groups_from_order(predicted, order[:P], n, gpus_per_actor)
+            pen[i] = float(penalty(n, groups, gt[base:base + n].tolist()))
+            base += n
+        ns = C.c_int32()
+        check(ctx.lib.rs_scale_select(ctx.handle, ptr(arr["t_total"], C.c_double),
+                                      ptr(pen, C.c_double), ptr(arr["cost"], C.c_double), Cn,
+                                      n_min, float(lambda_), ptr(arr["t_norm"], C.c_double),
+                                      ptr(arr["c_norm"], C.c_double),
+                                      ptr(arr["score"], C.c_double), C.byref(ns)))
+        arr["t_penalty"] = pen
+        n_star = ns.value
+        b = (n_star * (n_star - 1) - n_min * (n_min - 1)) // 2
+        at[:n_star] = gt[b:b + n_star]
+    res = ScaleResult(n_star=n_star)
+    for i, n in enumerate(range(n_min, n_max + 1)):
+        res.candidates.append(ScaleCandidate(n, arr["t_total"][i], arr["t_penalty"][i],
+                                             arr["cost"][i], arr["t_norm"][i], arr["c_norm"][i],
+                                             arr["score"][i]))
+    res.groups = _groups_from_order(predicted, order[:P], n_star, gpus_per_actor)
+    res.actor_times = at[:n_star].tolist()
+    res.idle_slot_ticks = idle
+    return res
+
+
+def lpt(pred, id_rank, responses_per_prompt, n_min, n_max):
+    """LPT extension: (makespan, idle) per candidate N."""
+    ctx = context()
+    pred = as_f64(pred)
+    rank = as_i32(id_rank) if id_rank is not None else None
+    C_ = n_max - n_min + 1
+    mk = np.zeros(max(C_, 1), np.int64)
+    idle = np.zeros(max(C_, 1), np.int64)
+    check(ctx.lib.rs_lpt(ctx.handle, ptr(pred, C.c_double),
+                         ptr(rank, C.c_int32) if rank is not None else None, len(pred),
+                         responses_per_prompt, n_min, n_max, ptr(mk, C.c_int64),
+                         ptr(idle, C.c_int64)))
+    return mk[:C_], idle[:C_]

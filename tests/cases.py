@@ -1,0 +1,98 @@
+"""Seeded test inputs shared by the CPU and GPU suites.
+
+Generators follow the reference tests' own fixtures:
+random_batch (proj/tests/test_dedup.cpp:52-65), criterion-2 batches
+(proj/tests/acceptance_main.cpp:97-106), constant_profile
+(proj/tests/helpers.hpp:38-50), small_profile (proj/tests/test_profile.cpp:26-38).
+"""
+import numpy as np
+
+from paper_2602_22718_b200 import _abi
+from paper_2602_22718_b200.rollsim import LatencyProfile, default_profile
+
+MASK = (1 << 64) - 1
+
+
+class Rng:
+    """rollsim::Rng (proj/include/rollsim/rng.hpp:14-49), integer draws only."""
+
+    def __init__(self, seed):
+        self.s = seed & MASK
+
+    def next_u64(self):
+        self.s = (self.s + 0x9E3779B97F4A7C15) & MASK
+        z = self.s
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK
+        return z ^ (z >> 31)
+
+    def uniform(self):
+        return (self.next_u64() >> 11) * 2.0 ** -53
+
+    def uniform_range(self, lo, hi):
+        return lo + (hi - lo) * self.uniform()
+
+    def uniform_int(self, lo, hi):
+        return lo + self.next_u64() % (hi - lo + 1)
+
+
+def csr(seqs):
+    off = np.zeros(len(seqs) + 1, np.int64)
+    off[1:] = np.cumsum([len(s) for s in seqs]) if seqs else []
+    tok = np.array([t for s in seqs for t in s], dtype=np.int32)
+    return tok, off
+
+
+def random_batch(rng, max_count=14, max_len=10, alphabet=3, min_len=1):
+    count = rng.uniform_int(1, max_count)
+    return [[rng.uniform_int(0, alphabet - 1) for _ in range(rng.uniform_int(min_len, max_len))]
+            for _ in range(count)]
+
+
+def constant_profile(tpot, rho=0.0005, gpus=2):
+    return LatencyProfile([1.0, 4096.0], [1.0, float(1 << 20)], [[tpot, tpot], [tpot, tpot]],
+                          rho, gpus)
+
+
+def small_profile():
+    return LatencyProfile([1.0, 4.0, 16.0], [100.0, 1000.0],
+                          [[0.010, 0.020], [0.012, 0.026], [0.020, 0.050]], 0.0005, 2)
+
+
+def profiles():
+    return {"default": default_profile(), "small": small_profile(),
+            "constant": constant_profile(0.01)}
+
+
+def random_predicted(rng, count, pred_lo=1.0, pred_hi=400.0, plen_lo=8, plen_hi=400,
+                     integer=False):
+    pred = [float(rng.uniform_int(int(pred_lo), int(pred_hi))) if integer
+            else rng.uniform_range(pred_lo, pred_hi) for _ in range(count)]
+    plen = [rng.uniform_int(plen_lo, plen_hi) for _ in range(count)]
+    return np.array(pred, np.float64), np.array(plen, np.int32)
+
+
+def c4_spec(n_scenarios, count=65536, first=0, seed=1234):
+    """The C4/C3 Monte-Carlo scenario definition."""
+    return _abi.RsScenarioSpec(seed, first, n_scenarios, count, 384.0, 96.0, 16, 1024,
+                               1024.0, 1.0, 16384.0)
+
+
+def c2_tokens(n_prompts=65536, shared=2048, unique=512, vocab=32000, seed=1):
+    """C2: Rng(1): a shared system prompt then per-prompt unique suffixes
+    (SURVEY.md §8d), vectorised splitmix64."""
+    n = shared + n_prompts * unique
+    k = np.arange(1, n + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed) + k * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    draws = (z % np.uint64(vocab)).astype(np.int32)
+    sys_prompt = draws[:shared]
+    uniq = draws[shared:].reshape(n_prompts, unique)
+    tok = np.empty((n_prompts, shared + unique), np.int32)
+    tok[:, :shared] = sys_prompt
+    tok[:, shared:] = uniq
+    off = np.arange(n_prompts + 1, dtype=np.int64) * (shared + unique)
+    return tok.reshape(-1), off
