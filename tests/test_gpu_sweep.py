@@ -1,0 +1,117 @@
+"""GPU parity for the Monte-Carlo scaling sweep (C4): device scenario
+generation, per (scenario, candidate) t_total / cost bit-exact, n_star exact,
+aggregates consistent."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from cases import c4_spec, profiles
+from oracle_lib import port
+from paper_2602_22718_b200 import _abi
+from paper_2602_22718_b200.lib import check, context, ptr
+from paper_2602_22718_b200.rollsim import default_profile
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.asarray(a, np.float64).view(np.uint64)
+
+
+def rs_generate(spec):
+    ctx = context()
+    n = spec.n_scenarios * spec.count
+    pred = np.zeros(n, np.float64)
+    plen = np.zeros(n, np.int32)
+    check(ctx.lib.rs_generate_scenarios(ctx.handle, C.byref(spec), pred.ctypes.data_as(C.c_void_p),
+                                        plen.ctypes.data_as(C.c_void_p), 0))
+    return pred, plen
+
+
+def rs_sweep(spec, prof, g, n_min, n_max, lam, gpus, arrays=None):
+    ctx = context()
+    S, Cn = spec.n_scenarios, n_max - n_min + 1
+    out = {"t_total": np.zeros(S * Cn), "cost": np.zeros(S * Cn),
+           "idle": np.zeros(S * Cn, np.int64), "n_star": np.zeros(S, np.int32),
+           "hist": np.zeros(Cn, np.int32), "sum_t": np.zeros(Cn), "sum_c": np.zeros(Cn)}
+    so = _abi.RsSweepOut(*[out[k].ctypes.data for k in
+                           ("t_total", "cost", "idle", "n_star", "hist", "sum_t", "sum_c")])
+    s, keep = prof.struct()
+    if arrays is None:
+        check(ctx.lib.rs_sweep(ctx.handle, C.byref(spec), C.byref(s), g, n_min, n_max, lam, gpus,
+                               C.byref(so), 0))
+    else:
+        pred, plen = arrays
+        check(ctx.lib.rs_sweep_arrays(ctx.handle, pred.ctypes.data, plen.ctypes.data, S,
+                                      spec.count, C.byref(s), g, n_min, n_max, lam, gpus,
+                                      C.byref(so), 0))
+    out["t_total"] = out["t_total"].reshape(S, Cn)
+    out["cost"] = out["cost"].reshape(S, Cn)
+    out["idle"] = out["idle"].reshape(S, Cn)
+    return out
+
+
+def test_generator_matches_oracle():
+    spec = c4_spec(3, count=20000, first=17)
+    p1, l1 = rs_generate(spec)
+    p2, l2 = port().generate_scenarios(spec)
+    assert np.array_equal(bits(p1), bits(p2)) and np.array_equal(l1, l2)
+    assert p1.min() >= 1.0 and p1.max() <= 16384.0 and (p1 == 16384.0).any()
+
+
+def check_sweep(spec, n_min, n_max, prof=None, lam=0.7, g=8, arrays=False):
+    prof = prof or default_profile()
+    pred, plen = port().generate_scenarios(spec)
+    got = rs_sweep(spec, prof, g, n_min, n_max, lam, 2, (pred, plen) if arrays else None)
+    S, P = spec.n_scenarios, spec.count
+    tt, cc, ns = port().sweep_arrays(pred, plen, S, P, prof, g, n_min, n_max, lam, 2, threads=8)
+    assert np.array_equal(bits(got["t_total"]), bits(tt))
+    assert np.array_equal(bits(got["cost"]), bits(cc))
+    assert np.array_equal(got["n_star"], ns)
+    for s in range(S):
+        idle = port().scale_idle(pred[s * P:(s + 1) * P], None, g, n_min, n_max)
+        assert np.array_equal(got["idle"][s], idle)
+    hist = np.bincount(ns - n_min, minlength=n_max - n_min + 1)
+    assert np.array_equal(got["hist"], hist)
+    np.testing.assert_allclose(got["sum_t"], tt.sum(axis=0), rtol=1e-12)
+    np.testing.assert_allclose(got["sum_c"], cc.sum(axis=0), rtol=1e-12)
+    return got
+
+
+def test_sweep_small_bitwise():
+    check_sweep(c4_spec(12, count=3000, first=5), 1, 64)
+
+
+def test_sweep_arrays_bitwise_and_nmin():
+    check_sweep(c4_spec(5, count=2048, first=100), 3, 50, arrays=True, lam=0.3, g=4)
+
+
+def test_sweep_other_profiles():
+    for name in ("small", "constant"):
+        check_sweep(c4_spec(3, count=1024, first=9), 1, 32, prof=profiles()[name], lam=1.0)
+
+
+def test_sweep_unbounded_arrays_generic_path():
+    spec = c4_spec(3, count=1500, first=1)
+    pred, plen = port().generate_scenarios(spec)
+    pred = pred * 7.0  # pushes finish ticks past the bucketed range
+    got = rs_sweep(spec, default_profile(), 8, 1, 40, 0.7, 2, (pred, plen))
+    tt, cc, ns = port().sweep_arrays(pred, plen, 3, 1500, default_profile(), 8, 1, 40, 0.7, 2)
+    assert np.array_equal(bits(got["t_total"]), bits(tt)) and np.array_equal(got["n_star"], ns)
+
+
+@pytest.mark.slow
+def test_sweep_full_size_scenarios_bitwise():
+    """C4 at full scenario size: 65,536 prompts x G=8, N in [1, 256]."""
+    check_sweep(c4_spec(2, count=65536, first=4242), 1, 256)
+
+
+def test_sweep_select_matches_oracle():
+    rng = np.random.RandomState(0)
+    st, sc = rng.rand(64) * 100, rng.rand(64) * 3
+    ctx = context()
+    ns = C.c_int32()
+    check(ctx.lib.rs_sweep_select(ptr(st, C.c_double), ptr(sc, C.c_double), 1000, 64, 1, 0.7,
+                                  C.byref(ns)))
+    assert ns.value == port().sweep_select(st, sc, 1000, 1, 0.7)
