@@ -1,0 +1,423 @@
+"""Benchmark of the B200-native RLHFless planning core (one JSON line).
+
+Headline (BASELINE.json metric, config C4): the cost-aware actor-scaling
+sweep — 10,000 Monte-Carlo length scenarios x 256 candidate actor counts,
+65,536 prompts x G=8 responses per scenario — reported as scenario x
+candidate evals/s. One step = the whole sweep. Scenarios are sharded in
+contiguous blocks over ranks (strong scaling: total work fixed); the only
+collective is an NCCL all-reduce of the per-candidate aggregates.
+
+  value        device-resident: scenarios generated in HBM, outputs in HBM
+  e2e          the public C-ABI call with HOST output buffers (rs_sweep,
+               device_ptrs=0): device->host copies inside the timed region
+  roofline     dominant kernel (group_eval), CUDA events inside the run
+  cpu_baseline the reference's own scale() (oracle/_ref) on host cores
+  dedup        secondary metric (C2 prefix dedup, tokens/s), same fields
+
+`--impl reference` runs only the reference CPU arm (rank 0), same metric.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+sys.path.insert(0, str(REPO / "tests"))
+
+METRIC = "scenario×candidate evals/sec (scaling sweep)"
+EVAL_BYTES = 65536 * 12 + 16  # P*(8 B pred + 4 B plen) + 16 B out
+
+
+def peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def init_dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from cases import c4_spec
+    from oracle_lib import port, ref
+    from paper_2602_22718_b200.rollsim import default_profile
+    R = ref()
+    kind = "reference" if R is not None else "port"
+    impl = R if R is not None else port()
+    threads = os.cpu_count() or 1
+    n_cand = args.n_max - args.n_min + 1
+    prof = default_profile()
+    times = []
+    for step in range(args.warmup + args.steps):
+        spec = c4_spec(threads, count=args.prompts, first=step * threads)
+        pred, plen = port().generate_scenarios(spec)
+        t0 = time.perf_counter()
+        impl.sweep_arrays(pred, plen, threads, args.prompts, prof, args.G, args.n_min,
+                          args.n_max, args.lam, 2, threads=threads)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+    evals = threads * n_cand
+    v = evals * len(times) / sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (Monte-Carlo scenarios, DESIGN.md §4.1)",
+        "config": config(args, world),
+        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": threads, "kind": kind,
+                         "sample": f"{threads} scenarios x {n_cand} candidates per step "
+                                   f"(one scenario per thread), {args.prompts} prompts x G={args.G}"},
+        "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config(args, world):
+    return {"workload": f"C4 actor-scaling sweep: {args.scenarios} scenarios x "
+                        f"{args.n_max - args.n_min + 1} candidate N, {args.prompts} prompts x "
+                        f"G={args.G} per scenario",
+            "scenarios": args.scenarios, "candidates": [args.n_min, args.n_max],
+            "prompts": args.prompts, "G": args.G, "lambda": args.lam, "gpus_per_actor": 2,
+            "profile": "default_profile()", "parallelism": f"scenario-sharded x{world}",
+            "l2": "inputs larger than L2 (per-batch scenario scratch ~2 GiB)"}
+
+
+# ----------------------------------------------------------------- our arm
+def cpu_baseline_sweep(args):
+    from cases import c4_spec
+    from oracle_lib import port, ref
+    from paper_2602_22718_b200.rollsim import default_profile
+    R = ref()
+    kind = "reference" if R is not None else "port"
+    impl = R if R is not None else port()
+    threads = os.cpu_count() or 1
+    n = threads * args.cpu_rounds
+    pred, plen = port().generate_scenarios(c4_spec(n, count=args.prompts, first=0))
+    t0 = time.perf_counter()
+    impl.sweep_arrays(pred, plen, n, args.prompts, default_profile(), args.G, args.n_min,
+                      args.n_max, args.lam, 2, threads=threads)
+    dt = time.perf_counter() - t0
+    n_cand = args.n_max - args.n_min + 1
+    return {"value": n * n_cand / dt, "unit": "evals/s", "cores": threads, "kind": kind,
+            "sample": f"{n} scenarios x {n_cand} candidates ({args.prompts} prompts x G={args.G}), "
+                      f"{threads} threads, {dt:.1f} s"}
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+    from cases import c4_spec
+    from paper_2602_22718_b200 import _abi
+    from paper_2602_22718_b200.lib import check, context, ensure_built
+    from paper_2602_22718_b200.rollsim import default_profile
+
+    ensure_built()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = context(local)
+    # A dedicated torch stream shared with the library so CUDA events and
+    # NCCL collectives order against our kernels (NULL would select the
+    # context's own stream).
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    prof = default_profile()
+    ps, keep = prof.struct()
+    n_cand = args.n_max - args.n_min + 1
+    s0 = rank * args.scenarios // world
+    s1 = (rank + 1) * args.scenarios // world
+    S = s1 - s0
+    spec = c4_spec(S, count=args.prompts, first=s0)
+    t_total = torch.empty(S * n_cand, dtype=torch.float64, device=dev)
+    cost = torch.empty(S * n_cand, dtype=torch.float64, device=dev)
+    idle = torch.empty(S * n_cand, dtype=torch.int64, device=dev)
+    n_star = torch.empty(S, dtype=torch.int32, device=dev)
+    agg_t = torch.empty(n_cand, dtype=torch.float64, device=dev)
+    agg_c = torch.empty(n_cand, dtype=torch.float64, device=dev)
+    agg_h = torch.empty(n_cand, dtype=torch.int32, device=dev)
+    out_dev = _abi.RsSweepOut(t_total.data_ptr(), cost.data_ptr(), idle.data_ptr(),
+                              n_star.data_ptr(), agg_h.data_ptr(), agg_t.data_ptr(),
+                              agg_c.data_ptr())
+
+    def step_device():
+        check(ctx.lib.rs_sweep(ctx.handle, C.byref(spec), C.byref(ps), args.G, args.n_min,
+                               args.n_max, args.lam, 2, C.byref(out_dev), 1))
+        if world > 1:
+            dist.all_reduce(agg_t)
+            dist.all_reduce(agg_c)
+            dist.all_reduce(agg_h)
+
+    def timed(fn, k):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(k):
+            fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    launches0 = ctx.kernel_launches()
+    ctx.enable_kernel_timing(True)
+    ctx.reset_kernel_timing()
+    with ClockSampler(local) as clk:
+        ms = timed(step_device, args.steps)
+    launches = (ctx.kernel_launches() - launches0) // args.steps
+    ge_ms, ge_n = ctx.kernel_time("group_eval")
+    ctx.enable_kernel_timing(False)
+    total_evals = args.scenarios * n_cand
+    value = total_evals * args.steps / (ms / 1e3)
+
+    # e2e: the same call with host (pinned) output buffers
+    pin = {k: torch.empty(S * n_cand, dtype=t, pin_memory=True)
+           for k, t in (("t", torch.float64), ("c", torch.float64), ("i", torch.int64))}
+    pin_ns = torch.empty(S, dtype=torch.int32, pin_memory=True)
+    pin_agg = [torch.empty(n_cand, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    pin_h = torch.empty(n_cand, dtype=torch.int32, pin_memory=True)
+    out_host = _abi.RsSweepOut(pin["t"].data_ptr(), pin["c"].data_ptr(), pin["i"].data_ptr(),
+                               pin_ns.data_ptr(), pin_h.data_ptr(), pin_agg[0].data_ptr(),
+                               pin_agg[1].data_ptr())
+    d2h = S * n_cand * 24 + S * 4 + n_cand * 20
+    h2d = C.sizeof(spec) + 8 * (9 + 5 + 45)
+
+    def step_host():
+        check(ctx.lib.rs_sweep(ctx.handle, C.byref(spec), C.byref(ps), args.G, args.n_min,
+                               args.n_max, args.lam, 2, C.byref(out_host), 0))
+        if world > 1:
+            agg = torch.cat([pin_agg[0], pin_agg[1]]).to(dev)
+            dist.all_reduce(agg)
+            agg.cpu()
+
+    step_host()
+    e2e_ms = timed(step_host, max(1, args.steps // 2)) / max(1, args.steps // 2)
+    e2e = total_evals / (e2e_ms / 1e3)
+
+    # parity spot check of this run's first scenario against the oracle
+    parity = None
+    if rank == 0 and args.check:
+        from oracle_lib import port
+        pred, plen = port().generate_scenarios(c4_spec(1, count=args.prompts, first=0))
+        tt, cc, ns = port().sweep_arrays(pred, plen, 1, args.prompts, prof, args.G, args.n_min,
+                                         args.n_max, args.lam, 2)
+        got_t = t_total[:n_cand].cpu().numpy()
+        parity = bool(np.array_equal(got_t.view(np.uint64), tt[0].view(np.uint64)) and
+                      int(n_star[0].item()) == int(ns[0]))
+
+    peak, peak_kind = peaks()
+    ge_avg_ms = ge_ms / max(ge_n, 1)
+    per_launch_evals = total_evals / world * args.steps / max(ge_n, 1)
+    achieved = per_launch_evals * EVAL_BYTES / (ge_avg_ms / 1e3) / 1e9
+    traffic = None
+    tf = REPO / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("group_eval_bytes_per_launch")
+    result = {
+        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (device-generated Monte-Carlo scenarios, DESIGN.md §4.1)",
+        "config": config(args, world),
+        "e2e": {"value": e2e, "unit": "evals/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h * world},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": "group_eval",
+                     "peak_kind": peak_kind, "launch_ms": ge_avg_ms,
+                     "algorithmic_bytes_per_launch": per_launch_evals * EVAL_BYTES,
+                     "kernel_share_of_step": ge_ms / ms if ms else None},
+        "gpu_launches": int(launches),
+        "parity_first_scenario": parity,
+    }
+    if rank == 0:
+        result["clocks"] = clk.summary()
+        if world == 1 and not args.no_dedup:
+            result["dedup"] = bench_dedup(args, ctx, torch, dev, stream)
+        if world == 1 and not args.no_cpu:
+            result["cpu_baseline"] = cpu_baseline_sweep(args)
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def bench_dedup(args, ctx, torch, dev, stream):
+    """C2: PrefixIndex::build over 65,536 x 2,560 tokens (2,048 shared)."""
+    from cases import c2_tokens
+    from paper_2602_22718_b200.lib import check
+    tok, off = c2_tokens()
+    n_tok = int(tok.size)
+    d_tok = torch.from_numpy(tok).to(dev)
+    d_off = torch.from_numpy(off).to(dev)
+    h = C.c_void_p()
+    lib = ctx.lib
+
+    def build_dev():
+        check(lib.rs_prefix_index_build_device(ctx.handle, C.c_void_p(d_tok.data_ptr()),
+                                               C.c_void_p(d_off.data_ptr()), len(off) - 1,
+                                               C.byref(h)))
+        lib.rs_prefix_index_free(h)
+
+    for _ in range(3):
+        build_dev()
+    ctx.enable_kernel_timing(True)
+    ctx.reset_kernel_timing()
+    k = 5
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(k):
+        build_dev()
+    torch.cuda.synchronize()
+    dev_s = (time.perf_counter() - t0) / k
+    cmp_ms, cmp_n = ctx.kernel_time("dedup_compare_r0")
+    ctx.enable_kernel_timing(False)
+    pt = torch.from_numpy(tok).pin_memory()
+    po = torch.from_numpy(off).pin_memory()
+    tptr = pt.numpy().ctypes.data_as(C.POINTER(C.c_int32))
+    optr = po.numpy().ctypes.data_as(C.POINTER(C.c_int64))
+
+    def build_host():
+        check(lib.rs_prefix_index_build(ctx.handle, tptr, optr, len(off) - 1, C.byref(h)))
+        lib.rs_prefix_index_free(h)
+
+    build_host()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        build_host()
+    host_s = (time.perf_counter() - t0) / 3
+    peak, _ = peaks()
+    r0_ms = cmp_ms / max(cmp_n, 1)
+    achieved = n_tok * 4 / (r0_ms / 1e3) / 1e9
+    out = {
+        "metric": "prefix-dedup tokens/sec", "value": n_tok / dev_s, "unit": "tokens/s",
+        "config": {"workload": "C2 prefix dedup: 65536 prompts x (2048 shared + 512 unique) "
+                               "tokens, vocab 32000", "tokens": n_tok},
+        "ms_per_build": dev_s * 1e3,
+        "e2e": {"value": n_tok / host_s, "unit": "tokens/s", "h2d_bytes_per_step": n_tok * 4 + off.nbytes,
+                "d2h_bytes_per_step": 5 * 8 * 2562},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": "dedup_compare (round 1)",
+                     "launch_ms": r0_ms, "kernel_share_of_step": r0_ms / (dev_s * 1e3)},
+    }
+    if not args.no_cpu:
+        from oracle_lib import port, ref
+        R = ref()
+        impl = R if R is not None else port()
+        t0 = time.perf_counter()
+        impl.prefix_curves(tok, off, 1)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": n_tok / dt, "unit": "tokens/s", "cores": 1,
+                               "kind": "reference" if R is not None else "port",
+                               "sample": f"full C2 input, one PrefixIndex::build, {dt:.1f} s"}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scenarios", type=int, default=10000)
+    ap.add_argument("--prompts", type=int, default=65536)
+    ap.add_argument("--n-min", type=int, default=1)
+    ap.add_argument("--n-max", type=int, default=256)
+    ap.add_argument("--G", type=int, default=8)
+    ap.add_argument("--lam", type=float, default=0.7)
+    ap.add_argument("--cpu-rounds", type=int, default=1)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dedup", action="store_true")
+    ap.add_argument("--check", action="store_true", default=True)
+    args = ap.parse_args()
+    world, rank, local = init_dist()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -384,7 +384,8 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
     RS_CUDA_TRY(cudaMemsetAsync(st.b_cnt, 0, 4ull * c, ctx->stream));
     RS_CUDA_TRY(cudaMemsetAsync(st.counter, 0, 4, ctx->stream));
     int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)K + 7) / 8, 64 * ctx->num_sms));
-    RS_LAUNCH(ctx, "dedup_compare", compare_kernel, wblocks, 256, 0, st, cur, K, c - 1);
+    RS_LAUNCH(ctx, K == P - 1 ? "dedup_compare_r0" : "dedup_compare", compare_kernel, wblocks,
+              256, 0, st, cur, K, c - 1);
     int fb = (int)std::max<int64_t>(1, std::min<int64_t>((c + 255) / 256, 8 * ctx->num_sms));
     RS_LAUNCH(ctx, "dedup_finalize", finalize_kernel, fb, 256, 0, st, cur, c);
     int kb = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)K + 255) / 256, 8 * ctx->num_sms));

@@ -1,0 +1,781 @@
+// rs_fast.cu — the fast path of the scaling sweep on sm_100a.
+//
+// Applies when every finish tick ceil(pred) is in [1, 16384] and every
+// prompt_len in [0, 65535] (always true for the Monte-Carlo scenarios of
+// DESIGN.md §4.1); other inputs take the generic radix-sort path in
+// rs_planner.cu. Semantics are those of proj/src/planner.cpp (see the header
+// of rs_planner.cu); this file only changes how the work is laid out:
+//
+// build  (one CTA per scenario): counting sort by finish tick in shared
+//        memory, 16-byte records scattered into their bucket, each bucket
+//        ordered (pred desc, id asc) by one warp (bitonic in registers, or
+//        rank counting for wide buckets), then per-rank segment id and
+//        in-segment prefix / suffix prompt_len maxima, per-segment packed
+//        {finish | max_plen << 16, end_rank}.
+// eval   (persistent CTAs, one scenario's segment table staged in shared
+//        memory, 16-segment block maxima + sparse table for prefix-max
+//        queries, the clamped-batch tpot row and piece ends in shared
+//        memory): candidate groups with N >= 8 run one group per LANE, the
+//        lane walking its runs in ascending finish order and accumulating
+//        the FP64 total sequentially (exactly the reference order); the few
+//        huge groups (N < 8) run warp-cooperatively, 32 runs per step, the
+//        lane sums added in lane order by one lane.
+// reduce per (scenario, candidate): max / sequential cost sum / idle.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "rs_fast.cuh"
+
+namespace rs {
+
+size_t fast_ss_bytes(int64_t items, int S) {
+  int64_t segs = items + S;
+  return abytes(segs, 8) * 2 + abytes(S, 4) + abytes(items, 8) + abytes(items, 4) * 2 +
+         abytes(items, 16);
+}
+
+FastSS fast_ss_alloc(rs_ctx* ctx, const int64_t* d_off, int64_t items, int S) {
+  int64_t segs = items + S;
+  FastSS f;
+  f.item_off = d_off;
+  f.seg = arena_alloc<int2>(ctx, segs);
+  f.segCF = arena_alloc<int64_t>(ctx, segs);
+  f.nseg = arena_alloc<int32_t>(ctx, S);
+  f.rinfo = arena_alloc<int2>(ctx, items);
+  f.plen_r = arena_alloc<int32_t>(ctx, items);
+  f.order_r = arena_alloc<int32_t>(ctx, items);
+  f.rec = arena_alloc<int4>(ctx, items);
+  return f;
+}
+
+// ------------------------------------------------------------------ build --
+constexpr int kBuildT = 1024;
+constexpr int kWide = 4096;
+
+__device__ __forceinline__ bool before(double pa, int ia, double pb, int ib) {
+  return pa > pb || (pa == pb && ia < ib);
+}
+
+template <bool kGen>
+__global__ void __launch_bounds__(kBuildT)
+fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_io,
+                  int32_t* plen_io, FastSS ss, int* flags) {
+  extern __shared__ int32_t cur[];  // [kFastFmax + 2]
+  __shared__ int32_t wsum[32];
+  __shared__ long long wsum64[32];
+  __shared__ int bad;
+  const int s = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t i0 = ss.item_off[s];
+  const int P = (int)(ss.item_off[s + 1] - i0);
+  const int64_t so = i0 + s;
+  double* pred = pred_io + i0;
+  int32_t* plen = plen_io + i0;
+  for (int f = tid; f < kFastFmax + 2; f += kBuildT) cur[f] = 0;
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  const uint64_t seed = kGen ? hash_combine(gs.base_seed, (uint64_t)(gs.first + s)) : 0;
+  int lf = 0;
+  for (int i = tid; i < P; i += kBuildT) {
+    double p;
+    int32_t pl;
+    if (kGen) {
+      fast_gen(gs, nz, lnz, seed, i, &p, &pl);
+      pred[i] = p;
+      plen[i] = pl;
+    } else {
+      p = pred[i];
+      pl = plen[i];
+    }
+    double fc = ceil(p);
+    if (!(fc >= 1.0) || fc > (double)kFastFmax || pl < 0 || pl > kFastPlenMax) {
+      lf |= isfinite(p) ? kFlagBucketOverflow : kFlagNotFinite;
+      continue;
+    }
+    atomicAdd(&cur[(int)fc], 1);
+  }
+  if (lf) atomicOr(&bad, lf);
+  __syncthreads();
+  if (bad) {
+    if (tid == 0) atomicOr(flags, bad);
+    return;
+  }
+  // Descending exclusive scan over bins f = Fmax..1; thread t owns 16 bins.
+  constexpr int kPer = kFastFmax / kBuildT;
+  int cnt[kPer];
+  int csum = 0, nzc = 0;
+  long long cf = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    int f = kFastFmax - tid * kPer - j;
+    cnt[j] = cur[f];
+    csum += cnt[j];
+    nzc += cnt[j] ? 1 : 0;
+    cf += (long long)cnt[j] * f;
+  }
+  auto excl32 = [&](int v) -> int {
+    int incl = warp_incl_sum(v);
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int x = wsum[lane];
+      wsum[lane] = warp_incl_sum(x) - x;
+    }
+    __syncthreads();
+    int r = wsum[wid] + incl - v;
+    __syncthreads();
+    return r;
+  };
+  int start = excl32(csum);
+  int kbase = excl32(nzc);
+  long long cfb;
+  {
+    long long incl = warp_incl_sum(cf);
+    if (lane == 31) wsum64[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      long long x = wsum64[lane];
+      wsum64[lane] = warp_incl_sum(x) - x;
+    }
+    __syncthreads();
+    cfb = wsum64[wid] + incl - cf;
+  }
+  if (tid == kBuildT - 1) {
+    ss.nseg[s] = kbase + nzc;
+    ss.segCF[so + kbase + nzc] = cfb + cf;
+  }
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    int f = kFastFmax - tid * kPer - j;
+    cur[f] = start;
+    if (cnt[j]) {
+      ss.seg[so + kbase] = make_int2(f, start + cnt[j]);
+      ss.segCF[so + kbase] = cfb;
+      ++kbase;
+    }
+    start += cnt[j];
+    cfb += (long long)cnt[j] * f;
+  }
+  __syncthreads();
+  // Scatter 16-byte records into the buckets.
+  for (int i = tid; i < P; i += kBuildT) {
+    double p = pred[i];
+    int f = (int)ceil(p);
+    int pos = atomicAdd(&cur[f], 1);
+    long long bits = __double_as_longlong(p);
+    ss.rec[i0 + pos] = make_int4((int)(bits & 0xffffffffLL), (int)(bits >> 32), i, plen[i]);
+  }
+  __syncthreads();
+  const int D = ss.nseg[s];
+  for (int k = wid; k < D; k += kBuildT / 32) {
+    const int2 sk = ss.seg[so + k];
+    const int hi = sk.y;
+    const int lo = k == 0 ? 0 : ss.seg[so + k - 1].y;
+    const int m = hi - lo;
+    int mx;
+    if (m <= 32) {
+      int4 r = lane < m ? ss.rec[i0 + lo + lane] : make_int4(0, 0, INT32_MAX, 0);
+      double key = lane < m ? __longlong_as_double(((long long)r.y << 32) | (unsigned)r.x)
+                            : -INFINITY;
+      int idx = r.z, pl = r.w;
+#pragma unroll
+      for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          double ok = __shfl_xor_sync(0xffffffffu, key, stride);
+          int oi = __shfl_xor_sync(0xffffffffu, idx, stride);
+          int op = __shfl_xor_sync(0xffffffffu, pl, stride);
+          bool up = (lane & size) == 0;
+          bool lower = (lane & stride) == 0;
+          bool of = before(ok, oi, key, idx);
+          bool take = lower == up ? of : (!of && oi != idx);
+          if (take) {
+            key = ok;
+            idx = oi;
+            pl = op;
+          }
+        }
+      }
+      // in-segment prefix / suffix maxima over lanes [0, m)
+      int v = lane < m ? pl : INT32_MIN;
+      int pm = v, sm = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int u = __shfl_up_sync(0xffffffffu, pm, o);
+        if (lane >= o) pm = max(pm, u);
+        int w = __shfl_down_sync(0xffffffffu, sm, o);
+        if (lane + o < 32) sm = max(sm, w);
+      }
+      if (lane < m) {
+        int64_t r0 = i0 + lo + lane;
+        ss.plen_r[r0] = pl;
+        ss.order_r[r0] = idx;
+        ss.rinfo[r0] = make_int2(k, sm | (pm << 16));
+      }
+      mx = __shfl_sync(0xffffffffu, pm, m - 1);
+    } else if (m <= kWide) {
+      for (int e = lane; e < m; e += 32) {
+        int4 r = ss.rec[i0 + lo + e];
+        double key = __longlong_as_double(((long long)r.y << 32) | (unsigned)r.x);
+        int rank = 0;
+        for (int o = 0; o < m; ++o) {
+          int4 q = ss.rec[i0 + lo + o];
+          double ok = __longlong_as_double(((long long)q.y << 32) | (unsigned)q.x);
+          rank += before(ok, q.z, key, r.z) ? 1 : 0;
+        }
+        ss.plen_r[i0 + lo + rank] = r.w;
+        ss.order_r[i0 + lo + rank] = r.z;
+      }
+      __syncwarp();
+      int carry = INT32_MIN;
+      for (int c0 = 0; c0 < m; c0 += 32) {  // prefix maxima
+        int e = c0 + lane;
+        int v = e < m ? ss.plen_r[i0 + lo + e] : INT32_MIN;
+        int pm = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int u = __shfl_up_sync(0xffffffffu, pm, o);
+          if (lane >= o) pm = max(pm, u);
+        }
+        pm = max(pm, carry);
+        if (e < m) ss.rinfo[i0 + lo + e] = make_int2(k, pm << 16);
+        carry = __shfl_sync(0xffffffffu, pm, 31);
+      }
+      mx = carry;
+      __syncwarp();
+      carry = INT32_MIN;
+      for (int c0 = ((m - 1) / 32) * 32; c0 >= 0; c0 -= 32) {  // suffix maxima
+        int e = c0 + lane;
+        int v = e < m ? ss.plen_r[i0 + lo + e] : INT32_MIN;
+        int sm = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int w = __shfl_down_sync(0xffffffffu, sm, o);
+          if (lane + o < 32) sm = max(sm, w);
+        }
+        sm = max(sm, carry);
+        if (e < m) {
+          int2 ri = ss.rinfo[i0 + lo + e];
+          ss.rinfo[i0 + lo + e] = make_int2(k, ri.y | sm);
+        }
+        carry = __shfl_sync(0xffffffffu, sm, 0);
+      }
+    } else {
+      if (lane == 0) atomicOr(flags, kFlagBucketTooWide);
+      mx = 0;
+    }
+    if (lane == 0) ss.seg[so + k] = make_int2(sk.x | (mx << 16), hi);
+  }
+}
+
+int fast_build(rs_ctx* ctx, int S, const int64_t* d_off, double* pred, int32_t* plen,
+               FastSS ss, const GenSpec* gen, const double* nz, const double* lnz) {
+  (void)d_off;
+  const int smem = sizeof(int32_t) * (kFastFmax + 2);
+  RS_CUDA_TRY(cudaFuncSetAttribute(fast_build_kernel<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  RS_CUDA_TRY(cudaFuncSetAttribute(fast_build_kernel<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  GenSpec g{};
+  if (gen) {
+    g = *gen;
+    RS_LAUNCH(ctx, "fast_build", fast_build_kernel<true>, S, kBuildT, smem, g, nz, lnz, pred,
+              plen, ss, ctx->d_flags);
+  } else {
+    RS_LAUNCH(ctx, "fast_build", fast_build_kernel<false>, S, kBuildT, smem, g, nz, lnz, pred,
+              plen, ss, ctx->d_flags);
+  }
+  return RS_OK;
+}
+
+// ------------------------------------------------------------------- eval --
+constexpr int kEvalT = 768;
+constexpr int kEvalW = kEvalT / 32;
+constexpr int kNBlk = kMaxSeg / kBlk;  // 1024 blocks of 16 segments
+constexpr int kLevels = 11;            // floor(log2(1024)) + 1
+constexpr int kCoopCarry = 64;
+constexpr int kSegCap = 10752;         // segments staged in shared memory
+
+struct EvalShared {
+  int2 seg[kSegCap];
+  uint32_t pmsm[kSegCap];  // in-block prefix max | in-block suffix max << 16
+  uint16_t st[kLevels][kNBlk];
+  double top[kTopCap];
+  uint16_t pe[kTopCap];    // piece end - c_lo
+  double acc[kEvalW][32];
+  int32_t carry[kEvalW][kCoopCarry];
+  uint16_t lbuf[kEvalT][16];  // per-lane prefix maxima inside the first block
+  int task_next;
+  int lane_next;
+};
+
+// Device tpot rows of one (profile, G): rows[(live - 1) * ncm + (c - c_lo)]
+// = tpot(G * live, c) for live < live_top; live >= live_top uses `top`
+// (batch clamped to the last batch knot). Contexts and live counts are
+// 32-bit on this path (contexts <= 65535 + 16384).
+struct FastProf {
+  const double* top;
+  const double* rows;
+  const uint16_t* pe;
+  int c_lo, c_hi, cf_ceil, cb_ceil, cfront_m1, ncm, live_top;
+};
+
+// tpot_context_run_sum (proj/src/planner.cpp:61-84) for the live count
+// `live` (batch = G * live) over integer contexts [c0, c1].
+__device__ __forceinline__ double run_sum32(const FastProf& fp, int live, int c0, int c1) {
+  const double* row = live >= fp.live_top ? fp.top : fp.rows + (size_t)(live - 1) * fp.ncm;
+  double total = 0.0;
+  int c = c0;
+  while (c <= c1) {
+    const int e = c < fp.cf_ceil ? fp.cfront_m1
+                                 : (c >= fp.cb_ceil ? c1 : fp.c_lo + (int)fp.pe[c - fp.c_lo]);
+    const int pe = min(c1, e);
+    const double t0 = row[min(max(c, fp.c_lo), fp.c_hi) - fp.c_lo];
+    const double t1 = row[min(max(pe, fp.c_lo), fp.c_hi) - fp.c_lo];
+    total = dadd(total, dmul(dmul((double)(pe - c + 1), dadd(t0, t1)), 0.5));
+    c = pe + 1;
+  }
+  return total;
+}
+
+struct EvalArgs {
+  FastSS ss;
+  FastProf fp;  // global-memory tables (copied to shared memory per CTA)
+  CandRange cr;
+  int S;
+  int units;    // units per scenario
+  double* gt;
+  uint32_t* pmsm_scratch;  // per CTA, when a scenario exceeds kSegCap
+};
+
+__device__ __forceinline__ int64_t tri64(int64_t n) { return n * (n - 1) / 2; }
+
+__device__ __forceinline__ void flat_ng(int64_t flat, int n0, int* N, int* g) {
+  int64_t x = flat + tri64(n0);
+  int64_t n = (int64_t)floor((1.0 + sqrt(1.0 + 8.0 * (double)x)) * 0.5);
+  while (n > 1 && tri64(n) > x) --n;
+  while (tri64(n + 1) <= x) ++n;
+  *N = (int)n;
+  *g = (int)(x - tri64(n));
+}
+
+__device__ __forceinline__ int seg_f(int2 e) { return e.x & 0xffff; }
+__device__ __forceinline__ int seg_mx(int2 e) { return (e.x >> 16) & 0xffff; }
+
+struct SegView {
+  const int2* seg;
+  const uint32_t* pmsm;
+  const uint16_t (*st)[kNBlk];
+};
+
+__device__ __forceinline__ int rmq_blocks(const SegView& V, int jl, int jr) {
+  int len = jr - jl + 1;
+  int lev = 31 - __clz(len);
+  return max((int)V.st[lev][jl], (int)V.st[lev][jr - (1 << lev) + 1]);
+}
+
+// max MX over segments [l, r], l <= r (general, used by the coop path).
+__device__ __forceinline__ int range_max(const SegView& V, int l, int r) {
+  const int jl = l >> 4, jr = r >> 4;
+  if (jl == jr) {
+    int m = seg_mx(V.seg[l]);
+    for (int k = l + 1; k <= r; ++k) m = max(m, seg_mx(V.seg[k]));
+    return m;
+  }
+  int m = max((int)(V.pmsm[l] >> 16), (int)(V.pmsm[r] & 0xffff));
+  if (jl + 1 <= jr - 1) m = max(m, rmq_blocks(V, jl + 1, jr - 1));
+  return m;
+}
+
+// max plen over ranks [a, b) inside one run-segment.
+__device__ __forceinline__ int span_max(const FastSS& ss, int64_t i0, int a, int b) {
+  int m = INT32_MIN;
+  for (int r = a; r < b; ++r) m = max(m, ss.plen_r[i0 + r]);
+  return m;
+}
+
+// One group per warp (huge groups): 32 runs per step; the lane sums are
+// added in lane order (ascending finish) by lane 0.
+__device__ double coop_group(EvalShared& sh, const SegView& V, const EvalArgs& A,
+                             const FastProf& fp, int64_t i0, int a, int b, int wid) {
+  const int lane = threadIdx.x & 31;
+  const int2 ra = A.ss.rinfo[i0 + a];
+  const int2 rb = A.ss.rinfo[i0 + b - 1];
+  const int ka = ra.x, kb = rb.x;
+  if (ka == kb) {
+    int m = INT32_MIN;
+    for (int r = a + lane; r < b; r += 32) m = max(m, A.ss.plen_r[i0 + r]);
+    m = warp_max(m);
+    const int f = seg_f(V.seg[ka]);
+    return dadd(0.0, run_sum32(fp, b - a, m, m + f - 1));
+  }
+  const int va = ra.y & 0xffff;
+  const int vb = (rb.y >> 16) & 0xffff;
+  auto vk = [&](int k) -> int { return k == ka ? va : (k == kb ? vb : seg_mx(V.seg[k])); };
+  const int J = (kb - ka + 1 + 31) >> 5;
+  double total = 0.0;  // meaningful in lane 0
+  int fprev = 0;
+  int* carry = sh.carry[wid];
+  double* acc = sh.acc[wid];
+  for (int j0 = 0; j0 < J; j0 += kCoopCarry) {
+    const int j1 = min(J, j0 + kCoopCarry);
+    int run = INT32_MIN;
+    {
+      const int klo = kb - 32 * j1 + 1;  // everything below the window
+      if (klo - 1 >= ka) run = max(va, klo - 1 >= ka + 1 ? range_max(V, ka + 1, klo - 1) : va);
+    }
+    for (int j = j1 - 1; j >= j0; --j) {
+      if (lane == 0) carry[j - j0] = run;
+      const int k = kb - 32 * j - lane;
+      run = max(run, warp_max(k >= ka ? vk(k) : INT32_MIN));
+    }
+    __syncwarp();
+    for (int j = j0; j < j1; ++j) {
+      const int k = kb - 32 * j - lane;
+      const bool act = k >= ka;
+      const int2 sk = act ? V.seg[k] : make_int2(0, 0);
+      const int f = seg_f(sk);
+      int m = act ? vk(k) : INT32_MIN;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int u = __shfl_down_sync(0xffffffffu, m, o);
+        if (lane + o < 32) m = max(m, u);
+      }
+      const int base = max(m, carry[j - j0]);
+      int fup = __shfl_up_sync(0xffffffffu, f, 1);
+      if (lane == 0) fup = fprev;
+      double rsum = 0.0;
+      if (act) {
+        const int x = k == kb ? b : sk.y;
+        const int ts = k == kb ? 1 : fup + 1;
+        rsum = run_sum32(fp, x - a, base + ts - 1, base + f - 1);
+      }
+      acc[lane] = rsum;
+      __syncwarp();
+      if (lane == 0) {
+        const int nact = min(32, kb - 32 * j - ka + 1);
+#pragma unroll
+        for (int l = 0; l < 32; ++l)
+          if (l < nact) total = dadd(total, acc[l]);
+      }
+      __syncwarp();
+      fprev = __shfl_sync(0xffffffffu, f, 31);
+    }
+    __syncwarp();
+  }
+  return __shfl_sync(0xffffffffu, total, 0);
+}
+
+__global__ void __launch_bounds__(kEvalT, 1) fast_eval_kernel(EvalArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  EvalShared& sh = *reinterpret_cast<EvalShared*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  FastProf fp = A.fp;
+  if (fp.ncm <= kTopCap) {  // profile tables into shared memory (once per CTA)
+    for (int i = tid; i < fp.ncm; i += kEvalT) {
+      sh.top[i] = A.fp.top[i];
+      sh.pe[i] = A.fp.pe[i];
+    }
+    fp.top = sh.top;
+    fp.pe = sh.pe;
+  }
+  uint16_t* lbuf = sh.lbuf[tid];
+  const int C = A.cr.n_max - A.cr.n_min + 1;
+  const int n_units = A.S * A.units;
+  for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+    const int s = unit / A.units, u = unit % A.units;
+    const int c0 = (int)((int64_t)C * u / A.units), c1 = (int)((int64_t)C * (u + 1) / A.units);
+    if (c0 >= c1) continue;
+    const int nlo = A.cr.n_min + c0, nhi = A.cr.n_min + c1 - 1;
+    const int64_t i0 = A.ss.item_off[s];
+    const int P = (int)(A.ss.item_off[s + 1] - i0);
+    const int64_t so = i0 + s;
+    const int D = A.ss.nseg[s];
+    __syncthreads();  // the previous unit is done with shared memory
+    SegView V;
+    uint32_t* pmsm;
+    if (D <= kSegCap) {
+      for (int k = tid; k < D; k += kEvalT) sh.seg[k] = A.ss.seg[so + k];
+      V.seg = sh.seg;
+      pmsm = sh.pmsm;
+    } else {
+      V.seg = A.ss.seg + so;
+      pmsm = A.pmsm_scratch + (int64_t)blockIdx.x * kMaxSeg;
+    }
+    V.pmsm = pmsm;
+    V.st = sh.st;
+    if (tid == 0) {
+      sh.task_next = 0;
+      sh.lane_next = 0;
+    }
+    __syncthreads();
+    const int nblk = (D + kBlk - 1) / kBlk;
+    for (int jb = tid; jb < nblk; jb += kEvalT) {
+      const int k0 = jb * kBlk, k1 = min(D, k0 + kBlk);
+      int m = INT32_MIN;
+      for (int k = k0; k < k1; ++k) {
+        m = max(m, seg_mx(V.seg[k]));
+        pmsm[k] = (uint32_t)m;
+      }
+      sh.st[0][jb] = (uint16_t)m;
+      m = INT32_MIN;
+      for (int k = k1 - 1; k >= k0; --k) {
+        m = max(m, seg_mx(V.seg[k]));
+        pmsm[k] |= (uint32_t)m << 16;
+      }
+    }
+    __syncthreads();
+    for (int lev = 1; (1 << lev) <= nblk; ++lev) {
+      for (int jb = tid; jb + (1 << lev) <= nblk; jb += kEvalT)
+        sh.st[lev][jb] = max(sh.st[lev - 1][jb], sh.st[lev - 1][jb + (1 << (lev - 1))]);
+      __syncthreads();
+    }
+    // Coop tasks (N < kCoopN, one group per warp) first, then every warp
+    // joins the lane pool: each lane pulls the next group in (N asc, g asc)
+    // order whenever it is idle, so lanes stay busy whatever the run counts.
+    const int nc_hi = min(nhi, kCoopN - 1);
+    const int64_t n_coop = nlo <= nc_hi ? tri64(nc_hi + 1) - tri64(nlo) : 0;
+    const int nl_lo = max(nlo, kCoopN);
+    const int64_t n_lane_groups = nl_lo <= nhi ? tri64(nhi + 1) - tri64(nl_lo) : 0;
+    double* gt = A.gt + (int64_t)s * A.cr.T;
+    const int64_t flat0 = tri64(A.cr.n_min);
+    for (;;) {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(&sh.task_next, 1);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= n_coop) break;
+      int N, g;
+      flat_ng(t, nlo, &N, &g);
+      const int q = P / N, r = P % N;
+      const int a = g * q + min(g, r), b = a + q + (g < r ? 1 : 0);
+      double v = b > a ? coop_group(sh, V, A, fp, i0, a, b, wid) : 0.0;
+      if (lane == 0) gt[tri64(N) - flat0 + g] = v;
+    }
+    if (n_lane_groups > 0) {
+      // Per-lane group state. Runs go k = kb .. ka; base_k = max(va,
+      // max MX over (ka, k]) (vb instead of MX at kb): O(1) from the block
+      // tables, or from lbuf inside the group's first block.
+      int a = 0, b = 0, ka = 0, kb = 0, va = 0, vb = 0, k = 0, l = 0, jl = 0, smb = 0;
+      int fprev = 0, top_m = 0;
+      int64_t slot = 0;
+      double total = 0.0;
+      bool active = false, exhausted = false;
+      for (;;) {
+        if (!active && !exhausted) {
+          const int64_t idx = atomicAdd(&sh.lane_next, 1);
+          if (idx >= n_lane_groups) {
+            exhausted = true;
+          } else {
+            int N, g;
+            flat_ng(idx, nl_lo, &N, &g);
+            const int q = P / N, r = P % N;
+            a = g * q + min(g, r);
+            b = a + q + (g < r ? 1 : 0);
+            slot = tri64(N) - flat0 + g;
+            if (b <= a) {
+              gt[slot] = 0.0;
+            } else {
+              const int2 ra = A.ss.rinfo[i0 + a];
+              const int2 rb = A.ss.rinfo[i0 + b - 1];
+              ka = ra.x;
+              kb = rb.x;
+              if (ka == kb) {  // the whole group sits in one run-segment
+                const int m = span_max(A.ss, i0, a, b);
+                gt[slot] = dadd(0.0, run_sum32(fp, b - a, m, m + seg_f(V.seg[ka]) - 1));
+              } else {
+                va = ra.y & 0xffff;
+                vb = (rb.y >> 16) & 0xffff;
+                l = ka + 1;
+                jl = l >> 4;
+                const int e = min(16 * jl + 15, kb - 1);  // first block part of (ka, kb)
+                int m = INT32_MIN;
+                for (int kk = l; kk <= e; ++kk) {
+                  m = max(m, seg_mx(V.seg[kk]));
+                  lbuf[kk - l] = (uint16_t)m;
+                }
+                smb = m;
+                // base at kb: max over the whole group
+                int mid = INT32_MIN;
+                if (kb - 1 >= l) {
+                  const int jr = (kb - 1) >> 4;
+                  if (jr == jl) {
+                    mid = lbuf[kb - 1 - l];
+                  } else {
+                    mid = max(smb, (int)(V.pmsm[kb - 1] & 0xffff));
+                    if (jl + 1 <= jr - 1) mid = max(mid, rmq_blocks(V, jl + 1, jr - 1));
+                  }
+                }
+                top_m = max(max(va, vb), mid);
+                k = kb;
+                fprev = 0;
+                total = 0.0;
+                active = true;
+              }
+            }
+          }
+        }
+        if (!__any_sync(0xffffffffu, active)) {
+          if (__all_sync(0xffffffffu, exhausted)) break;
+          continue;
+        }
+#pragma unroll 1
+        for (int it = 0; it < 8 && active; ++it) {
+          const int2 sk = V.seg[k];
+          const int f = seg_f(sk);
+          int base, x, ts;
+          if (k == kb) {
+            base = top_m;
+            x = b;
+            ts = 1;
+          } else {
+            x = sk.y;
+            ts = fprev + 1;
+            if (k == ka) {
+              base = va;
+            } else {
+              const int jr = k >> 4;
+              int m;
+              if (jr == jl) {
+                m = lbuf[k - l];
+              } else {
+                m = max(smb, (int)(V.pmsm[k] & 0xffff));
+                if (jl + 1 <= jr - 1) m = max(m, rmq_blocks(V, jl + 1, jr - 1));
+              }
+              base = max(va, m);
+            }
+          }
+          total = dadd(total, run_sum32(fp, x - a, base + ts - 1, base + f - 1));
+          fprev = f;
+          if (--k < ka) {
+            gt[slot] = total;
+            active = false;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Small-batch tpot rows and piece ends of one (profile, G).
+__global__ void fast_tables_kernel(DevProfile p, int G, int live_top, double* rows,
+                                   uint16_t* pe, int cf_ceil, int cb_ceil) {
+  const int64_t ncm = p.c_hi - p.c_lo + 1;
+  const int64_t total = (int64_t)(live_top - 1) * ncm + ncm;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < (int64_t)(live_top - 1) * ncm) {
+      const int64_t live = i / ncm + 1, j = i % ncm;
+      rows[i] = tpot_int(p, (int64_t)G * live, p.c_lo + j);
+    } else {
+      const int64_t j = i - (int64_t)(live_top - 1) * ncm;
+      const int64_t c = p.c_lo + j;
+      int v = 0;
+      if (c >= cf_ceil && c < cb_ceil) v = (int)((int64_t)p.kfloor[p.ci[j] + 1] - p.c_lo);
+      pe[j] = (uint16_t)v;
+    }
+  }
+}
+
+bool fast_profile_ok(const DevProfile& prof, int G) {
+  if (!prof.has_cmemo || !prof.has_bmemo) return false;
+  const int64_t ncm = prof.c_hi - prof.c_lo + 1;
+  if (ncm > 65536 || prof.c_hi > (1 << 30)) return false;
+  const int64_t live_top = (prof.b_hi + G - 1) / G;
+  return (live_top - 1) * ncm <= (int64_t)1 << 26;  // <= 512 MiB of rows
+}
+
+size_t fast_eval_bytes(const DevProfile& prof, int G) {
+  const int64_t ncm = prof.c_hi - prof.c_lo + 1;
+  const int64_t live_top = std::max<int64_t>(1, (prof.b_hi + G - 1) / G);
+  return abytes((live_top - 1) * ncm, 8) + abytes(ncm, 2) + abytes((size_t)1024 * kMaxSeg, 4);
+}
+
+int fast_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, CandRange cr,
+              int units, double* gt) {
+  if (!fast_profile_ok(prof, cr.G)) return fail(RS_E_CONFIG, "profile not eligible for the fast path");
+  const int64_t ncm = prof.c_hi - prof.c_lo + 1;
+  const int live_top = (int)std::max<int64_t>(1, (prof.b_hi + cr.G - 1) / cr.G);
+  double* rows = arena_alloc<double>(ctx, std::max<int64_t>(1, (int64_t)(live_top - 1) * ncm));
+  uint16_t* pe = arena_alloc<uint16_t>(ctx, ncm);
+  const int grid = std::min(S * units, ctx->num_sms);
+  uint32_t* pmsm = arena_alloc<uint32_t>(ctx, (size_t)grid * kMaxSeg);
+  if (!rows || !pe || !pmsm) return fail(RS_E_NOMEM, "arena exhausted (fast eval)");
+  double front, back;
+  RS_CUDA_TRY(cudaMemcpyAsync(&front, prof.ck, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RS_CUDA_TRY(cudaMemcpyAsync(&back, prof.ck + prof.nc - 1, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  FastProf fp;
+  fp.top = prof.top_row;
+  fp.rows = rows;
+  fp.pe = pe;
+  fp.c_lo = (int)prof.c_lo;
+  fp.c_hi = (int)prof.c_hi;
+  fp.cf_ceil = (int)std::ceil(front);
+  fp.cb_ceil = (int)std::ceil(back);
+  fp.cfront_m1 = (int)prof.cfront_m1;
+  fp.ncm = (int)ncm;
+  fp.live_top = live_top;
+  const int64_t tot = (int64_t)live_top * ncm;
+  RS_LAUNCH(ctx, "fast_tables", fast_tables_kernel, (int)std::min<int64_t>((tot + 255) / 256, 4096),
+            256, 0, prof, cr.G, live_top, rows, pe, fp.cf_ceil, fp.cb_ceil);
+  EvalArgs A{ss, fp, cr, S, units, gt, pmsm};
+  const int smem = (int)sizeof(EvalShared);
+  RS_CUDA_TRY(cudaFuncSetAttribute(fast_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  RS_LAUNCH(ctx, "group_eval", fast_eval_kernel, grid, kEvalT, smem, A);
+  return RS_OK;
+}
+
+// ----------------------------------------------------------------- reduce --
+__global__ void fast_reduce_kernel(FastSS ss, int S, CandRange cr, double rho, int gpus,
+                                   const double* gt, double* t_total, double* cost,
+                                   int64_t* idle) {
+  const int C = cr.n_max - cr.n_min + 1;
+  const int64_t total = (int64_t)S * C;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(t / C), ci = (int)(t % C);
+    const int N = cr.n_min + ci;
+    const double* g = gt + (int64_t)s * cr.T + (tri64(N) - tri64(cr.n_min));
+    double tt = 0.0, dollars = 0.0;
+    const double gd = (double)gpus;
+    for (int k = 0; k < N; ++k) {
+      const double v = g[k];
+      tt = tt < v ? v : tt;                             // std::max(t_total, t)
+      dollars = dadd(dollars, dmul(dmul(rho, v), gd));  // rho * t * gpu_count
+    }
+    t_total[t] = tt;
+    cost[t] = dollars;
+    if (idle) {
+      const int64_t i0 = ss.item_off[s], so = i0 + s;
+      const int P = (int)(ss.item_off[s + 1] - i0);
+      const int D = ss.nseg[s];
+      auto cfpos = [&](int p) -> int64_t {
+        if (p >= P) return ss.segCF[so + D];
+        const int k = ss.rinfo[i0 + p].x;
+        const int sk = k == 0 ? 0 : ss.seg[so + k - 1].y;
+        return ss.segCF[so + k] + (int64_t)(p - sk) * (ss.seg[so + k].x & 0xffff);
+      };
+      const int q = P / N, r = P % N;
+      int64_t acc = 0;
+      for (int k = 0; k < N; ++k) {
+        const int a = k * q + min(k, r), b = a + q + (k < r ? 1 : 0);
+        if (b <= a) continue;
+        const int64_t fa = ss.seg[so + ss.rinfo[i0 + a].x].x & 0xffff;
+        acc += (int64_t)(b - a) * fa - (cfpos(b) - cfpos(a));
+      }
+      idle[t] = acc * cr.G;
+    }
+  }
+}
+
+int fast_reduce(rs_ctx* ctx, int S, const FastSS& ss, CandRange cr, double rho, int gpus,
+                const double* gt, double* t_total, double* cost, int64_t* idle) {
+  const int64_t n = (int64_t)S * (cr.n_max - cr.n_min + 1);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 127) / 128, 8 * ctx->num_sms));
+  RS_LAUNCH(ctx, "candidate_reduce", fast_reduce_kernel, grid, 128, 0, ss, S, cr, rho, gpus, gt,
+            t_total, cost, idle);
+  return RS_OK;
+}
+
+}  // namespace rs

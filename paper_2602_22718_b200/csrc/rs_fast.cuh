@@ -1,0 +1,95 @@
+// rs_fast.cuh — the fast scaling-sweep path (bucketed finish ticks).
+#pragma once
+#include "rs_internal.cuh"
+
+namespace rs {
+
+// Packed, rank-ordered scenario structure of the fast path. Scenario s owns
+// items [item_off[s], item_off[s+1]) and segment slots starting at
+// item_off[s] + s (D_s + 1 slots).
+//   seg[k]   = {F_k | MX_k << 16, E_k}: finish tick, max prompt_len and end
+//              rank of run-segment k (segments in descending finish order)
+//   segCF[k] = sum_{k' < k} count_k' * F_k'   (segCF[D] = total)
+//   rinfo[r] = {seg_of(r), smx(r) | pmx(r) << 16} with smx / pmx the max
+//              prompt_len from r to the end / from the start of r's segment
+struct FastSS {
+  const int64_t* item_off;
+  int2* seg;
+  int64_t* segCF;
+  int32_t* nseg;
+  int2* rinfo;
+  int32_t* plen_r;
+  int32_t* order_r;
+  int4* rec;  // scratch: scattered {pred lo, pred hi, idx, plen}
+};
+
+constexpr int kFastFmax = 16384;   // finish ticks of the fast path
+constexpr int kFastPlenMax = 65535;
+constexpr int kBlk = 16;           // segment block of the lane evaluator
+constexpr int kMaxSeg = kFastFmax; // D <= Fmax
+constexpr int kTopCap = 4096;      // smem tpot row entries
+constexpr int kCoopN = 4;          // N < kCoopN: warp-cooperative groups
+
+size_t fast_ss_bytes(int64_t items, int S);
+FastSS fast_ss_alloc(rs_ctx* ctx, const int64_t* d_off, int64_t items, int S);
+
+struct GenSpec {
+  uint64_t base_seed;
+  int64_t first;
+  int count;
+  double plen_mean, plen_sigma;
+  int plen_min, plen_max;
+  double pred_scale, pred_min, pred_max;
+};
+
+__device__ __forceinline__ double fast_qinterp(const double* t, uint64_t u) {
+  uint64_t j = u >> 52;
+  double f = dmul((double)((u >> 11) & ((1ULL << 41) - 1)), 0x1.0p-41);
+  double a = __ldg(t + j), b = __ldg(t + j + 1);
+  return dadd(a, dmul(dsub(b, a), f));
+}
+
+// Scenario item i of one Monte-Carlo scenario (oracle:
+// orc_generate_scenarios): two splitmix64 draws -> quantile interpolation.
+__device__ __forceinline__ void fast_gen(const GenSpec& g, const double* nz, const double* lnz,
+                                         uint64_t seed, int i, double* pred, int32_t* plen) {
+  uint64_t u1 = draw_at(seed, 2 * (uint64_t)i + 1);
+  uint64_t u2 = draw_at(seed, 2 * (uint64_t)i + 2);
+  double z = fast_qinterp(nz, u1);
+  double pl = round(dadd(g.plen_mean, dmul(g.plen_sigma, z)));
+  pl = pl < (double)g.plen_min ? (double)g.plen_min : pl;
+  pl = pl > (double)g.plen_max ? (double)g.plen_max : pl;
+  double pr = dmul(g.pred_scale, fast_qinterp(lnz, u2));
+  pr = pr < g.pred_min ? g.pred_min : pr;
+  pr = pr > g.pred_max ? g.pred_max : pr;
+  *pred = pr;
+  *plen = (int32_t)pl;
+}
+
+// Build the fast structure for S scenarios (one CTA each). When gen is
+// non-null the scenarios are generated on the device (and written to
+// pred/plen); otherwise pred/plen are read. Sets kFlagBucketOverflow in
+// ctx->d_flags if an input is outside the fast path's range.
+int fast_build(rs_ctx* ctx, int S, const int64_t* d_off, double* pred, int32_t* plen,
+               FastSS ss, const GenSpec* gen, const double* nz, const double* lnz);
+
+struct CandRange {
+  int n_min, n_max;
+  int64_t T;  // groups per scenario over [n_min, n_max]
+  int G;
+};
+
+// Evaluate every group of every candidate for S scenarios: gt[s*T + flat].
+// units_per_scenario splits a scenario's candidates over several CTAs.
+int fast_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, CandRange cr,
+              int units_per_scenario, double* gt);
+
+// The fast evaluator needs exact memo tables small enough for its row cache.
+bool fast_profile_ok(const DevProfile& prof, int G);
+size_t fast_eval_bytes(const DevProfile& prof, int G);
+
+// Per (scenario, candidate): t_total, cost, idle slot-ticks.
+int fast_reduce(rs_ctx* ctx, int S, const FastSS& ss, CandRange cr, double rho, int gpus,
+                const double* gt, double* t_total, double* cost, int64_t* idle);
+
+}  // namespace rs

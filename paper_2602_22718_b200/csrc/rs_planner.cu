@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "rs_scenario_tables.h"
+#include "rs_fast.cuh"
 #include "rs_sort.cuh"
 
 namespace rs {
@@ -85,39 +86,6 @@ static SSView ss_view(const SSBuffers& b, const int64_t* item_off, int S) {
 }
 
 // --------------------------------------------------- scenario generation --
-struct GenSpec {
-  uint64_t base_seed;
-  int64_t first;
-  int count;
-  double plen_mean, plen_sigma;
-  int plen_min, plen_max;
-  double pred_scale, pred_min, pred_max;
-};
-
-// Quantile interpolation (oracle: orc_generate_scenarios).
-__device__ __forceinline__ double qinterp(const double* t, uint64_t u) {
-  uint64_t j = u >> 52;
-  double f = dmul((double)((u >> 11) & ((1ULL << 41) - 1)), 0x1.0p-41);
-  double a = __ldg(t + j), b = __ldg(t + j + 1);
-  return dadd(a, dmul(dsub(b, a), f));
-}
-
-__device__ __forceinline__ void gen_item(const GenSpec& g, const double* nz,
-                                         const double* lnz, uint64_t seed,
-                                         int i, double* pred, int32_t* plen) {
-  uint64_t u1 = draw_at(seed, 2 * (uint64_t)i + 1);
-  uint64_t u2 = draw_at(seed, 2 * (uint64_t)i + 2);
-  double z = qinterp(nz, u1);
-  double pl = round(dadd(g.plen_mean, dmul(g.plen_sigma, z)));
-  pl = pl < (double)g.plen_min ? (double)g.plen_min : pl;
-  pl = pl > (double)g.plen_max ? (double)g.plen_max : pl;
-  double pr = dmul(g.pred_scale, qinterp(lnz, u2));
-  pr = pr < g.pred_min ? g.pred_min : pr;
-  pr = pr > g.pred_max ? g.pred_max : pr;
-  *pred = pr;
-  *plen = (int32_t)pl;
-}
-
 __global__ void gen_scenarios_kernel(GenSpec g, const double* nz,
                                      const double* lnz, int S, double* pred,
                                      int32_t* plen) {
@@ -126,187 +94,11 @@ __global__ void gen_scenarios_kernel(GenSpec g, const double* nz,
        t += (int64_t)gridDim.x * blockDim.x) {
     int s = (int)(t / g.count), i = (int)(t % g.count);
     uint64_t seed = hash_combine(g.base_seed, (uint64_t)(g.first + s));
-    gen_item(g, nz, lnz, seed, i, pred + t, plen + t);
+    fast_gen(g, nz, lnz, seed, i, pred + t, plen + t);
   }
 }
 
-// ------------------------------------------ bucketed structure builder --
-// One CTA per scenario. Counting sort by finish tick f = ceil(pred) in
-// descending order (shared-memory histogram over [1, Fmax]), then each
-// bucket is ordered by (pred desc, input index asc) inside one warp.
 constexpr int kBuildThreads = 1024;
-constexpr int kWideBucket = 4096;
-
-__device__ __forceinline__ bool rank_less(double pa, int ia, double pb, int ib) {
-  return pa > pb || (pa == pb && ia < ib);
-}
-
-template <bool kGenerate>
-__global__ void __launch_bounds__(kBuildThreads)
-build_bucketed_kernel(GenSpec gs, const double* nz, const double* lnz,
-                      double* pred_io, int32_t* plen_io,
-                      const int64_t* item_off, SSBuffers ss, int* flags) {
-  extern __shared__ int32_t smem[];
-  int32_t* endb = smem;                      // [kBucketFmax + 2] cursors
-  int32_t* segid = smem + kBucketFmax + 2;   // [kBucketFmax + 2]
-  __shared__ int32_t wsum[32];
-  __shared__ int64_t wsum64[32];
-  __shared__ int bad;
-  const int s = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t i0 = item_off[s];
-  const int P = (int)(item_off[s + 1] - i0);
-  double* pred = pred_io + i0;
-  int32_t* plen = plen_io + i0;
-  const int64_t so = i0 + s;
-  for (int f = tid; f < kBucketFmax + 2; f += kBuildThreads) endb[f] = 0;
-  if (tid == 0) bad = 0;
-  __syncthreads();
-  uint64_t seed = kGenerate ? hash_combine(gs.base_seed, (uint64_t)(gs.first + s)) : 0;
-  int lflags = 0;
-  for (int i = tid; i < P; i += kBuildThreads) {
-    double p;
-    if (kGenerate) {
-      int32_t pl;
-      gen_item(gs, nz, lnz, seed, i, &p, &pl);
-      pred[i] = p;
-      plen[i] = pl;
-    } else {
-      p = pred[i];
-    }
-    if (!isfinite(p)) { lflags |= kFlagNotFinite; continue; }
-    double fc = ceil(p);
-    if (!(fc >= 1.0) || fc > (double)kBucketFmax) { lflags |= kFlagBucketOverflow; continue; }
-    atomicAdd(&endb[(int)fc], 1);
-  }
-  if (lflags) atomicOr(&bad, lflags);
-  __syncthreads();
-  if (bad) {
-    if (tid == 0) atomicOr(flags, bad);
-    return;
-  }
-  // Descending exclusive scan over f = Fmax..1 (thread t owns 16 bins).
-  constexpr int kPer = kBucketFmax / kBuildThreads;  // 16
-  int cnt[kPer];
-  int csum = 0, nz_cnt = 0;
-  int64_t cf = 0;
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    int f = kBucketFmax - tid * kPer - j;
-    cnt[j] = endb[f];
-    csum += cnt[j];
-    nz_cnt += cnt[j] ? 1 : 0;
-    cf += (int64_t)cnt[j] * f;
-  }
-  // block exclusive scans of csum, nz_cnt, cf
-  auto block_excl = [&](int v) -> int {
-    int incl = warp_incl_sum(v);
-    if (lane == 31) wsum[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-      int x = wsum[lane];
-      wsum[lane] = warp_incl_sum(x) - x;
-    }
-    __syncthreads();
-    int r = wsum[wid] + incl - v;
-    __syncthreads();
-    return r;
-  };
-  int start = block_excl(csum);
-  int kbase = block_excl(nz_cnt);
-  int64_t cfbase;
-  {
-    int64_t incl = warp_incl_sum(cf);
-    if (lane == 31) wsum64[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-      int64_t x = wsum64[lane];
-      wsum64[lane] = warp_incl_sum(x) - x;
-    }
-    __syncthreads();
-    cfbase = wsum64[wid] + incl - cf;
-    if (tid == kBuildThreads - 1) {
-      ss.nseg[s] = kbase + nz_cnt;
-      ss.segS[so + kbase + nz_cnt] = P;
-      ss.segCF[so + kbase + nz_cnt] = cfbase + cf;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    int f = kBucketFmax - tid * kPer - j;
-    endb[f] = start;
-    if (cnt[j]) {
-      segid[f] = kbase;
-      ss.segF[so + kbase] = f;
-      ss.segS[so + kbase] = start;
-      ss.segCF[so + kbase] = cfbase;
-      ++kbase;
-    }
-    start += cnt[j];
-    cfbase += (int64_t)cnt[j] * f;
-  }
-  __syncthreads();
-  // Scatter input indices into their bucket (unordered inside it).
-  for (int i = tid; i < P; i += kBuildThreads) {
-    int f = (int)ceil(pred[i]);
-    int pos = atomicAdd(&endb[f], 1);
-    ss.tmp_idx[i0 + pos] = i;
-  }
-  __syncthreads();
-  // Order each bucket by (pred desc, index asc); one warp per bucket.
-  const int D = ss.nseg[s];
-  const int nwarps = kBuildThreads / 32;
-  for (int k = wid; k < D; k += nwarps) {
-    int lo = ss.segS[so + k], hi = ss.segS[so + k + 1], m = hi - lo;
-    int mx = INT32_MIN;
-    if (m <= 32) {
-      int idx = lane < m ? ss.tmp_idx[i0 + lo + lane] : INT32_MAX;
-      double key = lane < m ? pred[idx] : -INFINITY;
-      // bitonic sort over the 32 lanes; inactive lanes sort last
-#pragma unroll
-      for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-          double ok = __shfl_xor_sync(0xffffffffu, key, stride);
-          int oi = __shfl_xor_sync(0xffffffffu, idx, stride);
-          bool up = ((lane & size) == 0);
-          bool lower = (lane & stride) == 0;
-          bool other_first = rank_less(ok, oi, key, idx);
-          // lower lane keeps the "first" element when ascending in rank
-          bool take = lower == up ? other_first : !other_first && !(ok == key && oi == idx);
-          if (take) { key = ok; idx = oi; }
-        }
-      }
-      if (lane < m) {
-        int pl = plen[idx];
-        ss.order_r[i0 + lo + lane] = idx;
-        ss.plen_r[i0 + lo + lane] = pl;
-        ss.seg_of[i0 + lo + lane] = k;
-        mx = pl;
-      }
-    } else if (m <= kWideBucket) {
-      for (int e = lane; e < m; e += 32) {
-        int idx = ss.tmp_idx[i0 + lo + e];
-        double key = pred[idx];
-        int rank = 0;
-        for (int o = 0; o < m; ++o) {
-          int oi = ss.tmp_idx[i0 + lo + o];
-          rank += rank_less(pred[oi], oi, key, idx) ? 1 : 0;
-        }
-        int pl = plen[idx];
-        ss.order_r[i0 + lo + rank] = idx;
-        ss.plen_r[i0 + lo + rank] = pl;
-        ss.seg_of[i0 + lo + rank] = k;
-        mx = max(mx, pl);
-      }
-    } else {
-      if (lane == 0) atomicOr(flags, kFlagBucketTooWide);
-    }
-    mx = warp_max(mx);
-    if (lane == 0) ss.segMX[so + k] = mx;
-  }
-}
 
 // --------------------------------------------- generic structure builder --
 // Input: rank-ordered pred_r / plen_r (after the radix sort). One CTA per
@@ -686,11 +478,6 @@ __global__ void gather_ranked_kernel(const int64_t* item_off, int S,
 }
 
 // ----------------------------------------------------- host orchestration --
-struct Built {
-  SSBuffers ss;
-  SSView view;
-};
-
 static int grid_for(rs_ctx* ctx, int64_t n, int threads) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads,
                                                      (int64_t)ctx->num_sms * 8));
@@ -730,49 +517,12 @@ static size_t generic_scratch_bytes(int64_t n) {
   return abytes(n, 8) * 2 + abytes(n, 4) + radix_sort_scratch_bytes64(n);
 }
 
-static const size_t kBucketSmem = sizeof(int32_t) * 2 * (kBucketFmax + 2);
-
-static int build_bucketed(rs_ctx* ctx, int S, const int64_t* d_off, double* pred,
-                          int32_t* plen, SSBuffers ss, const GenSpec* gen,
-                          const double* nz, const double* lnz) {
-  RS_CUDA_TRY(cudaFuncSetAttribute(build_bucketed_kernel<true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBucketSmem));
-  RS_CUDA_TRY(cudaFuncSetAttribute(build_bucketed_kernel<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBucketSmem));
-  GenSpec g{};
-  if (gen) g = *gen;
-  if (gen)
-    RS_LAUNCH(ctx, "build_bucketed", build_bucketed_kernel<true>, S, kBuildThreads,
-              kBucketSmem, g, nz, lnz, pred, plen, d_off, ss, ctx->d_flags);
-  else
-    RS_LAUNCH(ctx, "build_bucketed", build_bucketed_kernel<false>, S, kBuildThreads,
-              kBucketSmem, g, nz, lnz, pred, plen, d_off, ss, ctx->d_flags);
-  return RS_OK;
-}
-
 static int read_flags(rs_ctx* ctx, int* flags) {
   RS_CUDA_TRY(cudaMemcpyAsync(ctx->h_flags, ctx->d_flags, sizeof(int),
                               cudaMemcpyDeviceToHost, ctx->stream));
   RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   *flags = *ctx->h_flags;
   return RS_OK;
-}
-
-// Build the SS for S scenarios laid out by d_off (host copy h_off) over
-// id-ordered pred/plen already in HBM. Tries the bucketed path first.
-static int build_any(rs_ctx* ctx, int S, const int64_t* d_off, int64_t n,
-                     double* pred, int32_t* plen, SSBuffers ss, char* scratch,
-                     bool allow_bucket) {
-  if (allow_bucket) {
-    RS_TRY(clear_flags(ctx));
-    RS_TRY(build_bucketed(ctx, S, d_off, pred, plen, ss, nullptr, nullptr, nullptr));
-    int fl;
-    RS_TRY(read_flags(ctx, &fl));
-    if (fl & kFlagNotFinite) return flags_to_status(fl);
-    if (!(fl & (kFlagBucketOverflow | kFlagBucketTooWide))) return RS_OK;
-    RS_TRY(clear_flags(ctx));
-  }
-  return build_generic(ctx, S, d_off, n, pred, plen, ss, scratch);
 }
 
 static int64_t groups_per_scenario(int n_min, int n_max) {
@@ -822,27 +572,113 @@ static int check_spec(const rs_scenario_spec* sp) {
   return RS_OK;
 }
 
+
+// A built batch of scenario structures: the fast packed layout (bucketed
+// finish ticks, rs_fast.cu) or the generic one (radix sort).
+struct Built {
+  bool fast = false;
+  FastSS fss{};
+  SSBuffers gss{};
+  SSView gview{};
+  const int32_t* order_r() const { return fast ? fss.order_r : gss.order_r; }
+};
+
+static size_t built_bytes(int64_t n, int S, bool with_generic) {
+  return fast_ss_bytes(n, S) + (with_generic ? ss_bytes(n, S) + generic_scratch_bytes(n) : 0) +
+         (1 << 16);
+}
+
+
+// pred / plen: id-ordered device arrays (written by the generator when gen).
+static int build_batch(rs_ctx* ctx, int S, const int64_t* d_off, int64_t n, double* pred,
+                       int32_t* plen, const GenSpec* gen, const double* nz, const double* lnz,
+                       bool allow_fast, Built* out) {
+  if (allow_fast) {
+    out->fss = fast_ss_alloc(ctx, d_off, n, S);
+    if (!out->fss.rec) return fail(RS_E_NOMEM, "arena exhausted (fast structure)");
+    RS_TRY(clear_flags(ctx));
+    RS_TRY(fast_build(ctx, S, d_off, pred, plen, out->fss, gen, nz, lnz));
+    if (gen) {  // in range by construction (fast_spec_ok)
+      out->fast = true;
+      return RS_OK;
+    }
+    int fl;
+    RS_TRY(read_flags(ctx, &fl));
+    if (fl & kFlagNotFinite) return flags_to_status(fl);
+    if (!(fl & (kFlagBucketOverflow | kFlagBucketTooWide))) {
+      out->fast = true;
+      return RS_OK;
+    }
+    RS_TRY(clear_flags(ctx));
+  }
+  out->fast = false;
+  out->gss = ss_alloc(ctx, n, S);
+  char* scratch = arena_alloc<char>(ctx, generic_scratch_bytes(n));
+  if (!scratch) return fail(RS_E_NOMEM, "arena exhausted (generic structure)");
+  RS_TRY(build_generic(ctx, S, d_off, n, pred, plen, out->gss, scratch));
+  out->gview = ss_view(out->gss, d_off, S);
+  return RS_OK;
+}
+
+static int units_for(rs_ctx* ctx, int S, int C) {
+  int want = (2 * ctx->num_sms + S - 1) / S;
+  return std::max(1, std::min(want, C));
+}
+
+static int eval_batch(rs_ctx* ctx, const Built& b, int S, const DevProfile& dp, int n_min,
+                      int n_max, int G, double* gt) {
+  const int64_t T = groups_per_scenario(n_min, n_max);
+  if (b.fast) {
+    CandRange cr{n_min, n_max, T, G};
+    return fast_eval(ctx, S, b.fss, dp, cr, units_for(ctx, S, n_max - n_min + 1), gt);
+  }
+  CandSpec cs{n_min, n_max, T, G};
+  RS_LAUNCH(ctx, "group_eval", group_eval_kernel, eval_grid(ctx, (int64_t)S * T), kEvalThreads,
+            0, b.gview, dp, cs, gt);
+  return RS_OK;
+}
+
+static int reduce_batch(rs_ctx* ctx, const Built& b, int S, int n_min, int n_max, int G,
+                        double rho, int gpus, const double* gt, double* tt, double* cc,
+                        int64_t* idle) {
+  const int64_t T = groups_per_scenario(n_min, n_max);
+  if (b.fast) {
+    CandRange cr{n_min, n_max, T, G};
+    return fast_reduce(ctx, S, b.fss, cr, rho, gpus, gt, tt, cc, idle);
+  }
+  CandSpec cs{n_min, n_max, T, G};
+  RS_LAUNCH(ctx, "candidate_reduce", candidate_reduce_kernel,
+            grid_for(ctx, (int64_t)S * (n_max - n_min + 1), 128), 128, 0, b.gview, cs, rho, gpus,
+            gt, tt, cc, idle);
+  return RS_OK;
+}
+
+static bool fast_spec_ok(const rs_scenario_spec* sp) {
+  return std::ceil(sp->pred_max) <= (double)kFastFmax && sp->pred_min >= 1.0 &&
+         sp->plen_min >= 0 && sp->plen_max <= kFastPlenMax;
+}
+
 // Shared sweep driver: scenarios either generated (spec) or from arrays.
-static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec,
-                      const double* h_pred, const int32_t* h_plen, int S,
-                      int P, const rs_profile* profile, int G, int n_min,
-                      int n_max, double lambda, int gpus, rs_sweep_out* out,
+static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h_pred,
+                      const int32_t* h_plen, int S, int P, const rs_profile* profile, int G,
+                      int n_min, int n_max, double lambda, int gpus, rs_sweep_out* out,
                       int device_ptrs) {
   RS_TRY(check_scale_args(P, G, n_min, n_max, lambda));
   DevProfile dp;
   RS_TRY(get_profile(ctx, profile, &dp));
   const int C = n_max - n_min + 1;
   const int64_t T = groups_per_scenario(n_min, n_max);
-  // Batch size: keep per-batch scratch near 2 GiB.
-  const size_t per_scen = abytes(P, 8) + abytes(P, 4) + ss_bytes(P, 1) + abytes(T, 8) +
-                          abytes(C, 8) * 2 + abytes(C, 8) + 1024;
-  int B = (int)std::max<size_t>(1, std::min<size_t>((size_t)S, (size_t)(2ull << 30) / per_scen));
-  if (B > 1024) B = 1024;
   const bool generated = spec != nullptr;
-  bool bucket_ok = !generated || std::ceil(spec->pred_max) <= (double)kBucketFmax;
-  size_t need = (size_t)B * per_scen + abytes(B + 1, 8) + abytes(2 * (RS_QTABLE_N + 1), 8) +
-                abytes(C, 8) * 2 + abytes(C, 4) + (size_t)B * abytes(1, 8) * 4 + (1 << 20);
-  if (!bucket_ok || !generated) need += generic_scratch_bytes((int64_t)B * P);
+  const bool allow_fast = fast_profile_ok(dp, G);
+  const bool gen_fast = generated && allow_fast && fast_spec_ok(spec);
+  const bool with_generic = !gen_fast;
+  const size_t per_scen = abytes(P, 8) + abytes(P, 4) + built_bytes(P, 1, with_generic) +
+                          abytes(T, 8) + abytes(C, 8) * 3 + abytes(1, 4) + 2048;
+  int B = (int)std::max<size_t>(1, std::min<size_t>((size_t)S, (size_t)(3ull << 30) / per_scen));
+  if (B > 2048) B = 2048;
+  size_t need = (size_t)B * per_scen + fast_eval_bytes(dp, G) + abytes(B + 1, 8) +
+                abytes(2 * (RS_QTABLE_N + 1), 8) +
+                abytes(C, 8) * 2 + abytes(C, 4) + abytes(dp.c_hi - dp.c_lo + 1, 4) + (4 << 20);
   RS_TRY(arena_reserve(ctx, need));
   double* nz = nullptr;
   double* lnz = nullptr;
@@ -850,18 +686,16 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec,
   int64_t* d_off = arena_alloc<int64_t>(ctx, B + 1);
   double* pred = arena_alloc<double>(ctx, (size_t)B * P);
   int32_t* plen = arena_alloc<int32_t>(ctx, (size_t)B * P);
-  SSBuffers ss = ss_alloc(ctx, (int64_t)B * P, B);
   double* gt = arena_alloc<double>(ctx, (size_t)B * T);
   double* agg_t = arena_alloc<double>(ctx, C);
   double* agg_c = arena_alloc<double>(ctx, C);
   int32_t* agg_h = arena_alloc<int32_t>(ctx, C);
-  // per-batch outputs when the caller wants host results
   double* b_tt = arena_alloc<double>(ctx, (size_t)B * C);
   double* b_cc = arena_alloc<double>(ctx, (size_t)B * C);
   int64_t* b_idle = arena_alloc<int64_t>(ctx, (size_t)B * C);
   int32_t* b_ns = arena_alloc<int32_t>(ctx, B);
-  char* gscratch = (!bucket_ok || !generated) ? arena_alloc<char>(ctx, generic_scratch_bytes((int64_t)B * P)) : nullptr;
-  if (!b_ns || !agg_h || !gt || !ss.nseg) return fail(RS_E_NOMEM, "arena exhausted (sweep)");
+  if (!b_ns) return fail(RS_E_NOMEM, "arena exhausted (sweep)");
+  const size_t mark = ctx->arena_used;  // per-batch structures live above
   {
     std::vector<int64_t> off(B + 1);
     for (int i = 0; i <= B; ++i) off[i] = (int64_t)i * P;
@@ -871,50 +705,50 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec,
   RS_CUDA_TRY(cudaMemsetAsync(agg_c, 0, 8 * C, ctx->stream));
   RS_CUDA_TRY(cudaMemsetAsync(agg_h, 0, 4 * C, ctx->stream));
   RS_TRY(clear_flags(ctx));
-  CandSpec cs{n_min, n_max, T, G};
   for (int s0 = 0; s0 < S; s0 += B) {
     const int Sb = std::min(B, S - s0);
-    // When the final batch is short, the offsets prefix still applies.
-    SSView view = ss_view(ss, d_off, Sb);
+    const int64_t n = (int64_t)Sb * P;
+    ctx->arena_used = mark;
+    Built built;
     if (generated) {
       GenSpec g = to_gen(spec, spec->first_scenario + s0);
-      if (bucket_ok) {
-        RS_TRY(build_bucketed(ctx, Sb, d_off, pred, plen, ss, &g, nz, lnz));
+      if (gen_fast) {
+        RS_TRY(build_batch(ctx, Sb, d_off, n, pred, plen, &g, nz, lnz, true, &built));
       } else {
-        RS_LAUNCH(ctx, "gen_scenarios", gen_scenarios_kernel, grid_for(ctx, (int64_t)Sb * P, 256),
-                  256, 0, g, nz, lnz, Sb, pred, plen);
-        RS_TRY(build_generic(ctx, Sb, d_off, (int64_t)Sb * P, pred, plen, ss, gscratch));
+        RS_LAUNCH(ctx, "gen_scenarios", gen_scenarios_kernel, grid_for(ctx, n, 256), 256, 0, g,
+                  nz, lnz, Sb, pred, plen);
+        RS_TRY(build_batch(ctx, Sb, d_off, n, pred, plen, nullptr, nullptr, nullptr, allow_fast,
+                           &built));
       }
     } else {
       const double* src_p = h_pred + (size_t)s0 * P;
       const int32_t* src_l = h_plen + (size_t)s0 * P;
       if (device_ptrs) {
-        RS_CUDA_TRY(cudaMemcpyAsync(pred, src_p, 8ull * Sb * P, cudaMemcpyDeviceToDevice, ctx->stream));
-        RS_CUDA_TRY(cudaMemcpyAsync(plen, src_l, 4ull * Sb * P, cudaMemcpyDeviceToDevice, ctx->stream));
+        RS_CUDA_TRY(cudaMemcpyAsync(pred, src_p, 8ull * n, cudaMemcpyDeviceToDevice, ctx->stream));
+        RS_CUDA_TRY(cudaMemcpyAsync(plen, src_l, 4ull * n, cudaMemcpyDeviceToDevice, ctx->stream));
       } else {
-        RS_TRY(h2d(ctx, pred, src_p, 8ull * Sb * P));
-        RS_TRY(h2d(ctx, plen, src_l, 4ull * Sb * P));
+        RS_TRY(h2d(ctx, pred, src_p, 8ull * n));
+        RS_TRY(h2d(ctx, plen, src_l, 4ull * n));
       }
-      RS_LAUNCH(ctx, "validate_inputs", to_id_order_kernel, grid_for(ctx, (int64_t)Sb * P, 256), 256, 0,
-                pred, (const int32_t*)nullptr, (const int32_t*)nullptr, (int64_t)Sb * P,
-                pred, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr, ctx->d_flags, 1);
+      RS_LAUNCH(ctx, "validate_inputs", to_id_order_kernel, grid_for(ctx, n, 256), 256, 0, pred,
+                (const int32_t*)nullptr, (const int32_t*)nullptr, n, pred, (int32_t*)nullptr,
+                (int32_t*)nullptr, (int32_t*)nullptr, ctx->d_flags, 1);
       int fl;
       RS_TRY(read_flags(ctx, &fl));
       if (fl) return flags_to_status(fl);
-      RS_TRY(build_any(ctx, Sb, d_off, (int64_t)Sb * P, pred, plen, ss, gscratch, true));
+      RS_TRY(build_batch(ctx, Sb, d_off, n, pred, plen, nullptr, nullptr, nullptr, allow_fast,
+                         &built));
     }
     double* o_tt = (device_ptrs && out->t_total) ? out->t_total + (size_t)s0 * C : b_tt;
     double* o_cc = (device_ptrs && out->cost) ? out->cost + (size_t)s0 * C : b_cc;
-    int64_t* o_idle = (device_ptrs && out->idle_slot_ticks) ? out->idle_slot_ticks + (size_t)s0 * C : b_idle;
+    int64_t* o_idle =
+        (device_ptrs && out->idle_slot_ticks) ? out->idle_slot_ticks + (size_t)s0 * C : b_idle;
     int32_t* o_ns = (device_ptrs && out->n_star) ? out->n_star + s0 : b_ns;
-    const int64_t items = (int64_t)Sb * T;
-    RS_LAUNCH(ctx, "group_eval", group_eval_kernel, eval_grid(ctx, items), kEvalThreads, 0,
-              view, dp, cs, gt);
-    RS_LAUNCH(ctx, "candidate_reduce", candidate_reduce_kernel,
-              grid_for(ctx, (int64_t)Sb * C, 128), 128, 0, view, cs, dp.rho, gpus, gt,
-              o_tt, o_cc, out->idle_slot_ticks ? o_idle : (int64_t*)nullptr);
-    RS_LAUNCH(ctx, "select", select_kernel, grid_for(ctx, Sb, 128), 128, 0, Sb, C, n_min,
-              lambda, o_tt, (const double*)nullptr, o_cc, (double*)nullptr, (double*)nullptr,
+    RS_TRY(eval_batch(ctx, built, Sb, dp, n_min, n_max, G, gt));
+    RS_TRY(reduce_batch(ctx, built, Sb, n_min, n_max, G, dp.rho, gpus, gt, o_tt, o_cc,
+                        out->idle_slot_ticks ? o_idle : (int64_t*)nullptr));
+    RS_LAUNCH(ctx, "select", select_kernel, grid_for(ctx, Sb, 128), 128, 0, Sb, C, n_min, lambda,
+              o_tt, (const double*)nullptr, o_cc, (double*)nullptr, (double*)nullptr,
               (double*)nullptr, o_ns);
     RS_LAUNCH(ctx, "aggregate", aggregate_kernel, grid_for(ctx, C, 128), 128, 0, Sb, C, n_min,
               o_tt, o_cc, o_ns, agg_t, agg_c, agg_h);
@@ -928,9 +762,12 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec,
     }
   }
   if (device_ptrs) {
-    if (out->sum_t) RS_CUDA_TRY(cudaMemcpyAsync(out->sum_t, agg_t, 8 * C, cudaMemcpyDeviceToDevice, ctx->stream));
-    if (out->sum_c) RS_CUDA_TRY(cudaMemcpyAsync(out->sum_c, agg_c, 8 * C, cudaMemcpyDeviceToDevice, ctx->stream));
-    if (out->nstar_hist) RS_CUDA_TRY(cudaMemcpyAsync(out->nstar_hist, agg_h, 4 * C, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (out->sum_t)
+      RS_CUDA_TRY(cudaMemcpyAsync(out->sum_t, agg_t, 8 * C, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (out->sum_c)
+      RS_CUDA_TRY(cudaMemcpyAsync(out->sum_c, agg_c, 8 * C, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (out->nstar_hist)
+      RS_CUDA_TRY(cudaMemcpyAsync(out->nstar_hist, agg_h, 4 * C, cudaMemcpyDeviceToDevice, ctx->stream));
     return RS_OK;
   }
   if (out->sum_t) RS_TRY(d2h(ctx, out->sum_t, agg_t, 8 * C));
@@ -939,8 +776,7 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec,
   return sync_and_check(ctx);
 }
 
-// Single-set pipeline used by scale / assign / integrate / estimate_*:
-// S sets of caller items (host SoA), each its own scenario, id order given.
+// S caller item sets (host SoA), each its own scenario, in id order.
 struct SetRun {
   int S;
   int64_t n;
@@ -948,17 +784,18 @@ struct SetRun {
   double* pred;
   int32_t* plen;
   int32_t* orig;
-  SSBuffers ss;
-  SSView view;
+  Built built;
 };
 
 static int prepare_sets(rs_ctx* ctx, const double* h_pred, const int32_t* h_plen,
                         const int32_t* h_id_rank, const std::vector<int64_t>& off,
-                        int require_ge1, size_t extra_bytes, SetRun* run) {
+                        int require_ge1, const DevProfile* dp, int G, size_t extra_bytes,
+                        SetRun* run) {
   const int S = (int)off.size() - 1;
   const int64_t n = off.back();
-  size_t need = abytes(S + 1, 8) + abytes(n, 8) * 2 + abytes(n, 4) * 4 + ss_bytes(n, S) +
-                generic_scratch_bytes(n) + extra_bytes + (1 << 20);
+  size_t need = abytes(S + 1, 8) + abytes(n, 8) * 2 + abytes(n, 4) * 4 +
+                built_bytes(n, S, true) + extra_bytes + (1 << 20);
+  if (dp) need += fast_eval_bytes(*dp, G);
   RS_TRY(arena_reserve(ctx, need));
   run->S = S;
   run->n = n;
@@ -970,9 +807,7 @@ static int prepare_sets(rs_ctx* ctx, const double* h_pred, const int32_t* h_plen
   run->pred = arena_alloc<double>(ctx, n);
   run->plen = arena_alloc<int32_t>(ctx, n);
   run->orig = arena_alloc<int32_t>(ctx, n);
-  run->ss = ss_alloc(ctx, n, S);
-  char* gscratch = arena_alloc<char>(ctx, generic_scratch_bytes(n));
-  if (!gscratch) return fail(RS_E_NOMEM, "arena exhausted (sets)");
+  if (!run->orig) return fail(RS_E_NOMEM, "arena exhausted (sets)");
   RS_TRY(h2d(ctx, run->d_off, off.data(), 8 * (S + 1)));
   RS_TRY(clear_flags(ctx));
   if (n > 0) {
@@ -984,15 +819,17 @@ static int prepare_sets(rs_ctx* ctx, const double* h_pred, const int32_t* h_plen
     }
     RS_LAUNCH(ctx, "to_id_order", to_id_order_kernel, grid_for(ctx, n, 256), 256, 0, raw_pred,
               h_plen ? raw_plen : (const int32_t*)nullptr,
-              h_id_rank ? raw_rank : (const int32_t*)nullptr, n, run->pred, run->plen,
-              run->orig, h_id_rank ? seen : (int32_t*)nullptr, ctx->d_flags, require_ge1);
+              h_id_rank ? raw_rank : (const int32_t*)nullptr, n, run->pred, run->plen, run->orig,
+              h_id_rank ? seen : (int32_t*)nullptr, ctx->d_flags, require_ge1);
     int fl;
     RS_TRY(read_flags(ctx, &fl));
-    if (fl & (kFlagWorkOverflow << 1)) return fail(RS_E_ARG, "id_rank is not a permutation of [0, count)");
+    if (fl & (kFlagWorkOverflow << 1))
+      return fail(RS_E_ARG, "id_rank is not a permutation of [0, count)");
     if (fl) return flags_to_status(fl);
-    RS_TRY(build_any(ctx, S, run->d_off, n, run->pred, run->plen, run->ss, gscratch, true));
+    const bool allow_fast = dp == nullptr || fast_profile_ok(*dp, G);
+    RS_TRY(build_batch(ctx, S, run->d_off, n, run->pred, run->plen, nullptr, nullptr, nullptr,
+                       allow_fast, &run->built));
   }
-  run->view = ss_view(run->ss, run->d_off, S);
   return RS_OK;
 }
 
@@ -1184,7 +1021,7 @@ int rs_scale(rs_ctx* ctx, const double* pred, const int32_t* plen, const int32_t
   std::vector<int64_t> off = {0, count};
   SetRun run;
   size_t extra = abytes(T, 8) + abytes(C, 8) * 7 + abytes(count, 4) + abytes(C, 8) + 4096;
-  RS_TRY(prepare_sets(ctx, pred, plen, id_rank, off, 1, extra, &run));
+  RS_TRY(prepare_sets(ctx, pred, plen, id_rank, off, 1, &dp, G, extra, &run));
   double* gt = arena_alloc<double>(ctx, T);
   double* tt = arena_alloc<double>(ctx, C);
   double* cc = arena_alloc<double>(ctx, C);
@@ -1197,15 +1034,12 @@ int rs_scale(rs_ctx* ctx, const double* pred, const int32_t* plen, const int32_t
   int32_t* ns = arena_alloc<int32_t>(ctx, 1);
   if (!ns) return fail(RS_E_NOMEM, "arena exhausted (scale)");
   if (t_penalty) RS_TRY(h2d(ctx, tp, t_penalty, 8 * C));
-  CandSpec cs{n_min, n_max, T, G};
-  RS_LAUNCH(ctx, "group_eval", group_eval_kernel, eval_grid(ctx, T), kEvalThreads, 0, run.view,
-            dp, cs, gt);
-  RS_LAUNCH(ctx, "candidate_reduce", candidate_reduce_kernel, grid_for(ctx, C, 128), 128, 0,
-            run.view, cs, dp.rho, gpus, gt, tt, cc, idle);
+  RS_TRY(eval_batch(ctx, run.built, 1, dp, n_min, n_max, G, gt));
+  RS_TRY(reduce_batch(ctx, run.built, 1, n_min, n_max, G, dp.rho, gpus, gt, tt, cc, idle));
   RS_LAUNCH(ctx, "select", select_kernel, 1, 32, 0, 1, C, n_min, lambda, tt,
             t_penalty ? tp : (const double*)nullptr, cc, tn, cn, sc, ns);
   RS_LAUNCH(ctx, "map_order", map_order_kernel, grid_for(ctx, count, 256), 256, 0,
-            run.ss.order_r, run.orig, (int64_t)count, order);
+            run.built.order_r(), run.orig, (int64_t)count, order);
   RS_TRY(d2h(ctx, &out->n_star, ns, 4));
   if (out->t_total) RS_TRY(d2h(ctx, out->t_total, tt, 8 * C));
   if (out->cost) RS_TRY(d2h(ctx, out->cost, cc, 8 * C));
@@ -1258,12 +1092,12 @@ int rs_assign(rs_ctx* ctx, const double* pred, const int32_t* id_rank, int32_t c
   if (!pred || !order || !group_offsets) return fail(RS_E_ARG, "NULL argument");
   std::vector<int64_t> off = {0, count};
   SetRun run;
-  RS_TRY(prepare_sets(ctx, pred, nullptr, id_rank, off, 0,
+  RS_TRY(prepare_sets(ctx, pred, nullptr, id_rank, off, 0, nullptr, 1,
                       abytes(count, 4) + abytes(n_actors + 1, 4) + 4096, &run));
   int32_t* d_order = arena_alloc<int32_t>(ctx, count);
   int32_t* d_off = arena_alloc<int32_t>(ctx, n_actors + 1);
   RS_LAUNCH(ctx, "map_order", map_order_kernel, grid_for(ctx, count, 256), 256, 0,
-            run.ss.order_r, run.orig, (int64_t)count, d_order);
+            run.built.order_r(), run.orig, (int64_t)count, d_order);
   RS_LAUNCH(ctx, "chunk_offsets", chunk_offsets_kernel, grid_for(ctx, n_actors + 1, 256), 256, 0,
             count, n_actors, d_off);
   RS_TRY(d2h(ctx, order, d_order, 4 * count));
@@ -1279,14 +1113,12 @@ static int integrate_sets(rs_ctx* ctx, const int32_t* plen, const double* target
   RS_TRY(get_profile(ctx, profile, &dp));
   const int S = (int)off.size() - 1;
   SetRun run;
-  RS_TRY(prepare_sets(ctx, target, plen, nullptr, off, 1,
+  RS_TRY(prepare_sets(ctx, target, plen, nullptr, off, 1, &dp, G,
                       abytes(S, 8) + abytes(S, 4) + abytes(1, 8) + 4096, &run));
   double* gt = arena_alloc<double>(ctx, S);
   int32_t* gc = arena_alloc<int32_t>(ctx, S);
   double* dcost = arena_alloc<double>(ctx, 1);
-  CandSpec cs{1, 1, 1, G};
-  RS_LAUNCH(ctx, "group_eval", group_eval_kernel, eval_grid(ctx, S), kEvalThreads, 0, run.view,
-            dp, cs, gt);
+  RS_TRY(eval_batch(ctx, run.built, S, dp, 1, 1, G, gt));
   if (cost_host) {
     RS_TRY(h2d(ctx, gc, gpu_count, 4 * S));
     RS_LAUNCH(ctx, "cost_sum", cost_sum_kernel, 1, 32, 0, gt, gc, S, dp.rho, dcost);
