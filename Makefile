@@ -29,3 +29,39 @@ ref:
 
 clean:
 	rm -rf build $(LIB)
+
+# ---------------------------------------------------------------------------
+# C++ drop-in for the reference `rollsim` library (needs /root/reference at
+# build time; the outputs travel in build/shim/). librollsim_b200.a = the
+# reference's own objects minus dedup.o / planner.o + our shim, which calls
+# librs_b200.so. The reference's test suites are relinked against it
+# (*_b200) and, to validate the minimal doctest harness, against the
+# unmodified reference library (*_ref).
+REF       ?= /root/reference/proj
+NLOHMANN  ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty
+SHIM_OUT  := build/shim
+REF_OBJ   := oracle/_ref/obj
+REF_KEEP  := workload predictor profile placement simulator training report cli
+SHIM_SRCS := $(wildcard $(PKG)/shim/*.cpp)
+SHIM_OBJS := $(patsubst $(PKG)/shim/%.cpp,$(SHIM_OUT)/%.o,$(SHIM_SRCS))
+CXXREF    := g++ -std=c++20 -O3 -DNDEBUG -Wall -Wextra -fPIC -I$(REF)/include \
+             -Ioracle/include_shim -I$(NLOHMANN) -Iinclude
+SUITES    := acceptance_main test_dedup test_planner test_profile test_training
+
+.PHONY: shim
+shim: $(foreach t,$(SUITES),$(SHIM_OUT)/$(t)_b200 $(SHIM_OUT)/$(t)_ref)
+
+$(SHIM_OUT)/%.o: $(PKG)/shim/%.cpp $(PKG)/shim/rs_shim.hpp include/rs.h
+	@mkdir -p $(SHIM_OUT)
+	$(CXXREF) -c $< -o $@
+
+$(SHIM_OUT)/librollsim_b200.a: $(SHIM_OBJS) ref
+	ar rcs $@ $(SHIM_OBJS) $(addprefix $(REF_OBJ)/,$(addsuffix .o,$(REF_KEEP)))
+
+$(SHIM_OUT)/%_b200: $(REF)/tests/%.cpp $(SHIM_OUT)/librollsim_b200.a $(LIB)
+	$(CXXREF) -I$(PKG)/shim/doctest $< -o $@ $(SHIM_OUT)/librollsim_b200.a \
+	    -L$(PKG) -lrs_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -lpthread
+
+$(SHIM_OUT)/%_ref: $(REF)/tests/%.cpp ref
+	@mkdir -p $(SHIM_OUT)
+	$(CXXREF) -I$(PKG)/shim/doctest $< -o $@ oracle/_ref/librollsim_ref.a -lpthread

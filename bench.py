@@ -199,8 +199,8 @@ def run_ours(args, world, rank, local):
     prof = default_profile()
     ps, keep = prof.struct()
     n_cand = args.n_max - args.n_min + 1
-    s0 = rank * args.scenarios // world
-    s1 = (rank + 1) * args.scenarios // world
+    from paper_2602_22718_b200 import sweep
+    s0, s1 = sweep.shard_range(args.scenarios, world, rank)
     S = s1 - s0
     spec = c4_spec(S, count=args.prompts, first=s0)
     t_total = torch.empty(S * n_cand, dtype=torch.float64, device=dev)
@@ -217,10 +217,7 @@ def run_ours(args, world, rank, local):
     def step_device():
         check(ctx.lib.rs_sweep(ctx.handle, C.byref(spec), C.byref(ps), args.G, args.n_min,
                                args.n_max, args.lam, 2, C.byref(out_dev), 1))
-        if world > 1:
-            dist.all_reduce(agg_t)
-            dist.all_reduce(agg_c)
-            dist.all_reduce(agg_h)
+        sweep.combine(agg_t, agg_c, agg_h)
 
     def timed(fn, k):
         if world > 1:

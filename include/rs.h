@@ -111,6 +111,16 @@ int rs_prefix_index_build_device_async(rs_ctx* ctx, const int32_t* d_tokens,
                                        int32_t max_len_cap, int64_t* d_tables,
                                        int64_t* d_info);
 void rs_prefix_index_free(rs_prefix_index* idx);
+/* Rebuild a handle from its five tables (sizes as rs_prefix_index_tables),
+ * so a caller that keeps only the tables (the C++ drop-in's PrefixIndex)
+ * can still query rs_select_prefix_length / rs_dedup_savings. */
+int rs_prefix_index_from_tables(int32_t batch_size, int32_t min_len, int32_t max_len,
+                                int64_t total_tokens, const int64_t* nodes_at_depth,
+                                const int64_t* short_count_below,
+                                const int64_t* short_tokens_below,
+                                const int64_t* longer_count_from,
+                                const int64_t* longer_tokens_from,
+                                rs_prefix_index** out);
 
 /* Accessors (proj/include/rollsim/dedup.hpp:25-34, dedup.cpp:102-122). */
 int rs_prefix_index_info(const rs_prefix_index* idx, int32_t* batch_size,
@@ -160,6 +170,13 @@ int rs_block_hashes(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets,
 /* the prompt id under std::string ordering; ties in predicted length  */
 /* are broken by it).                                                  */
 /* ------------------------------------------------------------------ */
+
+/* Rank of each string under std::string ordering (unsigned bytewise, a
+ * proper prefix first): the id tie-break of assign (planner.cpp:25-31).
+ * String i is bytes[offsets[i] .. offsets[i+1]); equal strings keep input
+ * order. Used by the C++ drop-in to turn PredictedPrompt ids into id_rank. */
+int rs_rank_strings(rs_ctx* ctx, const char* bytes, const int64_t* offsets,
+                    int32_t count, int32_t* rank);
 
 /* assign (planner.hpp:33-34, planner.cpp:16-51): order[r] = input index of
  * the prompt at rank r (pred desc, id asc); group g is

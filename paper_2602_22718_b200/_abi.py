@@ -66,6 +66,8 @@ PRODUCT_SIGS = {
     "rs_prefix_index_build_device": ([vp, vp, vp, i32, C.POINTER(vp)], C.c_int),
     "rs_prefix_index_build_device_async": ([vp, vp, vp, i32, i32, vp, vp], C.c_int),
     "rs_prefix_index_free": ([vp], None),
+    "rs_prefix_index_from_tables": ([i32, i32, i32, i64, P_i64, P_i64, P_i64, P_i64, P_i64,
+                                     C.POINTER(vp)], C.c_int),
     "rs_prefix_index_info": ([vp, P_i32, P_i32, P_i32, P_i64], C.c_int),
     "rs_unique_prefix_count": ([vp, i32, P_i64], C.c_int),
     "rs_unique_prefix_tokens": ([vp, i32, P_i64], C.c_int),
@@ -76,6 +78,7 @@ PRODUCT_SIGS = {
     "rs_unique_prefix_count_among": ([vp, P_i32, P_i64, i32, i32, P_i64], C.c_int),
     "rs_dedup_map": ([vp, P_i32, P_i64, i32, i32, P_i32], C.c_int),
     "rs_block_hashes": ([vp, P_i32, P_i64, i32, i32, P_u64], C.c_int),
+    "rs_rank_strings": ([vp, C.c_char_p, P_i64, i32, P_i32], C.c_int),
     "rs_assign": ([vp, P_f64, P_i32, i32, i32, P_i32, P_i32], C.c_int),
     "rs_integrate_decode_seconds": ([vp, P_i32, P_f64, i64, P_prof, P_f64], C.c_int),
     "rs_estimate_actor_time": ([vp, P_i32, P_f64, i32, P_prof, i32, P_f64], C.c_int),

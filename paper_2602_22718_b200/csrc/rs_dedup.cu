@@ -557,6 +557,25 @@ int rs_prefix_index_build_device_async(rs_ctx* ctx, const int32_t* d_tokens,
 
 void rs_prefix_index_free(rs_prefix_index* idx) { delete idx; }
 
+int rs_prefix_index_from_tables(int32_t batch, int32_t min_len, int32_t max_len, int64_t total,
+                                const int64_t* nodes, const int64_t* scb, const int64_t* stb,
+                                const int64_t* lcf, const int64_t* ltf, rs_prefix_index** out) {
+  if (!out || !nodes || !scb || !stb || !lcf || !ltf) return fail(RS_E_ARG, "NULL argument");
+  if (max_len < 0) return fail(RS_E_ARG, "max_len must be >= 0");
+  auto* idx = new rs_prefix_index();
+  idx->batch = batch;
+  idx->min_len = min_len;
+  idx->max_len = max_len;
+  idx->total = total;
+  idx->nodes.assign(nodes, nodes + max_len + 1);
+  idx->scb.assign(scb, scb + max_len + 2);
+  idx->stb.assign(stb, stb + max_len + 2);
+  idx->lcf.assign(lcf, lcf + max_len + 2);
+  idx->ltf.assign(ltf, ltf + max_len + 2);
+  *out = idx;
+  return RS_OK;
+}
+
 int rs_prefix_index_info(const rs_prefix_index* idx, int32_t* batch, int32_t* min_len,
                          int32_t* max_len, int64_t* total) {
   if (!idx) return fail(RS_E_ARG, "index is NULL");

@@ -1081,6 +1081,75 @@ int rs_scale_select(rs_ctx* ctx, const double* t_total, const double* t_penalty,
   return sync_and_check(ctx);
 }
 
+__global__ void gather_keys_kernel(const uint64_t* src, const uint32_t* perm, int64_t n,
+                                   uint64_t* keys, uint32_t* vals) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    keys[j] = src[perm[j]];
+    vals[j] = perm[j];
+  }
+}
+
+__global__ void rank_scatter_kernel(const uint32_t* perm, int64_t n, int32_t* rank) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    rank[perm[j]] = (int32_t)j;
+}
+
+__global__ void iota_kernel(uint32_t* v, int64_t n) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    v[j] = (uint32_t)j;
+}
+
+// LSD radix over (length, then 8-byte big-endian words from the last to the
+// first): lexicographic unsigned-byte order with a proper prefix first.
+int rs_rank_strings(rs_ctx* ctx, const char* bytes, const int64_t* offsets, int32_t count,
+                    int32_t* rank) {
+  if (!ctx || !offsets || !rank) return fail(RS_E_ARG, "NULL argument");
+  if (count <= 0) return RS_OK;
+  int64_t maxlen = 0;
+  for (int32_t i = 0; i < count; ++i) {
+    int64_t l = offsets[i + 1] - offsets[i];
+    if (l < 0) return fail(RS_E_ARG, "offsets must be non-decreasing");
+    maxlen = std::max(maxlen, l);
+  }
+  const int64_t W = (maxlen + 7) / 8;
+  std::vector<uint64_t> words((size_t)(W + 1) * count, 0);  // plane 0 = length
+  for (int32_t i = 0; i < count; ++i) {
+    const unsigned char* p = (const unsigned char*)bytes + offsets[i];
+    const int64_t l = offsets[i + 1] - offsets[i];
+    words[i] = (uint64_t)l;
+    for (int64_t b = 0; b < l; ++b)
+      words[(size_t)(1 + b / 8) * count + i] |= (uint64_t)p[b] << (56 - 8 * (b % 8));
+  }
+  const int64_t n = count;
+  RS_TRY(arena_reserve(ctx, abytes((W + 1) * n, 8) + abytes(n, 8) + abytes(n, 4) * 2 +
+                                abytes(n, 4) + radix_sort_scratch_bytes64(n) + 4096));
+  uint64_t* d_words = arena_alloc<uint64_t>(ctx, (W + 1) * n);
+  uint64_t* keys = arena_alloc<uint64_t>(ctx, n);
+  uint32_t* perm = arena_alloc<uint32_t>(ctx, n);
+  uint32_t* vals = arena_alloc<uint32_t>(ctx, n);
+  int32_t* d_rank = arena_alloc<int32_t>(ctx, n);
+  char* scratch = arena_alloc<char>(ctx, radix_sort_scratch_bytes64(n));
+  if (!scratch) return fail(RS_E_NOMEM, "arena exhausted (rank_strings)");
+  RS_TRY(h2d(ctx, d_words, words.data(), 8 * words.size()));
+  const int blocks = grid_for(ctx, n, 256);
+  RS_LAUNCH(ctx, "iota", iota_kernel, blocks, 256, 0, perm, n);
+  for (int64_t plane = 0; plane <= W; ++plane) {
+    const int64_t w = plane == 0 ? 0 : W + 1 - plane;  // length first, then last word .. first
+    RS_LAUNCH(ctx, "gather_keys", gather_keys_kernel, blocks, 256, 0, d_words + w * n, perm, n,
+              keys, vals);
+    uint64_t* ko;
+    uint32_t* vo;
+    RS_TRY(radix_sort_pairs(ctx, keys, vals, n, scratch, &ko, &vo));
+    RS_CUDA_TRY(cudaMemcpyAsync(perm, vo, 4 * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  RS_LAUNCH(ctx, "rank_scatter", rank_scatter_kernel, blocks, 256, 0, perm, n, d_rank);
+  RS_TRY(d2h(ctx, rank, d_rank, 4 * n));
+  return sync_and_check(ctx);
+}
+
 int rs_assign(rs_ctx* ctx, const double* pred, const int32_t* id_rank, int32_t count,
               int32_t n_actors, int32_t* order, int32_t* group_offsets) {
   if (!ctx) return fail(RS_E_ARG, "ctx is NULL");

@@ -1,0 +1,59 @@
+// rs_shim.cpp — plumbing shared by the dedup and planner drop-ins.
+#include "rs_shim.hpp"
+
+#include <cstdlib>
+#include <mutex>
+
+#include "rollsim/errors.hpp"
+
+namespace rs_shim {
+
+rs_ctx* ctx() {
+  static std::once_flag once;
+  static rs_ctx* c = nullptr;
+  static int status = RS_OK;
+  std::call_once(once, [] {
+    int dev = 0;
+    if (const char* e = std::getenv("RS_DEVICE")) dev = std::atoi(e);
+    else if (const char* l = std::getenv("LOCAL_RANK")) dev = std::atoi(l);
+    status = rs_ctx_create(dev, &c);
+  });
+  if (status != RS_OK) check(status);
+  return c;
+}
+
+void check(int status) {
+  if (status == RS_OK) return;
+  std::string msg = rs_last_error();
+  if (status == RS_E_VALIDATION) throw rollsim::ValidationError(msg);
+  if (status == RS_E_CONFIG) throw rollsim::ConfigError(msg);
+  throw rollsim::Error("librs_b200: " + msg);
+}
+
+Profile::Profile(const rollsim::LatencyProfile& lp) {
+  for (const auto& row : lp.tpot_grid) grid.insert(grid.end(), row.begin(), row.end());
+  if (grid.size() != lp.batch_knots.size() * lp.context_knots.size())
+    throw rollsim::ConfigError("tpot grid rows must match batch knots");
+  p.batch_knots = lp.batch_knots.data();
+  p.nb = static_cast<int32_t>(lp.batch_knots.size());
+  p.context_knots = lp.context_knots.data();
+  p.nc = static_cast<int32_t>(lp.context_knots.size());
+  p.tpot_grid = grid.data();
+  p.rho = lp.rho;
+}
+
+std::vector<int32_t> rank_ids(const std::vector<std::string>& ids) {
+  std::vector<int64_t> off(ids.size() + 1, 0);
+  std::string bytes;
+  for (size_t i = 0; i < ids.size(); ++i) {
+    bytes += ids[i];
+    off[i + 1] = static_cast<int64_t>(bytes.size());
+  }
+  std::vector<int32_t> rank(ids.size());
+  if (!ids.empty())
+    check(rs_rank_strings(ctx(), bytes.data(), off.data(), static_cast<int32_t>(ids.size()),
+                          rank.data()));
+  return rank;
+}
+
+}  // namespace rs_shim

@@ -1,0 +1,55 @@
+"""The reference's OWN test suites (proj/tests/test_dedup.cpp,
+test_planner.cpp, test_profile.cpp, test_training.cpp, acceptance_main.cpp),
+compiled unchanged against the C++ drop-in (build/shim/*_b200: reference
+objects minus dedup/planner + our shim over librs_b200.so). The *_ref twins
+link the unmodified reference library and pin the minimal doctest harness.
+The binaries are built where /root/reference exists (`make shim`) and travel
+with the repo; without them these tests are skipped."""
+import pathlib
+import re
+import subprocess
+
+import pytest
+
+REPO = pathlib.Path(__file__).resolve().parents[1]
+SHIM = REPO / "build" / "shim"
+SUITES = ["test_dedup", "test_planner", "test_profile", "test_training"]
+# The unmodified reference fails this one case itself (cmd_plan_bench with a
+# 1-prompt batch asks scale() for n_max > prompts); the drop-in must match.
+KNOWN_REF_FAILURES = {"test_training": {"plan bench runs on small batches"}}
+
+
+def run(binary, timeout=900):
+    if not binary.exists():
+        pytest.skip(f"{binary.name} not built (needs /root/reference at build time)")
+    p = subprocess.run([str(binary)], capture_output=True, text=True, timeout=timeout)
+    return p.returncode, p.stdout + p.stderr
+
+
+def failed_cases(out):
+    return set(re.findall(r"\[case failed\] (.*)", out))
+
+
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_suite_on_reference(suite):
+    code, out = run(SHIM / f"{suite}_ref")
+    assert failed_cases(out) == KNOWN_REF_FAILURES.get(suite, set()), out[-3000:]
+
+
+def test_acceptance_on_reference():
+    code, out = run(SHIM / "acceptance_main_ref")
+    assert out.count("[PASS]") == 10, out[-3000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_suite_on_dropin(suite):
+    code, out = run(SHIM / f"{suite}_b200")
+    assert "test cases:" in out, out[-3000:]
+    assert failed_cases(out) == KNOWN_REF_FAILURES.get(suite, set()), out[-3000:]
+
+
+@pytest.mark.gpu
+def test_acceptance_on_dropin():
+    code, out = run(SHIM / "acceptance_main_b200")
+    assert out.count("[PASS]") == 10, out[-3000:]
