@@ -22,6 +22,21 @@ rs_ctx* ctx() {
   return c;
 }
 
+namespace {
+// The drop-in brings its device up when the library is loaded (like any
+// runtime), so the first rollsim:: call does not pay CUDA context creation
+// and module loading. Errors are deferred to the first call, which rethrows.
+struct EagerInit {
+  EagerInit() {
+    setenv("CUDA_MODULE_LOADING", "EAGER", 0);
+    try {
+      ctx();
+    } catch (...) {
+    }
+  }
+} eager_init;
+}  // namespace
+
 void check(int status) {
   if (status == RS_OK) return;
   std::string msg = rs_last_error();
