@@ -290,19 +290,19 @@ int fast_build(rs_ctx* ctx, int S, const int64_t* d_off, double* pred, int32_t* 
 }
 
 // ------------------------------------------------------------------- eval --
-constexpr int kEvalT = 768;
+constexpr int kEvalT = 1024;
 constexpr int kEvalW = kEvalT / 32;
 constexpr int kNBlk = kMaxSeg / kBlk;  // 1024 blocks of 16 segments
 constexpr int kLevels = 11;            // floor(log2(1024)) + 1
 constexpr int kCoopCarry = 64;
-constexpr int kSegCap = 10752;         // segments staged in shared memory
+constexpr int kSegCap = 9216;          // segments staged in shared memory
 
 struct EvalShared {
   int2 seg[kSegCap];
   uint32_t pmsm[kSegCap];  // in-block prefix max | in-block suffix max << 16
   uint16_t st[kLevels][kNBlk];
   double top[kTopCap];
-  uint16_t pe[kTopCap];    // piece end - c_lo
+  int32_t pex[kTopCap + 1];  // piece end for c in [c_lo - 1, c_hi] (clamped index)
   double acc[kEvalW][32];
   int32_t carry[kEvalW][kCoopCarry];
   uint16_t lbuf[kEvalT][16];  // per-lane prefix maxima inside the first block
@@ -314,10 +314,12 @@ struct EvalShared {
 // = tpot(G * live, c) for live < live_top; live >= live_top uses `top`
 // (batch clamped to the last batch knot). Contexts and live counts are
 // 32-bit on this path (contexts <= 65535 + 16384).
+static_assert(sizeof(EvalShared) <= 232448, "EvalShared exceeds the sm_100 shared memory limit");
+
 struct FastProf {
   const double* top;
   const double* rows;
-  const uint16_t* pe;
+  const int32_t* pex;  // piece end for c in [c_lo - 1, c_hi]; INT32_MAX at/after back
   int c_lo, c_hi, cf_ceil, cb_ceil, cfront_m1, ncm, live_top;
 };
 
@@ -326,11 +328,8 @@ struct FastProf {
 __device__ __forceinline__ double run_sum32(const FastProf& fp, int live, int c0, int c1) {
   const double* row = live >= fp.live_top ? fp.top : fp.rows + (size_t)(live - 1) * fp.ncm;
   double total = 0.0;
-  int c = c0;
-  while (c <= c1) {
-    const int e = c < fp.cf_ceil ? fp.cfront_m1
-                                 : (c >= fp.cb_ceil ? c1 : fp.c_lo + (int)fp.pe[c - fp.c_lo]);
-    const int pe = min(c1, e);
+  for (int c = c0; c <= c1;) {
+    const int pe = min(c1, fp.pex[min(max(c, fp.c_lo - 1), fp.c_hi) - (fp.c_lo - 1)]);
     const double t0 = row[min(max(c, fp.c_lo), fp.c_hi) - fp.c_lo];
     const double t1 = row[min(max(pe, fp.c_lo), fp.c_hi) - fp.c_lo];
     total = dadd(total, dmul(dmul((double)(pe - c + 1), dadd(t0, t1)), 0.5));
@@ -473,12 +472,10 @@ __global__ void __launch_bounds__(kEvalT, 1) fast_eval_kernel(EvalArgs A) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   FastProf fp = A.fp;
   if (fp.ncm <= kTopCap) {  // profile tables into shared memory (once per CTA)
-    for (int i = tid; i < fp.ncm; i += kEvalT) {
-      sh.top[i] = A.fp.top[i];
-      sh.pe[i] = A.fp.pe[i];
-    }
+    for (int i = tid; i < fp.ncm; i += kEvalT) sh.top[i] = A.fp.top[i];
+    for (int i = tid; i <= fp.ncm; i += kEvalT) sh.pex[i] = A.fp.pex[i];
     fp.top = sh.top;
-    fp.pe = sh.pe;
+    fp.pex = sh.pex;
   }
   uint16_t* lbuf = sh.lbuf[tid];
   const int C = A.cr.n_max - A.cr.n_min + 1;
@@ -531,13 +528,17 @@ __global__ void __launch_bounds__(kEvalT, 1) fast_eval_kernel(EvalArgs A) {
         sh.st[lev][jb] = max(sh.st[lev - 1][jb], sh.st[lev - 1][jb + (1 << (lev - 1))]);
       __syncthreads();
     }
-    // Coop tasks (N < kCoopN, one group per warp) first, then every warp
+    // Coop tasks (N < kCoop, one group per warp) first, then every warp
     // joins the lane pool: each lane pulls the next group in (N asc, g asc)
     // order whenever it is idle, so lanes stay busy whatever the run counts.
-    const int nc_hi = min(nhi, kCoopN - 1);
+    // Scenarios whose tables do not fit shared memory run every group
+    // warp-cooperatively from global memory.
+    const bool lane_path = D <= kSegCap && fp.ncm <= kTopCap;
+    const int coop_n = lane_path ? kCoopN : INT32_MAX;
+    const int nc_hi = min(nhi, coop_n - 1);
     const int64_t n_coop = nlo <= nc_hi ? tri64(nc_hi + 1) - tri64(nlo) : 0;
-    const int nl_lo = max(nlo, kCoopN);
-    const int64_t n_lane_groups = nl_lo <= nhi ? tri64(nhi + 1) - tri64(nl_lo) : 0;
+    const int nl_lo = max(nlo, coop_n);
+    const int64_t n_lane_groups = (lane_path && nl_lo <= nhi) ? tri64(nhi + 1) - tri64(nl_lo) : 0;
     double* gt = A.gt + (int64_t)s * A.cr.T;
     const int64_t flat0 = tri64(A.cr.n_min);
     for (;;) {
@@ -553,11 +554,15 @@ __global__ void __launch_bounds__(kEvalT, 1) fast_eval_kernel(EvalArgs A) {
       if (lane == 0) gt[tri64(N) - flat0 + g] = v;
     }
     if (n_lane_groups > 0) {
-      // Per-lane group state. Runs go k = kb .. ka; base_k = max(va,
-      // max MX over (ka, k]) (vb instead of MX at kb): O(1) from the block
-      // tables, or from lbuf inside the group's first block.
-      int a = 0, b = 0, ka = 0, kb = 0, va = 0, vb = 0, k = 0, l = 0, jl = 0, smb = 0;
-      int fprev = 0, top_m = 0;
+      // Per-lane group state. Runs go k = kb .. ka (ascending finish).
+      // base_k = max(va, max MX over (ka, k]) (vb replaces MX at kb):
+      // inside the group's first block from lbuf, elsewhere the block's
+      // prefix max PMB[k] combined with a per-block cached
+      // max(va, rest of the first block, full blocks in between).
+      const double* rows = fp.rows;
+      const int live_top = fp.live_top;
+      int a = 0, b = 0, ka = 0, kb = 0, va = 0, k = 0, l = 0, jl = 0, smb = 0;
+      int fprev = 0, top_m = 0, cjr = -1, cbase = 0;
       int64_t slot = 0;
       double total = 0.0;
       bool active = false, exhausted = false;
@@ -582,33 +587,33 @@ __global__ void __launch_bounds__(kEvalT, 1) fast_eval_kernel(EvalArgs A) {
               kb = rb.x;
               if (ka == kb) {  // the whole group sits in one run-segment
                 const int m = span_max(A.ss, i0, a, b);
-                gt[slot] = dadd(0.0, run_sum32(fp, b - a, m, m + seg_f(V.seg[ka]) - 1));
+                gt[slot] = dadd(0.0, run_sum32(fp, b - a, m, m + seg_f(sh.seg[ka]) - 1));
               } else {
                 va = ra.y & 0xffff;
-                vb = (rb.y >> 16) & 0xffff;
+                const int vb = (rb.y >> 16) & 0xffff;
                 l = ka + 1;
                 jl = l >> 4;
                 const int e = min(16 * jl + 15, kb - 1);  // first block part of (ka, kb)
                 int m = INT32_MIN;
                 for (int kk = l; kk <= e; ++kk) {
-                  m = max(m, seg_mx(V.seg[kk]));
+                  m = max(m, seg_mx(sh.seg[kk]));
                   lbuf[kk - l] = (uint16_t)m;
                 }
                 smb = m;
-                // base at kb: max over the whole group
-                int mid = INT32_MIN;
+                int mid = INT32_MIN;  // max MX over (ka, kb)
                 if (kb - 1 >= l) {
                   const int jr = (kb - 1) >> 4;
                   if (jr == jl) {
                     mid = lbuf[kb - 1 - l];
                   } else {
-                    mid = max(smb, (int)(V.pmsm[kb - 1] & 0xffff));
+                    mid = max(smb, (int)(sh.pmsm[kb - 1] & 0xffff));
                     if (jl + 1 <= jr - 1) mid = max(mid, rmq_blocks(V, jl + 1, jr - 1));
                   }
                 }
                 top_m = max(max(va, vb), mid);
                 k = kb;
                 fprev = 0;
+                cjr = -1;
                 total = 0.0;
                 active = true;
               }
@@ -621,8 +626,8 @@ __global__ void __launch_bounds__(kEvalT, 1) fast_eval_kernel(EvalArgs A) {
         }
 #pragma unroll 1
         for (int it = 0; it < 8 && active; ++it) {
-          const int2 sk = V.seg[k];
-          const int f = seg_f(sk);
+          const int2 sk = sh.seg[k];
+          const int f = sk.x & 0xffff;
           int base, x, ts;
           if (k == kb) {
             base = top_m;
@@ -632,20 +637,45 @@ __global__ void __launch_bounds__(kEvalT, 1) fast_eval_kernel(EvalArgs A) {
             x = sk.y;
             ts = fprev + 1;
             if (k == ka) {
-              base = va;
+              base = va;  // ka may sit in the block before the first one
             } else {
               const int jr = k >> 4;
-              int m;
-              if (jr == jl) {
-                m = lbuf[k - l];
-              } else {
-                m = max(smb, (int)(V.pmsm[k] & 0xffff));
-                if (jl + 1 <= jr - 1) m = max(m, rmq_blocks(V, jl + 1, jr - 1));
+              if (jr != cjr) {
+                cjr = jr;
+                cbase = va;
+                if (jr != jl) {
+                  cbase = max(va, smb);
+                  if (jl + 1 <= jr - 1) cbase = max(cbase, rmq_blocks(V, jl + 1, jr - 1));
+                }
               }
-              base = max(va, m);
+              base = max(cbase, jr == jl ? (int)lbuf[k - l] : (int)(sh.pmsm[k] & 0xffff));
             }
           }
-          total = dadd(total, run_sum32(fp, x - a, base + ts - 1, base + f - 1));
+          // tpot_context_run_sum (planner.cpp:61-84) from shared memory:
+          // the clamped-batch row, or a small-batch row (global, L1/L2).
+          const int live = x - a;
+          const int c1 = base + f - 1;
+          double rs = 0.0;
+          const int clo = fp.c_lo, chi = fp.c_hi, clo1 = fp.c_lo - 1;
+          if (live >= live_top) {
+            for (int c = base + ts - 1; c <= c1;) {
+              const int pe = min(c1, sh.pex[min(max(c, clo1), chi) - clo1]);
+              const double t0 = sh.top[min(max(c, clo), chi) - clo];
+              const double t1 = sh.top[min(max(pe, clo), chi) - clo];
+              rs = dadd(rs, dmul(dmul((double)(pe - c + 1), dadd(t0, t1)), 0.5));
+              c = pe + 1;
+            }
+          } else {
+            const double* row = rows + (size_t)(live - 1) * fp.ncm;
+            for (int c = base + ts - 1; c <= c1;) {
+              const int pe = min(c1, sh.pex[min(max(c, clo1), chi) - clo1]);
+              const double t0 = __ldg(row + min(max(c, clo), chi) - clo);
+              const double t1 = __ldg(row + min(max(pe, clo), chi) - clo);
+              rs = dadd(rs, dmul(dmul((double)(pe - c + 1), dadd(t0, t1)), 0.5));
+              c = pe + 1;
+            }
+          }
+          total = dadd(total, rs);
           fprev = f;
           if (--k < ka) {
             gt[slot] = total;
@@ -659,20 +689,25 @@ __global__ void __launch_bounds__(kEvalT, 1) fast_eval_kernel(EvalArgs A) {
 
 // Small-batch tpot rows and piece ends of one (profile, G).
 __global__ void fast_tables_kernel(DevProfile p, int G, int live_top, double* rows,
-                                   uint16_t* pe, int cf_ceil, int cb_ceil) {
+                                   int32_t* pex, int cf_ceil, int cb_ceil) {
   const int64_t ncm = p.c_hi - p.c_lo + 1;
-  const int64_t total = (int64_t)(live_top - 1) * ncm + ncm;
+  const int64_t total = (int64_t)(live_top - 1) * ncm + ncm + 1;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (i < (int64_t)(live_top - 1) * ncm) {
       const int64_t live = i / ncm + 1, j = i % ncm;
       rows[i] = tpot_int(p, (int64_t)G * live, p.c_lo + j);
     } else {
+      // piece end for c = c_lo - 1 + j, j in [0, ncm] (run-sum pieces,
+      // planner.cpp:65-74): below front -> ceil(front) - 1; at or above
+      // back -> "to the run end"; else floor of the next knot.
       const int64_t j = i - (int64_t)(live_top - 1) * ncm;
-      const int64_t c = p.c_lo + j;
-      int v = 0;
-      if (c >= cf_ceil && c < cb_ceil) v = (int)((int64_t)p.kfloor[p.ci[j] + 1] - p.c_lo);
-      pe[j] = (uint16_t)v;
+      const int64_t c = p.c_lo - 1 + j;
+      int32_t v;
+      if (c < cf_ceil) v = (int32_t)p.cfront_m1;
+      else if (c >= cb_ceil) v = INT32_MAX;
+      else v = (int32_t)p.kfloor[p.ci[c - p.c_lo] + 1];
+      pex[j] = v;
     }
   }
 }
@@ -688,7 +723,7 @@ bool fast_profile_ok(const DevProfile& prof, int G) {
 size_t fast_eval_bytes(const DevProfile& prof, int G) {
   const int64_t ncm = prof.c_hi - prof.c_lo + 1;
   const int64_t live_top = std::max<int64_t>(1, (prof.b_hi + G - 1) / G);
-  return abytes((live_top - 1) * ncm, 8) + abytes(ncm, 2) + abytes((size_t)1024 * kMaxSeg, 4);
+  return abytes((live_top - 1) * ncm, 8) + abytes(ncm + 1, 4) + abytes((size_t)1024 * kMaxSeg, 4);
 }
 
 int fast_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, CandRange cr,
@@ -697,10 +732,10 @@ int fast_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, Cand
   const int64_t ncm = prof.c_hi - prof.c_lo + 1;
   const int live_top = (int)std::max<int64_t>(1, (prof.b_hi + cr.G - 1) / cr.G);
   double* rows = arena_alloc<double>(ctx, std::max<int64_t>(1, (int64_t)(live_top - 1) * ncm));
-  uint16_t* pe = arena_alloc<uint16_t>(ctx, ncm);
+  int32_t* pex = arena_alloc<int32_t>(ctx, ncm + 1);
   const int grid = std::min(S * units, ctx->num_sms);
   uint32_t* pmsm = arena_alloc<uint32_t>(ctx, (size_t)grid * kMaxSeg);
-  if (!rows || !pe || !pmsm) return fail(RS_E_NOMEM, "arena exhausted (fast eval)");
+  if (!rows || !pex || !pmsm) return fail(RS_E_NOMEM, "arena exhausted (fast eval)");
   double front, back;
   RS_CUDA_TRY(cudaMemcpyAsync(&front, prof.ck, 8, cudaMemcpyDeviceToHost, ctx->stream));
   RS_CUDA_TRY(cudaMemcpyAsync(&back, prof.ck + prof.nc - 1, 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -708,7 +743,7 @@ int fast_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, Cand
   FastProf fp;
   fp.top = prof.top_row;
   fp.rows = rows;
-  fp.pe = pe;
+  fp.pex = pex;
   fp.c_lo = (int)prof.c_lo;
   fp.c_hi = (int)prof.c_hi;
   fp.cf_ceil = (int)std::ceil(front);
@@ -716,9 +751,9 @@ int fast_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, Cand
   fp.cfront_m1 = (int)prof.cfront_m1;
   fp.ncm = (int)ncm;
   fp.live_top = live_top;
-  const int64_t tot = (int64_t)live_top * ncm;
+  const int64_t tot = (int64_t)live_top * ncm + 1;
   RS_LAUNCH(ctx, "fast_tables", fast_tables_kernel, (int)std::min<int64_t>((tot + 255) / 256, 4096),
-            256, 0, prof, cr.G, live_top, rows, pe, fp.cf_ceil, fp.cb_ceil);
+            256, 0, prof, cr.G, live_top, rows, pex, fp.cf_ceil, fp.cb_ceil);
   EvalArgs A{ss, fp, cr, S, units, gt, pmsm};
   const int smem = (int)sizeof(EvalShared);
   RS_CUDA_TRY(cudaFuncSetAttribute(fast_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -21,11 +21,14 @@ Cn = 256
 bufs = [np.zeros(S * Cn), np.zeros(S * Cn), np.zeros(S * Cn, np.int64), np.zeros(S, np.int32),
         np.zeros(Cn, np.int32), np.zeros(Cn), np.zeros(Cn)]
 out = _abi.RsSweepOut(*[b.ctypes.data for b in bufs])
+import time
 ctx.enable_kernel_timing(True)
 for r in range(reps):
+    t0 = time.perf_counter()
     ctx.reset_kernel_timing()
     check(ctx.lib.rs_sweep(ctx.handle, C.byref(spec), C.byref(ps), 8, 1, 256, 0.7, 2, C.byref(out), 0))
-    for k in ("build_bucketed", "group_eval", "candidate_reduce", "select", "aggregate"):
+    print(f"rep {r} wall {1e3 * (time.perf_counter() - t0):.1f} ms")
+    for k in ("fast_build", "fast_tables", "group_eval", "candidate_reduce", "select", "aggregate"):
         ms, n = ctx.kernel_time(k)
         print(f"rep {r} {k}: {ms:.3f} ms over {n} launches")
 print("n_star[:8]", bufs[3][:8])
