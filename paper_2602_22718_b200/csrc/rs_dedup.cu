@@ -194,8 +194,50 @@ __device__ __forceinline__ int warp_lcp(const int32_t* __restrict__ pm,
   return n;
 }
 
+__device__ __forceinline__ uint32_t dev_cap(int K) {
+  const uint32_t need = 2u * (uint32_t)K + 2u;
+  uint32_t c = 64;
+  while (c < need) c <<= 1;
+  return c;
+}
+
+// Clears the grouping tables for this round (capacity from the device-side
+// member count) and the next round's counter.
+__global__ void round_prep_kernel(DedupState st, const int* kcur, int* knext) {
+  const int K = *kcur;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *knext = 0;
+  if (K <= 0) return;
+  const uint32_t cap = dev_cap(K);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
+    st.a_keys[i] = kEmpty;
+    st.b_keys[i] = kEmpty;
+    st.b_rep[i] = INT32_MAX;
+    st.b_cnt[i] = 0;
+  }
+}
+
+// Record member k's branch (x, t) against representative r of class c.
+__device__ __forceinline__ void record_member(const DedupState& st, int64_t k, int m, int c, int r,
+                                              int x, int lm, int lr, uint32_t mask) {
+  if (x == lm && x == lr) {  // exact duplicate of r: skipped (dedup.cpp:62)
+    st.m_slot[k] = -1;
+    if (st.labels) st.labels[m] = r;
+    return;
+  }
+  const uint64_t t = x < lm ? (uint64_t)(uint32_t)st.tok[st.off[m] + x] : kEnd;
+  bool created;
+  const uint32_t sa = table_insert(st.a_keys, mask, ((uint64_t)c << 32) | (uint32_t)x, &created);
+  const uint32_t sb = table_insert(st.b_keys, mask, ((uint64_t)sa << 33) | t, &created);
+  atomicMin(st.b_rep + sb, m);
+  atomicAdd(st.b_cnt + sb, 1);
+  st.m_slot[k] = (int32_t)sb;
+}
+
 __global__ void __launch_bounds__(256)
-compare_kernel(DedupState st, int cur, int K, uint32_t mask) {
+compare_kernel(DedupState st, int cur, const int* kcur) {
+  const int K = *kcur;
+  if (K <= 0) return;
+  const uint32_t mask = dev_cap(K) - 1;
   const int lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < K; k += W) {
@@ -206,25 +248,164 @@ compare_kernel(DedupState st, int cur, int K, uint32_t mask) {
     const int lm = st.len[m], lr = st.len[r];
     const int n = min(lm, lr);
     const int x = warp_lcp(st.tok + st.off[m], st.tok + st.off[r], l0, n);
-    if (lane == 0) {
-      if (x == lm && x == lr) {  // exact duplicate of r: skipped (dedup.cpp:62)
-        st.m_slot[k] = -1;
-        if (st.labels) st.labels[m] = r;
-      } else {
-        uint64_t t = x < lm ? (uint64_t)(uint32_t)st.tok[st.off[m] + x] : kEnd;
-        bool created;
-        uint32_t sa = table_insert(st.a_keys, mask, ((uint64_t)c << 32) | (uint32_t)x, &created);
-        uint32_t sb = table_insert(st.b_keys, mask, ((uint64_t)sa << 33) | t, &created);
-        atomicMin(st.b_rep + sb, m);
-        atomicAdd(st.b_cnt + sb, 1);
-        st.m_slot[k] = (int32_t)sb;
-      }
+    if (lane == 0) record_member(st, k, m, c, r, x, lm, lr, mask);
+  }
+}
+
+// Round 0 (one class, representative = prompt 0): the HBM-bound pass.
+// The representative is staged once per CTA in shared memory; every warp
+// streams its member through a 4-stage cp.async ring (2 KB per stage) so
+// ~8 KB per warp are in flight without holding registers, and compares
+// 512 tokens per stage with a warp-min for the first mismatch.
+constexpr int kStreamStages = 4;
+constexpr int kStageTok = 512;
+constexpr int kStreamWarps = 8;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+__global__ void __launch_bounds__(kStreamWarps * 32)
+compare_stream_kernel(DedupState st, const int* kcur) {
+  extern __shared__ __align__(16) int32_t sm[];
+  __shared__ int2 slot_meta[kStreamWarps][kStreamStages];  // (member, window) per ring slot
+  const int K = *kcur;
+  if (K <= 0) return;
+  const uint32_t mask = dev_cap(K) - 1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lr = st.len[0];
+  int32_t* rep = sm;  // [lr padded to 4]
+  int32_t* ring = sm + ((lr + 3) & ~3) + kStageTok * kStreamStages * wid;
+  int2* meta = slot_meta[wid];
+  const int32_t* pr = st.tok + st.off[0];
+  for (int i = threadIdx.x; i < lr; i += blockDim.x) rep[i] = pr[i];
+  __syncthreads();
+  // Each warp owns a contiguous block of members (adjacent prompts are
+  // adjacent in the CSR) and streams their windows back to back: the issue
+  // cursor runs kStreamStages-1 windows ahead of the compare cursor across
+  // member boundaries, so the ring never drains between members; windows of
+  // a member whose mismatch is already known are not issued.
+  const int64_t nw = (int64_t)gridDim.x * kStreamWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kStreamWarps + wid;
+  const int64_t k_begin = K * gw / nw, k_end = K * (gw + 1) / nw;
+  for (int64_t kb0 = k_begin; kb0 < k_end; kb0 += 32) {
+    const int cnt = (int)(k_end - kb0 < 32 ? k_end - kb0 : 32);
+    int my_m = 0, my_n = 0, my_lm = 0, my_shift = 0, my_nwin = 0;
+    unsigned long long my_src = 0;
+    if (lane < cnt) {  // lane i holds member kb0 + i
+      my_m = st.mem_idx[0][kb0 + lane];
+      my_lm = st.len[my_m];
+      my_n = min(my_lm, lr);
+      const int32_t* pm = st.tok + st.off[my_m];
+      my_shift = (int)(((uintptr_t)pm >> 2) & 3);
+      my_src = reinterpret_cast<unsigned long long>(pm - my_shift);
+      my_nwin = (my_n + my_shift + kStageTok - 1) / kStageTok;
     }
+    int im = 0, iwin = 0;           // next window to issue
+    int seq_issue = 0, seq_cmp = 0;
+    int cur = -1, found = INT32_MAX;  // member being compared, its mismatch
+    auto issue_next = [&]() {
+      if (im == cur && found != INT32_MAX) {  // mismatch known: skip the rest
+        ++im;
+        iwin = 0;
+      }
+      while (im < cnt && iwin >= __shfl_sync(0xffffffffu, my_nwin, im)) {
+        ++im;
+        iwin = 0;
+      }
+      const int slot = seq_issue % kStreamStages;
+      if (im < cnt) {
+        const int n = __shfl_sync(0xffffffffu, my_n, im);
+        const int sh = __shfl_sync(0xffffffffu, my_shift, im);
+        const int32_t* src = reinterpret_cast<const int32_t*>(__shfl_sync(0xffffffffu, my_src, im));
+        int32_t* dst = ring + slot * kStageTok;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = lane + 32 * q;
+          const int p = -sh + iwin * kStageTok + 4 * j;
+          const int valid = min(4, max(0, n - p));
+          cp_async16(dst + 4 * j, valid > 0 ? src + iwin * kStageTok + 4 * j : src, valid * 4);
+        }
+        if (lane == 0) meta[slot] = make_int2(im, iwin);
+        ++iwin;
+      } else if (lane == 0) {
+        meta[slot] = make_int2(-1, 0);
+      }
+      cp_async_commit();
+      ++seq_issue;
+    };
+    auto finish = [&](int i) {  // record member i
+      const int m = __shfl_sync(0xffffffffu, my_m, i);
+      const int lm = __shfl_sync(0xffffffffu, my_lm, i);
+      const int n = __shfl_sync(0xffffffffu, my_n, i);
+      if (lane == 0) record_member(st, kb0 + i, m, 0, 0, found == INT32_MAX ? n : found, lm, lr, mask);
+    };
+    for (int s0 = 0; s0 < kStreamStages - 1; ++s0) issue_next();
+    for (;;) {
+      issue_next();
+      cp_async_wait<kStreamStages - 1>();
+      __syncwarp();
+      const int slot = seq_cmp % kStreamStages;
+      const int2 mw = meta[slot];
+      ++seq_cmp;
+      if (mw.x < 0) break;  // the issuer ran dry and everything issued is consumed
+      if (mw.x != cur) {
+        if (cur >= 0) finish(cur);
+        cur = mw.x;
+        found = INT32_MAX;
+      }
+      if (found != INT32_MAX) continue;  // already resolved: skip this window
+      const int n = __shfl_sync(0xffffffffu, my_n, cur);
+      const int sh = __shfl_sync(0xffffffffu, my_shift, cur);
+      const int32_t* buf = ring + slot * kStageTok;
+      int best = INT32_MAX;
+      if (sh == 0) {  // member and representative chunks are both 16B aligned
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = lane + 32 * q;
+          const int p = mw.y * kStageTok + 4 * j;
+          if (best == INT32_MAX && p < n) {
+            const int4 a4 = *reinterpret_cast<const int4*>(buf + 4 * j);
+            const int4 b4 = *reinterpret_cast<const int4*>(rep + p);
+            const int e[4] = {a4.x, a4.y, a4.z, a4.w};
+            const int f[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if (best == INT32_MAX && p + t < n && e[t] != f[t]) best = p + t;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = lane + 32 * q;
+          const int p = -sh + mw.y * kStageTok + 4 * j;
+          const int4 a4 = *reinterpret_cast<const int4*>(buf + 4 * j);
+          const int e[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int pos = p + t;
+            if (pos >= 0 && pos < n && best == INT32_MAX && e[t] != rep[pos]) best = pos;
+          }
+        }
+      }
+      found = warp_min(best);
+      __syncwarp();
+    }
+    if (cur >= 0) finish(cur);
+    cp_async_wait<0>();
+    __syncwarp();
   }
 }
 
 // One thread per B slot: branch children, leaves, next classes.
-__global__ void finalize_kernel(DedupState st, int cur, uint32_t cap) {
+__global__ void finalize_kernel(DedupState st, int cur, const int* kcur) {
+  const int K = *kcur;
+  if (K <= 0) return;
+  const uint32_t cap = dev_cap(K);
   const int nxt = cur ^ 1;
   for (uint32_t sb = blockIdx.x * blockDim.x + threadIdx.x; sb < cap; sb += gridDim.x * blockDim.x) {
     uint64_t key = st.b_keys[sb];
@@ -250,7 +431,9 @@ __global__ void finalize_kernel(DedupState st, int cur, uint32_t cap) {
   }
 }
 
-__global__ void compact_kernel(DedupState st, int cur, int K) {
+__global__ void compact_kernel(DedupState st, int cur, const int* kcur, int* knext) {
+  const int K = *kcur;
+  if (K <= 0) return;
   const int nxt = cur ^ 1;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
     int sb = st.m_slot[k];
@@ -268,7 +451,7 @@ __global__ void compact_kernel(DedupState st, int cur, int K) {
     int leader = __ffs(act) - 1;
     int rank = __popc(act & ((1u << (threadIdx.x & 31)) - 1));
     int base = 0;
-    if ((threadIdx.x & 31) == leader) base = atomicAdd(st.counter, __popc(act));
+    if ((threadIdx.x & 31) == leader) base = atomicAdd(knext, __popc(act));
     base = __shfl_sync(act, base, leader);
     st.mem_idx[nxt][base + rank] = m;
     st.mem_cls[nxt][base + rank] = sb;
@@ -276,34 +459,80 @@ __global__ void compact_kernel(DedupState st, int cur, int K) {
 }
 
 // The five PrefixIndex tables from the difference array and the counts
-// (dedup.cpp:73-98). One CTA; maxd is small (max prompt length).
-__global__ void tables_kernel(DedupState st, int maxd, int64_t* out /*5*(maxd+2)*/) {
-  if (threadIdx.x != 0) return;
+// (dedup.cpp:73-98): one CTA, chunked block scans with a carried total.
+constexpr int kTabT = 1024;
+
+__device__ __forceinline__ int64_t block_incl_scan64(int64_t v, int64_t* wsum) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t incl = warp_incl_sum(v);
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int64_t x = wsum[lane];
+    wsum[lane] = warp_incl_sum(x) - x;
+  }
+  __syncthreads();
+  int64_t r = wsum[wid] + incl;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kTabT) tables_kernel(DedupState st, int maxd, int64_t* out) {
+  __shared__ int64_t wsum[32];
   int64_t* nodes = out;
   int64_t* scb = out + (maxd + 2);
   int64_t* stb = out + 2 * (int64_t)(maxd + 2);
   int64_t* lcf = out + 3 * (int64_t)(maxd + 2);
   int64_t* ltf = out + 4 * (int64_t)(maxd + 2);
-  int64_t run = 0;
-  nodes[0] = 0;
-  for (int d = 1; d <= maxd; ++d) {
-    run += st.node_diff[d];
-    nodes[d] = run;
+  const int n = maxd + 2;  // indices 0 .. maxd+1
+  int64_t c_nodes = 0, c_scb = 0, c_stb = 0;
+  for (int d0 = 0; d0 < n; d0 += kTabT) {
+    const int d = d0 + threadIdx.x;
+    // nodes[d] = sum_{1<=i<=d} node_diff[i] for 1<=d<=maxd; 0 elsewhere
+    const int64_t nd = (d >= 1 && d <= maxd) ? st.node_diff[d] : 0;
+    // short tables: scb[d] = sum_{1<=i<d} end_count[i] (exclusive)
+    const int64_t ec = (d >= 1 && d <= maxd) ? st.end_count[d] : 0;
+    const int64_t in = block_incl_scan64(nd, wsum) + c_nodes;
+    const int64_t ic = block_incl_scan64(ec, wsum) + c_scb;
+    const int64_t it = block_incl_scan64(ec * d, wsum) + c_stb;
+    if (d < n) {
+      nodes[d] = (d >= 1 && d <= maxd) ? in : 0;
+      scb[d] = ic - ec;
+      stb[d] = it - ec * d;
+    }
+    __shared__ int64_t carry[3];
+    if (threadIdx.x == kTabT - 1) {
+      carry[0] = in;
+      carry[1] = ic;
+      carry[2] = it;
+    }
+    __syncthreads();
+    c_nodes = carry[0];
+    c_scb = carry[1];
+    c_stb = carry[2];
+    __syncthreads();
   }
-  nodes[maxd + 1] = 0;
-  scb[0] = 0;
-  stb[0] = 0;
-  for (int d = 1; d <= maxd + 1; ++d) {
-    int64_t ec = d - 1 >= 1 ? st.end_count[d - 1] : 0;
-    scb[d] = scb[d - 1] + ec;
-    stb[d] = stb[d - 1] + ec * (d - 1);
-  }
-  lcf[maxd + 1] = 0;
-  ltf[maxd + 1] = 0;
-  for (int d = maxd; d >= 0; --d) {
-    int64_t lc = d + 1 <= maxd ? st.len_count[d + 1] : 0;
-    lcf[d] = lcf[d + 1] + lc;
-    ltf[d] = ltf[d + 1] + lc * (d + 1);
+  // longer tables: lcf[d] = sum_{d<i<=maxd} len_count[i] (suffix, exclusive)
+  int64_t c_lc = 0, c_lt = 0;
+  for (int e0 = 0; e0 < n; e0 += kTabT) {
+    const int d = maxd + 1 - (e0 + (int)threadIdx.x);  // descending d
+    const int i = d + 1;
+    const int64_t lc = (d >= 0 && i <= maxd) ? st.len_count[i] : 0;
+    const int64_t ilc = block_incl_scan64(lc, wsum) + c_lc;
+    const int64_t ilt = block_incl_scan64(lc * i, wsum) + c_lt;
+    if (d >= 0) {
+      lcf[d] = ilc;
+      ltf[d] = ilt;
+    }
+    __shared__ int64_t carry2[2];
+    if (threadIdx.x == kTabT - 1) {
+      carry2[0] = ilc;
+      carry2[1] = ilt;
+    }
+    __syncthreads();
+    c_lc = carry2[0];
+    c_lt = carry2[1];
+    __syncthreads();
   }
 }
 
@@ -321,15 +550,20 @@ uint32_t pow2_at_least(int64_t v) {
 static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off, int P,
                         int32_t cap_len, int strict, bool want_labels, int32_t max_len_hint,
                         DedupState* out_state, int64_t* h_stats, int32_t* h_labels) {
-  // Pass 1: lengths + stats (needs maxd to size the tables).
+  constexpr int kRoundsPerSync = 4;
+  constexpr int kMaxRounds = 1 << 20;
   const uint32_t cap = pow2_at_least(2 * (int64_t)P + 2);
   const size_t base_bytes = abytes(P, 4) + abytes(4, 8) + abytes(P, 4) * 4 +
                             abytes(cap, 4) * 4 + abytes(P, 4) + abytes(cap, 8) * 2 +
-                            abytes(cap, 4) * 2 + abytes(1, 4) + abytes(P, 4);
-  int64_t maxd = max_len_hint > 0 ? max_len_hint : 0;
+                            abytes(cap, 4) * 2 + abytes(kRoundsPerSync + 2, 4) + abytes(P, 4);
+  // Tables are sized by the longest prompt; guess generously so the usual
+  // case needs a single lengths pass and one host read.
+  int64_t maxd = std::max<int64_t>(max_len_hint, 16384);
   DedupState st{};
+  int64_t hs[4];
+  int64_t off01[2];
   for (int attempt = 0; attempt < 2; ++attempt) {
-    size_t need = base_bytes + abytes(maxd + 2, 8) * 3 + 5 * abytes(maxd + 2, 8) + (1 << 16);
+    size_t need = base_bytes + 8 * abytes(maxd + 2, 8) + (1 << 16);
     RS_TRY(arena_reserve(ctx, need));
     st.P = P;
     st.tok = d_tok;
@@ -341,16 +575,13 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
     RS_TRY(h2d(ctx, st.stats, init, sizeof(init)));
     int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, 8 * ctx->num_sms));
     RS_LAUNCH(ctx, "dedup_lengths", lengths_kernel, blocks, 256, 0, st, cap_len, strict, ctx->d_flags);
-    int64_t hs[4];
     RS_TRY(d2h(ctx, hs, st.stats, sizeof(hs)));
+    RS_TRY(d2h(ctx, off01, d_off, sizeof(off01)));
     RS_TRY(sync_and_check(ctx));
-    if (hs[1] <= maxd || attempt == 1) {
-      maxd = std::max<int64_t>(maxd, hs[1]);
-      break;
-    }
+    if (hs[1] <= maxd) break;
     maxd = hs[1];
   }
-  const int md = (int)maxd;
+  const int md = (int)hs[1];
   st.node_diff = arena_alloc<int64_t>(ctx, md + 2);
   st.end_count = arena_alloc<int64_t>(ctx, md + 2);
   st.len_count = arena_alloc<int64_t>(ctx, md + 2);
@@ -365,36 +596,55 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
   st.b_keys = arena_alloc<uint64_t>(ctx, cap);
   st.b_rep = arena_alloc<int32_t>(ctx, cap);
   st.b_cnt = arena_alloc<int32_t>(ctx, cap);
-  st.counter = arena_alloc<int32_t>(ctx, 1);
+  int* kc = arena_alloc<int32_t>(ctx, kRoundsPerSync + 2);  // member counts per round
+  st.counter = kc;
   st.labels = want_labels ? arena_alloc<int32_t>(ctx, std::max(P, 1)) : nullptr;
-  if (!st.counter || (want_labels && !st.labels)) return fail(RS_E_NOMEM, "arena exhausted (dedup)");
+  if (!kc || (want_labels && !st.labels)) return fail(RS_E_NOMEM, "arena exhausted (dedup)");
   RS_CUDA_TRY(cudaMemsetAsync(st.node_diff, 0, 8 * (md + 2), ctx->stream));
   RS_CUDA_TRY(cudaMemsetAsync(st.end_count, 0, 8 * (md + 2), ctx->stream));
   RS_CUDA_TRY(cudaMemsetAsync(st.len_count, 0, 8 * (md + 2), ctx->stream));
   int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, 8 * ctx->num_sms));
   RS_LAUNCH(ctx, "dedup_len_hist", len_hist_kernel, blocks, 256, 0, st);
   RS_LAUNCH(ctx, "dedup_init", init_root_kernel, blocks, 256, 0, st);
-  int K = P - 1;
+  // Rounds run back to back on the device, each reading its member count
+  // from HBM; the host checks for completion once per kRoundsPerSync.
+  int k0 = P - 1;
+  RS_TRY(h2d(ctx, kc, &k0, 4));
+  const int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)P + 7) / 8, 64 * ctx->num_sms));
+  const int cblocks = (int)std::max<int64_t>(1, std::min<int64_t>((cap + 255) / 256, 8 * ctx->num_sms));
+  const int pblocks = (int)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, 8 * ctx->num_sms));
+  // round-0 streaming kernel: representative + per-warp rings in smem
+  const int len0 = (int)std::min<int64_t>(off01[1] - off01[0], cap_len);
+  const int stream_smem = (int)(sizeof(int32_t) * (((len0 + 3) & ~3) + kStageTok * kStreamStages * kStreamWarps));
+  int sblocks = 1;
+  if (stream_smem <= 200 * 1024) {
+    RS_CUDA_TRY(cudaFuncSetAttribute(compare_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, stream_smem));
+    int per_sm = 1;
+    RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compare_stream_kernel, kStreamWarps * 32, stream_smem));
+    sblocks = std::max(1, per_sm) * ctx->num_sms;
+  }
   int cur = 0;
-  while (K > 0) {
-    uint32_t c = pow2_at_least(2 * (int64_t)K + 2);
-    RS_CUDA_TRY(cudaMemsetAsync(st.a_keys, 0xff, 8ull * c, ctx->stream));
-    RS_CUDA_TRY(cudaMemsetAsync(st.b_keys, 0xff, 8ull * c, ctx->stream));
-    RS_CUDA_TRY(cudaMemsetAsync(st.b_rep, 0x7f, 4ull * c, ctx->stream));
-    RS_CUDA_TRY(cudaMemsetAsync(st.b_cnt, 0, 4ull * c, ctx->stream));
-    RS_CUDA_TRY(cudaMemsetAsync(st.counter, 0, 4, ctx->stream));
-    int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)K + 7) / 8, 64 * ctx->num_sms));
-    RS_LAUNCH(ctx, K == P - 1 ? "dedup_compare_r0" : "dedup_compare", compare_kernel, wblocks,
-              256, 0, st, cur, K, c - 1);
-    int fb = (int)std::max<int64_t>(1, std::min<int64_t>((c + 255) / 256, 8 * ctx->num_sms));
-    RS_LAUNCH(ctx, "dedup_finalize", finalize_kernel, fb, 256, 0, st, cur, c);
-    int kb = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)K + 255) / 256, 8 * ctx->num_sms));
-    RS_LAUNCH(ctx, "dedup_compact", compact_kernel, kb, 256, 0, st, cur, K);
-    int nk = 0;
-    RS_TRY(d2h(ctx, &nk, st.counter, 4));
+  for (int round = 0; round < kMaxRounds; round += kRoundsPerSync) {
+    for (int r = 0; r < kRoundsPerSync; ++r) {
+      const int* kcur = kc + r;
+      int* knext = kc + r + 1;
+      RS_LAUNCH(ctx, "dedup_prep", round_prep_kernel, cblocks, 256, 0, st, kcur, knext);
+      if (round + r == 0 && stream_smem <= 200 * 1024) {
+        RS_LAUNCH(ctx, "dedup_compare_r0", compare_stream_kernel, sblocks, kStreamWarps * 32,
+                  stream_smem, st, kcur);
+      } else {
+        RS_LAUNCH(ctx, round + r == 0 ? "dedup_compare_r0" : "dedup_compare", compare_kernel,
+                  wblocks, 256, 0, st, cur, kcur);
+      }
+      RS_LAUNCH(ctx, "dedup_finalize", finalize_kernel, cblocks, 256, 0, st, cur, kcur);
+      RS_LAUNCH(ctx, "dedup_compact", compact_kernel, pblocks, 256, 0, st, cur, kcur, knext);
+      cur ^= 1;
+    }
+    int left = 0;
+    RS_TRY(d2h(ctx, &left, kc + kRoundsPerSync, 4));
     RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    K = nk;
-    cur ^= 1;
+    if (left <= 0) break;
+    RS_CUDA_TRY(cudaMemcpyAsync(kc, kc + kRoundsPerSync, 4, cudaMemcpyDeviceToDevice, ctx->stream));
   }
   if (h_stats) RS_TRY(d2h(ctx, h_stats, st.stats, 4 * 8));
   if (h_labels && P > 0) RS_TRY(d2h(ctx, h_labels, st.labels, 4ull * P));
@@ -421,7 +671,7 @@ static int build_index_device(rs_ctx* ctx, const int32_t* d_tok, const int64_t* 
   const int md = (int)stats[1];
   int64_t* d_tables = arena_alloc<int64_t>(ctx, 5ull * (md + 2));
   if (!d_tables) return fail(RS_E_NOMEM, "arena exhausted (tables)");
-  RS_LAUNCH(ctx, "dedup_tables", tables_kernel, 1, 32, 0, st, md, d_tables);
+  RS_LAUNCH(ctx, "dedup_tables", tables_kernel, 1, kTabT, 0, st, md, d_tables);
   std::vector<int64_t> h(5ull * (md + 2));
   RS_TRY(d2h(ctx, h.data(), d_tables, 8 * h.size()));
   RS_TRY(sync_and_check(ctx));
@@ -549,7 +799,7 @@ int rs_prefix_index_build_device_async(rs_ctx* ctx, const int32_t* d_tokens,
   RS_TRY(dedup_refine(ctx, d_tokens, d_offsets, batch, INT32_MAX, 1, false, max_len_cap, &st,
                       stats, nullptr));
   if (stats[1] > max_len_cap) return fail(RS_E_ARG, "max_len_cap below the longest prompt");
-  RS_LAUNCH(ctx, "dedup_tables", tables_kernel, 1, 32, 0, st, max_len_cap, d_tables);
+  RS_LAUNCH(ctx, "dedup_tables", tables_kernel, 1, kTabT, 0, st, max_len_cap, d_tables);
   int64_t info[5] = {batch, stats[0], stats[1], stats[2], 0};
   RS_TRY(h2d(ctx, d_info, info, sizeof(info)));
   return RS_OK;
