@@ -32,7 +32,8 @@ namespace rs {
 size_t fast_ss_bytes(int64_t items, int S) {
   int64_t segs = items + S;
   return abytes(segs, 8) * 2 + abytes(S, 4) + abytes(items, 8) + abytes(items, 4) * 2 +
-         abytes(items, 16);
+         abytes(items, 16) + abytes(segs, 4) + abytes(segs, 1) + abytes((int64_t)S * kStStride, 2) +
+         abytes(segs, 8);
 }
 
 FastSS fast_ss_alloc(rs_ctx* ctx, const int64_t* d_off, int64_t items, int S) {
@@ -46,6 +47,10 @@ FastSS fast_ss_alloc(rs_ctx* ctx, const int64_t* d_off, int64_t items, int S) {
   f.plen_r = arena_alloc<int32_t>(ctx, items);
   f.order_r = arena_alloc<int32_t>(ctx, items);
   f.rec = arena_alloc<int4>(ctx, items);
+  f.pmsm = arena_alloc<uint32_t>(ctx, segs);
+  f.pgo = arena_alloc<uint8_t>(ctx, segs);
+  f.st = arena_alloc<uint16_t>(ctx, (int64_t)S * kStStride);
+  f.sts = arena_alloc<uint2>(ctx, segs);
   return f;
 }
 
@@ -266,6 +271,71 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
       mx = 0;
     }
     if (lane == 0) ss.seg[so + k] = make_int2(sk.x | (mx << 16), hi);
+  }
+  // Range-max helpers: per 16-segment block the in-block prefix / suffix
+  // maxima and previous-greater distances, then a sparse table over block
+  // maxima (levels double the span).
+  __syncthreads();
+  const int nblk = (D + kBlk - 1) / kBlk;
+  uint16_t* st = ss.st + (int64_t)s * kStStride;
+  for (int jb = tid; jb < nblk; jb += kBuildT) {
+    const int k0 = jb * kBlk, k1 = min(D, k0 + kBlk);
+    int v[kBlk], pg[kBlk];
+    int m = 0;
+#pragma unroll
+    for (int i = 0; i < kBlk; ++i) {
+      v[i] = k0 + i < k1 ? (ss.seg[so + k0 + i].x >> 16) & 0xffff : 0;
+      m = max(m, v[i]);
+    }
+    st[jb] = (uint16_t)m;
+    int pm = 0;
+#pragma unroll
+    for (int i = 0; i < kBlk; ++i) {
+      pm = max(pm, v[i]);
+      int j = i - 1;
+      while (j >= 0 && v[j] <= v[i]) j = pg[j];
+      pg[i] = j;
+      if (k0 + i < k1) {
+        ss.pmsm[so + k0 + i] = (uint32_t)pm;
+        ss.pgo[so + k0 + i] = (uint8_t)(j >= 0 ? i - j : 0);
+      }
+    }
+    int sm = 0;
+#pragma unroll
+    for (int i = kBlk - 1; i >= 0; --i) {
+      sm = max(sm, v[i]);
+      if (k0 + i < k1) ss.pmsm[so + k0 + i] |= (uint32_t)sm << 16;
+    }
+    // within-block sparse table: lv[L][i] = max v[i .. min(i + 2^L, 16))
+    int lv[kBlk];
+#pragma unroll
+    for (int i = 0; i < kBlk; ++i) lv[i] = v[i];
+    uint32_t packed[kBlk][2];
+#pragma unroll
+    for (int L = 1; L <= 4; ++L) {
+#pragma unroll
+      for (int i = 0; i < kBlk; ++i) {
+        const int h = 1 << (L - 1);
+        lv[i] = i + h < kBlk ? max(lv[i], lv[i + h]) : lv[i];
+      }
+#pragma unroll
+      for (int i = 0; i < kBlk; ++i) {
+        if (L == 1) packed[i][0] = (uint32_t)lv[i];
+        if (L == 2) packed[i][0] |= (uint32_t)lv[i] << 16;
+        if (L == 3) packed[i][1] = (uint32_t)lv[i];
+        if (L == 4) packed[i][1] |= (uint32_t)lv[i] << 16;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kBlk; ++i)
+      if (k0 + i < k1) ss.sts[so + k0 + i] = make_uint2(packed[i][0], packed[i][1]);
+  }
+  __syncthreads();
+  for (int lev = 1; (1 << lev) <= nblk; ++lev) {
+    for (int jb = tid; jb + (1 << lev) <= nblk; jb += kBuildT)
+      st[lev * kStBlocks + jb] =
+          max(st[(lev - 1) * kStBlocks + jb], st[(lev - 1) * kStBlocks + jb + (1 << (lev - 1))]);
+    __syncthreads();
   }
 }
 
@@ -758,6 +828,279 @@ int fast_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, Cand
   const int smem = (int)sizeof(EvalShared);
   RS_CUDA_TRY(cudaFuncSetAttribute(fast_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   RS_LAUNCH(ctx, "group_eval", fast_eval_kernel, grid, kEvalT, smem, A);
+  return RS_OK;
+}
+
+// ------------------------------------------------------ lockstep evaluator --
+// Lanes are candidates N. Every lane walks the scenario's run-segments
+// k = D-1 .. 0 (ascending finish) in lockstep with its warp: at step k, lane
+// N evaluates the run of segment k in its current group g (groups of N are
+// visited g = N-1 .. 0) and adds it to the group's FP64 total, so each
+// group's sum is sequential in the reference order. Segment data, block
+// tables and the profile row are the same for every lane at a step (uniform
+// loads); only the group bounds differ. The base (max prompt_len of the
+// group's live prefix) comes from O(1) range-max queries: the group's first
+// block via previous-greater chains, full blocks via the block sparse table,
+// the current block via its in-block prefix max.
+constexpr int kLsThreads = 256;
+
+struct LsArgs {
+  FastSS ss;
+  FastProf fp;
+  CandRange cr;
+  int S;
+  int cand_units;  // units per scenario (candidate slices of kLsThreads)
+  double* gt;
+  const int4* gtab;  // per (scenario, flat group): see group_table_kernel
+};
+
+struct LsView {
+  const int2* seg;
+  const uint32_t* pmsm;
+  const uint8_t* pgo;
+  const uint16_t* st;
+  const uint2* sts;
+};
+
+// max MX over [l, r] inside one 16-segment block (O(1): two lookups in the
+// within-block sparse table).
+__device__ __forceinline__ int ls_inblock(const LsView& V, int l, int r) {
+  const int len = r - l + 1;
+  const int lev = 31 - __clz(len);
+  auto at = [&](int k) -> int {
+    if (lev == 0) return (__ldg(&V.seg[k].x) >> 16) & 0xffff;
+    const uint2 w = __ldg(V.sts + k);
+    const uint32_t word = lev <= 2 ? w.x : w.y;
+    return (int)((lev & 1 ? word : word >> 16) & 0xffff);
+  };
+  return max(at(l), at(r - (1 << lev) + 1));
+}
+
+__device__ __forceinline__ int ls_mx(const LsView& V, int k) { return (__ldg(&V.seg[k].x) >> 16) & 0xffff; }
+
+// max MX over [l, r] (l <= r) inside one 16-segment block: walk the
+// previous-greater chain from r while it stays at or right of l.
+__device__ __forceinline__ int ls_chain(const LsView& V, int l, int r) {
+  int j = r, m = ls_mx(V, r);
+  for (;;) {
+    const int d = __ldg(V.pgo + j);
+    if (d == 0 || j - d < l) return m;
+    j -= d;
+    m = ls_mx(V, j);
+  }
+}
+
+__device__ __forceinline__ int ls_blocks(const LsView& V, int jl, int jr) {  // jl <= jr
+  const int len = jr - jl + 1;
+  const int lev = 31 - __clz(len);
+  return max((int)__ldg(V.st + lev * kStBlocks + jl),
+             (int)__ldg(V.st + lev * kStBlocks + jr - (1 << lev) + 1));
+}
+
+// max MX over [l, r], l <= r.
+__device__ __forceinline__ int ls_range(const LsView& V, int l, int r) {
+  const int jl = l >> 4, jr = r >> 4;
+  if (jl == jr) return ls_inblock(V, l, r);
+  int m = max((int)(__ldg(V.pmsm + l) >> 16), (int)(__ldg(V.pmsm + r) & 0xffff));
+  if (jl + 1 <= jr - 1) m = max(m, ls_blocks(V, jl + 1, jr - 1));
+  return m;
+}
+
+// Per group (scenario, N, g): {ka, kb, va | vb << 16, top_m | smb << 16}.
+__global__ void group_table_kernel(FastSS ss, CandRange cr, int S, int4* gtab) {
+  const int64_t total = (int64_t)S * cr.T;
+  const int64_t flat0 = tri64(cr.n_min);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(t / cr.T);
+    const int64_t fl = t - (int64_t)s * cr.T;
+    int N, g;
+    flat_ng(fl, cr.n_min, &N, &g);
+    const int64_t i0 = ss.item_off[s], so = i0 + s;
+    const int P = (int)(ss.item_off[s + 1] - i0);
+    const int q = P / N, rem = P % N;
+    const int a = g * q + min(g, rem), b = a + q + (g < rem ? 1 : 0);
+    if (b <= a) {
+      gtab[t] = make_int4(0, -1, 0, 0);
+      continue;
+    }
+    LsView V{ss.seg + so, ss.pmsm + so, ss.pgo + so, ss.st + (int64_t)s * kStStride, ss.sts + so};
+    const int2 ra = ss.rinfo[i0 + a], rb = ss.rinfo[i0 + b - 1];
+    const int ka = ra.x, kb = rb.x;
+    const int va = ra.y & 0xffff, vb = (rb.y >> 16) & 0xffff;
+    int top_m, smb = 0;
+    if (ka == kb) {
+      top_m = INT32_MIN;
+      for (int r = a; r < b; ++r) top_m = max(top_m, ss.plen_r[i0 + r]);
+    } else {
+      top_m = max(va, vb);
+      if (ka + 1 <= kb - 1) top_m = max(top_m, ls_range(V, ka + 1, kb - 1));
+      smb = (int)(__ldg(V.pmsm + ka + 1) >> 16);
+    }
+    (void)flat0;
+    gtab[t] = make_int4(ka, kb, va | (vb << 16), top_m | (smb << 16));
+  }
+}
+
+__global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
+  extern __shared__ __align__(16) unsigned char ls_smem[];
+  double* s_top = reinterpret_cast<double*>(ls_smem);
+  int32_t* s_pex = reinterpret_cast<int32_t*>(s_top + kTopCap);
+  const FastProf& fp0 = A.fp;
+  for (int i = threadIdx.x; i < fp0.ncm; i += kLsThreads) s_top[i] = fp0.top[i];
+  for (int i = threadIdx.x; i <= fp0.ncm; i += kLsThreads) s_pex[i] = fp0.pex[i];
+  __syncthreads();
+  const int clo = fp0.c_lo, chi = fp0.c_hi, clo1 = fp0.c_lo - 1, ncm = fp0.ncm;
+  const int live_top = fp0.live_top;
+  const double* rows = fp0.rows;
+  const int C = A.cr.n_max - A.cr.n_min + 1;
+  const int64_t G = A.cr.G;
+  const int64_t flat0 = tri64(A.cr.n_min);
+  for (int unit = blockIdx.x; unit < A.S * A.cand_units; unit += gridDim.x) {
+    const int s = unit / A.cand_units;
+    const int c = (unit % A.cand_units) * kLsThreads + threadIdx.x;
+    const bool on = c < C;
+    const int N = A.cr.n_min + (on ? c : 0);
+    const int64_t i0 = A.ss.item_off[s];
+    const int P = (int)(A.ss.item_off[s + 1] - i0);
+    const int64_t so = i0 + s;
+    const int D = A.ss.nseg[s];
+    LsView V{A.ss.seg + so, A.ss.pmsm + so, A.ss.pgo + so, A.ss.st + (int64_t)s * kStStride,
+             A.ss.sts + so};
+    double* gt = A.gt + (int64_t)s * A.cr.T + (tri64(N) - flat0);
+    const int4* gtab = A.gtab + (int64_t)s * A.cr.T + (tri64(N) - flat0);
+    const int q = P / N, rem = P % N;
+    // current group state; the next group's table entry is prefetched
+    int g = N, a = 0, b = 0, ka = 0, kb = -1, va = 0, vb = 0, l = 0, jl = 0;
+    int smb = 0, top_m = 0, cjr = -1, cbase = 0;
+    double total = 0.0;
+    bool need_setup = on;  // enter the next group (g - 1) when the current one is done
+    bool done = !on;
+    int fnext = 0;         // finish tick of segment k + 1 (uniform)
+    int4 nxt = on ? __ldg(gtab + N - 1) : make_int4(0, -1, 0, 0);
+    for (int k = D - 1; k >= 0; --k) {
+      const int2 sk = __ldg(&V.seg[k]);
+      const int f = sk.x & 0xffff;
+      const int E = sk.y;
+      const int jr = k >> 4;
+      while (!done) {
+        if (need_setup) {  // group g-1 from the prefetched table entry
+          --g;
+          a = g * q + min(g, rem);
+          b = a + q + (g < rem ? 1 : 0);
+          ka = nxt.x;
+          kb = nxt.y;
+          va = nxt.z & 0xffff;
+          vb = (nxt.z >> 16) & 0xffff;
+          top_m = nxt.w & 0xffff;
+          smb = (nxt.w >> 16) & 0xffff;
+          l = ka + 1;
+          jl = l >> 4;
+          cjr = -1;
+          total = 0.0;
+          need_setup = false;
+          if (g > 0) nxt = __ldg(gtab + g - 1);
+          if (b <= a) {  // empty group (cannot happen for N <= P)
+            gt[g] = 0.0;
+            if (g == 0) done = true;
+            need_setup = !done;
+            continue;
+          }
+        }
+        if (kb < k) break;  // this lane's next group starts at a lower segment
+        int base, x, ts;
+        if (k == kb) {
+          base = top_m;
+          x = b;
+          ts = 1;
+        } else if (k == ka) {
+          base = va;
+          x = E;
+          ts = fnext + 1;
+        } else {
+          x = E;
+          ts = fnext + 1;
+          if (jr == jl) {
+            base = max(va, ls_inblock(V, l, k));
+          } else {
+            if (jr != cjr) {
+              cjr = jr;
+              cbase = max(va, smb);
+              if (jl + 1 <= jr - 1) cbase = max(cbase, ls_blocks(V, jl + 1, jr - 1));
+            }
+            base = max(cbase, (int)(__ldg(V.pmsm + k) & 0xffff));
+          }
+        }
+        // tpot_context_run_sum (planner.cpp:61-84): one code path; the row is
+        // the clamped-batch row in shared memory or a small-batch row.
+        const int live = x - a;
+        const int c1 = base + f - 1;
+        const double* row = live >= live_top ? s_top : rows + (size_t)(live - 1) * ncm;
+        double rs = 0.0;
+        for (int cc = base + ts - 1; cc <= c1;) {
+          const int pe = min(c1, s_pex[min(max(cc, clo1), chi) - clo1]);
+          const double t0 = row[min(max(cc, clo), chi) - clo];
+          const double t1 = row[min(max(pe, clo), chi) - clo];
+          rs = dadd(rs, dmul(dmul((double)(pe - cc + 1), dadd(t0, t1)), 0.5));
+          cc = pe + 1;
+        }
+        total = dadd(total, rs);
+        if (k != ka) break;
+        gt[g] = total;  // group complete
+        if (g == 0) {
+          done = true;
+        } else {
+          need_setup = true;  // the next group may start inside this segment
+        }
+      }
+      fnext = f;
+    }
+  }
+}
+
+int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, CandRange cr,
+                  double* gt) {
+  if (!fast_profile_ok(prof, cr.G)) return fail(RS_E_CONFIG, "profile not eligible for the fast path");
+  const int64_t ncm = prof.c_hi - prof.c_lo + 1;
+  if (ncm > kTopCap) return fail(RS_E_CONFIG, "context memo too large for the lockstep evaluator");
+  const int live_top = (int)std::max<int64_t>(1, (prof.b_hi + cr.G - 1) / cr.G);
+  double* rows = arena_alloc<double>(ctx, std::max<int64_t>(1, (int64_t)(live_top - 1) * ncm));
+  int32_t* pex = arena_alloc<int32_t>(ctx, ncm + 1);
+  if (!rows || !pex) return fail(RS_E_NOMEM, "arena exhausted (lockstep)");
+  double front, back;
+  RS_CUDA_TRY(cudaMemcpyAsync(&front, prof.ck, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RS_CUDA_TRY(cudaMemcpyAsync(&back, prof.ck + prof.nc - 1, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  FastProf fp;
+  fp.top = prof.top_row;
+  fp.rows = rows;
+  fp.pex = pex;
+  fp.c_lo = (int)prof.c_lo;
+  fp.c_hi = (int)prof.c_hi;
+  fp.cf_ceil = (int)std::ceil(front);
+  fp.cb_ceil = (int)std::ceil(back);
+  fp.cfront_m1 = (int)prof.cfront_m1;
+  fp.ncm = (int)ncm;
+  fp.live_top = live_top;
+  const int64_t tot = (int64_t)live_top * ncm + 1;
+  RS_LAUNCH(ctx, "fast_tables", fast_tables_kernel, (int)std::min<int64_t>((tot + 255) / 256, 4096),
+            256, 0, prof, cr.G, live_top, rows, pex, fp.cf_ceil, fp.cb_ceil);
+  const int C = cr.n_max - cr.n_min + 1;
+  int4* gtab = arena_alloc<int4>(ctx, (size_t)S * cr.T);
+  if (!gtab) return fail(RS_E_NOMEM, "arena exhausted (group table)");
+  {
+    const int64_t n = (int64_t)S * cr.T;
+    RS_LAUNCH(ctx, "group_table", group_table_kernel,
+              (int)std::min<int64_t>((n + 255) / 256, 16 * ctx->num_sms), 256, 0, ss, cr, S, gtab);
+  }
+  LsArgs A{ss, fp, cr, S, (C + kLsThreads - 1) / kLsThreads, gt, gtab};
+  const int smem = (int)(sizeof(double) * kTopCap + sizeof(int32_t) * (kTopCap + 1));
+  RS_CUDA_TRY(cudaFuncSetAttribute(lockstep_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 1;
+  RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lockstep_eval_kernel, kLsThreads, smem));
+  const int units = S * A.cand_units;
+  const int grid = std::max(1, std::min(units, std::max(1, per_sm) * ctx->num_sms));
+  RS_LAUNCH(ctx, "group_eval", lockstep_eval_kernel, grid, kLsThreads, smem, A);
   return RS_OK;
 }
 

@@ -21,6 +21,11 @@ struct FastSS {
   int32_t* plen_r;
   int32_t* order_r;
   int4* rec;  // scratch: scattered {pred lo, pred hi, idx, plen}
+  // Range-max helpers over the per-segment max prompt_len (16-segment blocks):
+  uint32_t* pmsm;  // per segment slot: in-block prefix max | in-block suffix max << 16
+  uint8_t* pgo;    // per segment slot: distance to the previous greater MX in its block (0 = none)
+  uint16_t* st;    // per scenario: sparse table over block maxima, [kStLevels][kStBlocks]
+  uint2* sts;      // per segment slot: in-block max over [k, k + 2^L) for L = 1..4 (u16 x 4)
 };
 
 constexpr int kFastFmax = 16384;   // finish ticks of the fast path
@@ -29,6 +34,9 @@ constexpr int kBlk = 16;           // segment block of the lane evaluator
 constexpr int kMaxSeg = kFastFmax; // D <= Fmax
 constexpr int kTopCap = 4096;      // smem tpot row entries
 constexpr int kCoopN = 4;          // N < kCoopN: warp-cooperative groups
+constexpr int kStBlocks = kMaxSeg / kBlk;  // 1024
+constexpr int kStLevels = 11;              // floor(log2(1024)) + 1
+constexpr int kStStride = kStBlocks * kStLevels;
 
 size_t fast_ss_bytes(int64_t items, int S);
 FastSS fast_ss_alloc(rs_ctx* ctx, const int64_t* d_off, int64_t items, int S);
@@ -87,6 +95,11 @@ int fast_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, Cand
 // The fast evaluator needs exact memo tables small enough for its row cache.
 bool fast_profile_ok(const DevProfile& prof, int G);
 size_t fast_eval_bytes(const DevProfile& prof, int G);
+
+// Candidate-lockstep evaluator (large S): lanes are candidates walking
+// the scenario's segments k = D-1 .. 0 together.
+int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, CandRange cr,
+                  double* gt);
 
 // Per (scenario, candidate): t_total, cost, idle slot-ticks.
 int fast_reduce(rs_ctx* ctx, int S, const FastSS& ss, CandRange cr, double rho, int gpus,

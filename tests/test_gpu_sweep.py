@@ -115,3 +115,12 @@ def test_sweep_select_matches_oracle():
     check(ctx.lib.rs_sweep_select(ptr(st, C.c_double), ptr(sc, C.c_double), 1000, 64, 1, 0.7,
                                   C.byref(ns)))
     assert ns.value == port().sweep_select(st, sc, 1000, 1, 0.7)
+
+
+def test_sweep_many_scenarios_lockstep_bitwise():
+    """S >= #SMs takes the candidate-lockstep evaluator."""
+    check_sweep(c4_spec(160, count=2048, first=77), 1, 96)
+
+
+def test_sweep_many_scenarios_other_profile_lockstep():
+    check_sweep(c4_spec(150, count=1500, first=5), 2, 70, prof=profiles()["small"], g=3, lam=0.4)
