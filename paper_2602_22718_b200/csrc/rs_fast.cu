@@ -851,7 +851,8 @@ struct LsArgs {
   int S;
   int cand_units;  // units per scenario (candidate slices of kLsThreads)
   double* gt;
-  const int4* gtab;  // per (scenario, flat group): see group_table_kernel
+  const int4* gtab;      // per (scenario, flat group): see group_table_kernel
+  const double* gfirst;  // per (scenario, flat group): value after the first run
 };
 
 struct LsView {
@@ -906,10 +907,14 @@ __device__ __forceinline__ int ls_range(const LsView& V, int l, int r) {
   return m;
 }
 
-// Per group (scenario, N, g): {ka, kb, va | vb << 16, top_m | smb << 16}.
-__global__ void group_table_kernel(FastSS ss, CandRange cr, int S, int4* gtab) {
+// Per group (scenario, N, g): {ka, kb, va | vb << 16, smb} and the value of
+// its first run (k = kb: whole group live, base = max prompt_len of the
+// group, ticks 1 .. F_kb), i.e. the group's total after one run. The first
+// run spans the longest context range (often several knot pieces), so it is
+// evaluated here in parallel rather than inside the lockstep walk.
+__global__ void group_table_kernel(FastSS ss, DevProfile prof, CandRange cr, int S, int4* gtab,
+                                   double* gfirst) {
   const int64_t total = (int64_t)S * cr.T;
-  const int64_t flat0 = tri64(cr.n_min);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int s = (int)(t / cr.T);
@@ -920,10 +925,6 @@ __global__ void group_table_kernel(FastSS ss, CandRange cr, int S, int4* gtab) {
     const int P = (int)(ss.item_off[s + 1] - i0);
     const int q = P / N, rem = P % N;
     const int a = g * q + min(g, rem), b = a + q + (g < rem ? 1 : 0);
-    if (b <= a) {
-      gtab[t] = make_int4(0, -1, 0, 0);
-      continue;
-    }
     LsView V{ss.seg + so, ss.pmsm + so, ss.pgo + so, ss.st + (int64_t)s * kStStride, ss.sts + so};
     const int2 ra = ss.rinfo[i0 + a], rb = ss.rinfo[i0 + b - 1];
     const int ka = ra.x, kb = rb.x;
@@ -937,8 +938,9 @@ __global__ void group_table_kernel(FastSS ss, CandRange cr, int S, int4* gtab) {
       if (ka + 1 <= kb - 1) top_m = max(top_m, ls_range(V, ka + 1, kb - 1));
       smb = (int)(__ldg(V.pmsm + ka + 1) >> 16);
     }
-    (void)flat0;
-    gtab[t] = make_int4(ka, kb, va | (vb << 16), top_m | (smb << 16));
+    const int64_t f = ss.seg[so + kb].x & 0xffff;
+    gtab[t] = make_int4(ka, kb, va | (vb << 16), smb);
+    gfirst[t] = dadd(0.0, run_sum_int(prof, (int64_t)cr.G * (b - a), top_m, (int64_t)top_m + f - 1));
   }
 }
 
@@ -954,7 +956,6 @@ __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
   const int live_top = fp0.live_top;
   const double* rows = fp0.rows;
   const int C = A.cr.n_max - A.cr.n_min + 1;
-  const int64_t G = A.cr.G;
   const int64_t flat0 = tri64(A.cr.n_min);
   for (int unit = blockIdx.x; unit < A.S * A.cand_units; unit += gridDim.x) {
     const int s = unit / A.cand_units;
@@ -967,59 +968,45 @@ __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
     const int D = A.ss.nseg[s];
     LsView V{A.ss.seg + so, A.ss.pmsm + so, A.ss.pgo + so, A.ss.st + (int64_t)s * kStStride,
              A.ss.sts + so};
-    double* gt = A.gt + (int64_t)s * A.cr.T + (tri64(N) - flat0);
-    const int4* gtab = A.gtab + (int64_t)s * A.cr.T + (tri64(N) - flat0);
+    const int64_t gbase = (int64_t)s * A.cr.T + (tri64(N) - flat0);
+    double* gt = A.gt + gbase;
+    const int4* gtab = A.gtab + gbase;
+    const double* gfirst = A.gfirst + gbase;
     const int q = P / N, rem = P % N;
-    // current group state; the next group's table entry is prefetched
-    int g = N, a = 0, b = 0, ka = 0, kb = -1, va = 0, vb = 0, l = 0, jl = 0;
-    int smb = 0, top_m = 0, cjr = -1, cbase = 0;
+    // Current group (g, counting down from N-1). Its first run (k = kb) is
+    // preloaded into `total`; steps ka <= k < kb evaluate one run each.
+    int g = N - 1, a = 0, b = 0, ka = 0, kb = 0, va = 0, l = 0, jl = 0;
+    int smb = 0, cjr = -1, cbase = 0;
     double total = 0.0;
-    bool need_setup = on;  // enter the next group (g - 1) when the current one is done
     bool done = !on;
-    int fnext = 0;         // finish tick of segment k + 1 (uniform)
-    int4 nxt = on ? __ldg(gtab + N - 1) : make_int4(0, -1, 0, 0);
+    int4 nxt = make_int4(0, 0, 0, 0);
+    double nfirst = 0.0;
+    auto enter = [&](int4 e, double first) {  // start group g
+      a = g * q + min(g, rem);
+      b = a + q + (g < rem ? 1 : 0);
+      ka = e.x;
+      kb = e.y;
+      va = e.z & 0xffff;
+      smb = e.w;
+      l = ka + 1;
+      jl = l >> 4;
+      cjr = -1;
+      total = first;
+      if (g > 0) {  // prefetch the next group's entry
+        nxt = __ldg(gtab + g - 1);
+        nfirst = __ldg(gfirst + g - 1);
+      }
+    };
+    if (on) enter(__ldg(gtab + g), __ldg(gfirst + g));
+    int fnext = 0;  // finish tick of segment k + 1 (uniform)
     for (int k = D - 1; k >= 0; --k) {
       const int2 sk = __ldg(&V.seg[k]);
       const int f = sk.x & 0xffff;
-      const int E = sk.y;
       const int jr = k >> 4;
-      while (!done) {
-        if (need_setup) {  // group g-1 from the prefetched table entry
-          --g;
-          a = g * q + min(g, rem);
-          b = a + q + (g < rem ? 1 : 0);
-          ka = nxt.x;
-          kb = nxt.y;
-          va = nxt.z & 0xffff;
-          vb = (nxt.z >> 16) & 0xffff;
-          top_m = nxt.w & 0xffff;
-          smb = (nxt.w >> 16) & 0xffff;
-          l = ka + 1;
-          jl = l >> 4;
-          cjr = -1;
-          total = 0.0;
-          need_setup = false;
-          if (g > 0) nxt = __ldg(gtab + g - 1);
-          if (b <= a) {  // empty group (cannot happen for N <= P)
-            gt[g] = 0.0;
-            if (g == 0) done = true;
-            need_setup = !done;
-            continue;
-          }
-        }
-        if (kb < k) break;  // this lane's next group starts at a lower segment
-        int base, x, ts;
-        if (k == kb) {
-          base = top_m;
-          x = b;
-          ts = 1;
-        } else if (k == ka) {
-          base = va;
-          x = E;
-          ts = fnext + 1;
-        } else {
-          x = E;
-          ts = fnext + 1;
+      if (!done && k < kb) {
+        // run k of group g: live ranks [a, E_k), base = max(va, MX over (ka, k])
+        int base = va;
+        if (k != ka) {
           if (jr == jl) {
             base = max(va, ls_inblock(V, l, k));
           } else {
@@ -1033,11 +1020,11 @@ __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
         }
         // tpot_context_run_sum (planner.cpp:61-84): one code path; the row is
         // the clamped-batch row in shared memory or a small-batch row.
-        const int live = x - a;
+        const int live = sk.y - a;
         const int c1 = base + f - 1;
         const double* row = live >= live_top ? s_top : rows + (size_t)(live - 1) * ncm;
         double rs = 0.0;
-        for (int cc = base + ts - 1; cc <= c1;) {
+        for (int cc = base + fnext; cc <= c1;) {
           const int pe = min(c1, s_pex[min(max(cc, clo1), chi) - clo1]);
           const double t0 = row[min(max(cc, clo), chi) - clo];
           const double t1 = row[min(max(pe, clo), chi) - clo];
@@ -1045,12 +1032,15 @@ __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
           cc = pe + 1;
         }
         total = dadd(total, rs);
-        if (k != ka) break;
-        gt[g] = total;  // group complete
+      }
+      // groups completing at this segment (several when groups are small)
+      while (!done && k == ka) {
+        gt[g] = total;
         if (g == 0) {
           done = true;
         } else {
-          need_setup = true;  // the next group may start inside this segment
+          --g;
+          enter(nxt, nfirst);
         }
       }
       fnext = f;
@@ -1087,13 +1077,15 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
             256, 0, prof, cr.G, live_top, rows, pex, fp.cf_ceil, fp.cb_ceil);
   const int C = cr.n_max - cr.n_min + 1;
   int4* gtab = arena_alloc<int4>(ctx, (size_t)S * cr.T);
-  if (!gtab) return fail(RS_E_NOMEM, "arena exhausted (group table)");
+  double* gfirst = arena_alloc<double>(ctx, (size_t)S * cr.T);
+  if (!gtab || !gfirst) return fail(RS_E_NOMEM, "arena exhausted (group table)");
   {
     const int64_t n = (int64_t)S * cr.T;
     RS_LAUNCH(ctx, "group_table", group_table_kernel,
-              (int)std::min<int64_t>((n + 255) / 256, 16 * ctx->num_sms), 256, 0, ss, cr, S, gtab);
+              (int)std::min<int64_t>((n + 255) / 256, 16 * ctx->num_sms), 256, 0, ss, prof, cr, S,
+              gtab, gfirst);
   }
-  LsArgs A{ss, fp, cr, S, (C + kLsThreads - 1) / kLsThreads, gt, gtab};
+  LsArgs A{ss, fp, cr, S, (C + kLsThreads - 1) / kLsThreads, gt, gtab, gfirst};
   const int smem = (int)(sizeof(double) * kTopCap + sizeof(int32_t) * (kTopCap + 1));
   RS_CUDA_TRY(cudaFuncSetAttribute(lockstep_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 1;

@@ -677,7 +677,7 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
   const bool gen_fast = generated && allow_fast && fast_spec_ok(spec);
   const bool with_generic = !gen_fast;
   const size_t per_scen = abytes(P, 8) + abytes(P, 4) + built_bytes(P, 1, with_generic) +
-                          abytes(T, 8) + abytes(T, 16) + abytes(C, 8) * 3 + abytes(1, 4) + 2048;
+                          abytes(T, 8) * 2 + abytes(T, 16) + abytes(C, 8) * 3 + abytes(1, 4) + 2048;
   int B = (int)std::max<size_t>(1, std::min<size_t>((size_t)S, (size_t)(3ull << 30) / per_scen));
   if (B > 2048) B = 2048;
   size_t need = (size_t)B * per_scen + fast_eval_bytes(dp, G) + abytes(B + 1, 8) +

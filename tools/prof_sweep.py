@@ -28,7 +28,7 @@ for r in range(reps):
     ctx.reset_kernel_timing()
     check(ctx.lib.rs_sweep(ctx.handle, C.byref(spec), C.byref(ps), 8, 1, 256, 0.7, 2, C.byref(out), 0))
     print(f"rep {r} wall {1e3 * (time.perf_counter() - t0):.1f} ms")
-    for k in ("fast_build", "fast_tables", "group_eval", "candidate_reduce", "select", "aggregate"):
+    for k in ("gen_scenarios", "fast_build", "fast_tables", "group_table", "group_eval", "candidate_reduce", "select", "aggregate"):
         ms, n = ctx.kernel_time(k)
         print(f"rep {r} {k}: {ms:.3f} ms over {n} launches")
 print("n_star[:8]", bufs[3][:8])
