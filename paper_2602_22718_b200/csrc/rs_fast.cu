@@ -7,10 +7,10 @@
 // of rs_planner.cu); this file only changes how the work is laid out:
 //
 // build  (one CTA per scenario): counting sort by finish tick in shared
-//        memory, 16-byte records scattered into their bucket, each bucket
-//        ordered (pred desc, id asc) by one warp (bitonic in registers, or
-//        rank counting for wide buckets), then per-rank segment id and
-//        in-segment prefix / suffix prompt_len maxima, per-segment packed
+//        memory, 16-byte records scattered into their bucket, buckets
+//        ordered (pred desc, id asc) by rank counting inside shared-memory
+//        windows of whole buckets, then per-rank segment id and in-segment
+//        prefix / suffix prompt_len maxima, per-segment packed
 //        {finish | max_plen << 16, end_rank}.
 // eval   (persistent CTAs, one scenario's segment table staged in shared
 //        memory, 16-segment block maxima + sparse table for prefix-max
@@ -56,20 +56,27 @@ FastSS fast_ss_alloc(rs_ctx* ctx, const int64_t* d_off, int64_t items, int S) {
 
 // ------------------------------------------------------------------ build --
 constexpr int kBuildT = 1024;
-constexpr int kWide = 4096;
-
-__device__ __forceinline__ bool before(double pa, int ia, double pb, int ib) {
-  return pa > pb || (pa == pb && ia < ib);
-}
+constexpr int kWide = 4096;                 // records per sorting window (max bucket size)
+constexpr int kBuildCur = kFastFmax + 4;     // cur[] ints (16-byte aligned end)
+constexpr int kBuildSmem = kBuildCur * 4 + kWide * 20;
+static_assert(kWide * 20 >= (kFastFmax + 2) * 2, "window region must hold the bucket map");
 
 template <bool kGen>
 __global__ void __launch_bounds__(kBuildT)
 fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_io,
                   int32_t* plen_io, FastSS ss, int* flags) {
-  extern __shared__ int32_t cur[];  // [kFastFmax + 2]
+  // dynamic shared memory: cur (bucket cursors, then segment ends) and a
+  // second region holding the bucket -> segment map during the scatter and
+  // the sorting window afterwards
+  extern __shared__ __align__(16) int32_t cur[];  // [kFastFmax + 2]
+  uint16_t* skf = reinterpret_cast<uint16_t*>(cur + kBuildCur);
+  long long* w_key = reinterpret_cast<long long*>(cur + kBuildCur);
+  int32_t* w_id = reinterpret_cast<int32_t*>(w_key + kWide);
+  int32_t* w_pk = w_id + kWide;
+  int32_t* w_pl = w_pk + kWide;
   __shared__ int32_t wsum[32];
   __shared__ long long wsum64[32];
-  __shared__ int bad;
+  __shared__ int bad, s_k1;
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t i0 = ss.item_off[s];
@@ -154,6 +161,7 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
   for (int j = 0; j < kPer; ++j) {
     int f = kFastFmax - tid * kPer - j;
     cur[f] = start;
+    skf[f] = (uint16_t)kbase;
     if (cnt[j]) {
       ss.seg[so + kbase] = make_int2(f, start + cnt[j]);
       ss.segCF[so + kbase] = cfb;
@@ -163,114 +171,83 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
     cfb += (long long)cnt[j] * f;
   }
   __syncthreads();
-  // Scatter 16-byte records into the buckets.
+  // Scatter 16-byte records {pred bits, id, plen | segment << 16} into the
+  // buckets (bucket order: finish tick descending).
   for (int i = tid; i < P; i += kBuildT) {
     double p = pred[i];
     int f = (int)ceil(p);
     int pos = atomicAdd(&cur[f], 1);
     long long bits = __double_as_longlong(p);
-    ss.rec[i0 + pos] = make_int4((int)(bits & 0xffffffffLL), (int)(bits >> 32), i, plen[i]);
+    ss.rec[i0 + pos] = make_int4((int)(bits & 0xffffffffLL), (int)(bits >> 32), i,
+                                 plen[i] | ((int)skf[f] << 16));
   }
   __syncthreads();
+  // Order each bucket (pred desc, id asc) — planner.cpp:121-126 ranks by
+  // predicted length — one window of whole buckets (<= kWide records) at a
+  // time in shared memory: every record counts the records of its bucket
+  // that precede it (buckets are small: median 3, ~50 at the 99th
+  // percentile), then every sorted position takes its in-bucket prefix /
+  // suffix prompt_len maxima.
   const int D = ss.nseg[s];
-  for (int k = wid; k < D; k += kBuildT / 32) {
-    const int2 sk = ss.seg[so + k];
-    const int hi = sk.y;
-    const int lo = k == 0 ? 0 : ss.seg[so + k - 1].y;
-    const int m = hi - lo;
-    int mx;
-    if (m <= 32) {
-      int4 r = lane < m ? ss.rec[i0 + lo + lane] : make_int4(0, 0, INT32_MAX, 0);
-      double key = lane < m ? __longlong_as_double(((long long)r.y << 32) | (unsigned)r.x)
-                            : -INFINITY;
-      int idx = r.z, pl = r.w;
-#pragma unroll
-      for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-          double ok = __shfl_xor_sync(0xffffffffu, key, stride);
-          int oi = __shfl_xor_sync(0xffffffffu, idx, stride);
-          int op = __shfl_xor_sync(0xffffffffu, pl, stride);
-          bool up = (lane & size) == 0;
-          bool lower = (lane & stride) == 0;
-          bool of = before(ok, oi, key, idx);
-          bool take = lower == up ? of : (!of && oi != idx);
-          if (take) {
-            key = ok;
-            idx = oi;
-            pl = op;
-          }
+  int32_t* segend = cur;  // cur is dead after the scatter
+  for (int k = tid; k < D; k += kBuildT) segend[k] = ss.seg[so + k].y;
+  __syncthreads();
+  for (int k0 = 0, ws = 0; k0 < D;) {
+    if (tid == 0) {
+      int k1 = -1;
+      if (segend[k0] - ws <= kWide) {  // largest k1 with segend[k1 - 1] <= ws + kWide
+        int lo = k0 + 1, hi = D;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (segend[mid - 1] - ws <= kWide) lo = mid;
+          else hi = mid - 1;
         }
+        k1 = lo;
       }
-      // in-segment prefix / suffix maxima over lanes [0, m)
-      int v = lane < m ? pl : INT32_MIN;
-      int pm = v, sm = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int u = __shfl_up_sync(0xffffffffu, pm, o);
-        if (lane >= o) pm = max(pm, u);
-        int w = __shfl_down_sync(0xffffffffu, sm, o);
-        if (lane + o < 32) sm = max(sm, w);
-      }
-      if (lane < m) {
-        int64_t r0 = i0 + lo + lane;
-        ss.plen_r[r0] = pl;
-        ss.order_r[r0] = idx;
-        ss.rinfo[r0] = make_int2(k, sm | (pm << 16));
-      }
-      mx = __shfl_sync(0xffffffffu, pm, m - 1);
-    } else if (m <= kWide) {
-      for (int e = lane; e < m; e += 32) {
-        int4 r = ss.rec[i0 + lo + e];
-        double key = __longlong_as_double(((long long)r.y << 32) | (unsigned)r.x);
-        int rank = 0;
-        for (int o = 0; o < m; ++o) {
-          int4 q = ss.rec[i0 + lo + o];
-          double ok = __longlong_as_double(((long long)q.y << 32) | (unsigned)q.x);
-          rank += before(ok, q.z, key, r.z) ? 1 : 0;
-        }
-        ss.plen_r[i0 + lo + rank] = r.w;
-        ss.order_r[i0 + lo + rank] = r.z;
-      }
-      __syncwarp();
-      int carry = INT32_MIN;
-      for (int c0 = 0; c0 < m; c0 += 32) {  // prefix maxima
-        int e = c0 + lane;
-        int v = e < m ? ss.plen_r[i0 + lo + e] : INT32_MIN;
-        int pm = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int u = __shfl_up_sync(0xffffffffu, pm, o);
-          if (lane >= o) pm = max(pm, u);
-        }
-        pm = max(pm, carry);
-        if (e < m) ss.rinfo[i0 + lo + e] = make_int2(k, pm << 16);
-        carry = __shfl_sync(0xffffffffu, pm, 31);
-      }
-      mx = carry;
-      __syncwarp();
-      carry = INT32_MIN;
-      for (int c0 = ((m - 1) / 32) * 32; c0 >= 0; c0 -= 32) {  // suffix maxima
-        int e = c0 + lane;
-        int v = e < m ? ss.plen_r[i0 + lo + e] : INT32_MIN;
-        int sm = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int w = __shfl_down_sync(0xffffffffu, sm, o);
-          if (lane + o < 32) sm = max(sm, w);
-        }
-        sm = max(sm, carry);
-        if (e < m) {
-          int2 ri = ss.rinfo[i0 + lo + e];
-          ss.rinfo[i0 + lo + e] = make_int2(k, ri.y | sm);
-        }
-        carry = __shfl_sync(0xffffffffu, sm, 0);
-      }
-    } else {
-      if (lane == 0) atomicOr(flags, kFlagBucketTooWide);
-      mx = 0;
+      s_k1 = k1;
     }
-    if (lane == 0) ss.seg[so + k] = make_int2(sk.x | (mx << 16), hi);
+    __syncthreads();
+    const int k1 = s_k1;
+    if (k1 < 0) {
+      if (tid == 0) atomicOr(flags, kFlagBucketTooWide);
+      return;
+    }
+    const int n = segend[k1 - 1] - ws;
+    for (int i = tid; i < n; i += kBuildT) {
+      const int4 r = ss.rec[i0 + ws + i];
+      w_key[i] = ((long long)r.y << 32) | (unsigned)r.x;  // positive doubles order as integers
+      w_id[i] = r.z;
+      w_pk[i] = r.w;
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += kBuildT) {
+      const int k = w_pk[i] >> 16;
+      const int lo = (k == 0 ? 0 : segend[k - 1]) - ws, hi = segend[k] - ws;
+      const long long key = w_key[i];
+      const int id = w_id[i];
+      int rank = 0;
+      for (int j = lo; j < hi; ++j) {
+        const long long kj = w_key[j];
+        rank += (kj > key || (kj == key && w_id[j] < id)) ? 1 : 0;
+      }
+      const int pl = w_pk[i] & 0xffff;
+      w_pl[lo + rank] = pl;
+      ss.plen_r[i0 + ws + lo + rank] = pl;
+      ss.order_r[i0 + ws + lo + rank] = id;
+    }
+    __syncthreads();
+    for (int r = tid; r < n; r += kBuildT) {
+      const int k = w_pk[r] >> 16;  // sorting stays inside the bucket
+      const int lo = (k == 0 ? 0 : segend[k - 1]) - ws, hi = segend[k] - ws;
+      int pm = 0, sm = 0;
+      for (int j = lo; j <= r; ++j) pm = max(pm, w_pl[j]);
+      for (int j = r; j < hi; ++j) sm = max(sm, w_pl[j]);
+      ss.rinfo[i0 + ws + r] = make_int2(k, sm | (pm << 16));
+      if (r == hi - 1) ss.seg[so + k].x |= pm << 16;
+    }
+    __syncthreads();
+    k0 = k1;
+    ws += n;
   }
   // Range-max helpers: per 16-segment block the in-block prefix / suffix
   // maxima and previous-greater distances, then a sparse table over block
@@ -342,7 +319,7 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
 int fast_build(rs_ctx* ctx, int S, const int64_t* d_off, double* pred, int32_t* plen,
                FastSS ss, const GenSpec* gen, const double* nz, const double* lnz) {
   (void)d_off;
-  const int smem = sizeof(int32_t) * (kFastFmax + 2);
+  const int smem = kBuildSmem;
   RS_CUDA_TRY(cudaFuncSetAttribute(fast_build_kernel<true>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   RS_CUDA_TRY(cudaFuncSetAttribute(fast_build_kernel<false>,
@@ -372,7 +349,7 @@ struct EvalShared {
   uint32_t pmsm[kSegCap];  // in-block prefix max | in-block suffix max << 16
   uint16_t st[kLevels][kNBlk];
   double top[kTopCap];
-  int32_t pex[kTopCap + 1];  // piece end for c in [c_lo - 1, c_hi] (clamped index)
+  uint16_t pex[kTopCap + 2];  // piece ends, see FastProf
   double acc[kEvalW][32];
   int32_t carry[kEvalW][kCoopCarry];
   uint16_t lbuf[kEvalT][16];  // per-lane prefix maxima inside the first block
@@ -380,18 +357,36 @@ struct EvalShared {
   int lane_next;
 };
 
-// Device tpot rows of one (profile, G): rows[(live - 1) * ncm + (c - c_lo)]
-// = tpot(G * live, c) for live < live_top; live >= live_top uses `top`
-// (batch clamped to the last batch knot). Contexts and live counts are
-// 32-bit on this path (contexts <= 65535 + 16384).
 static_assert(sizeof(EvalShared) <= 232448, "EvalShared exceeds the sm_100 shared memory limit");
+
+// Device tpot tables of one (profile, G), stored HALVED:
+// rows[(live - 1) * ncm + (c - c_lo)] = tpot(G * live, c) / 2 for
+// live < live_top; live >= live_top uses `top` (batch clamped to the last
+// batch knot). Halving is exact and commutes with round-to-nearest, so the
+// reference's piece term count * (a + b) / 2 (planner.cpp:78) equals
+// count * (a/2 + b/2) bit for bit, one multiply shorter on the FP64 chain.
+// Piece ends: pex[j] for c = c_lo - 1 + j (j in [0, ncm]) is the last
+// context of c's piece as an offset from c_lo - 1, or kPexToEnd ("to the run
+// end", at or after the back knot). Contexts and live counts are 32-bit on
+// this path (contexts <= 65535 + 16384).
+constexpr uint16_t kPexToEnd = 0xffff;
 
 struct FastProf {
   const double* top;
   const double* rows;
-  const int32_t* pex;  // piece end for c in [c_lo - 1, c_hi]; INT32_MAX at/after back
+  const uint16_t* pex;
   int c_lo, c_hi, cf_ceil, cb_ceil, cfront_m1, ncm, live_top;
 };
+
+__device__ __forceinline__ int piece_end(const uint16_t* pex, int c, int c1, int clo1, int chi) {
+  const int p = pex[min(max(c, clo1), chi) - clo1];
+  return p == kPexToEnd ? c1 : min(c1, p + clo1);
+}
+
+// one piece term count * (t(c) + t(pe)) / 2 from halved tables
+__device__ __forceinline__ double piece_term(int count, double h0, double h1) {
+  return dmul((double)count, dadd(h0, h1));
+}
 
 // tpot_context_run_sum (proj/src/planner.cpp:61-84) for the live count
 // `live` (batch = G * live) over integer contexts [c0, c1].
@@ -399,10 +394,10 @@ __device__ __forceinline__ double run_sum32(const FastProf& fp, int live, int c0
   const double* row = live >= fp.live_top ? fp.top : fp.rows + (size_t)(live - 1) * fp.ncm;
   double total = 0.0;
   for (int c = c0; c <= c1;) {
-    const int pe = min(c1, fp.pex[min(max(c, fp.c_lo - 1), fp.c_hi) - (fp.c_lo - 1)]);
+    const int pe = piece_end(fp.pex, c, c1, fp.c_lo - 1, fp.c_hi);
     const double t0 = row[min(max(c, fp.c_lo), fp.c_hi) - fp.c_lo];
     const double t1 = row[min(max(pe, fp.c_lo), fp.c_hi) - fp.c_lo];
-    total = dadd(total, dmul(dmul((double)(pe - c + 1), dadd(t0, t1)), 0.5));
+    total = dadd(total, piece_term(pe - c + 1, t0, t1));
     c = pe + 1;
   }
   return total;
@@ -729,19 +724,19 @@ __global__ void __launch_bounds__(kEvalT, 1) fast_eval_kernel(EvalArgs A) {
           const int clo = fp.c_lo, chi = fp.c_hi, clo1 = fp.c_lo - 1;
           if (live >= live_top) {
             for (int c = base + ts - 1; c <= c1;) {
-              const int pe = min(c1, sh.pex[min(max(c, clo1), chi) - clo1]);
+              const int pe = piece_end(sh.pex, c, c1, clo1, chi);
               const double t0 = sh.top[min(max(c, clo), chi) - clo];
               const double t1 = sh.top[min(max(pe, clo), chi) - clo];
-              rs = dadd(rs, dmul(dmul((double)(pe - c + 1), dadd(t0, t1)), 0.5));
+              rs = dadd(rs, piece_term(pe - c + 1, t0, t1));
               c = pe + 1;
             }
           } else {
             const double* row = rows + (size_t)(live - 1) * fp.ncm;
             for (int c = base + ts - 1; c <= c1;) {
-              const int pe = min(c1, sh.pex[min(max(c, clo1), chi) - clo1]);
+              const int pe = piece_end(sh.pex, c, c1, clo1, chi);
               const double t0 = __ldg(row + min(max(c, clo), chi) - clo);
               const double t1 = __ldg(row + min(max(pe, clo), chi) - clo);
-              rs = dadd(rs, dmul(dmul((double)(pe - c + 1), dadd(t0, t1)), 0.5));
+              rs = dadd(rs, piece_term(pe - c + 1, t0, t1));
               c = pe + 1;
             }
           }
@@ -758,26 +753,29 @@ __global__ void __launch_bounds__(kEvalT, 1) fast_eval_kernel(EvalArgs A) {
 }
 
 // Small-batch tpot rows and piece ends of one (profile, G).
-__global__ void fast_tables_kernel(DevProfile p, int G, int live_top, double* rows,
-                                   int32_t* pex, int cf_ceil, int cb_ceil) {
+__global__ void fast_tables_kernel(DevProfile p, int G, int live_top, double* rows, double* top,
+                                   uint16_t* pex, int cf_ceil, int cb_ceil) {
   const int64_t ncm = p.c_hi - p.c_lo + 1;
-  const int64_t total = (int64_t)(live_top - 1) * ncm + ncm + 1;
+  const int64_t nrows = (int64_t)(live_top - 1) * ncm;
+  const int64_t total = nrows + ncm + ncm + 1;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    if (i < (int64_t)(live_top - 1) * ncm) {
+    if (i < nrows) {
       const int64_t live = i / ncm + 1, j = i % ncm;
-      rows[i] = tpot_int(p, (int64_t)G * live, p.c_lo + j);
+      rows[i] = dmul(tpot_int(p, (int64_t)G * live, p.c_lo + j), 0.5);
+    } else if (i < nrows + ncm) {
+      top[i - nrows] = dmul(p.top_row[i - nrows], 0.5);
     } else {
       // piece end for c = c_lo - 1 + j, j in [0, ncm] (run-sum pieces,
       // planner.cpp:65-74): below front -> ceil(front) - 1; at or above
       // back -> "to the run end"; else floor of the next knot.
-      const int64_t j = i - (int64_t)(live_top - 1) * ncm;
+      const int64_t j = i - nrows - ncm;
       const int64_t c = p.c_lo - 1 + j;
-      int32_t v;
-      if (c < cf_ceil) v = (int32_t)p.cfront_m1;
-      else if (c >= cb_ceil) v = INT32_MAX;
-      else v = (int32_t)p.kfloor[p.ci[c - p.c_lo] + 1];
-      pex[j] = v;
+      int64_t v;
+      if (c < cf_ceil) v = p.cfront_m1;
+      else if (c >= cb_ceil) v = -1;
+      else v = p.kfloor[p.ci[c - p.c_lo] + 1];
+      pex[j] = v < 0 ? kPexToEnd : (uint16_t)(v - (p.c_lo - 1));
     }
   }
 }
@@ -785,7 +783,7 @@ __global__ void fast_tables_kernel(DevProfile p, int G, int live_top, double* ro
 bool fast_profile_ok(const DevProfile& prof, int G) {
   if (!prof.has_cmemo || !prof.has_bmemo) return false;
   const int64_t ncm = prof.c_hi - prof.c_lo + 1;
-  if (ncm > 65536 || prof.c_hi > (1 << 30)) return false;
+  if (ncm > 65000 || prof.c_hi > (1 << 30)) return false;
   const int64_t live_top = (prof.b_hi + G - 1) / G;
   return (live_top - 1) * ncm <= (int64_t)1 << 26;  // <= 512 MiB of rows
 }
@@ -793,25 +791,24 @@ bool fast_profile_ok(const DevProfile& prof, int G) {
 size_t fast_eval_bytes(const DevProfile& prof, int G) {
   const int64_t ncm = prof.c_hi - prof.c_lo + 1;
   const int64_t live_top = std::max<int64_t>(1, (prof.b_hi + G - 1) / G);
-  return abytes((live_top - 1) * ncm, 8) + abytes(ncm + 1, 4) + abytes((size_t)1024 * kMaxSeg, 4);
+  return abytes((live_top - 1) * ncm, 8) + abytes(ncm, 8) + abytes(ncm + 1, 2) +
+         abytes((size_t)1024 * kMaxSeg, 4);
 }
 
-int fast_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, CandRange cr,
-              int units, double* gt) {
-  if (!fast_profile_ok(prof, cr.G)) return fail(RS_E_CONFIG, "profile not eligible for the fast path");
+// Halved tpot tables and piece ends of (profile, G) in the arena.
+static int fast_prof_make(rs_ctx* ctx, const DevProfile& prof, int G, FastProf* out) {
   const int64_t ncm = prof.c_hi - prof.c_lo + 1;
-  const int live_top = (int)std::max<int64_t>(1, (prof.b_hi + cr.G - 1) / cr.G);
+  const int live_top = (int)std::max<int64_t>(1, (prof.b_hi + G - 1) / G);
   double* rows = arena_alloc<double>(ctx, std::max<int64_t>(1, (int64_t)(live_top - 1) * ncm));
-  int32_t* pex = arena_alloc<int32_t>(ctx, ncm + 1);
-  const int grid = std::min(S * units, ctx->num_sms);
-  uint32_t* pmsm = arena_alloc<uint32_t>(ctx, (size_t)grid * kMaxSeg);
-  if (!rows || !pex || !pmsm) return fail(RS_E_NOMEM, "arena exhausted (fast eval)");
+  double* top = arena_alloc<double>(ctx, ncm);
+  uint16_t* pex = arena_alloc<uint16_t>(ctx, ncm + 1);
+  if (!rows || !top || !pex) return fail(RS_E_NOMEM, "arena exhausted (tpot tables)");
   double front, back;
   RS_CUDA_TRY(cudaMemcpyAsync(&front, prof.ck, 8, cudaMemcpyDeviceToHost, ctx->stream));
   RS_CUDA_TRY(cudaMemcpyAsync(&back, prof.ck + prof.nc - 1, 8, cudaMemcpyDeviceToHost, ctx->stream));
   RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  FastProf fp;
-  fp.top = prof.top_row;
+  FastProf& fp = *out;
+  fp.top = top;
   fp.rows = rows;
   fp.pex = pex;
   fp.c_lo = (int)prof.c_lo;
@@ -821,9 +818,20 @@ int fast_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, Cand
   fp.cfront_m1 = (int)prof.cfront_m1;
   fp.ncm = (int)ncm;
   fp.live_top = live_top;
-  const int64_t tot = (int64_t)live_top * ncm + 1;
+  const int64_t tot = (int64_t)(live_top - 1) * ncm + 2 * ncm + 1;
   RS_LAUNCH(ctx, "fast_tables", fast_tables_kernel, (int)std::min<int64_t>((tot + 255) / 256, 4096),
-            256, 0, prof, cr.G, live_top, rows, pex, fp.cf_ceil, fp.cb_ceil);
+            256, 0, prof, G, live_top, rows, top, pex, fp.cf_ceil, fp.cb_ceil);
+  return RS_OK;
+}
+
+int fast_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, CandRange cr,
+              int units, double* gt) {
+  if (!fast_profile_ok(prof, cr.G)) return fail(RS_E_CONFIG, "profile not eligible for the fast path");
+  const int grid = std::min(S * units, ctx->num_sms);
+  uint32_t* pmsm = arena_alloc<uint32_t>(ctx, (size_t)grid * kMaxSeg);
+  if (!pmsm) return fail(RS_E_NOMEM, "arena exhausted (fast eval)");
+  FastProf fp;
+  if (int st = fast_prof_make(ctx, prof, cr.G, &fp)) return st;
   EvalArgs A{ss, fp, cr, S, units, gt, pmsm};
   const int smem = (int)sizeof(EvalShared);
   RS_CUDA_TRY(cudaFuncSetAttribute(fast_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -946,9 +954,9 @@ __global__ void group_table_kernel(FastSS ss, DevProfile prof, CandRange cr, int
 
 __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
   extern __shared__ __align__(16) unsigned char ls_smem[];
-  double* s_top = reinterpret_cast<double*>(ls_smem);
-  int32_t* s_pex = reinterpret_cast<int32_t*>(s_top + kTopCap);
   const FastProf& fp0 = A.fp;
+  double* s_top = reinterpret_cast<double*>(ls_smem);
+  uint16_t* s_pex = reinterpret_cast<uint16_t*>(s_top + fp0.ncm);
   for (int i = threadIdx.x; i < fp0.ncm; i += kLsThreads) s_top[i] = fp0.top[i];
   for (int i = threadIdx.x; i <= fp0.ncm; i += kLsThreads) s_pex[i] = fp0.pex[i];
   __syncthreads();
@@ -999,8 +1007,21 @@ __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
     };
     if (on) enter(__ldg(gtab + g), __ldg(gfirst + g));
     int fnext = 0;  // finish tick of segment k + 1 (uniform)
+    // segment k's entry and in-block maxima are the same for every lane:
+    // fetched one step ahead to take their latency off the k chain
+    int2 sk_n = make_int2(0, 0);
+    uint32_t pm_n = 0;
+    if (D > 0) {
+      sk_n = __ldg(&V.seg[D - 1]);
+      pm_n = __ldg(V.pmsm + D - 1);
+    }
     for (int k = D - 1; k >= 0; --k) {
-      const int2 sk = __ldg(&V.seg[k]);
+      const int2 sk = sk_n;
+      const uint32_t pmk = pm_n;
+      if (k > 0) {
+        sk_n = __ldg(&V.seg[k - 1]);
+        pm_n = __ldg(V.pmsm + k - 1);
+      }
       const int f = sk.x & 0xffff;
       const int jr = k >> 4;
       if (!done && k < kb) {
@@ -1015,21 +1036,24 @@ __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
               cbase = max(va, smb);
               if (jl + 1 <= jr - 1) cbase = max(cbase, ls_blocks(V, jl + 1, jr - 1));
             }
-            base = max(cbase, (int)(__ldg(V.pmsm + k) & 0xffff));
+            base = max(cbase, (int)(pmk & 0xffff));
           }
         }
         // tpot_context_run_sum (planner.cpp:61-84): one code path; the row is
         // the clamped-batch row in shared memory or a small-batch row.
         const int live = sk.y - a;
         const int c1 = base + f - 1;
+        // The run has at least one context (f > fnext); its first piece
+        // term starts the sum (0.0 + x == x for the non-negative terms).
         const double* row = live >= live_top ? s_top : rows + (size_t)(live - 1) * ncm;
-        double rs = 0.0;
-        for (int cc = base + fnext; cc <= c1;) {
-          const int pe = min(c1, s_pex[min(max(cc, clo1), chi) - clo1]);
-          const double t0 = row[min(max(cc, clo), chi) - clo];
-          const double t1 = row[min(max(pe, clo), chi) - clo];
-          rs = dadd(rs, dmul(dmul((double)(pe - cc + 1), dadd(t0, t1)), 0.5));
-          cc = pe + 1;
+        int cc = base + fnext;
+        int pe = piece_end(s_pex, cc, c1, clo1, chi);
+        double rs = piece_term(pe - cc + 1, row[min(max(cc, clo), chi) - clo],
+                               row[min(max(pe, clo), chi) - clo]);
+        for (cc = pe + 1; cc <= c1; cc = pe + 1) {
+          pe = piece_end(s_pex, cc, c1, clo1, chi);
+          rs = dadd(rs, piece_term(pe - cc + 1, row[min(max(cc, clo), chi) - clo],
+                                   row[min(max(pe, clo), chi) - clo]));
         }
         total = dadd(total, rs);
       }
@@ -1053,28 +1077,8 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
   if (!fast_profile_ok(prof, cr.G)) return fail(RS_E_CONFIG, "profile not eligible for the fast path");
   const int64_t ncm = prof.c_hi - prof.c_lo + 1;
   if (ncm > kTopCap) return fail(RS_E_CONFIG, "context memo too large for the lockstep evaluator");
-  const int live_top = (int)std::max<int64_t>(1, (prof.b_hi + cr.G - 1) / cr.G);
-  double* rows = arena_alloc<double>(ctx, std::max<int64_t>(1, (int64_t)(live_top - 1) * ncm));
-  int32_t* pex = arena_alloc<int32_t>(ctx, ncm + 1);
-  if (!rows || !pex) return fail(RS_E_NOMEM, "arena exhausted (lockstep)");
-  double front, back;
-  RS_CUDA_TRY(cudaMemcpyAsync(&front, prof.ck, 8, cudaMemcpyDeviceToHost, ctx->stream));
-  RS_CUDA_TRY(cudaMemcpyAsync(&back, prof.ck + prof.nc - 1, 8, cudaMemcpyDeviceToHost, ctx->stream));
-  RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   FastProf fp;
-  fp.top = prof.top_row;
-  fp.rows = rows;
-  fp.pex = pex;
-  fp.c_lo = (int)prof.c_lo;
-  fp.c_hi = (int)prof.c_hi;
-  fp.cf_ceil = (int)std::ceil(front);
-  fp.cb_ceil = (int)std::ceil(back);
-  fp.cfront_m1 = (int)prof.cfront_m1;
-  fp.ncm = (int)ncm;
-  fp.live_top = live_top;
-  const int64_t tot = (int64_t)live_top * ncm + 1;
-  RS_LAUNCH(ctx, "fast_tables", fast_tables_kernel, (int)std::min<int64_t>((tot + 255) / 256, 4096),
-            256, 0, prof, cr.G, live_top, rows, pex, fp.cf_ceil, fp.cb_ceil);
+  if (int st = fast_prof_make(ctx, prof, cr.G, &fp)) return st;
   const int C = cr.n_max - cr.n_min + 1;
   int4* gtab = arena_alloc<int4>(ctx, (size_t)S * cr.T);
   double* gfirst = arena_alloc<double>(ctx, (size_t)S * cr.T);
@@ -1086,7 +1090,7 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
               gtab, gfirst);
   }
   LsArgs A{ss, fp, cr, S, (C + kLsThreads - 1) / kLsThreads, gt, gtab, gfirst};
-  const int smem = (int)(sizeof(double) * kTopCap + sizeof(int32_t) * (kTopCap + 1));
+  const int smem = (int)(sizeof(double) * ncm + sizeof(uint16_t) * (ncm + 1));
   RS_CUDA_TRY(cudaFuncSetAttribute(lockstep_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 1;
   RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lockstep_eval_kernel, kLsThreads, smem));
