@@ -58,8 +58,8 @@ FastSS fast_ss_alloc(rs_ctx* ctx, const int64_t* d_off, int64_t items, int S) {
 constexpr int kBuildT = 1024;
 constexpr int kWide = 4096;                 // records per sorting window (max bucket size)
 constexpr int kBuildCur = kFastFmax + 4;     // cur[] ints (16-byte aligned end)
-constexpr int kBuildSmem = kBuildCur * 4 + kWide * 20;
-static_assert(kWide * 20 >= (kFastFmax + 2) * 2, "window region must hold the bucket map");
+constexpr int kBuildSmem = kBuildCur * 4 + kWide * 28;
+static_assert(kWide * 28 >= (kFastFmax + 2) * 2, "window region must hold the bucket map");
 
 template <bool kGen>
 __global__ void __launch_bounds__(kBuildT)
@@ -74,6 +74,8 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
   int32_t* w_id = reinterpret_cast<int32_t*>(w_key + kWide);
   int32_t* w_pk = w_id + kWide;
   int32_t* w_pl = w_pk + kWide;
+  int32_t* w_pm = w_pl + kWide;
+  uint32_t* w_q = reinterpret_cast<uint32_t*>(w_pm + kWide);
   __shared__ int32_t wsum[32];
   __shared__ long long wsum64[32];
   __shared__ int bad, s_k1;
@@ -173,21 +175,39 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
   __syncthreads();
   // Scatter 16-byte records {pred bits, id, plen | segment << 16} into the
   // buckets (bucket order: finish tick descending).
-  for (int i = tid; i < P; i += kBuildT) {
-    double p = pred[i];
-    int f = (int)ceil(p);
-    int pos = atomicAdd(&cur[f], 1);
-    long long bits = __double_as_longlong(p);
-    ss.rec[i0 + pos] = make_int4((int)(bits & 0xffffffffLL), (int)(bits >> 32), i,
-                                 plen[i] | ((int)skf[f] << 16));
+  constexpr int kScat = 4;  // loads batched ahead of the atomics
+  for (int i = tid; i < P; i += kScat * kBuildT) {
+    double p[kScat];
+    int pl[kScat];
+#pragma unroll
+    for (int u = 0; u < kScat; ++u) {
+      const int j = i + u * kBuildT;
+      p[u] = j < P ? pred[j] : 0.0;
+      pl[u] = j < P ? plen[j] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kScat; ++u) {
+      const int j = i + u * kBuildT;
+      if (j < P) {
+        const int f = (int)ceil(p[u]);
+        const int pos = atomicAdd(&cur[f], 1);
+        const long long bits = __double_as_longlong(p[u]);
+        ss.rec[i0 + pos] = make_int4((int)(bits & 0xffffffffLL), (int)(bits >> 32), j,
+                                     pl[u] | ((int)skf[f] << 16));
+      }
+    }
   }
   __syncthreads();
   // Order each bucket (pred desc, id asc) — planner.cpp:121-126 ranks by
   // predicted length — one window of whole buckets (<= kWide records) at a
   // time in shared memory: every record counts the records of its bucket
   // that precede it (buckets are small: median 3, ~50 at the 99th
-  // percentile), then every sorted position takes its in-bucket prefix /
-  // suffix prompt_len maxima.
+  // percentile), then one thread per bucket writes the in-bucket prefix /
+  // suffix prompt_len maxima. The count compares a 32-bit in-bucket key
+  // q = (bits(pred) - bits(f - 1)) >> 21 first: positive doubles order as
+  // their bit patterns and a bucket (f - 1, f], f >= 2, spans < 2^53
+  // patterns, so q is monotone in pred and only q ties need the full
+  // (pred, id) comparison. Bucket f = 1 has q = 0 (always the full one).
   const int D = ss.nseg[s];
   int32_t* segend = cur;  // cur is dead after the scatter
   for (int k = tid; k < D; k += kBuildT) segend[k] = ss.seg[so + k].y;
@@ -215,7 +235,11 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
     const int n = segend[k1 - 1] - ws;
     for (int i = tid; i < n; i += kBuildT) {
       const int4 r = ss.rec[i0 + ws + i];
-      w_key[i] = ((long long)r.y << 32) | (unsigned)r.x;  // positive doubles order as integers
+      const long long bits = ((long long)r.y << 32) | (unsigned)r.x;
+      const double p = __longlong_as_double(bits);
+      const double fm1 = ceil(p) - 1.0;
+      w_key[i] = bits;
+      w_q[i] = fm1 >= 1.0 ? (uint32_t)((bits - __double_as_longlong(fm1)) >> 21) : 0u;
       w_id[i] = r.z;
       w_pk[i] = r.w;
     }
@@ -223,27 +247,35 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
     for (int i = tid; i < n; i += kBuildT) {
       const int k = w_pk[i] >> 16;
       const int lo = (k == 0 ? 0 : segend[k - 1]) - ws, hi = segend[k] - ws;
-      const long long key = w_key[i];
-      const int id = w_id[i];
+      const uint32_t q = w_q[i];
       int rank = 0;
       for (int j = lo; j < hi; ++j) {
-        const long long kj = w_key[j];
-        rank += (kj > key || (kj == key && w_id[j] < id)) ? 1 : 0;
+        const uint32_t qj = w_q[j];
+        rank += qj > q ? 1 : 0;
+        if (qj == q && j != i) {
+          const long long kj = w_key[j], key = w_key[i];
+          rank += (kj > key || (kj == key && w_id[j] < w_id[i])) ? 1 : 0;
+        }
       }
       const int pl = w_pk[i] & 0xffff;
       w_pl[lo + rank] = pl;
       ss.plen_r[i0 + ws + lo + rank] = pl;
-      ss.order_r[i0 + ws + lo + rank] = id;
+      ss.order_r[i0 + ws + lo + rank] = w_id[i];
     }
     __syncthreads();
-    for (int r = tid; r < n; r += kBuildT) {
-      const int k = w_pk[r] >> 16;  // sorting stays inside the bucket
+    for (int k = k0 + tid; k < k1; k += kBuildT) {  // one thread per bucket
       const int lo = (k == 0 ? 0 : segend[k - 1]) - ws, hi = segend[k] - ws;
-      int pm = 0, sm = 0;
-      for (int j = lo; j <= r; ++j) pm = max(pm, w_pl[j]);
-      for (int j = r; j < hi; ++j) sm = max(sm, w_pl[j]);
-      ss.rinfo[i0 + ws + r] = make_int2(k, sm | (pm << 16));
-      if (r == hi - 1) ss.seg[so + k].x |= pm << 16;
+      int pm = 0;
+      for (int j = lo; j < hi; ++j) {
+        pm = max(pm, w_pl[j]);
+        w_pm[j] = pm;
+      }
+      ss.seg[so + k].x |= pm << 16;
+      int sm = 0;
+      for (int j = hi - 1; j >= lo; --j) {
+        sm = max(sm, w_pl[j]);
+        ss.rinfo[i0 + ws + j] = make_int2(k, sm | (w_pm[j] << 16));
+      }
     }
     __syncthreads();
     k0 = k1;
