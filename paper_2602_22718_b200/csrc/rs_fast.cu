@@ -823,7 +823,7 @@ bool fast_profile_ok(const DevProfile& prof, int G) {
 size_t fast_eval_bytes(const DevProfile& prof, int G) {
   const int64_t ncm = prof.c_hi - prof.c_lo + 1;
   const int64_t live_top = std::max<int64_t>(1, (prof.b_hi + G - 1) / G);
-  return abytes((live_top - 1) * ncm, 8) + abytes(ncm, 8) + abytes(ncm + 1, 2) +
+  return abytes(live_top * ncm, 8) + abytes(ncm + 1, 2) +
          abytes((size_t)1024 * kMaxSeg, 4);
 }
 
@@ -831,8 +831,9 @@ size_t fast_eval_bytes(const DevProfile& prof, int G) {
 static int fast_prof_make(rs_ctx* ctx, const DevProfile& prof, int G, FastProf* out) {
   const int64_t ncm = prof.c_hi - prof.c_lo + 1;
   const int live_top = (int)std::max<int64_t>(1, (prof.b_hi + G - 1) / G);
-  double* rows = arena_alloc<double>(ctx, std::max<int64_t>(1, (int64_t)(live_top - 1) * ncm));
-  double* top = arena_alloc<double>(ctx, ncm);
+  // rows for live = 1 .. live_top - 1, then the clamped row: one table
+  double* rows = arena_alloc<double>(ctx, (int64_t)live_top * ncm);
+  double* top = rows ? rows + (int64_t)(live_top - 1) * ncm : nullptr;
   uint16_t* pex = arena_alloc<uint16_t>(ctx, ncm + 1);
   if (!rows || !top || !pex) return fail(RS_E_NOMEM, "arena exhausted (tpot tables)");
   double front, back;
@@ -987,9 +988,7 @@ __global__ void group_table_kernel(FastSS ss, DevProfile prof, CandRange cr, int
 __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
   extern __shared__ __align__(16) unsigned char ls_smem[];
   const FastProf& fp0 = A.fp;
-  double* s_top = reinterpret_cast<double*>(ls_smem);
-  uint16_t* s_pex = reinterpret_cast<uint16_t*>(s_top + fp0.ncm);
-  for (int i = threadIdx.x; i < fp0.ncm; i += kLsThreads) s_top[i] = fp0.top[i];
+  uint16_t* s_pex = reinterpret_cast<uint16_t*>(ls_smem);
   for (int i = threadIdx.x; i <= fp0.ncm; i += kLsThreads) s_pex[i] = fp0.pex[i];
   __syncthreads();
   const int clo = fp0.c_lo, chi = fp0.c_hi, clo1 = fp0.c_lo - 1, ncm = fp0.ncm;
@@ -1077,15 +1076,16 @@ __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
         const int c1 = base + f - 1;
         // The run has at least one context (f > fnext); its first piece
         // term starts the sum (0.0 + x == x for the non-negative terms).
-        const double* row = live >= live_top ? s_top : rows + (size_t)(live - 1) * ncm;
+        // rows are contiguous: live >= live_top reads the clamped row
+        const double* row = rows + (size_t)(min(live, live_top) - 1) * ncm - clo;
         int cc = base + fnext;
         int pe = piece_end(s_pex, cc, c1, clo1, chi);
-        double rs = piece_term(pe - cc + 1, row[min(max(cc, clo), chi) - clo],
-                               row[min(max(pe, clo), chi) - clo]);
+        double rs = piece_term(pe - cc + 1, __ldg(row + min(max(cc, clo), chi)),
+                               __ldg(row + min(max(pe, clo), chi)));
         for (cc = pe + 1; cc <= c1; cc = pe + 1) {
           pe = piece_end(s_pex, cc, c1, clo1, chi);
-          rs = dadd(rs, piece_term(pe - cc + 1, row[min(max(cc, clo), chi) - clo],
-                                   row[min(max(pe, clo), chi) - clo]));
+          rs = dadd(rs, piece_term(pe - cc + 1, __ldg(row + min(max(cc, clo), chi)),
+                                   __ldg(row + min(max(pe, clo), chi))));
         }
         total = dadd(total, rs);
       }
@@ -1122,7 +1122,7 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
               gtab, gfirst);
   }
   LsArgs A{ss, fp, cr, S, (C + kLsThreads - 1) / kLsThreads, gt, gtab, gfirst};
-  const int smem = (int)(sizeof(double) * ncm + sizeof(uint16_t) * (ncm + 1));
+  const int smem = (int)(sizeof(uint16_t) * (ncm + 1));
   RS_CUDA_TRY(cudaFuncSetAttribute(lockstep_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 1;
   RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lockstep_eval_kernel, kLsThreads, smem));
