@@ -988,12 +988,22 @@ __global__ void group_table_kernel(FastSS ss, DevProfile prof, CandRange cr, int
 __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
   extern __shared__ __align__(16) unsigned char ls_smem[];
   const FastProf& fp0 = A.fp;
-  uint16_t* s_pex = reinterpret_cast<uint16_t*>(ls_smem);
-  for (int i = threadIdx.x; i <= fp0.ncm; i += kLsThreads) s_pex[i] = fp0.pex[i];
-  __syncthreads();
+  double* s_tail = reinterpret_cast<double*>(ls_smem);
+  uint16_t* s_pex = reinterpret_cast<uint16_t*>(s_tail + fp0.live_top);
   const int clo = fp0.c_lo, chi = fp0.c_hi, clo1 = fp0.c_lo - 1, ncm = fp0.ncm;
   const int live_top = fp0.live_top;
   const double* rows = fp0.rows;
+  // tpot(G * live, c_hi) for live = 1 .. live_top (the halved entry doubled)
+  for (int i = threadIdx.x; i < live_top; i += kLsThreads) {
+    const double h = rows[(size_t)i * ncm + (ncm - 1)];
+    s_tail[i] = dadd(h, h);
+  }
+  for (int i = threadIdx.x; i <= ncm; i += kLsThreads) s_pex[i] = fp0.pex[i];
+  __syncthreads();
+  // Contexts c >= tail_from are past the memo (clamped to c_hi) and past the
+  // back knot (one piece to the run end): a run starting there is the single
+  // piece (f - fnext) * (t(c_hi) + t(c_hi)) / 2 = (f - fnext) * t(c_hi).
+  const int tail_from = max(chi, fp0.cb_ceil);
   const int C = A.cr.n_max - A.cr.n_min + 1;
   const int64_t flat0 = tri64(A.cr.n_min);
   for (int unit = blockIdx.x; unit < A.S * A.cand_units; unit += gridDim.x) {
@@ -1046,7 +1056,20 @@ __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
       sk_n = __ldg(&V.seg[D - 1]);
       pm_n = __ldg(V.pmsm + D - 1);
     }
-    for (int k = D - 1; k >= 0; --k) {
+    auto complete = [&](int k) {  // groups completing at segment k
+      while (!done && k == ka) {
+        gt[g] = total;
+        if (g == 0) {
+          done = true;
+        } else {
+          --g;
+          enter(nxt, nfirst);
+        }
+      }
+    };
+    int k = D - 1;
+    // Phase 1 (fnext < tail_from): runs may start inside the memo.
+    for (; k >= 0 && fnext < tail_from; --k) {
       const int2 sk = sk_n;
       const uint32_t pmk = pm_n;
       if (k > 0) {
@@ -1070,35 +1093,40 @@ __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
             base = max(cbase, (int)(pmk & 0xffff));
           }
         }
-        // tpot_context_run_sum (planner.cpp:61-84): one code path; the row is
-        // the clamped-batch row in shared memory or a small-batch row.
-        const int live = sk.y - a;
-        const int c1 = base + f - 1;
-        // The run has at least one context (f > fnext); its first piece
-        // term starts the sum (0.0 + x == x for the non-negative terms).
-        // rows are contiguous: live >= live_top reads the clamped row
-        const double* row = rows + (size_t)(min(live, live_top) - 1) * ncm - clo;
+        // tpot_context_run_sum (planner.cpp:61-84). The run has at least one
+        // context (f > fnext); its first piece term starts the sum
+        // (0.0 + x == x for the non-negative terms). Rows are contiguous:
+        // live >= live_top reads the clamped row.
+        const int live = min(sk.y - a, live_top);
         int cc = base + fnext;
-        int pe = piece_end(s_pex, cc, c1, clo1, chi);
-        double rs = piece_term(pe - cc + 1, __ldg(row + min(max(cc, clo), chi)),
-                               __ldg(row + min(max(pe, clo), chi)));
-        for (cc = pe + 1; cc <= c1; cc = pe + 1) {
-          pe = piece_end(s_pex, cc, c1, clo1, chi);
-          rs = dadd(rs, piece_term(pe - cc + 1, __ldg(row + min(max(cc, clo), chi)),
-                                   __ldg(row + min(max(pe, clo), chi))));
+        double rs;
+        if (cc >= tail_from) {
+          rs = dmul((double)(f - fnext), s_tail[live - 1]);
+        } else {
+          const int c1 = base + f - 1;
+          const double* row = rows + (size_t)(live - 1) * ncm - clo;
+          int pe = piece_end(s_pex, cc, c1, clo1, chi);
+          rs = piece_term(pe - cc + 1, __ldg(row + min(max(cc, clo), chi)),
+                          __ldg(row + min(max(pe, clo), chi)));
+          for (cc = pe + 1; cc <= c1; cc = pe + 1) {
+            pe = piece_end(s_pex, cc, c1, clo1, chi);
+            rs = dadd(rs, piece_term(pe - cc + 1, __ldg(row + min(max(cc, clo), chi)),
+                                     __ldg(row + min(max(pe, clo), chi))));
+          }
         }
         total = dadd(total, rs);
       }
-      // groups completing at this segment (several when groups are small)
-      while (!done && k == ka) {
-        gt[g] = total;
-        if (g == 0) {
-          done = true;
-        } else {
-          --g;
-          enter(nxt, nfirst);
-        }
-      }
+      complete(k);
+      fnext = f;
+    }
+    // Phase 2 (fnext >= tail_from, uniform): every run is one clamped piece.
+    for (; k >= 0; --k) {
+      const int2 sk = sk_n;
+      if (k > 0) sk_n = __ldg(&V.seg[k - 1]);
+      const int f = sk.x & 0xffff;
+      if (!done && k < kb)
+        total = dadd(total, dmul((double)(f - fnext), s_tail[min(sk.y - a, live_top) - 1]));
+      complete(k);
       fnext = f;
     }
   }
@@ -1122,7 +1150,7 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
               gtab, gfirst);
   }
   LsArgs A{ss, fp, cr, S, (C + kLsThreads - 1) / kLsThreads, gt, gtab, gfirst};
-  const int smem = (int)(sizeof(uint16_t) * (ncm + 1));
+  const int smem = (int)(sizeof(double) * fp.live_top + sizeof(uint16_t) * (ncm + 1));
   RS_CUDA_TRY(cudaFuncSetAttribute(lockstep_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 1;
   RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lockstep_eval_kernel, kLsThreads, smem));
