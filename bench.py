@@ -289,10 +289,12 @@ def run_ours(args, world, rank, local):
     ge_avg_ms = ge_ms / max(ge_n, 1)
     per_launch_evals = total_evals / world * args.steps / max(ge_n, 1)
     achieved = per_launch_evals * EVAL_BYTES / (ge_avg_ms / 1e3) / 1e9
-    traffic = None
+    traffic = None  # ncu dram read+write per launch (profiles/traffic.json, per eval x evals)
     tf = REPO / "profiles" / "traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get("group_eval_bytes_per_launch")
+        bpe = json.loads(tf.read_text()).get("group_eval_dram_bytes_per_eval")
+        if bpe:
+            traffic = bpe * per_launch_evals
     result = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -404,7 +406,7 @@ def main():
     ap.add_argument("--n-max", type=int, default=256)
     ap.add_argument("--G", type=int, default=8)
     ap.add_argument("--lam", type=float, default=0.7)
-    ap.add_argument("--cpu-rounds", type=int, default=1)
+    ap.add_argument("--cpu-rounds", type=int, default=4)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dedup", action="store_true")
     ap.add_argument("--check", action="store_true", default=True)

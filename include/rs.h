@@ -39,7 +39,8 @@ typedef enum rs_status {
   RS_E_CONFIG = 2,     /* rollsim::ConfigError */
   RS_E_CUDA = 3,       /* CUDA runtime / launch failure, or no device */
   RS_E_NOMEM = 4,      /* device or pinned allocation failed */
-  RS_E_ARG = 5         /* NULL handle / pointer misuse (programming error) */
+  RS_E_ARG = 5,        /* NULL handle / pointer misuse (programming error) */
+  RS_E_PLACEMENT = 6   /* rollsim::PlacementError (cluster cannot host the plan) */
 } rs_status;
 
 const char* rs_last_error(void);
@@ -234,6 +235,46 @@ int rs_scale(rs_ctx* ctx, const double* pred, const int32_t* prompt_len,
              int32_t responses_per_prompt, int32_t n_min, int32_t n_max,
              double lambda, int32_t gpus_per_actor, const double* t_penalty,
              rs_scale_out* out);
+
+/* ------------------------------------------------------------------ */
+/* (3b) scale() with the placement penalty on the device               */
+/* ------------------------------------------------------------------ */
+/* ClusterTopology (placement.hpp:14-38). bw_matrix, when non-NULL, is
+ * n_nodes x n_nodes row-major and wins over the two-tier bandwidths. */
+typedef struct rs_topology {
+  int32_t n_nodes;
+  const int32_t* node_gpus;     /* GPUs per node */
+  double intra_node_bw, inter_node_bw; /* bytes/s */
+  const double* bw_matrix;
+  int32_t learner_node;
+  int32_t n_learner_gpus;
+  const int32_t* learner_gpus;  /* local GPU indices on learner_node */
+} rs_topology;
+
+/* The TimePenaltyFn plan_rlhfless installs (training.cpp:150-164): place the
+ * candidate (placement.cpp:177-291: heaviest actor on the learner node, the
+ * rest by descending estimated time onto the highest-bandwidth node with room),
+ * then charge max(0, max_i -slack_i) with slack_i = (l_prefill + T_heaviest)
+ * - (model_bytes/bw_i + kv_bytes_i/bw_i + T_i) (placement.cpp:339-363), where
+ * kv_bytes_i = kv_bytes_per_token * sum of the group's prompt lengths
+ * (transfers_for, training.cpp:68-80). */
+typedef struct rs_placement_penalty {
+  const rs_topology* topology;
+  double model_bytes;
+  double kv_bytes_per_token;
+  double l_prefill_seconds;
+} rs_placement_penalty;
+
+/* scale() with that penalty computed on the device for every candidate.
+ * Errors in the reference's order: scale's own argument checks, then
+ * ClusterTopology::validate / transfer checks (RS_E_CONFIG), then
+ * RS_E_PLACEMENT when a candidate's actors do not fit the cluster.
+ * out->t_penalty receives the per-candidate penalties. */
+int rs_scale_placed(rs_ctx* ctx, const double* pred, const int32_t* prompt_len,
+                    const int32_t* id_rank, int32_t count, const rs_profile* profile,
+                    int32_t responses_per_prompt, int32_t n_min, int32_t n_max,
+                    double lambda, int32_t gpus_per_actor,
+                    const rs_placement_penalty* penalty, rs_scale_out* out);
 
 /* The normalise + argmin tail of scale() (planner.cpp:196-217) on
  * caller-provided per-candidate totals; used after host penalty callbacks. */

@@ -14,7 +14,7 @@
  * --impl reference legs may load these libraries.
  *
  * Status codes match include/rs.h: 0 ok, 1 ValidationError, 2 ConfigError,
- * 5 other error.
+ * 5 other error, 6 PlacementError.
  */
 #ifndef RS_ORACLE_H_
 #define RS_ORACLE_H_
@@ -72,7 +72,16 @@ extern "C" {
                            const rs_profile* p, int32_t g, int32_t n_min,      \
                            int32_t n_max, double lambda, int32_t gpus,         \
                            int32_t n_threads, double* t_total, double* cost,   \
-                           int32_t* n_star);
+                           int32_t* n_star);                            \
+  /* scale() with plan_rlhfless's placement penalty (training.cpp:150-164) */  \
+  int prefix##scale_placed(const double* pred, const int32_t* plen,            \
+                           const int32_t* id_rank, int32_t count,              \
+                           const rs_profile* p, int32_t g, int32_t n_min,      \
+                           int32_t n_max, double lambda, int32_t gpus,         \
+                           const rs_placement_penalty* pen, int32_t* n_star,   \
+                           double* t_total, double* t_pen_out, double* cost,   \
+                           double* t_norm, double* c_norm, double* score,      \
+                           int32_t* order, double* actor_times);
 
 ORACLE_API(ref_)
 ORACLE_API(orc_)

@@ -18,6 +18,7 @@
 #include "oracle.h"
 #include "rollsim/dedup.hpp"
 #include "rollsim/errors.hpp"
+#include "rollsim/placement.hpp"
 #include "rollsim/planner.hpp"
 #include "rollsim/profile.hpp"
 #include "rollsim/workload.hpp"
@@ -37,6 +38,9 @@ int guarded(F&& f) {
   } catch (const rollsim::ConfigError& e) {
     g_err = e.what();
     return 2;
+  } catch (const rollsim::PlacementError& e) {
+    g_err = e.what();
+    return 6;
   } catch (const std::exception& e) {
     g_err = e.what();
     return 5;
@@ -253,6 +257,80 @@ int ref_scale(const double* pred, const int32_t* plen, const int32_t* id_rank,
         actor_times[i] = r.actor_times[i];
     if (order) {
       // Map rank ids back to input indices.
+      std::vector<int32_t> by_rank;
+      if (id_rank) {
+        by_rank.assign(count, 0);
+        for (int32_t i = 0; i < count; ++i) by_rank[id_rank[i]] = i;
+      }
+      int32_t pos = 0;
+      for (const auto& grp : r.groups)
+        for (const std::string& id : grp.prompt_ids) {
+          int32_t rk = std::stoi(id.substr(1));
+          order[pos++] = id_rank ? by_rank[rk] : rk;
+        }
+    }
+  });
+}
+
+// plan_rlhfless's penalty (training.cpp:150-164) around the reference's own
+// place() / check_overlap(); transfers as transfers_for (training.cpp:68-80).
+int ref_scale_placed(const double* pred, const int32_t* plen, const int32_t* id_rank,
+                     int32_t count, const rs_profile* p, int32_t g, int32_t n_min,
+                     int32_t n_max, double lambda, int32_t gpus,
+                     const rs_placement_penalty* pen, int32_t* n_star, double* t_total,
+                     double* t_pen_out, double* cost, double* t_norm, double* c_norm,
+                     double* score, int32_t* order, double* actor_times) {
+  return guarded([&] {
+    const rs_topology& t = *pen->topology;
+    rollsim::ClusterTopology topo;
+    topo.nodes.clear();
+    for (int i = 0; i < t.n_nodes; ++i) topo.nodes.push_back({t.node_gpus[i]});
+    topo.intra_node_bw = t.intra_node_bw;
+    topo.inter_node_bw = t.inter_node_bw;
+    if (t.bw_matrix)
+      for (int i = 0; i < t.n_nodes; ++i)
+        topo.bw_matrix.emplace_back(t.bw_matrix + (size_t)i * t.n_nodes,
+                                    t.bw_matrix + (size_t)(i + 1) * t.n_nodes);
+    topo.learner_node = t.learner_node;
+    topo.learner_gpus.assign(t.learner_gpus, t.learner_gpus + t.n_learner_gpus);
+    rollsim::TimePenaltyFn fn = [&](int n, const std::vector<rollsim::ActorGroup>& groups,
+                                    const std::vector<double>& times) {
+      rollsim::GenerationPlan probe;
+      probe.responses_per_prompt = g;
+      probe.prefill_mode = rollsim::PrefillMode::shared_dedup;
+      probe.n_actors = n;
+      probe.groups = groups;
+      probe.est_time_per_actor = times;
+      probe.prefill_gpu_count = t.n_learner_gpus;
+      rollsim::TransferSizes tr;
+      tr.model_bytes = pen->model_bytes;
+      tr.kv_bytes_per_actor.clear();
+      for (const auto& grp : groups) {
+        int64_t tokens = 0;
+        for (int pl : grp.prompt_lens) tokens += pl;
+        tr.kv_bytes_per_actor.push_back(static_cast<double>(tokens) * pen->kv_bytes_per_token);
+      }
+      rollsim::PlacementPlan pl = rollsim::place(probe, topo, tr);
+      double exposed = 0;
+      for (const rollsim::OverlapSlack& s : rollsim::check_overlap(pl, probe, pen->l_prefill_seconds))
+        exposed = std::max(exposed, -s.slack);
+      return exposed;
+    };
+    auto v = to_predicted(pred, plen, id_rank, count);
+    rollsim::ScaleResult r = rollsim::scale(v, to_profile(p), g, n_min, n_max, lambda, gpus, fn);
+    *n_star = r.n_star;
+    for (size_t i = 0; i < r.candidates.size(); ++i) {
+      const auto& c = r.candidates[i];
+      if (t_total) t_total[i] = c.t_total;
+      if (t_pen_out) t_pen_out[i] = c.t_penalty;
+      if (cost) cost[i] = c.cost;
+      if (t_norm) t_norm[i] = c.t_norm;
+      if (c_norm) c_norm[i] = c.c_norm;
+      if (score) score[i] = c.score;
+    }
+    if (actor_times)
+      for (size_t i = 0; i < r.actor_times.size(); ++i) actor_times[i] = r.actor_times[i];
+    if (order) {
       std::vector<int32_t> by_rank;
       if (id_rank) {
         by_rank.assign(count, 0);

@@ -341,6 +341,151 @@ int orc_scale(const double* pred, const int32_t* plen, const int32_t* id_rank,
   return 0;
 }
 
+/* ---- placement penalty: plan_rlhfless's TimePenaltyFn
+ * (training.cpp:150-164) = place() (placement.cpp:177-291) + check_overlap()
+ * (placement.cpp:339-363) with transfers_for (training.cpp:68-80). Restated
+ * actor by actor, as the reference does it. */
+static double topo_bw(const rs_topology* t, int a, int b) {
+  if (t->bw_matrix) return t->bw_matrix[(size_t)a * t->n_nodes + b];
+  return a == b ? t->intra_node_bw : t->inter_node_bw;
+}
+
+static int topo_validate(const rs_topology* t) {                 /* placement.cpp:28-62 */
+  if (t->n_nodes < 1) return fail(2, "topology needs at least one node");
+  for (int i = 0; i < t->n_nodes; ++i)
+    if (t->node_gpus[i] < 1) return fail(2, "every node needs at least one GPU");
+  if (!t->bw_matrix) {
+    if (!(t->intra_node_bw > 0) || !(t->inter_node_bw > 0)) return fail(2, "bandwidths must be positive");
+    if (t->intra_node_bw < t->inter_node_bw) return fail(2, "intra-node bandwidth below inter-node bandwidth");
+  } else {
+    for (int i = 0; i < t->n_nodes; ++i)
+      for (int j = 0; j < t->n_nodes; ++j) {
+        double v = t->bw_matrix[(size_t)i * t->n_nodes + j];
+        if (!(v > 0)) return fail(2, "bandwidth matrix entries must be positive");
+        if (v != t->bw_matrix[(size_t)j * t->n_nodes + i]) return fail(2, "bandwidth matrix must be symmetric");
+      }
+  }
+  if (t->learner_node < 0 || t->learner_node >= t->n_nodes) return fail(2, "learner_node out of range");
+  if (t->n_learner_gpus < 1) return fail(2, "learner needs at least one GPU");
+  for (int k = 0; k < t->n_learner_gpus; ++k)
+    if (t->learner_gpus[k] < 0 || t->learner_gpus[k] >= t->node_gpus[t->learner_node])
+      return fail(2, "learner GPU index out of range");
+  return 0;
+}
+
+static int placement_penalty(const rs_placement_penalty* pen, int32_t n, const double* times,
+                             const int64_t* tokens, int32_t gpus, double* out) {
+  const rs_topology* t = pen->topology;
+  int rc = topo_validate(t);
+  if (rc) return rc;
+  if (!(pen->model_bytes >= 0) || !isfinite(pen->model_bytes))    /* placement.cpp:151-152 */
+    return fail(2, "model_bytes must be finite and >= 0");
+  double* kv = malloc(sizeof(double) * n);
+  double* lm = calloc(n, sizeof(double));
+  double* lkv = calloc(n, sizeof(double));
+  int32_t* order = malloc(sizeof(int32_t) * n);
+  int32_t* rank = malloc(sizeof(int32_t) * t->n_nodes);
+  int32_t* freeg = malloc(sizeof(int32_t) * t->n_nodes);
+  rc = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    kv[i] = (double)tokens[i] * pen->kv_bytes_per_token;           /* training.cpp:76-77 */
+    if (!(kv[i] >= 0) || !isfinite(kv[i])) rc = fail(2, "kv bytes must be finite and >= 0");
+  }
+  if (!rc) {
+    int32_t heaviest = 0;                                           /* placement.cpp:193-197 */
+    for (int32_t i = 1; i < n; ++i) if (times[i] > times[heaviest]) heaviest = i;
+    int32_t m = 0;
+    order[m++] = heaviest;
+    for (int32_t i = 0; i < n; ++i) if (i != heaviest) order[m++] = i;
+    for (int32_t i = 2; i < n; ++i) {                               /* :201-205 stable by (t desc, idx asc) */
+      int32_t x = order[i], j = i - 1;
+      while (j >= 1 && (times[order[j]] < times[x] ||
+                        (times[order[j]] == times[x] && order[j] > x))) {
+        order[j + 1] = order[j];
+        --j;
+      }
+      order[j + 1] = x;
+    }
+    for (int k = 0; k < t->n_nodes; ++k) { rank[k] = k; freeg[k] = t->node_gpus[k]; }
+    for (int k = 1; k < t->n_nodes; ++k) {                          /* :209-215 */
+      int32_t x = rank[k], j = k - 1;
+      double bx = topo_bw(t, x, t->learner_node);
+      while (j >= 0) {
+        double bj = topo_bw(t, rank[j], t->learner_node);
+        if (bj < bx || (bj == bx && rank[j] > x)) { rank[j + 1] = rank[j]; --j; } else break;
+      }
+      rank[j + 1] = x;
+    }
+    int32_t coloc = -1;
+    for (int32_t oi = 0; oi < n && !rc; ++oi) {                     /* :233-270 */
+      int32_t actor = order[oi], placed = 0;
+      if (oi == 0 && freeg[t->learner_node] >= gpus) {
+        freeg[t->learner_node] -= gpus;
+        coloc = actor;
+        placed = 1;
+      }
+      for (int k = 0; k < t->n_nodes && !placed; ++k) {
+        int nd = rank[k];
+        if (freeg[nd] < gpus) continue;
+        freeg[nd] -= gpus;
+        double bw = topo_bw(t, nd, t->learner_node);
+        lm[actor] = pen->model_bytes / bw;
+        lkv[actor] = kv[actor] / bw;
+        placed = 1;
+      }
+      if (!placed) rc = fail(6, "cannot place actor");
+    }
+    if (!rc) {
+      int32_t ref = coloc;                                          /* :342-347 */
+      if (ref < 0) { ref = 0; for (int32_t i = 1; i < n; ++i) if (times[i] > times[ref]) ref = i; }
+      double d1 = times[ref], exposed = 0;
+      for (int32_t i = 0; i < n; ++i) {
+        if (i == ref) continue;
+        double slack = (pen->l_prefill_seconds + d1) - (lm[i] + lkv[i] + times[i]);
+        exposed = exposed < -slack ? -slack : exposed;              /* training.cpp:161-162 */
+      }
+      *out = exposed;
+    }
+  }
+  free(kv); free(lm); free(lkv); free(order); free(rank); free(freeg);
+  return rc;
+}
+
+int orc_scale_placed(const double* pred, const int32_t* plen, const int32_t* id_rank,
+                     int32_t count, const rs_profile* p, int32_t g, int32_t n_min,
+                     int32_t n_max, double lambda, int32_t gpus,
+                     const rs_placement_penalty* pen, int32_t* n_star, double* t_total,
+                     double* t_pen_out, double* cost, double* t_norm, double* c_norm,
+                     double* score, int32_t* order, double* actor_times) {
+  /* scale()'s own checks first (the penalty runs inside its loop) */
+  int rc = orc_scale(pred, plen, id_rank, count, p, g, n_min, n_max, lambda, gpus, NULL, n_star,
+                     NULL, NULL, NULL, NULL, NULL, NULL, NULL, NULL);
+  if (rc) return rc;
+  int32_t nc = n_max - n_min + 1;
+  rank_t* v = rank_prompts(pred, id_rank, count);
+  resp_t* scratch = malloc(sizeof(resp_t) * count);
+  int32_t* suf = malloc(sizeof(int32_t) * (count + 1));
+  double* tp = malloc(sizeof(double) * nc);
+  double* times = malloc(sizeof(double) * n_max);
+  int64_t* tokens = malloc(sizeof(int64_t) * n_max);
+  for (int32_t n = n_min; n <= n_max && !rc; ++n) {
+    int32_t q = count / n, r = count % n, pos = 0;
+    for (int32_t a = 0; a < n; ++a) {
+      int32_t size = q + (a < r ? 1 : 0);
+      times[a] = group_time(v, plen, pos, pos + size, g, p, scratch, suf);
+      tokens[a] = 0;
+      for (int32_t k = pos; k < pos + size; ++k) tokens[a] += plen[v[k].idx];
+      pos += size;
+    }
+    rc = placement_penalty(pen, n, times, tokens, gpus, &tp[n - n_min]);
+  }
+  if (!rc)
+    rc = orc_scale(pred, plen, id_rank, count, p, g, n_min, n_max, lambda, gpus, tp, n_star,
+                   t_total, t_pen_out, cost, t_norm, c_norm, score, order, actor_times);
+  free(v); free(scratch); free(suf); free(tp); free(times); free(tokens);
+  return rc;
+}
+
 typedef struct {
   const double* pred; const int32_t* plen; int32_t s0, s1, count;
   const rs_profile* p; int32_t g, n_min, n_max; double lambda; int32_t gpus;

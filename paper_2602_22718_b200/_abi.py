@@ -47,7 +47,23 @@ class RsSweepOut(C.Structure):
     ]
 
 
+class RsTopology(C.Structure):
+    _fields_ = [
+        ("n_nodes", i32), ("node_gpus", P_i32),
+        ("intra_node_bw", f64), ("inter_node_bw", f64), ("bw_matrix", P_f64),
+        ("learner_node", i32), ("n_learner_gpus", i32), ("learner_gpus", P_i32),
+    ]
+
+
+class RsPlacementPenalty(C.Structure):
+    _fields_ = [
+        ("topology", C.POINTER(RsTopology)), ("model_bytes", f64),
+        ("kv_bytes_per_token", f64), ("l_prefill_seconds", f64),
+    ]
+
+
 P_prof = C.POINTER(RsProfile)
+P_pen = C.POINTER(RsPlacementPenalty)
 
 # name -> argtypes (without the leading ctx for rs_* compute calls)
 PRODUCT_SIGS = {
@@ -85,6 +101,8 @@ PRODUCT_SIGS = {
     "rs_estimate_cost": ([vp, P_i32, P_f64, P_i32, P_i32, i32, P_prof, i32, P_f64, P_f64], C.c_int),
     "rs_scale": ([vp, P_f64, P_i32, P_i32, i32, P_prof, i32, i32, i32, f64, i32, P_f64,
                   C.POINTER(RsScaleOut)], C.c_int),
+    "rs_scale_placed": ([vp, P_f64, P_i32, P_i32, i32, P_prof, i32, i32, i32, f64, i32, P_pen,
+                         C.POINTER(RsScaleOut)], C.c_int),
     "rs_scale_select": ([vp, P_f64, P_f64, P_f64, i32, i32, f64, P_f64, P_f64, P_f64, P_i32], C.c_int),
     "rs_generate_scenarios": ([vp, C.POINTER(RsScenarioSpec), vp, vp, C.c_int], C.c_int),
     "rs_sweep": ([vp, C.POINTER(RsScenarioSpec), P_prof, i32, i32, i32, f64, i32,
@@ -111,6 +129,8 @@ ORACLE_SIGS = {
                P_f64, P_f64, P_f64, P_f64, P_f64, P_f64, P_i32, P_f64], C.c_int),
     "sweep_arrays": ([P_f64, P_i32, i32, i32, P_prof, i32, i32, i32, f64, i32, i32,
                       P_f64, P_f64, P_i32], C.c_int),
+    "scale_placed": ([P_f64, P_i32, P_i32, i32, P_prof, i32, i32, i32, f64, i32, P_pen, P_i32,
+                      P_f64, P_f64, P_f64, P_f64, P_f64, P_f64, P_i32, P_f64], C.c_int),
 }
 
 PORT_ONLY_SIGS = {

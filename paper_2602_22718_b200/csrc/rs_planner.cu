@@ -29,6 +29,7 @@
 
 #include "rs_scenario_tables.h"
 #include "rs_fast.cuh"
+#include "rs_placement.cuh"
 #include "rs_sort.cuh"
 
 namespace rs {
@@ -581,6 +582,7 @@ struct Built {
   SSBuffers gss{};
   SSView gview{};
   const int32_t* order_r() const { return fast ? fss.order_r : gss.order_r; }
+  const int32_t* plen_r() const { return fast ? fss.plen_r : gss.plen_r; }
 };
 
 static size_t built_bytes(int64_t n, int S, bool with_generic) {
@@ -1011,20 +1013,35 @@ int rs_sweep_select(const double* sum_t, const double* sum_c, int64_t n_scenario
   return RS_OK;
 }
 
-int rs_scale(rs_ctx* ctx, const double* pred, const int32_t* plen, const int32_t* id_rank,
-             int32_t count, const rs_profile* profile, int32_t G, int32_t n_min,
-             int32_t n_max, double lambda, int32_t gpus, const double* t_penalty,
-             rs_scale_out* out) {
+// scale() with either a caller-provided penalty array (t_penalty) or the
+// device placement penalty (pen), or neither.
+static int scale_impl(rs_ctx* ctx, const double* pred, const int32_t* plen,
+                      const int32_t* id_rank, int32_t count, const rs_profile* profile, int32_t G,
+                      int32_t n_min, int32_t n_max, double lambda, int32_t gpus,
+                      const double* t_penalty, const rs_placement_penalty* pen,
+                      rs_scale_out* out) {
   if (!ctx || !out) return fail(RS_E_ARG, "NULL argument");
   RS_TRY(check_scale_args(count, G, n_min, n_max, lambda));
   if (!pred || !plen) return fail(RS_E_ARG, "NULL argument");
+  PlacementSlots slots;
+  if (pen) {
+    // the penalty runs inside scale's candidate loop: topology / transfer
+    // errors first, then the first candidate whose actors do not fit
+    RS_TRY(placement_slots(pen, gpus, n_max, &slots));
+    if (slots.n_placeable < n_max)
+      return fail(RS_E_PLACEMENT,
+                  "cannot place actor: candidate N=" + std::to_string(std::max(n_min, slots.n_placeable + 1)) +
+                      " needs " + std::to_string(gpus) + " GPUs on one node per actor, the cluster hosts " +
+                      std::to_string(slots.n_placeable) + " such actors");
+  }
   DevProfile dp;
   RS_TRY(get_profile(ctx, profile, &dp));
   const int C = n_max - n_min + 1;
   const int64_t T = groups_per_scenario(n_min, n_max);
   std::vector<int64_t> off = {0, count};
   SetRun run;
-  size_t extra = abytes(T, 8) + abytes(C, 8) * 7 + abytes(count, 4) + abytes(C, 8) + 4096;
+  size_t extra = abytes(T, 8) + abytes(C, 8) * 7 + abytes(count, 4) + abytes(C, 8) + 4096 +
+                 (pen ? placement_bytes(count, n_max) : 0);
   RS_TRY(prepare_sets(ctx, pred, plen, id_rank, off, 1, &dp, G, extra, &run));
   double* gt = arena_alloc<double>(ctx, T);
   double* tt = arena_alloc<double>(ctx, C);
@@ -1040,8 +1057,11 @@ int rs_scale(rs_ctx* ctx, const double* pred, const int32_t* plen, const int32_t
   if (t_penalty) RS_TRY(h2d(ctx, tp, t_penalty, 8 * C));
   RS_TRY(eval_batch(ctx, run.built, 1, dp, n_min, n_max, G, gt));
   RS_TRY(reduce_batch(ctx, run.built, 1, n_min, n_max, G, dp.rho, gpus, gt, tt, cc, idle));
+  if (pen)
+    RS_TRY(placement_penalties(ctx, gt, run.built.plen_r(), count, n_min, n_max, slots, pen, tp));
+  const bool with_pen = t_penalty || pen;
   RS_LAUNCH(ctx, "select", select_kernel, 1, 32, 0, 1, C, n_min, lambda, tt,
-            t_penalty ? tp : (const double*)nullptr, cc, tn, cn, sc, ns);
+            with_pen ? tp : (const double*)nullptr, cc, tn, cn, sc, ns);
   RS_LAUNCH(ctx, "map_order", map_order_kernel, grid_for(ctx, count, 256), 256, 0,
             run.built.order_r(), run.orig, (int64_t)count, order);
   RS_TRY(d2h(ctx, &out->n_star, ns, 4));
@@ -1053,8 +1073,9 @@ int rs_scale(rs_ctx* ctx, const double* pred, const int32_t* plen, const int32_t
   if (out->idle_slot_ticks) RS_TRY(d2h(ctx, out->idle_slot_ticks, idle, 8 * C));
   if (out->order) RS_TRY(d2h(ctx, out->order, order, 4 * count));
   if (out->group_times) RS_TRY(d2h(ctx, out->group_times, gt, 8 * T));
+  if (out->t_penalty && pen) RS_TRY(d2h(ctx, out->t_penalty, tp, 8 * C));
   RS_TRY(sync_and_check(ctx));
-  if (out->t_penalty)
+  if (out->t_penalty && !pen)
     for (int i = 0; i < C; ++i) out->t_penalty[i] = t_penalty ? t_penalty[i] : 0.0;
   if (out->actor_times) {
     int n = out->n_star;
@@ -1062,6 +1083,23 @@ int rs_scale(rs_ctx* ctx, const double* pred, const int32_t* plen, const int32_t
     RS_CUDA_TRY(cudaMemcpy(out->actor_times, gt + base, 8 * n, cudaMemcpyDeviceToHost));
   }
   return RS_OK;
+}
+
+int rs_scale(rs_ctx* ctx, const double* pred, const int32_t* plen, const int32_t* id_rank,
+             int32_t count, const rs_profile* profile, int32_t G, int32_t n_min,
+             int32_t n_max, double lambda, int32_t gpus, const double* t_penalty,
+             rs_scale_out* out) {
+  return scale_impl(ctx, pred, plen, id_rank, count, profile, G, n_min, n_max, lambda, gpus,
+                    t_penalty, nullptr, out);
+}
+
+int rs_scale_placed(rs_ctx* ctx, const double* pred, const int32_t* plen,
+                    const int32_t* id_rank, int32_t count, const rs_profile* profile, int32_t G,
+                    int32_t n_min, int32_t n_max, double lambda, int32_t gpus,
+                    const rs_placement_penalty* penalty, rs_scale_out* out) {
+  if (!penalty) return fail(RS_E_ARG, "NULL placement penalty");
+  return scale_impl(ctx, pred, plen, id_rank, count, profile, G, n_min, n_max, lambda, gpus,
+                    nullptr, penalty, out);
 }
 
 int rs_scale_select(rs_ctx* ctx, const double* t_total, const double* t_penalty,

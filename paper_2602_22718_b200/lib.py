@@ -18,7 +18,7 @@ PKG_DIR = pathlib.Path(__file__).resolve().parent
 REPO = PKG_DIR.parent
 LIB_PATH = PKG_DIR / "librs_b200.so"
 
-RS_OK, RS_E_VALIDATION, RS_E_CONFIG, RS_E_CUDA, RS_E_NOMEM, RS_E_ARG = range(6)
+RS_OK, RS_E_VALIDATION, RS_E_CONFIG, RS_E_CUDA, RS_E_NOMEM, RS_E_ARG, RS_E_PLACEMENT = range(7)
 
 
 class Error(RuntimeError):
@@ -31,6 +31,10 @@ class ConfigError(Error):
 
 class ValidationError(Error):
     """rollsim::ValidationError (errors.hpp:29-32)."""
+
+
+class PlacementError(Error):
+    """rollsim::PlacementError (errors.hpp:35-38)."""
 
 
 class DeviceError(Error):
@@ -68,6 +72,8 @@ def check(status):
         raise ValidationError(msg)
     if status == RS_E_CONFIG:
         raise ConfigError(msg)
+    if status == RS_E_PLACEMENT:
+        raise PlacementError(msg)
     raise DeviceError(f"rs status {status}: {msg}")
 
 

@@ -14,11 +14,12 @@ from typing import Callable, List, Optional, Sequence
 import numpy as np
 
 from . import _abi
-from .lib import (ConfigError, DeviceError, Error, ValidationError, as_f64, as_i32,
-                  as_i64, check, context, profile_struct, ptr)
+from .lib import (ConfigError, DeviceError, Error, PlacementError, ValidationError, as_f64,
+                  as_i32, as_i64, check, context, profile_struct, ptr)
 
 __all__ = [
-    "Error", "ConfigError", "ValidationError", "DeviceError",
+    "Error", "ConfigError", "ValidationError", "PlacementError", "DeviceError",
+    "ClusterTopology", "default_topology", "PlacementPenalty",
     "LatencyProfile", "default_profile", "Prompt", "PrefixIndex", "PrefillCapacity",
     "PrefixSelection", "DedupSavings", "select_prefix_length", "dedup_savings",
     "unique_prefix_count_among", "dedup_map", "block_hashes", "PredictedPrompt",
@@ -371,11 +372,61 @@ def estimate_cost(groups: Sequence[ActorGroup], profile: LatencyProfile, respons
 TimePenaltyFn = Callable[[int, List[ActorGroup], List[float]], float]
 
 
+# ---------------------------------------------------------------- placement
+@dataclass
+class ClusterTopology:
+    """ClusterTopology (proj/include/rollsim/placement.hpp:14-38): GPUs per
+    node, two-tier bandwidths (or a full symmetric matrix), learner node and
+    its local GPUs. Validated by the library like ClusterTopology::validate."""
+    node_gpus: List[int]
+    intra_node_bw: float = 2.5e10
+    inter_node_bw: float = 3.0e9
+    bw_matrix: Optional[List[List[float]]] = None
+    learner_node: int = 0
+    learner_gpus: List[int] = field(default_factory=lambda: [0, 1, 2, 3])
+
+    def struct(self):
+        ng = as_i32(self.node_gpus if self.node_gpus else [0])
+        lg = as_i32(self.learner_gpus if self.learner_gpus else [0])
+        bw = as_f64(np.asarray(self.bw_matrix, np.float64).ravel()) if self.bw_matrix else None
+        t = _abi.RsTopology(len(self.node_gpus), ptr(ng, C.c_int32), float(self.intra_node_bw),
+                            float(self.inter_node_bw), ptr(bw, C.c_double) if bw is not None else None,
+                            int(self.learner_node), len(self.learner_gpus), ptr(lg, C.c_int32))
+        return t, (ng, lg, bw)
+
+
+def default_topology(node_count=2, gpus_per_node=8, learner_gpu_count=4) -> ClusterTopology:
+    """default_topology (placement.cpp:118-128)."""
+    return ClusterTopology(node_gpus=[gpus_per_node] * node_count,
+                           learner_gpus=list(range(min(learner_gpu_count, gpus_per_node))))
+
+
+@dataclass
+class PlacementPenalty:
+    """The TimePenaltyFn plan_rlhfless builds (proj/src/training.cpp:150-164):
+    place each candidate on `topology` (placement.cpp:177-291) and charge the
+    worst exposed transfer (check_overlap, placement.cpp:339-363), with
+    kv bytes = kv_bytes_per_token x the group's prompt tokens
+    (transfers_for, training.cpp:68-80). Passed as scale()'s `penalty`, it
+    runs on the device for every candidate (rs_scale_placed)."""
+    topology: ClusterTopology
+    l_prefill_seconds: float
+    model_bytes: float = 6e9
+    kv_bytes_per_token: float = 36864.0
+
+    def struct(self):
+        t, keep = self.topology.struct()
+        p = _abi.RsPlacementPenalty(C.pointer(t), float(self.model_bytes),
+                                    float(self.kv_bytes_per_token), float(self.l_prefill_seconds))
+        return p, (t, keep)
+
+
 def scale(predicted: Sequence[PredictedPrompt], profile: LatencyProfile, responses_per_prompt,
-          n_min, n_max, lambda_, gpus_per_actor, penalty: Optional[TimePenaltyFn] = None):
+          n_min, n_max, lambda_, gpus_per_actor, penalty=None):
     """scale (proj/src/planner.cpp:159-218). A Python `penalty` is called per
     candidate in ascending N with that candidate's groups and times, like
-    TimePenaltyFn (planner.hpp:80-82)."""
+    TimePenaltyFn (planner.hpp:80-82); a `PlacementPenalty` is evaluated on
+    the device instead (rs_scale_placed)."""
     ctx = context()
     P = len(predicted)
     if P:
@@ -393,13 +444,20 @@ def scale(predicted: Sequence[PredictedPrompt], profile: LatencyProfile, respons
     out = _abi.RsScaleOut(0, *[ptr(arr[k], C.c_double) for k in
                                ("t_total", "t_penalty", "cost", "t_norm", "c_norm", "score")],
                           ptr(idle, C.c_int64), ptr(order, C.c_int32), ptr(at, C.c_double),
-                          ptr(gt, C.c_double) if penalty else None)
+                          ptr(gt, C.c_double) if callable(penalty) else None)
     s, keep = profile.struct()
-    check(ctx.lib.rs_scale(ctx.handle, ptr(pred, C.c_double), ptr(plen, C.c_int32),
-                           ptr(rank, C.c_int32), P, C.byref(s), responses_per_prompt, n_min,
-                           n_max, float(lambda_), gpus_per_actor, None, C.byref(out)))
+    if isinstance(penalty, PlacementPenalty):
+        pp, keep_p = penalty.struct()
+        check(ctx.lib.rs_scale_placed(ctx.handle, ptr(pred, C.c_double), ptr(plen, C.c_int32),
+                                      ptr(rank, C.c_int32), P, C.byref(s), responses_per_prompt,
+                                      n_min, n_max, float(lambda_), gpus_per_actor, C.byref(pp),
+                                      C.byref(out)))
+    else:
+        check(ctx.lib.rs_scale(ctx.handle, ptr(pred, C.c_double), ptr(plen, C.c_int32),
+                               ptr(rank, C.c_int32), P, C.byref(s), responses_per_prompt, n_min,
+                               n_max, float(lambda_), gpus_per_actor, None, C.byref(out)))
     n_star = out.n_star
-    if penalty is not None:
+    if callable(penalty) and not isinstance(penalty, PlacementPenalty):
         pen = np.zeros(Cn, np.float64)
         base = 0
         for i, n in enumerate(range(n_min, n_max + 1)):

@@ -96,3 +96,27 @@ def c2_tokens(n_prompts=65536, shared=2048, unique=512, vocab=32000, seed=1):
     tok[:, shared:] = uniq
     off = np.arange(n_prompts + 1, dtype=np.int64) * (shared + unique)
     return tok.reshape(-1), off
+
+
+def placement_cases():
+    """(penalty, gpus_per_actor, capacity) triples covering the placement
+    rules of proj/src/placement.cpp:177-291: learner-node co-location, node
+    ranking by bandwidth (ties by index), a bandwidth matrix, a learner node
+    too small to host the heaviest actor, heterogeneous nodes, and penalties
+    dominated by model sync or by KV shipping. capacity = actors that fit."""
+    from paper_2602_22718_b200.rollsim import ClusterTopology, PlacementPenalty, default_topology
+    bw3 = [[4e10, 1e10, 5e9], [1e10, 4e10, 1e10], [5e9, 1e10, 4e10]]
+    return [
+        (PlacementPenalty(default_topology(2, 8, 4), l_prefill_seconds=0.5, model_bytes=6e10), 2, 8),
+        (PlacementPenalty(default_topology(4, 8, 4), l_prefill_seconds=0.05, model_bytes=1e9), 2, 16),
+        (PlacementPenalty(ClusterTopology([8, 8, 8], bw_matrix=bw3, learner_node=2,
+                                          learner_gpus=[1, 3]), l_prefill_seconds=0.2,
+                          model_bytes=3e11), 2, 12),
+        (PlacementPenalty(ClusterTopology([1, 4, 4], learner_gpus=[0]), l_prefill_seconds=0.1,
+                          model_bytes=4e10), 2, 4),
+        (PlacementPenalty(ClusterTopology([4, 6, 2, 8], learner_node=2, learner_gpus=[0, 1]),
+                          l_prefill_seconds=1.0, kv_bytes_per_token=4e6), 2, 10),
+        (PlacementPenalty(ClusterTopology([3, 5, 7], intra_node_bw=1e10, inter_node_bw=1e10,
+                                          learner_node=1, learner_gpus=[4]),
+                          l_prefill_seconds=0.0, model_bytes=1e11), 1, 15),
+    ]

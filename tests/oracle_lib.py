@@ -143,6 +143,28 @@ class Oracle:
         out.update(n_star=ns.value, order=order[:len(pred)], actor_times=at[:ns.value])
         return out
 
+    def scale_placed(self, pred, plen, id_rank, prof, g, n_min, n_max, lam, gpus, placement):
+        """scale() with plan_rlhfless's placement penalty (a PlacementPenalty)."""
+        pred, plen = as_f64(pred), as_i32(plen)
+        rank = as_i32(id_rank) if id_rank is not None else None
+        Cn = max(n_max - n_min + 1, 1)
+        arrs = [np.zeros(Cn, np.float64) for _ in range(6)]
+        order = np.zeros(max(len(pred), 1), np.int32)
+        at = np.zeros(max(n_max, 1), np.float64)
+        ns = C.c_int32()
+        s, keep = prof.struct()
+        pp, keep_p = placement.struct()
+        self._chk(self.fn("scale_placed")(ptr(pred, C.c_double), ptr(plen, C.c_int32),
+                                          ptr(rank, C.c_int32) if rank is not None else None,
+                                          len(pred), C.byref(s), g, n_min, n_max, float(lam), gpus,
+                                          C.byref(pp), C.byref(ns),
+                                          *[ptr(a, C.c_double) for a in arrs],
+                                          ptr(order, C.c_int32), ptr(at, C.c_double)))
+        keys = ("t_total", "t_penalty", "cost", "t_norm", "c_norm", "score")
+        out = dict(zip(keys, arrs))
+        out.update(n_star=ns.value, order=order[:len(pred)], actor_times=at[:ns.value])
+        return out
+
     def sweep_arrays(self, pred, plen, S, P, prof, g, n_min, n_max, lam, gpus, threads=1):
         pred, plen = as_f64(pred), as_i32(plen)
         Cn = n_max - n_min + 1

@@ -193,3 +193,44 @@ def test_port_matches_reference_c3_sized():
     assert a["n_star"] == b["n_star"]
     assert np.array_equal(bits(a["t_total"]), bits(b["t_total"]))
     assert np.array_equal(bits(a["cost"]), bits(b["cost"]))
+
+
+@needs_ref
+def test_port_matches_reference_placement_penalty():
+    """scale() with plan_rlhfless's placement penalty: the C restatement
+    against the reference's own place() / check_overlap(), bitwise."""
+    from cases import placement_cases
+    rng = Rng(515)
+    for ci, (pen, gpus, cap) in enumerate(placement_cases()):
+        for trial in range(6):
+            count = rng.uniform_int(cap, 60)
+            pred, plen = random_predicted(rng, count, 1.0, 900.0, 1, 900, integer=trial % 2 == 0)
+            rank = np.random.RandomState(trial).permutation(count).astype(np.int32)
+            prof = [default_profile(), small_profile()][trial % 2]
+            n_max = min(cap, count)
+            a = port().scale_placed(pred, plen, rank, prof, 4, 1, n_max, 0.6, gpus, pen)
+            b = ref().scale_placed(pred, plen, rank, prof, 4, 1, n_max, 0.6, gpus, pen)
+            assert a["n_star"] == b["n_star"], (ci, trial)
+            for k in ("t_total", "t_penalty", "cost", "t_norm", "c_norm", "score"):
+                assert np.array_equal(bits(a[k]), bits(b[k])), (ci, trial, k)
+            assert a["order"].tolist() == b["order"].tolist()
+
+
+@needs_ref
+def test_placement_penalty_errors_match_reference():
+    from cases import placement_cases
+    from paper_2602_22718_b200.rollsim import ClusterTopology, PlacementPenalty
+    pen, gpus, cap = placement_cases()[0]
+    pred, plen = random_predicted(Rng(3), 40)
+    for o in (port(), ref()):
+        with pytest.raises(OracleError) as e:  # more actors than the cluster hosts
+            o.scale_placed(pred, plen, None, default_profile(), 2, 1, cap + 1, 0.5, gpus, pen)
+        assert e.value.status == 6
+        bad = PlacementPenalty(ClusterTopology([8, 8], intra_node_bw=1e9, inter_node_bw=2e9),
+                               l_prefill_seconds=0.1)
+        with pytest.raises(OracleError) as e:
+            o.scale_placed(pred, plen, None, default_profile(), 2, 1, 4, 0.5, gpus, bad)
+        assert e.value.status == 2
+        with pytest.raises(OracleError) as e:  # scale's own checks come first
+            o.scale_placed(pred, plen, None, default_profile(), 2, 1, 41, 0.5, gpus, bad)
+        assert e.value.status == 1
