@@ -49,9 +49,15 @@ CXXREF    := g++ -std=c++20 -O3 -DNDEBUG -Wall -Wextra -fPIC -I$(REF)/include \
 SUITES    := acceptance_main test_dedup test_planner test_profile test_training
 
 .PHONY: shim
-shim: $(foreach t,$(SUITES),$(SHIM_OUT)/$(t)_b200 $(SHIM_OUT)/$(t)_ref)
+shim: $(foreach t,$(SUITES),$(SHIM_OUT)/$(t)_b200 $(SHIM_OUT)/$(t)_ref) \
+      $(SHIM_OUT)/test_placement_b200
 
-$(SHIM_OUT)/%.o: $(PKG)/shim/%.cpp $(PKG)/shim/rs_shim.hpp include/rs.h
+# drop-in extension suite (rollsim_b200.hpp) against the stock penalty path
+$(SHIM_OUT)/test_placement_b200: $(PKG)/shim/tests/test_placement_b200.cpp $(SHIM_OUT)/librollsim_b200.a $(LIB)
+	$(CXXREF) -I$(PKG)/shim -I$(PKG)/shim/doctest $< -o $@ $(SHIM_OUT)/librollsim_b200.a \
+	    -L$(PKG) -lrs_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -lpthread
+
+$(SHIM_OUT)/%.o: $(PKG)/shim/%.cpp $(PKG)/shim/rs_shim.hpp $(PKG)/shim/rollsim_b200.hpp include/rs.h
 	@mkdir -p $(SHIM_OUT)
 	$(CXXREF) -c $< -o $@
 

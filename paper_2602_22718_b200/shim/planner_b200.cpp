@@ -4,10 +4,13 @@
 // top of librs_b200: assign, integrate_decode_seconds, estimate_actor_time,
 // estimate_cost and scale run on the GPU; this file marshals the reference's
 // AoS types (strings, vectors) into the C-ABI's SoA arrays and back.
+#include <cmath>
+
 #include <nlohmann/json.hpp>
 
 #include "rollsim/errors.hpp"
 #include "rollsim/planner.hpp"
+#include "rollsim_b200.hpp"
 #include "rs_shim.hpp"
 
 namespace rollsim {
@@ -125,10 +128,17 @@ double estimate_cost(const std::vector<ActorGroup>& groups, const LatencyProfile
   return cost;
 }
 
-ScaleResult scale(const std::vector<PredictedPrompt>& predicted, const LatencyProfile& profile,
-                  int responses_per_prompt, int n_min, int n_max, double lambda,
-                  int gpus_per_actor, const TimePenaltyFn& penalty) {
+namespace {
+
+// scale() over the C-ABI. The penalty is either a host TimePenaltyFn (called
+// per candidate in ascending N, planner.hpp:80-82) or the device placement
+// penalty (rs_scale_placed); at most one is set.
+ScaleResult run_scale(const std::vector<PredictedPrompt>& predicted, const LatencyProfile& profile,
+                      int responses_per_prompt, int n_min, int n_max, double lambda,
+                      int gpus_per_actor, const TimePenaltyFn* penalty,
+                      const rs_placement_penalty* placed) {
   const int P = static_cast<int>(predicted.size());
+  const bool callback = penalty && *penalty;
   SoA s = to_soa(predicted);
   if (s.pred.empty()) {  // the C-ABI still reports the reference's error
     s.pred.push_back(1.0);
@@ -141,7 +151,7 @@ ScaleResult scale(const std::vector<PredictedPrompt>& predicted, const LatencyPr
   std::vector<double> t_total(C), t_pen(C), cost(C), t_norm(C), c_norm(C), score(C);
   std::vector<int32_t> order(std::max(P, 1));
   std::vector<double> actor_times(std::max(n_max, 1));
-  std::vector<double> group_times(penalty ? T : 0);
+  std::vector<double> group_times(callback ? T : 0);
   rs_scale_out out{};
   out.t_total = t_total.data();
   out.t_penalty = t_pen.data();
@@ -151,20 +161,23 @@ ScaleResult scale(const std::vector<PredictedPrompt>& predicted, const LatencyPr
   out.score = score.data();
   out.order = order.data();
   out.actor_times = actor_times.data();
-  out.group_times = penalty ? group_times.data() : nullptr;
+  out.group_times = callback ? group_times.data() : nullptr;
   rs_shim::Profile prof(profile);
-  rs_shim::check(rs_scale(rs_shim::ctx(), s.pred.data(), s.plen.data(), s.rank.data(), P,
-                          &prof.p, responses_per_prompt, n_min, n_max, lambda, gpus_per_actor,
-                          nullptr, &out));
+  if (placed)
+    rs_shim::check(rs_scale_placed(rs_shim::ctx(), s.pred.data(), s.plen.data(), s.rank.data(), P,
+                                   &prof.p, responses_per_prompt, n_min, n_max, lambda,
+                                   gpus_per_actor, placed, &out));
+  else
+    rs_shim::check(rs_scale(rs_shim::ctx(), s.pred.data(), s.plen.data(), s.rank.data(), P,
+                            &prof.p, responses_per_prompt, n_min, n_max, lambda, gpus_per_actor,
+                            nullptr, &out));
   int n_star = out.n_star;
-  if (penalty) {
-    // TimePenaltyFn is a host callback (planner.hpp:80-82): called per
-    // candidate in ascending N with that candidate's groups and times.
+  if (callback) {
     int64_t base = 0;
     for (int n = n_min; n <= n_max; ++n) {
       std::vector<ActorGroup> g = groups_from_order(predicted, order.data(), n, gpus_per_actor);
       std::vector<double> times(group_times.begin() + base, group_times.begin() + base + n);
-      t_pen[n - n_min] = penalty(n, g, times);
+      t_pen[n - n_min] = (*penalty)(n, g, times);
       base += n;
     }
     rs_shim::check(rs_scale_select(rs_shim::ctx(), t_total.data(), t_pen.data(), cost.data(), C,
@@ -191,6 +204,51 @@ ScaleResult scale(const std::vector<PredictedPrompt>& predicted, const LatencyPr
   r.actor_times.assign(actor_times.begin(), actor_times.begin() + n_star);
   return r;
 }
+
+}  // namespace
+
+ScaleResult scale(const std::vector<PredictedPrompt>& predicted, const LatencyProfile& profile,
+                  int responses_per_prompt, int n_min, int n_max, double lambda,
+                  int gpus_per_actor, const TimePenaltyFn& penalty) {
+  return run_scale(predicted, profile, responses_per_prompt, n_min, n_max, lambda, gpus_per_actor,
+                   &penalty, nullptr);
+}
+
+namespace b200 {
+
+ScaleResult scale_placed(const std::vector<PredictedPrompt>& predicted,
+                         const LatencyProfile& profile, int responses_per_prompt, int n_min,
+                         int n_max, double lambda, int gpus_per_actor,
+                         const ClusterTopology& topo, double model_bytes,
+                         double kv_bytes_per_token, double l_prefill_seconds) {
+  std::vector<int32_t> node_gpus;
+  for (const ClusterTopology::Node& n : topo.nodes) node_gpus.push_back(n.gpu_count);
+  std::vector<double> bw;
+  bool ragged = topo.bw_matrix.size() != node_gpus.size();
+  for (const auto& row : topo.bw_matrix) {
+    ragged = ragged || row.size() != node_gpus.size();
+    bw.insert(bw.end(), row.begin(), row.end());
+  }
+  // A ragged matrix is a ConfigError raised after scale's own checks, like
+  // ClusterTopology::validate inside the penalty; NaN entries make the
+  // library's validation report it at that point.
+  if (!topo.bw_matrix.empty() && ragged)
+    bw.assign(node_gpus.size() * node_gpus.size(), std::nan(""));
+  rs_topology t{};
+  t.n_nodes = static_cast<int32_t>(node_gpus.size());
+  t.node_gpus = node_gpus.data();
+  t.intra_node_bw = topo.intra_node_bw;
+  t.inter_node_bw = topo.inter_node_bw;
+  t.bw_matrix = bw.empty() ? nullptr : bw.data();
+  t.learner_node = topo.learner_node;
+  t.n_learner_gpus = static_cast<int32_t>(topo.learner_gpus.size());
+  t.learner_gpus = topo.learner_gpus.data();
+  rs_placement_penalty pen{&t, model_bytes, kv_bytes_per_token, l_prefill_seconds};
+  return run_scale(predicted, profile, responses_per_prompt, n_min, n_max, lambda, gpus_per_actor,
+                   nullptr, &pen);
+}
+
+}  // namespace b200
 
 nlohmann::json GenerationPlan::to_json() const {
   using nlohmann::json;

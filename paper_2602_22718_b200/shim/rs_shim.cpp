@@ -42,6 +42,7 @@ void check(int status) {
   std::string msg = rs_last_error();
   if (status == RS_E_VALIDATION) throw rollsim::ValidationError(msg);
   if (status == RS_E_CONFIG) throw rollsim::ConfigError(msg);
+  if (status == RS_E_PLACEMENT) throw rollsim::PlacementError(msg);
   throw rollsim::Error("librs_b200: " + msg);
 }
 

@@ -53,3 +53,11 @@ def test_reference_suite_on_dropin(suite):
 def test_acceptance_on_dropin():
     code, out = run(SHIM / "acceptance_main_b200")
     assert out.count("[PASS]") == 10, out[-3000:]
+
+
+@pytest.mark.gpu
+def test_placement_extension_on_dropin():
+    """rollsim::b200::scale_placed (rollsim_b200.hpp) against scale() with
+    plan_rlhfless's stock penalty lambda, bitwise (shim/tests/)."""
+    code, out = run(SHIM / "test_placement_b200")
+    assert "test cases:" in out and code == 0 and not failed_cases(out), out[-3000:]
