@@ -284,6 +284,31 @@ int rs_scale_select(rs_ctx* ctx, const double* t_total, const double* t_penalty,
                     double* score, int32_t* n_star);
 
 /* ------------------------------------------------------------------ */
+/* (3c) Prediction snapshot                             */
+/* ------------------------------------------------------------------ */
+/* NoiseModel (predictor.hpp:18-27). kind 0 = identity, 1 = bucket. */
+typedef struct rs_noise_model {
+  int32_t kind;
+  double bucket_accuracy;
+  int32_t bucket_width;
+  uint64_t seed;
+} rs_noise_model;
+
+/* LengthHistory::predict / predict_noisy (predictor.cpp:52-98) for a batch of
+ * prompts, i.e. snapshot_predictions (training.cpp:53-66):
+ *   obs[i * window + k], k < depth[i]: prompt i's retained per-step means,
+ *   oldest first (depth 0 = never observed: ground_truth_len[i] is used);
+ *   noise NULL or kind 0 = predict(); kind 1 needs the prompt ids as CSR
+ *   bytes (id_bytes, id_offsets[count+1]) for its fnv1a-keyed stream.
+ * device_ptrs != 0: every array, out included, is device memory (the result
+ * can feed rs_sweep_arrays directly). out[i] = the prediction. */
+int rs_predict_lengths(rs_ctx* ctx, const double* obs, const int32_t* depth,
+                       const int32_t* ground_truth_len, int32_t count, int32_t window,
+                       double alpha, int32_t max_response_len, const rs_noise_model* noise,
+                       const char* id_bytes, const int64_t* id_offsets, int device_ptrs,
+                       double* out);
+
+/* ------------------------------------------------------------------ */
 /* Monte-Carlo scaling sweep: scale() for every        */
 /* scenario x candidate, scenarios generated on the device.            */
 /* ------------------------------------------------------------------ */

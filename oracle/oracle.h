@@ -81,7 +81,14 @@ extern "C" {
                            const rs_placement_penalty* pen, int32_t* n_star,   \
                            double* t_total, double* t_pen_out, double* cost,   \
                            double* t_norm, double* c_norm, double* score,      \
-                           int32_t* order, double* actor_times);
+                           int32_t* order, double* actor_times);         \
+  /* LengthHistory::predict / predict_noisy per prompt (predictor.cpp:52-98) */\
+  int prefix##predict_lengths(const double* obs, const int32_t* depth,         \
+                              const int32_t* gt, int32_t count,                \
+                              int32_t window, double alpha, int32_t max_len,   \
+                              const rs_noise_model* noise,                     \
+                              const char* id_bytes, const int64_t* id_offsets, \
+                              double* out);
 
 ORACLE_API(ref_)
 ORACLE_API(orc_)

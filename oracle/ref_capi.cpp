@@ -18,7 +18,10 @@
 #include "oracle.h"
 #include "rollsim/dedup.hpp"
 #include "rollsim/errors.hpp"
+#include <nlohmann/json.hpp>
+
 #include "rollsim/placement.hpp"
+#include "rollsim/predictor.hpp"
 #include "rollsim/planner.hpp"
 #include "rollsim/profile.hpp"
 #include "rollsim/workload.hpp"
@@ -342,6 +345,45 @@ int ref_scale_placed(const double* pred, const int32_t* plen, const int32_t* id_
           int32_t rk = std::stoi(id.substr(1));
           order[pos++] = id_rank ? by_rank[rk] : rk;
         }
+    }
+  });
+}
+
+// The reference's own LengthHistory, loaded with the same observations
+// (LengthHistory::from_json, predictor.cpp:120-133).
+int ref_predict_lengths(const double* obs, const int32_t* depth, const int32_t* gt,
+                        int32_t count, int32_t window, double alpha, int32_t max_len,
+                        const rs_noise_model* noise, const char* id_bytes,
+                        const int64_t* id_offsets, double* out) {
+  return guarded([&] {
+    rollsim::LengthHistory check(window, alpha, max_len);  // constructor validation
+    (void)check;
+    nlohmann::json j;
+    j["window"] = window;
+    j["alpha"] = alpha;
+    j["max_response_len"] = max_len;
+    nlohmann::json o = nlohmann::json::object();
+    std::vector<std::string> ids(count);
+    for (int32_t i = 0; i < count; ++i) {
+      ids[i] = id_bytes ? std::string(id_bytes + id_offsets[i], id_bytes + id_offsets[i + 1])
+                        : "p" + std::to_string(i);
+      if (depth[i] > 0)
+        o[ids[i]] = std::vector<double>(obs + (size_t)i * window, obs + (size_t)i * window + depth[i]);
+    }
+    j["observations"] = std::move(o);
+    rollsim::LengthHistory h = rollsim::LengthHistory::from_json(j);
+    rollsim::NoiseModel nm;
+    if (noise && noise->kind == 1) {
+      nm.kind = rollsim::NoiseModel::Kind::bucket;
+      nm.bucket_accuracy = noise->bucket_accuracy;
+      nm.bucket_width = noise->bucket_width;
+      nm.seed = noise->seed;
+    }
+    for (int32_t i = 0; i < count; ++i) {
+      rollsim::Prompt p;
+      p.id = ids[i];
+      p.ground_truth_len = gt[i];
+      out[i] = nm.kind == rollsim::NoiseModel::Kind::identity ? h.predict(p) : h.predict_noisy(p, nm);
     }
   });
 }

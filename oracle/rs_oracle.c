@@ -486,6 +486,80 @@ int orc_scale_placed(const double* pred, const int32_t* plen, const int32_t* id_
   return rc;
 }
 
+/* ---- prediction snapshot: LengthHistory::predict / predict_noisy
+ * (predictor.cpp:52-98), splitmix Rng (rng.hpp:14-49), fnv1a (rng.hpp:64-71). */
+static uint64_t ors_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+static uint64_t ors_hash(uint64_t x) {
+  x ^= x >> 33; x *= 0xff51afd7ed558ccdULL; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ULL; x ^= x >> 33;
+  return x;
+}
+static uint64_t ors_combine(uint64_t a, uint64_t b) {
+  return ors_hash(a ^ (b + 0x9e3779b97f4a7c15ULL + (a << 6) + (a >> 2)));
+}
+static uint64_t ors_next(uint64_t* st) { *st += 0x9e3779b97f4a7c15ULL; return ors_mix(*st); }
+static double ors_uniform(uint64_t* st) { return (double)(ors_next(st) >> 11) * 0x1.0p-53; }
+static double clamp_len(double est, double mlen) {                 /* predictor.cpp:64 */
+  double lo = 1.0 < est ? est : 1.0;
+  return lo < mlen ? lo : mlen;
+}
+
+int orc_predict_lengths(const double* obs, const int32_t* depth, const int32_t* gt,
+                        int32_t count, int32_t window, double alpha, int32_t max_len,
+                        const rs_noise_model* noise, const char* id_bytes,
+                        const int64_t* id_offsets, double* out) {
+  if (window < 1) return fail(2, "predictor window must be >= 1");  /* :24-31 */
+  if (!(alpha > 0) || alpha > 1) return fail(2, "predictor alpha must be in (0, 1]");
+  if (max_len < 1) return fail(2, "predictor max_response_len must be >= 1");
+  int noisy = noise && noise->kind != 0;
+  if (noisy) {                                                      /* :17-22 */
+    if (noise->bucket_accuracy < 0 || noise->bucket_accuracy > 1)
+      return fail(2, "noise bucket_accuracy must be in [0, 1]");
+    if (noise->bucket_width < 1 || noise->bucket_width > max_len)
+      return fail(2, "noise bucket_width must be in [1, max_response_len]");
+  }
+  double mlen = (double)max_len;
+  for (int32_t i = 0; i < count; ++i) {
+    double est;
+    if (depth[i] == 0) {
+      est = (double)gt[i];
+    } else {                                                        /* :58-62 */
+      const double* q = obs + (size_t)i * window;
+      est = q[0];
+      for (int32_t k = 1; k < depth[i]; ++k) est = alpha * q[k] + (1.0 - alpha) * est;
+    }
+    double base = clamp_len(est, mlen);
+    out[i] = base;
+    if (!noisy) continue;
+    int32_t bc = (max_len + noise->bucket_width - 1) / noise->bucket_width;   /* :73-75 */
+    if (bc <= 1) continue;
+    uint64_t h = 0xcbf29ce484222325ULL, bits;
+    for (int64_t b = id_offsets[i]; b < id_offsets[i + 1]; ++b) {
+      h ^= (unsigned char)id_bytes[b];
+      h *= 0x100000001b3ULL;
+    }
+    memcpy(&bits, &base, sizeof bits);
+    uint64_t key = ors_combine(noise->seed, h);                     /* :79-84 */
+    key = ors_combine(key, (uint64_t)depth[i]);
+    key = ors_combine(key, bits);
+    uint64_t st = key;
+    if (ors_uniform(&st) < noise->bucket_accuracy) continue;        /* :86 */
+    int32_t tb = (int32_t)((base - 1.0) / noise->bucket_width);
+    if (tb > bc - 1) tb = bc - 1;
+    int32_t wrong = (int32_t)(ors_next(&st) % (uint64_t)(bc - 1));  /* uniform_int(0, bc-2) */
+    if (wrong >= tb) ++wrong;
+    double lo = wrong * noise->bucket_width + 1.0;
+    double hb = (double)((wrong + 1) * noise->bucket_width);
+    double hi = mlen < hb ? mlen : hb;
+    double v = lo + (hi - lo) * ors_uniform(&st);
+    out[i] = clamp_len(v, mlen);
+  }
+  return 0;
+}
+
 typedef struct {
   const double* pred; const int32_t* plen; int32_t s0, s1, count;
   const rs_profile* p; int32_t g, n_min, n_max; double lambda; int32_t gpus;

@@ -62,8 +62,13 @@ class RsPlacementPenalty(C.Structure):
     ]
 
 
+class RsNoiseModel(C.Structure):
+    _fields_ = [("kind", i32), ("bucket_accuracy", f64), ("bucket_width", i32), ("seed", u64)]
+
+
 P_prof = C.POINTER(RsProfile)
 P_pen = C.POINTER(RsPlacementPenalty)
+P_noise = C.POINTER(RsNoiseModel)
 
 # name -> argtypes (without the leading ctx for rs_* compute calls)
 PRODUCT_SIGS = {
@@ -103,6 +108,8 @@ PRODUCT_SIGS = {
                   C.POINTER(RsScaleOut)], C.c_int),
     "rs_scale_placed": ([vp, P_f64, P_i32, P_i32, i32, P_prof, i32, i32, i32, f64, i32, P_pen,
                          C.POINTER(RsScaleOut)], C.c_int),
+    "rs_predict_lengths": ([vp, vp, vp, vp, i32, i32, f64, i32, P_noise, vp, vp, C.c_int, vp],
+                           C.c_int),
     "rs_scale_select": ([vp, P_f64, P_f64, P_f64, i32, i32, f64, P_f64, P_f64, P_f64, P_i32], C.c_int),
     "rs_generate_scenarios": ([vp, C.POINTER(RsScenarioSpec), vp, vp, C.c_int], C.c_int),
     "rs_sweep": ([vp, C.POINTER(RsScenarioSpec), P_prof, i32, i32, i32, f64, i32,
@@ -131,6 +138,8 @@ ORACLE_SIGS = {
                       P_f64, P_f64, P_i32], C.c_int),
     "scale_placed": ([P_f64, P_i32, P_i32, i32, P_prof, i32, i32, i32, f64, i32, P_pen, P_i32,
                       P_f64, P_f64, P_f64, P_f64, P_f64, P_f64, P_i32, P_f64], C.c_int),
+    "predict_lengths": ([P_f64, P_i32, P_i32, i32, i32, f64, i32, P_noise, C.c_char_p, P_i64,
+                         P_f64], C.c_int),
 }
 
 PORT_ONLY_SIGS = {

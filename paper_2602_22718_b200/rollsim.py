@@ -19,7 +19,8 @@ from .lib import (ConfigError, DeviceError, Error, PlacementError, ValidationErr
 
 __all__ = [
     "Error", "ConfigError", "ValidationError", "PlacementError", "DeviceError",
-    "ClusterTopology", "default_topology", "PlacementPenalty",
+    "ClusterTopology", "default_topology", "PlacementPenalty", "NoiseModel", "LengthHistory",
+    "predict_lengths",
     "LatencyProfile", "default_profile", "Prompt", "PrefixIndex", "PrefillCapacity",
     "PrefixSelection", "DedupSavings", "select_prefix_length", "dedup_savings",
     "unique_prefix_count_among", "dedup_map", "block_hashes", "PredictedPrompt",
@@ -370,6 +371,121 @@ def estimate_cost(groups: Sequence[ActorGroup], profile: LatencyProfile, respons
 
 
 TimePenaltyFn = Callable[[int, List[ActorGroup], List[float]], float]
+
+
+# ---------------------------------------------------------------- predictor
+@dataclass
+class NoiseModel:
+    """NoiseModel (proj/include/rollsim/predictor.hpp:18-27)."""
+    kind: str = "identity"  # or "bucket"
+    bucket_accuracy: float = 1.0
+    bucket_width: int = 100
+    seed: int = 0
+
+    def struct(self):
+        return _abi.RsNoiseModel(0 if self.kind == "identity" else 1, float(self.bucket_accuracy),
+                                 int(self.bucket_width), int(self.seed) & (2**64 - 1))
+
+
+def predict_lengths(obs, depth, ground_truth_len, window, alpha, max_response_len,
+                    noise: Optional[NoiseModel] = None, ids=None, device=False):
+    """Batch LengthHistory::predict / predict_noisy on the GPU
+    (rs_predict_lengths). obs: (count, window) oldest-first observation means,
+    depth[i] of them valid. With device=True the arrays are torch CUDA tensors
+    and the result stays on the device (a float64 tensor)."""
+    ctx = context()
+    nm = noise.struct() if noise is not None and noise.kind != "identity" else None
+    if device:
+        import torch
+        n = int(depth.numel())
+        out = torch.empty(n, dtype=torch.float64, device=depth.device)
+        check(ctx.lib.rs_predict_lengths(ctx.handle, obs.data_ptr(), depth.data_ptr(),
+                                         ground_truth_len.data_ptr(), n, window, float(alpha),
+                                         max_response_len, C.byref(nm) if nm else None,
+                                         ids[0].data_ptr() if ids is not None else None,
+                                         ids[1].data_ptr() if ids is not None else None, 1,
+                                         out.data_ptr()))
+        return out
+    depth, gt = as_i32(depth), as_i32(ground_truth_len)
+    n = len(depth)
+    obs = as_f64(np.asarray(obs, np.float64).reshape(-1)) if np.size(obs) else as_f64([0.0])
+    out = np.zeros(max(n, 1), np.float64)
+    blob = off = None
+    if ids is not None:
+        enc = [s.encode() for s in ids]
+        blob = C.create_string_buffer(b"".join(enc) or b"\0")
+        off = as_i64(np.cumsum([0] + [len(e) for e in enc]))
+    check(ctx.lib.rs_predict_lengths(ctx.handle, obs.ctypes.data, depth.ctypes.data,
+                                     gt.ctypes.data, n, window, float(alpha), max_response_len,
+                                     C.byref(nm) if nm else None,
+                                     C.cast(blob, C.c_void_p) if blob is not None else None,
+                                     off.ctypes.data if off is not None else None, 0,
+                                     out.ctypes.data))
+    return out[:n]
+
+
+class LengthHistory:
+    """Sliding-window EWMA estimator (proj/include/rollsim/predictor.hpp:30-65).
+    observe() keeps the reference's host bookkeeping; predictions run on the
+    GPU, one batch per snapshot (snapshot_predictions, training.cpp:53-66)."""
+
+    def __init__(self, window=1, alpha=0.5, max_response_len=2048):
+        if window < 1:
+            raise ConfigError("predictor window must be >= 1")
+        if not alpha > 0 or alpha > 1:
+            raise ConfigError("predictor alpha must be in (0, 1]")
+        if max_response_len < 1:
+            raise ConfigError("predictor max_response_len must be >= 1")
+        self._window, self._alpha, self._max = window, alpha, max_response_len
+        self._obs, self._last_step = {}, {}
+
+    def window(self):
+        return self._window
+
+    def alpha(self):
+        return self._alpha
+
+    def max_response_len(self):
+        return self._max
+
+    def observe(self, step_idx, prompt_id, lengths):
+        """predictor.cpp:33-50: store the step's mean length."""
+        if not lengths:
+            raise ValidationError(f"observe: empty length list for prompt '{prompt_id}'")
+        total = 0.0
+        for v in lengths:
+            if v < 1 or v > self._max:
+                raise ValidationError(f"observe: length out of range for prompt '{prompt_id}': {v}")
+            total += v
+        q = self._obs.setdefault(prompt_id, [])
+        q.append(total / float(len(lengths)))
+        del q[:max(0, len(q) - self._window)]
+        self._last_step[prompt_id] = step_idx
+
+    def observations(self, prompt_id):
+        return self._obs.get(prompt_id)
+
+    def snapshot(self, prompts, noise: Optional[NoiseModel] = None):
+        """Predictions for (id, ground_truth_len) pairs, or objects with .id and
+        .ground_truth_len, in one device call."""
+        items = [(p.id, p.ground_truth_len) if hasattr(p, "id") else tuple(p) for p in prompts]
+        n = len(items)
+        if n == 0:
+            return np.zeros(0, np.float64)
+        obs = np.zeros((n, self._window), np.float64)
+        depth = np.zeros(n, np.int32)
+        for i, (pid, _) in enumerate(items):
+            q = self._obs.get(pid) or []
+            depth[i] = len(q)
+            obs[i, :len(q)] = q
+        return predict_lengths(obs, depth, [g for _, g in items], self._window, self._alpha,
+                               self._max, noise, [pid for pid, _ in items] if noise else None)
+
+    def predict(self, prompt):
+        return float(self.snapshot([prompt])[0])
+
+    def predict_noisy(self, prompt, noise: NoiseModel):
+        return float(self.snapshot([prompt], noise)[0])
 
 
 # ---------------------------------------------------------------- placement

@@ -5,11 +5,14 @@
 // estimate_cost and scale run on the GPU; this file marshals the reference's
 // AoS types (strings, vectors) into the C-ABI's SoA arrays and back.
 #include <cmath>
+#include <deque>
+#include <string>
 
 #include <nlohmann/json.hpp>
 
 #include "rollsim/errors.hpp"
 #include "rollsim/planner.hpp"
+#include "rollsim/predictor.hpp"
 #include "rollsim_b200.hpp"
 #include "rs_shim.hpp"
 
@@ -246,6 +249,33 @@ ScaleResult scale_placed(const std::vector<PredictedPrompt>& predicted,
   rs_placement_penalty pen{&t, model_bytes, kv_bytes_per_token, l_prefill_seconds};
   return run_scale(predicted, profile, responses_per_prompt, n_min, n_max, lambda, gpus_per_actor,
                    nullptr, &pen);
+}
+
+std::vector<double> predict_lengths(const LengthHistory& history,
+                                    const std::vector<const Prompt*>& prompts,
+                                    const NoiseModel* noise) {
+  const int32_t n = static_cast<int32_t>(prompts.size());
+  const int32_t w = history.window();
+  std::vector<double> obs(static_cast<size_t>(n) * w, 0.0), out(n);
+  std::vector<int32_t> depth(n), gt(n);
+  std::string ids;
+  std::vector<int64_t> off(1, 0);
+  for (int32_t i = 0; i < n; ++i) {
+    const Prompt& p = *prompts[i];
+    const std::deque<double>* q = history.observations(p.id);
+    depth[i] = q ? static_cast<int32_t>(q->size()) : 0;
+    if (q) std::copy(q->begin(), q->end(), obs.begin() + static_cast<size_t>(i) * w);
+    gt[i] = p.ground_truth_len;
+    ids += p.id;
+    off.push_back(static_cast<int64_t>(ids.size()));
+  }
+  rs_noise_model nm{};
+  const bool noisy = noise && noise->kind == NoiseModel::Kind::bucket;
+  if (noisy) nm = {1, noise->bucket_accuracy, noise->bucket_width, noise->seed};
+  rs_shim::check(rs_predict_lengths(rs_shim::ctx(), obs.data(), depth.data(), gt.data(), n, w,
+                                    history.alpha(), history.max_response_len(),
+                                    noisy ? &nm : nullptr, ids.data(), off.data(), 0, out.data()));
+  return out;
 }
 
 }  // namespace b200

@@ -14,6 +14,7 @@
 
 #include "rollsim/placement.hpp"
 #include "rollsim/planner.hpp"
+#include "rollsim/predictor.hpp"
 
 namespace rollsim::b200 {
 
@@ -22,5 +23,12 @@ ScaleResult scale_placed(const std::vector<PredictedPrompt>& predicted,
                          int n_max, double lambda, int gpus_per_actor,
                          const ClusterTopology& topo, double model_bytes,
                          double kv_bytes_per_token, double l_prefill_seconds);
+
+// snapshot_predictions (training.cpp:53-66) in one device call:
+// history.predict(p), or history.predict_noisy(p, *noise) when noise is set
+// (predictor.cpp:52-98), for every prompt, bit for bit.
+std::vector<double> predict_lengths(const LengthHistory& history,
+                                    const std::vector<const Prompt*>& prompts,
+                                    const NoiseModel* noise = nullptr);
 
 }  // namespace rollsim::b200

@@ -100,3 +100,38 @@ TEST_CASE("scale_placed raises the reference's error types") {
   CHECK_THROWS_AS(b200::scale_placed(v, default_profile(), 8, 1, 41, 0.7, 2, bad, 6e9, 36864.0, 0.1),
                   ValidationError);
 }
+
+TEST_CASE("predict_lengths matches LengthHistory::predict / predict_noisy bitwise") {
+  LengthHistory h(3, 0.35, 1500);
+  Rng rng(77);
+  std::vector<Prompt> prompts(400);
+  for (int i = 0; i < 400; ++i) {
+    char id[16];
+    std::snprintf(id, sizeof(id), "q%05d", i);
+    prompts[i].id = id;
+    prompts[i].ground_truth_len = static_cast<int>(rng.uniform_int(1, 3000));
+  }
+  for (int step = 0; step < 6; ++step)
+    for (int i = 0; i < 100 + 50 * step; ++i) {
+      std::vector<int> ls;
+      for (int k = 0, m = static_cast<int>(rng.uniform_int(1, 5)); k < m; ++k)
+        ls.push_back(static_cast<int>(rng.uniform_int(1, 1500)));
+      h.observe(step, prompts[i].id, ls);
+    }
+  std::vector<const Prompt*> ptrs;
+  for (const Prompt& p : prompts) ptrs.push_back(&p);
+  NoiseModel noise;
+  noise.kind = NoiseModel::Kind::bucket;
+  noise.bucket_accuracy = 0.4;
+  noise.bucket_width = 37;
+  noise.seed = 12345;
+  std::vector<double> a = b200::predict_lengths(h, ptrs);
+  std::vector<double> b = b200::predict_lengths(h, ptrs, &noise);
+  int differs = 0;
+  for (size_t i = 0; i < prompts.size(); ++i) {
+    CHECK(same_bits(a[i], h.predict(prompts[i])));
+    CHECK(same_bits(b[i], h.predict_noisy(prompts[i], noise)));
+    differs += a[i] != b[i];
+  }
+  CHECK(differs > 0);
+}

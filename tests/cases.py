@@ -120,3 +120,37 @@ def placement_cases():
                                           learner_node=1, learner_gpus=[4]),
                           l_prefill_seconds=0.0, model_bytes=1e11), 1, 15),
     ]
+
+
+def predictor_cases():
+    """Histories for LengthHistory::predict / predict_noisy
+    (proj/src/predictor.cpp:52-98): (window, alpha, max_len, obs, depth,
+    ground_truth, ids, noise). Observation means come from integer length
+    lists like observe() stores them; some prompts are never observed, some
+    estimates clamp at max_len, and bucket noise runs at several accuracies
+    (0 forces the wrong-bucket branch), widths and seeds."""
+    from paper_2602_22718_b200.rollsim import NoiseModel
+    rng = Rng(2718)
+    out = []
+    for t in range(24):
+        window = [1, 2, 3, 5, 8][t % 5]
+        alpha = [0.5, 0.3, 1.0, 0.9, 0.125][t % 5]
+        max_len = [2048, 700, 16384, 100, 3][t % 5]
+        n = rng.uniform_int(1, 300)
+        obs = np.zeros((n, window))
+        depth = np.zeros(n, np.int32)
+        gt = np.zeros(n, np.int32)
+        for i in range(n):
+            gt[i] = rng.uniform_int(1, max_len + max_len // 2)
+            d = rng.uniform_int(0, window) if rng.uniform() < 0.8 else 0
+            depth[i] = d
+            for k in range(d):
+                ls = [rng.uniform_int(1, max_len) for _ in range(rng.uniform_int(1, 8))]
+                obs[i, k] = sum(float(x) for x in ls) / len(ls)
+        ids = [f"p{rng.uniform_int(0, 999999):06d}-{i}" for i in range(n)]
+        noise = None
+        if t % 3:
+            noise = NoiseModel("bucket", [0.0, 0.25, 0.8, 1.0][t % 4],
+                               max(1, min(max_len, [1, 7, 100, 512][t % 4])), rng.next_u64())
+        out.append((window, alpha, max_len, obs, depth, gt, ids, noise))
+    return out

@@ -165,6 +165,25 @@ class Oracle:
         out.update(n_star=ns.value, order=order[:len(pred)], actor_times=at[:ns.value])
         return out
 
+    def predict_lengths(self, obs, depth, gt, window, alpha, max_len, noise=None, ids=None):
+        """LengthHistory::predict / predict_noisy per prompt. obs: count x window."""
+        obs = as_f64(np.asarray(obs, np.float64).reshape(-1) if np.size(obs) else [0.0])
+        depth, gt = as_i32(depth), as_i32(gt)
+        n = len(depth)
+        out = np.zeros(max(n, 1), np.float64)
+        nm = noise.struct() if noise is not None else None
+        if ids is not None:
+            blob = b"".join(s.encode() for s in ids)
+            off = as_i64(np.cumsum([0] + [len(s.encode()) for s in ids]))
+        else:
+            blob, off = None, None
+        self._chk(self.fn("predict_lengths")(ptr(obs, C.c_double), ptr(depth, C.c_int32),
+                                             ptr(gt, C.c_int32), n, window, float(alpha), max_len,
+                                             C.byref(nm) if nm is not None else None, blob,
+                                             ptr(off, C.c_int64) if off is not None else None,
+                                             ptr(out, C.c_double)))
+        return out[:n]
+
     def sweep_arrays(self, pred, plen, S, P, prof, g, n_min, n_max, lam, gpus, threads=1):
         pred, plen = as_f64(pred), as_i32(plen)
         Cn = n_max - n_min + 1

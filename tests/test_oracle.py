@@ -234,3 +234,29 @@ def test_placement_penalty_errors_match_reference():
         with pytest.raises(OracleError) as e:  # scale's own checks come first
             o.scale_placed(pred, plen, None, default_profile(), 2, 1, 41, 0.5, gpus, bad)
         assert e.value.status == 1
+
+
+@needs_ref
+def test_port_matches_reference_predictor():
+    """The C restatement of LengthHistory::predict / predict_noisy against
+    the reference's own LengthHistory (loaded via from_json), bitwise."""
+    from cases import predictor_cases
+    for t, (w, a, m, obs, depth, gt, ids, noise) in enumerate(predictor_cases()):
+        x = port().predict_lengths(obs, depth, gt, w, a, m, noise, ids)
+        y = ref().predict_lengths(obs, depth, gt, w, a, m, noise, ids)
+        assert np.array_equal(bits(x), bits(y)), t
+        if noise is not None and noise.bucket_accuracy == 0.0 and m > noise.bucket_width:
+            assert (x != port().predict_lengths(obs, depth, gt, w, a, m)).any(), t
+
+
+@needs_ref
+def test_predictor_config_errors_match_reference():
+    from paper_2602_22718_b200.rollsim import NoiseModel
+    obs, depth, gt = np.zeros((1, 1)), np.zeros(1, np.int32), np.ones(1, np.int32)
+    for o in (port(), ref()):
+        for args in ((0, 0.5, 10, None), (1, 0.0, 10, None), (1, 0.5, 0, None),
+                     (1, 0.5, 10, NoiseModel("bucket", 1.5, 5, 0)),
+                     (1, 0.5, 10, NoiseModel("bucket", 0.5, 11, 0))):
+            with pytest.raises(OracleError) as e:
+                o.predict_lengths(obs, depth, gt, *args[:3], args[3], ["p0"])
+            assert e.value.status == 2, args
