@@ -885,6 +885,22 @@ int fast_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, Cand
 // the current block via its in-block prefix max.
 constexpr int kLsThreads = 256;
 
+// Fused tail of scale() per (scenario, candidate), when tt != nullptr:
+// t_total = max group time, cost = sum rho*t*gpus in group order
+// (planner.cpp:180-186), exact idle slot-ticks; and, when one CTA holds every
+// candidate of its scenario (select != 0), the normalisation + first strict
+// argmin of planner.cpp:196-217 with block reductions.
+struct LsEpilogue {
+  double* tt;
+  double* cc;
+  int64_t* idle;
+  int32_t* n_star;
+  double rho;
+  double lambda;
+  int gpus;
+  int select;
+};
+
 struct LsArgs {
   FastSS ss;
   FastProf fp;
@@ -982,6 +998,118 @@ __global__ void group_table_kernel(FastSS ss, DevProfile prof, CandRange cr, int
     const int64_t f = ss.seg[so + kb].x & 0xffff;
     gtab[t] = make_int4(ka, kb, va | (vb << 16), smb);
     gfirst[t] = dadd(0.0, run_sum_int(prof, (int64_t)cr.G * (b - a), top_m, (int64_t)top_m + f - 1));
+  }
+}
+
+// see LsEpilogue. gt: this lane's N group times (just written by this lane).
+// idle_fa = sum over groups of (b - a) * F(first segment of the group), from
+// the walk; the per-group CF differences telescope to CF(P) (segCF[D]).
+// fast_reduce + select for the lockstep evaluator's batch in one kernel: one
+// CTA per scenario, one candidate per thread (C <= kLsThreads). Group times
+// are read 8 ahead of the sequential cost sum; idle slot-ticks use the
+// telescoped form sum_g (b - a) * F(ka_g) - CF(P) with ka_g from the group
+// table; n_star comes from block reductions with the reference's min/max and
+// first-strict-minimum semantics (planner.cpp:196-217).
+__global__ void __launch_bounds__(kLsThreads)
+fast_finish_kernel(FastSS ss, CandRange cr, const double* gt_all, const int4* gtab_all,
+                   LsEpilogue ep) {
+  __shared__ double r_d[4][kLsThreads / 32];
+  __shared__ int r_i[kLsThreads / 32];
+  const int C = cr.n_max - cr.n_min + 1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int s = blockIdx.x, c = threadIdx.x;
+  const bool on = c < C;
+  const int N = cr.n_min + (on ? c : 0);
+  const int64_t gbase = (int64_t)s * cr.T + (tri64(N) - tri64(cr.n_min));
+  const double* gt = gt_all + gbase;
+  double tt = 0.0, dollars = 0.0;
+  if (on) {
+    const double gd = (double)ep.gpus;
+    constexpr int U = 8;  // loads issued ahead of the sequential sum
+    int g = 0;
+    for (; g + U <= N; g += U) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = gt[g + u];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        tt = tt < v[u] ? v[u] : tt;                               // std::max(t_total, t)
+        dollars = dadd(dollars, dmul(dmul(ep.rho, v[u]), gd));    // rho * t * gpu_count
+      }
+    }
+    for (; g < N; ++g) {
+      const double v = gt[g];
+      tt = tt < v ? v : tt;
+      dollars = dadd(dollars, dmul(dmul(ep.rho, v), gd));
+    }
+    const int64_t o = (int64_t)s * C + c;
+    ep.tt[o] = tt;
+    ep.cc[o] = dollars;
+    if (ep.idle) {
+      const int64_t i0 = ss.item_off[s], so = i0 + s;
+      const int P = (int)(ss.item_off[s + 1] - i0);
+      const int D = ss.nseg[s];
+      const int4* gtab = gtab_all + gbase;
+      const int q = P / N, rem = P % N;
+      int64_t acc = 0;
+      for (int h = 0; h < N; ++h) {
+        const int size = q + (h < rem ? 1 : 0);
+        if (size > 0) acc += (int64_t)size * (__ldg(&ss.seg[so + __ldg(&gtab[h].x)].x) & 0xffff);
+      }
+      ep.idle[o] = (acc - ss.segCF[so + D]) * cr.G;
+    }
+  }
+  if (!ep.select) return;
+  // t / c minima and maxima over the scenario's candidates (exact, order-free)
+  double v[4] = {on ? tt : INFINITY, on ? tt : -INFINITY, on ? dollars : INFINITY,
+                 on ? dollars : -INFINITY};
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double w = __shfl_xor_sync(0xffffffffu, v[j], o);
+      v[j] = (j & 1) ? (v[j] < w ? w : v[j]) : (w < v[j] ? w : v[j]);
+    }
+  }
+  if (lane == 0)
+    for (int j = 0; j < 4; ++j) r_d[j][wid] = v[j];
+  __syncthreads();
+  for (int w = 0; w < kLsThreads / 32; ++w)
+    for (int j = 0; j < 4; ++j) {
+      const double x = r_d[j][w];
+      v[j] = (j & 1) ? (v[j] < x ? x : v[j]) : (x < v[j] ? x : v[j]);
+    }
+  const double t_min = v[0], t_max = v[1], c_min = v[2], c_max = v[3];
+  double sc = INFINITY;
+  if (on) {  // planner.cpp:196-209
+    const double tn = t_max > t_min ? ddiv(dsub(tt, t_min), dsub(t_max, t_min)) : 0.0;
+    const double cn = c_max > c_min ? ddiv(dsub(dollars, c_min), dsub(c_max, c_min)) : 0.0;
+    sc = dadd(dmul(ep.lambda, tn), dmul(dsub(1.0, ep.lambda), cn));
+  }
+  // first strict minimum (planner.cpp:210-214) = lexicographic (score, index) minimum
+  int bi = on ? c : INT32_MAX;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double w = __shfl_xor_sync(0xffffffffu, sc, o);
+    const int wi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (w < sc || (!(sc < w) && wi < bi)) {
+      sc = w;
+      bi = wi;
+    }
+  }
+  __syncthreads();
+  if (lane == 0) {
+    r_d[0][wid] = sc;
+    r_i[wid] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kLsThreads / 32; ++w)
+      if (r_d[0][w] < sc || (!(sc < r_d[0][w]) && r_i[w] < bi)) {
+        sc = r_d[0][w];
+        bi = r_i[w];
+      }
+    ep.n_star[s] = cr.n_min + bi;
   }
 }
 
@@ -1133,7 +1261,7 @@ __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
 }
 
 int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, CandRange cr,
-                  double* gt) {
+                  double* gt, const LsFuse* fuse) {
   if (!fast_profile_ok(prof, cr.G)) return fail(RS_E_CONFIG, "profile not eligible for the fast path");
   const int64_t ncm = prof.c_hi - prof.c_lo + 1;
   if (ncm > kTopCap) return fail(RS_E_CONFIG, "context memo too large for the lockstep evaluator");
@@ -1149,7 +1277,8 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
               (int)std::min<int64_t>((n + 255) / 256, 16 * ctx->num_sms), 256, 0, ss, prof, cr, S,
               gtab, gfirst);
   }
-  LsArgs A{ss, fp, cr, S, (C + kLsThreads - 1) / kLsThreads, gt, gtab, gfirst};
+  const int cand_units = (C + kLsThreads - 1) / kLsThreads;
+  LsArgs A{ss, fp, cr, S, cand_units, gt, gtab, gfirst};
   const int smem = (int)(sizeof(double) * fp.live_top + sizeof(uint16_t) * (ncm + 1));
   RS_CUDA_TRY(cudaFuncSetAttribute(lockstep_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 1;
@@ -1157,8 +1286,16 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
   const int units = S * A.cand_units;
   const int grid = std::max(1, std::min(units, std::max(1, per_sm) * ctx->num_sms));
   RS_LAUNCH(ctx, "group_eval", lockstep_eval_kernel, grid, kLsThreads, smem, A);
+  if (fuse) {  // the caller skips fast_reduce / select
+    if (!lockstep_fuses_select(cr)) return fail(RS_E_ARG, "finish kernel needs <= 256 candidates");
+    LsEpilogue ep{fuse->tt, fuse->cc, fuse->idle, fuse->n_star, fuse->rho, fuse->lambda,
+                  fuse->gpus, fuse->n_star ? 1 : 0};
+    RS_LAUNCH(ctx, "finish", fast_finish_kernel, S, kLsThreads, 0, ss, cr, gt, gtab, ep);
+  }
   return RS_OK;
 }
+
+bool lockstep_fuses_select(CandRange cr) { return cr.n_max - cr.n_min + 1 <= kLsThreads; }
 
 // ----------------------------------------------------------------- reduce --
 __global__ void fast_reduce_kernel(FastSS ss, int S, CandRange cr, double rho, int gpus,

@@ -98,8 +98,21 @@ size_t fast_eval_bytes(const DevProfile& prof, int G);
 
 // Candidate-lockstep evaluator (large S): lanes are candidates walking
 // the scenario's segments k = D-1 .. 0 together.
+// Optional fused tail for the lockstep evaluator: per (scenario, candidate)
+// t_total / cost / idle (like fast_reduce) and, when the candidate range fits
+// one CTA (lockstep_fuses_select), n_star (like select_kernel).
+struct LsFuse {
+  double* tt;
+  double* cc;
+  int64_t* idle;
+  int32_t* n_star;
+  double rho;
+  double lambda;
+  int gpus;
+};
 int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, CandRange cr,
-                  double* gt);
+                  double* gt, const LsFuse* fuse = nullptr);
+bool lockstep_fuses_select(CandRange cr);
 
 // Per (scenario, candidate): t_total, cost, idle slot-ticks.
 int fast_reduce(rs_ctx* ctx, int S, const FastSS& ss, CandRange cr, double rho, int gpus,

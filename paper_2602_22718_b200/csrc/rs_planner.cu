@@ -384,22 +384,33 @@ __global__ void select_kernel(int S, int C, int n_min, double lambda,
   }
 }
 
-// Sweep aggregate over this batch's scenarios, fixed order (deterministic).
+// Sweep aggregate over this batch's scenarios: one warp per candidate, lane l
+// sums scenarios l, l+32, ... in order, then a fixed shuffle tree
+// (deterministic; the per-candidate sums are aggregates, compared at 1e-12).
 __global__ void aggregate_kernel(int S, int C, int n_min, const double* t_total,
                                  const double* cost, const int32_t* n_star,
                                  double* sum_t, double* sum_c, int32_t* hist) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < C;
-       i += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < C;
+       i += (gridDim.x * blockDim.x) >> 5) {
     double st = 0.0, sc = 0.0;
     int h = 0;
-    for (int s = 0; s < S; ++s) {
+    for (int s = lane; s < S; s += 32) {
       st = dadd(st, t_total[(int64_t)s * C + i]);
       sc = dadd(sc, cost[(int64_t)s * C + i]);
       h += n_star[s] == n_min + i ? 1 : 0;
     }
-    sum_t[i] = dadd(sum_t[i], st);
-    sum_c[i] = dadd(sum_c[i], sc);
-    hist[i] += h;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      st = dadd(st, __shfl_xor_sync(0xffffffffu, st, o));
+      sc = dadd(sc, __shfl_xor_sync(0xffffffffu, sc, o));
+      h += __shfl_xor_sync(0xffffffffu, h, o);
+    }
+    if (lane == 0) {
+      sum_t[i] = dadd(sum_t[i], st);
+      sum_c[i] = dadd(sum_c[i], sc);
+      hist[i] += h;
+    }
   }
 }
 
@@ -627,15 +638,26 @@ static int units_for(rs_ctx* ctx, int S, int C) {
   return std::max(1, std::min(want, C));
 }
 
+// fuse (nullable): when the lockstep evaluator runs it also produces the
+// reduce (and, if *fused_select, select) outputs; *fused is set accordingly.
 static int eval_batch(rs_ctx* ctx, const Built& b, int S, const DevProfile& dp, int n_min,
-                      int n_max, int G, double* gt) {
+                      int n_max, int G, double* gt, const LsFuse* fuse = nullptr,
+                      bool* fused = nullptr, bool* fused_select = nullptr) {
+  if (fused) *fused = false;
+  if (fused_select) *fused_select = false;
   const int64_t T = groups_per_scenario(n_min, n_max);
   if (b.fast) {
     CandRange cr{n_min, n_max, T, G};
     // Many scenarios: candidates in lockstep (one lane per candidate).
     // Few scenarios: one group per lane, candidates split over CTAs.
-    if (S >= ctx->num_sms && dp.c_hi - dp.c_lo + 1 <= kTopCap)
-      return lockstep_eval(ctx, S, b.fss, dp, cr, gt);
+    if (S >= ctx->num_sms && dp.c_hi - dp.c_lo + 1 <= kTopCap) {
+      const bool f = fuse && fused && lockstep_fuses_select(cr);
+      if (f) {
+        *fused = true;
+        if (fused_select) *fused_select = fuse->n_star != nullptr;
+      }
+      return lockstep_eval(ctx, S, b.fss, dp, cr, gt, f ? fuse : nullptr);
+    }
     return fast_eval(ctx, S, b.fss, dp, cr, units_for(ctx, S, n_max - n_min + 1), gt);
   }
   CandSpec cs{n_min, n_max, T, G};
@@ -750,13 +772,20 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
     int64_t* o_idle =
         (device_ptrs && out->idle_slot_ticks) ? out->idle_slot_ticks + (size_t)s0 * C : b_idle;
     int32_t* o_ns = (device_ptrs && out->n_star) ? out->n_star + s0 : b_ns;
-    RS_TRY(eval_batch(ctx, built, Sb, dp, n_min, n_max, G, gt));
-    RS_TRY(reduce_batch(ctx, built, Sb, n_min, n_max, G, dp.rho, gpus, gt, o_tt, o_cc,
-                        out->idle_slot_ticks ? o_idle : (int64_t*)nullptr));
-    RS_LAUNCH(ctx, "select", select_kernel, grid_for(ctx, Sb, 128), 128, 0, Sb, C, n_min, lambda,
-              o_tt, (const double*)nullptr, o_cc, (double*)nullptr, (double*)nullptr,
-              (double*)nullptr, o_ns);
-    RS_LAUNCH(ctx, "aggregate", aggregate_kernel, grid_for(ctx, C, 128), 128, 0, Sb, C, n_min,
+    LsFuse fuse{o_tt, o_cc, out->idle_slot_ticks ? o_idle : (int64_t*)nullptr, o_ns, dp.rho,
+                lambda, gpus};
+    bool fused = false, fused_select = false;
+    static const bool no_fuse = getenv("RS_NO_FUSE") != nullptr;  // A/B switch
+    RS_TRY(eval_batch(ctx, built, Sb, dp, n_min, n_max, G, gt, no_fuse ? nullptr : &fuse, &fused,
+                      &fused_select));
+    if (!fused)
+      RS_TRY(reduce_batch(ctx, built, Sb, n_min, n_max, G, dp.rho, gpus, gt, o_tt, o_cc,
+                          out->idle_slot_ticks ? o_idle : (int64_t*)nullptr));
+    if (!fused_select)
+      RS_LAUNCH(ctx, "select", select_kernel, grid_for(ctx, Sb, 128), 128, 0, Sb, C, n_min,
+                lambda, o_tt, (const double*)nullptr, o_cc, (double*)nullptr, (double*)nullptr,
+                (double*)nullptr, o_ns);
+    RS_LAUNCH(ctx, "aggregate", aggregate_kernel, grid_for(ctx, (int64_t)C * 32, 256), 256, 0, Sb, C, n_min,
               o_tt, o_cc, o_ns, agg_t, agg_c, agg_h);
     if (!device_ptrs) {
       if (out->t_total) RS_TRY(d2h(ctx, out->t_total + (size_t)s0 * C, o_tt, 8ull * Sb * C));

@@ -17,6 +17,8 @@ from . import _abi
 PKG_DIR = pathlib.Path(__file__).resolve().parent
 REPO = PKG_DIR.parent
 LIB_PATH = PKG_DIR / "librs_b200.so"
+if os.environ.get("RS_B200_LIB"):  # A/B runs of another build of the same C-ABI
+    LIB_PATH = pathlib.Path(os.environ["RS_B200_LIB"]).resolve()
 
 RS_OK, RS_E_VALIDATION, RS_E_CONFIG, RS_E_CUDA, RS_E_NOMEM, RS_E_ARG, RS_E_PLACEMENT = range(7)
 

@@ -20,7 +20,10 @@ spec = c4_spec(S, count=65536)
 Cn = 256
 bufs = [np.zeros(S * Cn), np.zeros(S * Cn), np.zeros(S * Cn, np.int64), np.zeros(S, np.int32),
         np.zeros(Cn, np.int32), np.zeros(Cn), np.zeros(Cn)]
-out = _abi.RsSweepOut(*[b.ctypes.data for b in bufs])
+ptrs = [b.ctypes.data for b in bufs]
+if "noidle" in sys.argv[3:]:
+    ptrs[2] = None  # no idle_slot_ticks output
+out = _abi.RsSweepOut(*ptrs)
 import time
 ctx.enable_kernel_timing(True)
 for r in range(reps):
@@ -28,7 +31,7 @@ for r in range(reps):
     ctx.reset_kernel_timing()
     check(ctx.lib.rs_sweep(ctx.handle, C.byref(spec), C.byref(ps), 8, 1, 256, 0.7, 2, C.byref(out), 0))
     print(f"rep {r} wall {1e3 * (time.perf_counter() - t0):.1f} ms")
-    for k in ("gen_scenarios", "fast_build", "fast_tables", "group_table", "group_eval", "candidate_reduce", "select", "aggregate"):
+    for k in ("gen_scenarios", "fast_build", "fast_tables", "group_table", "group_eval", "finish", "candidate_reduce", "select", "aggregate"):
         ms, n = ctx.kernel_time(k)
         print(f"rep {r} {k}: {ms:.3f} ms over {n} launches")
 print("n_star[:8]", bufs[3][:8])
