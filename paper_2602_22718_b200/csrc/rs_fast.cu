@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "rs_fast.cuh"
+#include "rs_scenario_tables.h"
 
 namespace rs {
 
@@ -61,10 +62,18 @@ constexpr int kBuildCur = kFastFmax + 4;     // cur[] ints (16-byte aligned end)
 constexpr int kBuildSmem = kBuildCur * 4 + kWide * 28;
 static_assert(kWide * 28 >= (kFastFmax + 2) * 2, "window region must hold the bucket map");
 
+constexpr int kQTab = RS_QTABLE_N + 1;        // quantile table entries
+constexpr int kSkfBytes = ((kFastFmax + 2) * 2 + 15) / 16 * 16;
+static_assert(kSkfBytes + 2 * kQTab * 8 <= kWide * 28, "bucket map + tables must fit region 2");
+
+// kGen: scenarios generated here from the quantile tables, staged in shared
+// memory next to the bucket map; they are generated twice (histogram, then
+// scatter) instead of being stored and re-read, and written out only when
+// keep is set.
 template <bool kGen>
 __global__ void __launch_bounds__(kBuildT)
 fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_io,
-                  int32_t* plen_io, FastSS ss, int* flags) {
+                  int32_t* plen_io, FastSS ss, int* flags, int keep) {
   // dynamic shared memory: cur (bucket cursors, then segment ends) and a
   // second region holding the bucket -> segment map during the scatter and
   // the sorting window afterwards
@@ -86,7 +95,14 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
   const int64_t so = i0 + s;
   double* pred = pred_io + i0;
   int32_t* plen = plen_io + i0;
+  double* t_nz = reinterpret_cast<double*>(reinterpret_cast<char*>(cur + kBuildCur) + kSkfBytes);
+  double* t_lnz = t_nz + kQTab;
   for (int f = tid; f < kFastFmax + 2; f += kBuildT) cur[f] = 0;
+  if (kGen)
+    for (int j = tid; j < kQTab; j += kBuildT) {
+      t_nz[j] = nz[j];
+      t_lnz[j] = lnz[j];
+    }
   if (tid == 0) bad = 0;
   __syncthreads();
   const uint64_t seed = kGen ? hash_combine(gs.base_seed, (uint64_t)(gs.first + s)) : 0;
@@ -95,9 +111,11 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
     double p;
     int32_t pl;
     if (kGen) {
-      fast_gen(gs, nz, lnz, seed, i, &p, &pl);
-      pred[i] = p;
-      plen[i] = pl;
+      fast_gen<true>(gs, t_nz, t_lnz, seed, i, &p, &pl);
+      if (keep) {
+        pred[i] = p;
+        plen[i] = pl;
+      }
     } else {
       p = pred[i];
       pl = plen[i];
@@ -182,8 +200,12 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
 #pragma unroll
     for (int u = 0; u < kScat; ++u) {
       const int j = i + u * kBuildT;
-      p[u] = j < P ? pred[j] : 0.0;
-      pl[u] = j < P ? plen[j] : 0;
+      if (kGen) {
+        if (j < P) fast_gen<true>(gs, t_nz, t_lnz, seed, j, &p[u], &pl[u]);
+      } else {
+        p[u] = j < P ? pred[j] : 0.0;
+        pl[u] = j < P ? plen[j] : 0;
+      }
     }
 #pragma unroll
     for (int u = 0; u < kScat; ++u) {
@@ -349,7 +371,8 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
 }
 
 int fast_build(rs_ctx* ctx, int S, const int64_t* d_off, double* pred, int32_t* plen,
-               FastSS ss, const GenSpec* gen, const double* nz, const double* lnz) {
+               FastSS ss, const GenSpec* gen, const double* nz, const double* lnz,
+               bool keep_inputs) {
   (void)d_off;
   const int smem = kBuildSmem;
   RS_CUDA_TRY(cudaFuncSetAttribute(fast_build_kernel<true>,
@@ -360,10 +383,10 @@ int fast_build(rs_ctx* ctx, int S, const int64_t* d_off, double* pred, int32_t* 
   if (gen) {
     g = *gen;
     RS_LAUNCH(ctx, "fast_build", fast_build_kernel<true>, S, kBuildT, smem, g, nz, lnz, pred,
-              plen, ss, ctx->d_flags);
+              plen, ss, ctx->d_flags, keep_inputs ? 1 : 0);
   } else {
     RS_LAUNCH(ctx, "fast_build", fast_build_kernel<false>, S, kBuildT, smem, g, nz, lnz, pred,
-              plen, ss, ctx->d_flags);
+              plen, ss, ctx->d_flags, 1);
   }
   return RS_OK;
 }

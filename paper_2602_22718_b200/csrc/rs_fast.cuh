@@ -50,24 +50,27 @@ struct GenSpec {
   double pred_scale, pred_min, pred_max;
 };
 
+// kShared: t is a shared-memory copy of the table (generic loads).
+template <bool kShared = false>
 __device__ __forceinline__ double fast_qinterp(const double* t, uint64_t u) {
   uint64_t j = u >> 52;
   double f = dmul((double)((u >> 11) & ((1ULL << 41) - 1)), 0x1.0p-41);
-  double a = __ldg(t + j), b = __ldg(t + j + 1);
+  double a = kShared ? t[j] : __ldg(t + j), b = kShared ? t[j + 1] : __ldg(t + j + 1);
   return dadd(a, dmul(dsub(b, a), f));
 }
 
 // Scenario item i of one Monte-Carlo scenario (oracle:
 // orc_generate_scenarios): two splitmix64 draws -> quantile interpolation.
+template <bool kShared = false>
 __device__ __forceinline__ void fast_gen(const GenSpec& g, const double* nz, const double* lnz,
                                          uint64_t seed, int i, double* pred, int32_t* plen) {
   uint64_t u1 = draw_at(seed, 2 * (uint64_t)i + 1);
   uint64_t u2 = draw_at(seed, 2 * (uint64_t)i + 2);
-  double z = fast_qinterp(nz, u1);
+  double z = fast_qinterp<kShared>(nz, u1);
   double pl = round(dadd(g.plen_mean, dmul(g.plen_sigma, z)));
   pl = pl < (double)g.plen_min ? (double)g.plen_min : pl;
   pl = pl > (double)g.plen_max ? (double)g.plen_max : pl;
-  double pr = dmul(g.pred_scale, fast_qinterp(lnz, u2));
+  double pr = dmul(g.pred_scale, fast_qinterp<kShared>(lnz, u2));
   pr = pr < g.pred_min ? g.pred_min : pr;
   pr = pr > g.pred_max ? g.pred_max : pr;
   *pred = pr;
@@ -75,11 +78,13 @@ __device__ __forceinline__ void fast_gen(const GenSpec& g, const double* nz, con
 }
 
 // Build the fast structure for S scenarios (one CTA each). When gen is
-// non-null the scenarios are generated on the device (and written to
-// pred/plen); otherwise pred/plen are read. Sets kFlagBucketOverflow in
-// ctx->d_flags if an input is outside the fast path's range.
+// non-null the scenarios are generated on the device (written to pred/plen
+// only when keep_inputs; the sweep does not need them); otherwise pred/plen
+// are read. Sets kFlagBucketOverflow in ctx->d_flags if an input is outside
+// the fast path's range.
 int fast_build(rs_ctx* ctx, int S, const int64_t* d_off, double* pred, int32_t* plen,
-               FastSS ss, const GenSpec* gen, const double* nz, const double* lnz);
+               FastSS ss, const GenSpec* gen, const double* nz, const double* lnz,
+               bool keep_inputs = true);
 
 struct CandRange {
   int n_min, n_max;

@@ -124,3 +124,24 @@ def test_sweep_many_scenarios_lockstep_bitwise():
 
 def test_sweep_many_scenarios_other_profile_lockstep():
     check_sweep(c4_spec(150, count=1500, first=5), 2, 70, prof=profiles()["small"], g=3, lam=0.4)
+
+
+def test_sweep_wide_buckets_bitwise():
+    """Buckets wider than a shared-memory window (~3,000 equal finish ticks,
+    ranked in global memory) and wider than the fast path allows (> 4,096,
+    generic path), with duplicate predictions tie-broken by id."""
+    rng = np.random.RandomState(21)
+    S, P = 3, 9000
+    pred = rng.uniform(1.0, 3000.0, S * P)
+    plen = rng.randint(0, 2000, S * P).astype(np.int32)
+    pred[0:3000] = 512.0                                   # scenario 0: one 3,000-wide bucket
+    pred[P:P + 2000] = 7.25
+    pred[P + 2000:P + 3500] = rng.uniform(99.0, 100.0, 1500)  # scenario 1: two wide buckets
+    pred[2 * P:2 * P + 5000] = 40.0                        # scenario 2: > 4,096 -> generic path
+    spec = c4_spec(S, count=P)
+    got = rs_sweep(spec, default_profile(), 8, 1, 64, 0.6, 2, (pred, plen))
+    tt, cc, ns = port().sweep_arrays(pred, plen, S, P, default_profile(), 8, 1, 64, 0.6, 2,
+                                     threads=3)
+    assert np.array_equal(bits(got["t_total"]), bits(tt))
+    assert np.array_equal(bits(got["cost"]), bits(cc))
+    assert np.array_equal(got["n_star"], ns)
