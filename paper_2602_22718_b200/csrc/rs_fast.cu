@@ -1321,6 +1321,20 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
   return RS_OK;
 }
 
+int lockstep_slots(rs_ctx* ctx, const DevProfile& prof, int G) {
+  const int64_t ncm = prof.c_hi - prof.c_lo + 1;
+  const int64_t live_top = std::max<int64_t>(1, (prof.b_hi + G - 1) / G);
+  const int smem = (int)(sizeof(double) * live_top + sizeof(uint16_t) * (ncm + 1));
+  if (cudaFuncSetAttribute(lockstep_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+      cudaSuccess)
+    return ctx->num_sms;
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lockstep_eval_kernel, kLsThreads, smem) !=
+      cudaSuccess)
+    per_sm = 1;
+  return std::max(1, per_sm) * ctx->num_sms;
+}
+
 bool lockstep_fuses_select(CandRange cr) { return cr.n_max - cr.n_min + 1 <= kLsThreads; }
 
 // ----------------------------------------------------------------- reduce --

@@ -118,6 +118,8 @@ struct LsFuse {
 int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, CandRange cr,
                   double* gt, const LsFuse* fuse = nullptr);
 bool lockstep_fuses_select(CandRange cr);
+// CTA slots of the lockstep evaluator on this device (one scenario each).
+int lockstep_slots(rs_ctx* ctx, const DevProfile& prof, int G);
 
 // Per (scenario, candidate): t_total, cost, idle slot-ticks.
 int fast_reduce(rs_ctx* ctx, int S, const FastSS& ss, CandRange cr, double rho, int gpus,

@@ -702,8 +702,15 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
   const bool with_generic = !gen_fast;
   const size_t per_scen = abytes(P, 8) + abytes(P, 4) + built_bytes(P, 1, with_generic) +
                           abytes(T, 8) * 2 + abytes(T, 16) + abytes(C, 8) * 3 + abytes(1, 4) + 2048;
-  int B = (int)std::max<size_t>(1, std::min<size_t>((size_t)S, (size_t)(3ull << 30) / per_scen));
+  // Batch size: what an 8 GiB scratch budget holds (<= 2048), rounded down to
+  // a multiple of the lockstep evaluator's CTA slots so every batch is whole
+  // waves (S = 10,000 on 148 SMs x 4: batches of 1,184, 17 waves in all).
+  int B = (int)std::max<size_t>(1, std::min<size_t>((size_t)S, (size_t)(8ull << 30) / per_scen));
   if (B > 2048) B = 2048;
+  if (allow_fast) {
+    const int slots = lockstep_slots(ctx, dp, G);
+    if (B > slots) B = B / slots * slots;
+  }
   size_t need = (size_t)B * per_scen + fast_eval_bytes(dp, G) + abytes(B + 1, 8) +
                 abytes(2 * (RS_QTABLE_N + 1), 8) +
                 abytes(C, 8) * 2 + abytes(C, 4) + abytes(dp.c_hi - dp.c_lo + 1, 4) + (4 << 20);
