@@ -34,7 +34,7 @@ size_t fast_ss_bytes(int64_t items, int S) {
   int64_t segs = items + S;
   return abytes(segs, 8) * 2 + abytes(S, 4) + abytes(items, 8) + abytes(items, 4) * 2 +
          abytes(items, 16) + abytes(segs, 4) + abytes(segs, 1) + abytes((int64_t)S * kStStride, 2) +
-         abytes(segs, 8);
+         abytes((segs / kBlk + S + 2) * kBlkPairs, 2);
 }
 
 FastSS fast_ss_alloc(rs_ctx* ctx, const int64_t* d_off, int64_t items, int S) {
@@ -51,7 +51,7 @@ FastSS fast_ss_alloc(rs_ctx* ctx, const int64_t* d_off, int64_t items, int S) {
   f.pmsm = arena_alloc<uint32_t>(ctx, segs);
   f.pgo = arena_alloc<uint8_t>(ctx, segs);
   f.st = arena_alloc<uint16_t>(ctx, (int64_t)S * kStStride);
-  f.sts = arena_alloc<uint2>(ctx, segs);
+  f.bq = arena_alloc<uint16_t>(ctx, (segs / kBlk + S + 2) * kBlkPairs);
   return f;
 }
 
@@ -337,29 +337,24 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
       sm = max(sm, v[i]);
       if (k0 + i < k1) ss.pmsm[so + k0 + i] |= (uint32_t)sm << 16;
     }
-    // within-block sparse table: lv[L][i] = max v[i .. min(i + 2^L, 16))
-    int lv[kBlk];
+    // every in-block range max: bq[blk_pair(i, j)] = max v[i .. j], in
+    // flat order, packed four to a 64-bit store (136 = 34 x 4; 272-byte rows)
+    uint64_t* bq = reinterpret_cast<uint64_t*>(ss.bq + (size_t)((so >> 4) + s + jb) * kBlkPairs);
+    uint64_t word = 0;
+    int t = 0;
 #pragma unroll
-    for (int i = 0; i < kBlk; ++i) lv[i] = v[i];
-    uint32_t packed[kBlk][2];
+    for (int i = 0; i < kBlk; ++i) {
+      int m2 = 0;
 #pragma unroll
-    for (int L = 1; L <= 4; ++L) {
-#pragma unroll
-      for (int i = 0; i < kBlk; ++i) {
-        const int h = 1 << (L - 1);
-        lv[i] = i + h < kBlk ? max(lv[i], lv[i + h]) : lv[i];
-      }
-#pragma unroll
-      for (int i = 0; i < kBlk; ++i) {
-        if (L == 1) packed[i][0] = (uint32_t)lv[i];
-        if (L == 2) packed[i][0] |= (uint32_t)lv[i] << 16;
-        if (L == 3) packed[i][1] = (uint32_t)lv[i];
-        if (L == 4) packed[i][1] |= (uint32_t)lv[i] << 16;
+      for (int j = i; j < kBlk; ++j, ++t) {
+        m2 = max(m2, v[j]);
+        word |= (uint64_t)(uint16_t)m2 << (16 * (t & 3));
+        if ((t & 3) == 3) {
+          bq[t >> 2] = word;
+          word = 0;
+        }
       }
     }
-#pragma unroll
-    for (int i = 0; i < kBlk; ++i)
-      if (k0 + i < k1) ss.sts[so + k0 + i] = make_uint2(packed[i][0], packed[i][1]);
   }
   __syncthreads();
   for (int lev = 1; (1 << lev) <= nblk; ++lev) {
@@ -940,21 +935,13 @@ struct LsView {
   const uint32_t* pmsm;
   const uint8_t* pgo;
   const uint16_t* st;
-  const uint2* sts;
+  const uint16_t* bq;  // this scenario's block 0 in FastSS::bq
 };
 
-// max MX over [l, r] inside one 16-segment block (O(1): two lookups in the
-// within-block sparse table).
+// max MX over [l, r] inside one 16-segment block: one lookup in the block's
+// all-pairs table.
 __device__ __forceinline__ int ls_inblock(const LsView& V, int l, int r) {
-  const int len = r - l + 1;
-  const int lev = 31 - __clz(len);
-  auto at = [&](int k) -> int {
-    if (lev == 0) return (__ldg(&V.seg[k].x) >> 16) & 0xffff;
-    const uint2 w = __ldg(V.sts + k);
-    const uint32_t word = lev <= 2 ? w.x : w.y;
-    return (int)((lev & 1 ? word : word >> 16) & 0xffff);
-  };
-  return max(at(l), at(r - (1 << lev) + 1));
+  return __ldg(V.bq + (l >> 4) * kBlkPairs + blk_pair(l & (kBlk - 1), r & (kBlk - 1)));
 }
 
 __device__ __forceinline__ int ls_mx(const LsView& V, int k) { return (__ldg(&V.seg[k].x) >> 16) & 0xffff; }
@@ -1005,7 +992,8 @@ __global__ void group_table_kernel(FastSS ss, DevProfile prof, CandRange cr, int
     const int P = (int)(ss.item_off[s + 1] - i0);
     const int q = P / N, rem = P % N;
     const int a = g * q + min(g, rem), b = a + q + (g < rem ? 1 : 0);
-    LsView V{ss.seg + so, ss.pmsm + so, ss.pgo + so, ss.st + (int64_t)s * kStStride, ss.sts + so};
+    LsView V{ss.seg + so, ss.pmsm + so, ss.pgo + so, ss.st + (int64_t)s * kStStride,
+             ss.bq + (size_t)((so >> 4) + s) * kBlkPairs};
     const int2 ra = ss.rinfo[i0 + a], rb = ss.rinfo[i0 + b - 1];
     const int ka = ra.x, kb = rb.x;
     const int va = ra.y & 0xffff, vb = (rb.y >> 16) & 0xffff;
@@ -1167,7 +1155,7 @@ __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
     const int64_t so = i0 + s;
     const int D = A.ss.nseg[s];
     LsView V{A.ss.seg + so, A.ss.pmsm + so, A.ss.pgo + so, A.ss.st + (int64_t)s * kStStride,
-             A.ss.sts + so};
+             A.ss.bq + (size_t)((so >> 4) + s) * kBlkPairs};
     const int64_t gbase = (int64_t)s * A.cr.T + (tri64(N) - flat0);
     double* gt = A.gt + gbase;
     const int4* gtab = A.gtab + gbase;

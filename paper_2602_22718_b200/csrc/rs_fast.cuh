@@ -25,12 +25,16 @@ struct FastSS {
   uint32_t* pmsm;  // per segment slot: in-block prefix max | in-block suffix max << 16
   uint8_t* pgo;    // per segment slot: distance to the previous greater MX in its block (0 = none)
   uint16_t* st;    // per scenario: sparse table over block maxima, [kStLevels][kStBlocks]
-  uint2* sts;      // per segment slot: in-block max over [k, k + 2^L) for L = 1..4 (u16 x 4)
+  uint16_t* bq;    // per 16-segment block: max MX over [i, j], in-block i <= j (kBlkPairs u16,
+                   // upper triangle row-major); block jb of scenario s at slot (so >> 4) + s + jb
 };
 
 constexpr int kFastFmax = 16384;   // finish ticks of the fast path
 constexpr int kFastPlenMax = 65535;
 constexpr int kBlk = 16;           // segment block of the lane evaluator
+constexpr int kBlkPairs = kBlk * (kBlk + 1) / 2;  // 136 in-block ranges
+static_assert(kBlkPairs % 4 == 0, "bq rows are written as 64-bit words");
+__host__ __device__ constexpr int blk_pair(int i, int j) { return i * (2 * kBlk + 1 - i) / 2 + (j - i); }
 constexpr int kMaxSeg = kFastFmax; // D <= Fmax
 constexpr int kTopCap = 4096;      // smem tpot row entries
 constexpr int kCoopN = 4;          // N < kCoopN: warp-cooperative groups
