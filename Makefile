@@ -50,7 +50,16 @@ SUITES    := acceptance_main test_dedup test_planner test_profile test_training
 
 .PHONY: shim
 shim: $(foreach t,$(SUITES),$(SHIM_OUT)/$(t)_b200 $(SHIM_OUT)/$(t)_ref) \
-      $(SHIM_OUT)/test_placement_b200
+      $(SHIM_OUT)/test_placement_b200 $(SHIM_OUT)/c5_bench_b200 $(SHIM_OUT)/c5_bench_ref
+
+# C5 driver (shim/tools/c5_bench.cpp), linked against the drop-in and the reference
+$(SHIM_OUT)/c5_bench_b200: $(PKG)/shim/tools/c5_bench.cpp $(SHIM_OUT)/librollsim_b200.a $(LIB)
+	$(CXXREF) -DRS_B200 -I$(PKG)/shim $< -o $@ $(SHIM_OUT)/librollsim_b200.a -L$(PKG) -lrs_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -lpthread
+
+$(SHIM_OUT)/c5_bench_ref: $(PKG)/shim/tools/c5_bench.cpp ref
+	@mkdir -p $(SHIM_OUT)
+	$(CXXREF) $< -o $@ oracle/_ref/librollsim_ref.a -lpthread
 
 # drop-in extension suite (rollsim_b200.hpp) against the stock penalty path
 $(SHIM_OUT)/test_placement_b200: $(PKG)/shim/tests/test_placement_b200.cpp $(SHIM_OUT)/librollsim_b200.a $(LIB)

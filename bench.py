@@ -361,10 +361,41 @@ def run_ours(args, world, rank, local):
             result["dedup"] = bench_dedup(args, ctx, torch, dev, stream)
         if world == 1 and not args.no_cpu:
             result["cpu_baseline"] = cpu_baseline_sweep(args)
+        if world == 1 and not args.no_c5:
+            result["c5"] = bench_c5()
         print(json.dumps(result), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def bench_c5(steps=20):
+    """C5: the reference's run_training(rlhfless) on
+    default_topology(128, 8, 4), 512 prompts x G=8, through the C++ drop-in
+    (build/shim/c5_bench_b200) and the unmodified reference
+    (build/shim/c5_bench_ref), iterations/s on this host; plus scale() with
+    plan_rlhfless's placement penalty at that size, stock vs the device
+    penalty (rollsim::b200::scale_placed)."""
+    out = {}
+    for arm in ("b200", "ref"):
+        exe = REPO / "build" / "shim" / f"c5_bench_{arm}"
+        if not exe.exists():
+            return {"unavailable": "build/shim not built (make shim)"}
+        p = subprocess.run([str(exe), str(steps)], capture_output=True, text=True, timeout=900)
+        if p.returncode != 0:
+            return {"unavailable": f"c5_bench_{arm} exit {p.returncode}"}
+        out[arm] = json.loads(p.stdout.strip().splitlines()[-1])
+    b, r = out["b200"], out["ref"]
+    return {"metric": "C5 iterations/sec (run_training, simulated 1,024-GPU cluster)",
+            "value": b["iterations_per_s"], "unit": "iterations/s", "steps": steps,
+            "reference": r["iterations_per_s"], "plan_ms_per_step": b["plan_ms_per_step"],
+            "reference_plan_ms_per_step": r["plan_ms_per_step"],
+            "identical_to_reference": b["digest"] == r["digest"],
+            "scale_with_placement_penalty_ms": {
+                "reference": r["scale_with_penalty_ms"]["stock"],
+                "dropin_callback": b["scale_with_penalty_ms"]["stock"],
+                "device": b["scale_with_penalty_ms"]["device"]},
+            "config": b["config"]}
 
 
 def bench_dedup(args, ctx, torch, dev, stream):
@@ -453,6 +484,7 @@ def main():
     ap.add_argument("--cpu-rounds", type=int, default=4)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dedup", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--check", action="store_true", default=True)
     args = ap.parse_args()
     world, rank, local = init_dist()

@@ -61,3 +61,22 @@ def test_placement_extension_on_dropin():
     plan_rlhfless's stock penalty lambda, bitwise (shim/tests/)."""
     code, out = run(SHIM / "test_placement_b200")
     assert "test cases:" in out and code == 0 and not failed_cases(out), out[-3000:]
+
+
+@pytest.mark.gpu
+def test_c5_training_loop_dropin_matches_reference():
+    """C5: the reference's run_training(rlhfless) on
+    default_topology(128, 8, 4) linked against the drop-in gives the same
+    plans and simulated steps, bit for bit, as the unmodified reference; and
+    rollsim::b200::scale_placed matches scale() + the stock penalty lambda."""
+    import json
+    outs = []
+    for name in ("c5_bench_ref", "c5_bench_b200"):
+        code, out = run(SHIM / name, timeout=600)
+        assert code == 0, out[-2000:]
+        outs.append(json.loads(out.strip().splitlines()[-1]))
+    ref_run, b200_run = outs
+    assert ref_run["digest"] == b200_run["digest"]
+    assert ref_run["total_cost"] == b200_run["total_cost"]
+    stock, device = b200_run["scale_with_penalty_ms"]["n_star"]
+    assert device == stock == ref_run["scale_with_penalty_ms"]["n_star"][0]
