@@ -57,14 +57,22 @@ FastSS fast_ss_alloc(rs_ctx* ctx, const int64_t* d_off, int64_t items, int S) {
 
 // ------------------------------------------------------------------ build --
 constexpr int kBuildT = 1024;
-constexpr int kWide = 4096;                 // records per sorting window (max bucket size)
+constexpr int kHalfT = kBuildT / 2;          // the sorting windows run on two half-CTAs
+constexpr int kWin = 2048;                   // records per half-CTA sorting window
+constexpr int kWide = 4096;                  // widest bucket (wider: generic path)
+constexpr int kMaxWin = 1024;                // windows per scenario (more: generic path)
 constexpr int kBuildCur = kFastFmax + 4;     // cur[] ints (16-byte aligned end)
-constexpr int kBuildSmem = kBuildCur * 4 + kWide * 28;
-static_assert(kWide * 28 >= (kFastFmax + 2) * 2, "window region must hold the bucket map");
+constexpr int kWinBytes = kWin * 28;         // key 8 + id 4 + pk 4 + pl 4 + pm 4 + q 4
+constexpr int kBuildSmem = kBuildCur * 4 + 2 * kWinBytes;
+static_assert(2 * kWinBytes >= (kFastFmax + 2) * 2, "window region must hold the bucket map");
 
 constexpr int kQTab = RS_QTABLE_N + 1;        // quantile table entries
 constexpr int kSkfBytes = ((kFastFmax + 2) * 2 + 15) / 16 * 16;
-static_assert(kSkfBytes + 2 * kQTab * 8 <= kWide * 28, "bucket map + tables must fit region 2");
+static_assert(kSkfBytes + 2 * kQTab * 8 <= 2 * kWinBytes, "bucket map + tables must fit region 2");
+
+__device__ __forceinline__ void half_sync(int h) {  // named barrier of one half-CTA
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + h), "r"(kHalfT) : "memory");
+}
 
 // kGen: scenarios generated here from the quantile tables, staged in shared
 // memory next to the bucket map; they are generated twice (histogram, then
@@ -73,21 +81,16 @@ static_assert(kSkfBytes + 2 * kQTab * 8 <= kWide * 28, "bucket map + tables must
 template <bool kGen>
 __global__ void __launch_bounds__(kBuildT)
 fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_io,
-                  int32_t* plen_io, FastSS ss, int* flags, int keep) {
+                  int32_t* plen_io, FastSS ss, int* flags, int keep, int need_order) {
   // dynamic shared memory: cur (bucket cursors, then segment ends) and a
   // second region holding the bucket -> segment map during the scatter and
   // the sorting window afterwards
   extern __shared__ __align__(16) int32_t cur[];  // [kFastFmax + 2]
   uint16_t* skf = reinterpret_cast<uint16_t*>(cur + kBuildCur);
-  long long* w_key = reinterpret_cast<long long*>(cur + kBuildCur);
-  int32_t* w_id = reinterpret_cast<int32_t*>(w_key + kWide);
-  int32_t* w_pk = w_id + kWide;
-  int32_t* w_pl = w_pk + kWide;
-  int32_t* w_pm = w_pl + kWide;
-  uint32_t* w_q = reinterpret_cast<uint32_t*>(w_pm + kWide);
   __shared__ int32_t wsum[32];
   __shared__ long long wsum64[32];
-  __shared__ int bad, s_k1;
+  __shared__ int bad, s_nw;
+  __shared__ int wb[kMaxWin + 1];  // window w = buckets [wb[w], wb[w + 1])
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t i0 = ss.item_off[s];
@@ -234,74 +237,125 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
   int32_t* segend = cur;  // cur is dead after the scatter
   for (int k = tid; k < D; k += kBuildT) segend[k] = ss.seg[so + k].y;
   __syncthreads();
-  for (int k0 = 0, ws = 0; k0 < D;) {
-    if (tid == 0) {
-      int k1 = -1;
-      if (segend[k0] - ws <= kWide) {  // largest k1 with segend[k1 - 1] <= ws + kWide
+  if (tid == 0) {  // greedy windows of whole buckets (<= kWin records; a wider bucket alone)
+    int nw = 0, k0 = 0, ws = 0;
+    while (k0 < D && nw < kMaxWin) {
+      wb[nw++] = k0;
+      int k1 = k0 + 1;
+      if (segend[k0] - ws <= kWin) {  // largest k1 with segend[k1 - 1] <= ws + kWin
         int lo = k0 + 1, hi = D;
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
-          if (segend[mid - 1] - ws <= kWide) lo = mid;
+          if (segend[mid - 1] - ws <= kWin) lo = mid;
           else hi = mid - 1;
         }
         k1 = lo;
+      } else if (segend[k0] - ws > kWide) {
+        nw = -1;
+        break;
       }
-      s_k1 = k1;
+      ws = segend[k1 - 1];
+      k0 = k1;
     }
-    __syncthreads();
-    const int k1 = s_k1;
-    if (k1 < 0) {
-      if (tid == 0) atomicOr(flags, kFlagBucketTooWide);
-      return;
-    }
-    const int n = segend[k1 - 1] - ws;
-    for (int i = tid; i < n; i += kBuildT) {
-      const int4 r = ss.rec[i0 + ws + i];
-      const long long bits = ((long long)r.y << 32) | (unsigned)r.x;
-      const double p = __longlong_as_double(bits);
-      const double fm1 = ceil(p) - 1.0;
-      w_key[i] = bits;
-      w_q[i] = fm1 >= 1.0 ? (uint32_t)((bits - __double_as_longlong(fm1)) >> 21) : 0u;
-      w_id[i] = r.z;
-      w_pk[i] = r.w;
-    }
-    __syncthreads();
-    for (int i = tid; i < n; i += kBuildT) {
-      const int k = w_pk[i] >> 16;
-      const int lo = (k == 0 ? 0 : segend[k - 1]) - ws, hi = segend[k] - ws;
-      const uint32_t q = w_q[i];
-      int rank = 0;
-      for (int j = lo; j < hi; ++j) {
-        const uint32_t qj = w_q[j];
-        rank += qj > q ? 1 : 0;
-        if (qj == q && j != i) {
-          const long long kj = w_key[j], key = w_key[i];
-          rank += (kj > key || (kj == key && w_id[j] < w_id[i])) ? 1 : 0;
+    if (nw >= 0 && k0 < D) nw = -1;  // more windows than kMaxWin
+    if (nw >= 0) wb[nw] = D;
+    s_nw = nw;
+  }
+  __syncthreads();
+  if (s_nw < 0) {
+    if (tid == 0) atomicOr(flags, kFlagBucketTooWide);
+    return;
+  }
+  {
+    const int h = tid / kHalfT, ht = tid % kHalfT;
+    char* wbase = reinterpret_cast<char*>(cur + kBuildCur) + h * kWinBytes;
+    long long* w_key = reinterpret_cast<long long*>(wbase);
+    int32_t* w_id = reinterpret_cast<int32_t*>(w_key + kWin);
+    int32_t* w_pk = w_id + kWin;
+    int32_t* w_pl = w_pk + kWin;
+    int32_t* w_pm = w_pl + kWin;
+    uint32_t* w_q = reinterpret_cast<uint32_t*>(w_pm + kWin);
+    for (int w = h; w < s_nw; w += 2) {
+      const int k0 = wb[w], k1 = wb[w + 1];
+      const int ws = k0 == 0 ? 0 : segend[k0 - 1];
+      const int n = segend[k1 - 1] - ws;
+      if (n > kWin) {  // one bucket wider than a window: rank in global memory
+        const int4* rec = ss.rec + i0 + ws;
+        for (int i = ht; i < n; i += kHalfT) {
+          const int4 r = rec[i];
+          const long long key = ((long long)r.y << 32) | (unsigned)r.x;
+          int rank = 0;
+          for (int j = 0; j < n; ++j) {
+            const int4 o = rec[j];
+            const long long kj = ((long long)o.y << 32) | (unsigned)o.x;
+            rank += (kj > key || (kj == key && o.z < r.z)) ? 1 : 0;
+          }
+          ss.plen_r[i0 + ws + rank] = r.w & 0xffff;
+          if (need_order) ss.order_r[i0 + ws + rank] = r.z;
+        }
+        half_sync(h);
+        if (ht == 0) {
+          int pm = 0;
+          for (int j = 0; j < n; ++j) {
+            pm = max(pm, ss.plen_r[i0 + ws + j]);
+            ss.rinfo[i0 + ws + j] = make_int2(k0, pm << 16);
+          }
+          ss.seg[so + k0].x |= pm << 16;
+          int sm = 0;
+          for (int j = n - 1; j >= 0; --j) {
+            sm = max(sm, ss.plen_r[i0 + ws + j]);
+            ss.rinfo[i0 + ws + j].y |= sm;
+          }
+        }
+        half_sync(h);
+        continue;
+      }
+      for (int i = ht; i < n; i += kHalfT) {
+        const int4 r = ss.rec[i0 + ws + i];
+        const long long bits = ((long long)r.y << 32) | (unsigned)r.x;
+        const double p = __longlong_as_double(bits);
+        const double fm1 = ceil(p) - 1.0;
+        w_key[i] = bits;
+        w_q[i] = fm1 >= 1.0 ? (uint32_t)((bits - __double_as_longlong(fm1)) >> 21) : 0u;
+        w_id[i] = r.z;
+        w_pk[i] = r.w;
+      }
+      half_sync(h);
+      for (int i = ht; i < n; i += kHalfT) {
+        const int k = w_pk[i] >> 16;
+        const int lo = (k == 0 ? 0 : segend[k - 1]) - ws, hi = segend[k] - ws;
+        const uint32_t q = w_q[i];
+        int rank = 0;
+        for (int j = lo; j < hi; ++j) {
+          const uint32_t qj = w_q[j];
+          rank += qj > q ? 1 : 0;
+          if (qj == q && j != i) {
+            const long long kj = w_key[j], key = w_key[i];
+            rank += (kj > key || (kj == key && w_id[j] < w_id[i])) ? 1 : 0;
+          }
+        }
+        const int pl = w_pk[i] & 0xffff;
+        w_pl[lo + rank] = pl;
+        ss.plen_r[i0 + ws + lo + rank] = pl;
+        if (need_order) ss.order_r[i0 + ws + lo + rank] = w_id[i];
+      }
+      half_sync(h);
+      for (int k = k0 + ht; k < k1; k += kHalfT) {  // one thread per bucket
+        const int lo = (k == 0 ? 0 : segend[k - 1]) - ws, hi = segend[k] - ws;
+        int pm = 0;
+        for (int j = lo; j < hi; ++j) {
+          pm = max(pm, w_pl[j]);
+          w_pm[j] = pm;
+        }
+        ss.seg[so + k].x |= pm << 16;
+        int sm = 0;
+        for (int j = hi - 1; j >= lo; --j) {
+          sm = max(sm, w_pl[j]);
+          ss.rinfo[i0 + ws + j] = make_int2(k, sm | (w_pm[j] << 16));
         }
       }
-      const int pl = w_pk[i] & 0xffff;
-      w_pl[lo + rank] = pl;
-      ss.plen_r[i0 + ws + lo + rank] = pl;
-      ss.order_r[i0 + ws + lo + rank] = w_id[i];
+      half_sync(h);
     }
-    __syncthreads();
-    for (int k = k0 + tid; k < k1; k += kBuildT) {  // one thread per bucket
-      const int lo = (k == 0 ? 0 : segend[k - 1]) - ws, hi = segend[k] - ws;
-      int pm = 0;
-      for (int j = lo; j < hi; ++j) {
-        pm = max(pm, w_pl[j]);
-        w_pm[j] = pm;
-      }
-      ss.seg[so + k].x |= pm << 16;
-      int sm = 0;
-      for (int j = hi - 1; j >= lo; --j) {
-        sm = max(sm, w_pl[j]);
-        ss.rinfo[i0 + ws + j] = make_int2(k, sm | (w_pm[j] << 16));
-      }
-    }
-    __syncthreads();
-    k0 = k1;
-    ws += n;
   }
   // Range-max helpers: per 16-segment block the in-block prefix / suffix
   // maxima and previous-greater distances, then a sparse table over block
@@ -367,7 +421,7 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
 
 int fast_build(rs_ctx* ctx, int S, const int64_t* d_off, double* pred, int32_t* plen,
                FastSS ss, const GenSpec* gen, const double* nz, const double* lnz,
-               bool keep_inputs) {
+               bool keep_inputs, bool need_order) {
   (void)d_off;
   const int smem = kBuildSmem;
   RS_CUDA_TRY(cudaFuncSetAttribute(fast_build_kernel<true>,
@@ -378,10 +432,10 @@ int fast_build(rs_ctx* ctx, int S, const int64_t* d_off, double* pred, int32_t* 
   if (gen) {
     g = *gen;
     RS_LAUNCH(ctx, "fast_build", fast_build_kernel<true>, S, kBuildT, smem, g, nz, lnz, pred,
-              plen, ss, ctx->d_flags, keep_inputs ? 1 : 0);
+              plen, ss, ctx->d_flags, keep_inputs ? 1 : 0, need_order ? 1 : 0);
   } else {
     RS_LAUNCH(ctx, "fast_build", fast_build_kernel<false>, S, kBuildT, smem, g, nz, lnz, pred,
-              plen, ss, ctx->d_flags, 1);
+              plen, ss, ctx->d_flags, 1, need_order ? 1 : 0);
   }
   return RS_OK;
 }

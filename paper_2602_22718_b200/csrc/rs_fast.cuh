@@ -88,7 +88,7 @@ __device__ __forceinline__ void fast_gen(const GenSpec& g, const double* nz, con
 // the fast path's range.
 int fast_build(rs_ctx* ctx, int S, const int64_t* d_off, double* pred, int32_t* plen,
                FastSS ss, const GenSpec* gen, const double* nz, const double* lnz,
-               bool keep_inputs = true);
+               bool keep_inputs = true, bool need_order = true);
 
 struct CandRange {
   int n_min, n_max;

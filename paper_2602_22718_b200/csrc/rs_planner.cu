@@ -605,12 +605,13 @@ static size_t built_bytes(int64_t n, int S, bool with_generic) {
 // pred / plen: id-ordered device arrays (written by the generator when gen).
 static int build_batch(rs_ctx* ctx, int S, const int64_t* d_off, int64_t n, double* pred,
                        int32_t* plen, const GenSpec* gen, const double* nz, const double* lnz,
-                       bool allow_fast, Built* out, bool keep_inputs = true) {
+                       bool allow_fast, Built* out, bool keep_inputs = true,
+                       bool need_order = true) {
   if (allow_fast) {
     out->fss = fast_ss_alloc(ctx, d_off, n, S);
     if (!out->fss.rec) return fail(RS_E_NOMEM, "arena exhausted (fast structure)");
     RS_TRY(clear_flags(ctx));
-    RS_TRY(fast_build(ctx, S, d_off, pred, plen, out->fss, gen, nz, lnz, keep_inputs));
+    RS_TRY(fast_build(ctx, S, d_off, pred, plen, out->fss, gen, nz, lnz, keep_inputs, need_order));
     if (gen) {  // in range by construction (fast_spec_ok)
       out->fast = true;
       return RS_OK;
@@ -749,12 +750,12 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
       GenSpec g = to_gen(spec, spec->first_scenario + s0);
       if (gen_fast) {
         // the generated scenarios only feed the structure: not stored
-        RS_TRY(build_batch(ctx, Sb, d_off, n, pred, plen, &g, nz, lnz, true, &built, false));
+        RS_TRY(build_batch(ctx, Sb, d_off, n, pred, plen, &g, nz, lnz, true, &built, false, false));
       } else {
         RS_LAUNCH(ctx, "gen_scenarios", gen_scenarios_kernel, grid_for(ctx, n, 256), 256, 0, g,
                   nz, lnz, Sb, pred, plen);
         RS_TRY(build_batch(ctx, Sb, d_off, n, pred, plen, nullptr, nullptr, nullptr, allow_fast,
-                           &built));
+                           &built, true, false));
       }
     } else {
       const double* src_p = h_pred + (size_t)s0 * P;
@@ -773,7 +774,7 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
       RS_TRY(read_flags(ctx, &fl));
       if (fl) return flags_to_status(fl);
       RS_TRY(build_batch(ctx, Sb, d_off, n, pred, plen, nullptr, nullptr, nullptr, allow_fast,
-                         &built));
+                         &built, true, false));
     }
     double* o_tt = (device_ptrs && out->t_total) ? out->t_total + (size_t)s0 * C : b_tt;
     double* o_cc = (device_ptrs && out->cost) ? out->cost + (size_t)s0 * C : b_cc;
