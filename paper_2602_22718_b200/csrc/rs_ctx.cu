@@ -310,6 +310,7 @@ int rs_ctx_destroy(rs_ctx* ctx) {
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
   for (auto& pc : ctx->profiles) cudaFree(pc.mem);
   if (ctx->arena) cudaFree(ctx->arena);
+  if (ctx->in_buf) cudaFree(ctx->in_buf);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->d_flags) cudaFree(ctx->d_flags);
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);

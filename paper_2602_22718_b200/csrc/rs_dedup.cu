@@ -547,9 +547,18 @@ uint32_t pow2_at_least(int64_t v) {
 // Runs the refinement on device-resident CSR. cap_len = INT32_MAX for the
 // full index. Fills node_diff/end_count/len_count/stats (and labels if
 // non-null). Host-synchronous (one flag read per round).
+// tail (nullable): enqueued after every block of rounds, before the host
+// checks for completion, so work that consumes the final state (the tables
+// and their read-back) shares that synchronisation; it runs again if more
+// rounds follow.
+struct RefineTail {
+  virtual int enqueue(rs_ctx* ctx, const DedupState& st, int max_len) = 0;
+};
+
 static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off, int P,
                         int32_t cap_len, int strict, bool want_labels, int32_t max_len_hint,
-                        DedupState* out_state, int64_t* h_stats, int32_t* h_labels) {
+                        DedupState* out_state, int64_t* h_stats, int32_t* h_labels,
+                        RefineTail* tail = nullptr) {
   constexpr int kRoundsPerSync = 4;
   constexpr int kMaxRounds = 1 << 20;
   const uint32_t cap = pow2_at_least(2 * (int64_t)P + 2);
@@ -642,11 +651,15 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
     }
     int left = 0;
     RS_TRY(d2h(ctx, &left, kc + kRoundsPerSync, 4));
+    if (tail) {
+      if (h_stats) RS_TRY(d2h(ctx, h_stats, st.stats, 4 * 8));
+      RS_TRY(tail->enqueue(ctx, st, md));
+    }
     RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     if (left <= 0) break;
     RS_CUDA_TRY(cudaMemcpyAsync(kc, kc + kRoundsPerSync, 4, cudaMemcpyDeviceToDevice, ctx->stream));
   }
-  if (h_stats) RS_TRY(d2h(ctx, h_stats, st.stats, 4 * 8));
+  if (h_stats && !tail) RS_TRY(d2h(ctx, h_stats, st.stats, 4 * 8));
   if (h_labels && P > 0) RS_TRY(d2h(ctx, h_labels, st.labels, 4ull * P));
   *out_state = st;
   return RS_OK;
@@ -665,16 +678,29 @@ struct rs_prefix_index {
 static int build_index_device(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
                               int32_t P, rs_prefix_index** out) {
   if (P <= 0) return fail(RS_E_VALIDATION, "prefix index needs a non-empty batch");
+  // The tables kernel and its read-back ride on the refinement's final
+  // synchronisation (max_len is known after the lengths pass).
+  struct Tables : RefineTail {
+    int64_t* d = nullptr;
+    std::vector<int64_t> h;
+    int md = -1;
+    int enqueue(rs_ctx* c, const DedupState& st, int max_len) override {
+      if (md < 0) {
+        md = max_len;
+        d = arena_alloc<int64_t>(c, 5ull * (md + 2));
+        if (!d) return fail(RS_E_NOMEM, "arena exhausted (tables)");
+        h.resize(5ull * (md + 2));
+      }
+      RS_LAUNCH(c, "dedup_tables", tables_kernel, 1, kTabT, 0, st, md, d);
+      return d2h(c, h.data(), d, 8 * h.size());
+    }
+  } tab;
   DedupState st;
   int64_t stats[4];
-  RS_TRY(dedup_refine(ctx, d_tok, d_off, P, INT32_MAX, 1, false, 0, &st, stats, nullptr));
-  const int md = (int)stats[1];
-  int64_t* d_tables = arena_alloc<int64_t>(ctx, 5ull * (md + 2));
-  if (!d_tables) return fail(RS_E_NOMEM, "arena exhausted (tables)");
-  RS_LAUNCH(ctx, "dedup_tables", tables_kernel, 1, kTabT, 0, st, md, d_tables);
-  std::vector<int64_t> h(5ull * (md + 2));
-  RS_TRY(d2h(ctx, h.data(), d_tables, 8 * h.size()));
+  RS_TRY(dedup_refine(ctx, d_tok, d_off, P, INT32_MAX, 1, false, 0, &st, stats, nullptr, &tab));
   RS_TRY(sync_and_check(ctx));
+  const int md = (int)stats[1];
+  std::vector<int64_t>& h = tab.h;
   auto* idx = new rs_prefix_index();
   idx->batch = P;
   idx->min_len = (int32_t)stats[0];
@@ -689,15 +715,11 @@ static int build_index_device(rs_ctx* ctx, const int32_t* d_tok, const int64_t* 
   return RS_OK;
 }
 
-// Copy a host CSR into dedicated device buffers (kept outside the arena,
-// which the refinement re-reserves).
+// Copy a host CSR into the context's grow-only input buffer (outside the
+// arena, which the refinement re-reserves): no per-call allocation.
 struct DeviceCSR {
   int32_t* tok = nullptr;
   int64_t* off = nullptr;
-  ~DeviceCSR() {
-    if (tok) cudaFree(tok);
-    if (off) cudaFree(off);
-  }
 };
 
 static int upload_csr(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets, int32_t count,
@@ -706,15 +728,30 @@ static int upload_csr(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets
   if (!offsets) return fail(RS_E_ARG, "offsets is NULL");
   int64_t ntok = offsets[count] - offsets[0];
   if (ntok < 0) return fail(RS_E_VALIDATION, "offsets must be non-decreasing");
-  if (cudaMalloc(&d->tok, std::max<int64_t>(ntok, 1) * 4 + 16) != cudaSuccess ||
-      cudaMalloc(&d->off, 8ull * (count + 1)) != cudaSuccess) {
-    cudaGetLastError();
-    return fail(RS_E_NOMEM, "device CSR allocation failed");
+  const size_t tok_bytes = abytes(std::max<int64_t>(ntok, 1) + 4, 4);
+  const size_t need = tok_bytes + abytes((size_t)count + 1, 8);
+  if (need > ctx->in_cap) {
+    RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (ctx->in_buf) cudaFree(ctx->in_buf);
+    ctx->in_buf = nullptr;
+    ctx->in_cap = 0;
+    if (cudaMalloc(&ctx->in_buf, need) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(RS_E_NOMEM, "device CSR allocation failed");
+    }
+    ctx->in_cap = need;
   }
-  std::vector<int64_t> rel(count + 1);
-  for (int32_t i = 0; i <= count; ++i) rel[i] = offsets[i] - offsets[0];
+  d->tok = reinterpret_cast<int32_t*>(ctx->in_buf);
+  d->off = reinterpret_cast<int64_t*>(ctx->in_buf + tok_bytes);
   if (ntok) RS_TRY(h2d(ctx, d->tok, tokens + offsets[0], 4ull * ntok));
-  RS_TRY(h2d(ctx, d->off, rel.data(), 8ull * (count + 1)));
+  if (offsets[0] == 0) {
+    RS_TRY(h2d(ctx, d->off, offsets, 8ull * (count + 1)));
+  } else {
+    std::vector<int64_t> rel(count + 1);
+    for (int32_t i = 0; i <= count; ++i) rel[i] = offsets[i] - offsets[0];
+    RS_TRY(h2d(ctx, d->off, rel.data(), 8ull * (count + 1)));
+    RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // rel is a local
+  }
   return RS_OK;
 }
 

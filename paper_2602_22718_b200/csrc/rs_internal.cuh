@@ -115,6 +115,10 @@ struct rs_ctx {
   std::vector<cudaEvent_t> event_pool;
   std::vector<rs::ProfileCache> profiles;
   int num_sms = 148;
+  // Grow-only device copy of host inputs (CSR token batches), kept apart
+  // from the arena, which may grow during a call.
+  char* in_buf = nullptr;
+  size_t in_cap = 0;
 };
 
 namespace rs {
