@@ -190,7 +190,7 @@ def config(args, world):
             "scenarios": args.scenarios, "candidates": [args.n_min, args.n_max],
             "prompts": args.prompts, "G": args.G, "lambda": args.lam, "gpus_per_actor": 2,
             "profile": "default_profile()", "parallelism": f"scenario-sharded x{world}",
-            "l2": "inputs larger than L2 (per-batch scenario scratch ~2 GiB)"}
+            "l2": "inputs larger than L2 (per-batch scenario structures ~7 GiB, batches of 1,184 scenarios)"}
 
 
 # ----------------------------------------------------------------- our arm
