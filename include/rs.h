@@ -40,7 +40,8 @@ typedef enum rs_status {
   RS_E_CUDA = 3,       /* CUDA runtime / launch failure, or no device */
   RS_E_NOMEM = 4,      /* device or pinned allocation failed */
   RS_E_ARG = 5,        /* NULL handle / pointer misuse (programming error) */
-  RS_E_PLACEMENT = 6   /* rollsim::PlacementError (cluster cannot host the plan) */
+  RS_E_PLACEMENT = 6,  /* rollsim::PlacementError (cluster cannot host the plan) */
+  RS_E_PARSE = 7       /* rollsim::ParseError (malformed trace text) */
 } rs_status;
 
 const char* rs_last_error(void);
@@ -307,6 +308,32 @@ int rs_predict_lengths(rs_ctx* ctx, const double* obs, const int32_t* depth,
                        double alpha, int32_t max_response_len, const rs_noise_model* noise,
                        const char* id_bytes, const int64_t* id_offsets, int device_ptrs,
                        double* out);
+
+/* ------------------------------------------------------------------ */
+/* (1b) Trace prompt table -> device CSR                */
+/* ------------------------------------------------------------------ */
+/* The '# prompt <id> <ground_truth> <tok>...' metadata of a CSV trace
+ * (csv_from_string, workload.cpp:169-263; the step rows are not parsed
+ * here), parsed on the device from the file bytes (host, or device memory
+ * when device_ptr != 0) into an id-sorted token CSR in HBM that
+ * rs_prefix_index_build_device takes directly. Errors in the reference's
+ * order: RS_E_PARSE (malformed metadata, missing or misplaced column
+ * header), then RS_E_VALIDATION (WorkloadTrace::validate's prompt rules). */
+typedef struct rs_trace_csr rs_trace_csr;
+int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes, int device_ptr,
+                       rs_trace_csr** out);
+int rs_trace_csr_info(const rs_trace_csr* trace, int32_t* count, int64_t* n_tokens,
+                      int64_t* id_bytes, int32_t* g, int32_t* max_prompt_len,
+                      int32_t* max_response_len);
+/* Device views, valid until rs_trace_csr_free: tokens[n_tokens] (int32),
+ * offsets[count + 1] (int64), prompts in id order. */
+int rs_trace_csr_device(const rs_trace_csr* trace, const int32_t** d_tokens,
+                        const int64_t** d_offsets);
+/* Host copies (any pointer may be NULL): tokens[n_tokens], offsets[count+1],
+ * id_bytes[id_bytes], id_offsets[count+1], ground_truth[count]. */
+int rs_trace_csr_copy(rs_ctx* ctx, const rs_trace_csr* trace, int32_t* tokens, int64_t* offsets,
+                      char* id_bytes, int64_t* id_offsets, int32_t* ground_truth);
+void rs_trace_csr_free(rs_trace_csr* trace);
 
 /* ------------------------------------------------------------------ */
 /* Monte-Carlo scaling sweep: scale() for every        */

@@ -14,7 +14,7 @@
  * --impl reference legs may load these libraries.
  *
  * Status codes match include/rs.h: 0 ok, 1 ValidationError, 2 ConfigError,
- * 5 other error, 6 PlacementError.
+ * 5 other error, 6 PlacementError, 7 ParseError.
  */
 #ifndef RS_ORACLE_H_
 #define RS_ORACLE_H_
@@ -92,6 +92,10 @@ extern "C" {
 
 ORACLE_API(ref_)
 ORACLE_API(orc_)
+
+/* Reference-only: the prompt table of a CSV trace via trace_from_string. */
+int ref_trace_prompts(const char* text, int64_t n_bytes, int64_t* info, int32_t* tokens,
+                      int64_t* offsets, char* ids, int64_t* id_offsets, int32_t* gt);
 
 /* Builder-defined oracles (port only). */
 int orc_generate_scenarios(const rs_scenario_spec* spec, double* pred,

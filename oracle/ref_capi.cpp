@@ -44,6 +44,9 @@ int guarded(F&& f) {
   } catch (const rollsim::PlacementError& e) {
     g_err = e.what();
     return 6;
+  } catch (const rollsim::ParseError& e) {
+    g_err = e.what();
+    return 7;
   } catch (const std::exception& e) {
     g_err = e.what();
     return 5;
@@ -385,6 +388,42 @@ int ref_predict_lengths(const double* obs, const int32_t* depth, const int32_t* 
       p.ground_truth_len = gt[i];
       out[i] = nm.kind == rollsim::NoiseModel::Kind::identity ? h.predict(p) : h.predict_noisy(p, nm);
     }
+  });
+}
+
+// The prompt table of a CSV trace through the reference's own reader
+// (trace_from_string, workload.cpp:355-359): info = {count, n_tokens,
+// id_bytes, g, max_prompt_len, max_response_len}; the arrays (nullable) get
+// the id-sorted prompts.
+int ref_trace_prompts(const char* text, int64_t n_bytes, int64_t* info, int32_t* tokens,
+                      int64_t* offsets, char* ids, int64_t* id_offsets, int32_t* gt) {
+  return guarded([&] {
+    rollsim::WorkloadTrace t =
+        rollsim::trace_from_string(std::string(text, text + n_bytes), rollsim::TraceFormat::csv);
+    int64_t ntok = 0, nid = 0;
+    for (const auto& p : t.prompts) {
+      ntok += (int64_t)p.token_ids.size();
+      nid += (int64_t)p.id.size();
+    }
+    info[0] = (int64_t)t.prompts.size();
+    info[1] = ntok;
+    info[2] = nid;
+    info[3] = t.responses_per_prompt;
+    info[4] = t.limits.max_prompt_len;
+    info[5] = t.limits.max_response_len;
+    int64_t to = 0, io = 0;
+    for (size_t i = 0; i < t.prompts.size(); ++i) {
+      const auto& p = t.prompts[i];
+      if (offsets) offsets[i] = to;
+      if (id_offsets) id_offsets[i] = io;
+      if (tokens) std::copy(p.token_ids.begin(), p.token_ids.end(), tokens + to);
+      if (ids) std::copy(p.id.begin(), p.id.end(), ids + io);
+      if (gt) gt[i] = p.ground_truth_len;
+      to += (int64_t)p.token_ids.size();
+      io += (int64_t)p.id.size();
+    }
+    if (offsets) offsets[t.prompts.size()] = to;
+    if (id_offsets) id_offsets[t.prompts.size()] = io;
   });
 }
 

@@ -110,6 +110,11 @@ PRODUCT_SIGS = {
                          C.POINTER(RsScaleOut)], C.c_int),
     "rs_predict_lengths": ([vp, vp, vp, vp, i32, i32, f64, i32, P_noise, vp, vp, C.c_int, vp],
                            C.c_int),
+    "rs_trace_csr_parse": ([vp, vp, i64, C.c_int, C.POINTER(vp)], C.c_int),
+    "rs_trace_csr_info": ([vp, P_i32, P_i64, P_i64, P_i32, P_i32, P_i32], C.c_int),
+    "rs_trace_csr_device": ([vp, C.POINTER(vp), C.POINTER(vp)], C.c_int),
+    "rs_trace_csr_copy": ([vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "rs_trace_csr_free": ([vp], None),
     "rs_scale_select": ([vp, P_f64, P_f64, P_f64, i32, i32, f64, P_f64, P_f64, P_f64, P_i32], C.c_int),
     "rs_generate_scenarios": ([vp, C.POINTER(RsScenarioSpec), vp, vp, C.c_int], C.c_int),
     "rs_sweep": ([vp, C.POINTER(RsScenarioSpec), P_prof, i32, i32, i32, f64, i32,
@@ -140,6 +145,10 @@ ORACLE_SIGS = {
                       P_f64, P_f64, P_f64, P_f64, P_f64, P_f64, P_i32, P_f64], C.c_int),
     "predict_lengths": ([P_f64, P_i32, P_i32, i32, i32, f64, i32, P_noise, C.c_char_p, P_i64,
                          P_f64], C.c_int),
+}
+
+REF_ONLY_SIGS = {
+    "ref_trace_prompts": ([vp, i64, P_i64, vp, vp, vp, vp, vp], C.c_int),
 }
 
 PORT_ONLY_SIGS = {

@@ -975,6 +975,88 @@ __global__ void lpt_gather_kernel(const double* pred_id, const uint32_t* vals,
 
 using namespace rs;
 
+__global__ void gather_keys_kernel(const uint64_t* src, const uint32_t* perm, int64_t n,
+                                   uint64_t* keys, uint32_t* vals) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    keys[j] = src[perm[j]];
+    vals[j] = perm[j];
+  }
+}
+
+__global__ void rank_scatter_kernel(const uint32_t* perm, int64_t n, int32_t* rank) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    rank[perm[j]] = (int32_t)j;
+}
+
+__global__ void iota_kernel(uint32_t* v, int64_t n) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    v[j] = (uint32_t)j;
+}
+
+// LSD radix over (length, then 8-byte big-endian words from the last to the
+// first): lexicographic unsigned-byte order with a proper prefix first.
+// Big-endian 8-byte words of each string (zero padded); plane 0 = length.
+__global__ void string_words_kernel(const char* bytes, const int64_t* off, int64_t n, int64_t W,
+                                    uint64_t* words) {
+  const int64_t total = (W + 1) * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t plane = t / n, i = t - plane * n;
+    const int64_t a = off[i], len = off[i + 1] - a;
+    uint64_t w = 0;
+    if (plane == 0) {
+      w = (uint64_t)len;
+    } else {
+      const int64_t b0 = (plane - 1) * 8;
+      for (int b = 0; b < 8 && b0 + b < len; ++b)
+        w |= (uint64_t)(unsigned char)bytes[a + b0 + b] << (56 - 8 * b);
+    }
+    words[t] = w;
+  }
+}
+
+namespace rs {
+
+size_t rank_strings_device_bytes(int64_t n, int64_t maxlen) {
+  const int64_t W = (maxlen + 7) / 8;
+  return abytes((W + 1) * n, 8) + abytes(n, 8) + abytes(n, 4) + radix_sort_scratch_bytes64(n) + 1024;
+}
+
+// d_perm[r] = index of the string of rank r in std::string order: LSD radix
+// passes over the length plane, then the word planes last to first (a
+// shorter string that is a prefix of a longer one sorts first, as its zero
+// padding ties and the length decides). Allocates from the arena (the caller
+// reserves rank_strings_device_bytes).
+int rank_strings_device(rs_ctx* ctx, const char* d_bytes, const int64_t* d_off, int64_t n,
+                        int64_t maxlen, uint32_t* d_perm) {
+  if (n <= 0) return RS_OK;
+  const int64_t W = (maxlen + 7) / 8;
+  uint64_t* d_words = arena_alloc<uint64_t>(ctx, (W + 1) * n);
+  uint64_t* keys = arena_alloc<uint64_t>(ctx, n);
+  uint32_t* vals = arena_alloc<uint32_t>(ctx, n);
+  char* scratch = arena_alloc<char>(ctx, radix_sort_scratch_bytes64(n));
+  if (!scratch) return fail(RS_E_NOMEM, "arena exhausted (rank_strings)");
+  RS_LAUNCH(ctx, "string_words", string_words_kernel, grid_for(ctx, (W + 1) * n, 256), 256, 0,
+            d_bytes, d_off, n, W, d_words);
+  const int blocks = grid_for(ctx, n, 256);
+  RS_LAUNCH(ctx, "iota", iota_kernel, blocks, 256, 0, d_perm, n);
+  for (int64_t plane = 0; plane <= W; ++plane) {
+    const int64_t w = plane == 0 ? 0 : W + 1 - plane;  // length first, then last word .. first
+    RS_LAUNCH(ctx, "gather_keys", gather_keys_kernel, blocks, 256, 0, d_words + w * n, d_perm, n,
+              keys, vals);
+    uint64_t* ko;
+    uint32_t* vo;
+    RS_TRY(radix_sort_pairs(ctx, keys, vals, n, scratch, &ko, &vo));
+    RS_CUDA_TRY(cudaMemcpyAsync(d_perm, vo, 4 * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  return RS_OK;
+}
+
+}  // namespace rs
+
 extern "C" {
 
 int rs_generate_scenarios(rs_ctx* ctx, const rs_scenario_spec* spec, double* pred,
@@ -1161,29 +1243,6 @@ int rs_scale_select(rs_ctx* ctx, const double* t_total, const double* t_penalty,
   return sync_and_check(ctx);
 }
 
-__global__ void gather_keys_kernel(const uint64_t* src, const uint32_t* perm, int64_t n,
-                                   uint64_t* keys, uint32_t* vals) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    keys[j] = src[perm[j]];
-    vals[j] = perm[j];
-  }
-}
-
-__global__ void rank_scatter_kernel(const uint32_t* perm, int64_t n, int32_t* rank) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x)
-    rank[perm[j]] = (int32_t)j;
-}
-
-__global__ void iota_kernel(uint32_t* v, int64_t n) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x)
-    v[j] = (uint32_t)j;
-}
-
-// LSD radix over (length, then 8-byte big-endian words from the last to the
-// first): lexicographic unsigned-byte order with a proper prefix first.
 int rs_rank_strings(rs_ctx* ctx, const char* bytes, const int64_t* offsets, int32_t count,
                     int32_t* rank) {
   if (!ctx || !offsets || !rank) return fail(RS_E_ARG, "NULL argument");
@@ -1194,38 +1253,20 @@ int rs_rank_strings(rs_ctx* ctx, const char* bytes, const int64_t* offsets, int3
     if (l < 0) return fail(RS_E_ARG, "offsets must be non-decreasing");
     maxlen = std::max(maxlen, l);
   }
-  const int64_t W = (maxlen + 7) / 8;
-  std::vector<uint64_t> words((size_t)(W + 1) * count, 0);  // plane 0 = length
-  for (int32_t i = 0; i < count; ++i) {
-    const unsigned char* p = (const unsigned char*)bytes + offsets[i];
-    const int64_t l = offsets[i + 1] - offsets[i];
-    words[i] = (uint64_t)l;
-    for (int64_t b = 0; b < l; ++b)
-      words[(size_t)(1 + b / 8) * count + i] |= (uint64_t)p[b] << (56 - 8 * (b % 8));
-  }
-  const int64_t n = count;
-  RS_TRY(arena_reserve(ctx, abytes((W + 1) * n, 8) + abytes(n, 8) + abytes(n, 4) * 2 +
-                                abytes(n, 4) + radix_sort_scratch_bytes64(n) + 4096));
-  uint64_t* d_words = arena_alloc<uint64_t>(ctx, (W + 1) * n);
-  uint64_t* keys = arena_alloc<uint64_t>(ctx, n);
+  const int64_t n = count, nb = offsets[count] - offsets[0];
+  RS_TRY(arena_reserve(ctx, abytes(nb + 1, 1) + abytes(n + 1, 8) + abytes(n, 4) * 2 +
+                                rank_strings_device_bytes(n, maxlen) + 4096));
+  char* d_bytes = arena_alloc<char>(ctx, nb + 1);
+  int64_t* d_off = arena_alloc<int64_t>(ctx, n + 1);
   uint32_t* perm = arena_alloc<uint32_t>(ctx, n);
-  uint32_t* vals = arena_alloc<uint32_t>(ctx, n);
   int32_t* d_rank = arena_alloc<int32_t>(ctx, n);
-  char* scratch = arena_alloc<char>(ctx, radix_sort_scratch_bytes64(n));
-  if (!scratch) return fail(RS_E_NOMEM, "arena exhausted (rank_strings)");
-  RS_TRY(h2d(ctx, d_words, words.data(), 8 * words.size()));
-  const int blocks = grid_for(ctx, n, 256);
-  RS_LAUNCH(ctx, "iota", iota_kernel, blocks, 256, 0, perm, n);
-  for (int64_t plane = 0; plane <= W; ++plane) {
-    const int64_t w = plane == 0 ? 0 : W + 1 - plane;  // length first, then last word .. first
-    RS_LAUNCH(ctx, "gather_keys", gather_keys_kernel, blocks, 256, 0, d_words + w * n, perm, n,
-              keys, vals);
-    uint64_t* ko;
-    uint32_t* vo;
-    RS_TRY(radix_sort_pairs(ctx, keys, vals, n, scratch, &ko, &vo));
-    RS_CUDA_TRY(cudaMemcpyAsync(perm, vo, 4 * n, cudaMemcpyDeviceToDevice, ctx->stream));
-  }
-  RS_LAUNCH(ctx, "rank_scatter", rank_scatter_kernel, blocks, 256, 0, perm, n, d_rank);
+  if (!d_rank) return fail(RS_E_NOMEM, "arena exhausted (rank_strings)");
+  std::vector<int64_t> rel(n + 1);
+  for (int64_t i = 0; i <= n; ++i) rel[i] = offsets[i] - offsets[0];
+  if (nb) RS_TRY(h2d(ctx, d_bytes, bytes + offsets[0], nb));
+  RS_TRY(h2d(ctx, d_off, rel.data(), 8 * (n + 1)));
+  RS_TRY(rank_strings_device(ctx, d_bytes, d_off, n, maxlen, perm));
+  RS_LAUNCH(ctx, "rank_scatter", rank_scatter_kernel, grid_for(ctx, n, 256), 256, 0, perm, n, d_rank);
   RS_TRY(d2h(ctx, rank, d_rank, 4 * n));
   return sync_and_check(ctx);
 }

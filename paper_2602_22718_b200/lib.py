@@ -20,7 +20,7 @@ LIB_PATH = PKG_DIR / "librs_b200.so"
 if os.environ.get("RS_B200_LIB"):  # A/B runs of another build of the same C-ABI
     LIB_PATH = pathlib.Path(os.environ["RS_B200_LIB"]).resolve()
 
-RS_OK, RS_E_VALIDATION, RS_E_CONFIG, RS_E_CUDA, RS_E_NOMEM, RS_E_ARG, RS_E_PLACEMENT = range(7)
+RS_OK, RS_E_VALIDATION, RS_E_CONFIG, RS_E_CUDA, RS_E_NOMEM, RS_E_ARG, RS_E_PLACEMENT, RS_E_PARSE = range(8)
 
 
 class Error(RuntimeError):
@@ -37,6 +37,10 @@ class ValidationError(Error):
 
 class PlacementError(Error):
     """rollsim::PlacementError (errors.hpp:35-38)."""
+
+
+class ParseError(Error):
+    """rollsim::ParseError (errors.hpp:23-26)."""
 
 
 class DeviceError(Error):
@@ -76,6 +80,8 @@ def check(status):
         raise ConfigError(msg)
     if status == RS_E_PLACEMENT:
         raise PlacementError(msg)
+    if status == RS_E_PARSE:
+        raise ParseError(msg)
     raise DeviceError(f"rs status {status}: {msg}")
 
 

@@ -14,11 +14,12 @@ from typing import Callable, List, Optional, Sequence
 import numpy as np
 
 from . import _abi
-from .lib import (ConfigError, DeviceError, Error, PlacementError, ValidationError, as_f64,
-                  as_i32, as_i64, check, context, profile_struct, ptr)
+from .lib import (ConfigError, DeviceError, Error, ParseError, PlacementError,
+                  ValidationError, as_f64, as_i32, as_i64, check, context, profile_struct, ptr)
 
 __all__ = [
-    "Error", "ConfigError", "ValidationError", "PlacementError", "DeviceError",
+    "Error", "ConfigError", "ValidationError", "PlacementError", "ParseError", "DeviceError",
+    "TraceCSR",
     "ClusterTopology", "default_topology", "PlacementPenalty", "NoiseModel", "LengthHistory",
     "predict_lengths",
     "LatencyProfile", "default_profile", "Prompt", "PrefixIndex", "PrefillCapacity",
@@ -167,6 +168,69 @@ class PrefixIndex:
         arrs = [np.zeros(m + 1, np.int64)] + [np.zeros(m + 2, np.int64) for _ in range(4)]
         check(self._ctx.lib.rs_prefix_index_tables(self._h, *[ptr(a, C.c_int64) for a in arrs]))
         return arrs
+
+
+class TraceCSR:
+    """The prompt table of a CSV workload trace (csv_from_string,
+    proj/src/workload.cpp:169-263) parsed on the GPU into an id-sorted token
+    CSR in HBM (rs_trace_csr_parse). `prefix_index()` builds the dedup index
+    from that CSR without a host round trip."""
+
+    def __init__(self, text, device=False):
+        ctx = context()
+        self._ctx = ctx
+        h = C.c_void_p()
+        if device:  # a torch uint8 CUDA tensor
+            check(ctx.lib.rs_trace_csr_parse(ctx.handle, C.c_void_p(text.data_ptr()), text.numel(),
+                                             1, C.byref(h)))
+        else:
+            data = text.encode() if isinstance(text, str) else bytes(text)
+            buf = C.create_string_buffer(data, len(data))
+            check(ctx.lib.rs_trace_csr_parse(ctx.handle, buf, len(data), 0, C.byref(h)))
+        self._h = h
+        n, nt, nb = C.c_int32(), C.c_int64(), C.c_int64()
+        g, mp, mr = C.c_int32(), C.c_int32(), C.c_int32()
+        check(ctx.lib.rs_trace_csr_info(h, C.byref(n), C.byref(nt), C.byref(nb), C.byref(g),
+                                        C.byref(mp), C.byref(mr)))
+        self.count, self.n_tokens, self._nb = n.value, nt.value, nb.value
+        self.responses_per_prompt, self.max_prompt_len, self.max_response_len = (
+            g.value, mp.value, mr.value)
+
+    @staticmethod
+    def load(path):
+        with open(path, "rb") as f:
+            return TraceCSR(f.read())
+
+    def device(self):
+        """(tokens, offsets) device pointers, valid while this object lives."""
+        t, o = C.c_void_p(), C.c_void_p()
+        check(self._ctx.lib.rs_trace_csr_device(self._h, C.byref(t), C.byref(o)))
+        return t.value, o.value
+
+    def host(self):
+        tok = np.zeros(max(self.n_tokens, 1), np.int32)
+        off = np.zeros(self.count + 1, np.int64)
+        ids = C.create_string_buffer(max(self._nb, 1))
+        ioff = np.zeros(self.count + 1, np.int64)
+        gt = np.zeros(max(self.count, 1), np.int32)
+        check(self._ctx.lib.rs_trace_csr_copy(self._ctx.handle, self._h, tok.ctypes.data,
+                                              off.ctypes.data, ids, ioff.ctypes.data,
+                                              gt.ctypes.data))
+        raw = ids.raw[:self._nb]
+        return {"ids": [raw[ioff[i]:ioff[i + 1]].decode("latin-1") for i in range(self.count)],
+                "gt": gt[:self.count], "tokens": tok[:self.n_tokens], "offsets": off}
+
+    def prefix_index(self) -> "PrefixIndex":
+        t, o = self.device()
+        return PrefixIndex.build_device(t, o, self.count)
+
+    def __del__(self):
+        try:
+            if self._h:
+                self._ctx.lib.rs_trace_csr_free(self._h)
+                self._h = None
+        except Exception:
+            pass
 
 
 @dataclass

@@ -154,3 +154,35 @@ def predictor_cases():
                                max(1, min(max_len, [1, 7, 100, 512][t % 4])), rng.next_u64())
         out.append((window, alpha, max_len, obs, depth, gt, ids, noise))
     return out
+
+
+def trace_csv(prompts, g=1, max_prompt_len=None, max_response_len=None, steps=(), header=True,
+              extra_meta=()):
+    """A CSV workload trace in the reference's text format (csv_to_string,
+    proj/src/workload.cpp:146-167): prompts = [(id, gt, tokens)], steps =
+    [(step_idx, [(id, [lengths])])]."""
+    lines = ["# rollsim-trace v1", f"# g {g}"]
+    if max_prompt_len is not None:
+        lines.append(f"# max_prompt_len {max_prompt_len}")
+    if max_response_len is not None:
+        lines.append(f"# max_response_len {max_response_len}")
+    lines += list(extra_meta)
+    for pid, gt, toks in prompts:
+        lines.append(f"# prompt {pid} {gt} " + " ".join(str(t) for t in toks))
+    if header:
+        lines.append("step_idx,prompt_id,response_idx,actual_len")
+    for st, rows in steps:
+        for pid, lens in rows:
+            lines += [f"{st},{pid},{r},{v}" for r, v in enumerate(lens)]
+    return ("\n".join(lines) + "\n").encode()
+
+
+def random_trace(seed, n, max_len=64, g=2, shared=0):
+    rng = np.random.RandomState(seed)
+    head = rng.randint(0, 32000, shared).tolist()
+    prompts = []
+    for i in rng.permutation(n):
+        toks = head + rng.randint(0, 32000, rng.randint(1, max_len + 1)).tolist()
+        prompts.append((f"p{i:06d}", int(rng.randint(1, 2048)), toks))
+    steps = [(0, [(p[0], [int(x) for x in rng.randint(1, 2048, g)]) for p in prompts[: n // 2]])]
+    return trace_csv(prompts, g=g, max_prompt_len=max_len + shared, steps=steps)

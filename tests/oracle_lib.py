@@ -34,6 +34,8 @@ class Oracle:
         _abi.bind(self.lib, _abi.ORACLE_SIGS, prefix)
         if prefix == "orc_":
             _abi.bind(self.lib, _abi.PORT_ONLY_SIGS)
+        else:
+            _abi.bind(self.lib, _abi.REF_ONLY_SIGS)
 
     def fn(self, name):
         return getattr(self.lib, self.prefix + name)
@@ -183,6 +185,25 @@ class Oracle:
                                              ptr(off, C.c_int64) if off is not None else None,
                                              ptr(out, C.c_double)))
         return out[:n]
+
+    def trace_prompts(self, text: bytes):
+        """Reference only: the id-sorted prompt table of a CSV trace."""
+        info = np.zeros(6, np.int64)
+        buf = C.create_string_buffer(text, len(text))
+        self._chk(self.lib.ref_trace_prompts(buf, len(text), ptr(info, C.c_int64), None, None, None,
+                                             None, None))
+        n, nt, nb = (int(x) for x in info[:3])
+        tok = np.zeros(max(nt, 1), np.int32)
+        off = np.zeros(n + 1, np.int64)
+        ids = C.create_string_buffer(max(nb, 1))
+        ioff = np.zeros(n + 1, np.int64)
+        gt = np.zeros(max(n, 1), np.int32)
+        self._chk(self.lib.ref_trace_prompts(buf, len(text), ptr(info, C.c_int64), tok.ctypes.data,
+                                             off.ctypes.data, ids, ioff.ctypes.data, gt.ctypes.data))
+        raw = ids.raw[:nb]
+        return {"ids": [raw[ioff[i]:ioff[i + 1]].decode("latin-1") for i in range(n)],
+                "gt": gt[:n], "tokens": tok[:nt], "offsets": off, "g": int(info[3]),
+                "max_prompt_len": int(info[4]), "max_response_len": int(info[5])}
 
     def sweep_arrays(self, pred, plen, S, P, prof, g, n_min, n_max, lam, gpus, threads=1):
         pred, plen = as_f64(pred), as_i32(plen)
