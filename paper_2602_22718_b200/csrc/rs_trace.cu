@@ -112,27 +112,50 @@ __global__ void nl_count_kernel(const char* text, int64_t n, uint32_t* cnt) {
 }
 
 // line_start[0] = 0; line_start[1 + k] = position after the k-th newline.
+// Warp w of a block owns the contiguous eighth of the chunk; lane l holds
+// the 16-byte slice l of each 512-byte step, so slices, lanes and warps are
+// in byte order and exclusive scans give every newline its index.
 __global__ void nl_write_kernel(const char* text, int64_t n, const uint32_t* base,
                                 int64_t* line_start) {
-  __shared__ uint32_t wsum[kNlT / 32];
-  const int64_t b0 = blockIdx.x * kChunk, b1 = min(n, b0 + kChunk);
-  const int64_t per = kChunk / kNlT;  // 256 contiguous bytes per thread
-  const int64_t t0 = b0 + per * threadIdx.x, t1 = min(b1, t0 + per);
-  uint32_t c = 0;
-  for (int64_t j = t0; j < t1; ++j) c += text[j] == '\n';
+  __shared__ uint32_t wtot[kNlT / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t incl = warp_incl_sum(c);
-  if (lane == 31) wsum[w] = incl;
+  const int64_t b0 = blockIdx.x * kChunk, b1 = min(n, b0 + kChunk);
+  const int64_t per_w = kChunk / (kNlT / 32);
+  const int64_t w0 = min(b1, b0 + w * per_w), w1 = min(b1, w0 + per_w);
+  auto slice_mask = [&](int64_t i) -> uint32_t {  // bit j: byte i + j is '\n'
+    uint32_t m = 0;
+    if (i + 16 <= w1) {
+      const uint4 v = *reinterpret_cast<const uint4*>(text + i);
+      const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) m |= (uint32_t)(((ws[q] >> (8 * bb)) & 0xff) == '\n') << (4 * q + bb);
+    } else {
+      for (int64_t j = i; j < w1; ++j) m |= (uint32_t)(text[j] == '\n') << (j - i);
+    }
+    return m;
+  };
+  uint32_t tot = 0;
+  for (int64_t i = w0 + 16 * lane; i < w1; i += 512) tot += __popc(slice_mask(i));
+  tot = warp_sum(tot);
+  if (lane == 0) wtot[w] = tot;
   __syncthreads();
-  if (w == 0) {
-    const uint32_t x = lane < kNlT / 32 ? wsum[lane] : 0;
-    const uint32_t xi = warp_incl_sum(x);
-    if (lane < kNlT / 32) wsum[lane] = xi - x;
+  int64_t k = base[blockIdx.x];
+  for (int q = 0; q < w; ++q) k += wtot[q];
+  for (int64_t s0 = w0; s0 < w1; s0 += 512) {
+    const int64_t i = s0 + 16 * lane;
+    uint32_t m = i < w1 ? slice_mask(i) : 0u;
+    const uint32_t c = __popc(m);
+    const uint32_t incl = warp_incl_sum(c);
+    int64_t pos = k + incl - c;
+    while (m) {
+      const int j = __ffs(m) - 1;
+      line_start[1 + pos++] = i + j + 1;
+      m &= m - 1;
+    }
+    k += __shfl_sync(0xffffffffu, incl, 31);
   }
-  __syncthreads();
-  int64_t k = (int64_t)base[blockIdx.x] + wsum[w] + incl - c;
-  for (int64_t j = t0; j < t1; ++j)
-    if (text[j] == '\n') line_start[1 + k++] = j + 1;
   if (blockIdx.x == 0 && threadIdx.x == 0) line_start[0] = 0;
 }
 
@@ -217,29 +240,35 @@ __global__ void classify_kernel(const char* text_c, const int64_t* line_start, i
       const int64_t ts = li.tok_pos;
       int count = 0;       // complete fields so far (warp-uniform)
       int stop = -1;       // tokens when the list ended (warp-uniform)
+      int run = 0;         // non-space characters ending the previous chunk
       bool prev_ws = true;
       if (ts < e && !is_ws(t[ts])) li.serial = 1;  // something glued to gt
       for (int64_t c0 = ts; c0 < e && stop < 0 && !li.serial; c0 += 32) {
         const int64_t i = c0 + lane;
         const bool in = i < e;
-        const bool ws = in ? is_ws(t[i]) : true;
+        const unsigned char ch = in ? t[i] : ' ';
+        const bool ws = is_ws(ch);
         const bool up = __shfl_up_sync(0xffffffffu, ws, 1);  // every lane takes part
-      const bool pws = lane == 0 ? prev_ws : up;
-        const bool start = in && !ws && pws;
+        const bool start = !ws && (lane == 0 ? prev_ws : up);
+        const unsigned char nx = i + 1 < e ? t[i + 1] : ' ';
+        const bool digit = ch >= '0' && ch <= '9';
+        const bool sign_ok = start && (ch == '+' || ch == '-') && nx >= '0' && nx <= '9';
         const unsigned sm = __ballot_sync(0xffffffffu, start);
-        int kind = 2;  // 0 complete, 1 prefix then stop, 2 invalid (stop)
-        if (start) {
-          long long v;
-          const int64_t q = parse_long_at(t, i, e, &v);
-          if (q >= 0) kind = (q >= e || is_ws(t[q])) ? 0 : 1;
+        const unsigned wsm = __ballot_sync(0xffffffffu, ws);
+        const unsigned badm = __ballot_sync(0xffffffffu, !ws && !digit && !sign_ok);
+        // non-space run ending at this lane: fields of 19+ characters may
+        // overflow long, so such lines take the exact path
+        const unsigned wsle = wsm & ((2u << lane) - 1);
+        const int r = wsle ? lane - (31 - __clz(wsle)) : lane + 1 + run;
+        if (__any_sync(0xffffffffu, r >= 19)) {
+          li.serial = 1;
+          break;
         }
-        const unsigned bad = __ballot_sync(0xffffffffu, start && kind != 0);
-        if (bad) {
-          const int fl = __ffs(bad) - 1;  // first non-complete field in this chunk
-          const int before = __popc(sm & ((1u << fl) - 1));
-          const int pk = __shfl_sync(0xffffffffu, kind, fl);
-          if (pk == 1) li.serial = 1;       // a number with more characters glued on
-          else stop = count + before;
+        run = __shfl_sync(0xffffffffu, r, 31);
+        if (badm) {
+          const int bpos = __ffs(badm) - 1;  // the line's first bad character
+          if ((sm >> bpos) & 1u) stop = count + __popc(sm & ((1u << bpos) - 1));  // field fails
+          else li.serial = 1;  // a number with more characters glued on
         } else {
           count += __popc(sm);
         }
@@ -252,12 +281,20 @@ __global__ void classify_kernel(const char* text_c, const int64_t* line_start, i
   }
 }
 
-// One warp per prompt (line order): the token values.
-__global__ void tokens_kernel(const char* text_c, const int64_t* line_start, int64_t L,
-                              int64_t n, const LineInfo* info, const int32_t* pline,
-                              int32_t P, const int64_t* tok_off, int32_t* tok) {
+// One warp per prompt (line order): the token values. Fast-path lines hold
+// complete integer fields only: per 1,024-character window the warp records
+// its field starts (u16 offsets, shared memory), then every lane parses
+// fields lane, lane + 32, ...; serial lines are parsed by one lane.
+constexpr int kTokT = 256;
+constexpr int kTokWin = 1024;
+__global__ void __launch_bounds__(kTokT)
+tokens_kernel(const char* text_c, const int64_t* line_start, int64_t L, int64_t n,
+              const LineInfo* info, const int32_t* pline, int32_t P, const int64_t* tok_off,
+              int32_t* tok) {
+  __shared__ uint16_t s_fs[kTokT / 32][kTokWin / 2 + 32];
   const unsigned char* t = reinterpret_cast<const unsigned char*>(text_c);
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint16_t* fs = s_fs[w];
   for (int64_t pi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; pi < P;
        pi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t ln = pline[pi];
@@ -271,21 +308,26 @@ __global__ void tokens_kernel(const char* text_c, const int64_t* line_start, int
     }
     int count = 0;
     bool prev_ws = true;
-    for (int64_t c0 = li.tok_pos; c0 < e && count < li.ntok; c0 += 32) {
-      const int64_t i = c0 + lane;
-      const bool in = i < e;
-      const bool ws = in ? is_ws(t[i]) : true;
-      const bool up = __shfl_up_sync(0xffffffffu, ws, 1);  // every lane takes part
-      const bool pws = lane == 0 ? prev_ws : up;
-      const bool start = in && !ws && pws;
-      const unsigned sm = __ballot_sync(0xffffffffu, start);
-      if (start) {
-        const int k = count + __popc(sm & ((1u << lane) - 1));
-        long long v = 0;
-        if (k < li.ntok && parse_long_at(t, i, e, &v) >= 0) out[k] = (int32_t)v;
+    for (int64_t w0 = li.tok_pos; w0 < e && count < li.ntok; w0 += kTokWin) {
+      int nf = 0;
+      for (int c = 0; c < kTokWin; c += 32) {
+        const int64_t i = w0 + c + lane;
+        const bool ws = i < e ? is_ws(t[i]) : true;
+        const bool up = __shfl_up_sync(0xffffffffu, ws, 1);
+        const bool start = !ws && (lane == 0 ? prev_ws : up);
+        const unsigned sm = __ballot_sync(0xffffffffu, start);
+        if (start) fs[nf + __popc(sm & ((1u << lane) - 1))] = (uint16_t)(c + lane);
+        nf += __popc(sm);
+        prev_ws = __shfl_sync(0xffffffffu, ws, 31);
       }
-      count += __popc(sm);
-      prev_ws = __shfl_sync(0xffffffffu, ws, 31);
+      __syncwarp();
+      for (int f = lane; f < nf && count + f < li.ntok; f += 32) {
+        long long v = 0;
+        parse_long_at(t, w0 + fs[f], e, &v);
+        out[count + f] = (int32_t)v;
+      }
+      __syncwarp();
+      count += nf;
     }
   }
 }
@@ -475,8 +517,8 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
       RS_TRY(h2d(ctx, d_pline, pline.data(), 4ull * P));
       RS_TRY(h2d(ctx, d_tok_off, tok_off.data(), 8ull * (P + 1)));
       RS_TRY(h2d(ctx, d_id_off, id_off.data(), 8ull * (P + 1)));
-      const int pgrid = (int)std::min<int64_t>(((int64_t)P * 32 + 255) / 256, 64 * (int64_t)ctx->num_sms);
-      RS_LAUNCH(ctx, "trace_tokens", tokens_kernel, pgrid, 256, 0, d_text, line_start, L, n_bytes,
+      const int pgrid = (int)std::min<int64_t>(((int64_t)P * 32 + kTokT - 1) / kTokT, 64 * (int64_t)ctx->num_sms);
+      RS_LAUNCH(ctx, "trace_tokens", tokens_kernel, pgrid, kTokT, 0, d_text, line_start, L, n_bytes,
                 info, d_pline, P, d_tok_off, d_tok_line);
       RS_LAUNCH(ctx, "trace_ids", ids_gather_kernel,
                 (int)std::min<int64_t>(P, 16 * (int64_t)ctx->num_sms), 32, 0, d_text, info, d_pline,
@@ -509,18 +551,24 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
     if (tr->g < 1) return fail(RS_E_VALIDATION, "responses_per_prompt must be >= 1");
     if (tr->max_prompt_len < 1 || tr->max_response_len < 1)
       return fail(RS_E_VALIDATION, "trace limits must be positive");
+    auto id_of = [&](int32_t r) {
+      return std::string(tr->ids.data() + tr->id_off[r], tr->ids.data() + tr->id_off[r + 1]);
+    };
     for (int32_t r = 0; r < P; ++r) {
-      const std::string id(tr->ids.data() + tr->id_off[r], tr->ids.data() + tr->id_off[r + 1]);
-      if (r > 0) {
-        const std::string prev(tr->ids.data() + tr->id_off[r - 1], tr->ids.data() + tr->id_off[r]);
-        if (!(prev < id)) return fail(RS_E_VALIDATION, "prompts not sorted by unique id near '" + id + "'");
+      if (r > 0) {  // std::string order: bytes, then length
+        const char* pa = tr->ids.data() + tr->id_off[r - 1];
+        const char* pb = tr->ids.data() + tr->id_off[r];
+        const int64_t la = tr->id_off[r] - tr->id_off[r - 1], lb = tr->id_off[r + 1] - tr->id_off[r];
+        const int c = std::memcmp(pa, pb, (size_t)std::min(la, lb));
+        if (!(c < 0 || (c == 0 && la < lb)))
+          return fail(RS_E_VALIDATION, "prompts not sorted by unique id near '" + id_of(r) + "'");
       }
       const int64_t len = tr->offsets[r + 1] - tr->offsets[r];
-      if (len < 1) return fail(RS_E_VALIDATION, "prompt '" + id + "' has no tokens");
+      if (len < 1) return fail(RS_E_VALIDATION, "prompt '" + id_of(r) + "' has no tokens");
       if (len > tr->max_prompt_len)
-        return fail(RS_E_VALIDATION, "prompt '" + id + "' longer than max_prompt_len");
+        return fail(RS_E_VALIDATION, "prompt '" + id_of(r) + "' longer than max_prompt_len");
       if (tr->gt[r] < 1 || tr->gt[r] > tr->max_response_len)
-        return fail(RS_E_VALIDATION, "prompt '" + id + "' ground_truth_len out of range");
+        return fail(RS_E_VALIDATION, "prompt '" + id_of(r) + "' ground_truth_len out of range");
     }
     // 8. the id-ordered token CSR, owned by the handle
     if (cudaMalloc(&tr->d_tokens, 4ull * std::max<int64_t>(T, 1)) != cudaSuccess ||

@@ -186,3 +186,29 @@ def random_trace(seed, n, max_len=64, g=2, shared=0):
         prompts.append((f"p{i:06d}", int(rng.randint(1, 2048)), toks))
     steps = [(0, [(p[0], [int(x) for x in rng.randint(1, 2048, g)]) for p in prompts[: n // 2]])]
     return trace_csv(prompts, g=g, max_prompt_len=max_len + shared, steps=steps)
+
+
+def c2_trace_text(n_prompts=65536, shared=2048, unique=512, vocab=32000, seed=1):
+    """The C2 batch (c2_tokens) as CSV trace text: '# prompt p%06d 100 '
+    then the tokens as zero-padded 5-digit decimals (valid istream integers,
+    vocab < 100000), so every line has the same width and numpy builds the
+    ~1 GB text directly. Returns (text uint8 array, tokens, offsets)."""
+    tok, off = c2_tokens(n_prompts, shared, unique, vocab, seed)
+    L = shared + unique
+    assert vocab <= 100000 and np.all(np.diff(off) == L)
+    head = np.frombuffer(b"# max_prompt_len 4096\n", np.uint8)
+    tail = np.frombuffer(b"step_idx,prompt_id,response_idx,actual_len\n", np.uint8)
+    pre = 20  # '# prompt p000000 100'
+    width = pre + 6 * L + 1
+    body = np.empty((n_prompts, width), np.uint8)
+    ids = np.arange(n_prompts)
+    body[:, :pre] = np.frombuffer(b"# prompt p000000 100", np.uint8)
+    for k in range(6):  # the id digits
+        body[:, 15 - k] = ord("0") + (ids // 10 ** k) % 10
+    t = tok.reshape(n_prompts, L)
+    cols = body[:, pre:pre + 6 * L].reshape(n_prompts, L, 6)
+    cols[:, :, 0] = ord(" ")
+    for k in range(5):
+        cols[:, :, 5 - k] = ord("0") + (t // 10 ** k) % 10
+    body[:, -1] = ord("\n")
+    return np.concatenate([head, body.reshape(-1), tail]), tok, off

@@ -1,0 +1,54 @@
+"""Time the trace prompt-table parse (rs_trace_csr_parse) per kernel on the
+C2-shaped trace text (tests/cases.py c2_trace_text)."""
+import ctypes as C
+import pathlib
+import sys
+import time
+
+REPO = pathlib.Path(__file__).resolve().parents[1]
+sys.path[:0] = [str(REPO), str(REPO / "tests")]
+import torch  # noqa: E402
+from cases import c2_trace_text  # noqa: E402
+from paper_2602_22718_b200.lib import check, context  # noqa: E402
+
+t0 = time.perf_counter()
+text, tok, off = c2_trace_text()
+print(f"text {text.nbytes / 1e9:.3f} GB built in {time.perf_counter() - t0:.1f} s")
+ctx = context(0)
+d = torch.from_numpy(text).cuda()
+h = C.c_void_p()
+names = ["trace_nl_count", "trace_nl_scan", "trace_nl_write", "trace_classify", "trace_tokens",
+         "trace_ids", "string_words", "gather_keys", "trace_gather"]
+for rep in range(4):
+    timing = rep == 3
+    ctx.enable_kernel_timing(timing)
+    ctx.reset_kernel_timing()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    check(ctx.lib.rs_trace_csr_parse(ctx.handle, C.c_void_p(d.data_ptr()), text.nbytes, 1, C.byref(h)))
+    dt = time.perf_counter() - t0
+    ctx.lib.rs_trace_csr_free(h)
+    print(f"rep {rep}: device parse {dt * 1e3:.2f} ms ({text.nbytes / dt / 1e9:.1f} GB/s)")
+    if timing:
+        for n in names:
+            ms, k = ctx.kernel_time(n)
+            print(f"   {n:16s} {ms:8.3f} ms over {k}")
+pt = torch.from_numpy(text).pin_memory()
+for rep in range(2):
+    t0 = time.perf_counter()
+    check(ctx.lib.rs_trace_csr_parse(ctx.handle, C.c_void_p(pt.data_ptr()), text.nbytes, 0, C.byref(h)))
+    dt = time.perf_counter() - t0
+    ctx.lib.rs_trace_csr_free(h)
+    print(f"host-text parse {dt * 1e3:.2f} ms")
+for rep in range(3):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    d.copy_(pt, non_blocking=True)
+    torch.cuda.synchronize()
+    print(f"torch pinned H2D of the text {1e3 * (time.perf_counter() - t0):.2f} ms")
+for rep in range(3):
+    t0 = time.perf_counter()
+    check(ctx.lib.rs_trace_csr_parse(ctx.handle, C.c_void_p(pt.data_ptr()), text.nbytes, 0, C.byref(h)))
+    dt = time.perf_counter() - t0
+    ctx.lib.rs_trace_csr_free(h)
+    print(f"host-text parse {dt * 1e3:.2f} ms")
