@@ -366,10 +366,76 @@ def run_ours(args, world, rank, local):
             result["cpu_baseline"] = cpu_baseline_sweep(args)
         if world == 1 and not args.no_c5:
             result["c5"] = bench_c5()
+        if world == 1 and not args.no_trace:
+            result["trace"] = bench_trace(args, ctx, torch, dev)
         print(json.dumps(result), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def bench_trace(args, ctx, torch, dev):
+    """the C2 batch written as a CSV trace (~1 GB of text,
+    tests/cases.py c2_trace_text) -> id-sorted token CSR in HBM
+    (rs_trace_csr_parse), tokens/s. value: text already in HBM; e2e: from
+    pinned host text; cpu_baseline: the reference's trace_from_string on the
+    first 4,096 prompts."""
+    from cases import c2_trace_text
+    from paper_2602_22718_b200.lib import check
+    text, tok, off = c2_trace_text()
+    n_tok = int(tok.size)
+    d_text = torch.from_numpy(text).to(dev)
+    h = C.c_void_p()
+    lib = ctx.lib
+
+    def parse(ptr, device):
+        check(lib.rs_trace_csr_parse(ctx.handle, C.c_void_p(ptr), text.nbytes, device, C.byref(h)))
+        lib.rs_trace_csr_free(h)
+
+    for _ in range(3):
+        parse(d_text.data_ptr(), 1)
+    k = 10
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(k):
+        parse(d_text.data_ptr(), 1)
+    dev_s = (time.perf_counter() - t0) / k
+    ctx.enable_kernel_timing(True)
+    ctx.reset_kernel_timing()
+    parse(d_text.data_ptr(), 1)
+    kt = {n: ctx.kernel_time(n)[0] for n in ("trace_classify", "trace_tokens", "trace_nl_write")}
+    ctx.enable_kernel_timing(False)
+    pt = torch.from_numpy(text).pin_memory()
+    parse(pt.data_ptr(), 0)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        parse(pt.data_ptr(), 0)
+    host_s = (time.perf_counter() - t0) / 3
+    peak, _ = peaks()
+    top = max(kt, key=kt.get)
+    achieved = text.nbytes / (kt[top] / 1e3) / 1e9  # the dominant pass reads the text once
+    out = {"metric": "trace prompt-table parse tokens/sec (CSV -> device CSR)", "value": n_tok / dev_s,
+           "unit": "tokens/s", "text_bytes": int(text.nbytes), "ms_per_parse": dev_s * 1e3,
+           "config": {"workload": "C2 batch as CSV trace text: 65536 '# prompt' lines x 2560 tokens"},
+           "e2e": {"value": n_tok / host_s, "unit": "tokens/s", "h2d_bytes_per_step": int(text.nbytes),
+                   "d2h_bytes_per_step": 0},
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak, "traffic": None, "kernel": top,
+                        "launch_ms": kt[top], "kernel_ms": kt}}
+    if not args.no_cpu:
+        from oracle_lib import ref
+        R = ref()
+        if R is not None:
+            sample = text[: 22 + 4096 * (20 + 6 * 2560 + 1)].tobytes() + \
+                b"step_idx,prompt_id,response_idx,actual_len\n"
+            t0 = time.perf_counter()
+            R.trace_prompts(sample)
+            dt = time.perf_counter() - t0
+            out["cpu_baseline"] = {"value": 4096 * 2560 / dt, "unit": "tokens/s", "cores": 1,
+                                   "kind": "reference",
+                                   "sample": f"first 4,096 prompts ({len(sample) / 1e6:.0f} MB), "
+                                             f"trace_from_string, {dt:.1f} s"}
+    return out
 
 
 def bench_c5(steps=20):
@@ -491,6 +557,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dedup", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-trace", action="store_true")
     ap.add_argument("--check", action="store_true", default=True)
     args = ap.parse_args()
     world, rank, local = init_dist()

@@ -289,6 +289,14 @@ int rs_ctx_create(int device, rs_ctx** out) {
     return fail(RS_E_CUDA, "stream creation failed");
   }
   c->stream = c->own_stream;
+  {  // stream-ordered temporaries (trace parsing) stay cached in the pool
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  }
   if (cudaMalloc(&c->d_flags, sizeof(int)) != cudaSuccess ||
       cudaMallocHost(&c->h_flags, sizeof(int)) != cudaSuccess) {
     delete c;

@@ -364,9 +364,10 @@ struct rs_trace_csr {
   std::vector<int64_t> id_off;
   std::vector<int32_t> gt;
   std::vector<int64_t> offsets;
+  cudaStream_t stream = nullptr;  // the outputs are stream-ordered allocations
   ~rs_trace_csr() {
-    if (d_tokens) cudaFree(d_tokens);
-    if (d_offsets) cudaFree(d_offsets);
+    if (d_tokens) cudaFreeAsync(d_tokens, stream);
+    if (d_offsets) cudaFreeAsync(d_offsets, stream);
   }
 };
 
@@ -571,8 +572,9 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
         return fail(RS_E_VALIDATION, "prompt '" + id_of(r) + "' ground_truth_len out of range");
     }
     // 8. the id-ordered token CSR, owned by the handle
-    if (cudaMalloc(&tr->d_tokens, 4ull * std::max<int64_t>(T, 1)) != cudaSuccess ||
-        cudaMalloc(&tr->d_offsets, 8ull * (P + 1)) != cudaSuccess) {
+    tr->stream = ctx->own_stream;  // outlives any caller stream set on the context
+    if (cudaMallocAsync(&tr->d_tokens, 4ull * std::max<int64_t>(T, 1), ctx->stream) != cudaSuccess ||
+        cudaMallocAsync(&tr->d_offsets, 8ull * (P + 1), ctx->stream) != cudaSuccess) {
       cudaGetLastError();
       return fail(RS_E_NOMEM, "trace CSR allocation failed");
     }
