@@ -33,7 +33,7 @@ namespace rs {
 size_t fast_ss_bytes(int64_t items, int S) {
   int64_t segs = items + S;
   return abytes(segs, 8) * 2 + abytes(S, 4) + abytes(items, 8) + abytes(items, 4) * 2 +
-         abytes(items, 16) + abytes(segs, 4) + abytes(segs, 1) + abytes((int64_t)S * kStStride, 2) +
+         abytes(items, 16) + abytes(segs, 4) + abytes((int64_t)S * kStStride, 2) +
          abytes((segs / kBlk + S + 2) * kBlkPairs, 2);
 }
 
@@ -49,7 +49,6 @@ FastSS fast_ss_alloc(rs_ctx* ctx, const int64_t* d_off, int64_t items, int S) {
   f.order_r = arena_alloc<int32_t>(ctx, items);
   f.rec = arena_alloc<int4>(ctx, items);
   f.pmsm = arena_alloc<uint32_t>(ctx, segs);
-  f.pgo = arena_alloc<uint8_t>(ctx, segs);
   f.st = arena_alloc<uint16_t>(ctx, (int64_t)S * kStStride);
   f.bq = arena_alloc<uint16_t>(ctx, (segs / kBlk + S + 2) * kBlkPairs);
   return f;
@@ -358,14 +357,14 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
     }
   }
   // Range-max helpers: per 16-segment block the in-block prefix / suffix
-  // maxima and previous-greater distances, then a sparse table over block
+  // maxima and the all-pairs range maxima, then a sparse table over block
   // maxima (levels double the span).
   __syncthreads();
   const int nblk = (D + kBlk - 1) / kBlk;
   uint16_t* st = ss.st + (int64_t)s * kStStride;
   for (int jb = tid; jb < nblk; jb += kBuildT) {
     const int k0 = jb * kBlk, k1 = min(D, k0 + kBlk);
-    int v[kBlk], pg[kBlk];
+    int v[kBlk];
     int m = 0;
 #pragma unroll
     for (int i = 0; i < kBlk; ++i) {
@@ -377,13 +376,7 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
 #pragma unroll
     for (int i = 0; i < kBlk; ++i) {
       pm = max(pm, v[i]);
-      int j = i - 1;
-      while (j >= 0 && v[j] <= v[i]) j = pg[j];
-      pg[i] = j;
-      if (k0 + i < k1) {
-        ss.pmsm[so + k0 + i] = (uint32_t)pm;
-        ss.pgo[so + k0 + i] = (uint8_t)(j >= 0 ? i - j : 0);
-      }
+      if (k0 + i < k1) ss.pmsm[so + k0 + i] = (uint32_t)pm;
     }
     int sm = 0;
 #pragma unroll
@@ -953,7 +946,7 @@ int fast_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, Cand
 // tables and the profile row are the same for every lane at a step (uniform
 // loads); only the group bounds differ. The base (max prompt_len of the
 // group's live prefix) comes from O(1) range-max queries: the group's first
-// block via previous-greater chains, full blocks via the block sparse table,
+// block via its all-pairs table, full blocks via the block sparse table,
 // the current block via its in-block prefix max.
 constexpr int kLsThreads = 256;
 
@@ -987,7 +980,6 @@ struct LsArgs {
 struct LsView {
   const int2* seg;
   const uint32_t* pmsm;
-  const uint8_t* pgo;
   const uint16_t* st;
   const uint16_t* bq;  // this scenario's block 0 in FastSS::bq
 };
@@ -996,20 +988,6 @@ struct LsView {
 // all-pairs table.
 __device__ __forceinline__ int ls_inblock(const LsView& V, int l, int r) {
   return __ldg(V.bq + (l >> 4) * kBlkPairs + blk_pair(l & (kBlk - 1), r & (kBlk - 1)));
-}
-
-__device__ __forceinline__ int ls_mx(const LsView& V, int k) { return (__ldg(&V.seg[k].x) >> 16) & 0xffff; }
-
-// max MX over [l, r] (l <= r) inside one 16-segment block: walk the
-// previous-greater chain from r while it stays at or right of l.
-__device__ __forceinline__ int ls_chain(const LsView& V, int l, int r) {
-  int j = r, m = ls_mx(V, r);
-  for (;;) {
-    const int d = __ldg(V.pgo + j);
-    if (d == 0 || j - d < l) return m;
-    j -= d;
-    m = ls_mx(V, j);
-  }
 }
 
 __device__ __forceinline__ int ls_blocks(const LsView& V, int jl, int jr) {  // jl <= jr
@@ -1046,7 +1024,7 @@ __global__ void group_table_kernel(FastSS ss, DevProfile prof, CandRange cr, int
     const int P = (int)(ss.item_off[s + 1] - i0);
     const int q = P / N, rem = P % N;
     const int a = g * q + min(g, rem), b = a + q + (g < rem ? 1 : 0);
-    LsView V{ss.seg + so, ss.pmsm + so, ss.pgo + so, ss.st + (int64_t)s * kStStride,
+    LsView V{ss.seg + so, ss.pmsm + so, ss.st + (int64_t)s * kStStride,
              ss.bq + (size_t)((so >> 4) + s) * kBlkPairs};
     const int2 ra = ss.rinfo[i0 + a], rb = ss.rinfo[i0 + b - 1];
     const int ka = ra.x, kb = rb.x;
@@ -1208,7 +1186,7 @@ __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
     const int P = (int)(A.ss.item_off[s + 1] - i0);
     const int64_t so = i0 + s;
     const int D = A.ss.nseg[s];
-    LsView V{A.ss.seg + so, A.ss.pmsm + so, A.ss.pgo + so, A.ss.st + (int64_t)s * kStStride,
+    LsView V{A.ss.seg + so, A.ss.pmsm + so, A.ss.st + (int64_t)s * kStStride,
              A.ss.bq + (size_t)((so >> 4) + s) * kBlkPairs};
     const int64_t gbase = (int64_t)s * A.cr.T + (tri64(N) - flat0);
     double* gt = A.gt + gbase;

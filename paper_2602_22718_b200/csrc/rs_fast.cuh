@@ -23,7 +23,6 @@ struct FastSS {
   int4* rec;  // scratch: scattered {pred lo, pred hi, idx, plen}
   // Range-max helpers over the per-segment max prompt_len (16-segment blocks):
   uint32_t* pmsm;  // per segment slot: in-block prefix max | in-block suffix max << 16
-  uint8_t* pgo;    // per segment slot: distance to the previous greater MX in its block (0 = none)
   uint16_t* st;    // per scenario: sparse table over block maxima, [kStLevels][kStBlocks]
   uint16_t* bq;    // per 16-segment block: max MX over [i, j], in-block i <= j (kBlkPairs u16,
                    // upper triangle row-major); block jb of scenario s at slot (so >> 4) + s + jb
