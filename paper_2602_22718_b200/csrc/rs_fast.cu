@@ -1011,7 +1011,7 @@ __device__ __forceinline__ int ls_range(const LsView& V, int l, int r) {
 // group, ticks 1 .. F_kb), i.e. the group's total after one run. The first
 // run spans the longest context range (often several knot pieces), so it is
 // evaluated here in parallel rather than inside the lockstep walk.
-__global__ void group_table_kernel(FastSS ss, DevProfile prof, CandRange cr, int S, int4* gtab,
+__global__ void group_table_kernel(FastSS ss, FastProf fp, CandRange cr, int S, int4* gtab,
                                    double* gfirst) {
   const int64_t total = (int64_t)S * cr.T;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
@@ -1038,15 +1038,26 @@ __global__ void group_table_kernel(FastSS ss, DevProfile prof, CandRange cr, int
       if (ka + 1 <= kb - 1) top_m = max(top_m, ls_range(V, ka + 1, kb - 1));
       smb = (int)(__ldg(V.pmsm + ka + 1) >> 16);
     }
-    const int64_t f = ss.seg[so + kb].x & 0xffff;
+    const int f = ss.seg[so + kb].x & 0xffff;
     gtab[t] = make_int4(ka, kb, va | (vb << 16), smb);
-    gfirst[t] = dadd(0.0, run_sum_int(prof, (int64_t)cr.G * (b - a), top_m, (int64_t)top_m + f - 1));
+    // run_sum(G * (b - a), top_m, top_m + f - 1) from the halved tables
+    // (piece terms and their order as tpot_context_run_sum; 0.0 + x == x)
+    const int clo = fp.c_lo, chi = fp.c_hi, clo1 = fp.c_lo - 1;
+    const double* row = fp.rows + (size_t)(min(b - a, fp.live_top) - 1) * fp.ncm - clo;
+    const int c1 = top_m + f - 1;
+    int cc = top_m;
+    int pe = piece_end(fp.pex, cc, c1, clo1, chi);
+    double rs = piece_term(pe - cc + 1, __ldg(row + min(max(cc, clo), chi)),
+                           __ldg(row + min(max(pe, clo), chi)));
+    for (cc = pe + 1; cc <= c1; cc = pe + 1) {
+      pe = piece_end(fp.pex, cc, c1, clo1, chi);
+      rs = dadd(rs, piece_term(pe - cc + 1, __ldg(row + min(max(cc, clo), chi)),
+                               __ldg(row + min(max(pe, clo), chi))));
+    }
+    gfirst[t] = rs;
   }
 }
 
-// see LsEpilogue. gt: this lane's N group times (just written by this lane).
-// idle_fa = sum over groups of (b - a) * F(first segment of the group), from
-// the walk; the per-group CF differences telescope to CF(P) (segCF[D]).
 // fast_reduce + select for the lockstep evaluator's batch in one kernel: one
 // CTA per scenario, one candidate per thread (C <= kLsThreads). Group times
 // are read 8 ahead of the sequential cost sum; idle slot-ticks use the
@@ -1320,7 +1331,7 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
   {
     const int64_t n = (int64_t)S * cr.T;
     RS_LAUNCH(ctx, "group_table", group_table_kernel,
-              (int)std::min<int64_t>((n + 255) / 256, 16 * ctx->num_sms), 256, 0, ss, prof, cr, S,
+              (int)std::min<int64_t>((n + 255) / 256, 16 * ctx->num_sms), 256, 0, ss, fp, cr, S,
               gtab, gfirst);
   }
   const int cand_units = (C + kLsThreads - 1) / kLsThreads;
