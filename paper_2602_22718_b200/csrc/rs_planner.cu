@@ -634,6 +634,8 @@ static int build_batch(rs_ctx* ctx, int S, const int64_t* d_off, int64_t n, doub
   return RS_OK;
 }
 
+constexpr int kLockstepMinScenarios = 32;
+
 static int units_for(rs_ctx* ctx, int S, int C) {
   int want = (2 * ctx->num_sms + S - 1) / S;
   return std::max(1, std::min(want, C));
@@ -651,7 +653,10 @@ static int eval_batch(rs_ctx* ctx, const Built& b, int S, const DevProfile& dp, 
     CandRange cr{n_min, n_max, T, G};
     // Many scenarios: candidates in lockstep (one lane per candidate).
     // Few scenarios: one group per lane, candidates split over CTAs.
-    if (S >= ctx->num_sms && dp.c_hi - dp.c_lo + 1 <= kTopCap) {
+    // the lockstep evaluator runs one CTA per scenario: even a partial wave
+    // (a sweep's last batch) beats splitting candidates over CTAs from about
+    // 32 scenarios on
+    if (S >= kLockstepMinScenarios && dp.c_hi - dp.c_lo + 1 <= kTopCap) {
       const bool f = fuse && fused && lockstep_fuses_select(cr);
       if (f) {
         *fused = true;
