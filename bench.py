@@ -460,6 +460,10 @@ def bench_c5(steps=20):
             "reference": r["iterations_per_s"], "plan_ms_per_step": b["plan_ms_per_step"],
             "reference_plan_ms_per_step": r["plan_ms_per_step"],
             "identical_to_reference": b["digest"] == r["digest"],
+            "with_device_planning": {  # plan_rlhfless's scale+penalty and snapshot swapped
+                "value": b["swapped"]["iterations_per_s"],
+                "plan_ms_per_step": b["swapped"]["plan_ms_per_step"],
+                "identical_to_reference": b["swapped"]["digest"] == r["digest"]},
             "scale_with_placement_penalty_ms": {
                 "reference": r["scale_with_penalty_ms"]["stock"],
                 "dropin_callback": b["scale_with_penalty_ms"]["stock"],

@@ -77,6 +77,8 @@ def test_c5_training_loop_dropin_matches_reference():
         outs.append(json.loads(out.strip().splitlines()[-1]))
     ref_run, b200_run = outs
     assert ref_run["digest"] == b200_run["digest"]
+    # the loop with the INTEGRATION.md swap (b200::predict_lengths, scale_placed)
+    assert b200_run["swapped"]["digest"] == ref_run["digest"]
     assert ref_run["total_cost"] == b200_run["total_cost"]
     stock, device = b200_run["scale_with_penalty_ms"]["n_star"]
     assert device == stock == ref_run["scale_with_penalty_ms"]["n_star"][0]
