@@ -1318,7 +1318,7 @@ __global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
 }
 
 int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, CandRange cr,
-                  double* gt, const LsFuse* fuse) {
+                  double* gt, const LsFuse* fuse, int ctas_per_sm) {
   if (!fast_profile_ok(prof, cr.G)) return fail(RS_E_CONFIG, "profile not eligible for the fast path");
   const int64_t ncm = prof.c_hi - prof.c_lo + 1;
   if (ncm > kTopCap) return fail(RS_E_CONFIG, "context memo too large for the lockstep evaluator");
@@ -1341,7 +1341,8 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
   int per_sm = 1;
   RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lockstep_eval_kernel, kLsThreads, smem));
   const int units = S * A.cand_units;
-  const int grid = std::max(1, std::min(units, std::max(1, per_sm) * ctx->num_sms));
+  const int per = ctas_per_sm > 0 ? std::min(ctas_per_sm, std::max(1, per_sm)) : std::max(1, per_sm);
+  const int grid = std::max(1, std::min(units, per * ctx->num_sms));
   RS_LAUNCH(ctx, "group_eval", lockstep_eval_kernel, grid, kLsThreads, smem, A);
   if (fuse) {  // the caller skips fast_reduce / select
     if (!lockstep_fuses_select(cr)) return fail(RS_E_ARG, "finish kernel needs <= 256 candidates");

@@ -118,8 +118,10 @@ struct LsFuse {
   double lambda;
   int gpus;
 };
+// ctas_per_sm > 0: persistent grid of that many CTAs per SM (each loops over
+// scenarios); 0: as many as fit.
 int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, CandRange cr,
-                  double* gt, const LsFuse* fuse = nullptr);
+                  double* gt, const LsFuse* fuse = nullptr, int ctas_per_sm = 0);
 bool lockstep_fuses_select(CandRange cr);
 // CTA slots of the lockstep evaluator on this device (one scenario each).
 int lockstep_slots(rs_ctx* ctx, const DevProfile& prof, int G);

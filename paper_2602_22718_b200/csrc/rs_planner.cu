@@ -23,6 +23,7 @@
 // scan + carry), and the lanes' run sums are added in lane order so the FP64
 // sum is the reference's sequential sum bit for bit.
 #include <algorithm>
+#include <numeric>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -645,7 +646,7 @@ static int units_for(rs_ctx* ctx, int S, int C) {
 // reduce (and, if *fused_select, select) outputs; *fused is set accordingly.
 static int eval_batch(rs_ctx* ctx, const Built& b, int S, const DevProfile& dp, int n_min,
                       int n_max, int G, double* gt, const LsFuse* fuse = nullptr,
-                      bool* fused = nullptr, bool* fused_select = nullptr) {
+                      bool* fused = nullptr, bool* fused_select = nullptr, int ctas_per_sm = 0) {
   if (fused) *fused = false;
   if (fused_select) *fused_select = false;
   const int64_t T = groups_per_scenario(n_min, n_max);
@@ -662,7 +663,7 @@ static int eval_batch(rs_ctx* ctx, const Built& b, int S, const DevProfile& dp, 
         *fused = true;
         if (fused_select) *fused_select = fuse->n_star != nullptr;
       }
-      return lockstep_eval(ctx, S, b.fss, dp, cr, gt, f ? fuse : nullptr);
+      return lockstep_eval(ctx, S, b.fss, dp, cr, gt, f ? fuse : nullptr, ctas_per_sm);
     }
     return fast_eval(ctx, S, b.fss, dp, cr, units_for(ctx, S, n_max - n_min + 1), gt);
   }
@@ -692,6 +693,62 @@ static bool fast_spec_ok(const rs_scenario_spec* sp) {
          sp->plen_min >= 0 && sp->plen_max <= kFastPlenMax;
 }
 
+// Relative round time of the lockstep evaluator at c resident CTAs per SM
+// (c = 1..4, measured on B200 with the C4 workload: 3.16 / 3.28 / 3.53 /
+// 4.01 ms): a lone CTA is latency-bound, four share the issue slots.
+static double lockstep_round_cost(int c) {
+  static const double rel[5] = {0.0, 1.00, 1.04, 1.12, 1.27};
+  return c <= 4 ? rel[c] : rel[4] * c / 4.0;
+}
+
+// Modelled time of one lockstep batch of U scenarios and the CTAs per SM
+// that achieve it (rounds x round cost, minimised over 1..cmax).
+static double lockstep_batch_cost(int U, int cmax, int nsm, int* best_c) {
+  double best = 1e300;
+  *best_c = cmax;
+  for (int c = 1; c <= cmax; ++c) {
+    const int64_t rounds = (U + (int64_t)c * nsm - 1) / ((int64_t)c * nsm);
+    const double t = rounds * lockstep_round_cost(c);
+    if (t < best - 1e-12) {
+      best = t;
+      *best_c = c;
+    }
+  }
+  return best;
+}
+
+// Batch sizes for S scenarios under a budget of Bmem per batch: full batches
+// of whole waves, with the remainder alone or merged into the last one —
+// whichever the round model prefers — and each batch's CTAs per SM.
+static void plan_batches(int S, int Bmem, int cmax, int nsm, std::vector<int>* sizes,
+                         std::vector<int>* cps) {
+  cmax = std::max(1, cmax);
+  const int slots = cmax * nsm;
+  const int F = Bmem >= slots ? Bmem / slots * slots : Bmem;
+  std::vector<std::vector<int>> plans;
+  {
+    std::vector<int> a;
+    for (int s0 = 0; s0 < S; s0 += F) a.push_back(std::min(F, S - s0));
+    plans.push_back(a);
+    if (a.size() >= 2 && a[a.size() - 2] + a.back() <= Bmem) {
+      std::vector<int> m(a.begin(), a.end() - 1);
+      m.back() += a.back();
+      plans.push_back(m);
+    }
+  }
+  double best = 1e300;
+  for (const auto& pl : plans) {
+    double t = 0;
+    std::vector<int> c(pl.size());
+    for (size_t i = 0; i < pl.size(); ++i) t += lockstep_batch_cost(pl[i], cmax, nsm, &c[i]);
+    if (t < best - 1e-12) {
+      best = t;
+      *sizes = pl;
+      *cps = c;
+    }
+  }
+}
+
 // Shared sweep driver: scenarios either generated (spec) or from arrays.
 static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h_pred,
                       const int32_t* h_plen, int S, int P, const rs_profile* profile, int G,
@@ -708,15 +765,24 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
   const bool with_generic = !gen_fast;
   const size_t per_scen = abytes(P, 8) + abytes(P, 4) + built_bytes(P, 1, with_generic) +
                           abytes(T, 8) * 2 + abytes(T, 16) + abytes(C, 8) * 3 + abytes(1, 4) + 2048;
-  // Batch size: what an 8 GiB scratch budget holds (<= 2048), rounded down to
-  // a multiple of the lockstep evaluator's CTA slots so every batch is whole
-  // waves (S = 10,000 on 148 SMs x 4: batches of 1,184, 17 waves in all).
-  int B = (int)std::max<size_t>(1, std::min<size_t>((size_t)S, (size_t)(8ull << 30) / per_scen));
-  if (B > 2048) B = 2048;
+  // Batches: what an 8 GiB scratch budget holds (<= 2048 scenarios), planned
+  // as whole waves of the lockstep evaluator (S = 10,000 on 148 SMs x 4:
+  // batches of 1,184) with the remainder merged into the last batch when it
+  // fits, each batch run at the CTAs per SM that minimise its rounds x round
+  // cost (plan_batches); e.g. a rank's 1,250 scenarios at 8 GPUs run as one
+  // batch at 3 CTAs per SM instead of 1,184 + a lone 66.
+  const int Bmem = (int)std::max<size_t>(
+      1, std::min<size_t>({(size_t)S, (size_t)(8ull << 30) / per_scen, (size_t)2048}));
+  std::vector<int> sizes, cps;  // scenarios and lockstep CTAs per SM, per batch
   if (allow_fast) {
-    const int slots = lockstep_slots(ctx, dp, G);
-    if (B > slots) B = B / slots * slots;
+    plan_batches(S, Bmem, lockstep_slots(ctx, dp, G) / ctx->num_sms, ctx->num_sms, &sizes, &cps);
+  } else {
+    for (int s0 = 0; s0 < S; s0 += Bmem) {
+      sizes.push_back(std::min(Bmem, S - s0));
+      cps.push_back(0);
+    }
   }
+  const int B = *std::max_element(sizes.begin(), sizes.end());
   size_t need = (size_t)B * per_scen + fast_eval_bytes(dp, G) + abytes(B + 1, 8) +
                 abytes(2 * (RS_QTABLE_N + 1), 8) +
                 abytes(C, 8) * 2 + abytes(C, 4) + abytes(dp.c_hi - dp.c_lo + 1, 4) + (4 << 20);
@@ -746,8 +812,8 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
   RS_CUDA_TRY(cudaMemsetAsync(agg_c, 0, 8 * C, ctx->stream));
   RS_CUDA_TRY(cudaMemsetAsync(agg_h, 0, 4 * C, ctx->stream));
   RS_TRY(clear_flags(ctx));
-  for (int s0 = 0; s0 < S; s0 += B) {
-    const int Sb = std::min(B, S - s0);
+  for (size_t bi = 0, s0 = 0; bi < sizes.size(); s0 += sizes[bi], ++bi) {
+    const int Sb = sizes[bi];
     const int64_t n = (int64_t)Sb * P;
     ctx->arena_used = mark;
     Built built;
@@ -791,7 +857,7 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
     bool fused = false, fused_select = false;
     static const bool no_fuse = getenv("RS_NO_FUSE") != nullptr;  // A/B switch
     RS_TRY(eval_batch(ctx, built, Sb, dp, n_min, n_max, G, gt, no_fuse ? nullptr : &fuse, &fused,
-                      &fused_select));
+                      &fused_select, cps[bi]));
     if (!fused)
       RS_TRY(reduce_batch(ctx, built, Sb, n_min, n_max, G, dp.rho, gpus, gt, o_tt, o_cc,
                           out->idle_slot_ticks ? o_idle : (int64_t*)nullptr));
