@@ -145,3 +145,9 @@ def test_sweep_wide_buckets_bitwise():
     assert np.array_equal(bits(got["t_total"]), bits(tt))
     assert np.array_equal(bits(got["cost"]), bits(cc))
     assert np.array_equal(got["n_star"], ns)
+
+
+def test_sweep_lockstep_wide_candidate_range():
+    """More than 256 candidates: two lockstep CTAs per scenario, select and
+    aggregate unfused (S >= 32 takes the lockstep evaluator)."""
+    check_sweep(c4_spec(40, count=1400, first=321), 2, 320, lam=0.55, g=4)
