@@ -206,6 +206,8 @@ int get_profile(rs_ctx* ctx, const rs_profile* p, DevProfile* out) {
   d.c_hi = d.has_cmemo ? (int64_t)cb : -1;
   if (!d.has_bmemo) d.b_hi = INT64_MAX;  // never takes the top-row shortcut
   d.cfront_m1 = std::ceil(p->context_knots[0]) - 1.0;
+  d.ck_front = p->context_knots[0];
+  d.ck_back = p->context_knots[p->nc - 1];
   size_t nbm = d.has_bmemo ? (size_t)(d.b_hi - d.b_lo + 1) : 0;
   size_t ncm = d.has_cmemo ? (size_t)(d.c_hi - d.c_lo + 1) : 0;
   size_t grid_n = (size_t)p->nb * p->nc;

@@ -901,10 +901,7 @@ static int fast_prof_make(rs_ctx* ctx, const DevProfile& prof, int G, FastProf* 
   double* top = rows ? rows + (int64_t)(live_top - 1) * ncm : nullptr;
   uint16_t* pex = arena_alloc<uint16_t>(ctx, ncm + 1);
   if (!rows || !top || !pex) return fail(RS_E_NOMEM, "arena exhausted (tpot tables)");
-  double front, back;
-  RS_CUDA_TRY(cudaMemcpyAsync(&front, prof.ck, 8, cudaMemcpyDeviceToHost, ctx->stream));
-  RS_CUDA_TRY(cudaMemcpyAsync(&back, prof.ck + prof.nc - 1, 8, cudaMemcpyDeviceToHost, ctx->stream));
-  RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  const double front = prof.ck_front, back = prof.ck_back;
   FastProf& fp = *out;
   fp.top = top;
   fp.rows = rows;

@@ -75,6 +75,7 @@ struct DevProfile {
   const double* top_row;  // tpot(batch_knots.back(), c) for c in memo range
   const double* kfloor;   // floor(context_knots[i])
   double cfront_m1;       // ceil(front) - 1
+  double ck_front, ck_back;  // context_knots.front() / .back(), host copies
   int has_bmemo, has_cmemo;
 };
 

@@ -873,7 +873,8 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
       if (out->idle_slot_ticks)
         RS_TRY(d2h(ctx, out->idle_slot_ticks + (size_t)s0 * C, o_idle, 8ull * Sb * C));
       if (out->n_star) RS_TRY(d2h(ctx, out->n_star + s0, o_ns, 4ull * Sb));
-      RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+      // no sync: the next batch's kernels reuse these buffers on the same
+      // stream, after the copies
     }
   }
   if (device_ptrs) {
