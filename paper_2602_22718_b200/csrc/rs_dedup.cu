@@ -254,9 +254,11 @@ compare_kernel(DedupState st, int cur, const int* kcur) {
 
 // Round 0 (one class, representative = prompt 0): the HBM-bound pass.
 // The representative is staged once per CTA in shared memory; every warp
-// streams its member through a 4-stage cp.async ring (2 KB per stage) so
-// ~8 KB per warp are in flight without holding registers, and compares
-// 512 tokens per stage with a warp-min for the first mismatch.
+// streams its member through a 4-stage ring of 2 KB windows filled by bulk
+// TMA copies (cp.async.bulk, one elected lane, completion on a per-slot
+// mbarrier), so ~8 KB per warp are in flight with no per-lane copy
+// instructions, and compares 512 tokens per stage with a warp-min for the
+// first mismatch.
 constexpr int kStreamStages = 4;
 constexpr int kStageTok = 512;
 constexpr int kStreamWarps = 8;
@@ -269,10 +271,44 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// 1D bulk TMA global -> shared, completing `bytes` on bar (16-byte aligned,
+// bytes a multiple of 16).
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __global__ void __launch_bounds__(kStreamWarps * 32)
 compare_stream_kernel(DedupState st, const int* kcur) {
   extern __shared__ __align__(16) int32_t sm[];
   __shared__ int2 slot_meta[kStreamWarps][kStreamStages];  // (member, window) per ring slot
+  __shared__ __align__(8) uint64_t slot_bar[kStreamWarps][kStreamStages];
   const int K = *kcur;
   if (K <= 0) return;
   const uint32_t mask = dev_cap(K) - 1;
@@ -282,8 +318,14 @@ compare_stream_kernel(DedupState st, const int* kcur) {
   int32_t* ring = sm + ((lr + 3) & ~3) + kStageTok * kStreamStages * wid;
   int2* meta = slot_meta[wid];
   const int32_t* pr = st.tok + st.off[0];
+  const int32_t* tok_end = st.tok + st.off[st.P];  // bulk copies must not read past it
   for (int i = threadIdx.x; i < lr; i += blockDim.x) rep[i] = pr[i];
+  uint64_t* bars = slot_bar[wid];
+  if (lane == 0)
+    for (int q = 0; q < kStreamStages; ++q) mbar_init(&bars[q], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
+  uint32_t parity = 0;  // bit s: phase parity to wait for on slot s (warp-uniform)
   // Each warp owns a contiguous block of members (adjacent prompts are
   // adjacent in the CSR) and streams their windows back to back: the issue
   // cursor runs kStreamStages-1 windows ahead of the compare cursor across
@@ -318,24 +360,36 @@ compare_stream_kernel(DedupState st, const int* kcur) {
         iwin = 0;
       }
       const int slot = seq_issue % kStreamStages;
+      // the slot was consumed by this warp one window ago (the __syncwarp
+      // after its compare); order those generic reads before the async write
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (im < cnt) {
         const int n = __shfl_sync(0xffffffffu, my_n, im);
         const int sh = __shfl_sync(0xffffffffu, my_shift, im);
-        const int32_t* src = reinterpret_cast<const int32_t*>(__shfl_sync(0xffffffffu, my_src, im));
+        const int32_t* src = reinterpret_cast<const int32_t*>(__shfl_sync(0xffffffffu, my_src, im)) +
+                             iwin * kStageTok;
         int32_t* dst = ring + slot * kStageTok;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int j = lane + 32 * q;
-          const int p = -sh + iwin * kStageTok + 4 * j;
-          const int valid = min(4, max(0, n - p));
-          cp_async16(dst + 4 * j, valid > 0 ? src + iwin * kStageTok + 4 * j : src, valid * 4);
+        const int need = min(kStageTok, n + sh - iwin * kStageTok);  // tokens this window uses
+        const uint32_t bytes = (uint32_t)((need * 4 + 15) & ~15);
+        if (src + bytes / 4 <= tok_end) {
+          if (lane == 0) {
+            meta[slot] = make_int2(im, iwin);
+            mbar_arrive_tx(&bars[slot], bytes);
+            tma_load_1d(dst, src, bytes, &bars[slot]);
+          }
+        } else {  // the batch's last window: plain loads up to the end
+          for (int j = lane; j < need; j += 32) dst[j] = src + j < tok_end ? src[j] : 0;
+          __syncwarp();
+          if (lane == 0) {
+            meta[slot] = make_int2(im, iwin);
+            mbar_arrive(&bars[slot]);
+          }
         }
-        if (lane == 0) meta[slot] = make_int2(im, iwin);
         ++iwin;
       } else if (lane == 0) {
         meta[slot] = make_int2(-1, 0);
+        mbar_arrive(&bars[slot]);
       }
-      cp_async_commit();
       ++seq_issue;
     };
     auto finish = [&](int i) {  // record member i
@@ -347,9 +401,10 @@ compare_stream_kernel(DedupState st, const int* kcur) {
     for (int s0 = 0; s0 < kStreamStages - 1; ++s0) issue_next();
     for (;;) {
       issue_next();
-      cp_async_wait<kStreamStages - 1>();
-      __syncwarp();
       const int slot = seq_cmp % kStreamStages;
+      mbar_wait(&bars[slot], (parity >> slot) & 1u);
+      parity ^= 1u << slot;
+      __syncwarp();
       const int2 mw = meta[slot];
       ++seq_cmp;
       if (mw.x < 0) break;  // the issuer ran dry and everything issued is consumed
@@ -396,7 +451,14 @@ compare_stream_kernel(DedupState st, const int* kcur) {
       __syncwarp();
     }
     if (cur >= 0) finish(cur);
-    cp_async_wait<0>();
+    // drain the windows issued ahead of the last compare (their phases must
+    // complete before the slots are reused by the next block of members)
+    while (seq_cmp < seq_issue) {
+      const int slot = seq_cmp % kStreamStages;
+      mbar_wait(&bars[slot], (parity >> slot) & 1u);
+      parity ^= 1u << slot;
+      ++seq_cmp;
+    }
     __syncwarp();
   }
 }
