@@ -260,3 +260,18 @@ def test_predictor_config_errors_match_reference():
             with pytest.raises(OracleError) as e:
                 o.predict_lengths(obs, depth, gt, *args[:3], args[3], ["p0"])
             assert e.value.status == 2, args
+
+
+@needs_ref
+def test_reference_trace_reader_wrapper():
+    """The trace oracle (ref_trace_prompts) returns the reference reader's
+    id-sorted prompt table, limits and error types."""
+    from cases import trace_csv
+    text = trace_csv([("b", 5, [1, 2, 3]), ("a", 9, ["4", "7x"])], g=3, max_prompt_len=8)
+    t = ref().trace_prompts(text)
+    assert t["ids"] == ["a", "b"] and t["gt"].tolist() == [9, 5]
+    assert t["offsets"].tolist() == [0, 2, 5] and t["tokens"].tolist() == [4, 7, 1, 2, 3]
+    assert (t["g"], t["max_prompt_len"], t["max_response_len"]) == (3, 8, 2048)
+    with pytest.raises(OracleError) as e:
+        ref().trace_prompts(trace_csv([("a", 1, [1])], header=False))
+    assert e.value.status == 7
