@@ -417,6 +417,8 @@ compare_stream_kernel(DedupState st, const int* kcur) {
       const int n = __shfl_sync(0xffffffffu, my_n, cur);
       const int sh = __shfl_sync(0xffffffffu, my_shift, cur);
       const int32_t* buf = ring + slot * kStageTok;
+      // per int4: a 4-bit mismatch mask over the positions in [0, n); the
+      // lane keeps its first mismatch (q ascending = position ascending)
       int best = INT32_MAX;
       if (sh == 0) {  // member and representative chunks are both 16B aligned
 #pragma unroll
@@ -426,11 +428,10 @@ compare_stream_kernel(DedupState st, const int* kcur) {
           if (best == INT32_MAX && p < n) {
             const int4 a4 = *reinterpret_cast<const int4*>(buf + 4 * j);
             const int4 b4 = *reinterpret_cast<const int4*>(rep + p);
-            const int e[4] = {a4.x, a4.y, a4.z, a4.w};
-            const int f[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-              if (best == INT32_MAX && p + t < n && e[t] != f[t]) best = p + t;
+            uint32_t m = (uint32_t)(a4.x != b4.x) | ((uint32_t)(a4.y != b4.y) << 1) |
+                         ((uint32_t)(a4.z != b4.z) << 2) | ((uint32_t)(a4.w != b4.w) << 3);
+            if (n - p < 4) m &= (1u << (n - p)) - 1;
+            if (m) best = p + __ffs(m) - 1;
           }
         }
       } else {
@@ -438,16 +439,20 @@ compare_stream_kernel(DedupState st, const int* kcur) {
         for (int q = 0; q < 4; ++q) {
           const int j = lane + 32 * q;
           const int p = -sh + mw.y * kStageTok + 4 * j;
-          const int4 a4 = *reinterpret_cast<const int4*>(buf + 4 * j);
-          const int e[4] = {a4.x, a4.y, a4.z, a4.w};
+          if (best == INT32_MAX && p < n && p + 3 >= 0) {
+            const int4 a4 = *reinterpret_cast<const int4*>(buf + 4 * j);
+            const int e[4] = {a4.x, a4.y, a4.z, a4.w};
+            uint32_t m = 0;
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int pos = p + t;
-            if (pos >= 0 && pos < n && best == INT32_MAX && e[t] != rep[pos]) best = pos;
+            for (int t = 0; t < 4; ++t) {
+              const int pos = p + t;
+              if (pos >= 0 && pos < n) m |= (uint32_t)(e[t] != rep[pos]) << t;
+            }
+            if (m) best = p + __ffs(m) - 1;
           }
         }
       }
-      found = warp_min(best);
+      found = __any_sync(0xffffffffu, best != INT32_MAX) ? warp_min(best) : INT32_MAX;
       __syncwarp();
     }
     if (cur >= 0) finish(cur);
