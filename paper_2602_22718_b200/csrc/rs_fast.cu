@@ -1350,6 +1350,14 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
   return RS_OK;
 }
 
+bool lockstep_ok(const DevProfile& prof, int G) {
+  const int64_t ncm = prof.c_hi - prof.c_lo + 1;
+  const int64_t live_top = std::max<int64_t>(1, (prof.b_hi + G - 1) / G);
+  // clamped tail + piece ends in shared memory, well inside one SM's share
+  return fast_profile_ok(prof, G) && ncm <= kTopCap &&
+         sizeof(double) * live_top + sizeof(uint16_t) * (ncm + 1) <= 96 * 1024;
+}
+
 int lockstep_slots(rs_ctx* ctx, const DevProfile& prof, int G) {
   const int64_t ncm = prof.c_hi - prof.c_lo + 1;
   const int64_t live_top = std::max<int64_t>(1, (prof.b_hi + G - 1) / G);

@@ -123,6 +123,8 @@ struct LsFuse {
 int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, CandRange cr,
                   double* gt, const LsFuse* fuse = nullptr, int ctas_per_sm = 0);
 bool lockstep_fuses_select(CandRange cr);
+// The lockstep evaluator's profile limits (context memo, shared memory).
+bool lockstep_ok(const DevProfile& prof, int G);
 // CTA slots of the lockstep evaluator on this device (one scenario each).
 int lockstep_slots(rs_ctx* ctx, const DevProfile& prof, int G);
 

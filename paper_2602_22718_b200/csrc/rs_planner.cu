@@ -657,7 +657,7 @@ static int eval_batch(rs_ctx* ctx, const Built& b, int S, const DevProfile& dp, 
     // the lockstep evaluator runs one CTA per scenario: even a partial wave
     // (a sweep's last batch) beats splitting candidates over CTAs from about
     // 32 scenarios on
-    if (S >= kLockstepMinScenarios && dp.c_hi - dp.c_lo + 1 <= kTopCap) {
+    if (S >= kLockstepMinScenarios && lockstep_ok(dp, G)) {
       const bool f = fuse && fused && lockstep_fuses_select(cr);
       if (f) {
         *fused = true;
@@ -774,7 +774,7 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
   const int Bmem = (int)std::max<size_t>(
       1, std::min<size_t>({(size_t)S, (size_t)(8ull << 30) / per_scen, (size_t)2048}));
   std::vector<int> sizes, cps;  // scenarios and lockstep CTAs per SM, per batch
-  if (allow_fast) {
+  if (allow_fast && lockstep_ok(dp, G)) {
     plan_batches(S, Bmem, lockstep_slots(ctx, dp, G) / ctx->num_sms, ctx->num_sms, &sizes, &cps);
   } else {
     for (int s0 = 0; s0 < S; s0 += Bmem) {

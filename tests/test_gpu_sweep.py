@@ -151,3 +151,26 @@ def test_sweep_lockstep_wide_candidate_range():
     """More than 256 candidates: two lockstep CTAs per scenario, select and
     aggregate unfused (S >= 32 takes the lockstep evaluator)."""
     check_sweep(c4_spec(40, count=1400, first=321), 2, 320, lam=0.55, g=4)
+
+
+def test_sweep_lockstep_wide_batch_profile():
+    """Lockstep evaluator with a large batch axis (G=1, batch knots to 2,048:
+    2,047 small-batch rows, a 2,048-entry clamped tail) and fractional context
+    knots (piece ends from floor/ceil of non-integers)."""
+    from paper_2602_22718_b200.rollsim import LatencyProfile
+    bk = [1.0, 7.5, 64.0, 512.0, 2048.0]
+    ck = [50.0, 333.3, 1500.5, 3000.0]
+    grid = [[0.004 + 1e-5 * b + 2e-6 * c + 3e-9 * b * c for c in ck] for b in bk]
+    prof = LatencyProfile(bk, ck, grid, 0.0007, 2)
+    check_sweep(c4_spec(40, count=1000, first=888), 1, 64, prof=prof, lam=0.35, g=1)
+
+
+def test_sweep_huge_batch_axis_falls_back():
+    """A batch axis too long for the lockstep evaluator's shared-memory tail
+    (G=1, batch knots to 32,768) takes the per-group evaluator, same bits."""
+    from paper_2602_22718_b200.rollsim import LatencyProfile
+    bk = [1.0, 1024.0, 32768.0]
+    ck = [128.0, 4096.0]
+    grid = [[0.005 + 1e-6 * b + 1e-6 * c for c in ck] for b in bk]
+    prof = LatencyProfile(bk, ck, grid, 0.0005, 2)
+    check_sweep(c4_spec(36, count=600, first=5), 1, 40, prof=prof, lam=0.5, g=1)
