@@ -855,8 +855,7 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
     LsFuse fuse{o_tt, o_cc, out->idle_slot_ticks ? o_idle : (int64_t*)nullptr, o_ns, dp.rho,
                 lambda, gpus};
     bool fused = false, fused_select = false;
-    static const bool no_fuse = getenv("RS_NO_FUSE") != nullptr;  // A/B switch
-    RS_TRY(eval_batch(ctx, built, Sb, dp, n_min, n_max, G, gt, no_fuse ? nullptr : &fuse, &fused,
+    RS_TRY(eval_batch(ctx, built, Sb, dp, n_min, n_max, G, gt, &fuse, &fused,
                       &fused_select, cps[bi]));
     if (!fused)
       RS_TRY(reduce_batch(ctx, built, Sb, n_min, n_max, G, dp.rho, gpus, gt, o_tt, o_cc,
