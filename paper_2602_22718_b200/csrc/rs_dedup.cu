@@ -233,6 +233,11 @@ __device__ __forceinline__ void record_member(const DedupState& st, int64_t k, i
   st.m_slot[k] = (int32_t)sb;
 }
 
+// Rounds >= 1: one lane per member probes the first kProbe tokens past the
+// class LCP; nearly every member branches there. Members still matching
+// after the probe are handed, one at a time, to the whole warp (warp_lcp).
+constexpr int kProbe = 4;
+
 __global__ void __launch_bounds__(256)
 compare_kernel(DedupState st, int cur, const int* kcur) {
   const int K = *kcur;
@@ -240,15 +245,37 @@ compare_kernel(DedupState st, int cur, const int* kcur) {
   const uint32_t mask = dev_cap(K) - 1;
   const int lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < K; k += W) {
-    const int m = st.mem_idx[cur][k];
-    const int c = st.mem_cls[cur][k];
-    const int r = st.cls_rep[cur][c];
-    const int l0 = st.cls_lcp[cur][c];
-    const int lm = st.len[m], lr = st.len[r];
-    const int n = min(lm, lr);
-    const int x = warp_lcp(st.tok + st.off[m], st.tok + st.off[r], l0, n);
-    if (lane == 0) record_member(st, k, m, c, r, x, lm, lr, mask);
+  for (int64_t k0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; k0 < K;
+       k0 += W * 32) {
+    const int64_t k = k0 + lane;
+    int m = 0, c = 0, r = 0, lm = 0, lr = 0, n = 0, x = 0;
+    bool slow = false;
+    if (k < K) {
+      m = st.mem_idx[cur][k];
+      c = st.mem_cls[cur][k];
+      r = st.cls_rep[cur][c];
+      x = st.cls_lcp[cur][c];
+      lm = st.len[m];
+      lr = st.len[r];
+      n = min(lm, lr);
+      const int32_t* pm = st.tok + st.off[m];
+      const int32_t* pr = st.tok + st.off[r];
+      const int lim = min(n, x + kProbe);
+      while (x < lim && __ldg(pm + x) == __ldg(pr + x)) ++x;
+      slow = x == lim && lim < n;
+      if (!slow) record_member(st, k, m, c, r, x, lm, lr, mask);
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, slow);
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int sm = __shfl_sync(0xffffffffu, m, src);
+      const int sr = __shfl_sync(0xffffffffu, r, src);
+      const int sx = __shfl_sync(0xffffffffu, x, src);
+      const int sn = __shfl_sync(0xffffffffu, n, src);
+      const int xx = warp_lcp(st.tok + st.off[sm], st.tok + st.off[sr], sx, sn);
+      if (lane == src) record_member(st, k, m, c, r, xx, lm, lr, mask);
+    }
   }
 }
 
@@ -678,7 +705,6 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
   // from HBM; the host checks for completion once per kRoundsPerSync.
   int k0 = P - 1;
   RS_TRY(h2d(ctx, kc, &k0, 4));
-  const int wblocks = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)P + 7) / 8, 64 * ctx->num_sms));
   const int cblocks = (int)std::max<int64_t>(1, std::min<int64_t>((cap + 255) / 256, 8 * ctx->num_sms));
   const int pblocks = (int)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, 8 * ctx->num_sms));
   // round-0 streaming kernel: representative + per-warp rings in smem
@@ -702,7 +728,7 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
                   stream_smem, st, kcur);
       } else {
         RS_LAUNCH(ctx, round + r == 0 ? "dedup_compare_r0" : "dedup_compare", compare_kernel,
-                  wblocks, 256, 0, st, cur, kcur);
+                  pblocks, 256, 0, st, cur, kcur);
       }
       RS_LAUNCH(ctx, "dedup_finalize", finalize_kernel, cblocks, 256, 0, st, cur, kcur);
       RS_LAUNCH(ctx, "dedup_compact", compact_kernel, pblocks, 256, 0, st, cur, kcur, knext);
