@@ -90,6 +90,7 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
   __shared__ long long wsum64[32];
   __shared__ int bad, s_nw;
   __shared__ int wb[kMaxWin + 1];  // window w = buckets [wb[w], wb[w + 1])
+  __shared__ int2 s_scan[2][2][kHalfT / 32];  // per half: warp totals of the max scans
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t i0 = ss.item_off[s];
@@ -309,48 +310,157 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
         half_sync(h);
         continue;
       }
-      for (int i = ht; i < n; i += kHalfT) {
-        const int4 r = ss.rec[i0 + ws + i];
-        const long long bits = ((long long)r.y << 32) | (unsigned)r.x;
-        const double p = __longlong_as_double(bits);
-        const double fm1 = ceil(p) - 1.0;
-        w_key[i] = bits;
-        w_q[i] = fm1 >= 1.0 ? (uint32_t)((bits - __double_as_longlong(fm1)) >> 21) : 0u;
-        w_id[i] = r.z;
-        w_pk[i] = r.w;
+      {
+        int4 r[4];  // n <= 4 * kHalfT: all four loads in flight at once
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = ht + u * kHalfT;
+          if (i < n) r[u] = __ldcs(ss.rec + i0 + ws + i);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = ht + u * kHalfT;
+          if (i < n) {
+            const long long bits = ((long long)r[u].y << 32) | (unsigned)r[u].x;
+            const double fm1 = ceil(__longlong_as_double(bits)) - 1.0;
+            w_key[i] = bits;
+            w_q[i] = fm1 >= 1.0 ? (uint32_t)((bits - __double_as_longlong(fm1)) >> 21) : 0u;
+            w_id[i] = r[u].z;
+            w_pk[i] = r[u].w;
+          }
+        }
       }
       half_sync(h);
+      // rank: count the bucket's records with a larger q, four keys per
+      // 16-byte load; the full (pred, id) order only when q ties
+      const uint4* q4 = reinterpret_cast<const uint4*>(w_q);
       for (int i = ht; i < n; i += kHalfT) {
         const int k = w_pk[i] >> 16;
         const int lo = (k == 0 ? 0 : segend[k - 1]) - ws, hi = segend[k] - ws;
         const uint32_t q = w_q[i];
-        int rank = 0;
-        for (int j = lo; j < hi; ++j) {
+        int rank = 0, eq = 0;
+        int j = lo;
+        for (; j < hi && (j & 3); ++j) {
           const uint32_t qj = w_q[j];
           rank += qj > q ? 1 : 0;
-          if (qj == q && j != i) {
-            const long long kj = w_key[j], key = w_key[i];
-            rank += (kj > key || (kj == key && w_id[j] < w_id[i])) ? 1 : 0;
+          eq += qj == q ? 1 : 0;
+        }
+        for (; j + 4 <= hi; j += 4) {
+          const uint4 v = q4[j >> 2];
+          rank += (v.x > q ? 1 : 0) + (v.y > q ? 1 : 0) + (v.z > q ? 1 : 0) + (v.w > q ? 1 : 0);
+          eq += (v.x == q ? 1 : 0) + (v.y == q ? 1 : 0) + (v.z == q ? 1 : 0) + (v.w == q ? 1 : 0);
+        }
+        for (; j < hi; ++j) {
+          const uint32_t qj = w_q[j];
+          rank += qj > q ? 1 : 0;
+          eq += qj == q ? 1 : 0;
+        }
+        if (eq > 1) {  // q ties (always in bucket f = 1): full comparison
+          const long long key = w_key[i];
+          const int id = w_id[i];
+          rank = 0;
+          for (int jj = lo; jj < hi; ++jj) {
+            const uint32_t qj = w_q[jj];
+            const long long kj = w_key[jj];
+            rank += (qj > q || (qj == q && (kj > key || (kj == key && w_id[jj] < id)))) ? 1 : 0;
           }
         }
         const int pl = w_pk[i] & 0xffff;
-        w_pl[lo + rank] = pl;
+        w_pl[lo + rank] = pl | ((k - k0) << 16);
+        if (lo + rank == hi - 1)  // the bucket's finish tick, for its seg entry
+          w_pm[k - k0] = (int)ceil(__longlong_as_double(w_key[i]));
         ss.plen_r[i0 + ws + lo + rank] = pl;
         if (need_order) ss.order_r[i0 + ws + lo + rank] = w_id[i];
       }
       half_sync(h);
-      for (int k = k0 + ht; k < k1; k += kHalfT) {  // one thread per bucket
-        const int lo = (k == 0 ? 0 : segend[k - 1]) - ws, hi = segend[k] - ws;
-        int pm = 0;
-        for (int j = lo; j < hi; ++j) {
-          pm = max(pm, w_pl[j]);
-          w_pm[j] = pm;
+      // in-bucket prefix / suffix prompt_len maxima: segmented max scans
+      // over the window, four positions per thread (n <= 4 * kHalfT)
+      {
+        const int p0 = 4 * ht;
+        int v[4], kl[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int x = p0 + t < n ? w_pl[p0 + t] : 0;
+          v[t] = x & 0xffff;
+          kl[t] = p0 + t < n ? x >> 16 : -1;
         }
-        ss.seg[so + k].x |= pm << 16;
-        int sm = 0;
-        for (int j = hi - 1; j >= lo; --j) {
-          sm = max(sm, w_pl[j]);
-          ss.rinfo[i0 + ws + j] = make_int2(k, sm | (w_pm[j] << 16));
+        const int kprev = p0 > 0 && p0 - 1 < n ? w_pl[p0 - 1] >> 16 : -2;
+        const int knext = p0 + 4 < n ? w_pl[p0 + 4] >> 16 : -2;
+        bool head[4], tail[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          head[t] = kl[t] >= 0 && kl[t] != (t == 0 ? kprev : kl[t - 1]);
+          tail[t] = kl[t] >= 0 && kl[t] != (t == 3 ? knext : kl[t + 1]);
+        }
+        // thread aggregates (has boundary, value from the last boundary on)
+        int ff = 0, fv = 0, bf = 0, bv = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          fv = head[t] ? v[t] : max(fv, v[t]);
+          ff |= head[t];
+        }
+#pragma unroll
+        for (int t = 3; t >= 0; --t) {
+          bv = tail[t] ? v[t] : max(bv, v[t]);
+          bf |= tail[t];
+        }
+        const int hl = ht & 31, hw = ht >> 5;
+        int sf = ff, sv = fv, rf = bf, rv = bv;  // inclusive forward / backward
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int of = __shfl_up_sync(0xffffffffu, sf, d), ov = __shfl_up_sync(0xffffffffu, sv, d);
+          const int uf = __shfl_down_sync(0xffffffffu, rf, d), uv = __shfl_down_sync(0xffffffffu, rv, d);
+          if (hl >= d) {
+            sv = sf ? sv : max(sv, ov);
+            sf |= of;
+          }
+          if (hl + d < 32) {
+            rv = rf ? rv : max(rv, uv);
+            rf |= uf;
+          }
+        }
+        if (hl == 31) s_scan[h][0][hw] = make_int2(sf, sv);
+        if (hl == 0) s_scan[h][1][hw] = make_int2(rf, rv);
+        int ef = __shfl_up_sync(0xffffffffu, sf, 1), ev = __shfl_up_sync(0xffffffffu, sv, 1);
+        int gf = __shfl_down_sync(0xffffffffu, rf, 1), gv = __shfl_down_sync(0xffffffffu, rv, 1);
+        if (hl == 0) ef = ev = 0;
+        if (hl == 31) gf = gv = 0;
+        half_sync(h);
+        // carries from the other warps: segmented scans of the 16 warp
+        // totals, forward over lanes 0..15, backward over lanes 16..31
+        constexpr int kHW = kHalfT / 32;
+        int2 wt = hl < kHW ? s_scan[h][0][hl] : s_scan[h][1][kHW - 1 - (hl - kHW)];
+        int tf = wt.x, tv = wt.y;
+#pragma unroll
+        for (int d = 1; d < kHW; d <<= 1) {
+          const int of = __shfl_up_sync(0xffffffffu, tf, d), ov = __shfl_up_sync(0xffffffffu, tv, d);
+          if ((hl & (kHW - 1)) >= d) {
+            tv = tf ? tv : max(tv, ov);
+            tf |= of;
+          }
+        }
+        // forward carry of warp hw: inclusive total of warps < hw (lane hw - 1);
+        // backward carry: inclusive total of warps > hw (lane kHW + kHW - 2 - hw)
+        const int cvl = __shfl_sync(0xffffffffu, tv, max(hw - 1, 0));
+        const int dvl = __shfl_sync(0xffffffffu, tv, kHW + max(kHW - 2 - hw, 0));
+        const int cv = hw > 0 ? cvl : 0;
+        const int dv = hw < kHW - 1 ? dvl : 0;
+        int run = ef ? ev : max(cv, ev);
+        int pm[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          run = head[t] ? v[t] : max(run, v[t]);
+          pm[t] = run;
+        }
+        run = gf ? gv : max(dv, gv);
+#pragma unroll
+        for (int t = 3; t >= 0; --t) {
+          run = tail[t] ? v[t] : max(run, v[t]);
+          if (kl[t] >= 0) {
+            const int k = k0 + kl[t];
+            ss.rinfo[i0 + ws + p0 + t] = make_int2(k, run | (pm[t] << 16));
+            if (tail[t]) ss.seg[so + k].x = w_pm[kl[t]] | (pm[t] << 16);
+          }
         }
       }
       half_sync(h);
