@@ -203,10 +203,7 @@ __device__ __forceinline__ uint32_t dev_cap(int K) {
 
 // Clears the grouping tables for this round (capacity from the device-side
 // member count) and the next round's counter.
-__global__ void round_prep_kernel(DedupState st, const int* kcur, int* knext) {
-  const int K = *kcur;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *knext = 0;
-  if (K <= 0) return;
+__device__ __forceinline__ void prep_phase(const DedupState& st, int K) {
   const uint32_t cap = dev_cap(K);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
     st.a_keys[i] = kEmpty;
@@ -214,6 +211,12 @@ __global__ void round_prep_kernel(DedupState st, const int* kcur, int* knext) {
     st.b_rep[i] = INT32_MAX;
     st.b_cnt[i] = 0;
   }
+}
+
+__global__ void round_prep_kernel(DedupState st, const int* kcur, int* knext) {
+  const int K = *kcur;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *knext = 0;
+  if (K > 0) prep_phase(st, K);
 }
 
 // Record member k's branch (x, t) against representative r of class c.
@@ -238,10 +241,7 @@ __device__ __forceinline__ void record_member(const DedupState& st, int64_t k, i
 // after the probe are handed, one at a time, to the whole warp (warp_lcp).
 constexpr int kProbe = 4;
 
-__global__ void __launch_bounds__(256)
-compare_kernel(DedupState st, int cur, const int* kcur) {
-  const int K = *kcur;
-  if (K <= 0) return;
+__device__ __forceinline__ void compare_phase(const DedupState& st, int cur, int K) {
   const uint32_t mask = dev_cap(K) - 1;
   const int lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -277,6 +277,12 @@ compare_kernel(DedupState st, int cur, const int* kcur) {
       if (lane == src) record_member(st, k, m, c, r, xx, lm, lr, mask);
     }
   }
+}
+
+// Round 0 when the representative is too long for the streaming kernel.
+__global__ void __launch_bounds__(256) compare_kernel(DedupState st, int cur, const int* kcur) {
+  const int K = *kcur;
+  if (K > 0) compare_phase(st, cur, K);
 }
 
 // Round 0 (one class, representative = prompt 0): the HBM-bound pass.
@@ -488,9 +494,7 @@ compare_stream_kernel(DedupState st, const int* kcur) {
 }
 
 // One thread per B slot: branch children, leaves, next classes.
-__global__ void finalize_kernel(DedupState st, int cur, const int* kcur) {
-  const int K = *kcur;
-  if (K <= 0) return;
+__device__ __forceinline__ void finalize_phase(const DedupState& st, int cur, int K) {
   const uint32_t cap = dev_cap(K);
   const int nxt = cur ^ 1;
   for (uint32_t sb = blockIdx.x * blockDim.x + threadIdx.x; sb < cap; sb += gridDim.x * blockDim.x) {
@@ -517,9 +521,7 @@ __global__ void finalize_kernel(DedupState st, int cur, const int* kcur) {
   }
 }
 
-__global__ void compact_kernel(DedupState st, int cur, const int* kcur, int* knext) {
-  const int K = *kcur;
-  if (K <= 0) return;
+__device__ __forceinline__ void compact_phase(const DedupState& st, int cur, int K, int* knext) {
   const int nxt = cur ^ 1;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
     int sb = st.m_slot[k];
@@ -541,6 +543,53 @@ __global__ void compact_kernel(DedupState st, int cur, const int* kcur, int* kne
     base = __shfl_sync(act, base, leader);
     st.mem_idx[nxt][base + rank] = m;
     st.mem_cls[nxt][base + rank] = sb;
+  }
+}
+
+// Grid-wide barrier of the persistent refinement (all CTAs co-resident: the
+// kernel is launched cooperatively). A 64-bit arrival counter, zeroed before
+// the launch; barrier g completes when it reaches g * gridDim.x. The acquire
+// load invalidates the SM's L1, so plain loads after the barrier see the
+// other CTAs' writes (data written inside the kernel is never read via ldg).
+__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long* target) {
+  *target += gridDim.x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1ULL);
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+      if (v >= *target) break;
+      __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Every round after round 0's compare, in one persistent launch: finalize and
+// compact round r, then (while members remain) clear the tables and compare
+// round r + 1. kc[0..1] alternate as the current / next member counts.
+__global__ void __launch_bounds__(256)
+refine_kernel(DedupState st, int* kc, unsigned long long* bar) {
+  unsigned long long target = 0;
+  int cur = 0;
+  for (;;) {
+    const int K = *(volatile int*)(kc + cur);
+    if (K <= 0) break;  // a single prompt: no members at all
+    if (blockIdx.x == 0 && threadIdx.x == 0) kc[cur ^ 1] = 0;
+    finalize_phase(st, cur, K);
+    grid_barrier(bar, &target);
+    compact_phase(st, cur, K, kc + (cur ^ 1));
+    grid_barrier(bar, &target);
+    const int K2 = *(volatile int*)(kc + (cur ^ 1));
+    if (K2 <= 0) break;
+    prep_phase(st, K2);
+    grid_barrier(bar, &target);
+    compare_phase(st, cur ^ 1, K2);
+    grid_barrier(bar, &target);
+    cur ^= 1;
   }
 }
 
@@ -630,13 +679,30 @@ uint32_t pow2_at_least(int64_t v) {
 
 }  // namespace
 
+static int launch_refine(rs_ctx* ctx, DedupState st, int* kc, unsigned long long* bar) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, 256, 0));
+    per_sm = std::max(1, std::min(per_sm, 4));
+  }
+  const int blocks = per_sm * ctx->num_sms;
+  void* args[] = {&st, &kc, &bar};
+  cudaEvent_t ev = nullptr;
+  timer_begin(ctx, "dedup_refine", &ev);
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)refine_kernel, blocks, 256, args, 0, ctx->stream);
+  ctx->launches++;
+  if (e != cudaSuccess) return fail(RS_E_CUDA, std::string("launch dedup_refine: ") + cudaGetErrorString(e));
+  timer_end(ctx, "dedup_refine", ev);
+  return RS_OK;
+}
+
 // Runs the refinement on device-resident CSR. cap_len = INT32_MAX for the
 // full index. Fills node_diff/end_count/len_count/stats (and labels if
-// non-null). Host-synchronous (one flag read per round).
-// tail (nullable): enqueued after every block of rounds, before the host
-// checks for completion, so work that consumes the final state (the tables
-// and their read-back) shares that synchronisation; it runs again if more
-// rounds follow.
+// non-null). Two host synchronisations: after the lengths pass (sizes) and
+// after the persistent refinement.
+// tail (nullable): enqueued after the refinement, before that final
+// synchronisation, so work that consumes the final state (the tables and
+// their read-back) shares it.
 struct RefineTail {
   virtual int enqueue(rs_ctx* ctx, const DedupState& st, int max_len) = 0;
 };
@@ -645,12 +711,10 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
                         int32_t cap_len, int strict, bool want_labels, int32_t max_len_hint,
                         DedupState* out_state, int64_t* h_stats, int32_t* h_labels,
                         RefineTail* tail = nullptr) {
-  constexpr int kRoundsPerSync = 4;
-  constexpr int kMaxRounds = 1 << 20;
   const uint32_t cap = pow2_at_least(2 * (int64_t)P + 2);
   const size_t base_bytes = abytes(P, 4) + abytes(4, 8) + abytes(P, 4) * 4 +
                             abytes(cap, 4) * 4 + abytes(P, 4) + abytes(cap, 8) * 2 +
-                            abytes(cap, 4) * 2 + abytes(kRoundsPerSync + 2, 4) + abytes(P, 4);
+                            abytes(cap, 4) * 2 + abytes(2, 4) + abytes(1, 8) + abytes(P, 4);
   // Tables are sized by the longest prompt; guess generously so the usual
   // case needs a single lengths pass and one host read.
   int64_t maxd = std::max<int64_t>(max_len_hint, 16384);
@@ -691,20 +755,22 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
   st.b_keys = arena_alloc<uint64_t>(ctx, cap);
   st.b_rep = arena_alloc<int32_t>(ctx, cap);
   st.b_cnt = arena_alloc<int32_t>(ctx, cap);
-  int* kc = arena_alloc<int32_t>(ctx, kRoundsPerSync + 2);  // member counts per round
+  int* kc = arena_alloc<int32_t>(ctx, 2);  // current / next member count
+  unsigned long long* bar = arena_alloc<unsigned long long>(ctx, 1);  // grid barrier
   st.counter = kc;
   st.labels = want_labels ? arena_alloc<int32_t>(ctx, std::max(P, 1)) : nullptr;
-  if (!kc || (want_labels && !st.labels)) return fail(RS_E_NOMEM, "arena exhausted (dedup)");
+  if (!kc || !bar || (want_labels && !st.labels)) return fail(RS_E_NOMEM, "arena exhausted (dedup)");
   RS_CUDA_TRY(cudaMemsetAsync(st.node_diff, 0, 8 * (md + 2), ctx->stream));
   RS_CUDA_TRY(cudaMemsetAsync(st.end_count, 0, 8 * (md + 2), ctx->stream));
   RS_CUDA_TRY(cudaMemsetAsync(st.len_count, 0, 8 * (md + 2), ctx->stream));
   int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, 8 * ctx->num_sms));
   RS_LAUNCH(ctx, "dedup_len_hist", len_hist_kernel, blocks, 256, 0, st);
   RS_LAUNCH(ctx, "dedup_init", init_root_kernel, blocks, 256, 0, st);
-  // Rounds run back to back on the device, each reading its member count
-  // from HBM; the host checks for completion once per kRoundsPerSync.
-  int k0 = P - 1;
-  RS_TRY(h2d(ctx, kc, &k0, 4));
+  // Round 0's compare, then every later round inside one persistent launch
+  // (refine_kernel): no host round trips until the tables are read back.
+  const int k0[2] = {P - 1, 0};
+  RS_TRY(h2d(ctx, kc, k0, 8));
+  RS_CUDA_TRY(cudaMemsetAsync(bar, 0, 8, ctx->stream));
   const int cblocks = (int)std::max<int64_t>(1, std::min<int64_t>((cap + 255) / 256, 8 * ctx->num_sms));
   const int pblocks = (int)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, 8 * ctx->num_sms));
   // round-0 streaming kernel: representative + per-warp rings in smem
@@ -717,33 +783,19 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
     RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compare_stream_kernel, kStreamWarps * 32, stream_smem));
     sblocks = std::max(1, per_sm) * ctx->num_sms;
   }
-  int cur = 0;
-  for (int round = 0; round < kMaxRounds; round += kRoundsPerSync) {
-    for (int r = 0; r < kRoundsPerSync; ++r) {
-      const int* kcur = kc + r;
-      int* knext = kc + r + 1;
-      RS_LAUNCH(ctx, "dedup_prep", round_prep_kernel, cblocks, 256, 0, st, kcur, knext);
-      if (round + r == 0 && stream_smem <= 200 * 1024) {
-        RS_LAUNCH(ctx, "dedup_compare_r0", compare_stream_kernel, sblocks, kStreamWarps * 32,
-                  stream_smem, st, kcur);
-      } else {
-        RS_LAUNCH(ctx, round + r == 0 ? "dedup_compare_r0" : "dedup_compare", compare_kernel,
-                  pblocks, 256, 0, st, cur, kcur);
-      }
-      RS_LAUNCH(ctx, "dedup_finalize", finalize_kernel, cblocks, 256, 0, st, cur, kcur);
-      RS_LAUNCH(ctx, "dedup_compact", compact_kernel, pblocks, 256, 0, st, cur, kcur, knext);
-      cur ^= 1;
-    }
-    int left = 0;
-    RS_TRY(d2h(ctx, &left, kc + kRoundsPerSync, 4));
-    if (tail) {
-      if (h_stats) RS_TRY(d2h(ctx, h_stats, st.stats, 4 * 8));
-      RS_TRY(tail->enqueue(ctx, st, md));
-    }
-    RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    if (left <= 0) break;
-    RS_CUDA_TRY(cudaMemcpyAsync(kc, kc + kRoundsPerSync, 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  RS_LAUNCH(ctx, "dedup_prep", round_prep_kernel, cblocks, 256, 0, st, kc, kc + 1);
+  if (stream_smem <= 200 * 1024) {
+    RS_LAUNCH(ctx, "dedup_compare_r0", compare_stream_kernel, sblocks, kStreamWarps * 32,
+              stream_smem, st, kc);
+  } else {
+    RS_LAUNCH(ctx, "dedup_compare_r0", compare_kernel, pblocks, 256, 0, st, 0, kc);
   }
+  RS_TRY(launch_refine(ctx, st, kc, bar));
+  if (tail) {
+    if (h_stats) RS_TRY(d2h(ctx, h_stats, st.stats, 4 * 8));
+    RS_TRY(tail->enqueue(ctx, st, md));
+  }
+  RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   if (h_stats && !tail) RS_TRY(d2h(ctx, h_stats, st.stats, 4 * 8));
   if (h_labels && P > 0) RS_TRY(d2h(ctx, h_labels, st.labels, 4ull * P));
   *out_state = st;
