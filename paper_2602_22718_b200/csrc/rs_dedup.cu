@@ -203,9 +203,9 @@ __device__ __forceinline__ uint32_t dev_cap(int K) {
 
 // Clears the grouping tables for this round (capacity from the device-side
 // member count) and the next round's counter.
-__device__ __forceinline__ void prep_phase(const DedupState& st, int K) {
+__device__ __forceinline__ void prep_phase(const DedupState& st, int K, int bid, int nb) {
   const uint32_t cap = dev_cap(K);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
+  for (uint32_t i = bid * blockDim.x + threadIdx.x; i < cap; i += nb * blockDim.x) {
     st.a_keys[i] = kEmpty;
     st.b_keys[i] = kEmpty;
     st.b_rep[i] = INT32_MAX;
@@ -216,7 +216,7 @@ __device__ __forceinline__ void prep_phase(const DedupState& st, int K) {
 __global__ void round_prep_kernel(DedupState st, const int* kcur, int* knext) {
   const int K = *kcur;
   if (blockIdx.x == 0 && threadIdx.x == 0) *knext = 0;
-  if (K > 0) prep_phase(st, K);
+  if (K > 0) prep_phase(st, K, blockIdx.x, gridDim.x);
 }
 
 // Record member k's branch (x, t) against representative r of class c.
@@ -241,11 +241,11 @@ __device__ __forceinline__ void record_member(const DedupState& st, int64_t k, i
 // after the probe are handed, one at a time, to the whole warp (warp_lcp).
 constexpr int kProbe = 4;
 
-__device__ __forceinline__ void compare_phase(const DedupState& st, int cur, int K) {
+__device__ __forceinline__ void compare_phase(const DedupState& st, int cur, int K, int bid, int nb) {
   const uint32_t mask = dev_cap(K) - 1;
   const int lane = threadIdx.x & 31;
-  const int64_t W = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t k0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; k0 < K;
+  const int64_t W = (int64_t)nb * (blockDim.x >> 5);
+  for (int64_t k0 = ((int64_t)bid * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; k0 < K;
        k0 += W * 32) {
     const int64_t k = k0 + lane;
     int m = 0, c = 0, r = 0, lm = 0, lr = 0, n = 0, x = 0;
@@ -282,7 +282,7 @@ __device__ __forceinline__ void compare_phase(const DedupState& st, int cur, int
 // Round 0 when the representative is too long for the streaming kernel.
 __global__ void __launch_bounds__(256) compare_kernel(DedupState st, int cur, const int* kcur) {
   const int K = *kcur;
-  if (K > 0) compare_phase(st, cur, K);
+  if (K > 0) compare_phase(st, cur, K, blockIdx.x, gridDim.x);
 }
 
 // Round 0 (one class, representative = prompt 0): the HBM-bound pass.
@@ -494,10 +494,10 @@ compare_stream_kernel(DedupState st, const int* kcur) {
 }
 
 // One thread per B slot: branch children, leaves, next classes.
-__device__ __forceinline__ void finalize_phase(const DedupState& st, int cur, int K) {
+__device__ __forceinline__ void finalize_phase(const DedupState& st, int cur, int K, int bid, int nb) {
   const uint32_t cap = dev_cap(K);
   const int nxt = cur ^ 1;
-  for (uint32_t sb = blockIdx.x * blockDim.x + threadIdx.x; sb < cap; sb += gridDim.x * blockDim.x) {
+  for (uint32_t sb = bid * blockDim.x + threadIdx.x; sb < cap; sb += nb * blockDim.x) {
     uint64_t key = st.b_keys[sb];
     if (key == kEmpty) continue;
     uint32_t sa = (uint32_t)(key >> 33);
@@ -521,9 +521,10 @@ __device__ __forceinline__ void finalize_phase(const DedupState& st, int cur, in
   }
 }
 
-__device__ __forceinline__ void compact_phase(const DedupState& st, int cur, int K, int* knext) {
+__device__ __forceinline__ void compact_phase(const DedupState& st, int cur, int K, int* knext,
+                                              int bid, int nb) {
   const int nxt = cur ^ 1;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
+  for (int k = bid * blockDim.x + threadIdx.x; k < K; k += nb * blockDim.x) {
     int sb = st.m_slot[k];
     if (sb < 0) continue;
     int m = st.mem_idx[cur][k];
@@ -548,25 +549,27 @@ __device__ __forceinline__ void compact_phase(const DedupState& st, int cur, int
 
 // Grid-wide barrier of the persistent refinement (all CTAs co-resident: the
 // kernel is launched cooperatively). A 64-bit arrival counter, zeroed before
-// the launch; barrier g completes when it reaches g * gridDim.x. The acquire
-// load invalidates the SM's L1, so plain loads after the barrier see the
-// other CTAs' writes (data written inside the kernel is never read via ldg).
+// the launch; barrier g completes when it reaches g * gridDim.x. Arrival is a
+// release (cumulative over the CTA's writes ordered by the bar.sync before
+// it), the poll an acquire, which invalidates the SM's L1: plain loads after
+// the barrier see the other CTAs' writes (data written inside the kernel is
+// never read through the non-coherent path).
 __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long* target) {
   *target += gridDim.x;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1ULL);
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
     unsigned long long v;
-    for (;;) {
+    do {
       asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
-      if (v >= *target) break;
-      __nanosleep(64);
-    }
-    __threadfence();
+    } while (v < *target);
   }
   __syncthreads();
 }
+
+// Rounds with at most this many members finish on CTA 0 alone (CTA-wide
+// barriers instead of grid-wide ones: the last rounds hold a handful).
+constexpr int kSoloMembers = 1024;
 
 // Every round after round 0's compare, in one persistent launch: finalize and
 // compact round r, then (while members remain) clear the tables and compare
@@ -575,98 +578,122 @@ __global__ void __launch_bounds__(256)
 refine_kernel(DedupState st, int* kc, unsigned long long* bar) {
   unsigned long long target = 0;
   int cur = 0;
+  bool solo = false;  // CTA 0 alone from here on
+  int bid = blockIdx.x, nb = gridDim.x;
+  auto sync = [&]() {
+    if (solo) {  // the fence also invalidates L1 (table slots changed by atomics at L2)
+      __syncthreads();
+      if (threadIdx.x == 0) __threadfence();
+      __syncthreads();
+    } else {
+      grid_barrier(bar, &target);
+    }
+  };
   for (;;) {
     const int K = *(volatile int*)(kc + cur);
     if (K <= 0) break;  // a single prompt: no members at all
-    if (blockIdx.x == 0 && threadIdx.x == 0) kc[cur ^ 1] = 0;
-    finalize_phase(st, cur, K);
-    grid_barrier(bar, &target);
-    compact_phase(st, cur, K, kc + (cur ^ 1));
-    grid_barrier(bar, &target);
+    if (bid == 0 && threadIdx.x == 0) kc[cur ^ 1] = 0;
+    finalize_phase(st, cur, K, bid, nb);
+    sync();
+    compact_phase(st, cur, K, kc + (cur ^ 1), bid, nb);
+    sync();
     const int K2 = *(volatile int*)(kc + (cur ^ 1));
     if (K2 <= 0) break;
-    prep_phase(st, K2);
-    grid_barrier(bar, &target);
-    compare_phase(st, cur ^ 1, K2);
-    grid_barrier(bar, &target);
+    if (!solo && K2 <= kSoloMembers) {
+      if (blockIdx.x != 0) return;
+      solo = true;
+      nb = 1;
+    }
+    prep_phase(st, K2, bid, nb);
+    sync();
+    compare_phase(st, cur ^ 1, K2, bid, nb);
+    sync();
     cur ^= 1;
   }
 }
 
 // The five PrefixIndex tables from the difference array and the counts
-// (dedup.cpp:73-98): one CTA, chunked block scans with a carried total.
-constexpr int kTabT = 1024;
-
-__device__ __forceinline__ int64_t block_incl_scan64(int64_t v, int64_t* wsum) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int64_t incl = warp_incl_sum(v);
-  if (lane == 31) wsum[wid] = incl;
-  __syncthreads();
-  if (wid == 0) {
-    int64_t x = wsum[lane];
-    wsum[lane] = warp_incl_sum(x) - x;
-  }
-  __syncthreads();
-  int64_t r = wsum[wid] + incl;
-  __syncthreads();
-  return r;
-}
+// (dedup.cpp:73-98), one CTA. With x_m = x on depths 1..maxd and 0 elsewhere:
+//   nodes[d] = incl(node_diff_m)[d] (0 at d = 0 and d = maxd + 1)
+//   scb[d]   = incl(end_count_m)[d] - end_count_m[d]
+//   stb[d]   = incl(end_count_m * i)[d] - end_count_m[d] * d
+//   lcf[d]   = total(len_count_m) - incl(len_count_m)[d]
+//   ltf[d]   = total(len_count_m * i) - incl(len_count_m * i)[d]
+// Each thread scans kTabIPT consecutive depths; the five thread totals go
+// through one CTA scan per chunk of kTabT * kTabIPT depths.
+constexpr int kTabT = 512;
+constexpr int kTabIPT = 4;
+constexpr int kTabQ = 5;
 
 __global__ void __launch_bounds__(kTabT) tables_kernel(DedupState st, int maxd, int64_t* out) {
-  __shared__ int64_t wsum[32];
-  int64_t* nodes = out;
-  int64_t* scb = out + (maxd + 2);
-  int64_t* stb = out + 2 * (int64_t)(maxd + 2);
-  int64_t* lcf = out + 3 * (int64_t)(maxd + 2);
-  int64_t* ltf = out + 4 * (int64_t)(maxd + 2);
-  const int n = maxd + 2;  // indices 0 .. maxd+1
-  int64_t c_nodes = 0, c_scb = 0, c_stb = 0;
-  for (int d0 = 0; d0 < n; d0 += kTabT) {
-    const int d = d0 + threadIdx.x;
-    // nodes[d] = sum_{1<=i<=d} node_diff[i] for 1<=d<=maxd; 0 elsewhere
-    const int64_t nd = (d >= 1 && d <= maxd) ? st.node_diff[d] : 0;
-    // short tables: scb[d] = sum_{1<=i<d} end_count[i] (exclusive)
-    const int64_t ec = (d >= 1 && d <= maxd) ? st.end_count[d] : 0;
-    const int64_t in = block_incl_scan64(nd, wsum) + c_nodes;
-    const int64_t ic = block_incl_scan64(ec, wsum) + c_scb;
-    const int64_t it = block_incl_scan64(ec * d, wsum) + c_stb;
-    if (d < n) {
-      nodes[d] = (d >= 1 && d <= maxd) ? in : 0;
-      scb[d] = ic - ec;
-      stb[d] = it - ec * d;
+  __shared__ int64_t ws[kTabQ][32];
+  const int n = maxd + 2;  // depths 0 .. maxd + 1
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t* const tab[kTabQ] = {out, out + n, out + 2 * (int64_t)n, out + 3 * (int64_t)n,
+                               out + 4 * (int64_t)n};
+  // totals of the suffix tables: prompts of length >= 1, and all tokens
+  const int64_t tl = st.P - st.len_count[0], tt = st.stats[2];
+  int64_t carry[kTabQ] = {0, 0, 0, 0, 0};
+  for (int d0 = 0; d0 < n; d0 += kTabT * kTabIPT) {
+    int64_t v[kTabIPT][kTabQ];
+    int64_t run[kTabQ] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < kTabIPT; ++j) {
+      const int d = d0 + threadIdx.x * kTabIPT + j;
+      const bool in = d >= 1 && d <= maxd;
+      const int64_t nd = in ? st.node_diff[d] : 0;
+      const int64_t ec = in ? st.end_count[d] : 0;
+      const int64_t lc = in ? st.len_count[d] : 0;
+      const int64_t x[kTabQ] = {nd, ec, ec * d, lc, lc * d};
+#pragma unroll
+      for (int q = 0; q < kTabQ; ++q) {
+        run[q] += x[q];
+        v[j][q] = x[q];
+      }
     }
-    __shared__ int64_t carry[3];
+    // CTA exclusive scan of the thread totals, all five at once
+    int64_t incl[kTabQ];
+#pragma unroll
+    for (int q = 0; q < kTabQ; ++q) {
+      incl[q] = warp_incl_sum(run[q]);
+      if (lane == 31) ws[q][wid] = incl[q];
+    }
+    __syncthreads();
+    constexpr int kTabW = kTabT / 32;
+    if (wid == 0) {
+#pragma unroll
+      for (int q = 0; q < kTabQ; ++q) {
+        const int64_t x = lane < kTabW ? ws[q][lane] : 0;
+        ws[q][lane] = warp_incl_sum(x) - x;
+      }
+    }
+    __syncthreads();
+    int64_t pre[kTabQ];
+#pragma unroll
+    for (int q = 0; q < kTabQ; ++q) pre[q] = carry[q] + ws[q][wid] + incl[q] - run[q];
+#pragma unroll
+    for (int j = 0; j < kTabIPT; ++j) {
+      const int d = d0 + threadIdx.x * kTabIPT + j;
+#pragma unroll
+      for (int q = 0; q < kTabQ; ++q) pre[q] += v[j][q];
+      if (d < n) {
+        const bool in = d >= 1 && d <= maxd;
+        tab[0][d] = in ? pre[0] : 0;
+        tab[1][d] = pre[1] - v[j][1];
+        tab[2][d] = pre[2] - v[j][1] * d;
+        tab[3][d] = tl - pre[3];
+        tab[4][d] = tt - pre[4];
+      }
+    }
+    // carry = chunk total (the last warp's inclusive totals)
+    __syncthreads();
     if (threadIdx.x == kTabT - 1) {
-      carry[0] = in;
-      carry[1] = ic;
-      carry[2] = it;
+#pragma unroll
+      for (int q = 0; q < kTabQ; ++q) ws[q][0] = ws[q][kTabW - 1] + incl[q];
     }
     __syncthreads();
-    c_nodes = carry[0];
-    c_scb = carry[1];
-    c_stb = carry[2];
-    __syncthreads();
-  }
-  // longer tables: lcf[d] = sum_{d<i<=maxd} len_count[i] (suffix, exclusive)
-  int64_t c_lc = 0, c_lt = 0;
-  for (int e0 = 0; e0 < n; e0 += kTabT) {
-    const int d = maxd + 1 - (e0 + (int)threadIdx.x);  // descending d
-    const int i = d + 1;
-    const int64_t lc = (d >= 0 && i <= maxd) ? st.len_count[i] : 0;
-    const int64_t ilc = block_incl_scan64(lc, wsum) + c_lc;
-    const int64_t ilt = block_incl_scan64(lc * i, wsum) + c_lt;
-    if (d >= 0) {
-      lcf[d] = ilc;
-      ltf[d] = ilt;
-    }
-    __shared__ int64_t carry2[2];
-    if (threadIdx.x == kTabT - 1) {
-      carry2[0] = ilc;
-      carry2[1] = ilt;
-    }
-    __syncthreads();
-    c_lc = carry2[0];
-    c_lt = carry2[1];
+#pragma unroll
+    for (int q = 0; q < kTabQ; ++q) carry[q] += ws[q][0];
     __syncthreads();
   }
 }
@@ -703,8 +730,12 @@ static int launch_refine(rs_ctx* ctx, DedupState st, int* kc, unsigned long long
 // tail (nullable): enqueued after the refinement, before that final
 // synchronisation, so work that consumes the final state (the tables and
 // their read-back) shares it.
+// Pinned staging: the first kPinnedHead bytes hold the refinement's own
+// read-backs, a tail's follow.
+constexpr size_t kPinnedHead = 64;
 struct RefineTail {
   virtual int enqueue(rs_ctx* ctx, const DedupState& st, int max_len) = 0;
+  virtual void finish(rs_ctx* ctx) = 0;  // after the final synchronisation
 };
 
 static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off, int P,
@@ -734,9 +765,13 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
     RS_TRY(h2d(ctx, st.stats, init, sizeof(init)));
     int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, 8 * ctx->num_sms));
     RS_LAUNCH(ctx, "dedup_lengths", lengths_kernel, blocks, 256, 0, st, cap_len, strict, ctx->d_flags);
-    RS_TRY(d2h(ctx, hs, st.stats, sizeof(hs)));
-    RS_TRY(d2h(ctx, off01, d_off, sizeof(off01)));
+    RS_TRY(pinned_reserve(ctx, kPinnedHead));  // small read-backs stay asynchronous
+    int64_t* pin = reinterpret_cast<int64_t*>(ctx->pinned);
+    RS_CUDA_TRY(cudaMemcpyAsync(pin, st.stats, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+    RS_CUDA_TRY(cudaMemcpyAsync(pin + 4, d_off, sizeof(off01), cudaMemcpyDeviceToHost, ctx->stream));
     RS_TRY(sync_and_check(ctx));
+    std::memcpy(hs, pin, sizeof(hs));
+    std::memcpy(off01, pin + 4, sizeof(off01));
     if (hs[1] <= maxd) break;
     maxd = hs[1];
   }
@@ -791,12 +826,13 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
     RS_LAUNCH(ctx, "dedup_compare_r0", compare_kernel, pblocks, 256, 0, st, 0, kc);
   }
   RS_TRY(launch_refine(ctx, st, kc, bar));
-  if (tail) {
-    if (h_stats) RS_TRY(d2h(ctx, h_stats, st.stats, 4 * 8));
-    RS_TRY(tail->enqueue(ctx, st, md));
-  }
+  // read-backs through pinned memory: [stats | tail], one synchronisation
+  if (tail) RS_TRY(tail->enqueue(ctx, st, md));
+  if (h_stats)
+    RS_CUDA_TRY(cudaMemcpyAsync(ctx->pinned, st.stats, 4 * 8, cudaMemcpyDeviceToHost, ctx->stream));
   RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  if (h_stats && !tail) RS_TRY(d2h(ctx, h_stats, st.stats, 4 * 8));
+  if (h_stats) std::memcpy(h_stats, ctx->pinned, 4 * 8);
+  if (tail) tail->finish(ctx);
   if (h_labels && P > 0) RS_TRY(d2h(ctx, h_labels, st.labels, 4ull * P));
   *out_state = st;
   return RS_OK;
@@ -829,7 +865,13 @@ static int build_index_device(rs_ctx* ctx, const int32_t* d_tok, const int64_t* 
         h.resize(5ull * (md + 2));
       }
       RS_LAUNCH(c, "dedup_tables", tables_kernel, 1, kTabT, 0, st, md, d);
-      return d2h(c, h.data(), d, 8 * h.size());
+      RS_TRY(pinned_reserve(c, kPinnedHead + 8 * h.size()));
+      RS_CUDA_TRY(cudaMemcpyAsync(c->pinned + kPinnedHead, d, 8 * h.size(), cudaMemcpyDeviceToHost,
+                                  c->stream));
+      return RS_OK;
+    }
+    void finish(rs_ctx* c) override {
+      std::memcpy(h.data(), c->pinned + kPinnedHead, 8 * h.size());
     }
   } tab;
   DedupState st;

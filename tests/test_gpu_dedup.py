@@ -107,6 +107,20 @@ def test_larger_structured_batches():
         check_batch(seqs)
 
 
+def test_long_prompts_multi_chunk_tables():
+    """Prompts up to ~9,000 tokens: the tables kernel scans depths in several
+    chunks (2,048 per chunk) with carried totals."""
+    rng = np.random.RandomState(31)
+    head = rng.randint(0, 7, size=6000).tolist()
+    seqs = []
+    for i in range(60):
+        cut = rng.randint(1, len(head) + 1)
+        seqs.append(head[:cut] + rng.randint(0, 3, size=rng.randint(0, 3000)).tolist())
+    seqs = [s if s else [1] for s in seqs]
+    idx, _, _ = check_batch(seqs)
+    assert idx.max_prompt_len() > 4096
+
+
 def test_among_dedup_map_and_hashes():
     rng = Rng(77)
     for trial in range(40):
