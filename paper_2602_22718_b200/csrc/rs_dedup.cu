@@ -119,26 +119,35 @@ __global__ void lengths_kernel(DedupState st, int32_t cap_len, int strict, int* 
   }
 }
 
-__global__ void len_hist_kernel(DedupState st) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < st.P; i += gridDim.x * blockDim.x)
-    agg_add(st.len_count, st.len[i], 1);
-}
-
-__global__ void init_root_kernel(DedupState st) {
-  // Root class: rep = prompt 0 (smallest index), verified prefix 0.
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < st.P; i += gridDim.x * blockDim.x) {
-    if (i == 0) {
-      st.cls_rep[0][0] = 0;
-      st.cls_lcp[0][0] = 0;
-      int l0 = st.len[0];
-      atomicAdd((unsigned long long*)&st.node_diff[1], 1ULL);  // first sorted string
-      atomicAdd((unsigned long long*)&st.end_count[l0], 1ULL);
-      atomicAdd((unsigned long long*)&st.node_diff[l0 + 1], (unsigned long long)-1LL);
-      atomicAdd((unsigned long long*)&st.stats[3], 1ULL);
-      if (st.labels) st.labels[0] = 0;
-    } else {
-      st.mem_idx[0][i - 1] = i;
-      st.mem_cls[0][i - 1] = 0;
+// Length histogram, the root class (rep = prompt 0, the smallest index,
+// verified prefix 0; members 1 .. P-1), round 0's table clear and its member
+// count, in one pass over max(P, cap0).
+__global__ void init_kernel(DedupState st, int* kc, uint32_t cap0) {
+  const int P = st.P;
+  const uint32_t n = max((uint32_t)P, cap0);
+  if (blockIdx.x == 0 && threadIdx.x == 0) kc[0] = P - 1;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (i < cap0) {
+      st.a_keys[i] = kEmpty;
+      st.b_keys[i] = kEmpty;
+      st.b_rep[i] = INT32_MAX;
+      st.b_cnt[i] = 0;
+    }
+    if (i < (uint32_t)P) {
+      agg_add(st.len_count, st.len[i], 1);
+      if (i == 0) {
+        const int l0 = st.len[0];
+        st.cls_rep[0][0] = 0;
+        st.cls_lcp[0][0] = 0;
+        atomicAdd((unsigned long long*)&st.node_diff[1], 1ULL);  // first sorted string
+        atomicAdd((unsigned long long*)&st.end_count[l0], 1ULL);
+        atomicAdd((unsigned long long*)&st.node_diff[l0 + 1], (unsigned long long)-1LL);
+        atomicAdd((unsigned long long*)&st.stats[3], 1ULL);
+        if (st.labels) st.labels[0] = 0;
+      } else {
+        st.mem_idx[0][i - 1] = i;
+        st.mem_cls[0][i - 1] = 0;
+      }
     }
   }
 }
@@ -211,12 +220,6 @@ __device__ __forceinline__ void prep_phase(const DedupState& st, int K, int bid,
     st.b_rep[i] = INT32_MAX;
     st.b_cnt[i] = 0;
   }
-}
-
-__global__ void round_prep_kernel(DedupState st, const int* kcur, int* knext) {
-  const int K = *kcur;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *knext = 0;
-  if (K > 0) prep_phase(st, K, blockIdx.x, gridDim.x);
 }
 
 // Record member k's branch (x, t) against representative r of class c.
@@ -776,9 +779,13 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
     maxd = hs[1];
   }
   const int md = (int)hs[1];
-  st.node_diff = arena_alloc<int64_t>(ctx, md + 2);
-  st.end_count = arena_alloc<int64_t>(ctx, md + 2);
-  st.len_count = arena_alloc<int64_t>(ctx, md + 2);
+  // zero-initialised block: three histograms, the member counts, the barrier
+  const size_t zwords = 3 * ((size_t)md + 2) + 2;
+  int64_t* zero = arena_alloc<int64_t>(ctx, zwords);
+  if (!zero) return fail(RS_E_NOMEM, "arena exhausted (dedup)");
+  st.node_diff = zero;
+  st.end_count = zero + (md + 2);
+  st.len_count = zero + 2 * ((int64_t)md + 2);
   for (int b = 0; b < 2; ++b) {
     st.mem_idx[b] = arena_alloc<int32_t>(ctx, std::max(P, 1));
     st.mem_cls[b] = arena_alloc<int32_t>(ctx, std::max(P, 1));
@@ -790,23 +797,18 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
   st.b_keys = arena_alloc<uint64_t>(ctx, cap);
   st.b_rep = arena_alloc<int32_t>(ctx, cap);
   st.b_cnt = arena_alloc<int32_t>(ctx, cap);
-  int* kc = arena_alloc<int32_t>(ctx, 2);  // current / next member count
-  unsigned long long* bar = arena_alloc<unsigned long long>(ctx, 1);  // grid barrier
+  int* kc = reinterpret_cast<int*>(zero + zwords - 2);  // current / next member count
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(zero + zwords - 1);
   st.counter = kc;
   st.labels = want_labels ? arena_alloc<int32_t>(ctx, std::max(P, 1)) : nullptr;
   if (!kc || !bar || (want_labels && !st.labels)) return fail(RS_E_NOMEM, "arena exhausted (dedup)");
-  RS_CUDA_TRY(cudaMemsetAsync(st.node_diff, 0, 8 * (md + 2), ctx->stream));
-  RS_CUDA_TRY(cudaMemsetAsync(st.end_count, 0, 8 * (md + 2), ctx->stream));
-  RS_CUDA_TRY(cudaMemsetAsync(st.len_count, 0, 8 * (md + 2), ctx->stream));
-  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, 8 * ctx->num_sms));
-  RS_LAUNCH(ctx, "dedup_len_hist", len_hist_kernel, blocks, 256, 0, st);
-  RS_LAUNCH(ctx, "dedup_init", init_root_kernel, blocks, 256, 0, st);
+  RS_CUDA_TRY(cudaMemsetAsync(zero, 0, 8 * zwords, ctx->stream));
+  const uint32_t cap0 = pow2_at_least(2 * (int64_t)(P - 1) + 2);  // dev_cap(P - 1)
+  const int iblocks = (int)std::max<int64_t>(
+      1, std::min<int64_t>((std::max<int64_t>(P, cap0) + 255) / 256, 8 * ctx->num_sms));
+  RS_LAUNCH(ctx, "dedup_init", init_kernel, iblocks, 256, 0, st, kc, cap0);
   // Round 0's compare, then every later round inside one persistent launch
   // (refine_kernel): no host round trips until the tables are read back.
-  const int k0[2] = {P - 1, 0};
-  RS_TRY(h2d(ctx, kc, k0, 8));
-  RS_CUDA_TRY(cudaMemsetAsync(bar, 0, 8, ctx->stream));
-  const int cblocks = (int)std::max<int64_t>(1, std::min<int64_t>((cap + 255) / 256, 8 * ctx->num_sms));
   const int pblocks = (int)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, 8 * ctx->num_sms));
   // round-0 streaming kernel: representative + per-warp rings in smem
   const int len0 = (int)std::min<int64_t>(off01[1] - off01[0], cap_len);
@@ -818,7 +820,6 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
     RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compare_stream_kernel, kStreamWarps * 32, stream_smem));
     sblocks = std::max(1, per_sm) * ctx->num_sms;
   }
-  RS_LAUNCH(ctx, "dedup_prep", round_prep_kernel, cblocks, 256, 0, st, kc, kc + 1);
   if (stream_smem <= 200 * 1024) {
     RS_LAUNCH(ctx, "dedup_compare_r0", compare_stream_kernel, sblocks, kStreamWarps * 32,
               stream_smem, st, kc);
