@@ -36,6 +36,15 @@ namespace {
 constexpr uint64_t kEmpty = ~0ULL;
 constexpr uint64_t kEnd = 1ULL << 32;  // t value for "prompt ends at x"
 
+// One set of grouping tables: A keyed (class << 32 | x), B keyed
+// (slotA << 33 | t) with the branch's smallest member and its count.
+struct Tab {
+  uint64_t* a_keys;
+  uint64_t* b_keys;
+  int32_t* b_rep;
+  int32_t* b_cnt;
+};
+
 struct DedupState {
   int P;
   const int32_t* tok;
@@ -52,10 +61,7 @@ struct DedupState {
   int32_t* cls_rep[2];
   int32_t* cls_lcp[2];
   int32_t* m_slot;    // per member: B slot or -1
-  uint64_t* a_keys;
-  uint64_t* b_keys;
-  int32_t* b_rep;
-  int32_t* b_cnt;
+  Tab tab[2];         // grouping tables, alternating between rounds
   int32_t* counter;   // next member count
 };
 
@@ -128,10 +134,10 @@ __global__ void init_kernel(DedupState st, int* kc, uint32_t cap0) {
   if (blockIdx.x == 0 && threadIdx.x == 0) kc[0] = P - 1;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     if (i < cap0) {
-      st.a_keys[i] = kEmpty;
-      st.b_keys[i] = kEmpty;
-      st.b_rep[i] = INT32_MAX;
-      st.b_cnt[i] = 0;
+      st.tab[0].a_keys[i] = kEmpty;
+      st.tab[0].b_keys[i] = kEmpty;
+      st.tab[0].b_rep[i] = INT32_MAX;
+      st.tab[0].b_cnt[i] = 0;
     }
     if (i < (uint32_t)P) {
       agg_add(st.len_count, st.len[i], 1);
@@ -212,19 +218,18 @@ __device__ __forceinline__ uint32_t dev_cap(int K) {
 
 // Clears the grouping tables for this round (capacity from the device-side
 // member count) and the next round's counter.
-__device__ __forceinline__ void prep_phase(const DedupState& st, int K, int bid, int nb) {
-  const uint32_t cap = dev_cap(K);
+__device__ __forceinline__ void clear_phase(const Tab& t, uint32_t cap, int bid, int nb) {
   for (uint32_t i = bid * blockDim.x + threadIdx.x; i < cap; i += nb * blockDim.x) {
-    st.a_keys[i] = kEmpty;
-    st.b_keys[i] = kEmpty;
-    st.b_rep[i] = INT32_MAX;
-    st.b_cnt[i] = 0;
+    t.a_keys[i] = kEmpty;
+    t.b_keys[i] = kEmpty;
+    t.b_rep[i] = INT32_MAX;
+    t.b_cnt[i] = 0;
   }
 }
 
 // Record member k's branch (x, t) against representative r of class c.
-__device__ __forceinline__ void record_member(const DedupState& st, int64_t k, int m, int c, int r,
-                                              int x, int lm, int lr, uint32_t mask) {
+__device__ __forceinline__ void record_member(const DedupState& st, const Tab& tb, int64_t k, int m,
+                                              int c, int r, int x, int lm, int lr, uint32_t mask) {
   if (x == lm && x == lr) {  // exact duplicate of r: skipped (dedup.cpp:62)
     st.m_slot[k] = -1;
     if (st.labels) st.labels[m] = r;
@@ -232,10 +237,10 @@ __device__ __forceinline__ void record_member(const DedupState& st, int64_t k, i
   }
   const uint64_t t = x < lm ? (uint64_t)(uint32_t)st.tok[st.off[m] + x] : kEnd;
   bool created;
-  const uint32_t sa = table_insert(st.a_keys, mask, ((uint64_t)c << 32) | (uint32_t)x, &created);
-  const uint32_t sb = table_insert(st.b_keys, mask, ((uint64_t)sa << 33) | t, &created);
-  atomicMin(st.b_rep + sb, m);
-  atomicAdd(st.b_cnt + sb, 1);
+  const uint32_t sa = table_insert(tb.a_keys, mask, ((uint64_t)c << 32) | (uint32_t)x, &created);
+  const uint32_t sb = table_insert(tb.b_keys, mask, ((uint64_t)sa << 33) | t, &created);
+  atomicMin(tb.b_rep + sb, m);
+  atomicAdd(tb.b_cnt + sb, 1);
   st.m_slot[k] = (int32_t)sb;
 }
 
@@ -244,8 +249,9 @@ __device__ __forceinline__ void record_member(const DedupState& st, int64_t k, i
 // after the probe are handed, one at a time, to the whole warp (warp_lcp).
 constexpr int kProbe = 4;
 
-__device__ __forceinline__ void compare_phase(const DedupState& st, int cur, int K, int bid, int nb) {
-  const uint32_t mask = dev_cap(K) - 1;
+// tb: this round's tables, cleared over mask + 1 slots.
+__device__ __forceinline__ void compare_phase(const DedupState& st, const Tab& tb, uint32_t mask,
+                                              int cur, int K, int bid, int nb) {
   const int lane = threadIdx.x & 31;
   const int64_t W = (int64_t)nb * (blockDim.x >> 5);
   for (int64_t k0 = ((int64_t)bid * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; k0 < K;
@@ -266,7 +272,7 @@ __device__ __forceinline__ void compare_phase(const DedupState& st, int cur, int
       const int lim = min(n, x + kProbe);
       while (x < lim && __ldg(pm + x) == __ldg(pr + x)) ++x;
       slow = x == lim && lim < n;
-      if (!slow) record_member(st, k, m, c, r, x, lm, lr, mask);
+      if (!slow) record_member(st, tb, k, m, c, r, x, lm, lr, mask);
     }
     unsigned todo = __ballot_sync(0xffffffffu, slow);
     while (todo) {
@@ -277,7 +283,7 @@ __device__ __forceinline__ void compare_phase(const DedupState& st, int cur, int
       const int sx = __shfl_sync(0xffffffffu, x, src);
       const int sn = __shfl_sync(0xffffffffu, n, src);
       const int xx = warp_lcp(st.tok + st.off[sm], st.tok + st.off[sr], sx, sn);
-      if (lane == src) record_member(st, k, m, c, r, xx, lm, lr, mask);
+      if (lane == src) record_member(st, tb, k, m, c, r, xx, lm, lr, mask);
     }
   }
 }
@@ -285,7 +291,7 @@ __device__ __forceinline__ void compare_phase(const DedupState& st, int cur, int
 // Round 0 when the representative is too long for the streaming kernel.
 __global__ void __launch_bounds__(256) compare_kernel(DedupState st, int cur, const int* kcur) {
   const int K = *kcur;
-  if (K > 0) compare_phase(st, cur, K, blockIdx.x, gridDim.x);
+  if (K > 0) compare_phase(st, st.tab[0], dev_cap(K) - 1, cur, K, blockIdx.x, gridDim.x);
 }
 
 // Round 0 (one class, representative = prompt 0): the HBM-bound pass.
@@ -424,7 +430,8 @@ compare_stream_kernel(DedupState st, const int* kcur) {
       const int m = __shfl_sync(0xffffffffu, my_m, i);
       const int lm = __shfl_sync(0xffffffffu, my_lm, i);
       const int n = __shfl_sync(0xffffffffu, my_n, i);
-      if (lane == 0) record_member(st, kb0 + i, m, 0, 0, found == INT32_MAX ? n : found, lm, lr, mask);
+      if (lane == 0)
+        record_member(st, st.tab[0], kb0 + i, m, 0, 0, found == INT32_MAX ? n : found, lm, lr, mask);
     };
     for (int s0 = 0; s0 < kStreamStages - 1; ++s0) issue_next();
     for (;;) {
@@ -497,43 +504,36 @@ compare_stream_kernel(DedupState st, const int* kcur) {
 }
 
 // One thread per B slot: branch children, leaves, next classes.
-__device__ __forceinline__ void finalize_phase(const DedupState& st, int cur, int K, int bid, int nb) {
-  const uint32_t cap = dev_cap(K);
-  const int nxt = cur ^ 1;
-  for (uint32_t sb = bid * blockDim.x + threadIdx.x; sb < cap; sb += nb * blockDim.x) {
-    uint64_t key = st.b_keys[sb];
-    if (key == kEmpty) continue;
-    uint32_t sa = (uint32_t)(key >> 33);
-    uint64_t t = key & ((1ULL << 33) - 1);
-    int x = (int)(uint32_t)(st.a_keys[sa] & 0xffffffffULL);
-    agg_add(st.node_diff, x + 1, 1);  // one more child of the node at depth x
-    int rep = st.b_rep[sb];
-    int leaf_len = -1;
-    if (t == kEnd) {
-      leaf_len = x;
-    } else if (st.b_cnt[sb] == 1) {
-      leaf_len = st.len[rep];
-    } else {
-      st.cls_rep[nxt][sb] = rep;
-      st.cls_lcp[nxt][sb] = x + 1;
-      leaf_len = st.len[rep];  // the new class's representative is a leaf
-    }
-    agg_add(st.end_count, leaf_len, 1);
-    agg_add(st.node_diff, leaf_len + 1, -1);
-    agg_add(st.stats, 3, 1);
-  }
-}
-
-__device__ __forceinline__ void compact_phase(const DedupState& st, int cur, int K, int* knext,
-                                              int bid, int nb) {
+// Close round r (tables tb, members in buffer cur): every member that is
+// not an exact duplicate looks up its branch. The branch's representative
+// (its smallest member) accounts for it (dedup.cpp:58-78: one more child of
+// the node at depth x, one leaf of length x for END or len[rep] otherwise)
+// and, when the branch holds two or more members with a next token, opens
+// the class of round r + 1; every other member of such a branch is appended
+// to round r + 1's member list.
+__device__ __forceinline__ void compact_phase(const DedupState& st, const Tab& tb, int cur, int K,
+                                              int* knext, int bid, int nb) {
   const int nxt = cur ^ 1;
   for (int k = bid * blockDim.x + threadIdx.x; k < K; k += nb * blockDim.x) {
-    int sb = st.m_slot[k];
+    const int sb = st.m_slot[k];
     if (sb < 0) continue;
-    int m = st.mem_idx[cur][k];
-    int rep = st.b_rep[sb];
-    uint64_t t = st.b_keys[sb] & ((1ULL << 33) - 1);
-    bool leaf = t == kEnd || st.b_cnt[sb] == 1;
+    const int m = st.mem_idx[cur][k];
+    const int rep = tb.b_rep[sb];
+    const uint64_t key = tb.b_keys[sb];
+    const uint64_t t = key & ((1ULL << 33) - 1);
+    const bool leaf = t == kEnd || tb.b_cnt[sb] == 1;
+    if (m == rep) {
+      const int x = (int)(uint32_t)(tb.a_keys[(uint32_t)(key >> 33)] & 0xffffffffULL);
+      agg_add(st.node_diff, x + 1, 1);
+      const int leaf_len = t == kEnd ? x : st.len[rep];
+      if (!leaf) {
+        st.cls_rep[nxt][sb] = rep;
+        st.cls_lcp[nxt][sb] = x + 1;
+      }
+      agg_add(st.end_count, leaf_len, 1);
+      agg_add(st.node_diff, leaf_len + 1, -1);
+      agg_add(st.stats, 3, 1);
+    }
     if (leaf || m == rep) {
       if (st.labels) st.labels[m] = rep;
       continue;
@@ -574,9 +574,10 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned l
 // barriers instead of grid-wide ones: the last rounds hold a handful).
 constexpr int kSoloMembers = 1024;
 
-// Every round after round 0's compare, in one persistent launch: finalize and
-// compact round r, then (while members remain) clear the tables and compare
-// round r + 1. kc[0..1] alternate as the current / next member counts.
+// Every round after round 0's compare, in one persistent launch, two grid
+// barriers per round: close round r (compact_phase) while clearing the other
+// table set, then compare round r + 1 into it. kc[0..1] alternate as the
+// current / next member counts.
 __global__ void __launch_bounds__(256)
 refine_kernel(DedupState st, int* kc, unsigned long long* bar) {
   unsigned long long target = 0;
@@ -592,13 +593,16 @@ refine_kernel(DedupState st, int* kc, unsigned long long* bar) {
       grid_barrier(bar, &target);
     }
   };
+  int set = 0;  // round r's tables; round 0 (compared before this launch) used set 0
   for (;;) {
     const int K = *(volatile int*)(kc + cur);
     if (K <= 0) break;  // a single prompt: no members at all
     if (bid == 0 && threadIdx.x == 0) kc[cur ^ 1] = 0;
-    finalize_phase(st, cur, K, bid, nb);
-    sync();
-    compact_phase(st, cur, K, kc + (cur ^ 1), bid, nb);
+    // close round r; clear the other set for round r + 1, whose member count
+    // is at most K (its tables are sized by K)
+    compact_phase(st, st.tab[set], cur, K, kc + (cur ^ 1), bid, nb);
+    const uint32_t cap = dev_cap(K);
+    clear_phase(st.tab[set ^ 1], cap, bid, nb);
     sync();
     const int K2 = *(volatile int*)(kc + (cur ^ 1));
     if (K2 <= 0) break;
@@ -607,11 +611,10 @@ refine_kernel(DedupState st, int* kc, unsigned long long* bar) {
       solo = true;
       nb = 1;
     }
-    prep_phase(st, K2, bid, nb);
-    sync();
-    compare_phase(st, cur ^ 1, K2, bid, nb);
+    compare_phase(st, st.tab[set ^ 1], cap - 1, cur ^ 1, K2, bid, nb);
     sync();
     cur ^= 1;
+    set ^= 1;
   }
 }
 
@@ -747,8 +750,8 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
                         RefineTail* tail = nullptr) {
   const uint32_t cap = pow2_at_least(2 * (int64_t)P + 2);
   const size_t base_bytes = abytes(P, 4) + abytes(4, 8) + abytes(P, 4) * 4 +
-                            abytes(cap, 4) * 4 + abytes(P, 4) + abytes(cap, 8) * 2 +
-                            abytes(cap, 4) * 2 + abytes(2, 4) + abytes(1, 8) + abytes(P, 4);
+                            abytes(cap, 4) * 4 + abytes(P, 4) + 2 * (abytes(cap, 8) * 2 +
+                            abytes(cap, 4) * 2) + abytes(2, 4) + abytes(1, 8) + abytes(P, 4);
   // Tables are sized by the longest prompt; guess generously so the usual
   // case needs a single lengths pass and one host read.
   int64_t maxd = std::max<int64_t>(max_len_hint, 16384);
@@ -793,10 +796,12 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
     st.cls_lcp[b] = arena_alloc<int32_t>(ctx, cap);
   }
   st.m_slot = arena_alloc<int32_t>(ctx, std::max(P, 1));
-  st.a_keys = arena_alloc<uint64_t>(ctx, cap);
-  st.b_keys = arena_alloc<uint64_t>(ctx, cap);
-  st.b_rep = arena_alloc<int32_t>(ctx, cap);
-  st.b_cnt = arena_alloc<int32_t>(ctx, cap);
+  for (int b = 0; b < 2; ++b) {
+    st.tab[b].a_keys = arena_alloc<uint64_t>(ctx, cap);
+    st.tab[b].b_keys = arena_alloc<uint64_t>(ctx, cap);
+    st.tab[b].b_rep = arena_alloc<int32_t>(ctx, cap);
+    st.tab[b].b_cnt = arena_alloc<int32_t>(ctx, cap);
+  }
   int* kc = reinterpret_cast<int*>(zero + zwords - 2);  // current / next member count
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(zero + zwords - 1);
   st.counter = kc;
