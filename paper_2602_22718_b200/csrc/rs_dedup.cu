@@ -47,6 +47,8 @@ struct Tab {
 
 struct DedupState {
   int P;
+  int maxd;           // histogram depth bound (arrays hold maxd + 2); longer prompts clamp
+
   const int32_t* tok;
   const int64_t* off;
   int32_t* len;       // effective (possibly truncated) lengths
@@ -102,36 +104,18 @@ __device__ __forceinline__ uint32_t table_insert(uint64_t* keys, uint32_t mask,
   }
 }
 
-__global__ void lengths_kernel(DedupState st, int32_t cap_len, int strict, int* flags) {
-  long long mn = INT64_MAX, mx = 0;
-  unsigned long long sum = 0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < st.P; i += gridDim.x * blockDim.x) {
-    int64_t raw = st.off[i + 1] - st.off[i];
-    if (strict && raw < 1) atomicOr(flags, kFlagEmptyPrompt);
-    int32_t l = (int32_t)(raw < cap_len ? raw : cap_len);
-    if (l < 0) l = 0;
-    st.len[i] = l;
-    mn = l < mn ? l : mn;
-    mx = l > mx ? l : mx;
-    sum += (unsigned long long)l;
-  }
-  mn = warp_min(mn);
-  mx = warp_max(mx);
-  sum = warp_sum(sum);
-  if ((threadIdx.x & 31) == 0) {
-    atomicMin((long long*)&st.stats[0], mn);
-    atomicMax((long long*)&st.stats[1], mx);
-    atomicAdd((unsigned long long*)&st.stats[2], sum);
-  }
-}
-
-// Length histogram, the root class (rep = prompt 0, the smallest index,
-// verified prefix 0; members 1 .. P-1), round 0's table clear and its member
-// count, in one pass over max(P, cap0).
-__global__ void init_kernel(DedupState st, int* kc, uint32_t cap0) {
+// The lengths (capped at cap_len; min / max / total into stats), the length
+// histogram, the root class (rep = prompt 0, the smallest index, verified
+// prefix 0; members 1 .. P-1), round 0's table clear and its member count,
+// in one pass over max(P, cap0). Histogram indices clamp at maxd + 1: a
+// longer prompt makes the host redo the refinement with larger arrays.
+__global__ void init_kernel(DedupState st, int32_t cap_len, int strict, int* flags, int* kc,
+                            uint32_t cap0) {
   const int P = st.P;
   const uint32_t n = max((uint32_t)P, cap0);
   if (blockIdx.x == 0 && threadIdx.x == 0) kc[0] = P - 1;
+  long long mn = INT64_MAX, mx = 0;
+  unsigned long long sum = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     if (i < cap0) {
       st.tab[0].a_keys[i] = kEmpty;
@@ -140,14 +124,22 @@ __global__ void init_kernel(DedupState st, int* kc, uint32_t cap0) {
       st.tab[0].b_cnt[i] = 0;
     }
     if (i < (uint32_t)P) {
-      agg_add(st.len_count, st.len[i], 1);
+      const int64_t raw = st.off[i + 1] - st.off[i];
+      if (strict && raw < 1) atomicOr(flags, kFlagEmptyPrompt);
+      int32_t l = (int32_t)(raw < cap_len ? raw : cap_len);
+      if (l < 0) l = 0;
+      st.len[i] = l;
+      mn = l < mn ? l : mn;
+      mx = l > mx ? l : mx;
+      sum += (unsigned long long)l;
+      const int lc = min(l, st.maxd + 1);
+      agg_add(st.len_count, lc, 1);
       if (i == 0) {
-        const int l0 = st.len[0];
         st.cls_rep[0][0] = 0;
         st.cls_lcp[0][0] = 0;
         atomicAdd((unsigned long long*)&st.node_diff[1], 1ULL);  // first sorted string
-        atomicAdd((unsigned long long*)&st.end_count[l0], 1ULL);
-        atomicAdd((unsigned long long*)&st.node_diff[l0 + 1], (unsigned long long)-1LL);
+        atomicAdd((unsigned long long*)&st.end_count[lc], 1ULL);
+        atomicAdd((unsigned long long*)&st.node_diff[min(l + 1, st.maxd + 1)], (unsigned long long)-1LL);
         atomicAdd((unsigned long long*)&st.stats[3], 1ULL);
         if (st.labels) st.labels[0] = 0;
       } else {
@@ -155,6 +147,14 @@ __global__ void init_kernel(DedupState st, int* kc, uint32_t cap0) {
         st.mem_cls[0][i - 1] = 0;
       }
     }
+  }
+  mn = warp_min(mn);
+  mx = warp_max(mx);
+  sum = warp_sum(sum);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin((long long*)&st.stats[0], mn);
+    atomicMax((long long*)&st.stats[1], mx);
+    atomicAdd((unsigned long long*)&st.stats[2], sum);
   }
 }
 
@@ -288,12 +288,6 @@ __device__ __forceinline__ void compare_phase(const DedupState& st, const Tab& t
   }
 }
 
-// Round 0 when the representative is too long for the streaming kernel.
-__global__ void __launch_bounds__(256) compare_kernel(DedupState st, int cur, const int* kcur) {
-  const int K = *kcur;
-  if (K > 0) compare_phase(st, st.tab[0], dev_cap(K) - 1, cur, K, blockIdx.x, gridDim.x);
-}
-
 // Round 0 (one class, representative = prompt 0): the HBM-bound pass.
 // The representative is staged once per CTA in shared memory; every warp
 // streams its member through a 4-stage ring of 2 KB windows filled by bulk
@@ -304,6 +298,11 @@ __global__ void __launch_bounds__(256) compare_kernel(DedupState st, int cur, co
 constexpr int kStreamStages = 4;
 constexpr int kStageTok = 512;
 constexpr int kStreamWarps = 8;
+// The representative's first kRepSmemTok tokens are staged in shared memory
+// (10 KB: ring + staging still fit three CTAs per SM); the rest, if any, is
+// read through L1.
+constexpr int kRepSmemTok = 2560;
+constexpr int kStreamSmem = (int)sizeof(int32_t) * (kRepSmemTok + kStageTok * kStreamStages * kStreamWarps);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -348,12 +347,19 @@ compare_stream_kernel(DedupState st, const int* kcur) {
   const uint32_t mask = dev_cap(K) - 1;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int lr = st.len[0];
-  int32_t* rep = sm;  // [lr padded to 4]
-  int32_t* ring = sm + ((lr + 3) & ~3) + kStageTok * kStreamStages * wid;
+  int32_t* rep_s = sm;  // representative tokens [0, kRepSmemTok)
+  int32_t* ring = sm + kRepSmemTok + kStageTok * kStreamStages * wid;
   int2* meta = slot_meta[wid];
   const int32_t* pr = st.tok + st.off[0];
   const int32_t* tok_end = st.tok + st.off[st.P];  // bulk copies must not read past it
-  for (int i = threadIdx.x; i < lr; i += blockDim.x) rep[i] = pr[i];
+  for (int i = threadIdx.x; i < min(lr, kRepSmemTok); i += blockDim.x) rep_s[i] = pr[i];
+  // representative token / 16-byte chunk at p (chunks: p % 4 == 0)
+  const bool rep_aligned = (((uintptr_t)pr) & 15) == 0;
+  auto rep_at = [&](int p) { return p < kRepSmemTok ? rep_s[p] : __ldg(pr + p); };
+  auto rep4_at = [&](int p) {
+    return p < kRepSmemTok ? *reinterpret_cast<const int4*>(rep_s + p)
+                           : __ldg(reinterpret_cast<const int4*>(pr + p));
+  };
   uint64_t* bars = slot_bar[wid];
   if (lane == 0)
     for (int q = 0; q < kStreamStages; ++q) mbar_init(&bars[q], 1);
@@ -455,14 +461,14 @@ compare_stream_kernel(DedupState st, const int* kcur) {
       // per int4: a 4-bit mismatch mask over the positions in [0, n); the
       // lane keeps its first mismatch (q ascending = position ascending)
       int best = INT32_MAX;
-      if (sh == 0) {  // member and representative chunks are both 16B aligned
+      if (sh == 0 && rep_aligned) {  // member and representative chunks both 16B aligned
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int j = lane + 32 * q;
           const int p = mw.y * kStageTok + 4 * j;
           if (best == INT32_MAX && p < n) {
             const int4 a4 = *reinterpret_cast<const int4*>(buf + 4 * j);
-            const int4 b4 = *reinterpret_cast<const int4*>(rep + p);
+            const int4 b4 = rep4_at(p);
             uint32_t m = (uint32_t)(a4.x != b4.x) | ((uint32_t)(a4.y != b4.y) << 1) |
                          ((uint32_t)(a4.z != b4.z) << 2) | ((uint32_t)(a4.w != b4.w) << 3);
             if (n - p < 4) m &= (1u << (n - p)) - 1;
@@ -481,7 +487,7 @@ compare_stream_kernel(DedupState st, const int* kcur) {
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
               const int pos = p + t;
-              if (pos >= 0 && pos < n) m |= (uint32_t)(e[t] != rep[pos]) << t;
+              if (pos >= 0 && pos < n) m |= (uint32_t)(e[t] != rep_at(pos)) << t;
             }
             if (m) best = p + __ffs(m) - 1;
           }
@@ -524,14 +530,14 @@ __device__ __forceinline__ void compact_phase(const DedupState& st, const Tab& t
     const bool leaf = t == kEnd || tb.b_cnt[sb] == 1;
     if (m == rep) {
       const int x = (int)(uint32_t)(tb.a_keys[(uint32_t)(key >> 33)] & 0xffffffffULL);
-      agg_add(st.node_diff, x + 1, 1);
-      const int leaf_len = t == kEnd ? x : st.len[rep];
+      agg_add(st.node_diff, min(x + 1, st.maxd + 1), 1);
+      const int leaf_len = min(t == kEnd ? x : st.len[rep], st.maxd + 1);
       if (!leaf) {
         st.cls_rep[nxt][sb] = rep;
         st.cls_lcp[nxt][sb] = x + 1;
       }
       agg_add(st.end_count, leaf_len, 1);
-      agg_add(st.node_diff, leaf_len + 1, -1);
+      agg_add(st.node_diff, min(leaf_len + 1, st.maxd + 1), -1);
       agg_add(st.stats, 3, 1);
     }
     if (leaf || m == rep) {
@@ -626,13 +632,19 @@ refine_kernel(DedupState st, int* kc, unsigned long long* bar) {
 //   lcf[d]   = total(len_count_m) - incl(len_count_m)[d]
 //   ltf[d]   = total(len_count_m * i) - incl(len_count_m * i)[d]
 // Each thread scans kTabIPT consecutive depths; the five thread totals go
-// through one CTA scan per chunk of kTabT * kTabIPT depths.
+// through one CTA scan per chunk of kTabT * kTabIPT depths. maxd < 0: the
+// longest prompt from stats; the tables are written (stride maxd + 2) only
+// if maxd <= cap_md. stats_out (nullable) receives the four stats.
 constexpr int kTabT = 512;
 constexpr int kTabIPT = 4;
 constexpr int kTabQ = 5;
 
-__global__ void __launch_bounds__(kTabT) tables_kernel(DedupState st, int maxd, int64_t* out) {
+__global__ void __launch_bounds__(kTabT)
+tables_kernel(DedupState st, int maxd, int cap_md, int64_t* out, int64_t* stats_out) {
   __shared__ int64_t ws[kTabQ][32];
+  if (maxd < 0) maxd = (int)st.stats[1];
+  if (stats_out && threadIdx.x < 4) stats_out[threadIdx.x] = st.stats[threadIdx.x];
+  if (maxd > cap_md) return;
   const int n = maxd + 2;  // depths 0 .. maxd + 1
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int64_t* const tab[kTabQ] = {out, out + n, out + 2 * (int64_t)n, out + 3 * (int64_t)n,
@@ -731,18 +743,33 @@ static int launch_refine(rs_ctx* ctx, DedupState st, int* kc, unsigned long long
 
 // Runs the refinement on device-resident CSR. cap_len = INT32_MAX for the
 // full index. Fills node_diff/end_count/len_count/stats (and labels if
-// non-null). Two host synchronisations: after the lengths pass (sizes) and
-// after the persistent refinement.
-// tail (nullable): enqueued after the refinement, before that final
-// synchronisation, so work that consumes the final state (the tables and
-// their read-back) shares it.
-// Pinned staging: the first kPinnedHead bytes hold the refinement's own
-// read-backs, a tail's follow.
+// non-null). Everything is queued without a host round trip and
+// synchronised once at the end. The histograms are sized by a bound (the
+// hint, at least 16,384, at most cap_len); a longer prompt is seen in the
+// final stats and the refinement reruns once with the exact size.
+// tail (nullable): enqueued after the refinement, before the final
+// synchronisation; it writes the four stats to pinned + kStatsOff (else
+// they are copied there) and its own output behind kPinnedHead.
 constexpr size_t kPinnedHead = 64;
+constexpr int kStatsOff = 4;  // int64 index of the read-back stats in pinned
 struct RefineTail {
-  virtual int enqueue(rs_ctx* ctx, const DedupState& st, int max_len) = 0;
+  virtual size_t pinned_bytes(int cap_md) = 0;
+  virtual int enqueue(rs_ctx* ctx, const DedupState& st, int cap_md) = 0;
   virtual void finish(rs_ctx* ctx) = 0;  // after the final synchronisation
 };
+
+static int stream_kernel_setup(int* blocks_per_sm) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    RS_CUDA_TRY(cudaFuncSetAttribute(compare_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kStreamSmem));
+    RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compare_stream_kernel,
+                                                              kStreamWarps * 32, kStreamSmem));
+    per_sm = std::max(1, per_sm);
+  }
+  *blocks_per_sm = per_sm;
+  return RS_OK;
+}
 
 static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off, int P,
                         int32_t cap_len, int strict, bool want_labels, int32_t max_len_hint,
@@ -751,93 +778,75 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
   const uint32_t cap = pow2_at_least(2 * (int64_t)P + 2);
   const size_t base_bytes = abytes(P, 4) + abytes(4, 8) + abytes(P, 4) * 4 +
                             abytes(cap, 4) * 4 + abytes(P, 4) + 2 * (abytes(cap, 8) * 2 +
-                            abytes(cap, 4) * 2) + abytes(2, 4) + abytes(1, 8) + abytes(P, 4);
-  // Tables are sized by the longest prompt; guess generously so the usual
-  // case needs a single lengths pass and one host read.
+                            abytes(cap, 4) * 2) + abytes(P, 4);
   int64_t maxd = std::max<int64_t>(max_len_hint, 16384);
+  maxd = std::max<int64_t>(1, std::min<int64_t>(maxd, cap_len));
+  int per_sm = 1;
+  RS_TRY(stream_kernel_setup(&per_sm));
   DedupState st{};
   int64_t hs[4];
-  int64_t off01[2];
   for (int attempt = 0; attempt < 2; ++attempt) {
-    size_t need = base_bytes + 8 * abytes(maxd + 2, 8) + (1 << 16);
-    RS_TRY(arena_reserve(ctx, need));
+    const int md = (int)maxd;
+    const size_t zwords = 3 * ((size_t)md + 2) + 2;  // three histograms, member counts, barrier
+    RS_TRY(arena_reserve(ctx, base_bytes + 8 * abytes(zwords, 8) + (1 << 16)));
+    RS_TRY(pinned_reserve(ctx, kPinnedHead + (tail ? tail->pinned_bytes(md) : 0)));
+    st = DedupState{};
     st.P = P;
+    st.maxd = md;
     st.tok = d_tok;
     st.off = d_off;
     st.len = arena_alloc<int32_t>(ctx, P);
     st.stats = arena_alloc<int64_t>(ctx, 4);
+    int64_t* zero = arena_alloc<int64_t>(ctx, zwords);
+    if (!zero) return fail(RS_E_NOMEM, "arena exhausted (dedup)");
+    st.node_diff = zero;
+    st.end_count = zero + (md + 2);
+    st.len_count = zero + 2 * ((int64_t)md + 2);
+    for (int b = 0; b < 2; ++b) {
+      st.mem_idx[b] = arena_alloc<int32_t>(ctx, std::max(P, 1));
+      st.mem_cls[b] = arena_alloc<int32_t>(ctx, std::max(P, 1));
+      st.cls_rep[b] = arena_alloc<int32_t>(ctx, cap);
+      st.cls_lcp[b] = arena_alloc<int32_t>(ctx, cap);
+    }
+    st.m_slot = arena_alloc<int32_t>(ctx, std::max(P, 1));
+    for (int b = 0; b < 2; ++b) {
+      st.tab[b].a_keys = arena_alloc<uint64_t>(ctx, cap);
+      st.tab[b].b_keys = arena_alloc<uint64_t>(ctx, cap);
+      st.tab[b].b_rep = arena_alloc<int32_t>(ctx, cap);
+      st.tab[b].b_cnt = arena_alloc<int32_t>(ctx, cap);
+    }
+    int* kc = reinterpret_cast<int*>(zero + zwords - 2);  // current / next member count
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(zero + zwords - 1);
+    st.counter = kc;
+    st.labels = want_labels ? arena_alloc<int32_t>(ctx, std::max(P, 1)) : nullptr;
+    if (!st.tab[1].b_cnt || (want_labels && !st.labels)) return fail(RS_E_NOMEM, "arena exhausted (dedup)");
     RS_TRY(clear_flags(ctx));
-    int64_t init[4] = {INT64_MAX, 0, 0, 0};
-    RS_TRY(h2d(ctx, st.stats, init, sizeof(init)));
-    int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, 8 * ctx->num_sms));
-    RS_LAUNCH(ctx, "dedup_lengths", lengths_kernel, blocks, 256, 0, st, cap_len, strict, ctx->d_flags);
-    RS_TRY(pinned_reserve(ctx, kPinnedHead));  // small read-backs stay asynchronous
     int64_t* pin = reinterpret_cast<int64_t*>(ctx->pinned);
-    RS_CUDA_TRY(cudaMemcpyAsync(pin, st.stats, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
-    RS_CUDA_TRY(cudaMemcpyAsync(pin + 4, d_off, sizeof(off01), cudaMemcpyDeviceToHost, ctx->stream));
+    pin[0] = INT64_MAX;  // stats = {min, max, total, leaves}, uploaded from pinned memory
+    pin[1] = pin[2] = pin[3] = 0;
+    RS_CUDA_TRY(cudaMemcpyAsync(st.stats, pin, 4 * 8, cudaMemcpyHostToDevice, ctx->stream));
+    RS_CUDA_TRY(cudaMemsetAsync(zero, 0, 8 * zwords, ctx->stream));
+    const uint32_t cap0 = pow2_at_least(2 * (int64_t)(P - 1) + 2);  // dev_cap(P - 1)
+    const int iblocks = (int)std::max<int64_t>(
+        1, std::min<int64_t>((std::max<int64_t>(P, cap0) + 255) / 256, 8 * ctx->num_sms));
+    RS_LAUNCH(ctx, "dedup_init", init_kernel, iblocks, 256, 0, st, cap_len, strict, ctx->d_flags,
+              kc, cap0);
+    // round 0 (every member against prompt 0) streams the batch; every later
+    // round runs inside one persistent launch (refine_kernel)
+    RS_LAUNCH(ctx, "dedup_compare_r0", compare_stream_kernel, per_sm * ctx->num_sms,
+              kStreamWarps * 32, kStreamSmem, st, kc);
+    RS_TRY(launch_refine(ctx, st, kc, bar));
+    if (tail) {
+      RS_TRY(tail->enqueue(ctx, st, md));
+    } else {
+      RS_CUDA_TRY(cudaMemcpyAsync(pin + kStatsOff, st.stats, 4 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    }
     RS_TRY(sync_and_check(ctx));
-    std::memcpy(hs, pin, sizeof(hs));
-    std::memcpy(off01, pin + 4, sizeof(off01));
+    std::memcpy(hs, pin + kStatsOff, sizeof(hs));
     if (hs[1] <= maxd) break;
-    maxd = hs[1];
+    maxd = hs[1];  // a prompt longer than the bound: rerun with exact arrays
   }
-  const int md = (int)hs[1];
-  // zero-initialised block: three histograms, the member counts, the barrier
-  const size_t zwords = 3 * ((size_t)md + 2) + 2;
-  int64_t* zero = arena_alloc<int64_t>(ctx, zwords);
-  if (!zero) return fail(RS_E_NOMEM, "arena exhausted (dedup)");
-  st.node_diff = zero;
-  st.end_count = zero + (md + 2);
-  st.len_count = zero + 2 * ((int64_t)md + 2);
-  for (int b = 0; b < 2; ++b) {
-    st.mem_idx[b] = arena_alloc<int32_t>(ctx, std::max(P, 1));
-    st.mem_cls[b] = arena_alloc<int32_t>(ctx, std::max(P, 1));
-    st.cls_rep[b] = arena_alloc<int32_t>(ctx, cap);
-    st.cls_lcp[b] = arena_alloc<int32_t>(ctx, cap);
-  }
-  st.m_slot = arena_alloc<int32_t>(ctx, std::max(P, 1));
-  for (int b = 0; b < 2; ++b) {
-    st.tab[b].a_keys = arena_alloc<uint64_t>(ctx, cap);
-    st.tab[b].b_keys = arena_alloc<uint64_t>(ctx, cap);
-    st.tab[b].b_rep = arena_alloc<int32_t>(ctx, cap);
-    st.tab[b].b_cnt = arena_alloc<int32_t>(ctx, cap);
-  }
-  int* kc = reinterpret_cast<int*>(zero + zwords - 2);  // current / next member count
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(zero + zwords - 1);
-  st.counter = kc;
-  st.labels = want_labels ? arena_alloc<int32_t>(ctx, std::max(P, 1)) : nullptr;
-  if (!kc || !bar || (want_labels && !st.labels)) return fail(RS_E_NOMEM, "arena exhausted (dedup)");
-  RS_CUDA_TRY(cudaMemsetAsync(zero, 0, 8 * zwords, ctx->stream));
-  const uint32_t cap0 = pow2_at_least(2 * (int64_t)(P - 1) + 2);  // dev_cap(P - 1)
-  const int iblocks = (int)std::max<int64_t>(
-      1, std::min<int64_t>((std::max<int64_t>(P, cap0) + 255) / 256, 8 * ctx->num_sms));
-  RS_LAUNCH(ctx, "dedup_init", init_kernel, iblocks, 256, 0, st, kc, cap0);
-  // Round 0's compare, then every later round inside one persistent launch
-  // (refine_kernel): no host round trips until the tables are read back.
-  const int pblocks = (int)std::max<int64_t>(1, std::min<int64_t>((P + 255) / 256, 8 * ctx->num_sms));
-  // round-0 streaming kernel: representative + per-warp rings in smem
-  const int len0 = (int)std::min<int64_t>(off01[1] - off01[0], cap_len);
-  const int stream_smem = (int)(sizeof(int32_t) * (((len0 + 3) & ~3) + kStageTok * kStreamStages * kStreamWarps));
-  int sblocks = 1;
-  if (stream_smem <= 200 * 1024) {
-    RS_CUDA_TRY(cudaFuncSetAttribute(compare_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, stream_smem));
-    int per_sm = 1;
-    RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compare_stream_kernel, kStreamWarps * 32, stream_smem));
-    sblocks = std::max(1, per_sm) * ctx->num_sms;
-  }
-  if (stream_smem <= 200 * 1024) {
-    RS_LAUNCH(ctx, "dedup_compare_r0", compare_stream_kernel, sblocks, kStreamWarps * 32,
-              stream_smem, st, kc);
-  } else {
-    RS_LAUNCH(ctx, "dedup_compare_r0", compare_kernel, pblocks, 256, 0, st, 0, kc);
-  }
-  RS_TRY(launch_refine(ctx, st, kc, bar));
-  // read-backs through pinned memory: [stats | tail], one synchronisation
-  if (tail) RS_TRY(tail->enqueue(ctx, st, md));
-  if (h_stats)
-    RS_CUDA_TRY(cudaMemcpyAsync(ctx->pinned, st.stats, 4 * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  if (h_stats) std::memcpy(h_stats, ctx->pinned, 4 * 8);
+  if (h_stats) std::memcpy(h_stats, hs, sizeof(hs));
   if (tail) tail->finish(ctx);
   if (h_labels && P > 0) RS_TRY(d2h(ctx, h_labels, st.labels, 4ull * P));
   *out_state = st;
@@ -860,24 +869,20 @@ static int build_index_device(rs_ctx* ctx, const int32_t* d_tok, const int64_t* 
   // The tables kernel and its read-back ride on the refinement's final
   // synchronisation (max_len is known after the lengths pass).
   struct Tables : RefineTail {
-    int64_t* d = nullptr;
     std::vector<int64_t> h;
     int md = -1;
-    int enqueue(rs_ctx* c, const DedupState& st, int max_len) override {
-      if (md < 0) {
-        md = max_len;
-        d = arena_alloc<int64_t>(c, 5ull * (md + 2));
-        if (!d) return fail(RS_E_NOMEM, "arena exhausted (tables)");
-        h.resize(5ull * (md + 2));
-      }
-      RS_LAUNCH(c, "dedup_tables", tables_kernel, 1, kTabT, 0, st, md, d);
-      RS_TRY(pinned_reserve(c, kPinnedHead + 8 * h.size()));
-      RS_CUDA_TRY(cudaMemcpyAsync(c->pinned + kPinnedHead, d, 8 * h.size(), cudaMemcpyDeviceToHost,
-                                  c->stream));
+    size_t pinned_bytes(int cap_md) override { return 5 * 8 * ((size_t)cap_md + 2); }
+    int enqueue(rs_ctx* c, const DedupState& st, int cap_md) override {
+      // stats and tables go straight into mapped pinned host memory
+      int64_t* pin = reinterpret_cast<int64_t*>(c->pinned);
+      RS_LAUNCH(c, "dedup_tables", tables_kernel, 1, kTabT, 0, st, -1, cap_md,
+                reinterpret_cast<int64_t*>(c->pinned + kPinnedHead), pin + kStatsOff);
       return RS_OK;
     }
     void finish(rs_ctx* c) override {
-      std::memcpy(h.data(), c->pinned + kPinnedHead, 8 * h.size());
+      md = (int)reinterpret_cast<int64_t*>(c->pinned)[kStatsOff + 1];
+      const int64_t* t = reinterpret_cast<const int64_t*>(c->pinned + kPinnedHead);
+      h.assign(t, t + 5 * ((size_t)md + 2));
     }
   } tab;
   DedupState st;
@@ -1021,7 +1026,8 @@ int rs_prefix_index_build_device_async(rs_ctx* ctx, const int32_t* d_tokens,
   RS_TRY(dedup_refine(ctx, d_tokens, d_offsets, batch, INT32_MAX, 1, false, max_len_cap, &st,
                       stats, nullptr));
   if (stats[1] > max_len_cap) return fail(RS_E_ARG, "max_len_cap below the longest prompt");
-  RS_LAUNCH(ctx, "dedup_tables", tables_kernel, 1, kTabT, 0, st, max_len_cap, d_tables);
+  RS_LAUNCH(ctx, "dedup_tables", tables_kernel, 1, kTabT, 0, st, max_len_cap, max_len_cap, d_tables,
+            nullptr);
   int64_t info[5] = {batch, stats[0], stats[1], stats[2], 0};
   RS_TRY(h2d(ctx, d_info, info, sizeof(info)));
   return RS_OK;

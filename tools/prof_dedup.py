@@ -17,7 +17,7 @@ d_tok = torch.from_numpy(tok).cuda()
 d_off = torch.from_numpy(off).cuda()
 lib = ctx.lib
 h = C.c_void_p()
-names = ["dedup_lengths", "dedup_init", "dedup_compare_r0", "dedup_refine", "dedup_compare",
+names = ["dedup_init", "dedup_compare_r0", "dedup_refine", "dedup_compare",
          "dedup_finalize", "dedup_compact", "dedup_tables"]
 for rep in range(4):
     ctx.enable_kernel_timing(True)
