@@ -25,6 +25,7 @@
 // unique_prefix_count_among (dedup.cpp:163-183).
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "rs_internal.cuh"
@@ -866,11 +867,10 @@ struct rs_prefix_index {
 static int build_index_device(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
                               int32_t P, rs_prefix_index** out) {
   if (P <= 0) return fail(RS_E_VALIDATION, "prefix index needs a non-empty batch");
-  // The tables kernel and its read-back ride on the refinement's final
-  // synchronisation (max_len is known after the lengths pass).
+  // The tables kernel writes the stats and tables into mapped pinned memory
+  // before the refinement's single synchronisation.
   struct Tables : RefineTail {
-    std::vector<int64_t> h;
-    int md = -1;
+    rs_prefix_index* idx = nullptr;  // filled from pinned memory by finish()
     size_t pinned_bytes(int cap_md) override { return 5 * 8 * ((size_t)cap_md + 2); }
     int enqueue(rs_ctx* c, const DedupState& st, int cap_md) override {
       // stats and tables go straight into mapped pinned host memory
@@ -880,28 +880,27 @@ static int build_index_device(rs_ctx* ctx, const int32_t* d_tok, const int64_t* 
       return RS_OK;
     }
     void finish(rs_ctx* c) override {
-      md = (int)reinterpret_cast<int64_t*>(c->pinned)[kStatsOff + 1];
+      const int64_t* stats = reinterpret_cast<const int64_t*>(c->pinned) + kStatsOff;
+      const int md = (int)stats[1];
+      const size_t n = (size_t)md + 2;
       const int64_t* t = reinterpret_cast<const int64_t*>(c->pinned + kPinnedHead);
-      h.assign(t, t + 5 * ((size_t)md + 2));
+      idx->min_len = (int32_t)stats[0];
+      idx->max_len = md;
+      idx->total = stats[2];
+      idx->nodes.assign(t, t + md + 1);
+      idx->scb.assign(t + n, t + 2 * n);
+      idx->stb.assign(t + 2 * n, t + 3 * n);
+      idx->lcf.assign(t + 3 * n, t + 4 * n);
+      idx->ltf.assign(t + 4 * n, t + 5 * n);
     }
   } tab;
+  std::unique_ptr<rs_prefix_index> idx(new rs_prefix_index());
+  idx->batch = P;
+  tab.idx = idx.get();
   DedupState st;
   int64_t stats[4];
   RS_TRY(dedup_refine(ctx, d_tok, d_off, P, INT32_MAX, 1, false, 0, &st, stats, nullptr, &tab));
-  RS_TRY(sync_and_check(ctx));
-  const int md = (int)stats[1];
-  std::vector<int64_t>& h = tab.h;
-  auto* idx = new rs_prefix_index();
-  idx->batch = P;
-  idx->min_len = (int32_t)stats[0];
-  idx->max_len = md;
-  idx->total = stats[2];
-  idx->nodes.assign(h.begin(), h.begin() + md + 1);
-  idx->scb.assign(h.begin() + (md + 2), h.begin() + 2 * (md + 2));
-  idx->stb.assign(h.begin() + 2 * (md + 2), h.begin() + 3 * (md + 2));
-  idx->lcf.assign(h.begin() + 3 * (md + 2), h.begin() + 4 * (md + 2));
-  idx->ltf.assign(h.begin() + 4 * (md + 2), h.begin() + 5 * (md + 2));
-  *out = idx;
+  *out = idx.release();
   return RS_OK;
 }
 
