@@ -60,11 +60,8 @@ struct DedupState {
   int32_t* labels;    // optional
   // refinement
   int32_t* mem_idx[2];
-  int32_t* mem_cls[2];
-  int32_t* cls_rep[2];
-  int32_t* cls_lcp[2];
-  int32_t* m_slot;    // per member: B slot or -1
-  Tab tab[2];         // grouping tables, alternating between rounds
+  int32_t* m_slot[2];  // per member of a round: its B slot, or -1 (exact duplicate)
+  Tab tab[3];         // grouping tables, rotating over rounds (fill, read, clear)
   int32_t* counter;   // next member count
 };
 
@@ -118,11 +115,14 @@ __global__ void init_kernel(DedupState st, int32_t cap_len, int strict, int* fla
   long long mn = INT64_MAX, mx = 0;
   unsigned long long sum = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    if (i < cap0) {
-      st.tab[0].a_keys[i] = kEmpty;
-      st.tab[0].b_keys[i] = kEmpty;
-      st.tab[0].b_rep[i] = INT32_MAX;
-      st.tab[0].b_cnt[i] = 0;
+    if (i < cap0) {  // rounds 0 and 1 use sets 0 and 1
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        st.tab[b].a_keys[i] = kEmpty;
+        st.tab[b].b_keys[i] = kEmpty;
+        st.tab[b].b_rep[i] = INT32_MAX;
+        st.tab[b].b_cnt[i] = 0;
+      }
     }
     if (i < (uint32_t)P) {
       const int64_t raw = st.off[i + 1] - st.off[i];
@@ -136,8 +136,6 @@ __global__ void init_kernel(DedupState st, int32_t cap_len, int strict, int* fla
       const int lc = min(l, st.maxd + 1);
       agg_add(st.len_count, lc, 1);
       if (i == 0) {
-        st.cls_rep[0][0] = 0;
-        st.cls_lcp[0][0] = 0;
         atomicAdd((unsigned long long*)&st.node_diff[1], 1ULL);  // first sorted string
         atomicAdd((unsigned long long*)&st.end_count[lc], 1ULL);
         atomicAdd((unsigned long long*)&st.node_diff[min(l + 1, st.maxd + 1)], (unsigned long long)-1LL);
@@ -145,7 +143,6 @@ __global__ void init_kernel(DedupState st, int32_t cap_len, int strict, int* fla
         if (st.labels) st.labels[0] = 0;
       } else {
         st.mem_idx[0][i - 1] = i;
-        st.mem_cls[0][i - 1] = 0;
       }
     }
   }
@@ -229,10 +226,11 @@ __device__ __forceinline__ void clear_phase(const Tab& t, uint32_t cap, int bid,
 }
 
 // Record member k's branch (x, t) against representative r of class c.
-__device__ __forceinline__ void record_member(const DedupState& st, const Tab& tb, int64_t k, int m,
-                                              int c, int r, int x, int lm, int lr, uint32_t mask) {
+__device__ __forceinline__ void record_member(const DedupState& st, const Tab& tb, int32_t* mslot,
+                                              int64_t k, int m, int c, int r, int x, int lm, int lr,
+                                              uint32_t mask) {
   if (x == lm && x == lr) {  // exact duplicate of r: skipped (dedup.cpp:62)
-    st.m_slot[k] = -1;
+    mslot[k] = -1;
     if (st.labels) st.labels[m] = r;
     return;
   }
@@ -242,52 +240,14 @@ __device__ __forceinline__ void record_member(const DedupState& st, const Tab& t
   const uint32_t sb = table_insert(tb.b_keys, mask, ((uint64_t)sa << 33) | t, &created);
   atomicMin(tb.b_rep + sb, m);
   atomicAdd(tb.b_cnt + sb, 1);
-  st.m_slot[k] = (int32_t)sb;
+  mslot[k] = (int32_t)sb;
 }
 
-// Rounds >= 1: one lane per member probes the first kProbe tokens past the
-// class LCP; nearly every member branches there. Members still matching
-// after the probe are handed, one at a time, to the whole warp (warp_lcp).
+// Members of rounds >= 1 are compared inside round_phase: one lane per
+// member probes the first kProbe tokens past the class LCP (nearly every
+// member branches there); members still matching after the probe are handed,
+// one at a time, to the whole warp (warp_lcp).
 constexpr int kProbe = 4;
-
-// tb: this round's tables, cleared over mask + 1 slots.
-__device__ __forceinline__ void compare_phase(const DedupState& st, const Tab& tb, uint32_t mask,
-                                              int cur, int K, int bid, int nb) {
-  const int lane = threadIdx.x & 31;
-  const int64_t W = (int64_t)nb * (blockDim.x >> 5);
-  for (int64_t k0 = ((int64_t)bid * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; k0 < K;
-       k0 += W * 32) {
-    const int64_t k = k0 + lane;
-    int m = 0, c = 0, r = 0, lm = 0, lr = 0, n = 0, x = 0;
-    bool slow = false;
-    if (k < K) {
-      m = st.mem_idx[cur][k];
-      c = st.mem_cls[cur][k];
-      r = st.cls_rep[cur][c];
-      x = st.cls_lcp[cur][c];
-      lm = st.len[m];
-      lr = st.len[r];
-      n = min(lm, lr);
-      const int32_t* pm = st.tok + st.off[m];
-      const int32_t* pr = st.tok + st.off[r];
-      const int lim = min(n, x + kProbe);
-      while (x < lim && __ldg(pm + x) == __ldg(pr + x)) ++x;
-      slow = x == lim && lim < n;
-      if (!slow) record_member(st, tb, k, m, c, r, x, lm, lr, mask);
-    }
-    unsigned todo = __ballot_sync(0xffffffffu, slow);
-    while (todo) {
-      const int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const int sm = __shfl_sync(0xffffffffu, m, src);
-      const int sr = __shfl_sync(0xffffffffu, r, src);
-      const int sx = __shfl_sync(0xffffffffu, x, src);
-      const int sn = __shfl_sync(0xffffffffu, n, src);
-      const int xx = warp_lcp(st.tok + st.off[sm], st.tok + st.off[sr], sx, sn);
-      if (lane == src) record_member(st, tb, k, m, c, r, xx, lm, lr, mask);
-    }
-  }
-}
 
 // Round 0 (one class, representative = prompt 0): the HBM-bound pass.
 // The representative is staged once per CTA in shared memory; every warp
@@ -296,9 +256,15 @@ __device__ __forceinline__ void compare_phase(const DedupState& st, const Tab& t
 // mbarrier), so ~8 KB per warp are in flight with no per-lane copy
 // instructions, and compares 512 tokens per stage with a warp-min for the
 // first mismatch.
-constexpr int kStreamStages = 4;
-constexpr int kStageTok = 512;
-constexpr int kStreamWarps = 8;
+#ifndef RS_ST_STAGES
+#define RS_ST_STAGES 4
+#define RS_ST_TOK 512
+#define RS_ST_WARPS 8
+#endif
+constexpr int kStreamStages = RS_ST_STAGES;
+constexpr int kStageTok = RS_ST_TOK;
+constexpr int kStreamWarps = RS_ST_WARPS;
+static_assert(kStageTok % 128 == 0, "a window is whole int4 chunks per lane");
 // The representative's first kRepSmemTok tokens are staged in shared memory
 // (10 KB: ring + staging still fit three CTAs per SM); the rest, if any, is
 // read through L1.
@@ -438,7 +404,8 @@ compare_stream_kernel(DedupState st, const int* kcur) {
       const int lm = __shfl_sync(0xffffffffu, my_lm, i);
       const int n = __shfl_sync(0xffffffffu, my_n, i);
       if (lane == 0)
-        record_member(st, st.tab[0], kb0 + i, m, 0, 0, found == INT32_MAX ? n : found, lm, lr, mask);
+        record_member(st, st.tab[0], st.m_slot[0], kb0 + i, m, 0, 0, found == INT32_MAX ? n : found,
+                      lm, lr, mask);
     };
     for (int s0 = 0; s0 < kStreamStages - 1; ++s0) issue_next();
     for (;;) {
@@ -464,7 +431,7 @@ compare_stream_kernel(DedupState st, const int* kcur) {
       int best = INT32_MAX;
       if (sh == 0 && rep_aligned) {  // member and representative chunks both 16B aligned
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kStageTok / 128; ++q) {
           const int j = lane + 32 * q;
           const int p = mw.y * kStageTok + 4 * j;
           if (best == INT32_MAX && p < n) {
@@ -478,7 +445,7 @@ compare_stream_kernel(DedupState st, const int* kcur) {
         }
       } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kStageTok / 128; ++q) {
           const int j = lane + 32 * q;
           const int p = -sh + mw.y * kStageTok + 4 * j;
           if (best == INT32_MAX && p < n && p + 3 >= 0) {
@@ -511,49 +478,82 @@ compare_stream_kernel(DedupState st, const int* kcur) {
 }
 
 // One thread per B slot: branch children, leaves, next classes.
-// Close round r (tables tb, members in buffer cur): every member that is
-// not an exact duplicate looks up its branch. The branch's representative
-// (its smallest member) accounts for it (dedup.cpp:58-78: one more child of
-// the node at depth x, one leaf of length x for END or len[rep] otherwise)
-// and, when the branch holds two or more members with a next token, opens
-// the class of round r + 1; every other member of such a branch is appended
-// to round r + 1's member list.
-__device__ __forceinline__ void compact_phase(const DedupState& st, const Tab& tb, int cur, int K,
-                                              int* knext, int bid, int nb) {
+// One phase per round r >= 0 (members in buffer cur, their branches in
+// tables tr): every member that is not an exact duplicate looks up its
+// branch. The branch's representative (its smallest member) accounts for it
+// (dedup.cpp:58-78: one more child of the node at depth x, one leaf of
+// length x for END or len[rep] otherwise). Every other member of a branch
+// with two or more members and a next token continues: it is appended to
+// round r + 1 (class = the branch slot, representative = rep, verified
+// prefix x + 1) and compared right away, its branch recorded in tables tn.
+__device__ __forceinline__ void round_phase(const DedupState& st, const Tab& tr, const Tab& tn,
+                                            uint32_t mask_n, int cur, int K, int* knext, int bid,
+                                            int nb) {
   const int nxt = cur ^ 1;
-  for (int k = bid * blockDim.x + threadIdx.x; k < K; k += nb * blockDim.x) {
-    const int sb = st.m_slot[k];
-    if (sb < 0) continue;
-    const int m = st.mem_idx[cur][k];
-    const int rep = tb.b_rep[sb];
-    const uint64_t key = tb.b_keys[sb];
-    const uint64_t t = key & ((1ULL << 33) - 1);
-    const bool leaf = t == kEnd || tb.b_cnt[sb] == 1;
-    if (m == rep) {
-      const int x = (int)(uint32_t)(tb.a_keys[(uint32_t)(key >> 33)] & 0xffffffffULL);
-      agg_add(st.node_diff, min(x + 1, st.maxd + 1), 1);
-      const int leaf_len = min(t == kEnd ? x : st.len[rep], st.maxd + 1);
-      if (!leaf) {
-        st.cls_rep[nxt][sb] = rep;
-        st.cls_lcp[nxt][sb] = x + 1;
+  const int lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)nb * (blockDim.x >> 5);
+  for (int64_t k0 = ((int64_t)bid * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; k0 < K;
+       k0 += W * 32) {
+    const int64_t k = k0 + lane;
+    bool cont = false;
+    int m = 0, rep = 0, sb = 0, x = 0;
+    if (k < K) {
+      sb = st.m_slot[cur][k];
+      if (sb >= 0) {
+        m = st.mem_idx[cur][k];
+        rep = tr.b_rep[sb];
+        const uint64_t key = tr.b_keys[sb];
+        const uint64_t t = key & ((1ULL << 33) - 1);
+        const bool leaf = t == kEnd || tr.b_cnt[sb] == 1;
+        if (m == rep || !leaf) x = (int)(uint32_t)(tr.a_keys[(uint32_t)(key >> 33)] & 0xffffffffULL);
+        if (m == rep) {
+          agg_add(st.node_diff, min(x + 1, st.maxd + 1), 1);
+          const int leaf_len = min(t == kEnd ? x : st.len[rep], st.maxd + 1);
+          agg_add(st.end_count, leaf_len, 1);
+          agg_add(st.node_diff, min(leaf_len + 1, st.maxd + 1), -1);
+          agg_add(st.stats, 3, 1);
+        }
+        if (leaf || m == rep) {
+          if (st.labels) st.labels[m] = rep;
+        } else {
+          cont = true;
+          ++x;  // the class's verified prefix
+        }
       }
-      agg_add(st.end_count, leaf_len, 1);
-      agg_add(st.node_diff, min(leaf_len + 1, st.maxd + 1), -1);
-      agg_add(st.stats, 3, 1);
     }
-    if (leaf || m == rep) {
-      if (st.labels) st.labels[m] = rep;
-      continue;
-    }
-    // warp-aggregated append
-    unsigned act = __activemask();
-    int leader = __ffs(act) - 1;
-    int rank = __popc(act & ((1u << (threadIdx.x & 31)) - 1));
+    // warp-aggregated append to round r + 1
+    const unsigned cm = __ballot_sync(0xffffffffu, cont);
+    if (!cm) continue;
+    const int leader = __ffs(cm) - 1;
     int base = 0;
-    if ((threadIdx.x & 31) == leader) base = atomicAdd(knext, __popc(act));
-    base = __shfl_sync(act, base, leader);
-    st.mem_idx[nxt][base + rank] = m;
-    st.mem_cls[nxt][base + rank] = sb;
+    if (lane == leader) base = atomicAdd(knext, __popc(cm));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    const int kn = base + __popc(cm & ((1u << lane) - 1));
+    int lm = 0, lr = 0, n = 0;
+    bool slow = false;
+    if (cont) {
+      st.mem_idx[nxt][kn] = m;
+      lm = st.len[m];
+      lr = st.len[rep];
+      n = min(lm, lr);
+      const int32_t* pm = st.tok + st.off[m];
+      const int32_t* pr = st.tok + st.off[rep];
+      const int lim = min(n, x + kProbe);
+      while (x < lim && __ldg(pm + x) == __ldg(pr + x)) ++x;
+      slow = x == lim && lim < n;
+      if (!slow) record_member(st, tn, st.m_slot[nxt], kn, m, sb, rep, x, lm, lr, mask_n);
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, slow);
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int sm = __shfl_sync(0xffffffffu, m, src);
+      const int sr = __shfl_sync(0xffffffffu, rep, src);
+      const int sx = __shfl_sync(0xffffffffu, x, src);
+      const int sn = __shfl_sync(0xffffffffu, n, src);
+      const int xx = warp_lcp(st.tok + st.off[sm], st.tok + st.off[sr], sx, sn);
+      if (lane == src) record_member(st, tn, st.m_slot[nxt], kn, m, sb, rep, xx, lm, lr, mask_n);
+    }
   }
 }
 
@@ -581,10 +581,9 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned l
 // barriers instead of grid-wide ones: the last rounds hold a handful).
 constexpr int kSoloMembers = 1024;
 
-// Every round after round 0's compare, in one persistent launch, two grid
-// barriers per round: close round r (compact_phase) while clearing the other
-// table set, then compare round r + 1 into it. kc[0..1] alternate as the
-// current / next member counts.
+// Every round after round 0's compare, in one persistent launch, one grid
+// barrier per round: round_phase closes round r and compares round r + 1,
+// while the table set of round r + 2 is cleared.
 __global__ void __launch_bounds__(256)
 refine_kernel(DedupState st, int* kc, unsigned long long* bar) {
   unsigned long long target = 0;
@@ -600,28 +599,31 @@ refine_kernel(DedupState st, int* kc, unsigned long long* bar) {
       grid_barrier(bar, &target);
     }
   };
-  int set = 0;  // round r's tables; round 0 (compared before this launch) used set 0
+  // round r's branches are in set r % 3; round r + 1 fills set (r + 1) % 3,
+  // cleared two phases earlier (the init kernel clears sets 0 and 1) with a
+  // capacity from a member count >= its own
+  // The member counts rotate the same way: phase r reads kc[r % 3], appends
+  // to kc[(r + 1) % 3] and zeroes kc[(r + 2) % 3] (last read in phase r - 1).
+  uint32_t capset[3];
+  capset[0] = capset[1] = dev_cap(*(volatile int*)kc);
+  capset[2] = 0;
+  int set = 0;
   for (;;) {
-    const int K = *(volatile int*)(kc + cur);
-    if (K <= 0) break;  // a single prompt: no members at all
-    if (bid == 0 && threadIdx.x == 0) kc[cur ^ 1] = 0;
-    // close round r; clear the other set for round r + 1, whose member count
-    // is at most K (its tables are sized by K)
-    compact_phase(st, st.tab[set], cur, K, kc + (cur ^ 1), bid, nb);
-    const uint32_t cap = dev_cap(K);
-    clear_phase(st.tab[set ^ 1], cap, bid, nb);
-    sync();
-    const int K2 = *(volatile int*)(kc + (cur ^ 1));
-    if (K2 <= 0) break;
-    if (!solo && K2 <= kSoloMembers) {
+    const int s1 = set == 2 ? 0 : set + 1, s2 = s1 == 2 ? 0 : s1 + 1;
+    const int K = *(volatile int*)(kc + set);
+    if (K <= 0) break;  // no members left (or a single prompt)
+    if (!solo && K <= kSoloMembers) {
       if (blockIdx.x != 0) return;
       solo = true;
       nb = 1;
     }
-    compare_phase(st, st.tab[set ^ 1], cap - 1, cur ^ 1, K2, bid, nb);
+    if (bid == 0 && threadIdx.x == 0) kc[s2] = 0;
+    round_phase(st, st.tab[set], st.tab[s1], capset[s1] - 1, cur, K, kc + s1, bid, nb);
+    capset[s2] = dev_cap(K);  // round r + 2 has at most K members
+    clear_phase(st.tab[s2], capset[s2], bid, nb);
     sync();
     cur ^= 1;
-    set ^= 1;
+    set = s1;
   }
 }
 
@@ -778,8 +780,7 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
                         RefineTail* tail = nullptr) {
   const uint32_t cap = pow2_at_least(2 * (int64_t)P + 2);
   const size_t base_bytes = abytes(P, 4) + abytes(4, 8) + abytes(P, 4) * 4 +
-                            abytes(cap, 4) * 4 + abytes(P, 4) + 2 * (abytes(cap, 8) * 2 +
-                            abytes(cap, 4) * 2) + abytes(P, 4);
+                            3 * (abytes(cap, 8) * 2 + abytes(cap, 4) * 2) + abytes(P, 4);
   int64_t maxd = std::max<int64_t>(max_len_hint, 16384);
   maxd = std::max<int64_t>(1, std::min<int64_t>(maxd, cap_len));
   int per_sm = 1;
@@ -788,7 +789,7 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
   int64_t hs[4];
   for (int attempt = 0; attempt < 2; ++attempt) {
     const int md = (int)maxd;
-    const size_t zwords = 3 * ((size_t)md + 2) + 2;  // three histograms, member counts, barrier
+    const size_t zwords = 3 * ((size_t)md + 2) + 3;  // three histograms, member counts, barrier
     RS_TRY(arena_reserve(ctx, base_bytes + 8 * abytes(zwords, 8) + (1 << 16)));
     RS_TRY(pinned_reserve(ctx, kPinnedHead + (tail ? tail->pinned_bytes(md) : 0)));
     st = DedupState{};
@@ -805,22 +806,19 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
     st.len_count = zero + 2 * ((int64_t)md + 2);
     for (int b = 0; b < 2; ++b) {
       st.mem_idx[b] = arena_alloc<int32_t>(ctx, std::max(P, 1));
-      st.mem_cls[b] = arena_alloc<int32_t>(ctx, std::max(P, 1));
-      st.cls_rep[b] = arena_alloc<int32_t>(ctx, cap);
-      st.cls_lcp[b] = arena_alloc<int32_t>(ctx, cap);
+      st.m_slot[b] = arena_alloc<int32_t>(ctx, std::max(P, 1));
     }
-    st.m_slot = arena_alloc<int32_t>(ctx, std::max(P, 1));
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < 3; ++b) {
       st.tab[b].a_keys = arena_alloc<uint64_t>(ctx, cap);
       st.tab[b].b_keys = arena_alloc<uint64_t>(ctx, cap);
       st.tab[b].b_rep = arena_alloc<int32_t>(ctx, cap);
       st.tab[b].b_cnt = arena_alloc<int32_t>(ctx, cap);
     }
-    int* kc = reinterpret_cast<int*>(zero + zwords - 2);  // current / next member count
+    int* kc = reinterpret_cast<int*>(zero + zwords - 3);  // member counts of rounds r % 3
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(zero + zwords - 1);
     st.counter = kc;
     st.labels = want_labels ? arena_alloc<int32_t>(ctx, std::max(P, 1)) : nullptr;
-    if (!st.tab[1].b_cnt || (want_labels && !st.labels)) return fail(RS_E_NOMEM, "arena exhausted (dedup)");
+    if (!st.tab[2].b_cnt || (want_labels && !st.labels)) return fail(RS_E_NOMEM, "arena exhausted (dedup)");
     RS_TRY(clear_flags(ctx));
     int64_t* pin = reinterpret_cast<int64_t*>(ctx->pinned);
     pin[0] = INT64_MAX;  // stats = {min, max, total, leaves}, uploaded from pinned memory
