@@ -529,7 +529,7 @@ def bench_dedup(args, ctx, torch, dev, stream):
         "e2e": {"value": n_tok / host_s, "unit": "tokens/s", "h2d_bytes_per_step": n_tok * 4 + off.nbytes,
                 "d2h_bytes_per_step": 5 * 8 * 2562},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": "dedup_compare (round 1)",
+                     "frac": achieved / peak, "traffic": None, "kernel": "dedup_compare_r0 (round 0, streaming)",
                      "launch_ms": r0_ms, "kernel_share_of_step": r0_ms / (dev_s * 1e3)},
     }
     if not args.no_cpu:
