@@ -19,6 +19,9 @@ ncu --set full --clock-control none --import-source on \
 python tools/prof_dedup.py > $out/${tag}_dedup_plain.log 2>&1
 ncu --set full --clock-control none --import-source on -k "regex:compare_stream" -c 1 \
     -o $out/${tag}_dedup python tools/prof_dedup.py > $out/${tag}_ncu_dedup.log 2>&1
+# the persistent (cooperative) refinement and the init pass
+ncu --set full --clock-control none --import-source on -k "regex:refine_kernel|init_kernel" -c 2 \
+    -o $out/${tag}_dedup_refine python tools/prof_dedup.py > $out/${tag}_ncu_dedup_refine.log 2>&1 || true
 python tools/prof_trace.py > $out/${tag}_trace_plain.log 2>&1
 ncu --set full --clock-control none --import-source on \
     -k "regex:classify_kernel|tokens_kernel|nl_write_kernel" -c 3 \
