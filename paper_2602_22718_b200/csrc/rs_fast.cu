@@ -1274,7 +1274,12 @@ fast_finish_kernel(FastSS ss, CandRange cr, const double* gt_all, const int4* gt
   }
 }
 
-__global__ void __launch_bounds__(kLsThreads) lockstep_eval_kernel(LsArgs A) {
+// kMinB = 1: compiled freely (61 registers, four CTAs per SM); kMinB =
+// kLsDenseCtas: capped at 48 registers (a few spills) so that five CTAs fit,
+// used only for batches the planner runs five deep (a rank's 1,250 scenarios
+// at 8 GPUs: two rounds of 740 slots instead of three of 444).
+template <int kMinB>
+__global__ void __launch_bounds__(kLsThreads, kMinB) lockstep_eval_kernel(LsArgs A) {
   extern __shared__ __align__(16) unsigned char ls_smem[];
   const FastProf& fp0 = A.fp;
   double* s_tail = reinterpret_cast<double*>(ls_smem);
@@ -1444,13 +1449,15 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
   const int cand_units = (C + kLsThreads - 1) / kLsThreads;
   LsArgs A{ss, fp, cr, S, cand_units, gt, gtab, gfirst};
   const int smem = (int)(sizeof(double) * fp.live_top + sizeof(uint16_t) * (ncm + 1));
-  RS_CUDA_TRY(cudaFuncSetAttribute(lockstep_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  void (*kern)(LsArgs) = ctas_per_sm >= kLsDenseCtas ? lockstep_eval_kernel<kLsDenseCtas>
+                                                     : lockstep_eval_kernel<1>;
+  RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 1;
-  RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lockstep_eval_kernel, kLsThreads, smem));
+  RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLsThreads, smem));
   const int units = S * A.cand_units;
   const int per = ctas_per_sm > 0 ? std::min(ctas_per_sm, std::max(1, per_sm)) : std::max(1, per_sm);
   const int grid = std::max(1, std::min(units, per * ctx->num_sms));
-  RS_LAUNCH(ctx, "group_eval", lockstep_eval_kernel, grid, kLsThreads, smem, A);
+  RS_LAUNCH(ctx, "group_eval", kern, grid, kLsThreads, smem, A);
   if (fuse) {  // the caller skips fast_reduce / select
     if (!lockstep_fuses_select(cr)) return fail(RS_E_ARG, "finish kernel needs <= 256 candidates");
     LsEpilogue ep{fuse->tt, fuse->cc, fuse->idle, fuse->n_star, fuse->rho, fuse->lambda,
@@ -1472,14 +1479,20 @@ int lockstep_slots(rs_ctx* ctx, const DevProfile& prof, int G) {
   const int64_t ncm = prof.c_hi - prof.c_lo + 1;
   const int64_t live_top = std::max<int64_t>(1, (prof.b_hi + G - 1) / G);
   const int smem = (int)(sizeof(double) * live_top + sizeof(uint16_t) * (ncm + 1));
-  if (cudaFuncSetAttribute(lockstep_eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-      cudaSuccess)
-    return ctx->num_sms;
-  int per_sm = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lockstep_eval_kernel, kLsThreads, smem) !=
-      cudaSuccess)
-    per_sm = 1;
-  return std::max(1, per_sm) * ctx->num_sms;
+  auto occupancy = [&](void (*k)(LsArgs)) {
+    int per_sm = 1;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kLsThreads, smem) != cudaSuccess) {
+      cudaGetLastError();
+      return 1;
+    }
+    return std::max(1, per_sm);
+  };
+  const int free_ctas = occupancy(lockstep_eval_kernel<1>);
+  // five deep only on top of a full four (the dense build is slower per round)
+  if (free_ctas == kLsDenseCtas - 1 && occupancy(lockstep_eval_kernel<kLsDenseCtas>) >= kLsDenseCtas)
+    return kLsDenseCtas * ctx->num_sms;
+  return free_ctas * ctx->num_sms;
 }
 
 bool lockstep_fuses_select(CandRange cr) { return cr.n_max - cr.n_min + 1 <= kLsThreads; }

@@ -693,12 +693,15 @@ static bool fast_spec_ok(const rs_scenario_spec* sp) {
          sp->plen_min >= 0 && sp->plen_max <= kFastPlenMax;
 }
 
-// Relative round time of the lockstep evaluator at c resident CTAs per SM
-// (c = 1..4, measured on B200 with the C4 workload: 3.16 / 3.28 / 3.53 /
-// 4.01 ms): a lone CTA is latency-bound, four share the issue slots.
+// Relative round time of the lockstep evaluator at c resident CTAs per SM,
+// measured on B200 with the C4 workload (one round of c x 148 scenarios):
+// 3.05 / 3.19 / 3.44 / 3.82 ms for c = 1..4 (a lone CTA is latency-bound,
+// four share the issue slots) and 5.25 ms for c = 5, the register-capped
+// build (kLsDenseCtas): less throughput per scenario than four deep, but two
+// rounds instead of three for e.g. a rank's 1,250 scenarios at 8 GPUs.
 static double lockstep_round_cost(int c) {
-  static const double rel[5] = {0.0, 1.00, 1.04, 1.12, 1.27};
-  return c <= 4 ? rel[c] : rel[4] * c / 4.0;
+  static const double rel[6] = {0.0, 1.00, 1.05, 1.13, 1.25, 1.72};
+  return c <= 5 ? rel[c] : rel[5] * c / 5.0;
 }
 
 // Modelled time of one lockstep batch of U scenarios and the CTAs per SM
@@ -723,10 +726,10 @@ static double lockstep_batch_cost(int U, int cmax, int nsm, int* best_c) {
 static void plan_batches(int S, int Bmem, int cmax, int nsm, std::vector<int>* sizes,
                          std::vector<int>* cps) {
   cmax = std::max(1, cmax);
-  const int slots = cmax * nsm;
-  const int F = Bmem >= slots ? Bmem / slots * slots : Bmem;
   std::vector<std::vector<int>> plans;
-  {
+  for (int cw = 1; cw <= cmax; ++cw) {  // full batches in whole waves of cw CTAs per SM
+    const int slots = cw * nsm;
+    const int F = Bmem >= slots ? Bmem / slots * slots : Bmem;
     std::vector<int> a;
     for (int s0 = 0; s0 < S; s0 += F) a.push_back(std::min(F, S - s0));
     plans.push_back(a);
@@ -769,8 +772,8 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
   // as whole waves of the lockstep evaluator (S = 10,000 on 148 SMs x 4:
   // batches of 1,184) with the remainder merged into the last batch when it
   // fits, each batch run at the CTAs per SM that minimise its rounds x round
-  // cost (plan_batches); e.g. a rank's 1,250 scenarios at 8 GPUs run as one
-  // batch at 3 CTAs per SM instead of 1,184 + a lone 66.
+  // cost (plan_batches); e.g. a rank's 1,250 scenarios at 8 GPUs run as 740
+  // five deep + 510 four deep (two rounds) instead of 1,184 + a lone 66.
   const int Bmem = (int)std::max<size_t>(
       1, std::min<size_t>({(size_t)S, (size_t)(8ull << 30) / per_scen, (size_t)2048}));
   std::vector<int> sizes, cps;  // scenarios and lockstep CTAs per SM, per batch
