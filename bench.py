@@ -190,7 +190,8 @@ def config(args, world):
             "scenarios": args.scenarios, "candidates": [args.n_min, args.n_max],
             "prompts": args.prompts, "G": args.G, "lambda": args.lam, "gpus_per_actor": 2,
             "profile": "default_profile()", "parallelism": f"scenario-sharded x{world}",
-            "l2": "inputs larger than L2 (per-batch scenario structures ~7 GiB, batches of 1,184 scenarios)"}
+            "l2": "inputs larger than L2 (per-batch scenario structures of several GiB: "
+                  "~6 MB per scenario, batches of up to 2,048 scenarios planned in whole waves)"}
 
 
 # ----------------------------------------------------------------- our arm
