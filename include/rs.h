@@ -102,7 +102,7 @@ int rs_prefix_index_build_device(rs_ctx* ctx, const int32_t* d_tokens,
                                  const int64_t* d_offsets, int32_t batch,
                                  rs_prefix_index** out);
 /* Device-resident outputs for benchmarking: no host copies of the CSR or the
- * tables (the refinement rounds still read one counter per round). The five
+ * tables (the build still synchronises once, at its end, for the stats). The five
  * tables land in d_tables (5 consecutive int64 arrays of max_len_cap+2
  * entries: nodes_at_depth, short_count_below, short_tokens_below,
  * longer_count_from, longer_tokens_from) and d_info receives
