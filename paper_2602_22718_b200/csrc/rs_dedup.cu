@@ -56,7 +56,8 @@ struct DedupState {
   int64_t* node_diff; // maxd + 2
   int64_t* end_count; // maxd + 2
   int64_t* len_count; // maxd + 2
-  int64_t* stats;     // {min, max, total, leaves}
+  int64_t* stats;     // {INT64_MAX - min, max, total, leaves} (zero-initialised)
+  int* flags;         // kernel status bits of this build
   int32_t* labels;    // optional
   // refinement
   int32_t* mem_idx[2];
@@ -107,8 +108,7 @@ __device__ __forceinline__ uint32_t table_insert(uint64_t* keys, uint32_t mask,
 // prefix 0; members 1 .. P-1), round 0's table clear and its member count,
 // in one pass over max(P, cap0). Histogram indices clamp at maxd + 1: a
 // longer prompt makes the host redo the refinement with larger arrays.
-__global__ void init_kernel(DedupState st, int32_t cap_len, int strict, int* flags, int* kc,
-                            uint32_t cap0) {
+__global__ void init_kernel(DedupState st, int32_t cap_len, int strict, int* kc, uint32_t cap0) {
   const int P = st.P;
   const uint32_t n = max((uint32_t)P, cap0);
   if (blockIdx.x == 0 && threadIdx.x == 0) kc[0] = P - 1;
@@ -126,7 +126,7 @@ __global__ void init_kernel(DedupState st, int32_t cap_len, int strict, int* fla
     }
     if (i < (uint32_t)P) {
       const int64_t raw = st.off[i + 1] - st.off[i];
-      if (strict && raw < 1) atomicOr(flags, kFlagEmptyPrompt);
+      if (strict && raw < 1) atomicOr(st.flags, kFlagEmptyPrompt);
       int32_t l = (int32_t)(raw < cap_len ? raw : cap_len);
       if (l < 0) l = 0;
       st.len[i] = l;
@@ -150,7 +150,7 @@ __global__ void init_kernel(DedupState st, int32_t cap_len, int strict, int* fla
   mx = warp_max(mx);
   sum = warp_sum(sum);
   if ((threadIdx.x & 31) == 0) {
-    atomicMin((long long*)&st.stats[0], mn);
+    atomicMax((long long*)&st.stats[0], INT64_MAX - mn);  // min, stored inverted
     atomicMax((long long*)&st.stats[1], mx);
     atomicAdd((unsigned long long*)&st.stats[2], sum);
   }
@@ -633,7 +633,8 @@ refine_kernel(DedupState st, int* kc, unsigned long long* bar) {
 // Each thread scans kTabIPT consecutive depths; the five thread totals go
 // through one CTA scan per chunk of kTabT * kTabIPT depths. maxd < 0: the
 // longest prompt from stats; the tables are written (stride maxd + 2) only
-// if maxd <= cap_md. stats_out (nullable) receives the four stats.
+// if maxd <= cap_md. stats_out (nullable) receives {min, max, total, leaves,
+// flags}.
 constexpr int kTabT = 512;
 constexpr int kTabIPT = 4;
 constexpr int kTabQ = 5;
@@ -642,7 +643,9 @@ __global__ void __launch_bounds__(kTabT)
 tables_kernel(DedupState st, int maxd, int cap_md, int64_t* out, int64_t* stats_out) {
   __shared__ int64_t ws[kTabQ][32];
   if (maxd < 0) maxd = (int)st.stats[1];
-  if (stats_out && threadIdx.x < 4) stats_out[threadIdx.x] = st.stats[threadIdx.x];
+  if (stats_out && threadIdx.x < 5)
+    stats_out[threadIdx.x] = threadIdx.x == 0 ? INT64_MAX - st.stats[0]
+                             : threadIdx.x == 4 ? (int64_t)*st.flags : st.stats[threadIdx.x];
   if (maxd > cap_md) return;
   const int n = maxd + 2;  // depths 0 .. maxd + 1
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -749,8 +752,8 @@ static int launch_refine(rs_ctx* ctx, DedupState st, int* kc, unsigned long long
 // tail (nullable): enqueued after the refinement, before the final
 // synchronisation; it writes the four stats to pinned + kStatsOff (else
 // they are copied there) and its own output behind kPinnedHead.
-constexpr size_t kPinnedHead = 64;
-constexpr int kStatsOff = 4;  // int64 index of the read-back stats in pinned
+constexpr size_t kPinnedHead = 128;
+constexpr int kStatsOff = 4;  // int64 index of the read-back {stats, flags} in pinned
 struct RefineTail {
   virtual size_t pinned_bytes(int cap_md) = 0;
   virtual int enqueue(rs_ctx* ctx, const DedupState& st, int cap_md) = 0;
@@ -785,7 +788,9 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
   int64_t hs[4];
   for (int attempt = 0; attempt < 2; ++attempt) {
     const int md = (int)maxd;
-    const size_t zwords = 3 * ((size_t)md + 2) + 3;  // three histograms, member counts, barrier
+    // zero-initialised: three histograms, stats, flags, member counts, barrier
+    const size_t zh = 3 * ((size_t)md + 2);
+    const size_t zwords = zh + 8;
     RS_TRY(arena_reserve(ctx, base_bytes + 8 * abytes(zwords, 8) + (1 << 16)));
     RS_TRY(pinned_reserve(ctx, kPinnedHead + (tail ? tail->pinned_bytes(md) : 0)));
     st = DedupState{};
@@ -794,7 +799,6 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
     st.tok = d_tok;
     st.off = d_off;
     st.len = arena_alloc<int32_t>(ctx, P);
-    st.stats = arena_alloc<int64_t>(ctx, 4);
     int64_t* zero = arena_alloc<int64_t>(ctx, zwords);
     if (!zero) return fail(RS_E_NOMEM, "arena exhausted (dedup)");
     st.node_diff = zero;
@@ -810,33 +814,33 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
       st.tab[b].b_rep = arena_alloc<int32_t>(ctx, cap);
       st.tab[b].b_cnt = arena_alloc<int32_t>(ctx, cap);
     }
-    int* kc = reinterpret_cast<int*>(zero + zwords - 3);  // member counts of rounds r % 3
-    unsigned long long* bar = reinterpret_cast<unsigned long long*>(zero + zwords - 1);
+    st.stats = zero + zh;
+    st.flags = reinterpret_cast<int*>(zero + zh + 4);
+    int* kc = reinterpret_cast<int*>(zero + zh + 5);  // member counts of rounds r % 3
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(zero + zh + 7);
     st.counter = kc;
     st.labels = want_labels ? arena_alloc<int32_t>(ctx, std::max(P, 1)) : nullptr;
     if (!st.tab[2].b_cnt || (want_labels && !st.labels)) return fail(RS_E_NOMEM, "arena exhausted (dedup)");
-    RS_TRY(clear_flags(ctx));
     int64_t* pin = reinterpret_cast<int64_t*>(ctx->pinned);
-    pin[0] = INT64_MAX;  // stats = {min, max, total, leaves}, uploaded from pinned memory
-    pin[1] = pin[2] = pin[3] = 0;
-    RS_CUDA_TRY(cudaMemcpyAsync(st.stats, pin, 4 * 8, cudaMemcpyHostToDevice, ctx->stream));
     RS_CUDA_TRY(cudaMemsetAsync(zero, 0, 8 * zwords, ctx->stream));
     const uint32_t cap0 = pow2_at_least(2 * (int64_t)(P - 1) + 2);  // dev_cap(P - 1)
     const int iblocks = (int)std::max<int64_t>(
         1, std::min<int64_t>((std::max<int64_t>(P, cap0) + 255) / 256, 8 * ctx->num_sms));
-    RS_LAUNCH(ctx, "dedup_init", init_kernel, iblocks, 256, 0, st, cap_len, strict, ctx->d_flags,
-              kc, cap0);
+    RS_LAUNCH(ctx, "dedup_init", init_kernel, iblocks, 256, 0, st, cap_len, strict, kc, cap0);
     // round 0 (every member against prompt 0) streams the batch; every later
     // round runs inside one persistent launch (refine_kernel)
     RS_LAUNCH(ctx, "dedup_compare_r0", compare_stream_kernel, per_sm * ctx->num_sms,
               kStreamWarps * 32, kStreamSmem, st, kc);
     RS_TRY(launch_refine(ctx, st, kc, bar));
     if (tail) {
-      RS_TRY(tail->enqueue(ctx, st, md));
+      RS_TRY(tail->enqueue(ctx, st, md));  // writes {stats, flags} to pin + kStatsOff
     } else {
-      RS_CUDA_TRY(cudaMemcpyAsync(pin + kStatsOff, st.stats, 4 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      RS_CUDA_TRY(cudaMemcpyAsync(pin + kStatsOff, st.stats, 5 * 8, cudaMemcpyDeviceToHost, ctx->stream));
     }
-    RS_TRY(sync_and_check(ctx));
+    RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (!tail) pin[kStatsOff] = INT64_MAX - pin[kStatsOff];
+    if (ctx->timing) RS_TRY(collect_timers(ctx));
+    RS_TRY(flags_to_status((int)pin[kStatsOff + 4]));
     std::memcpy(hs, pin + kStatsOff, sizeof(hs));
     if (hs[1] <= maxd) break;
     maxd = hs[1];  // a prompt longer than the bound: rerun with exact arrays
@@ -1151,8 +1155,7 @@ int rs_unique_prefix_count_among(rs_ctx* ctx, const int32_t* tokens, const int64
   DedupState st;
   int64_t stats[4];
   RS_TRY(dedup_refine(ctx, d.tok, d.off, count, prefix_len, 0, false, prefix_len, &st, stats,
-                      nullptr));
-  RS_TRY(sync_and_check(ctx));
+                      nullptr));  // synchronised, its own status checked
   *out = stats[3];
   return RS_OK;
 }
@@ -1166,9 +1169,8 @@ int rs_dedup_map(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets, int
   RS_TRY(upload_csr(ctx, tokens, offsets, count, &d));
   DedupState st;
   int64_t stats[4];
-  RS_TRY(dedup_refine(ctx, d.tok, d.off, count, prefix_len, 0, true, prefix_len, &st, stats,
-                      labels));
-  return sync_and_check(ctx);
+  return dedup_refine(ctx, d.tok, d.off, count, prefix_len, 0, true, prefix_len, &st, stats,
+                      labels);  // synchronised (labels read back), its own status checked
 }
 
 int rs_block_hashes(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets, int32_t count,
