@@ -117,7 +117,12 @@ int sync_and_check(rs_ctx* ctx) {
                               cudaMemcpyDeviceToHost, ctx->stream));
   RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   if (ctx->timing) RS_TRY(collect_timers(ctx));
-  return flags_to_status(*ctx->h_flags);
+  const int flags = *ctx->h_flags;
+  if (flags) {  // reported once: the next call starts from a clean status
+    *ctx->h_flags = 0;
+    RS_TRY(clear_flags(ctx));
+  }
+  return flags_to_status(flags);
 }
 
 int h2d(rs_ctx* ctx, void* dst, const void* src, size_t bytes) {

@@ -1187,6 +1187,7 @@ int rs_block_hashes(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets, 
   }
   DeviceCSR d;
   RS_TRY(upload_csr(ctx, tokens, offsets, count, &d));
+  RS_TRY(clear_flags(ctx));
   const int64_t nh = hoff[count];
   RS_TRY(arena_reserve(ctx, abytes(count + 1, 8) + abytes(std::max<int64_t>(nh, 1), 8) + 4096));
   int64_t* dho = arena_alloc<int64_t>(ctx, count + 1);

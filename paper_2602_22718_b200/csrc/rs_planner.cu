@@ -535,6 +535,10 @@ static int read_flags(rs_ctx* ctx, int* flags) {
                               cudaMemcpyDeviceToHost, ctx->stream));
   RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   *flags = *ctx->h_flags;
+  if (*flags) {  // consumed here: the next call starts from a clean status
+    *ctx->h_flags = 0;
+    RS_TRY(clear_flags(ctx));
+  }
   return RS_OK;
 }
 

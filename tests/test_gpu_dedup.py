@@ -143,6 +143,20 @@ def test_repeated_builds_identical():
                 assert a.tolist() == b.tolist(), (trial, rep)
 
 
+def test_status_of_an_earlier_call_does_not_leak():
+    """A call that fails on a device-side check (target length < 1 in
+    integrate_decode_seconds) leaves its status bits set; the dedup calls that
+    follow must report their own status only."""
+    from paper_2602_22718_b200.rollsim import ResponseSpec, default_profile
+    with pytest.raises(rs.ValidationError):
+        rs.integrate_decode_seconds([ResponseSpec(10, 0.0)], default_profile())
+    seqs = [[1, 2, 3], [1, 2, 4], [1, 2, 3], [7]]
+    assert rs.unique_prefix_count_among(seqs, 3) == 3
+    assert rs.dedup_map(seqs, 3).tolist() == [0, 1, 0, 3]
+    idx = PrefixIndex.build(csr(seqs))
+    assert idx.unique_prefix_count(2) == 2
+
+
 def test_among_dedup_map_and_hashes():
     rng = Rng(77)
     for trial in range(40):
