@@ -632,19 +632,26 @@ refine_kernel(DedupState st, int* kc, unsigned long long* bar) {
 //   lcf[d]   = total(len_count_m) - incl(len_count_m)[d]
 //   ltf[d]   = total(len_count_m * i) - incl(len_count_m * i)[d]
 // Each thread scans kTabIPT consecutive depths; the five thread totals go
-// through one CTA scan per chunk of kTabT * kTabIPT depths. maxd < 0: the
+// through one CTA scan per chunk of kTabT * kTabIPT depths, and the chunk is
+// staged in shared memory and written out coalesced. Every CTA of the grid
+// runs the (cheap) scan; CTA b writes only depths [b n / G, (b + 1) n / G),
+// so the writes into mapped host memory leave from G SMs at once. maxd < 0: the
 // longest prompt from stats; the tables are written (stride maxd + 2) only
 // if maxd <= cap_md. stats_out (nullable) receives {min, max, total, leaves,
 // flags}.
 constexpr int kTabT = 512;
 constexpr int kTabIPT = 4;
 constexpr int kTabQ = 5;
+constexpr int kTabChunk = kTabT * kTabIPT;
+constexpr int kTabSmem = (int)sizeof(int64_t) * kTabQ * kTabChunk;
+constexpr int kTabCtas = 16;
 
 __global__ void __launch_bounds__(kTabT)
 tables_kernel(DedupState st, int maxd, int cap_md, int64_t* out, int64_t* stats_out) {
   __shared__ int64_t ws[kTabQ][32];
+  extern __shared__ int64_t stage[];  // [kTabQ][kTabChunk]
   if (maxd < 0) maxd = (int)st.stats[1];
-  if (stats_out && threadIdx.x < 5)
+  if (stats_out && blockIdx.x == 0 && threadIdx.x < 5)
     stats_out[threadIdx.x] = threadIdx.x == 0 ? INT64_MAX - st.stats[0]
                              : threadIdx.x == 4 ? (int64_t)*st.flags : st.stats[threadIdx.x];
   if (maxd > cap_md) return;
@@ -694,17 +701,23 @@ tables_kernel(DedupState st, int maxd, int cap_md, int64_t* out, int64_t* stats_
     for (int q = 0; q < kTabQ; ++q) pre[q] = carry[q] + ws[q][wid] + incl[q] - run[q];
 #pragma unroll
     for (int j = 0; j < kTabIPT; ++j) {
-      const int d = d0 + threadIdx.x * kTabIPT + j;
+      const int i = threadIdx.x * kTabIPT + j, d = d0 + i;
 #pragma unroll
       for (int q = 0; q < kTabQ; ++q) pre[q] += v[j][q];
-      if (d < n) {
-        const bool in = d >= 1 && d <= maxd;
-        tab[0][d] = in ? pre[0] : 0;
-        tab[1][d] = pre[1] - v[j][1];
-        tab[2][d] = pre[2] - v[j][1] * d;
-        tab[3][d] = tl - pre[3];
-        tab[4][d] = tt - pre[4];
-      }
+      const bool in = d >= 1 && d <= maxd;
+      stage[0 * kTabChunk + i] = in ? pre[0] : 0;
+      stage[1 * kTabChunk + i] = pre[1] - v[j][1];
+      stage[2 * kTabChunk + i] = pre[2] - v[j][1] * d;
+      stage[3 * kTabChunk + i] = tl - pre[3];
+      stage[4 * kTabChunk + i] = tt - pre[4];
+    }
+    __syncthreads();
+    {  // this CTA's slice of the chunk, consecutive depths per warp
+      const int lo = max(d0, (int)((int64_t)blockIdx.x * n / gridDim.x));
+      const int hi = min(min(d0 + kTabChunk, n), (int)((int64_t)(blockIdx.x + 1) * n / gridDim.x));
+      for (int d = lo + threadIdx.x; d < hi; d += kTabT)
+#pragma unroll
+        for (int q = 0; q < kTabQ; ++q) tab[q][d] = stage[q * kTabChunk + (d - d0)];
     }
     // carry = chunk total (the last warp's inclusive totals)
     __syncthreads();
@@ -760,6 +773,15 @@ struct RefineTail {
   virtual int enqueue(rs_ctx* ctx, const DedupState& st, int cap_md) = 0;
   virtual void finish(rs_ctx* ctx) = 0;  // after the final synchronisation
 };
+
+static int tables_setup() {
+  static bool done = false;
+  if (!done) {
+    RS_CUDA_TRY(cudaFuncSetAttribute(tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTabSmem));
+    done = true;
+  }
+  return RS_OK;
+}
 
 static int stream_kernel_setup(int* blocks_per_sm) {
   static int per_sm = 0;
@@ -874,7 +896,8 @@ static int build_index_device(rs_ctx* ctx, const int32_t* d_tok, const int64_t* 
     int enqueue(rs_ctx* c, const DedupState& st, int cap_md) override {
       // stats and tables go straight into mapped pinned host memory
       int64_t* pin = reinterpret_cast<int64_t*>(c->pinned);
-      RS_LAUNCH(c, "dedup_tables", tables_kernel, 1, kTabT, 0, st, -1, cap_md,
+      RS_TRY(tables_setup());
+      RS_LAUNCH(c, "dedup_tables", tables_kernel, kTabCtas, kTabT, kTabSmem, st, -1, cap_md,
                 reinterpret_cast<int64_t*>(c->pinned + kPinnedHead), pin + kStatsOff);
       return RS_OK;
     }
@@ -1024,7 +1047,8 @@ int rs_prefix_index_build_device_async(rs_ctx* ctx, const int32_t* d_tokens,
   RS_TRY(dedup_refine(ctx, d_tokens, d_offsets, batch, INT32_MAX, 1, false, max_len_cap, &st,
                       stats, nullptr));
   if (stats[1] > max_len_cap) return fail(RS_E_ARG, "max_len_cap below the longest prompt");
-  RS_LAUNCH(ctx, "dedup_tables", tables_kernel, 1, kTabT, 0, st, max_len_cap, max_len_cap, d_tables,
+  RS_TRY(tables_setup());
+  RS_LAUNCH(ctx, "dedup_tables", tables_kernel, kTabCtas, kTabT, kTabSmem, st, max_len_cap, max_len_cap, d_tables,
             nullptr);
   int64_t info[5] = {batch, stats[0], stats[1], stats[2], 0};
   RS_TRY(h2d(ctx, d_info, info, sizeof(info)));
