@@ -52,6 +52,39 @@ int pinned_reserve(rs_ctx* ctx, size_t bytes) {
   return RS_OK;
 }
 
+PinnedPool::~PinnedPool() {
+  for (auto& b : free) cudaFreeHost(b.first);
+}
+
+void* PinnedPool::take(size_t bytes, size_t* cap) {
+  {
+    std::lock_guard<std::mutex> g(m);
+    for (size_t i = 0; i < free.size(); ++i)
+      if (free[i].second >= bytes) {
+        const auto b = free[i];
+        free.erase(free.begin() + i);
+        *cap = b.second;
+        return b.first;
+      }
+  }
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  *cap = bytes;
+  return p;
+}
+
+void PinnedPool::give(void* p, size_t cap) {
+  std::lock_guard<std::mutex> g(m);
+  if (free.size() < 8) {
+    free.emplace_back(p, cap);
+    return;
+  }
+  cudaFreeHost(p);
+}
+
 void timer_begin(rs_ctx* ctx, const char* name, cudaEvent_t* a) {
   (void)name;
   *a = nullptr;

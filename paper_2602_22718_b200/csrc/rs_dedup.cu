@@ -109,47 +109,67 @@ __device__ __forceinline__ uint32_t table_insert(uint64_t* keys, uint32_t mask,
 // in one pass over max(P, cap0). Histogram indices clamp at maxd + 1: a
 // longer prompt makes the host redo the refinement with larger arrays.
 __global__ void init_kernel(DedupState st, int32_t cap_len, int strict, int* kc, uint32_t cap0) {
+  __shared__ long long s_mn[8], s_mx[8];
+  __shared__ unsigned long long s_sum[8];
   const int P = st.P;
-  const uint32_t n = max((uint32_t)P, cap0);
-  if (blockIdx.x == 0 && threadIdx.x == 0) kc[0] = P - 1;
-  long long mn = INT64_MAX, mx = 0;
-  unsigned long long sum = 0;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    if (i < cap0) {  // rounds 0 and 1 use sets 0 and 1
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t tid0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid0 == 0) kc[0] = P - 1;
+  // rounds 0 and 1 use table sets 0 and 1: cleared with 16-byte stores,
+  // four slots per thread (cap0 is a power of two >= 64)
+  for (uint32_t q = tid0; q < cap0 / 4; q += stride) {
+    const ulonglong2 e2 = make_ulonglong2(kEmpty, kEmpty);
 #pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        st.tab[b].a_keys[i] = kEmpty;
-        st.tab[b].b_keys[i] = kEmpty;
-        st.tab[b].b_rep[i] = INT32_MAX;
-        st.tab[b].b_cnt[i] = 0;
-      }
-    }
-    if (i < (uint32_t)P) {
-      const int64_t raw = st.off[i + 1] - st.off[i];
-      if (strict && raw < 1) atomicOr(st.flags, kFlagEmptyPrompt);
-      int32_t l = (int32_t)(raw < cap_len ? raw : cap_len);
-      if (l < 0) l = 0;
-      st.len[i] = l;
-      mn = l < mn ? l : mn;
-      mx = l > mx ? l : mx;
-      sum += (unsigned long long)l;
-      const int lc = min(l, st.maxd + 1);
-      agg_add(st.len_count, lc, 1);
-      if (i == 0) {
-        atomicAdd((unsigned long long*)&st.node_diff[1], 1ULL);  // first sorted string
-        atomicAdd((unsigned long long*)&st.end_count[lc], 1ULL);
-        atomicAdd((unsigned long long*)&st.node_diff[min(l + 1, st.maxd + 1)], (unsigned long long)-1LL);
-        atomicAdd((unsigned long long*)&st.stats[3], 1ULL);
-        if (st.labels) st.labels[0] = 0;
-      } else {
-        st.mem_idx[0][i - 1] = i;
-      }
+    for (int b = 0; b < 2; ++b) {
+      reinterpret_cast<ulonglong2*>(st.tab[b].a_keys)[2 * q] = e2;
+      reinterpret_cast<ulonglong2*>(st.tab[b].a_keys)[2 * q + 1] = e2;
+      reinterpret_cast<ulonglong2*>(st.tab[b].b_keys)[2 * q] = e2;
+      reinterpret_cast<ulonglong2*>(st.tab[b].b_keys)[2 * q + 1] = e2;
+      reinterpret_cast<int4*>(st.tab[b].b_rep)[q] = make_int4(INT32_MAX, INT32_MAX, INT32_MAX, INT32_MAX);
+      reinterpret_cast<int4*>(st.tab[b].b_cnt)[q] = make_int4(0, 0, 0, 0);
     }
   }
+  long long mn = INT64_MAX, mx = 0;
+  unsigned long long sum = 0;
+  for (uint32_t i = tid0; i < (uint32_t)P; i += stride) {
+    const int64_t raw = st.off[i + 1] - st.off[i];
+    if (strict && raw < 1) atomicOr(st.flags, kFlagEmptyPrompt);
+    int32_t l = (int32_t)(raw < cap_len ? raw : cap_len);
+    if (l < 0) l = 0;
+    st.len[i] = l;
+    mn = l < mn ? l : mn;
+    mx = l > mx ? l : mx;
+    sum += (unsigned long long)l;
+    const int lc = min(l, st.maxd + 1);
+    agg_add(st.len_count, lc, 1);
+    if (i == 0) {
+      atomicAdd((unsigned long long*)&st.node_diff[1], 1ULL);  // first sorted string
+      atomicAdd((unsigned long long*)&st.end_count[lc], 1ULL);
+      atomicAdd((unsigned long long*)&st.node_diff[min(l + 1, st.maxd + 1)], (unsigned long long)-1LL);
+      atomicAdd((unsigned long long*)&st.stats[3], 1ULL);
+      if (st.labels) st.labels[0] = 0;
+    } else {
+      st.mem_idx[0][i - 1] = i;
+    }
+  }
+  // one set of stats atomics per CTA
+  if (blockIdx.x * blockDim.x >= (uint32_t)P) return;  // CTA-uniform: no prompts here
   mn = warp_min(mn);
   mx = warp_max(mx);
   sum = warp_sum(sum);
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((threadIdx.x & 31) == 0) {
+    s_mn[w] = mn;
+    s_mx[w] = mx;
+    s_sum[w] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < nw; ++k) {
+      mn = s_mn[k] < mn ? s_mn[k] : mn;
+      mx = s_mx[k] > mx ? s_mx[k] : mx;
+      sum += s_sum[k];
+    }
     atomicMax((long long*)&st.stats[0], INT64_MAX - mn);  // min, stored inverted
     atomicMax((long long*)&st.stats[1], mx);
     atomicAdd((unsigned long long*)&st.stats[2], sum);
@@ -765,11 +785,11 @@ static int launch_refine(rs_ctx* ctx, DedupState st, int* kc, unsigned long long
 // final stats and the refinement reruns once with the exact size.
 // tail (nullable): enqueued after the refinement, before the final
 // synchronisation; it writes the four stats to pinned + kStatsOff (else
-// they are copied there) and its own output behind kPinnedHead.
+// they are copied there) and its own output (the index tables: into the
+// index's pinned block).
 constexpr size_t kPinnedHead = 128;
 constexpr int kStatsOff = 4;  // int64 index of the read-back {stats, flags} in pinned
 struct RefineTail {
-  virtual size_t pinned_bytes(int cap_md) = 0;
   virtual int enqueue(rs_ctx* ctx, const DedupState& st, int cap_md) = 0;
   virtual void finish(rs_ctx* ctx) = 0;  // after the final synchronisation
 };
@@ -815,7 +835,7 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
     const size_t zh = 3 * ((size_t)md + 2);
     const size_t zwords = zh + 8;
     RS_TRY(arena_reserve(ctx, base_bytes + 8 * abytes(zwords, 8) + (1 << 16)));
-    RS_TRY(pinned_reserve(ctx, kPinnedHead + (tail ? tail->pinned_bytes(md) : 0)));
+    RS_TRY(pinned_reserve(ctx, kPinnedHead));
     st = DedupState{};
     st.P = P;
     st.maxd = md;
@@ -848,7 +868,7 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
     RS_CUDA_TRY(cudaMemsetAsync(zero, 0, 8 * zwords, ctx->stream));
     const uint32_t cap0 = pow2_at_least(2 * (int64_t)(P - 1) + 2);  // dev_cap(P - 1)
     const int iblocks = (int)std::max<int64_t>(
-        1, std::min<int64_t>((std::max<int64_t>(P, cap0) + 255) / 256, 8 * ctx->num_sms));
+        1, std::min<int64_t>((std::max<int64_t>(P, cap0 / 4) + 255) / 256, 8 * ctx->num_sms));
     RS_LAUNCH(ctx, "dedup_init", init_kernel, iblocks, 256, 0, st, cap_len, strict, kc, cap0);
     // round 0 (every member against prompt 0) streams the batch; every later
     // round runs inside one persistent launch (refine_kernel)
@@ -882,38 +902,59 @@ using namespace rs;
 struct rs_prefix_index {
   int32_t batch = 0, min_len = 0, max_len = 0;
   int64_t total = 0;
-  std::vector<int64_t> nodes, scb, stb, lcf, ltf;
+  // the five tables, stride max_len + 2 (nodes has max_len + 1 entries)
+  const int64_t *nodes = nullptr, *scb = nullptr, *stb = nullptr, *lcf = nullptr, *ltf = nullptr;
+  std::vector<int64_t> own;  // storage of an index made from host tables
+  // storage of a device-built index: the pinned block the tables kernel
+  // wrote (zero-copy), returned to the context's pool on free
+  std::shared_ptr<rs::PinnedPool> pool;
+  void* blk = nullptr;
+  size_t blk_cap = 0;
+  ~rs_prefix_index() {
+    if (blk) pool->give(blk, blk_cap);
+  }
+  void view(const int64_t* t) {
+    const size_t n = (size_t)max_len + 2;
+    nodes = t;
+    scb = t + n;
+    stb = t + 2 * n;
+    lcf = t + 3 * n;
+    ltf = t + 4 * n;
+  }
 };
 
 static int build_index_device(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
                               int32_t P, rs_prefix_index** out) {
   if (P <= 0) return fail(RS_E_VALIDATION, "prefix index needs a non-empty batch");
-  // The tables kernel writes the stats and tables into mapped pinned memory
-  // before the refinement's single synchronisation.
+  // The tables kernel writes the stats (into the context's pinned staging)
+  // and the tables (into the index's own pinned block) through mapped host
+  // memory before the refinement's single synchronisation: no copy after it.
   struct Tables : RefineTail {
-    rs_prefix_index* idx = nullptr;  // filled from pinned memory by finish()
-    size_t pinned_bytes(int cap_md) override { return 5 * 8 * ((size_t)cap_md + 2); }
+    rs_prefix_index* idx = nullptr;
     int enqueue(rs_ctx* c, const DedupState& st, int cap_md) override {
-      // stats and tables go straight into mapped pinned host memory
+      const size_t need = 5 * 8 * ((size_t)cap_md + 2);
+      if (idx->blk && idx->blk_cap < need) {  // a rerun with a longer bound
+        RS_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        idx->pool->give(idx->blk, idx->blk_cap);
+        idx->blk = nullptr;
+      }
+      if (!idx->blk) {
+        idx->pool = c->pin_pool;
+        idx->blk = c->pin_pool->take(need, &idx->blk_cap);
+        if (!idx->blk) return fail(RS_E_NOMEM, "pinned allocation failed");
+      }
       int64_t* pin = reinterpret_cast<int64_t*>(c->pinned);
       RS_TRY(tables_setup());
       RS_LAUNCH(c, "dedup_tables", tables_kernel, kTabCtas, kTabT, kTabSmem, st, -1, cap_md,
-                reinterpret_cast<int64_t*>(c->pinned + kPinnedHead), pin + kStatsOff);
+                static_cast<int64_t*>(idx->blk), pin + kStatsOff);
       return RS_OK;
     }
     void finish(rs_ctx* c) override {
       const int64_t* stats = reinterpret_cast<const int64_t*>(c->pinned) + kStatsOff;
-      const int md = (int)stats[1];
-      const size_t n = (size_t)md + 2;
-      const int64_t* t = reinterpret_cast<const int64_t*>(c->pinned + kPinnedHead);
       idx->min_len = (int32_t)stats[0];
-      idx->max_len = md;
+      idx->max_len = (int32_t)stats[1];
       idx->total = stats[2];
-      idx->nodes.assign(t, t + md + 1);
-      idx->scb.assign(t + n, t + 2 * n);
-      idx->stb.assign(t + 2 * n, t + 3 * n);
-      idx->lcf.assign(t + 3 * n, t + 4 * n);
-      idx->ltf.assign(t + 4 * n, t + 5 * n);
+      idx->view(static_cast<const int64_t*>(idx->blk));
     }
   } tab;
   std::unique_ptr<rs_prefix_index> idx(new rs_prefix_index());
@@ -1067,11 +1108,16 @@ int rs_prefix_index_from_tables(int32_t batch, int32_t min_len, int32_t max_len,
   idx->min_len = min_len;
   idx->max_len = max_len;
   idx->total = total;
-  idx->nodes.assign(nodes, nodes + max_len + 1);
-  idx->scb.assign(scb, scb + max_len + 2);
-  idx->stb.assign(stb, stb + max_len + 2);
-  idx->lcf.assign(lcf, lcf + max_len + 2);
-  idx->ltf.assign(ltf, ltf + max_len + 2);
+  const size_t n = (size_t)max_len + 2;
+  idx->own.resize(5 * n);
+  int64_t* t = idx->own.data();
+  std::memcpy(t, nodes, 8 * (n - 1));
+  t[n - 1] = 0;
+  std::memcpy(t + n, scb, 8 * n);
+  std::memcpy(t + 2 * n, stb, 8 * n);
+  std::memcpy(t + 3 * n, lcf, 8 * n);
+  std::memcpy(t + 4 * n, ltf, 8 * n);
+  idx->view(t);
   *out = idx;
   return RS_OK;
 }
@@ -1117,11 +1163,12 @@ int rs_remainder_tokens(const rs_prefix_index* idx, int32_t l, int64_t* out) {
 int rs_prefix_index_tables(const rs_prefix_index* idx, int64_t* nodes, int64_t* scb,
                            int64_t* stb, int64_t* lcf, int64_t* ltf) {
   if (!idx) return fail(RS_E_ARG, "index is NULL");
-  if (nodes) std::memcpy(nodes, idx->nodes.data(), 8 * idx->nodes.size());
-  if (scb) std::memcpy(scb, idx->scb.data(), 8 * idx->scb.size());
-  if (stb) std::memcpy(stb, idx->stb.data(), 8 * idx->stb.size());
-  if (lcf) std::memcpy(lcf, idx->lcf.data(), 8 * idx->lcf.size());
-  if (ltf) std::memcpy(ltf, idx->ltf.data(), 8 * idx->ltf.size());
+  const size_t n = (size_t)idx->max_len + 2;
+  if (nodes) std::memcpy(nodes, idx->nodes, 8 * (n - 1));
+  if (scb) std::memcpy(scb, idx->scb, 8 * n);
+  if (stb) std::memcpy(stb, idx->stb, 8 * n);
+  if (lcf) std::memcpy(lcf, idx->lcf, 8 * n);
+  if (ltf) std::memcpy(ltf, idx->ltf, 8 * n);
   return RS_OK;
 }
 

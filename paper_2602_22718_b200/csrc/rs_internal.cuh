@@ -12,6 +12,8 @@
 #include <stdint.h>
 
 #include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -91,6 +93,18 @@ struct KernelTimer {
   uint64_t launches = 0;
 };
 
+// Recycled pinned host blocks. Shared by a context and the objects it
+// builds (a prefix index keeps its tables in the block the tables kernel
+// wrote), so a block outlives the context and returns here when the index
+// is freed.
+struct PinnedPool {
+  std::mutex m;
+  std::vector<std::pair<void*, size_t>> free;
+  ~PinnedPool();
+  void* take(size_t bytes, size_t* cap);  // nullptr if the allocation fails
+  void give(void* p, size_t cap);
+};
+
 }  // namespace rs
 
 struct rs_ctx {
@@ -105,6 +119,7 @@ struct rs_ctx {
   size_t pinned_cap = 0;
   int* d_flags = nullptr;  // kernel status bits
   int* h_flags = nullptr;  // pinned mirror
+  std::shared_ptr<rs::PinnedPool> pin_pool = std::make_shared<rs::PinnedPool>();
   uint64_t launches = 0;
   bool timing = false;
   std::map<std::string, rs::KernelTimer> timers;

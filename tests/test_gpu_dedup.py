@@ -143,6 +143,40 @@ def test_repeated_builds_identical():
                 assert a.tolist() == b.tolist(), (trial, rep)
 
 
+def test_live_indexes_keep_their_tables():
+    """A device-built index keeps its tables in its own pinned block (the one
+    the tables kernel wrote): later builds, freed indexes and even the
+    destruction of the building context leave a live index intact."""
+    import ctypes as C
+    from paper_2602_22718_b200.lib import Context, check
+    rng = np.random.RandomState(5)
+    batches = []
+    for _ in range(3):
+        head = rng.randint(0, 9, size=rng.randint(50, 400)).tolist()
+        seqs = [head[:rng.randint(1, len(head) + 1)] + rng.randint(0, 4, size=rng.randint(0, 40)).tolist()
+                for _ in range(rng.randint(100, 600))]
+        batches.append(csr(seqs))
+    live = [PrefixIndex.build(b) for b in batches]
+    PrefixIndex.build(batches[0])  # built and freed: its block returns to the pool
+    PrefixIndex.build(batches[2])
+    for idx, (tok, off) in zip(live, batches):
+        _, want = port().prefix_tables(tok, off)
+        for a, b in zip(idx.tables(), want):
+            assert a.tolist() == b.tolist()
+    tok, off = batches[1]
+    ctx = Context(0)
+    h = C.c_void_p()
+    check(ctx.lib.rs_prefix_index_build(ctx.handle, tok.ctypes.data_as(C.POINTER(C.c_int32)),
+                                        off.ctypes.data_as(C.POINTER(C.c_int64)), len(off) - 1,
+                                        C.byref(h)))
+    lib = ctx.lib
+    ctx.close()
+    idx = PrefixIndex(h, type("Lib", (), {"lib": lib})())  # no context behind it any more
+    _, want = port().prefix_tables(tok, off)
+    for a, b in zip(idx.tables(), want):
+        assert a.tolist() == b.tolist()
+
+
 def test_status_of_an_earlier_call_does_not_leak():
     """A call that fails on a device-side check (target length < 1 in
     integrate_decode_seconds) leaves its status bits set; the dedup calls that
