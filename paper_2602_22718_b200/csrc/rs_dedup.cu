@@ -663,13 +663,17 @@ constexpr int kTabT = 512;
 constexpr int kTabIPT = 4;
 constexpr int kTabQ = 5;
 constexpr int kTabChunk = kTabT * kTabIPT;
-constexpr int kTabSmem = (int)sizeof(int64_t) * kTabQ * kTabChunk;
+// staged as [q][j][thread], rows padded by 8 so a warp's reads of 32
+// consecutive depths (8 threads x 4 j) spread over all banks
+constexpr int kTabRow = kTabT + 8;
+constexpr int kTabStage = kTabIPT * kTabRow;
+constexpr int kTabSmem = (int)sizeof(int64_t) * kTabQ * kTabStage;
 constexpr int kTabCtas = 16;
 
 __global__ void __launch_bounds__(kTabT)
 tables_kernel(DedupState st, int maxd, int cap_md, int64_t* out, int64_t* stats_out) {
   __shared__ int64_t ws[kTabQ][32];
-  extern __shared__ int64_t stage[];  // [kTabQ][kTabChunk]
+  extern __shared__ int64_t stage[];  // [kTabQ][kTabIPT][kTabRow]
   if (maxd < 0) maxd = (int)st.stats[1];
   if (stats_out && blockIdx.x == 0 && threadIdx.x < 5)
     stats_out[threadIdx.x] = threadIdx.x == 0 ? INT64_MAX - st.stats[0]
@@ -721,23 +725,26 @@ tables_kernel(DedupState st, int maxd, int cap_md, int64_t* out, int64_t* stats_
     for (int q = 0; q < kTabQ; ++q) pre[q] = carry[q] + ws[q][wid] + incl[q] - run[q];
 #pragma unroll
     for (int j = 0; j < kTabIPT; ++j) {
-      const int i = threadIdx.x * kTabIPT + j, d = d0 + i;
+      const int d = d0 + threadIdx.x * kTabIPT + j;
 #pragma unroll
       for (int q = 0; q < kTabQ; ++q) pre[q] += v[j][q];
       const bool in = d >= 1 && d <= maxd;
-      stage[0 * kTabChunk + i] = in ? pre[0] : 0;
-      stage[1 * kTabChunk + i] = pre[1] - v[j][1];
-      stage[2 * kTabChunk + i] = pre[2] - v[j][1] * d;
-      stage[3 * kTabChunk + i] = tl - pre[3];
-      stage[4 * kTabChunk + i] = tt - pre[4];
+      int64_t* sj = stage + j * kTabRow + threadIdx.x;
+      sj[0 * kTabStage] = in ? pre[0] : 0;
+      sj[1 * kTabStage] = pre[1] - v[j][1];
+      sj[2 * kTabStage] = pre[2] - v[j][1] * d;
+      sj[3 * kTabStage] = tl - pre[3];
+      sj[4 * kTabStage] = tt - pre[4];
     }
     __syncthreads();
     {  // this CTA's slice of the chunk, consecutive depths per warp
       const int lo = max(d0, (int)((int64_t)blockIdx.x * n / gridDim.x));
       const int hi = min(min(d0 + kTabChunk, n), (int)((int64_t)(blockIdx.x + 1) * n / gridDim.x));
-      for (int d = lo + threadIdx.x; d < hi; d += kTabT)
+      for (int d = lo + threadIdx.x; d < hi; d += kTabT) {
+        const int i = d - d0, k = (i % kTabIPT) * kTabRow + i / kTabIPT;
 #pragma unroll
-        for (int q = 0; q < kTabQ; ++q) tab[q][d] = stage[q * kTabChunk + (d - d0)];
+        for (int q = 0; q < kTabQ; ++q) tab[q][d] = stage[q * kTabStage + k];
+      }
     }
     // carry = chunk total (the last warp's inclusive totals)
     __syncthreads();
