@@ -532,6 +532,9 @@ def bench_dedup(args, ctx, torch, dev, stream):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "kernel": "dedup_compare_r0 (round 0, streaming)",
                      "launch_ms": r0_ms, "kernel_share_of_step": r0_ms / (dev_s * 1e3)},
+        # the whole build call (host wall clock) against the same roofline:
+        # SURVEY §8d's 4 B per token read once
+        "build_roofline_frac": n_tok * 4 / dev_s / 1e9 / peak,
     }
     if not args.no_cpu:
         from oracle_lib import port, ref
