@@ -112,6 +112,10 @@ int rs_prefix_index_build_device_async(rs_ctx* ctx, const int32_t* d_tokens,
                                        const int64_t* d_offsets, int32_t batch,
                                        int32_t max_len_cap, int64_t* d_tables,
                                        int64_t* d_info);
+/* An index built on the device keeps its tables in a pinned host block the
+ * tables kernel wrote (no copy after the build's sync); the block belongs
+ * to a pool shared with the context, so an index may outlive its context.
+ * Freeing the index returns the block. */
 void rs_prefix_index_free(rs_prefix_index* idx);
 /* Rebuild a handle from its five tables (sizes as rs_prefix_index_tables),
  * so a caller that keeps only the tables (the C++ drop-in's PrefixIndex)
