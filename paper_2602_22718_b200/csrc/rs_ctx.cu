@@ -329,6 +329,18 @@ int rs_ctx_create(int device, rs_ctx** out) {
     return fail(RS_E_CUDA, "stream creation failed");
   }
   c->stream = c->own_stream;
+  if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaStreamDestroy(c->own_stream);
+    delete c;
+    return fail(RS_E_CUDA, "stream creation failed");
+  }
+  for (int i = 0; i < 2; ++i)
+    if (cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      rs_ctx_destroy(c);
+      return fail(RS_E_CUDA, "event creation failed");
+    }
   {  // stream-ordered temporaries (trace parsing) stay cached in the pool
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -362,6 +374,14 @@ int rs_ctx_destroy(rs_ctx* ctx) {
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->d_flags) cudaFree(ctx->d_flags);
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->ev_done[i]) cudaEventDestroy(ctx->ev_done[i]);
+    if (ctx->ev_copied[i]) cudaEventDestroy(ctx->ev_copied[i]);
+  }
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return RS_OK;

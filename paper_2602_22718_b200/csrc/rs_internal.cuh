@@ -120,6 +120,10 @@ struct rs_ctx {
   int* d_flags = nullptr;  // kernel status bits
   int* h_flags = nullptr;  // pinned mirror
   std::shared_ptr<rs::PinnedPool> pin_pool = std::make_shared<rs::PinnedPool>();
+  // Second stream for device-to-host result copies that overlap the next
+  // batch's kernels (the sweep), with per-buffer-set events.
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
   uint64_t launches = 0;
   bool timing = false;
   std::map<std::string, rs::KernelTimer> timers;

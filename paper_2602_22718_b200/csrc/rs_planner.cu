@@ -790,7 +790,9 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
     }
   }
   const int B = *std::max_element(sizes.begin(), sizes.end());
-  size_t need = (size_t)B * per_scen + fast_eval_bytes(dp, G) + abytes(B + 1, 8) +
+  // a second set of per-batch result buffers when host copies overlap
+  const size_t out_set = abytes((size_t)B * C, 8) * 3 + abytes(B, 4);
+  size_t need = (size_t)B * per_scen + out_set + fast_eval_bytes(dp, G) + abytes(B + 1, 8) +
                 abytes(2 * (RS_QTABLE_N + 1), 8) +
                 abytes(C, 8) * 2 + abytes(C, 4) + abytes(dp.c_hi - dp.c_lo + 1, 4) + (4 << 20);
   RS_TRY(arena_reserve(ctx, need));
@@ -804,11 +806,28 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
   double* agg_t = arena_alloc<double>(ctx, C);
   double* agg_c = arena_alloc<double>(ctx, C);
   int32_t* agg_h = arena_alloc<int32_t>(ctx, C);
-  double* b_tt = arena_alloc<double>(ctx, (size_t)B * C);
-  double* b_cc = arena_alloc<double>(ctx, (size_t)B * C);
-  int64_t* b_idle = arena_alloc<int64_t>(ctx, (size_t)B * C);
-  int32_t* b_ns = arena_alloc<int32_t>(ctx, B);
-  if (!b_ns) return fail(RS_E_NOMEM, "arena exhausted (sweep)");
+  // Host outputs of several batches: two buffer sets, each batch's results
+  // copied out on the context's copy stream while the next batch computes.
+  const bool overlap_out = !device_ptrs && sizes.size() > 1;
+  const int nsets = overlap_out ? 2 : 1;
+  double* b_tt[2] = {nullptr, nullptr};
+  double* b_cc[2] = {nullptr, nullptr};
+  int64_t* b_idle[2] = {nullptr, nullptr};
+  int32_t* b_ns[2] = {nullptr, nullptr};
+  for (int k = 0; k < nsets; ++k) {
+    b_tt[k] = arena_alloc<double>(ctx, (size_t)B * C);
+    b_cc[k] = arena_alloc<double>(ctx, (size_t)B * C);
+    b_idle[k] = arena_alloc<int64_t>(ctx, (size_t)B * C);
+    b_ns[k] = arena_alloc<int32_t>(ctx, B);
+    if (!b_ns[k]) return fail(RS_E_NOMEM, "arena exhausted (sweep)");
+  }
+  // every return below first drains the copies into the caller's buffers
+  struct CopyDrain {
+    cudaStream_t s;
+    ~CopyDrain() {
+      if (s) cudaStreamSynchronize(s);
+    }
+  } drain{overlap_out ? ctx->copy_stream : nullptr};
   const size_t mark = ctx->arena_used;  // per-batch structures live above
   {
     std::vector<int64_t> off(B + 1);
@@ -854,11 +873,14 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
       RS_TRY(build_batch(ctx, Sb, d_off, n, pred, plen, nullptr, nullptr, nullptr, allow_fast,
                          &built, true, false));
     }
-    double* o_tt = (device_ptrs && out->t_total) ? out->t_total + (size_t)s0 * C : b_tt;
-    double* o_cc = (device_ptrs && out->cost) ? out->cost + (size_t)s0 * C : b_cc;
-    int64_t* o_idle =
-        (device_ptrs && out->idle_slot_ticks) ? out->idle_slot_ticks + (size_t)s0 * C : b_idle;
-    int32_t* o_ns = (device_ptrs && out->n_star) ? out->n_star + s0 : b_ns;
+    const int set = overlap_out ? (int)(bi & 1) : 0;
+    // the copies out of this buffer set two batches ago must be done
+    if (overlap_out && bi >= 2) RS_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[set], 0));
+    double* o_tt = (device_ptrs && out->t_total) ? out->t_total + (size_t)s0 * C : b_tt[set];
+    double* o_cc = (device_ptrs && out->cost) ? out->cost + (size_t)s0 * C : b_cc[set];
+    int64_t* o_idle = (device_ptrs && out->idle_slot_ticks) ? out->idle_slot_ticks + (size_t)s0 * C
+                                                            : b_idle[set];
+    int32_t* o_ns = (device_ptrs && out->n_star) ? out->n_star + s0 : b_ns[set];
     LsFuse fuse{o_tt, o_cc, out->idle_slot_ticks ? o_idle : (int64_t*)nullptr, o_ns, dp.rho,
                 lambda, gpus};
     bool fused = false, fused_select = false;
@@ -874,13 +896,23 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
     RS_LAUNCH(ctx, "aggregate", aggregate_kernel, grid_for(ctx, (int64_t)C * 32, 256), 256, 0, Sb, C, n_min,
               o_tt, o_cc, o_ns, agg_t, agg_c, agg_h);
     if (!device_ptrs) {
-      if (out->t_total) RS_TRY(d2h(ctx, out->t_total + (size_t)s0 * C, o_tt, 8ull * Sb * C));
-      if (out->cost) RS_TRY(d2h(ctx, out->cost + (size_t)s0 * C, o_cc, 8ull * Sb * C));
+      // on the copy stream (overlapping the next batch), else in stream order
+      cudaStream_t cs = ctx->stream;
+      if (overlap_out) {
+        RS_CUDA_TRY(cudaEventRecord(ctx->ev_done[set], ctx->stream));
+        RS_CUDA_TRY(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_done[set], 0));
+        cs = ctx->copy_stream;
+      }
+      auto copy = [&](void* dst, const void* src, size_t bytes) -> int {
+        RS_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cs));
+        return RS_OK;
+      };
+      if (out->t_total) RS_TRY(copy(out->t_total + (size_t)s0 * C, o_tt, 8ull * Sb * C));
+      if (out->cost) RS_TRY(copy(out->cost + (size_t)s0 * C, o_cc, 8ull * Sb * C));
       if (out->idle_slot_ticks)
-        RS_TRY(d2h(ctx, out->idle_slot_ticks + (size_t)s0 * C, o_idle, 8ull * Sb * C));
-      if (out->n_star) RS_TRY(d2h(ctx, out->n_star + s0, o_ns, 4ull * Sb));
-      // no sync: the next batch's kernels reuse these buffers on the same
-      // stream, after the copies
+        RS_TRY(copy(out->idle_slot_ticks + (size_t)s0 * C, o_idle, 8ull * Sb * C));
+      if (out->n_star) RS_TRY(copy(out->n_star + s0, o_ns, 4ull * Sb));
+      if (overlap_out) RS_CUDA_TRY(cudaEventRecord(ctx->ev_copied[set], ctx->copy_stream));
     }
   }
   if (device_ptrs) {
@@ -892,6 +924,8 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
       RS_CUDA_TRY(cudaMemcpyAsync(out->nstar_hist, agg_h, 4 * C, cudaMemcpyDeviceToDevice, ctx->stream));
     return RS_OK;
   }
+  if (overlap_out)  // the final sync on the context stream covers every copy
+    for (int k = 0; k < 2; ++k) RS_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[k], 0));
   if (out->sum_t) RS_TRY(d2h(ctx, out->sum_t, agg_t, 8 * C));
   if (out->sum_c) RS_TRY(d2h(ctx, out->sum_c, agg_c, 8 * C));
   if (out->nstar_hist) RS_TRY(d2h(ctx, out->nstar_hist, agg_h, 4 * C));

@@ -83,6 +83,13 @@ def test_sweep_small_bitwise():
     check_sweep(c4_spec(12, count=3000, first=5), 1, 64)
 
 
+def test_sweep_multi_batch_host_outputs():
+    """More scenarios than one batch holds (<= 2,048): each batch's host
+    results leave on the copy stream while the next batch computes, through
+    two alternating buffer sets; every batch must land intact."""
+    check_sweep(c4_spec(4200, count=64, first=31), 1, 24)
+
+
 def test_sweep_arrays_bitwise_and_nmin():
     check_sweep(c4_spec(5, count=2048, first=100), 3, 50, arrays=True, lam=0.3, g=4)
 
