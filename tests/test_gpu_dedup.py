@@ -121,6 +121,25 @@ def test_long_prompts_multi_chunk_tables():
     assert idx.max_prompt_len() > 4096
 
 
+def test_prompts_longer_than_the_histogram_bound():
+    """Prompts longer than the first pass's histogram bound (16,384 tokens):
+    the build sees the longest prompt in its stats and reruns once with exact
+    arrays, taking a larger pinned table block; a short batch built next
+    (smaller block from the pool) is exact too."""
+    rng = np.random.RandomState(8)
+    head = rng.randint(0, 5, size=30000).tolist()
+    seqs = [head[:rng.randint(1, len(head) + 1)] + rng.randint(0, 3, size=rng.randint(0, 6000)).tolist()
+            for _ in range(24)]
+    seqs.append(head + [1] * 5000)
+    idx, _, _ = check_batch(seqs)
+    assert idx.max_prompt_len() > 16384
+    check_batch([[1, 2, 3], [1, 2, 4], [9]])
+    tok, off = csr(seqs)
+    for l in (16384, 20000, 40000):  # the subset count and the map rerun the same way
+        assert rs.unique_prefix_count_among(seqs, l) == port().unique_prefix_count_among(tok, off, l)
+        assert rs.dedup_map(seqs, l).tolist() == port().dedup_map(tok, off, l).tolist()
+
+
 def test_repeated_builds_identical():
     """The refinement runs its rounds in one persistent launch with grid-wide
     barriers and rotating counters; a race there shows up as a build that
