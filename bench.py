@@ -37,6 +37,14 @@ METRIC = "scenario×candidate evals/sec (scaling sweep)"
 EVAL_BYTES = 65536 * 12 + 16  # P*(8 B pred + 4 B plen) + 16 B out
 
 
+def _profile_traffic(key):
+    """ncu DRAM read + write per launch of a kernel (profiles/traffic.json), or None."""
+    tf = REPO / "profiles" / "traffic.json"
+    if not tf.exists():
+        return None
+    return json.loads(tf.read_text()).get(key)
+
+
 def peaks():
     p = REPO / "MEASURED_PEAKS.json"
     if p.exists():
@@ -337,12 +345,9 @@ def run_ours(args, world, rank, local):
     ge_avg_ms = ge_ms / max(ge_n, 1)
     per_launch_evals = total_evals / world * args.steps / max(ge_n, 1)
     achieved = per_launch_evals * EVAL_BYTES / (ge_avg_ms / 1e3) / 1e9
-    traffic = None  # ncu dram read+write per launch (profiles/traffic.json, per eval x evals)
-    tf = REPO / "profiles" / "traffic.json"
-    if tf.exists():
-        bpe = json.loads(tf.read_text()).get("group_eval_dram_bytes_per_eval")
-        if bpe:
-            traffic = bpe * per_launch_evals
+    # ncu dram read+write per launch (profiles/traffic.json: per eval x evals per launch)
+    bpe = _profile_traffic("group_eval_dram_bytes_per_eval")
+    traffic = bpe * per_launch_evals if bpe else None
     result = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -421,7 +426,9 @@ def bench_trace(args, ctx, torch, dev):
            "e2e": {"value": n_tok / host_s, "unit": "tokens/s", "h2d_bytes_per_step": int(text.nbytes),
                    "d2h_bytes_per_step": 0},
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                        "frac": achieved / peak, "traffic": None, "kernel": top,
+                        "frac": achieved / peak, "kernel": top,
+                        "traffic": (_profile_traffic("trace_tokens_dram_bytes_per_launch")
+                                    if top == "trace_tokens" else None),
                         "launch_ms": kt[top], "kernel_ms": kt}}
     if not args.no_cpu:
         from oracle_lib import ref
@@ -530,7 +537,8 @@ def bench_dedup(args, ctx, torch, dev, stream):
         "e2e": {"value": n_tok / host_s, "unit": "tokens/s", "h2d_bytes_per_step": n_tok * 4 + off.nbytes,
                 "d2h_bytes_per_step": 5 * 8 * 2562},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": "dedup_compare_r0 (round 0, streaming)",
+                     "frac": achieved / peak, "traffic": _profile_traffic("dedup_compare_r0_dram_bytes_per_launch"),
+                     "kernel": "dedup_compare_r0 (round 0, streaming)",
                      "launch_ms": r0_ms, "kernel_share_of_step": r0_ms / (dev_s * 1e3)},
         # the whole build call (host wall clock) against the same roofline:
         # SURVEY §8d's 4 B per token read once
