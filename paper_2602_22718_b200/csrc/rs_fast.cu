@@ -1080,7 +1080,7 @@ struct LsArgs {
   int S;
   int cand_units;  // units per scenario (candidate slices of kLsThreads)
   double* gt;
-  const int4* gtab;      // per (scenario, flat group): see group_table_kernel
+  const uint2* gtab;     // per (scenario, flat group): see group_table_kernel
   const double* gfirst;  // per (scenario, flat group): value after the first run
 };
 
@@ -1113,12 +1113,13 @@ __device__ __forceinline__ int ls_range(const LsView& V, int l, int r) {
   return m;
 }
 
-// Per group (scenario, N, g): {ka, kb, va | vb << 16, smb} and the value of
+// Per group (scenario, N, g): {ka | kb << 16, va | smb << 16} (each field
+// 16 bits: segment indices < kMaxSeg, maxima of 16-bit prompt lengths) and the value of
 // its first run (k = kb: whole group live, base = max prompt_len of the
 // group, ticks 1 .. F_kb), i.e. the group's total after one run. The first
 // run spans the longest context range (often several knot pieces), so it is
 // evaluated here in parallel rather than inside the lockstep walk.
-__global__ void group_table_kernel(FastSS ss, FastProf fp, CandRange cr, int S, int4* gtab,
+__global__ void group_table_kernel(FastSS ss, FastProf fp, CandRange cr, int S, uint2* gtab,
                                    double* gfirst) {
   const int64_t total = (int64_t)S * cr.T;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
@@ -1146,7 +1147,7 @@ __global__ void group_table_kernel(FastSS ss, FastProf fp, CandRange cr, int S, 
       smb = (int)(__ldg(V.pmsm + ka + 1) >> 16);
     }
     const int f = ss.seg[so + kb].x & 0xffff;
-    gtab[t] = make_int4(ka, kb, va | (vb << 16), smb);
+    gtab[t] = make_uint2((uint32_t)ka | ((uint32_t)kb << 16), (uint32_t)va | ((uint32_t)smb << 16));
     // run_sum(G * (b - a), top_m, top_m + f - 1) from the halved tables
     // (piece terms and their order as tpot_context_run_sum; 0.0 + x == x)
     const int clo = fp.c_lo, chi = fp.c_hi, clo1 = fp.c_lo - 1;
@@ -1172,7 +1173,7 @@ __global__ void group_table_kernel(FastSS ss, FastProf fp, CandRange cr, int S, 
 // table; n_star comes from block reductions with the reference's min/max and
 // first-strict-minimum semantics (planner.cpp:196-217).
 __global__ void __launch_bounds__(kLsThreads)
-fast_finish_kernel(FastSS ss, CandRange cr, const double* gt_all, const int4* gtab_all,
+fast_finish_kernel(FastSS ss, CandRange cr, const double* gt_all, const uint2* gtab_all,
                    LsEpilogue ep) {
   __shared__ double r_d[4][kLsThreads / 32];
   __shared__ int r_i[kLsThreads / 32];
@@ -1210,12 +1211,12 @@ fast_finish_kernel(FastSS ss, CandRange cr, const double* gt_all, const int4* gt
       const int64_t i0 = ss.item_off[s], so = i0 + s;
       const int P = (int)(ss.item_off[s + 1] - i0);
       const int D = ss.nseg[s];
-      const int4* gtab = gtab_all + gbase;
+      const uint2* gtab = gtab_all + gbase;
       const int q = P / N, rem = P % N;
       int64_t acc = 0;
       for (int h = 0; h < N; ++h) {
         const int size = q + (h < rem ? 1 : 0);
-        if (size > 0) acc += (int64_t)size * (__ldg(&ss.seg[so + __ldg(&gtab[h].x)].x) & 0xffff);
+        if (size > 0) acc += (int64_t)size * (__ldg(&ss.seg[so + (__ldg(&gtab[h].x) & 0xffffu)].x) & 0xffff);
       }
       ep.idle[o] = (acc - ss.segCF[so + D]) * cr.G;
     }
@@ -1313,7 +1314,7 @@ __global__ void __launch_bounds__(kLsThreads, kMinB) lockstep_eval_kernel(LsArgs
              A.ss.bq + (size_t)((so >> 4) + s) * kBlkPairs};
     const int64_t gbase = (int64_t)s * A.cr.T + (tri64(N) - flat0);
     double* gt = A.gt + gbase;
-    const int4* gtab = A.gtab + gbase;
+    const uint2* gtab = A.gtab + gbase;
     const double* gfirst = A.gfirst + gbase;
     const int q = P / N, rem = P % N;
     // Current group (g, counting down from N-1). Its first run (k = kb) is
@@ -1322,15 +1323,15 @@ __global__ void __launch_bounds__(kLsThreads, kMinB) lockstep_eval_kernel(LsArgs
     int smb = 0, cjr = -1, cbase = 0;
     double total = 0.0;
     bool done = !on;
-    int4 nxt = make_int4(0, 0, 0, 0);
+    uint2 nxt = make_uint2(0u, 0u);
     double nfirst = 0.0;
-    auto enter = [&](int4 e, double first) {  // start group g
+    auto enter = [&](uint2 e, double first) {  // start group g
       a = g * q + min(g, rem);
       b = a + q + (g < rem ? 1 : 0);
-      ka = e.x;
-      kb = e.y;
-      va = e.z & 0xffff;
-      smb = e.w;
+      ka = (int)(e.x & 0xffffu);
+      kb = (int)(e.x >> 16);
+      va = (int)(e.y & 0xffffu);
+      smb = (int)(e.y >> 16);
       l = ka + 1;
       jl = l >> 4;
       cjr = -1;
@@ -1437,7 +1438,7 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
   FastProf fp;
   if (int st = fast_prof_make(ctx, prof, cr.G, &fp)) return st;
   const int C = cr.n_max - cr.n_min + 1;
-  int4* gtab = arena_alloc<int4>(ctx, (size_t)S * cr.T);
+  uint2* gtab = arena_alloc<uint2>(ctx, (size_t)S * cr.T);
   double* gfirst = arena_alloc<double>(ctx, (size_t)S * cr.T);
   if (!gtab || !gfirst) return fail(RS_E_NOMEM, "arena exhausted (group table)");
   {
