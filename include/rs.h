@@ -17,7 +17,11 @@
  *    stream is synchronised before return. `*_device` entry points take
  *    device pointers and are asynchronous on the context stream.
  *  - Caller owns every buffer it passes. Opaque handles are freed with the
- *    matching *_free / *_destroy call.
+ *    matching *_free / *_destroy call. Index and trace handles may outlive
+ *    the context that built them.
+ *  - Every entry point taking a context runs on the context's device and
+ *    restores the caller's current device before returning, so contexts of
+ *    several GPUs can be driven from one host thread.
  *  - There is no CPU fallback: without a usable CUDA device every compute
  *    entry point fails with RS_E_CUDA.
  */
@@ -56,7 +60,8 @@ typedef struct rs_ctx rs_ctx;
 int rs_ctx_create(int device, rs_ctx** out);
 int rs_ctx_destroy(rs_ctx* ctx);
 /* Use a caller stream (e.g. torch.cuda.current_stream().cuda_stream). NULL
- * restores the context's own stream. */
+ * restores the context's own stream. Work queued on the previous stream is
+ * waited for first (it may still use the context's scratch). */
 int rs_ctx_set_stream(rs_ctx* ctx, void* cuda_stream);
 int rs_ctx_synchronize(rs_ctx* ctx);
 /* Number of kernels this context has launched since creation. */
@@ -106,8 +111,10 @@ int rs_prefix_index_build_device(rs_ctx* ctx, const int32_t* d_tokens,
  * tables land in d_tables (5 consecutive int64 arrays of max_len_cap+2
  * entries: nodes_at_depth, short_count_below, short_tokens_below,
  * longer_count_from, longer_tokens_from) and d_info receives
- * {batch, min_len, max_len, total_tokens, status}. max_len_cap must be >=
- * the longest prompt; status != 0 flags a validation failure. */
+ * {batch, min_len, max_len, total_tokens, 0}. max_len_cap must be >=
+ * the longest prompt. Validation errors (an empty prompt) are returned by the
+ * call itself (RS_E_VALIDATION) after its synchronisation; d_info[4] is
+ * always written as 0 and kept only for layout compatibility. */
 int rs_prefix_index_build_device_async(rs_ctx* ctx, const int32_t* d_tokens,
                                        const int64_t* d_offsets, int32_t batch,
                                        int32_t max_len_cap, int64_t* d_tables,
@@ -372,13 +379,19 @@ typedef struct rs_sweep_out {
 } rs_sweep_out;
 
 /* Sweep over generated scenarios. device_ptrs != 0: every out pointer is a
- * device pointer and the call is asynchronous on the context stream. */
+ * device pointer. Both forms return once every result is written (the call
+ * reads the device status once at the end: a scenario the bucketed fast path
+ * cannot take reruns the sweep on the generic path). Host outputs may be
+ * pageable (staged through pinned bounce buffers) or pinned (written
+ * directly, overlapping the next batch's kernels). */
 int rs_sweep(rs_ctx* ctx, const rs_scenario_spec* spec,
              const rs_profile* profile, int32_t responses_per_prompt,
              int32_t n_min, int32_t n_max, double lambda,
              int32_t gpus_per_actor, rs_sweep_out* out, int device_ptrs);
 
-/* Sweep over caller scenarios (pred/prompt_len: S*count, id_rank = index). */
+/* Sweep over caller scenarios (pred/prompt_len: S*count, id_rank = index).
+ * Host inputs stream in batch by batch on a separate copy stream while the
+ * previous batch computes (pinned inputs copy fully asynchronously). */
 int rs_sweep_arrays(rs_ctx* ctx, const double* pred, const int32_t* prompt_len,
                     int32_t n_scenarios, int32_t count,
                     const rs_profile* profile, int32_t responses_per_prompt,

@@ -135,8 +135,13 @@ int flags_to_status(int flags) {
     return fail(RS_E_VALIDATION, "predicted length is not finite");
   if (flags & kFlagTargetBelowOne)
     return fail(RS_E_VALIDATION, "integrate_decode_seconds: target length < 1");
+  if (flags & kFlagBadPerm)
+    return fail(RS_E_ARG, "id_rank is not a permutation of [0, count)");
   if (flags & kFlagWorkOverflow)
     return fail(RS_E_CUDA, "internal work capacity exceeded");
+  if (flags & (kFlagBucketOverflow | kFlagBucketTooWide))
+    return fail(RS_E_CUDA, "internal: fast scenario structure not applicable (unhandled fallback)");
+  if (flags) return fail(RS_E_CUDA, "internal: unhandled device status flags " + std::to_string(flags));
   return RS_OK;
 }
 
@@ -316,7 +321,7 @@ int rs_ctx_create(int device, rs_ctx** out) {
     return fail(RS_E_CUDA, "no CUDA device available (librs_b200 has no CPU fallback)");
   }
   if (device < 0 || device >= n) return fail(RS_E_ARG, "bad device index");
-  RS_CUDA_TRY(cudaSetDevice(device));
+  ::rs::DeviceGuard guard(device);  // the caller's current device is restored on return
   cudaDeviceProp prop;
   RS_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   if (prop.major < 10)
@@ -334,9 +339,16 @@ int rs_ctx_create(int device, rs_ctx** out) {
     delete c;
     return fail(RS_E_CUDA, "stream creation failed");
   }
+  if (cudaStreamCreateWithFlags(&c->in_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    rs_ctx_destroy(c);
+    return fail(RS_E_CUDA, "stream creation failed");
+  }
   for (int i = 0; i < 2; ++i)
     if (cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_inused[i], cudaEventDisableTiming) != cudaSuccess) {
       cudaGetLastError();
       rs_ctx_destroy(c);
       return fail(RS_E_CUDA, "event creation failed");
@@ -360,8 +372,8 @@ int rs_ctx_create(int device, rs_ctx** out) {
 }
 
 int rs_ctx_destroy(rs_ctx* ctx) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx) return RS_OK;
-  cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (auto& p : ctx->pending) {
     cudaEventDestroy(p.a);
@@ -374,26 +386,32 @@ int rs_ctx_destroy(rs_ctx* ctx) {
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->d_flags) cudaFree(ctx->d_flags);
   if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
-  if (ctx->copy_stream) {
-    cudaStreamSynchronize(ctx->copy_stream);
-    cudaStreamDestroy(ctx->copy_stream);
-  }
-  for (int i = 0; i < 2; ++i) {
-    if (ctx->ev_done[i]) cudaEventDestroy(ctx->ev_done[i]);
-    if (ctx->ev_copied[i]) cudaEventDestroy(ctx->ev_copied[i]);
-  }
+  for (cudaStream_t s : {ctx->copy_stream, ctx->in_stream})
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  if (ctx->bounce) cudaFreeHost(ctx->bounce);
+  for (int i = 0; i < 2; ++i)
+    for (cudaEvent_t e : {ctx->ev_done[i], ctx->ev_copied[i], ctx->ev_in[i], ctx->ev_inused[i]})
+      if (e) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return RS_OK;
 }
 
 int rs_ctx_set_stream(rs_ctx* ctx, void* stream) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx) return fail(RS_E_ARG, "ctx is NULL");
-  ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+  cudaStream_t next = stream ? (cudaStream_t)stream : ctx->own_stream;
+  // work still queued on the old stream may use the arena / input buffers
+  if (next != ctx->stream) RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  ctx->stream = next;
   return RS_OK;
 }
 
 int rs_ctx_synchronize(rs_ctx* ctx) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx) return fail(RS_E_ARG, "ctx is NULL");
   RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   if (ctx->timing) RS_TRY(collect_timers(ctx));
@@ -401,18 +419,21 @@ int rs_ctx_synchronize(rs_ctx* ctx) {
 }
 
 int rs_ctx_kernel_launches(const rs_ctx* ctx, uint64_t* count) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !count) return fail(RS_E_ARG, "NULL argument");
   *count = ctx->launches;
   return RS_OK;
 }
 
 int rs_ctx_enable_kernel_timing(rs_ctx* ctx, int enable) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx) return fail(RS_E_ARG, "ctx is NULL");
   ctx->timing = enable != 0;
   return RS_OK;
 }
 
 int rs_ctx_reset_kernel_timing(rs_ctx* ctx) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx) return fail(RS_E_ARG, "ctx is NULL");
   RS_TRY(collect_timers(ctx));
   ctx->timers.clear();
@@ -421,6 +442,7 @@ int rs_ctx_reset_kernel_timing(rs_ctx* ctx) {
 
 int rs_ctx_kernel_time(rs_ctx* ctx, const char* name, double* total_ms,
                        uint64_t* launches) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !name) return fail(RS_E_ARG, "NULL argument");
   RS_TRY(collect_timers(ctx));
   auto it = ctx->timers.find(name);
@@ -431,6 +453,7 @@ int rs_ctx_kernel_time(rs_ctx* ctx, const char* name, double* total_ms,
 
 int rs_tpot_seconds(rs_ctx* ctx, const rs_profile* profile, const double* b,
                     const double* c, int64_t n, double* out) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx) return fail(RS_E_ARG, "ctx is NULL");
   if (n <= 0) return RS_OK;
   DevProfile dp;

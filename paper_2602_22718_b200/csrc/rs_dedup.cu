@@ -768,7 +768,7 @@ uint32_t pow2_at_least(int64_t v) {
 }  // namespace
 
 static int launch_refine(rs_ctx* ctx, DedupState st, int* kc, unsigned long long* bar) {
-  static int per_sm = 0;
+  int& per_sm = ctx->dev_cache.refine_per_sm;  // per device: the context's
   if (!per_sm) {
     RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, 256, 0));
     per_sm = std::max(1, std::min(per_sm, 4));
@@ -801,8 +801,8 @@ struct RefineTail {
   virtual void finish(rs_ctx* ctx) = 0;  // after the final synchronisation
 };
 
-static int tables_setup() {
-  static bool done = false;
+static int tables_setup(rs_ctx* ctx) {
+  bool& done = ctx->dev_cache.tables_ready;
   if (!done) {
     RS_CUDA_TRY(cudaFuncSetAttribute(tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTabSmem));
     done = true;
@@ -810,8 +810,8 @@ static int tables_setup() {
   return RS_OK;
 }
 
-static int stream_kernel_setup(int* blocks_per_sm) {
-  static int per_sm = 0;
+static int stream_kernel_setup(rs_ctx* ctx, int* blocks_per_sm) {
+  int& per_sm = ctx->dev_cache.stream_per_sm;
   if (!per_sm) {
     RS_CUDA_TRY(cudaFuncSetAttribute(compare_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kStreamSmem));
@@ -833,7 +833,7 @@ static int dedup_refine(rs_ctx* ctx, const int32_t* d_tok, const int64_t* d_off,
   int64_t maxd = std::max<int64_t>(max_len_hint, 16384);
   maxd = std::max<int64_t>(1, std::min<int64_t>(maxd, cap_len));
   int per_sm = 1;
-  RS_TRY(stream_kernel_setup(&per_sm));
+  RS_TRY(stream_kernel_setup(ctx, &per_sm));
   DedupState st{};
   int64_t hs[4];
   for (int attempt = 0; attempt < 2; ++attempt) {
@@ -951,7 +951,7 @@ static int build_index_device(rs_ctx* ctx, const int32_t* d_tok, const int64_t* 
         if (!idx->blk) return fail(RS_E_NOMEM, "pinned allocation failed");
       }
       int64_t* pin = reinterpret_cast<int64_t*>(c->pinned);
-      RS_TRY(tables_setup());
+      RS_TRY(tables_setup(c));
       RS_LAUNCH(c, "dedup_tables", tables_kernel, kTabCtas, kTabT, kTabSmem, st, -1, cap_md,
                 static_cast<int64_t*>(idx->blk), pin + kStatsOff);
       return RS_OK;
@@ -1067,6 +1067,7 @@ extern "C" {
 
 int rs_prefix_index_build(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets,
                           int32_t batch, rs_prefix_index** out) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !out) return fail(RS_E_ARG, "NULL argument");
   *out = nullptr;
   if (batch <= 0) return fail(RS_E_VALIDATION, "prefix index needs a non-empty batch");
@@ -1080,6 +1081,7 @@ int rs_prefix_index_build(rs_ctx* ctx, const int32_t* tokens, const int64_t* off
 
 int rs_prefix_index_build_device(rs_ctx* ctx, const int32_t* d_tokens, const int64_t* d_offsets,
                                  int32_t batch, rs_prefix_index** out) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !out) return fail(RS_E_ARG, "NULL argument");
   *out = nullptr;
   return build_index_device(ctx, d_tokens, d_offsets, batch, out);
@@ -1088,6 +1090,7 @@ int rs_prefix_index_build_device(rs_ctx* ctx, const int32_t* d_tokens, const int
 int rs_prefix_index_build_device_async(rs_ctx* ctx, const int32_t* d_tokens,
                                        const int64_t* d_offsets, int32_t batch,
                                        int32_t max_len_cap, int64_t* d_tables, int64_t* d_info) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !d_tables || !d_info) return fail(RS_E_ARG, "NULL argument");
   if (batch <= 0) return fail(RS_E_VALIDATION, "prefix index needs a non-empty batch");
   DedupState st;
@@ -1095,7 +1098,7 @@ int rs_prefix_index_build_device_async(rs_ctx* ctx, const int32_t* d_tokens,
   RS_TRY(dedup_refine(ctx, d_tokens, d_offsets, batch, INT32_MAX, 1, false, max_len_cap, &st,
                       stats, nullptr));
   if (stats[1] > max_len_cap) return fail(RS_E_ARG, "max_len_cap below the longest prompt");
-  RS_TRY(tables_setup());
+  RS_TRY(tables_setup(ctx));
   RS_LAUNCH(ctx, "dedup_tables", tables_kernel, kTabCtas, kTabT, kTabSmem, st, max_len_cap, max_len_cap, d_tables,
             nullptr);
   int64_t info[5] = {batch, stats[0], stats[1], stats[2], 0};
@@ -1222,6 +1225,7 @@ int rs_dedup_savings(const rs_prefix_index* idx, int32_t l_star, int32_t g, int6
 
 int rs_unique_prefix_count_among(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets,
                                  int32_t count, int32_t prefix_len, int64_t* out) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !out) return fail(RS_E_ARG, "NULL argument");
   if (prefix_len < 1)
     return fail(RS_E_VALIDATION, "unique_prefix_count_among: prefix_len must be >= 1");
@@ -1241,6 +1245,7 @@ int rs_unique_prefix_count_among(rs_ctx* ctx, const int32_t* tokens, const int64
 
 int rs_dedup_map(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets, int32_t count,
                  int32_t prefix_len, int32_t* labels) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !labels) return fail(RS_E_ARG, "NULL argument");
   if (prefix_len < 1) return fail(RS_E_VALIDATION, "dedup_map: prefix_len must be >= 1");
   if (count <= 0) return RS_OK;
@@ -1254,6 +1259,7 @@ int rs_dedup_map(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets, int
 
 int rs_block_hashes(rs_ctx* ctx, const int32_t* tokens, const int64_t* offsets, int32_t count,
                     int32_t K, uint64_t* hashes) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !hashes) return fail(RS_E_ARG, "NULL argument");
   if (K < 4 || K > 128 || (K & (K - 1)))
     return fail(RS_E_CONFIG, "block_hashes: block_tokens must be a power of two in [4, 128]");

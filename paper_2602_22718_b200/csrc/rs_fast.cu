@@ -40,6 +40,7 @@ size_t fast_ss_bytes(int64_t items, int S) {
 FastSS fast_ss_alloc(rs_ctx* ctx, const int64_t* d_off, int64_t items, int S) {
   int64_t segs = items + S;
   FastSS f;
+  f.flags = ctx->d_flags;
   f.item_off = d_off;
   f.seg = arena_alloc<int2>(ctx, segs);
   f.segCF = arena_alloc<int64_t>(ctx, segs);
@@ -749,6 +750,7 @@ __global__ void __launch_bounds__(kEvalT, 1) fast_eval_kernel(EvalArgs A) {
     fp.top = sh.top;
     fp.pex = sh.pex;
   }
+  if (*A.ss.flags & kFastBad) return;
   uint16_t* lbuf = sh.lbuf[tid];
   const int C = A.cr.n_max - A.cr.n_min + 1;
   const int n_units = A.S * A.units;
@@ -1121,6 +1123,7 @@ __device__ __forceinline__ int ls_range(const LsView& V, int l, int r) {
 // evaluated here in parallel rather than inside the lockstep walk.
 __global__ void group_table_kernel(FastSS ss, FastProf fp, CandRange cr, int S, uint2* gtab,
                                    double* gfirst) {
+  if (*ss.flags & kFastBad) return;
   const int64_t total = (int64_t)S * cr.T;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -1177,6 +1180,7 @@ fast_finish_kernel(FastSS ss, CandRange cr, const double* gt_all, const uint2* g
                    LsEpilogue ep) {
   __shared__ double r_d[4][kLsThreads / 32];
   __shared__ int r_i[kLsThreads / 32];
+  if (*ss.flags & kFastBad) return;
   const int C = cr.n_max - cr.n_min + 1;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int s = blockIdx.x, c = threadIdx.x;
@@ -1282,6 +1286,7 @@ fast_finish_kernel(FastSS ss, CandRange cr, const double* gt_all, const uint2* g
 template <int kMinB>
 __global__ void __launch_bounds__(kLsThreads, kMinB) lockstep_eval_kernel(LsArgs A) {
   extern __shared__ __align__(16) unsigned char ls_smem[];
+  if (*A.ss.flags & kFastBad) return;
   const FastProf& fp0 = A.fp;
   double* s_tail = reinterpret_cast<double*>(ls_smem);
   uint16_t* s_pex = reinterpret_cast<uint16_t*>(s_tail + fp0.live_top);
@@ -1502,6 +1507,7 @@ bool lockstep_fuses_select(CandRange cr) { return cr.n_max - cr.n_min + 1 <= kLs
 __global__ void fast_reduce_kernel(FastSS ss, int S, CandRange cr, double rho, int gpus,
                                    const double* gt, double* t_total, double* cost,
                                    int64_t* idle) {
+  if (*ss.flags & kFastBad) return;
   const int C = cr.n_max - cr.n_min + 1;
   const int64_t total = (int64_t)S * C;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;

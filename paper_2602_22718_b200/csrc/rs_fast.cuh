@@ -13,6 +13,7 @@ namespace rs {
 //   rinfo[r] = {seg_of(r), smx(r) | pmx(r) << 16} with smx / pmx the max
 //              prompt_len from r to the end / from the start of r's segment
 struct FastSS {
+  const int* flags;  // the context's status word: kFastBad set -> structure unusable
   const int64_t* item_off;
   int2* seg;
   int64_t* segCF;
@@ -36,8 +37,8 @@ static_assert(kBlkPairs % 4 == 0, "bq rows are written as 64-bit words");
 __host__ __device__ constexpr int blk_pair(int i, int j) { return i * (2 * kBlk + 1 - i) / 2 + (j - i); }
 constexpr int kMaxSeg = kFastFmax; // D <= Fmax
 constexpr int kTopCap = 4096;      // smem tpot row entries
-constexpr int kCoopN = 4;
-constexpr int kLsDenseCtas = 5;   // CTAs per SM of the register-capped lockstep build          // N < kCoopN: warp-cooperative groups
+constexpr int kCoopN = 4;         // N < kCoopN: warp-cooperative groups
+constexpr int kLsDenseCtas = 5;   // CTAs per SM of the register-capped lockstep build
 constexpr int kStBlocks = kMaxSeg / kBlk;  // 1024
 constexpr int kStLevels = 11;              // floor(log2(1024)) + 1
 constexpr int kStStride = kStBlocks * kStLevels;

@@ -52,7 +52,12 @@ enum : int {
   kFlagBucketTooWide = 8,    // a finish bucket too wide for in-warp sort
   kFlagEmptyPrompt = 16,     // prefix index: prompt of length < 1
   kFlagWorkOverflow = 32,    // dedup refinement exceeded its work capacity
+  kFlagBadPerm = 64,         // id_rank is not a permutation of [0, count)
 };
+// Flags after which the fast scenario structure is not usable: every kernel
+// that reads it returns at once (the host reruns the batch on the generic path
+// or reports the validation error).
+constexpr int kFastBad = kFlagBucketOverflow | kFlagBucketTooWide | kFlagNotFinite;
 
 // -------------------------------------------------------------- profile --
 // Device view of a LatencyProfile. tpot(b, c) is only ever evaluated at
@@ -124,6 +129,13 @@ struct rs_ctx {
   // batch's kernels (the sweep), with per-buffer-set events.
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_done[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
+  // Third stream for host-to-device input copies of the next batch (the
+  // sweep over caller arrays), with per-input-set events.
+  cudaStream_t in_stream = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_inused[2] = {nullptr, nullptr};
+  // Pinned bounce buffers for results bound for pageable caller memory.
+  char* bounce = nullptr;
+  size_t bounce_cap = 0;
   uint64_t launches = 0;
   bool timing = false;
   std::map<std::string, rs::KernelTimer> timers;
@@ -135,6 +147,12 @@ struct rs_ctx {
   std::vector<cudaEvent_t> event_pool;
   std::vector<rs::ProfileCache> profiles;
   int num_sms = 148;
+  // Kernel attributes / occupancy are per device: cached on the context
+  // (one context per device), set under its device guard.
+  struct {
+    int refine_per_sm = 0, stream_per_sm = 0;
+    bool tables_ready = false;
+  } dev_cache;
   // Grow-only device copy of host inputs (CSR token batches), kept apart
   // from the arena, which may grow during a call.
   char* in_buf = nullptr;
@@ -178,6 +196,24 @@ int collect_timers(rs_ctx* ctx);
                                        cudaGetErrorString(le_));            \
     ::rs::timer_end((ctx), (name), ev_a_);                                  \
   } while (0)
+
+// Every entry point that takes a context runs on the context's device: the
+// guard makes it current and restores the caller's device on return.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const rs_ctx* c) : DeviceGuard(c ? c->device : -1) {}
+  explicit DeviceGuard(int device) {
+    int cur = -1;
+    if (device >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != device &&
+        cudaSetDevice(device) == cudaSuccess)
+      prev = cur;
+    cudaGetLastError();
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+#define RS_DEVICE_GUARD(ctx) ::rs::DeviceGuard rs_device_guard_(ctx)
 
 // Synchronise the context stream and translate kernel status flags.
 int sync_and_check(rs_ctx* ctx);

@@ -429,10 +429,10 @@ __global__ void to_id_order_kernel(const double* pred, const int32_t* plen,
     double p = pred[i];
     int64_t j = id_rank ? id_rank[i] : i;
     if (j < 0 || j >= n) {
-      atomicOr(flags, kFlagWorkOverflow << 1);
+      atomicOr(flags, kFlagBadPerm);
       continue;
     }
-    if (seen && atomicAdd(seen + j, 1) != 0) atomicOr(flags, kFlagWorkOverflow << 1);
+    if (seen && atomicAdd(seen + j, 1) != 0) atomicOr(flags, kFlagBadPerm);
     if (!isfinite(p)) atomicOr(flags, kFlagNotFinite);
     else if (require_ge1 && p < 1.0) atomicOr(flags, kFlagTargetBelowOne);
     pred_o[j] = p == 0.0 ? 0.0 : p;  // -0.0 == +0.0 in the reference order
@@ -608,16 +608,20 @@ static size_t built_bytes(int64_t n, int S, bool with_generic) {
 
 
 // pred / plen: id-ordered device arrays (written by the generator when gen).
+// defer: the fast build's status is not read here — the kernels that read the
+// structure skip themselves on kFastBad and the sweep driver checks the flags
+// (and reruns on the generic path) once per sweep; otherwise the flags are
+// read at once and an inapplicable fast build falls back to the generic one.
 static int build_batch(rs_ctx* ctx, int S, const int64_t* d_off, int64_t n, double* pred,
                        int32_t* plen, const GenSpec* gen, const double* nz, const double* lnz,
                        bool allow_fast, Built* out, bool keep_inputs = true,
-                       bool need_order = true) {
+                       bool need_order = true, bool defer = false) {
   if (allow_fast) {
     out->fss = fast_ss_alloc(ctx, d_off, n, S);
     if (!out->fss.rec) return fail(RS_E_NOMEM, "arena exhausted (fast structure)");
-    RS_TRY(clear_flags(ctx));
+    if (!defer) RS_TRY(clear_flags(ctx));
     RS_TRY(fast_build(ctx, S, d_off, pred, plen, out->fss, gen, nz, lnz, keep_inputs, need_order));
-    if (gen) {  // in range by construction (fast_spec_ok)
+    if (defer) {
       out->fast = true;
       return RS_OK;
     }
@@ -756,21 +760,55 @@ static void plan_batches(int S, int Bmem, int cmax, int nsm, std::vector<int>* s
   }
 }
 
-// Shared sweep driver: scenarios either generated (spec) or from arrays.
-static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h_pred,
-                      const int32_t* h_plen, int S, int P, const rs_profile* profile, int G,
+// True when p is page-locked (cudaMallocHost / cudaHostRegister) host memory:
+// device-to-host copies into it are asynchronous; pageable memory goes
+// through the context's pinned bounce buffers instead.
+static bool host_pinned(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+static int bounce_reserve(rs_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->bounce_cap) return RS_OK;
+  RS_CUDA_TRY(cudaStreamSynchronize(ctx->copy_stream));
+  if (ctx->bounce) cudaFreeHost(ctx->bounce);
+  ctx->bounce = nullptr;
+  ctx->bounce_cap = 0;
+  if (cudaMallocHost(&ctx->bounce, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(RS_E_NOMEM, "pinned bounce allocation failed");
+  }
+  ctx->bounce_cap = bytes;
+  return RS_OK;
+}
+
+// One pass of the sweep. allow_fast_in = false forces the generic structure
+// (radix sort) for every batch. *redo is set when a fast structure turned out
+// not to apply (a finish tick outside [1, 16384], a prompt_len outside
+// [0, 65535] or a finish bucket wider than the in-CTA sort): the caller then
+// reruns the whole sweep on the generic path. The status flags are read after
+// the first batch (so such a rerun wastes one batch at most) and at the end;
+// in between, the kernels that read a fast structure skip themselves when
+// the flags say it is unusable (kFastBad), so stale scratch is never indexed.
+static int sweep_pass(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h_pred,
+                      const int32_t* h_plen, int S, int P, const DevProfile& dp, int G,
                       int n_min, int n_max, double lambda, int gpus, rs_sweep_out* out,
-                      int device_ptrs) {
-  RS_TRY(check_scale_args(P, G, n_min, n_max, lambda));
-  DevProfile dp;
-  RS_TRY(get_profile(ctx, profile, &dp));
+                      int device_ptrs, bool allow_fast_in, bool* redo) {
+  *redo = false;
   const int C = n_max - n_min + 1;
   const int64_t T = groups_per_scenario(n_min, n_max);
   const bool generated = spec != nullptr;
-  const bool allow_fast = fast_profile_ok(dp, G);
+  const bool allow_fast = allow_fast_in && fast_profile_ok(dp, G);
   const bool gen_fast = generated && allow_fast && fast_spec_ok(spec);
-  const bool with_generic = !gen_fast;
-  const size_t per_scen = abytes(P, 8) + abytes(P, 4) + built_bytes(P, 1, with_generic) +
+  const bool with_generic = !allow_fast;
+  const bool host_in = !generated && !device_ptrs;  // caller arrays in host memory
+  const size_t in_bytes = abytes(P, 8) + abytes(P, 4);
+  const size_t per_scen = in_bytes * (host_in ? 2 : 1) + built_bytes(P, 1, with_generic) +
                           abytes(T, 8) * 2 + abytes(T, 16) + abytes(C, 8) * 3 + abytes(1, 4) + 2048;
   // Batches: what an 8 GiB scratch budget holds (<= 2048 scenarios), planned
   // as whole waves of the lockstep evaluator (S = 10,000 on 148 SMs x 4:
@@ -789,6 +827,7 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
       cps.push_back(0);
     }
   }
+  const int nb = (int)sizes.size();
   const int B = *std::max_element(sizes.begin(), sizes.end());
   // a second set of per-batch result buffers when host copies overlap
   const size_t out_set = abytes((size_t)B * C, 8) * 3 + abytes(B, 4);
@@ -800,15 +839,23 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
   double* lnz = nullptr;
   RS_TRY(gen_tables(ctx, &nz, &lnz));
   int64_t* d_off = arena_alloc<int64_t>(ctx, B + 1);
-  double* pred = arena_alloc<double>(ctx, (size_t)B * P);
-  int32_t* plen = arena_alloc<int32_t>(ctx, (size_t)B * P);
+  // input sets: two when host inputs stream in on in_stream ahead of compute
+  const int nin = host_in && nb > 1 ? 2 : 1;
+  double* pred[2] = {nullptr, nullptr};
+  int32_t* plen[2] = {nullptr, nullptr};
+  for (int k = 0; k < nin; ++k) {
+    pred[k] = arena_alloc<double>(ctx, (size_t)B * P);
+    plen[k] = arena_alloc<int32_t>(ctx, (size_t)B * P);
+  }
   double* gt = arena_alloc<double>(ctx, (size_t)B * T);
   double* agg_t = arena_alloc<double>(ctx, C);
   double* agg_c = arena_alloc<double>(ctx, C);
   int32_t* agg_h = arena_alloc<int32_t>(ctx, C);
   // Host outputs of several batches: two buffer sets, each batch's results
-  // copied out on the context's copy stream while the next batch computes.
-  const bool overlap_out = !device_ptrs && sizes.size() > 1;
+  // copied out on the context's copy stream while the next batch computes;
+  // pinned caller buffers receive them directly, pageable ones through the
+  // pinned bounce buffers (drained on the host once the copy's event is done).
+  const bool overlap_out = !device_ptrs && nb > 1;
   const int nsets = overlap_out ? 2 : 1;
   double* b_tt[2] = {nullptr, nullptr};
   double* b_cc[2] = {nullptr, nullptr};
@@ -821,13 +868,43 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
     b_ns[k] = arena_alloc<int32_t>(ctx, B);
     if (!b_ns[k]) return fail(RS_E_NOMEM, "arena exhausted (sweep)");
   }
-  // every return below first drains the copies into the caller's buffers
+  struct HostOut {
+    char* dst;        // caller array
+    size_t elem;      // bytes per scenario
+    bool direct;      // pinned: copy straight into dst
+    char* bounce[2];  // per buffer set otherwise
+  };
+  HostOut ho[4] = {{(char*)out->t_total, 8ull * C, false, {}}, {(char*)out->cost, 8ull * C, false, {}},
+                   {(char*)out->idle_slot_ticks, 8ull * C, false, {}}, {(char*)out->n_star, 4, false, {}}};
+  if (!device_ptrs) {
+    size_t bb = 0;
+    for (auto& h : ho)
+      if (h.dst && !(h.direct = host_pinned(h.dst))) bb += abytes(B * h.elem, 1) * nsets;
+    RS_TRY(bounce_reserve(ctx, bb));
+    char* q = ctx->bounce;
+    for (auto& h : ho)
+      if (h.dst && !h.direct)
+        for (int k = 0; k < nsets; ++k, q += abytes(B * h.elem, 1)) h.bounce[k] = q;
+  }
+  // pending bounce drains per buffer set: (first scenario, scenarios)
+  int pend_s0[2] = {-1, -1}, pend_n[2] = {0, 0};
+  auto drain = [&](int set) -> int {
+    if (pend_s0[set] < 0) return RS_OK;
+    RS_CUDA_TRY(cudaEventSynchronize(ctx->ev_copied[set]));
+    for (auto& h : ho)
+      if (h.dst && !h.direct)
+        std::memcpy(h.dst + (size_t)pend_s0[set] * h.elem, h.bounce[set], (size_t)pend_n[set] * h.elem);
+    pend_s0[set] = -1;
+    return RS_OK;
+  };
+  // every return below first waits for the copies (their buffers are the caller's)
   struct CopyDrain {
-    cudaStream_t s;
+    cudaStream_t a, b;
     ~CopyDrain() {
-      if (s) cudaStreamSynchronize(s);
+      if (a) cudaStreamSynchronize(a);
+      if (b) cudaStreamSynchronize(b);
     }
-  } drain{overlap_out ? ctx->copy_stream : nullptr};
+  } guard{overlap_out ? ctx->copy_stream : nullptr, nin > 1 ? ctx->in_stream : nullptr};
   const size_t mark = ctx->arena_used;  // per-batch structures live above
   {
     std::vector<int64_t> off(B + 1);
@@ -838,44 +915,65 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
   RS_CUDA_TRY(cudaMemsetAsync(agg_c, 0, 8 * C, ctx->stream));
   RS_CUDA_TRY(cudaMemsetAsync(agg_h, 0, 4 * C, ctx->stream));
   RS_TRY(clear_flags(ctx));
-  for (size_t bi = 0, s0 = 0; bi < sizes.size(); s0 += sizes[bi], ++bi) {
-    const int Sb = sizes[bi];
+  std::vector<int> first(nb);
+  for (int bi = 0, s0 = 0; bi < nb; s0 += sizes[bi], ++bi) first[bi] = s0;
+  // host inputs of batch bi into input set bi % nin, on in_stream once the
+  // set's previous batch has been consumed by its build
+  auto stage_in = [&](int bi) -> int {
+    const int k = bi % nin;
+    const int64_t n = (int64_t)sizes[bi] * P;
+    const size_t o = (size_t)first[bi] * P;
+    if (nin == 1) {
+      RS_TRY(h2d(ctx, pred[0], h_pred + o, 8ull * n));
+      RS_TRY(h2d(ctx, plen[0], h_plen + o, 4ull * n));
+      return RS_OK;
+    }
+    if (bi >= 2) RS_CUDA_TRY(cudaStreamWaitEvent(ctx->in_stream, ctx->ev_inused[k], 0));
+    RS_CUDA_TRY(cudaMemcpyAsync(pred[k], h_pred + o, 8ull * n, cudaMemcpyHostToDevice, ctx->in_stream));
+    RS_CUDA_TRY(cudaMemcpyAsync(plen[k], h_plen + o, 4ull * n, cudaMemcpyHostToDevice, ctx->in_stream));
+    RS_CUDA_TRY(cudaEventRecord(ctx->ev_in[k], ctx->in_stream));
+    return RS_OK;
+  };
+  if (host_in) RS_TRY(stage_in(0));
+  for (int bi = 0; bi < nb; ++bi) {
+    const int Sb = sizes[bi], s0 = first[bi];
     const int64_t n = (int64_t)Sb * P;
+    const int k_in = bi % nin;
     ctx->arena_used = mark;
     Built built;
     if (generated) {
       GenSpec g = to_gen(spec, spec->first_scenario + s0);
       if (gen_fast) {
         // the generated scenarios only feed the structure: not stored
-        RS_TRY(build_batch(ctx, Sb, d_off, n, pred, plen, &g, nz, lnz, true, &built, false, false));
+        RS_TRY(build_batch(ctx, Sb, d_off, n, pred[0], plen[0], &g, nz, lnz, true, &built, false,
+                           false, true));
       } else {
         RS_LAUNCH(ctx, "gen_scenarios", gen_scenarios_kernel, grid_for(ctx, n, 256), 256, 0, g,
-                  nz, lnz, Sb, pred, plen);
-        RS_TRY(build_batch(ctx, Sb, d_off, n, pred, plen, nullptr, nullptr, nullptr, allow_fast,
-                           &built, true, false));
+                  nz, lnz, Sb, pred[0], plen[0]);
+        RS_TRY(build_batch(ctx, Sb, d_off, n, pred[0], plen[0], nullptr, nullptr, nullptr,
+                           allow_fast, &built, true, false, true));
       }
     } else {
-      const double* src_p = h_pred + (size_t)s0 * P;
-      const int32_t* src_l = h_plen + (size_t)s0 * P;
       if (device_ptrs) {
-        RS_CUDA_TRY(cudaMemcpyAsync(pred, src_p, 8ull * n, cudaMemcpyDeviceToDevice, ctx->stream));
-        RS_CUDA_TRY(cudaMemcpyAsync(plen, src_l, 4ull * n, cudaMemcpyDeviceToDevice, ctx->stream));
-      } else {
-        RS_TRY(h2d(ctx, pred, src_p, 8ull * n));
-        RS_TRY(h2d(ctx, plen, src_l, 4ull * n));
+        const size_t o = (size_t)s0 * P;
+        RS_CUDA_TRY(cudaMemcpyAsync(pred[0], h_pred + o, 8ull * n, cudaMemcpyDeviceToDevice, ctx->stream));
+        RS_CUDA_TRY(cudaMemcpyAsync(plen[0], h_plen + o, 4ull * n, cudaMemcpyDeviceToDevice, ctx->stream));
+      } else if (nin > 1) {
+        RS_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_in[k_in], 0));
       }
-      RS_LAUNCH(ctx, "validate_inputs", to_id_order_kernel, grid_for(ctx, n, 256), 256, 0, pred,
-                (const int32_t*)nullptr, (const int32_t*)nullptr, n, pred, (int32_t*)nullptr,
-                (int32_t*)nullptr, (int32_t*)nullptr, ctx->d_flags, 1);
-      int fl;
-      RS_TRY(read_flags(ctx, &fl));
-      if (fl) return flags_to_status(fl);
-      RS_TRY(build_batch(ctx, Sb, d_off, n, pred, plen, nullptr, nullptr, nullptr, allow_fast,
-                         &built, true, false));
+      RS_LAUNCH(ctx, "validate_inputs", to_id_order_kernel, grid_for(ctx, n, 256), 256, 0,
+                pred[k_in], (const int32_t*)nullptr, (const int32_t*)nullptr, n, pred[k_in],
+                (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr, ctx->d_flags, 1);
+      RS_TRY(build_batch(ctx, Sb, d_off, n, pred[k_in], plen[k_in], nullptr, nullptr, nullptr,
+                         allow_fast, &built, true, false, true));
+      if (nin > 1) RS_CUDA_TRY(cudaEventRecord(ctx->ev_inused[k_in], ctx->stream));
     }
-    const int set = overlap_out ? (int)(bi & 1) : 0;
+    const int set = overlap_out ? (bi & 1) : 0;
     // the copies out of this buffer set two batches ago must be done
-    if (overlap_out && bi >= 2) RS_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[set], 0));
+    if (overlap_out && bi >= 2) {
+      RS_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[set], 0));
+      RS_TRY(drain(set));
+    }
     double* o_tt = (device_ptrs && out->t_total) ? out->t_total + (size_t)s0 * C : b_tt[set];
     double* o_cc = (device_ptrs && out->cost) ? out->cost + (size_t)s0 * C : b_cc[set];
     int64_t* o_idle = (device_ptrs && out->idle_slot_ticks) ? out->idle_slot_ticks + (size_t)s0 * C
@@ -903,33 +1001,74 @@ static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
         RS_CUDA_TRY(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_done[set], 0));
         cs = ctx->copy_stream;
       }
-      auto copy = [&](void* dst, const void* src, size_t bytes) -> int {
-        RS_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cs));
-        return RS_OK;
-      };
-      if (out->t_total) RS_TRY(copy(out->t_total + (size_t)s0 * C, o_tt, 8ull * Sb * C));
-      if (out->cost) RS_TRY(copy(out->cost + (size_t)s0 * C, o_cc, 8ull * Sb * C));
-      if (out->idle_slot_ticks)
-        RS_TRY(copy(out->idle_slot_ticks + (size_t)s0 * C, o_idle, 8ull * Sb * C));
-      if (out->n_star) RS_TRY(copy(out->n_star + s0, o_ns, 4ull * Sb));
+      const void* src[4] = {o_tt, o_cc, o_idle, o_ns};
+      for (int j = 0; j < 4; ++j) {
+        HostOut& h = ho[j];
+        if (!h.dst) continue;
+        void* dst = h.direct ? h.dst + (size_t)s0 * h.elem : h.bounce[set];
+        RS_CUDA_TRY(cudaMemcpyAsync(dst, src[j], (size_t)Sb * h.elem, cudaMemcpyDeviceToHost, cs));
+      }
       if (overlap_out) RS_CUDA_TRY(cudaEventRecord(ctx->ev_copied[set], ctx->copy_stream));
+      pend_s0[set] = s0;
+      pend_n[set] = Sb;
+      if (!overlap_out) RS_CUDA_TRY(cudaEventRecord(ctx->ev_copied[set], ctx->stream));
+    }
+    // the next batch's host inputs stream in while this batch computes
+    if (host_in && bi + 1 < nb) RS_TRY(stage_in(bi + 1));
+    if (bi == 0 && nb > 1 && allow_fast) {
+      // one early look at the status: an inapplicable fast structure costs
+      // one batch, not a whole sweep
+      int fl;
+      RS_TRY(read_flags(ctx, &fl));
+      if (fl & ~(kFlagBucketOverflow | kFlagBucketTooWide)) return flags_to_status(fl);
+      if (fl) {
+        *redo = true;
+        return RS_OK;
+      }
     }
   }
-  if (device_ptrs) {
+  if (!device_ptrs) {
+    if (overlap_out)  // the final sync on the context stream covers every copy
+      for (int k = 0; k < 2; ++k) RS_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[k], 0));
+    if (out->sum_t) RS_TRY(d2h(ctx, out->sum_t, agg_t, 8 * C));
+    if (out->sum_c) RS_TRY(d2h(ctx, out->sum_c, agg_c, 8 * C));
+    if (out->nstar_hist) RS_TRY(d2h(ctx, out->nstar_hist, agg_h, 4 * C));
+  } else {
     if (out->sum_t)
       RS_CUDA_TRY(cudaMemcpyAsync(out->sum_t, agg_t, 8 * C, cudaMemcpyDeviceToDevice, ctx->stream));
     if (out->sum_c)
       RS_CUDA_TRY(cudaMemcpyAsync(out->sum_c, agg_c, 8 * C, cudaMemcpyDeviceToDevice, ctx->stream));
     if (out->nstar_hist)
       RS_CUDA_TRY(cudaMemcpyAsync(out->nstar_hist, agg_h, 4 * C, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  int fl;
+  RS_TRY(read_flags(ctx, &fl));  // synchronises the context stream
+  if (ctx->timing) RS_TRY(collect_timers(ctx));
+  if (fl & ~(kFlagBucketOverflow | kFlagBucketTooWide)) return flags_to_status(fl);
+  if (fl) {
+    *redo = true;
     return RS_OK;
   }
-  if (overlap_out)  // the final sync on the context stream covers every copy
-    for (int k = 0; k < 2; ++k) RS_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[k], 0));
-  if (out->sum_t) RS_TRY(d2h(ctx, out->sum_t, agg_t, 8 * C));
-  if (out->sum_c) RS_TRY(d2h(ctx, out->sum_c, agg_c, 8 * C));
-  if (out->nstar_hist) RS_TRY(d2h(ctx, out->nstar_hist, agg_h, 4 * C));
-  return sync_and_check(ctx);
+  for (int k = 0; k < 2; ++k) RS_TRY(drain(k));
+  return RS_OK;
+}
+
+// Shared sweep driver: scenarios either generated (spec) or from arrays.
+// Synchronous: it returns once every result (device or host) is written.
+static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h_pred,
+                      const int32_t* h_plen, int S, int P, const rs_profile* profile, int G,
+                      int n_min, int n_max, double lambda, int gpus, rs_sweep_out* out,
+                      int device_ptrs) {
+  RS_TRY(check_scale_args(P, G, n_min, n_max, lambda));
+  DevProfile dp;
+  RS_TRY(get_profile(ctx, profile, &dp));
+  bool redo = false;
+  RS_TRY(sweep_pass(ctx, spec, h_pred, h_plen, S, P, dp, G, n_min, n_max, lambda, gpus, out,
+                    device_ptrs, true, &redo));
+  if (redo)
+    RS_TRY(sweep_pass(ctx, spec, h_pred, h_plen, S, P, dp, G, n_min, n_max, lambda, gpus, out,
+                      device_ptrs, false, &redo));
+  return redo ? fail(RS_E_CUDA, "internal: generic sweep pass flagged the fast path") : RS_OK;
 }
 
 // S caller item sets (host SoA), each its own scenario, in id order.
@@ -979,7 +1118,7 @@ static int prepare_sets(rs_ctx* ctx, const double* h_pred, const int32_t* h_plen
               h_id_rank ? seen : (int32_t*)nullptr, ctx->d_flags, require_ge1);
     int fl;
     RS_TRY(read_flags(ctx, &fl));
-    if (fl & (kFlagWorkOverflow << 1))
+    if (fl & (kFlagBadPerm))
       return fail(RS_E_ARG, "id_rank is not a permutation of [0, count)");
     if (fl) return flags_to_status(fl);
     const bool allow_fast = dp == nullptr || fast_profile_ok(*dp, G);
@@ -1173,6 +1312,7 @@ extern "C" {
 
 int rs_generate_scenarios(rs_ctx* ctx, const rs_scenario_spec* spec, double* pred,
                           int32_t* plen, int device_ptrs) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx) return fail(RS_E_ARG, "ctx is NULL");
   RS_TRY(check_spec(spec));
   int64_t n = (int64_t)spec->n_scenarios * spec->count;
@@ -1195,6 +1335,7 @@ int rs_generate_scenarios(rs_ctx* ctx, const rs_scenario_spec* spec, double* pre
 int rs_sweep(rs_ctx* ctx, const rs_scenario_spec* spec, const rs_profile* profile,
              int32_t G, int32_t n_min, int32_t n_max, double lambda, int32_t gpus,
              rs_sweep_out* out, int device_ptrs) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !out) return fail(RS_E_ARG, "NULL argument");
   RS_TRY(check_spec(spec));
   if (spec->n_scenarios == 0) return RS_OK;
@@ -1206,6 +1347,7 @@ int rs_sweep_arrays(rs_ctx* ctx, const double* pred, const int32_t* plen, int32_
                     int32_t count, const rs_profile* profile, int32_t G, int32_t n_min,
                     int32_t n_max, double lambda, int32_t gpus, rs_sweep_out* out,
                     int device_ptrs) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !out || !pred || !plen) return fail(RS_E_ARG, "NULL argument");
   if (S <= 0) return RS_OK;
   return sweep_impl(ctx, nullptr, pred, plen, S, count, profile, G, n_min, n_max, lambda,
@@ -1321,6 +1463,7 @@ int rs_scale(rs_ctx* ctx, const double* pred, const int32_t* plen, const int32_t
              int32_t count, const rs_profile* profile, int32_t G, int32_t n_min,
              int32_t n_max, double lambda, int32_t gpus, const double* t_penalty,
              rs_scale_out* out) {
+  RS_DEVICE_GUARD(ctx);
   return scale_impl(ctx, pred, plen, id_rank, count, profile, G, n_min, n_max, lambda, gpus,
                     t_penalty, nullptr, out);
 }
@@ -1329,6 +1472,7 @@ int rs_scale_placed(rs_ctx* ctx, const double* pred, const int32_t* plen,
                     const int32_t* id_rank, int32_t count, const rs_profile* profile, int32_t G,
                     int32_t n_min, int32_t n_max, double lambda, int32_t gpus,
                     const rs_placement_penalty* penalty, rs_scale_out* out) {
+  RS_DEVICE_GUARD(ctx);
   if (!penalty) return fail(RS_E_ARG, "NULL placement penalty");
   return scale_impl(ctx, pred, plen, id_rank, count, profile, G, n_min, n_max, lambda, gpus,
                     nullptr, penalty, out);
@@ -1337,6 +1481,7 @@ int rs_scale_placed(rs_ctx* ctx, const double* pred, const int32_t* plen,
 int rs_scale_select(rs_ctx* ctx, const double* t_total, const double* t_penalty,
                     const double* cost, int32_t C, int32_t n_min, double lambda,
                     double* t_norm, double* c_norm, double* score, int32_t* n_star) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !t_total || !cost || !n_star || C < 1) return fail(RS_E_ARG, "bad arguments");
   if (lambda < 0 || lambda > 1) return fail(RS_E_CONFIG, "scale: lambda must be in [0, 1]");
   RS_TRY(arena_reserve(ctx, abytes(C, 8) * 6 + 4096));
@@ -1357,6 +1502,7 @@ int rs_scale_select(rs_ctx* ctx, const double* t_total, const double* t_penalty,
 
 int rs_rank_strings(rs_ctx* ctx, const char* bytes, const int64_t* offsets, int32_t count,
                     int32_t* rank) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !offsets || !rank) return fail(RS_E_ARG, "NULL argument");
   if (count <= 0) return RS_OK;
   int64_t maxlen = 0;
@@ -1385,6 +1531,7 @@ int rs_rank_strings(rs_ctx* ctx, const char* bytes, const int64_t* offsets, int3
 
 int rs_assign(rs_ctx* ctx, const double* pred, const int32_t* id_rank, int32_t count,
               int32_t n_actors, int32_t* order, int32_t* group_offsets) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx) return fail(RS_E_ARG, "ctx is NULL");
   if (count <= 0) return fail(RS_E_VALIDATION, "assign: empty batch");
   if (n_actors < 1) return fail(RS_E_VALIDATION, "assign: n_actors must be >= 1");
@@ -1433,6 +1580,7 @@ static int integrate_sets(rs_ctx* ctx, const int32_t* plen, const double* target
 int rs_integrate_decode_seconds(rs_ctx* ctx, const int32_t* prompt_len,
                                 const double* target_len, int64_t count,
                                 const rs_profile* profile, double* out) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !out) return fail(RS_E_ARG, "NULL argument");
   if (count <= 0) {
     *out = 0.0;
@@ -1445,6 +1593,7 @@ int rs_integrate_decode_seconds(rs_ctx* ctx, const int32_t* prompt_len,
 
 int rs_estimate_actor_time(rs_ctx* ctx, const int32_t* prompt_len, const double* pred,
                            int32_t count, const rs_profile* profile, int32_t G, double* out) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !out) return fail(RS_E_ARG, "NULL argument");
   if (G < 1) return fail(RS_E_VALIDATION, "estimate_actor_time: responses_per_prompt >= 1");
   if (count <= 0) {
@@ -1458,6 +1607,7 @@ int rs_estimate_actor_time(rs_ctx* ctx, const int32_t* prompt_len, const double*
 int rs_estimate_cost(rs_ctx* ctx, const int32_t* prompt_len, const double* pred,
                      const int32_t* group_offsets, const int32_t* gpu_count, int32_t n_groups,
                      const rs_profile* profile, int32_t G, double* cost, double* times) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !cost) return fail(RS_E_ARG, "NULL argument");
   if (n_groups <= 0) {
     *cost = 0.0;
@@ -1475,6 +1625,7 @@ int rs_estimate_cost(rs_ctx* ctx, const int32_t* prompt_len, const double* pred,
 
 int rs_lpt(rs_ctx* ctx, const double* pred, const int32_t* id_rank, int32_t count, int32_t G,
            int32_t n_min, int32_t n_max, int64_t* makespan, int64_t* idle) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !pred || !makespan || !idle) return fail(RS_E_ARG, "NULL argument");
   if (count <= 0) return fail(RS_E_VALIDATION, "lpt: empty batch");
   if (n_min < 1 || n_min > n_max) return fail(RS_E_VALIDATION, "lpt: need 1 <= n_min <= n_max");
@@ -1516,7 +1667,7 @@ int rs_lpt(rs_ctx* ctx, const double* pred, const int32_t* id_rank, int32_t coun
             ctx->d_flags, 1);
   int fl;
   RS_TRY(read_flags(ctx, &fl));
-  if (fl & (kFlagWorkOverflow << 1)) return fail(RS_E_ARG, "id_rank is not a permutation of [0, count)");
+  if (fl & (kFlagBadPerm)) return fail(RS_E_ARG, "id_rank is not a permutation of [0, count)");
   if (fl) return flags_to_status(fl);
   RS_LAUNCH(ctx, "lpt_keys", lpt_keys_kernel, grid_for(ctx, count, 256), 256, 0, pid,
             (int64_t)count, keys, vals);

@@ -99,6 +99,7 @@ extern "C" int rs_predict_lengths(rs_ctx* ctx, const double* obs, const int32_t*
                                   double alpha, int32_t max_response_len,
                                   const rs_noise_model* noise, const char* id_bytes,
                                   const int64_t* id_offsets, int device_ptrs, double* out) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx) return fail(RS_E_ARG, "NULL context");
   // LengthHistory's constructor checks (predictor.cpp:24-31)
   if (window < 1) return fail(RS_E_CONFIG, "predictor window must be >= 1");

@@ -364,10 +364,19 @@ struct rs_trace_csr {
   std::vector<int64_t> id_off;
   std::vector<int32_t> gt;
   std::vector<int64_t> offsets;
-  cudaStream_t stream = nullptr;  // the outputs are stream-ordered allocations
+  // The outputs are stream-ordered allocations, complete when the parse
+  // returns. The handle may outlive its context (and the context's streams),
+  // so it is freed with the synchronous cudaFree on its own device.
+  int device = 0;
   ~rs_trace_csr() {
-    if (d_tokens) cudaFreeAsync(d_tokens, stream);
-    if (d_offsets) cudaFreeAsync(d_offsets, stream);
+    if (!d_tokens && !d_offsets) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != device) cudaSetDevice(device);
+    if (d_tokens) cudaFree(d_tokens);
+    if (d_offsets) cudaFree(d_offsets);
+    if (prev >= 0 && prev != device) cudaSetDevice(prev);
+    cudaGetLastError();
   }
 };
 
@@ -396,6 +405,7 @@ static int parse_error(int64_t line, const std::string& what) {
 
 extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes, int device_ptr,
                                   rs_trace_csr** out) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !out || (!text && n_bytes > 0)) return fail(RS_E_ARG, "NULL argument");
   if (n_bytes < 0) return fail(RS_E_ARG, "negative size");
   *out = nullptr;
@@ -572,7 +582,7 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
         return fail(RS_E_VALIDATION, "prompt '" + id_of(r) + "' ground_truth_len out of range");
     }
     // 8. the id-ordered token CSR, owned by the handle
-    tr->stream = ctx->own_stream;  // outlives any caller stream set on the context
+    tr->device = ctx->device;
     if (cudaMallocAsync(&tr->d_tokens, 4ull * std::max<int64_t>(T, 1), ctx->stream) != cudaSuccess ||
         cudaMallocAsync(&tr->d_offsets, 8ull * (P + 1), ctx->stream) != cudaSuccess) {
       cudaGetLastError();
@@ -617,6 +627,7 @@ extern "C" int rs_trace_csr_device(const rs_trace_csr* tr, const int32_t** d_tok
 extern "C" int rs_trace_csr_copy(rs_ctx* ctx, const rs_trace_csr* tr, int32_t* tokens,
                                  int64_t* offsets, char* id_bytes, int64_t* id_offsets,
                                  int32_t* ground_truth) {
+  RS_DEVICE_GUARD(ctx);
   if (!ctx || !tr) return fail(RS_E_ARG, "NULL argument");
   if (tokens && tr->n_tokens) RS_TRY(d2h(ctx, tokens, tr->d_tokens, 4ull * tr->n_tokens));
   if (offsets) std::memcpy(offsets, tr->offsets.data(), 8ull * (tr->count + 1));

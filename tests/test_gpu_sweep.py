@@ -181,3 +181,69 @@ def test_sweep_huge_batch_axis_falls_back():
     grid = [[0.005 + 1e-6 * b + 1e-6 * c for c in ck] for b in bk]
     prof = LatencyProfile(bk, ck, grid, 0.0005, 2)
     check_sweep(c4_spec(36, count=600, first=5), 1, 40, prof=prof, lam=0.5, g=1)
+
+
+def test_sweep_generated_wide_bucket_falls_back():
+    """a generated spec whose clamp puts > 4,096 prompts
+    into one finish bucket (pred_max = 2,048: ~24 % of 65,536 prompts) must
+    not reuse stale structure data: the fast build flags it, the kernels that
+    read the structure skip, and the sweep reruns on the generic path."""
+    spec = c4_spec(3, count=65536, first=11)
+    spec.pred_max = 2048.0
+    check_sweep(spec, 1, 48)
+
+
+def test_sweep_late_wide_bucket_reruns_generic():
+    """Several batches of caller arrays (host inputs streamed on in_stream),
+    the LAST scenario holding a bucket wider than the fast path takes: the
+    end-of-sweep status check reruns everything on the generic path."""
+    spec = c4_spec(2300, count=600, first=3)
+    pred, plen = port().generate_scenarios(spec)
+    pred[-600:] = 77.0
+    pred[-5000:-4700] = 12.5
+    got = rs_sweep(spec, default_profile(), 8, 1, 16, 0.7, 2, (pred, plen))
+    tt, cc, ns = port().sweep_arrays(pred, plen, 2300, 600, default_profile(), 8, 1, 16, 0.7, 2,
+                                     threads=8)
+    assert np.array_equal(bits(got["t_total"]), bits(tt))
+    assert np.array_equal(bits(got["cost"]), bits(cc))
+    assert np.array_equal(got["n_star"], ns)
+
+
+def test_sweep_first_batch_too_wide_reruns_generic():
+    """The same with the wide bucket in the first batch (caught by the early
+    status check after batch 0) — and > 4,096 equal predictions."""
+    spec = c4_spec(2200, count=4200, first=8)
+    pred, plen = port().generate_scenarios(spec)
+    pred[:4200] = 333.0
+    got = rs_sweep(spec, default_profile(), 8, 1, 8, 0.7, 2, (pred, plen))
+    tt, cc, ns = port().sweep_arrays(pred, plen, 2200, 4200, default_profile(), 8, 1, 8, 0.7, 2,
+                                     threads=8)
+    assert np.array_equal(bits(got["t_total"]), bits(tt))
+    assert np.array_equal(got["n_star"], ns)
+
+
+def test_sweep_arrays_multi_batch_streamed_inputs():
+    """Caller arrays over several batches: batch i+1's inputs are copied on
+    the input stream while batch i computes (two input sets)."""
+    check_sweep(c4_spec(4300, count=96, first=57), 1, 20, arrays=True, lam=0.45)
+
+
+def test_sweep_multi_batch_pinned_outputs():
+    """Pinned caller outputs take the direct (no bounce) copy path."""
+    import torch
+    spec = c4_spec(4200, count=64, first=31)
+    S, Cn = spec.n_scenarios, 24
+    prof = default_profile()
+    ctx = context()
+    t = {k: torch.zeros(n, dtype=d).pin_memory() for k, n, d in
+         (("t_total", S * Cn, torch.float64), ("cost", S * Cn, torch.float64),
+          ("idle", S * Cn, torch.int64), ("n_star", S, torch.int32))}
+    so = _abi.RsSweepOut(t["t_total"].data_ptr(), t["cost"].data_ptr(), t["idle"].data_ptr(),
+                         t["n_star"].data_ptr(), None, None, None)
+    s, keep = prof.struct()
+    check(ctx.lib.rs_sweep(ctx.handle, C.byref(spec), C.byref(s), 8, 1, Cn, 0.7, 2, C.byref(so), 0))
+    pred, plen = port().generate_scenarios(spec)
+    tt, cc, ns = port().sweep_arrays(pred, plen, S, 64, prof, 8, 1, Cn, 0.7, 2, threads=8)
+    assert np.array_equal(bits(t["t_total"].numpy().reshape(S, Cn)), bits(tt))
+    assert np.array_equal(bits(t["cost"].numpy().reshape(S, Cn)), bits(cc))
+    assert np.array_equal(t["n_star"].numpy(), ns)
