@@ -19,7 +19,7 @@ $(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -dc $< -o $@ 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; exit 1)
 
 $(LIB): $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(SRCS))
-	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -cudart static -o $@ $^
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -cudart static -o $@ $^ -ldl
 
 oracle:
 	$(MAKE) -C oracle port
@@ -50,7 +50,17 @@ SUITES    := acceptance_main test_dedup test_planner test_profile test_training
 
 .PHONY: shim
 shim: $(foreach t,$(SUITES),$(SHIM_OUT)/$(t)_b200 $(SHIM_OUT)/$(t)_ref) \
-      $(SHIM_OUT)/test_placement_b200 $(SHIM_OUT)/c5_bench_b200 $(SHIM_OUT)/c5_bench_ref
+      $(SHIM_OUT)/test_placement_b200 $(SHIM_OUT)/c5_bench_b200 $(SHIM_OUT)/c5_bench_ref \
+      $(SHIM_OUT)/c3_bench_b200 $(SHIM_OUT)/c3_bench_ref
+
+# C3 driver (shim/tools/c3_bench.cpp): scale() at 64K x G=8, N in [1, 512]
+$(SHIM_OUT)/c3_bench_b200: $(PKG)/shim/tools/c3_bench.cpp $(SHIM_OUT)/librollsim_b200.a $(LIB)
+	$(CXXREF) $< -o $@ $(SHIM_OUT)/librollsim_b200.a -L$(PKG) -lrs_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -lpthread
+
+$(SHIM_OUT)/c3_bench_ref: $(PKG)/shim/tools/c3_bench.cpp ref
+	@mkdir -p $(SHIM_OUT)
+	$(CXXREF) $< -o $@ oracle/_ref/librollsim_ref.a -lpthread
 
 # C5 driver (shim/tools/c5_bench.cpp), linked against the drop-in and the reference
 $(SHIM_OUT)/c5_bench_b200: $(PKG)/shim/tools/c5_bench.cpp $(SHIM_OUT)/librollsim_b200.a $(LIB)

@@ -218,16 +218,83 @@ def cpu_baseline_sweep(args):
                       args.n_max, args.lam, 2, threads=threads)
     dt = time.perf_counter() - t0
     n_cand = args.n_max - args.n_min + 1
+    # one thread: the reference's own single-threaded scale(), 2 scenarios
+    p1, l1 = port().generate_scenarios(c4_spec(2, count=args.prompts, first=n))
+    t1 = time.perf_counter()
+    impl.sweep_arrays(p1, l1, 2, args.prompts, default_profile(), args.G, args.n_min,
+                      args.n_max, args.lam, 2, threads=1)
+    d1 = time.perf_counter() - t1
     return {"value": n * n_cand / dt, "unit": "evals/s", "cores": threads, "kind": kind,
+            "cpu_model": cpu_model(),
+            "one_thread_value": 2 * n_cand / d1,
             "sample": f"{n} scenarios x {n_cand} candidates ({args.prompts} prompts x G={args.G}), "
-                      f"{threads} threads, {dt:.1f} s"}
+                      f"{threads} threads, {dt:.1f} s; one thread: 2 scenarios, {d1:.1f} s"}
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def counters(key):
+    """ncu counters per unit of the dominant kernels (profiles/kernel_counters.json,
+    written from a committed `ncu --set full` capture by tools/kernel_counters.py)."""
+    f = REPO / "profiles" / "kernel_counters.json"
+    if not f.exists():
+        return None
+    return json.loads(f.read_text()).get(key)
+
+
+def parity_sample(args, world, rank, S_local, s0, t_total, cost, idle, n_star, n_cand):
+    """Bitwise check of sampled scenarios of THIS rank's block (spread over
+    every batch, first and last included) against the C port, outside the
+    timed region; --parity-full checks every scenario (minutes of CPU)."""
+    import torch
+    from cases import c4_spec
+    from oracle_lib import port
+    from paper_2602_22718_b200.rollsim import default_profile
+    if S_local == 0:
+        return 0, True
+    want = S_local if args.parity_full else max(1, -(-args.parity_samples // world))
+    idx = np.unique(np.linspace(0, S_local - 1, min(want, S_local)).round().astype(np.int64))
+    tt_d = t_total.view(S_local, n_cand).cpu().numpy()
+    cc_d = cost.view(S_local, n_cand).cpu().numpy()
+    id_d = idle.view(S_local, n_cand).cpu().numpy()
+    ns_d = n_star.cpu().numpy()
+    threads = max(1, (os.cpu_count() or 1) // world)
+    ok = True
+    prof = default_profile()
+    chunk = 256
+    for c0 in range(0, len(idx), chunk):
+        sel = idx[c0:c0 + chunk]
+        preds, plens = [], []
+        for s in sel:  # each sampled scenario generated by the port itself
+            p, l = port().generate_scenarios(c4_spec(1, count=args.prompts, first=s0 + int(s)))
+            preds.append(p)
+            plens.append(l)
+        pred, plen = np.concatenate(preds), np.concatenate(plens)
+        tt, cc, ns = port().sweep_arrays(pred, plen, len(sel), args.prompts, prof, args.G,
+                                         args.n_min, args.n_max, args.lam, 2, threads=threads)
+        ok &= bool(np.array_equal(tt.view(np.uint64), tt_d[sel].view(np.uint64)))
+        ok &= bool(np.array_equal(cc.view(np.uint64), cc_d[sel].view(np.uint64)))
+        ok &= bool(np.array_equal(ns, ns_d[sel]))
+        for j, s in enumerate(sel):
+            ok &= bool(np.array_equal(port().scale_idle(preds[j], None, args.G, args.n_min,
+                                                        args.n_max), id_d[s]))
+    return len(idx), ok
 
 
 def run_ours(args, world, rank, local):
     import torch
     import torch.distributed as dist
     from cases import c4_spec
-    from paper_2602_22718_b200 import _abi
+    from paper_2602_22718_b200 import _abi, sweep
     from paper_2602_22718_b200.lib import check, context, ensure_built
     from paper_2602_22718_b200.rollsim import default_profile
 
@@ -237,34 +304,49 @@ def run_ours(args, world, rank, local):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = context(local)
-    # A dedicated torch stream shared with the library so CUDA events and
-    # NCCL collectives order against our kernels (NULL would select the
-    # context's own stream).
+    lib = ctx.lib
+    # A dedicated torch stream shared with the library so CUDA events order
+    # against our kernels (NULL would select the context's own stream).
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
+    comm = None
+    if world > 1:  # librs_b200's own NCCL communicator for the one aggregate all-reduce
+        def bcast(b):
+            o = [b]
+            dist.broadcast_object_list(o, src=0)
+            return o[0]
+        comm = sweep.Comm(ctx, world, rank, bcast)
     prof = default_profile()
     ps, keep = prof.struct()
     n_cand = args.n_max - args.n_min + 1
-    from paper_2602_22718_b200 import sweep
     s0, s1 = sweep.shard_range(args.scenarios, world, rank)
     S = s1 - s0
-    spec = c4_spec(S, count=args.prompts, first=s0)
-    t_total = torch.empty(S * n_cand, dtype=torch.float64, device=dev)
-    cost = torch.empty(S * n_cand, dtype=torch.float64, device=dev)
-    idle = torch.empty(S * n_cand, dtype=torch.int64, device=dev)
-    n_star = torch.empty(S, dtype=torch.int32, device=dev)
+    spec_all = c4_spec(args.scenarios, count=args.prompts, first=0)
+    spec_local = c4_spec(S, count=args.prompts, first=s0)
+    t_total = torch.empty(max(S, 1) * n_cand, dtype=torch.float64, device=dev)
+    cost = torch.empty_like(t_total)
+    idle = torch.empty(max(S, 1) * n_cand, dtype=torch.int64, device=dev)
+    n_star = torch.empty(max(S, 1), dtype=torch.int32, device=dev)
     agg_t = torch.empty(n_cand, dtype=torch.float64, device=dev)
     agg_c = torch.empty(n_cand, dtype=torch.float64, device=dev)
     agg_h = torch.empty(n_cand, dtype=torch.int32, device=dev)
     out_dev = _abi.RsSweepOut(t_total.data_ptr(), cost.data_ptr(), idle.data_ptr(),
                               n_star.data_ptr(), agg_h.data_ptr(), agg_t.data_ptr(),
                               agg_c.data_ptr())
+    pick = C.c_int32()
+
+    def sweep_call(out, device_ptrs):
+        if comm is not None:
+            check(lib.rs_sweep_sharded(ctx.handle, comm.handle, C.byref(spec_all), C.byref(ps),
+                                       args.G, args.n_min, args.n_max, args.lam, 2, C.byref(out),
+                                       device_ptrs, C.byref(pick)))
+        else:
+            check(lib.rs_sweep(ctx.handle, C.byref(spec_local), C.byref(ps), args.G, args.n_min,
+                               args.n_max, args.lam, 2, C.byref(out), device_ptrs))
 
     def step_device():
-        check(ctx.lib.rs_sweep(ctx.handle, C.byref(spec), C.byref(ps), args.G, args.n_min,
-                               args.n_max, args.lam, 2, C.byref(out_dev), 1))
-        sweep.combine(agg_t, agg_c, agg_h)
+        sweep_call(out_dev, 1)
 
     def timed(fn, k):
         if world > 1:
@@ -296,58 +378,62 @@ def run_ours(args, world, rank, local):
     with ClockSampler(local, pci) as clk:
         ms = timed(step_device, args.steps)
     launches = (ctx.kernel_launches() - launches0) // args.steps
-    # roofline attribution: the same steps again with per-kernel CUDA-event
+    # per-kernel attribution: the same steps again with per-kernel CUDA-event
     # timing on (kept out of the timed region above)
     ctx.enable_kernel_timing(True)
     ctx.reset_kernel_timing()
     attr_ms = timed(step_device, args.steps)
-    ge_ms, ge_n = ctx.kernel_time("group_eval")
+    kt = {k: ctx.kernel_time(k) for k in ("group_eval", "fast_build", "group_table", "finish",
+                                          "aggregate", "fast_tables", "pack_aggregates")}
     ctx.enable_kernel_timing(False)
     total_evals = args.scenarios * n_cand
     value = total_evals * args.steps / (ms / 1e3)
 
-    # e2e: the same call with host (pinned) output buffers
-    pin = {k: torch.empty(S * n_cand, dtype=t, pin_memory=True)
+    # e2e: the same public call with host (pinned) output buffers
+    pin = {k: torch.empty(max(S, 1) * n_cand, dtype=t, pin_memory=True)
            for k, t in (("t", torch.float64), ("c", torch.float64), ("i", torch.int64))}
-    pin_ns = torch.empty(S, dtype=torch.int32, pin_memory=True)
+    pin_ns = torch.empty(max(S, 1), dtype=torch.int32, pin_memory=True)
     pin_agg = [torch.empty(n_cand, dtype=torch.float64, pin_memory=True) for _ in range(2)]
     pin_h = torch.empty(n_cand, dtype=torch.int32, pin_memory=True)
     out_host = _abi.RsSweepOut(pin["t"].data_ptr(), pin["c"].data_ptr(), pin["i"].data_ptr(),
                                pin_ns.data_ptr(), pin_h.data_ptr(), pin_agg[0].data_ptr(),
                                pin_agg[1].data_ptr())
     d2h = S * n_cand * 24 + S * 4 + n_cand * 20
-    h2d = C.sizeof(spec) + 8 * (9 + 5 + 45)
-
-    def step_host():
-        check(ctx.lib.rs_sweep(ctx.handle, C.byref(spec), C.byref(ps), args.G, args.n_min,
-                               args.n_max, args.lam, 2, C.byref(out_host), 0))
-        if world > 1:
-            agg = torch.cat([pin_agg[0], pin_agg[1]]).to(dev)
-            dist.all_reduce(agg)
-            agg.cpu()
-
-    step_host()
-    e2e_ms = timed(step_host, max(1, args.steps // 2)) / max(1, args.steps // 2)
+    h2d = C.sizeof(spec_all) + 8 * (9 + 5 + 45)
+    sweep_call(out_host, 0)
+    e2e_steps = max(1, args.steps // 2)
+    e2e_ms = timed(lambda: sweep_call(out_host, 0), e2e_steps) / e2e_steps
     e2e = total_evals / (e2e_ms / 1e3)
 
-    # parity spot check of this run's first scenario against the oracle
-    parity = None
-    if rank == 0 and args.check:
-        from oracle_lib import port
-        pred, plen = port().generate_scenarios(c4_spec(1, count=args.prompts, first=0))
-        tt, cc, ns = port().sweep_arrays(pred, plen, 1, args.prompts, prof, args.G, args.n_min,
-                                         args.n_max, args.lam, 2)
-        got_t = t_total[:n_cand].cpu().numpy()
-        parity = bool(np.array_equal(got_t.view(np.uint64), tt[0].view(np.uint64)) and
-                      int(n_star[0].item()) == int(ns[0]))
+    # bit-exactness of sampled scenarios of every rank's block (outside timing)
+    sweep_call(out_dev, 1)
+    torch.cuda.synchronize()
+    n_chk, ok = (0, None)
+    if args.check:
+        n_chk, ok = parity_sample(args, world, rank, S, s0, t_total, cost, idle, n_star, n_cand)
+        if world > 1:
+            v = torch.tensor([n_chk, 1 if ok else 0], dtype=torch.int64, device=dev)
+            dist.all_reduce(v[:1])
+            dist.all_reduce(v[1:], op=dist.ReduceOp.MIN)
+            n_chk, ok = int(v[0].item()), bool(v[1].item())
 
     peak, peak_kind = peaks()
+    ge_ms, ge_n = kt["group_eval"]
     ge_avg_ms = ge_ms / max(ge_n, 1)
     per_launch_evals = total_evals / world * args.steps / max(ge_n, 1)
-    achieved = per_launch_evals * EVAL_BYTES / (ge_avg_ms / 1e3) / 1e9
-    # ncu dram read+write per launch (profiles/traffic.json: per eval x evals per launch)
-    bpe = _profile_traffic("group_eval_dram_bytes_per_eval")
-    traffic = bpe * per_launch_evals if bpe else None
+    clocks = clk.summary()
+    sm_mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+    n_sm = torch.cuda.get_device_properties(local).multi_processor_count
+    # The dominant kernel is issue-bound integer + FP64-scalar code (no
+    # contraction, DRAM ~3 % busy): its roofline is the SM issue rate, 4 warp
+    # instructions per SM per cycle. achieved = ncu's warp instructions per
+    # eval (committed capture) x evals per launch / the live launch time.
+    inst_pe = counters("group_eval_inst_issued_per_eval")
+    dram_pe = counters("group_eval_dram_bytes_per_eval")
+    issue_peak = n_sm * 4 * sm_mhz * 1e6 / 1e9  # G warp-inst/s
+    achieved_issue = (inst_pe * per_launch_evals / (ge_avg_ms / 1e3) / 1e9) if inst_pe else None
+    traffic = dram_pe * per_launch_evals if dram_pe else None
+    ref_equiv = per_launch_evals * EVAL_BYTES / (ge_avg_ms / 1e3) / 1e9
     result = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -355,17 +441,36 @@ def run_ours(args, world, rank, local):
         "data": "synthetic (device-generated Monte-Carlo scenarios, DESIGN.md §4.1)",
         "config": config(args, world),
         "e2e": {"value": e2e, "unit": "evals/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h * world},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": "group_eval",
-                     "peak_kind": peak_kind, "launch_ms": ge_avg_ms,
-                     "algorithmic_bytes_per_launch": per_launch_evals * EVAL_BYTES,
-                     "kernel_share_of_step": ge_ms / attr_ms if attr_ms else None},
+                "d2h_bytes_per_step": d2h * world,
+                "path": "rs_sweep / rs_sweep_sharded with pinned host outputs (C-ABI)"},
+        "roofline": {
+            "bound": "issue", "kernel": "group_eval (lockstep_eval_kernel)",
+            "achieved": achieved_issue, "peak": issue_peak, "unit": "G warp-inst/s",
+            "frac": achieved_issue / issue_peak if achieved_issue else None,
+            "inst_issued_per_eval": inst_pe, "sm_mhz": sm_mhz, "sms": n_sm,
+            "traffic": traffic,
+            "dram_frac": (traffic / (ge_avg_ms / 1e3) / 1e9 / peak) if traffic else None,
+            "hbm_peak_gbs": peak, "peak_kind": peak_kind,
+            "ref_equiv_frac": ref_equiv / peak,
+            "ref_equiv_note": "SURVEY §8d reference-equivalent bytes (786,448 B per eval) / HBM peak; "
+                              "reuse accounting, not a bound",
+            "launch_ms": ge_avg_ms, "evals_per_launch": per_launch_evals,
+            "counters_source": "profiles/kernel_counters.json",
+            "kernel_share_of_step": ge_ms / attr_ms if attr_ms else None},
+        "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kt.items() if v[1]},
         "gpu_launches": int(launches),
-        "parity_first_scenario": parity,
+        "parity_sampled": {"scenarios": n_chk, "ok": ok, "of": args.scenarios,
+                           "fields": "t_total, cost, idle_slot_ticks, n_star bitwise vs oracle/rs_oracle.c"},
     }
+    if comm is not None:
+        result["n_star_aggregate"] = pick.value
+        result["collective"] = "one NCCL all-reduce of 3 x C doubles inside librs_b200 (rs_sweep_sharded)"
     if rank == 0:
-        result["clocks"] = clk.summary()
+        result["clocks"] = clocks
+        if world == 1 and not args.no_arrays:
+            result["e2e_arrays"] = bench_arrays(args, ctx, torch, dev, ps)
+        if world == 1 and not args.no_c3:
+            result["c3"] = bench_c3(args)
         if world == 1 and not args.no_dedup:
             result["dedup"] = bench_dedup(args, ctx, torch, dev, stream)
         if world == 1 and not args.no_cpu:
@@ -375,9 +480,83 @@ def run_ours(args, world, rank, local):
         if world == 1 and not args.no_trace:
             result["trace"] = bench_trace(args, ctx, torch, dev)
         print(json.dumps(result), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def bench_arrays(args, ctx, torch, dev, ps):
+    """The sweep over CALLER arrays (rs_sweep_arrays: the reference API's input
+    form, predicted lengths from the caller) with pinned HOST inputs and
+    outputs: every step copies S x P x 12 B of inputs in (batch i+1's H2D on
+    its own stream while batch i computes) and the results out."""
+    from cases import c4_spec
+    from paper_2602_22718_b200 import _abi
+    from paper_2602_22718_b200.lib import check
+    S, P, n_cand = args.arrays_scenarios, args.prompts, args.n_max - args.n_min + 1
+    pred = torch.empty(S * P, dtype=torch.float64, pin_memory=True)
+    plen = torch.empty(S * P, dtype=torch.int32, pin_memory=True)
+    spec = c4_spec(S, count=P, first=0)
+    check(ctx.lib.rs_generate_scenarios(ctx.handle, C.byref(spec), C.c_void_p(pred.data_ptr()),
+                                        C.c_void_p(plen.data_ptr()), 0))
+    outs = [torch.empty(S * n_cand, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    idle = torch.empty(S * n_cand, dtype=torch.int64, pin_memory=True)
+    ns = torch.empty(S, dtype=torch.int32, pin_memory=True)
+    so = _abi.RsSweepOut(outs[0].data_ptr(), outs[1].data_ptr(), idle.data_ptr(), ns.data_ptr(),
+                         None, None, None)
+
+    def call():
+        check(ctx.lib.rs_sweep_arrays(ctx.handle, C.c_void_p(pred.data_ptr()),
+                                      C.c_void_p(plen.data_ptr()), S, P, C.byref(ps), args.G,
+                                      args.n_min, args.n_max, args.lam, 2, C.byref(so), 0))
+
+    call()
+    torch.cuda.synchronize()
+    k = 2
+    t0 = time.perf_counter()
+    for _ in range(k):
+        call()
+    dt = (time.perf_counter() - t0) / k
+    return {"metric": METRIC + " from caller arrays", "value": S * n_cand / dt, "unit": "evals/s",
+            "ms_per_step": dt * 1e3, "scenarios": S,
+            "h2d_bytes_per_step": S * P * 12, "d2h_bytes_per_step": S * n_cand * 24 + S * 4,
+            "h2d_gbs": S * P * 12 / dt / 1e9,
+            "path": "rs_sweep_arrays, pinned host inputs and outputs (host wall clock)"}
+
+
+def bench_c3(args):
+    """C3 (BASELINE config 3): scale() over one 65,536-prompt x G=8 scenario,
+    N in [1, 512], through the C++ drop-in (rollsim::scale over the C-ABI)
+    and the unmodified reference, both on this host (build/shim/c3_bench_*)."""
+    from cases import c4_spec
+    from oracle_lib import port
+    out = {}
+    pred, plen = port().generate_scenarios(c4_spec(1, count=65536, first=0))
+    path = REPO / "gpurun_out" / "c3_scenario.bin"
+    path.parent.mkdir(exist_ok=True)
+    with open(path, "wb") as f:
+        f.write(np.int64(len(pred)).tobytes() + pred.tobytes() + plen.astype(np.int32).tobytes())
+    for arm, reps in (("b200", 5), ("ref", 1)):
+        exe = REPO / "build" / "shim" / f"c3_bench_{arm}"
+        if not exe.exists():
+            return {"unavailable": "build/shim not built (make shim)"}
+        cmd = [str(exe), str(path), str(reps), "512"] + (["nowarm"] if arm == "ref" else [])
+        p = subprocess.run(cmd, capture_output=True, text=True, timeout=1200)
+        if p.returncode != 0:
+            return {"unavailable": f"c3_bench_{arm} exit {p.returncode}: {p.stderr[-300:]}"}
+        out[arm] = json.loads(p.stdout.strip().splitlines()[-1])
+    b, r = out["b200"], out["ref"]
+    return {"metric": "C3 scale() calls/sec (65,536 prompts x G=8, N in [1, 512])",
+            "value": 1e3 / b["ms_per_call"], "unit": "calls/s", "ms_per_call": b["ms_per_call"],
+            "evals_per_s": 512 * 1e3 / b["ms_per_call"],
+            "reference_ms_per_call": r["ms_per_call"],
+            "identical_to_reference": b["digest"] == r["digest"] and b["n_star"] == r["n_star"],
+            "n_star": b["n_star"], "path": "rollsim::scale (C++ drop-in, string ids ranked on the "
+                                           "device, groups of N* materialised) vs the reference",
+            "cpu_baseline": {"value": 1e3 / r["ms_per_call"], "unit": "calls/s", "cores": 1,
+                             "kind": "reference", "sample": "one scale() call, 1 thread"}}
 
 
 def bench_trace(args, ctx, torch, dev):
@@ -557,7 +736,20 @@ def bench_dedup(args, ctx, torch, dev, stream):
     return out
 
 
-def main():
+def relaunch_cmd(argv, n, port):
+    """The torchrun command that runs this bench on n ranks (one per GPU)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", str(REPO / "bench.py"), *argv]
+
+
+def free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -570,13 +762,31 @@ def main():
     ap.add_argument("--G", type=int, default=8)
     ap.add_argument("--lam", type=float, default=0.7)
     ap.add_argument("--cpu-rounds", type=int, default=4)
+    ap.add_argument("--arrays-scenarios", type=int, default=2368,
+                    help="scenarios of the e2e_arrays line (host inputs: 786 KB each)")
+    ap.add_argument("--parity-samples", type=int, default=64)
+    ap.add_argument("--parity-full", action="store_true", help="bit-check every scenario")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dedup", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-c3", action="store_true")
+    ap.add_argument("--no-arrays", action="store_true")
     ap.add_argument("--no-trace", action="store_true")
-    ap.add_argument("--check", action="store_true", default=True)
-    args = ap.parse_args()
+    ap.add_argument("--no-check", dest="check", action="store_false")
+    raw = sys.argv[1:] if argv is None else argv
+    args = ap.parse_args(raw)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch under torchrun (the driver may call
+        # `bench.py --gpus N` directly); NCCL's communicator log stays on so
+        # the rank count is visible in stderr
+        env = dict(os.environ)
+        sys.exit(subprocess.call(relaunch_cmd(raw, args.gpus, free_port()), env=env))
     world, rank, local = init_dist()
+    if world > 1:  # NCCL's communicator log (ranks, NVLS / NVLink paths) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, world, rank)
         return

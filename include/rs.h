@@ -406,6 +406,46 @@ int rs_sweep_select(const double* sum_t, const double* sum_c,
                     double lambda, int32_t* n_star);
 
 /* ------------------------------------------------------------------ */
+/* Multi-GPU sweep. Scenarios shard in contiguous blocks    */
+/* ([S*r/W, S*(r+1)/W) on rank r) with no data-path exchange; the one    */
+/* collective is a single NCCL all-reduce of the packed per-candidate    */
+/* aggregates (3 x C doubles), after which every rank computes the       */
+/* aggregate pick (as rs_sweep_select). NCCL is loaded at run time       */
+/* (libnccl.so.2); without it these calls fail with RS_E_CUDA and the    */
+/* single-GPU API is unaffected. The unit being sharded is scale()       */
+/* (proj/src/planner.cpp:159-218).                                        */
+/* ------------------------------------------------------------------ */
+#define RS_COMM_ID_BYTES 128
+typedef struct rs_comm rs_comm;
+/* One process per GPU: rank 0 makes the id, the caller ships it to every
+ * rank out of band (e.g. over its launcher's store), each rank joins. */
+int rs_comm_unique_id(uint8_t* id /* RS_COMM_ID_BYTES */);
+int rs_comm_init(rs_ctx* ctx, const uint8_t* id, int32_t n_ranks, int32_t rank, rs_comm** out);
+int rs_comm_destroy(rs_comm* comm);
+/* spec describes the WHOLE sweep; this rank evaluates its block. The
+ * per-scenario outputs of `out` hold this rank's block (scenario-major from
+ * its first scenario); sum_t / sum_c / nstar_hist receive the all-reduced
+ * aggregates over every rank; *n_star_all (nullable) the aggregate pick.
+ * Synchronous, like rs_sweep. */
+int rs_sweep_sharded(rs_ctx* ctx, rs_comm* comm, const rs_scenario_spec* spec,
+                     const rs_profile* profile, int32_t responses_per_prompt, int32_t n_min,
+                     int32_t n_max, double lambda, int32_t gpus_per_actor, rs_sweep_out* out,
+                     int device_ptrs, int32_t* n_star_all);
+
+/* One process driving several GPUs (one host thread each): the handle owns
+ * a context per device and an NCCL clique over them. */
+typedef struct rs_multi rs_multi;
+int rs_multi_create(const int32_t* devices, int32_t n_devices, rs_multi** out);
+int rs_multi_size(const rs_multi* m, int32_t* n_devices);
+int rs_multi_context(rs_multi* m, int32_t index, rs_ctx** out);
+int rs_multi_destroy(rs_multi* m);
+/* The whole sweep over the handle's devices; `out` holds HOST arrays for
+ * every scenario (as rs_sweep with device_ptrs = 0). */
+int rs_multi_sweep(rs_multi* m, const rs_scenario_spec* spec, const rs_profile* profile,
+                   int32_t responses_per_prompt, int32_t n_min, int32_t n_max, double lambda,
+                   int32_t gpus_per_actor, rs_sweep_out* out, int32_t* n_star_all);
+
+/* ------------------------------------------------------------------ */
 /* LPT extension: responses (prompt i, r<G) of length  */
 /* ceil(pred_i) sorted (len desc, id_rank asc, r asc) are placed one by */
 /* one on the least-loaded actor (ties -> lowest index).               */

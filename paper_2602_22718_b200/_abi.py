@@ -123,6 +123,17 @@ PRODUCT_SIGS = {
                          C.POINTER(RsSweepOut), C.c_int], C.c_int),
     "rs_sweep_select": ([P_f64, P_f64, i64, i32, i32, f64, P_i32], C.c_int),
     "rs_lpt": ([vp, P_f64, P_i32, i32, i32, i32, i32, P_i64, P_i64], C.c_int),
+    "rs_comm_unique_id": ([vp], C.c_int),
+    "rs_comm_init": ([vp, vp, i32, i32, C.POINTER(vp)], C.c_int),
+    "rs_comm_destroy": ([vp], C.c_int),
+    "rs_sweep_sharded": ([vp, vp, C.POINTER(RsScenarioSpec), P_prof, i32, i32, i32, f64, i32,
+                          C.POINTER(RsSweepOut), C.c_int, P_i32], C.c_int),
+    "rs_multi_create": ([P_i32, i32, C.POINTER(vp)], C.c_int),
+    "rs_multi_size": ([vp, P_i32], C.c_int),
+    "rs_multi_context": ([vp, i32, C.POINTER(vp)], C.c_int),
+    "rs_multi_destroy": ([vp], C.c_int),
+    "rs_multi_sweep": ([vp, C.POINTER(RsScenarioSpec), P_prof, i32, i32, i32, f64, i32,
+                        C.POINTER(RsSweepOut), P_i32], C.c_int),
 }
 
 # Plain-C oracle surface shared by ref_* and orc_* (oracle/oracle.h).

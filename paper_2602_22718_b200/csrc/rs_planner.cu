@@ -415,6 +415,17 @@ __global__ void aggregate_kernel(int S, int C, int n_min, const double* t_total,
   }
 }
 
+// {sum_t, sum_c, (double) hist} packed for the one cross-rank all-reduce
+// (rs_comm.cu; counts are exact in FP64).
+__global__ void pack_aggregates_kernel(int C, const double* sum_t, const double* sum_c,
+                                       const int32_t* hist, double* pack) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < C; i += gridDim.x * blockDim.x) {
+    pack[i] = sum_t[i];
+    pack[C + i] = sum_c[i];
+    pack[2 * C + i] = (double)hist[i];
+  }
+}
+
 // ------------------------------------------------------ input shaping --
 // Scatter caller SoA into id order (id_rank[i] = rank of prompt i's id) and
 // validate. The bucketed / generic builders then treat the position as the
@@ -798,7 +809,7 @@ static int bounce_reserve(rs_ctx* ctx, size_t bytes) {
 static int sweep_pass(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h_pred,
                       const int32_t* h_plen, int S, int P, const DevProfile& dp, int G,
                       int n_min, int n_max, double lambda, int gpus, rs_sweep_out* out,
-                      int device_ptrs, bool allow_fast_in, bool* redo) {
+                      int device_ptrs, bool allow_fast_in, bool* redo, double* agg_pack) {
   *redo = false;
   const int C = n_max - n_min + 1;
   const int64_t T = groups_per_scenario(n_min, n_max);
@@ -1041,6 +1052,9 @@ static int sweep_pass(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
     if (out->nstar_hist)
       RS_CUDA_TRY(cudaMemcpyAsync(out->nstar_hist, agg_h, 4 * C, cudaMemcpyDeviceToDevice, ctx->stream));
   }
+  if (agg_pack)
+    RS_LAUNCH(ctx, "pack_aggregates", pack_aggregates_kernel, (C + 255) / 256, 256, 0, C, agg_t,
+              agg_c, agg_h, agg_pack);
   int fl;
   RS_TRY(read_flags(ctx, &fl));  // synchronises the context stream
   if (ctx->timing) RS_TRY(collect_timers(ctx));
@@ -1053,22 +1067,76 @@ static int sweep_pass(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
   return RS_OK;
 }
 
+// Argument checks of a sweep, in scale()'s order (planner.cpp:164-168) —
+// also run by every rank of a sharded sweep before its collective, so a
+// rank with no scenarios fails exactly like the others.
+int sweep_validate(const rs_scenario_spec* spec, const rs_profile* profile, int P, int G,
+                   int n_min, int n_max, double lambda) {
+  if (spec) RS_TRY(check_spec(spec));
+  RS_TRY(check_scale_args(P, G, n_min, n_max, lambda));
+  return validate_profile_shape(profile);
+}
+
 // Shared sweep driver: scenarios either generated (spec) or from arrays.
 // Synchronous: it returns once every result (device or host) is written.
-static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h_pred,
+// agg_pack (device, nullable): also receives the packed aggregates.
+int sweep_impl_packed(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h_pred,
                       const int32_t* h_plen, int S, int P, const rs_profile* profile, int G,
                       int n_min, int n_max, double lambda, int gpus, rs_sweep_out* out,
-                      int device_ptrs) {
+                      int device_ptrs, double* agg_pack) {
   RS_TRY(check_scale_args(P, G, n_min, n_max, lambda));
   DevProfile dp;
   RS_TRY(get_profile(ctx, profile, &dp));
   bool redo = false;
   RS_TRY(sweep_pass(ctx, spec, h_pred, h_plen, S, P, dp, G, n_min, n_max, lambda, gpus, out,
-                    device_ptrs, true, &redo));
+                    device_ptrs, true, &redo, agg_pack));
   if (redo)
     RS_TRY(sweep_pass(ctx, spec, h_pred, h_plen, S, P, dp, G, n_min, n_max, lambda, gpus, out,
-                      device_ptrs, false, &redo));
+                      device_ptrs, false, &redo, agg_pack));
   return redo ? fail(RS_E_CUDA, "internal: generic sweep pass flagged the fast path") : RS_OK;
+}
+
+static int sweep_impl(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h_pred,
+                      const int32_t* h_plen, int S, int P, const rs_profile* profile, int G,
+                      int n_min, int n_max, double lambda, int gpus, rs_sweep_out* out,
+                      int device_ptrs) {
+  return sweep_impl_packed(ctx, spec, h_pred, h_plen, S, P, profile, G, n_min, n_max, lambda,
+                           gpus, out, device_ptrs, nullptr);
+}
+
+// Aggregate pick over a whole sweep (host, O(C)): mean t and mean c, min-max
+// normalised like scale() (planner.cpp:196-209), first strict minimum.
+int sweep_select_host(const double* sum_t, const double* sum_c, int64_t n_scenarios, int C,
+                      int n_min, double lambda, int32_t* n_star) {
+  if (!sum_t || !sum_c || !n_star || C < 1 || n_scenarios < 1)
+    return fail(RS_E_ARG, "bad arguments");
+  if (lambda < 0 || lambda > 1) return fail(RS_E_CONFIG, "lambda must be in [0, 1]");
+  std::vector<double> mt(C), mc(C);
+  for (int i = 0; i < C; ++i) {
+    mt[i] = sum_t[i] / (double)n_scenarios;
+    mc[i] = sum_c[i] / (double)n_scenarios;
+  }
+  double t_min = mt[0], t_max = mt[0], c_min = mc[0], c_max = mc[0];
+  for (int i = 0; i < C; ++i) {
+    t_min = mt[i] < t_min ? mt[i] : t_min;
+    t_max = t_max < mt[i] ? mt[i] : t_max;
+    c_min = mc[i] < c_min ? mc[i] : c_min;
+    c_max = c_max < mc[i] ? mc[i] : c_max;
+  }
+  int best = 0;
+  double bs = 0;
+  for (int i = 0; i < C; ++i) {
+    double tn = t_max > t_min ? (mt[i] - t_min) / (t_max - t_min) : 0.0;
+    double cn = c_max > c_min ? (mc[i] - c_min) / (c_max - c_min) : 0.0;
+    double sc = lambda * tn + (1.0 - lambda) * cn;
+    if (i == 0) bs = sc;
+    if (sc < bs) {
+      best = i;
+      bs = sc;
+    }
+  }
+  *n_star = n_min + best;
+  return RS_OK;
 }
 
 // S caller item sets (host SoA), each its own scenario, in id order.
@@ -1356,35 +1424,7 @@ int rs_sweep_arrays(rs_ctx* ctx, const double* pred, const int32_t* plen, int32_
 
 int rs_sweep_select(const double* sum_t, const double* sum_c, int64_t n_scenarios,
                     int32_t C, int32_t n_min, double lambda, int32_t* n_star) {
-  if (!sum_t || !sum_c || !n_star || C < 1 || n_scenarios < 1)
-    return fail(RS_E_ARG, "bad arguments");
-  if (lambda < 0 || lambda > 1) return fail(RS_E_CONFIG, "lambda must be in [0, 1]");
-  std::vector<double> mt(C), mc(C);
-  for (int i = 0; i < C; ++i) {
-    mt[i] = sum_t[i] / (double)n_scenarios;
-    mc[i] = sum_c[i] / (double)n_scenarios;
-  }
-  double t_min = mt[0], t_max = mt[0], c_min = mc[0], c_max = mc[0];
-  for (int i = 0; i < C; ++i) {
-    t_min = mt[i] < t_min ? mt[i] : t_min;
-    t_max = t_max < mt[i] ? mt[i] : t_max;
-    c_min = mc[i] < c_min ? mc[i] : c_min;
-    c_max = c_max < mc[i] ? mc[i] : c_max;
-  }
-  int best = 0;
-  double bs = 0;
-  for (int i = 0; i < C; ++i) {
-    double tn = t_max > t_min ? (mt[i] - t_min) / (t_max - t_min) : 0.0;
-    double cn = c_max > c_min ? (mc[i] - c_min) / (c_max - c_min) : 0.0;
-    double sc = lambda * tn + (1.0 - lambda) * cn;
-    if (i == 0) bs = sc;
-    if (sc < bs) {
-      best = i;
-      bs = sc;
-    }
-  }
-  *n_star = n_min + best;
-  return RS_OK;
+  return sweep_select_host(sum_t, sum_c, n_scenarios, C, n_min, lambda, n_star);
 }
 
 // scale() with either a caller-provided penalty array (t_penalty) or the

@@ -76,3 +76,13 @@ def test_gloo_two_ranks_combine_matches_single_process():
         assert pick == want_pick
     assert int(h.sum()) == S
     assert port().sweep_select(st, sc, S, N_MIN, LAM) == want_pick
+
+
+def test_bench_relaunches_under_torchrun():
+    """`bench.py --gpus N` without WORLD_SIZE re-executes itself with one
+    process per GPU (the driver may launch it either way)."""
+    import bench
+    cmd = bench.relaunch_cmd(["--gpus", "4", "--steps", "2"], 4, 29555)
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd and "--master-port=29555" in cmd
+    assert cmd[-3:] == ["--gpus", "4", "--steps", "2"][-3:]
