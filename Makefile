@@ -9,7 +9,16 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo --fmad=false -std=c++17 -Iinclude -Xcompiler -
 LIB      := $(PKG)/librs_b200.so
 OBJDIR   := build/obj
 
-.PHONY: all lib oracle ref clean
+.PHONY: all lib oracle ref clean prof
+# Phase-timing build (tools/phases.py; RS_B200_LIB selects it): not the product.
+PROF_LIB := build/librs_b200_prof.so
+prof: $(PROF_LIB)
+build/objp/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p build/objp
+	$(NVCC) $(NVFLAGS) -DRS_PROFILE_PHASES -dc $< -o $@ 2> build/objp/$*.ptxas.log || (cat build/objp/$*.ptxas.log; exit 1)
+$(PROF_LIB): $(patsubst $(PKG)/csrc/%.cu,build/objp/%.o,$(SRCS))
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -cudart static -o $@ $^ -ldl
+
 all: lib oracle
 
 lib: $(LIB)

@@ -30,6 +30,41 @@
 
 namespace rs {
 
+#ifdef RS_PROFILE_PHASES
+// Phase timing (a separate profiling build only): accumulated %globaltimer
+// nanoseconds (fast_build, thread 0 of each CTA) and SM cycles (lockstep,
+// lane 0 of each warp) per phase.
+__device__ unsigned long long g_phase[32];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define RS_PH_INIT unsigned long long ph_t = threadIdx.x == 0 ? gtimer() : 0ull
+#define RS_PH(slot)                                                    \
+  do {                                                                 \
+    if (threadIdx.x == 0) {                                            \
+      const unsigned long long n_ = gtimer();                          \
+      atomicAdd(&g_phase[slot], n_ - ph_t);                            \
+      ph_t = n_;                                                       \
+    }                                                                  \
+  } while (0)
+#define RS_LS_INIT long long ls_t = clock64()
+#define RS_LS(slot)                                                    \
+  do {                                                                 \
+    if ((threadIdx.x & 31) == 0) {                                     \
+      const long long n_ = clock64();                                  \
+      atomicAdd(&g_phase[slot], (unsigned long long)(n_ - ls_t));      \
+      ls_t = n_;                                                       \
+    }                                                                  \
+  } while (0)
+#else
+#define RS_PH_INIT
+#define RS_PH(slot)
+#define RS_LS_INIT
+#define RS_LS(slot)
+#endif
+
 size_t fast_ss_bytes(int64_t items, int S) {
   int64_t segs = items + S;
   return abytes(segs, 8) * 2 + abytes(S, 4) + abytes(items, 8) + abytes(items, 4) * 2 +
@@ -94,6 +129,7 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
   __shared__ int2 s_scan[2][2][kHalfT / 32];  // per half: warp totals of the max scans
   const int s = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  RS_PH_INIT;
   const int64_t i0 = ss.item_off[s];
   const int P = (int)(ss.item_off[s + 1] - i0);
   const int64_t so = i0 + s;
@@ -133,6 +169,7 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
   }
   if (lf) atomicOr(&bad, lf);
   __syncthreads();
+  RS_PH(0);
   if (bad) {
     if (tid == 0) atomicOr(flags, bad);
     return;
@@ -195,6 +232,7 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
     cfb += (long long)cnt[j] * f;
   }
   __syncthreads();
+  RS_PH(1);
   // Scatter 16-byte records {pred bits, id, plen | segment << 16} into the
   // buckets (bucket order: finish tick descending).
   constexpr int kScat = 4;  // loads batched ahead of the atomics
@@ -224,6 +262,7 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
     }
   }
   __syncthreads();
+  RS_PH(2);
   // Order each bucket (pred desc, id asc) — planner.cpp:121-126 ranks by
   // predicted length — one window of whole buckets (<= kWide records) at a
   // time in shared memory: every record counts the records of its bucket
@@ -263,6 +302,7 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
     s_nw = nw;
   }
   __syncthreads();
+  RS_PH(3);
   if (s_nw < 0) {
     if (tid == 0) atomicOr(flags, kFlagBucketTooWide);
     return;
@@ -471,6 +511,7 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
   // maxima and the all-pairs range maxima, then a sparse table over block
   // maxima (levels double the span).
   __syncthreads();
+  RS_PH(4);
   const int nblk = (D + kBlk - 1) / kBlk;
   uint16_t* st = ss.st + (int64_t)s * kStStride;
   for (int jb = tid; jb < nblk; jb += kBuildT) {
@@ -521,6 +562,7 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
           max(st[(lev - 1) * kStBlocks + jb], st[(lev - 1) * kStBlocks + jb + (1 << (lev - 1))]);
     __syncthreads();
   }
+  RS_PH(5);
 }
 
 int fast_build(rs_ctx* ctx, int S, const int64_t* d_off, double* pred, int32_t* plen,
@@ -581,6 +623,8 @@ constexpr uint16_t kPexToEnd = 0xffff;
 
 struct FastProf {
   const double* top;
+  const double* top_full;   // tpot(clamped batch, c) unhalved (DevProfile::top_row)
+  const double* rows_full;  // unhalved rows, live = 1 .. live_top (the last = top_full)
   const double* rows;
   const uint16_t* pex;
   int c_lo, c_hi, cf_ceil, cb_ceil, cfront_m1, ncm, live_top;
@@ -963,7 +1007,7 @@ __global__ void __launch_bounds__(kEvalT, 1) fast_eval_kernel(EvalArgs A) {
 
 // Small-batch tpot rows and piece ends of one (profile, G).
 __global__ void fast_tables_kernel(DevProfile p, int G, int live_top, double* rows, double* top,
-                                   uint16_t* pex, int cf_ceil, int cb_ceil) {
+                                   uint16_t* pex, int cf_ceil, int cb_ceil, double* rows_full) {
   const int64_t ncm = p.c_hi - p.c_lo + 1;
   const int64_t nrows = (int64_t)(live_top - 1) * ncm;
   const int64_t total = nrows + ncm + ncm + 1;
@@ -971,9 +1015,12 @@ __global__ void fast_tables_kernel(DevProfile p, int G, int live_top, double* ro
        i += (int64_t)gridDim.x * blockDim.x) {
     if (i < nrows) {
       const int64_t live = i / ncm + 1, j = i % ncm;
-      rows[i] = dmul(tpot_int(p, (int64_t)G * live, p.c_lo + j), 0.5);
+      const double t = tpot_int(p, (int64_t)G * live, p.c_lo + j);
+      rows[i] = dmul(t, 0.5);
+      rows_full[i] = t;
     } else if (i < nrows + ncm) {
       top[i - nrows] = dmul(p.top_row[i - nrows], 0.5);
+      rows_full[i] = p.top_row[i - nrows];
     } else {
       // piece end for c = c_lo - 1 + j, j in [0, ncm] (run-sum pieces,
       // planner.cpp:65-74): below front -> ceil(front) - 1; at or above
@@ -1000,7 +1047,7 @@ bool fast_profile_ok(const DevProfile& prof, int G) {
 size_t fast_eval_bytes(const DevProfile& prof, int G) {
   const int64_t ncm = prof.c_hi - prof.c_lo + 1;
   const int64_t live_top = std::max<int64_t>(1, (prof.b_hi + G - 1) / G);
-  return abytes(live_top * ncm, 8) + abytes(ncm + 1, 2) +
+  return abytes(live_top * ncm, 8) * 2 + abytes(ncm + 1, 2) +
          abytes((size_t)1024 * kMaxSeg, 4);
 }
 
@@ -1012,10 +1059,13 @@ static int fast_prof_make(rs_ctx* ctx, const DevProfile& prof, int G, FastProf* 
   double* rows = arena_alloc<double>(ctx, (int64_t)live_top * ncm);
   double* top = rows ? rows + (int64_t)(live_top - 1) * ncm : nullptr;
   uint16_t* pex = arena_alloc<uint16_t>(ctx, ncm + 1);
-  if (!rows || !top || !pex) return fail(RS_E_NOMEM, "arena exhausted (tpot tables)");
+  double* rows_full = arena_alloc<double>(ctx, (int64_t)live_top * ncm);
+  if (!rows || !top || !pex || !rows_full) return fail(RS_E_NOMEM, "arena exhausted (tpot tables)");
   const double front = prof.ck_front, back = prof.ck_back;
   FastProf& fp = *out;
   fp.top = top;
+  fp.top_full = prof.top_row;
+  fp.rows_full = rows_full;
   fp.rows = rows;
   fp.pex = pex;
   fp.c_lo = (int)prof.c_lo;
@@ -1027,7 +1077,7 @@ static int fast_prof_make(rs_ctx* ctx, const DevProfile& prof, int G, FastProf* 
   fp.live_top = live_top;
   const int64_t tot = (int64_t)(live_top - 1) * ncm + 2 * ncm + 1;
   RS_LAUNCH(ctx, "fast_tables", fast_tables_kernel, (int)std::min<int64_t>((tot + 255) / 256, 4096),
-            256, 0, prof, G, live_top, rows, top, pex, fp.cf_ceil, fp.cb_ceil);
+            256, 0, prof, G, live_top, rows, top, pex, fp.cf_ceil, fp.cb_ceil, rows_full);
   return RS_OK;
 }
 
@@ -1082,7 +1132,7 @@ struct LsArgs {
   int S;
   int cand_units;  // units per scenario (candidate slices of kLsThreads)
   double* gt;
-  const uint2* gtab;     // per (scenario, flat group): see group_table_kernel
+  const uint4* gtab;     // per (scenario, flat group): see group_table_kernel
   const double* gfirst;  // per (scenario, flat group): value after the first run
 };
 
@@ -1121,7 +1171,7 @@ __device__ __forceinline__ int ls_range(const LsView& V, int l, int r) {
 // group, ticks 1 .. F_kb), i.e. the group's total after one run. The first
 // run spans the longest context range (often several knot pieces), so it is
 // evaluated here in parallel rather than inside the lockstep walk.
-__global__ void group_table_kernel(FastSS ss, FastProf fp, CandRange cr, int S, uint2* gtab,
+__global__ void group_table_kernel(FastSS ss, FastProf fp, CandRange cr, int S, uint4* gtab,
                                    double* gfirst) {
   if (*ss.flags & kFastBad) return;
   const int64_t total = (int64_t)S * cr.T;
@@ -1150,7 +1200,13 @@ __global__ void group_table_kernel(FastSS ss, FastProf fp, CandRange cr, int S, 
       smb = (int)(__ldg(V.pmsm + ka + 1) >> 16);
     }
     const int f = ss.seg[so + kb].x & 0xffff;
-    gtab[t] = make_uint2((uint32_t)ka | ((uint32_t)kb << 16), (uint32_t)va | ((uint32_t)smb << 16));
+    // the walk's per-group constants, decoded once here: the first block
+    // jl of (ka, kb] and the offset of row (ka + 1) & 15 of its all-pairs
+    // table inside a staged chunk (lockstep2_kernel)
+    const int l = ka + 1, jl = l >> 4, i = l & (kBlk - 1);
+    const uint32_t bqo = (uint32_t)((jl & 15) * kBlkPairs + i * (2 * kBlk + 1 - i) / 2 - i);
+    gtab[t] = make_uint4((uint32_t)ka | ((uint32_t)kb << 16), (uint32_t)va | ((uint32_t)smb << 16),
+                         bqo | ((uint32_t)jl << 16), (uint32_t)a);
     // run_sum(G * (b - a), top_m, top_m + f - 1) from the halved tables
     // (piece terms and their order as tpot_context_run_sum; 0.0 + x == x)
     const int clo = fp.c_lo, chi = fp.c_hi, clo1 = fp.c_lo - 1;
@@ -1176,7 +1232,7 @@ __global__ void group_table_kernel(FastSS ss, FastProf fp, CandRange cr, int S, 
 // table; n_star comes from block reductions with the reference's min/max and
 // first-strict-minimum semantics (planner.cpp:196-217).
 __global__ void __launch_bounds__(kLsThreads)
-fast_finish_kernel(FastSS ss, CandRange cr, const double* gt_all, const uint2* gtab_all,
+fast_finish_kernel(FastSS ss, CandRange cr, const double* gt_all, const uint4* gtab_all,
                    LsEpilogue ep) {
   __shared__ double r_d[4][kLsThreads / 32];
   __shared__ int r_i[kLsThreads / 32];
@@ -1215,7 +1271,7 @@ fast_finish_kernel(FastSS ss, CandRange cr, const double* gt_all, const uint2* g
       const int64_t i0 = ss.item_off[s], so = i0 + s;
       const int P = (int)(ss.item_off[s + 1] - i0);
       const int D = ss.nseg[s];
-      const uint2* gtab = gtab_all + gbase;
+      const uint4* gtab = gtab_all + gbase;
       const int q = P / N, rem = P % N;
       int64_t acc = 0;
       for (int h = 0; h < N; ++h) {
@@ -1279,158 +1335,253 @@ fast_finish_kernel(FastSS ss, CandRange cr, const double* gt_all, const uint2* g
   }
 }
 
-// kMinB = 1: compiled freely (61 registers, four CTAs per SM); kMinB =
-// kLsDenseCtas: capped at 48 registers (a few spills) so that five CTAs fit,
-// used only for batches the planner runs five deep (a rank's 1,250 scenarios
-// at 8 GPUs: two rounds of 740 slots instead of three of 444).
-template <int kMinB>
-__global__ void __launch_bounds__(kLsThreads, kMinB) lockstep_eval_kernel(LsArgs A) {
+// --------------------------------------------------- lockstep evaluator v2 --
+// Same walk, same FP64 operation order as lockstep_eval_kernel; the per-step
+// path is rebuilt around shared memory so a step costs a few dozen
+// instructions instead of ~100:
+//  - the scenario's segment entries, in-block maxima and in-block all-pairs
+//    tables are staged in chunks of 256 segments (16 blocks) by cp.async,
+//    double-buffered, one CTA barrier per chunk (every warp of the CTA walks
+//    the same k sequence), so the uniform per-step reads are LDS with 32-bit
+//    addressing instead of 64-bit LDGs;
+//  - the clamped-batch tpot row is held UNHALVED in shared memory: a one-tick
+//    run is then one load (the reference's 1 * (t + t) / 2.0 == t exactly),
+//    and a multi-piece run uses count * (t0 + t1) * 0.5, bitwise
+//    count * (t0/2 + t1/2) (halving commutes with round-to-nearest);
+//  - the group's first-block row offset in the all-pairs table is computed
+//    once per group.
+constexpr int kChunk = 256;                       // segments per staged chunk
+constexpr int kChunkBlk = kChunk / kBlk;          // 16 blocks
+constexpr int kChunkBq = kChunkBlk * kBlkPairs;   // 2,176 u16 (4,352 B)
+static_assert(kChunk == kLsThreads, "one staged segment per thread");
+
+struct Ls2Layout {
+  int top_off, tail_off, seg_off, pm_off, bq_off, pex_off, bytes;
+};
+
+__host__ __device__ inline Ls2Layout ls2_layout(int ncm, int live_top, bool top_in_smem) {
+  Ls2Layout L;
+  int o = 0;
+  L.top_off = o;
+  o += top_in_smem ? 8 * ncm : 0;
+  L.tail_off = o;
+  o += 8 * live_top;
+  o = (o + 15) & ~15;
+  L.seg_off = o;
+  o += 2 * kChunk * 8;
+  L.pm_off = o;
+  o += 2 * kChunk * 4;
+  L.bq_off = o;
+  o += 2 * kChunkBq * 2;
+  L.pex_off = o;
+  o += 2 * (ncm + 1);
+  L.bytes = (o + 15) & ~15;
+  return L;
+}
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// the unhalved top row goes to shared memory when 4 CTAs per SM still fit
+static int ls2_top_in_smem(int64_t ncm, int live_top) {
+  return ls2_layout((int)ncm, live_top, true).bytes <= 55 * 1024 ? 1 : 0;
+}
+
+template <int kMinB, bool kTopSmem>
+__global__ void __launch_bounds__(kLsThreads, kMinB) lockstep2_kernel(LsArgs A) {
+  constexpr int top_in_smem = kTopSmem ? 1 : 0;
   extern __shared__ __align__(16) unsigned char ls_smem[];
   if (*A.ss.flags & kFastBad) return;
   const FastProf& fp0 = A.fp;
-  double* s_tail = reinterpret_cast<double*>(ls_smem);
-  uint16_t* s_pex = reinterpret_cast<uint16_t*>(s_tail + fp0.live_top);
   const int clo = fp0.c_lo, chi = fp0.c_hi, clo1 = fp0.c_lo - 1, ncm = fp0.ncm;
   const int live_top = fp0.live_top;
+  const Ls2Layout L = ls2_layout(ncm, live_top, top_in_smem != 0);
+  double* s_top = reinterpret_cast<double*>(ls_smem + L.top_off);
+  double* s_tail = reinterpret_cast<double*>(ls_smem + L.tail_off);
+  int2* s_seg = reinterpret_cast<int2*>(ls_smem + L.seg_off);
+  uint32_t* s_pm = reinterpret_cast<uint32_t*>(ls_smem + L.pm_off);
+  uint16_t* s_bq = reinterpret_cast<uint16_t*>(ls_smem + L.bq_off);
+  uint16_t* s_pex = reinterpret_cast<uint16_t*>(ls_smem + L.pex_off);
   const double* rows = fp0.rows;
-  // tpot(G * live, c_hi) for live = 1 .. live_top (the halved entry doubled)
+  const double* rows_full = fp0.rows_full;
   for (int i = threadIdx.x; i < live_top; i += kLsThreads) {
     const double h = rows[(size_t)i * ncm + (ncm - 1)];
     s_tail[i] = dadd(h, h);
   }
+  if (top_in_smem)
+    for (int i = threadIdx.x; i < ncm; i += kLsThreads) s_top[i] = fp0.top_full[i];
   for (int i = threadIdx.x; i <= ncm; i += kLsThreads) s_pex[i] = fp0.pex[i];
-  __syncthreads();
   // Contexts c >= tail_from are past the memo (clamped to c_hi) and past the
-  // back knot (one piece to the run end): a run starting there is the single
-  // piece (f - fnext) * (t(c_hi) + t(c_hi)) / 2 = (f - fnext) * t(c_hi).
+  // back knot: a run starting there is the single piece (f - fnext) * t(c_hi).
   const int tail_from = max(chi, fp0.cb_ceil);
   const int C = A.cr.n_max - A.cr.n_min + 1;
   const int64_t flat0 = tri64(A.cr.n_min);
+  const int t = threadIdx.x;
   for (int unit = blockIdx.x; unit < A.S * A.cand_units; unit += gridDim.x) {
     const int s = unit / A.cand_units;
-    const int c = (unit % A.cand_units) * kLsThreads + threadIdx.x;
+    const int c = (unit % A.cand_units) * kLsThreads + t;
     const bool on = c < C;
     const int N = A.cr.n_min + (on ? c : 0);
     const int64_t i0 = A.ss.item_off[s];
     const int P = (int)(A.ss.item_off[s + 1] - i0);
     const int64_t so = i0 + s;
     const int D = A.ss.nseg[s];
-    LsView V{A.ss.seg + so, A.ss.pmsm + so, A.ss.st + (int64_t)s * kStStride,
-             A.ss.bq + (size_t)((so >> 4) + s) * kBlkPairs};
-    const int64_t gbase = (int64_t)s * A.cr.T + (tri64(N) - flat0);
-    double* gt = A.gt + gbase;
-    const uint2* gtab = A.gtab + gbase;
-    const double* gfirst = A.gfirst + gbase;
-    const int q = P / N, rem = P % N;
-    // Current group (g, counting down from N-1). Its first run (k = kb) is
-    // preloaded into `total`; steps ka <= k < kb evaluate one run each.
-    int g = N - 1, a = 0, b = 0, ka = 0, kb = 0, va = 0, l = 0, jl = 0;
-    int smb = 0, cjr = -1, cbase = 0;
+    const int2* g_seg = A.ss.seg + so;
+    const uint32_t* g_pm = A.ss.pmsm + so;
+    const uint16_t* g_bq = A.ss.bq + (size_t)((so >> 4) + s) * kBlkPairs;
+    const uint16_t* g_st = A.ss.st + (int64_t)s * kStStride;
+    const int nblk = (D + kBlk - 1) / kBlk;
+    // stage chunk ch (segments [256 ch, 256 ch + 256)) into buffer b
+    auto stage = [&](int ch, int b) {
+      const int k = ch * kChunk + t;
+      if (k < D) {
+        cp_async8(s_seg + b * kChunk + t, g_seg + k);
+        cp_async4(s_pm + b * kChunk + t, g_pm + k);
+      }
+      const int jb0 = ch * kChunkBlk;
+      const int nb = min(kChunkBlk, nblk - jb0);  // blocks of this chunk that exist
+      const uint4* src = reinterpret_cast<const uint4*>(g_bq + (size_t)jb0 * kBlkPairs);
+      uint4* dst = reinterpret_cast<uint4*>(s_bq + b * kChunkBq);
+      for (int i = t; i < nb * (kBlkPairs / 8); i += kLsThreads) cp_async16(dst + i, src + i);
+      cp_async_commit();
+    };
+    __syncthreads();  // the previous unit's readers are done with the buffers
+    int k = D - 1;
+    int ch = k >= 0 ? k / kChunk : 0;
+    if (D > 0) {
+      stage(ch, ch & 1);
+      cp_async_wait_all();
+      __syncthreads();
+      if (ch > 0) stage(ch - 1, (ch - 1) & 1);
+    }
+    // running pointers at the current group g (counting down from N - 1)
+    const int64_t gbase = (int64_t)s * A.cr.T + (tri64(N) - flat0) + (N - 1);
+    double* gtp = A.gt + gbase;
+    const uint4* gtabp = A.gtab + gbase;
+    const double* gfp = A.gfirst + gbase;
+    int g = N - 1, a = 0, ka = 0, kb = 0, va = 0, jl = 0, smb = 0, cjr = -1, cbase = 0, bqo = 0;
     double total = 0.0;
     bool done = !on;
-    uint2 nxt = make_uint2(0u, 0u);
+    uint4 nxt = make_uint4(0u, 0u, 0u, 0u);
     double nfirst = 0.0;
-    auto enter = [&](uint2 e, double first) {  // start group g
-      a = g * q + min(g, rem);
-      b = a + q + (g < rem ? 1 : 0);
+    auto enter = [&](uint4 e, double first) {  // start group g (entry decoded by group_table)
       ka = (int)(e.x & 0xffffu);
       kb = (int)(e.x >> 16);
       va = (int)(e.y & 0xffffu);
       smb = (int)(e.y >> 16);
-      l = ka + 1;
-      jl = l >> 4;
+      bqo = (int)(e.z & 0xffffu);
+      jl = (int)(e.z >> 16);
+      a = (int)e.w;
       cjr = -1;
       total = first;
       if (g > 0) {  // prefetch the next group's entry
-        nxt = __ldg(gtab + g - 1);
-        nfirst = __ldg(gfirst + g - 1);
+        nxt = __ldg(gtabp - 1);
+        nfirst = __ldg(gfp - 1);
       }
     };
-    if (on) enter(__ldg(gtab + g), __ldg(gfirst + g));
+    if (on) enter(__ldg(gtabp), __ldg(gfp));
     int fnext = 0;  // finish tick of segment k + 1 (uniform)
-    // segment k's entry and in-block maxima are the same for every lane:
-    // fetched one step ahead to take their latency off the k chain
-    int2 sk_n = make_int2(0, 0);
-    uint32_t pm_n = 0;
-    if (D > 0) {
-      sk_n = __ldg(&V.seg[D - 1]);
-      pm_n = __ldg(V.pmsm + D - 1);
-    }
-    auto complete = [&](int k) {  // groups completing at segment k
-      while (!done && k == ka) {
-        gt[g] = total;
-        if (g == 0) {
-          done = true;
-        } else {
-          --g;
-          enter(nxt, nfirst);
-        }
-      }
-    };
-    int k = D - 1;
-    // Phase 1 (fnext < tail_from): runs may start inside the memo.
-    for (; k >= 0 && fnext < tail_from; --k) {
-      const int2 sk = sk_n;
-      const uint32_t pmk = pm_n;
-      if (k > 0) {
-        sk_n = __ldg(&V.seg[k - 1]);
-        pm_n = __ldg(V.pmsm + k - 1);
-      }
-      const int f = sk.x & 0xffff;
-      const int jr = k >> 4;
-      if (!done && k < kb) {
-        // run k of group g: live ranks [a, E_k), base = max(va, MX over (ka, k])
-        int base = va;
-        if (k != ka) {
-          if (jr == jl) {
-            base = max(va, ls_inblock(V, l, k));
+    while (k >= 0) {
+      const int klo = ch * kChunk;
+      const int b = ch & 1;
+      const int2* cs = s_seg + b * kChunk - klo;
+      const uint32_t* cpm = s_pm + b * kChunk - klo;
+      const uint16_t* cbq = s_bq + b * kChunkBq;
+      auto complete = [&]() {  // groups completing at segment k
+        while (!done && k == ka) {
+          *gtp = total;
+          if (g == 0) {
+            done = true;
           } else {
-            if (jr != cjr) {
-              cjr = jr;
-              cbase = max(va, smb);
-              if (jl + 1 <= jr - 1) cbase = max(cbase, ls_blocks(V, jl + 1, jr - 1));
+            --g;
+            --gtp;
+            --gtabp;
+            --gfp;
+            enter(nxt, nfirst);
+          }
+        }
+      };
+      // Phase 1 (fnext < tail_from): runs may start inside the context memo.
+      for (; k >= klo && fnext < tail_from; --k) {
+        const int2 sk = cs[k];
+        const int f = sk.x & 0xffff;
+        const int df = f - fnext;  // uniform: ticks of run k
+        if (!done && k < kb) {
+          const int live = min(sk.y - a, live_top);
+          // base = max(va, MX over (ka, k]): the group's first block from its
+          // all-pairs row, a later block from cbase and the in-block prefix
+          // max (one u16 load from either table, no divergent branch)
+          const int jr = k >> 4;
+          const bool at_a = k == ka, first_blk = jr == jl;
+          if (!first_blk && !at_a && jr != cjr) {
+            cjr = jr;
+            cbase = max(va, smb);
+            if (jl + 1 <= jr - 1) {
+              const int len = jr - jl - 1;
+              const int lev = 31 - __clz(len);
+              cbase = max(cbase, (int)max(__ldg(g_st + lev * kStBlocks + jl + 1),
+                                          __ldg(g_st + lev * kStBlocks + jr - (1 << lev))));
             }
-            base = max(cbase, (int)(pmk & 0xffff));
           }
-        }
-        // tpot_context_run_sum (planner.cpp:61-84). The run has at least one
-        // context (f > fnext); its first piece term starts the sum
-        // (0.0 + x == x for the non-negative terms). Rows are contiguous:
-        // live >= live_top reads the clamped row.
-        const int live = min(sk.y - a, live_top);
-        int cc = base + fnext;
-        double rs;
-        if (cc >= tail_from) {
-          rs = dmul((double)(f - fnext), s_tail[live - 1]);
-        } else if (f - fnext == 1) {  // one context: 1 * (h + h) == h + h
-          const double h = __ldg(rows + (size_t)(live - 1) * ncm + (min(max(cc, clo), chi) - clo));
-          rs = dadd(h, h);
-        } else {
-          const int c1 = base + f - 1;
-          const double* row = rows + (size_t)(live - 1) * ncm - clo;
-          int pe = piece_end(s_pex, cc, c1, clo1, chi);
-          rs = piece_term(pe - cc + 1, __ldg(row + min(max(cc, clo), chi)),
-                          __ldg(row + min(max(pe, clo), chi)));
-          for (cc = pe + 1; cc <= c1; cc = pe + 1) {
-            pe = piece_end(s_pex, cc, c1, clo1, chi);
-            rs = dadd(rs, piece_term(pe - cc + 1, __ldg(row + min(max(cc, clo), chi)),
-                                     __ldg(row + min(max(pe, clo), chi))));
+          const int v = first_blk ? (int)cbq[bqo + (k & (kBlk - 1))] : (int)(cpm[k] & 0xffffu);
+          const int base = at_a ? va : max(first_blk ? va : cbase, v);
+          const int cc = base + fnext;
+          double rs;
+          if (df == 1) {  // one context: 1 * (t + t) / 2.0 == t (uniform branch)
+            const int ci = min(max(cc, clo), chi) - clo;
+            if (kTopSmem)
+              rs = live >= live_top ? s_top[ci] : __ldg(rows_full + ((live - 1) * ncm + ci));
+            else
+              rs = __ldg(rows_full + ((live - 1) * ncm + ci));  // the last row is the clamped one
+          } else if (cc >= tail_from) {
+            rs = dmul((double)df, s_tail[live - 1]);
+          } else {  // tpot_context_run_sum (planner.cpp:61-84), piece by piece
+            const double* rp = rows_full + (live - 1) * ncm;
+            const int c1 = base + f - 1;
+            int x = cc;
+            int pe = piece_end(s_pex, x, c1, clo1, chi);
+            rs = dmul(dmul((double)(pe - x + 1),
+                           dadd(__ldg(rp + min(max(x, clo), chi) - clo), __ldg(rp + min(max(pe, clo), chi) - clo))),
+                      0.5);
+            for (x = pe + 1; x <= c1; x = pe + 1) {
+              pe = piece_end(s_pex, x, c1, clo1, chi);
+              rs = dadd(rs, dmul(dmul((double)(pe - x + 1),
+                                      dadd(__ldg(rp + min(max(x, clo), chi) - clo),
+                                           __ldg(rp + min(max(pe, clo), chi) - clo))),
+                                 0.5));
+            }
           }
+          total = dadd(total, rs);
         }
-        total = dadd(total, rs);
+        complete();
+        fnext = f;
       }
-      complete(k);
-      fnext = f;
-    }
-    // Phase 2 (fnext >= tail_from, uniform): every run is one clamped piece.
-    for (; k >= 0; --k) {
-      const int2 sk = sk_n;
-      if (k > 0) sk_n = __ldg(&V.seg[k - 1]);
-      const int f = sk.x & 0xffff;
-      if (!done && k < kb)
-        total = dadd(total, dmul((double)(f - fnext), s_tail[min(sk.y - a, live_top) - 1]));
-      complete(k);
-      fnext = f;
+      // Phase 2 (fnext >= tail_from, uniform): every run is one clamped piece.
+      for (; k >= klo; --k) {
+        const int2 sk = cs[k];
+        const int f = sk.x & 0xffff;
+        if (!done && k < kb)
+          total = dadd(total, dmul((double)(f - fnext), s_tail[min(sk.y - a, live_top) - 1]));
+        complete();
+        fnext = f;
+      }
+      if (ch == 0) break;
+      cp_async_wait_all();
+      __syncthreads();  // chunk ch - 1 is visible; every warp is done with chunk ch
+      --ch;
+      if (ch > 0) stage(ch - 1, (ch - 1) & 1);
     }
   }
 }
@@ -1443,7 +1594,7 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
   FastProf fp;
   if (int st = fast_prof_make(ctx, prof, cr.G, &fp)) return st;
   const int C = cr.n_max - cr.n_min + 1;
-  uint2* gtab = arena_alloc<uint2>(ctx, (size_t)S * cr.T);
+  uint4* gtab = arena_alloc<uint4>(ctx, (size_t)S * cr.T);
   double* gfirst = arena_alloc<double>(ctx, (size_t)S * cr.T);
   if (!gtab || !gfirst) return fail(RS_E_NOMEM, "arena exhausted (group table)");
   {
@@ -1454,13 +1605,13 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
   }
   const int cand_units = (C + kLsThreads - 1) / kLsThreads;
   LsArgs A{ss, fp, cr, S, cand_units, gt, gtab, gfirst};
-  const int smem = (int)(sizeof(double) * fp.live_top + sizeof(uint16_t) * (ncm + 1));
-  void (*kern)(LsArgs) = ctas_per_sm >= kLsDenseCtas ? lockstep_eval_kernel<kLsDenseCtas>
-                                                     : lockstep_eval_kernel<1>;
+  const int units = S * A.cand_units;
+  const int top_in = ls2_top_in_smem(ncm, fp.live_top);
+  const int smem = ls2_layout((int)ncm, fp.live_top, top_in != 0).bytes;
+  void (*kern)(LsArgs) = top_in ? lockstep2_kernel<4, true> : lockstep2_kernel<4, false>;
   RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 1;
   RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLsThreads, smem));
-  const int units = S * A.cand_units;
   const int per = ctas_per_sm > 0 ? std::min(ctas_per_sm, std::max(1, per_sm)) : std::max(1, per_sm);
   const int grid = std::max(1, std::min(units, per * ctx->num_sms));
   RS_LAUNCH(ctx, "group_eval", kern, grid, kLsThreads, smem, A);
@@ -1483,22 +1634,17 @@ bool lockstep_ok(const DevProfile& prof, int G) {
 
 int lockstep_slots(rs_ctx* ctx, const DevProfile& prof, int G) {
   const int64_t ncm = prof.c_hi - prof.c_lo + 1;
-  const int64_t live_top = std::max<int64_t>(1, (prof.b_hi + G - 1) / G);
-  const int smem = (int)(sizeof(double) * live_top + sizeof(uint16_t) * (ncm + 1));
-  auto occupancy = [&](void (*k)(LsArgs)) {
-    int per_sm = 1;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kLsThreads, smem) != cudaSuccess) {
-      cudaGetLastError();
-      return 1;
-    }
-    return std::max(1, per_sm);
-  };
-  const int free_ctas = occupancy(lockstep_eval_kernel<1>);
-  // five deep only on top of a full four (the dense build is slower per round)
-  if (free_ctas == kLsDenseCtas - 1 && occupancy(lockstep_eval_kernel<kLsDenseCtas>) >= kLsDenseCtas)
-    return kLsDenseCtas * ctx->num_sms;
-  return free_ctas * ctx->num_sms;
+  const int live_top = (int)std::max<int64_t>(1, (prof.b_hi + G - 1) / G);
+  const int top_in = ls2_top_in_smem(ncm, live_top);
+  const int smem = ls2_layout((int)ncm, live_top, top_in != 0).bytes;
+  void (*kern)(LsArgs) = top_in ? lockstep2_kernel<4, true> : lockstep2_kernel<4, false>;
+  int per_sm = 1;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLsThreads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return ctx->num_sms;
+  }
+  return std::max(1, per_sm) * ctx->num_sms;
 }
 
 bool lockstep_fuses_select(CandRange cr) { return cr.n_max - cr.n_min + 1 <= kLsThreads; }
@@ -1557,3 +1703,15 @@ int fast_reduce(rs_ctx* ctx, int S, const FastSS& ss, CandRange cr, double rho, 
 }
 
 }  // namespace rs
+
+#ifdef RS_PROFILE_PHASES
+extern "C" int rs_debug_phases(unsigned long long* out, int n, int reset) {
+  if (n > 32) n = 32;
+  if (cudaMemcpyFromSymbol(out, rs::g_phase, 8 * n) != cudaSuccess) return 3;
+  if (reset) {
+    unsigned long long z[32] = {};
+    cudaMemcpyToSymbol(rs::g_phase, z, sizeof z);
+  }
+  return 0;
+}
+#endif
