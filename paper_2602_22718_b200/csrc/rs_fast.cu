@@ -151,10 +151,13 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
     double p;
     int32_t pl;
     if (kGen) {
-      fast_gen<true>(gs, t_nz, t_lnz, seed, i, &p, &pl);
       if (keep) {
+        fast_gen<true>(gs, t_nz, t_lnz, seed, i, &p, &pl);
         pred[i] = p;
         plen[i] = pl;
+      } else {  // the histogram needs only the finish tick (plen is in range by spec)
+        p = fast_gen_pred<true>(gs, t_lnz, seed, i);
+        pl = 0;
       }
     } else {
       p = pred[i];

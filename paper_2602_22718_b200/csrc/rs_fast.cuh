@@ -64,21 +64,28 @@ __device__ __forceinline__ double fast_qinterp(const double* t, uint64_t u) {
   return dadd(a, dmul(dsub(b, a), f));
 }
 
+// The predicted length of scenario item i (its second draw).
+template <bool kShared = false>
+__device__ __forceinline__ double fast_gen_pred(const GenSpec& g, const double* lnz, uint64_t seed,
+                                                int i) {
+  uint64_t u2 = draw_at(seed, 2 * (uint64_t)i + 2);
+  double pr = dmul(g.pred_scale, fast_qinterp<kShared>(lnz, u2));
+  pr = pr < g.pred_min ? g.pred_min : pr;
+  pr = pr > g.pred_max ? g.pred_max : pr;
+  return pr;
+}
+
 // Scenario item i of one Monte-Carlo scenario (oracle:
 // orc_generate_scenarios): two splitmix64 draws -> quantile interpolation.
 template <bool kShared = false>
 __device__ __forceinline__ void fast_gen(const GenSpec& g, const double* nz, const double* lnz,
                                          uint64_t seed, int i, double* pred, int32_t* plen) {
   uint64_t u1 = draw_at(seed, 2 * (uint64_t)i + 1);
-  uint64_t u2 = draw_at(seed, 2 * (uint64_t)i + 2);
   double z = fast_qinterp<kShared>(nz, u1);
   double pl = round(dadd(g.plen_mean, dmul(g.plen_sigma, z)));
   pl = pl < (double)g.plen_min ? (double)g.plen_min : pl;
   pl = pl > (double)g.plen_max ? (double)g.plen_max : pl;
-  double pr = dmul(g.pred_scale, fast_qinterp<kShared>(lnz, u2));
-  pr = pr < g.pred_min ? g.pred_min : pr;
-  pr = pr > g.pred_max ? g.pred_max : pr;
-  *pred = pr;
+  *pred = fast_gen_pred<kShared>(g, lnz, seed, i);
   *plen = (int32_t)pl;
 }
 

@@ -212,3 +212,35 @@ def c2_trace_text(n_prompts=65536, shared=2048, unique=512, vocab=32000, seed=1)
         cols[:, :, 5 - k] = ord("0") + (t // 10 ** k) % 10
     body[:, -1] = ord("\n")
     return np.concatenate([head, body.reshape(-1), tail]), tok, off
+
+
+def c2_tokens_multi(n_prompts=65536, n_sys=8, shared=2048, unique=512, vocab=32000, seed=1):
+    """The C2 variant of SURVEY.md §8d with n_sys distinct system prompts
+    (prompt i carries system prompt i mod n_sys), so the prefix tree branches
+    at the root as well as after the system prompts."""
+    n = n_sys * shared + n_prompts * unique
+    k = np.arange(1, n + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed) + k * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    draws = (z % np.uint64(vocab)).astype(np.int32)
+    sys_prompts = draws[:n_sys * shared].reshape(n_sys, shared)
+    uniq = draws[n_sys * shared:].reshape(n_prompts, unique)
+    tok = np.empty((n_prompts, shared + unique), np.int32)
+    tok[:, :shared] = sys_prompts[np.arange(n_prompts) % n_sys]
+    tok[:, shared:] = uniq
+    off = np.arange(n_prompts + 1, dtype=np.int64) * (shared + unique)
+    return tok.reshape(-1), off
+
+
+def long_context_profile():
+    """A 32K-context latency profile (context knots to 32,768): its context
+    memo (> 4,096 entries) exceeds the lockstep evaluator's shared-memory
+    row, so every group of the sweep takes the warp-cooperative evaluator
+    reading the tables from global memory."""
+    bk = [1.0, 2.0, 4.0, 8.0, 16.0, 32.0, 64.0, 128.0, 256.0]
+    ck = [128.0, 1024.0, 4096.0, 16384.0, 32768.0]
+    grid = [[0.005 + 1e-5 * b + 2e-7 * c + 1e-10 * b * c for c in ck] for b in bk]
+    return LatencyProfile(bk, ck, grid, 0.0005, 2)
