@@ -60,6 +60,7 @@ SUITES    := acceptance_main test_dedup test_planner test_profile test_training
 .PHONY: shim
 shim: $(foreach t,$(SUITES),$(SHIM_OUT)/$(t)_b200 $(SHIM_OUT)/$(t)_ref) \
       $(SHIM_OUT)/test_placement_b200 $(SHIM_OUT)/c5_bench_b200 $(SHIM_OUT)/c5_bench_ref \
+      $(SHIM_OUT)/c5_bench_train $(SHIM_OUT)/test_training_train \
       $(SHIM_OUT)/c3_bench_b200 $(SHIM_OUT)/c3_bench_ref
 
 # C3 driver (shim/tools/c3_bench.cpp): scale() at 64K x G=8, N in [1, 512]
@@ -71,14 +72,36 @@ $(SHIM_OUT)/c3_bench_ref: $(PKG)/shim/tools/c3_bench.cpp ref
 	@mkdir -p $(SHIM_OUT)
 	$(CXXREF) $< -o $@ oracle/_ref/librollsim_ref.a -lpthread
 
-# C5 driver (shim/tools/c5_bench.cpp), linked against the drop-in and the reference
+# C5 driver (shim/tools/c5_bench.cpp): the reference's run_training linked three ways
 $(SHIM_OUT)/c5_bench_b200: $(PKG)/shim/tools/c5_bench.cpp $(SHIM_OUT)/librollsim_b200.a $(LIB)
-	$(CXXREF) -DRS_B200 -I$(PKG)/shim $< -o $@ $(SHIM_OUT)/librollsim_b200.a -L$(PKG) -lrs_b200 \
+	$(CXXREF) $< -o $@ $(SHIM_OUT)/librollsim_b200.a -L$(PKG) -lrs_b200 \
 	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -lpthread
 
 $(SHIM_OUT)/c5_bench_ref: $(PKG)/shim/tools/c5_bench.cpp ref
 	@mkdir -p $(SHIM_OUT)
 	$(CXXREF) $< -o $@ oracle/_ref/librollsim_ref.a -lpthread
+
+# INTEGRATION.md's swap as a maintainer applies it: the committed patch on a
+# build-time copy of the reference's training.cpp (outputs under build/ only)
+$(SHIM_OUT)/training_b200.cpp: $(REF)/src/training.cpp $(PKG)/shim/patches/training_b200.patch
+	@mkdir -p $(SHIM_OUT)
+	patch -s -o $@ $(REF)/src/training.cpp $(PKG)/shim/patches/training_b200.patch
+
+$(SHIM_OUT)/training_b200.o: $(SHIM_OUT)/training_b200.cpp $(PKG)/shim/rollsim_b200.hpp
+	$(CXXREF) -I$(PKG)/shim -c $< -o $@
+
+$(SHIM_OUT)/librollsim_b200_train.a: $(SHIM_OBJS) $(SHIM_OUT)/training_b200.o ref
+	ar rcs $@ $(SHIM_OBJS) $(SHIM_OUT)/training_b200.o \
+	    $(addprefix $(REF_OBJ)/,$(addsuffix .o,$(filter-out training,$(REF_KEEP))))
+
+$(SHIM_OUT)/c5_bench_train: $(PKG)/shim/tools/c5_bench.cpp $(SHIM_OUT)/librollsim_b200_train.a $(LIB)
+	$(CXXREF) $< -o $@ $(SHIM_OUT)/librollsim_b200_train.a -L$(PKG) -lrs_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -lpthread
+
+# the reference's own training suite against the patched training.cpp
+$(SHIM_OUT)/test_training_train: $(REF)/tests/test_training.cpp $(SHIM_OUT)/librollsim_b200_train.a $(LIB)
+	$(CXXREF) -I$(PKG)/shim/doctest $< -o $@ $(SHIM_OUT)/librollsim_b200_train.a \
+	    -L$(PKG) -lrs_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -lpthread
 
 # drop-in extension suite (rollsim_b200.hpp) against the stock penalty path
 $(SHIM_OUT)/test_placement_b200: $(PKG)/shim/tests/test_placement_b200.cpp $(SHIM_OUT)/librollsim_b200.a $(LIB)

@@ -38,8 +38,8 @@ EVAL_BYTES = 65536 * 12 + 16  # P*(8 B pred + 4 B plen) + 16 B
 
 
 def _profile_traffic(key):
-    """ncu DRAM read + write per launch of a kernel (profiles/traffic.json), or None."""
-    tf = REPO / "profiles" / "traffic.json"
+    """ncu DRAM read + write per launch of a kernel (profiles/kernel_counters.json), or None."""
+    tf = REPO / "profiles" / "kernel_counters.json"
     if not tf.exists():
         return None
     return json.loads(tf.read_text()).get(key)
@@ -462,6 +462,14 @@ def run_ours(args, world, rank, local):
         "parity_sampled": {"scenarios": n_chk, "ok": ok, "of": args.scenarios,
                            "fields": "t_total, cost, idle_slot_ticks, n_star bitwise vs oracle/rs_oracle.c"},
     }
+    if world > 1 and not args.no_c5:
+        its, err = bench_c5_replicas(world, rank, local)
+        v = torch.tensor([its, 1.0 if err is None else 0.0], dtype=torch.float64, device=dev)
+        dist.all_reduce(v[:1])
+        dist.all_reduce(v[1:], op=dist.ReduceOp.MIN)
+        result["c5_replicas"] = {"metric": "C5 iterations/sec, one independent replica per GPU",
+                                 "value": float(v[0].item()), "unit": "iterations/s",
+                                 "replicas": world, "steps_each": 200, "all_ok": bool(v[1].item())}
     if comm is not None:
         result["n_star_aggregate"] = pick.value
         result["collective"] = "one NCCL all-reduce of 3 x C doubles inside librs_b200 (rs_sweep_sharded)"
@@ -625,37 +633,61 @@ def bench_trace(args, ctx, torch, dev):
     return out
 
 
-def bench_c5(steps=20):
-    """C5: the reference's run_training(rlhfless) on
-    default_topology(128, 8, 4), 512 prompts x G=8, through the C++ drop-in
-    (build/shim/c5_bench_b200) and the unmodified reference
-    (build/shim/c5_bench_ref), iterations/s on this host; plus scale() with
-    plan_rlhfless's placement penalty at that size, stock vs the device
-    penalty (rollsim::b200::scale_placed)."""
-    out = {}
-    for arm in ("b200", "ref"):
-        exe = REPO / "build" / "shim" / f"c5_bench_{arm}"
-        if not exe.exists():
-            return {"unavailable": "build/shim not built (make shim)"}
-        p = subprocess.run([str(exe), str(steps)], capture_output=True, text=True, timeout=900)
-        if p.returncode != 0:
-            return {"unavailable": f"c5_bench_{arm} exit {p.returncode}"}
-        out[arm] = json.loads(p.stdout.strip().splitlines()[-1])
-    b, r = out["b200"], out["ref"]
+def c5_run(arm, steps, seed=11, checkpoint=None, device=None, timeout=1800, run=None):
+    exe = REPO / "build" / "shim" / f"c5_bench_{arm}"
+    if not exe.exists():
+        return None, "build/shim not built (make shim)"
+    env = dict(os.environ)
+    if device is not None:
+        env["RS_DEVICE"] = str(device)
+    cmd = [str(exe), str(steps), "512", str(seed), str(checkpoint or steps), str(run or steps)]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env)
+    if p.returncode != 0:
+        return None, f"c5_bench_{arm} exit {p.returncode}: {p.stderr[-300:]}"
+    return json.loads(p.stdout.strip().splitlines()[-1]), None
+
+
+def bench_c5(steps=1000, compare=50):
+    """C5 (BASELINE config 5): the reference's own
+    run_training(rlhfless) on default_topology(128, 8, 4) — 1,024 simulated
+    GPUs, 512 prompts x G=8 — for the configured 1,000 iterations, linked
+    against the drop-in with training.cpp patched as INTEGRATION.md describes
+    (c5_bench_train). The unmodified reference (c5_bench_ref) and the drop-in
+    under the stock training.cpp (c5_bench_b200) run the first `compare`
+    iterations of the same trace; all three must agree bit for bit there
+    (digest over those iterations)."""
+    train, err = c5_run("train", steps, checkpoint=compare)
+    if err:
+        return {"unavailable": err}
+    ref, err = c5_run("ref", steps, run=compare)  # the same 1,000-step trace, first iterations
+    if err:
+        return {"unavailable": err}
+    b200, err = c5_run("b200", steps, run=compare)
+    if err:
+        return {"unavailable": err}
+    same = train["digest_checkpoint"] == ref["digest"] == b200["digest"]
     return {"metric": "C5 iterations/sec (run_training, simulated 1,024-GPU cluster)",
-            "value": b["iterations_per_s"], "unit": "iterations/s", "steps": steps,
-            "reference": r["iterations_per_s"], "plan_ms_per_step": b["plan_ms_per_step"],
-            "reference_plan_ms_per_step": r["plan_ms_per_step"],
-            "identical_to_reference": b["digest"] == r["digest"],
-            "with_device_planning": {  # plan_rlhfless's scale+penalty and snapshot swapped (INTEGRATION.md)
-                "value": b["swapped"]["iterations_per_s"],
-                "plan_ms_per_step": b["swapped"]["plan_ms_per_step"],
-                "identical_to_reference": b["swapped"]["digest"] == r["digest"]},
-            "scale_with_placement_penalty_ms": {
-                "reference": r["scale_with_penalty_ms"]["stock"],
-                "dropin_callback": b["scale_with_penalty_ms"]["stock"],
-                "device": b["scale_with_penalty_ms"]["device"]},
-            "config": b["config"]}
+            "value": train["iterations_per_s"], "unit": "iterations/s", "steps": steps,
+            "plan_ms_per_step": train["plan_ms_per_step"],
+            "path": "reference run_training, training.cpp + shim/patches/training_b200.patch, "
+                    "drop-in planner on the GPU",
+            "identical_to_reference_first_steps": {"steps": compare, "ok": same},
+            "reference": {"value": ref["iterations_per_s"], "steps": compare,
+                          "plan_ms_per_step": ref["plan_ms_per_step"]},
+            "dropin_stock_training": {"value": b200["iterations_per_s"], "steps": compare,
+                                      "plan_ms_per_step": b200["plan_ms_per_step"]},
+            "cpu_baseline": {"value": ref["iterations_per_s"], "unit": "iterations/s", "cores": 1,
+                             "kind": "reference", "sample": f"first {compare} iterations"},
+            "config": train["config"]}
+
+
+def bench_c5_replicas(world, rank, local, steps=200):
+    """C5 at N GPUs (replicas only — the loop is sequential
+    through predictor state, training.cpp:303-317): every rank runs one
+    independent replica (seed 11 + rank) on its own GPU; the aggregate is the
+    sum of the replicas' iterations/s."""
+    r, err = c5_run("train", steps, seed=11 + rank, device=local)
+    return (r["iterations_per_s"] if r else 0.0), err
 
 
 def bench_dedup(args, ctx, torch, dev, stream):
