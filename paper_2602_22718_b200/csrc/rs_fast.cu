@@ -1339,7 +1339,8 @@ fast_finish_kernel(FastSS ss, CandRange cr, const double* gt_all, const uint4* g
 }
 
 // --------------------------------------------------- lockstep evaluator v2 --
-// Same walk, same FP64 operation order as lockstep_eval_kernel; the per-step
+// The walk described above (lanes = candidates, segments k = D-1 .. 0, one
+// run per step, FP64 sums in the reference order); the per-step
 // path is rebuilt around shared memory so a step costs a few dozen
 // instructions instead of ~100:
 //  - the scenario's segment entries, in-block maxima and in-block all-pairs

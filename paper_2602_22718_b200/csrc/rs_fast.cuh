@@ -38,7 +38,6 @@ __host__ __device__ constexpr int blk_pair(int i, int j) { return i * (2 * kBlk 
 constexpr int kMaxSeg = kFastFmax; // D <= Fmax
 constexpr int kTopCap = 4096;      // smem tpot row entries
 constexpr int kCoopN = 4;         // N < kCoopN: warp-cooperative groups
-constexpr int kLsDenseCtas = 5;   // CTAs per SM of the register-capped lockstep build
 constexpr int kStBlocks = kMaxSeg / kBlk;  // 1024
 constexpr int kStLevels = 11;              // floor(log2(1024)) + 1
 constexpr int kStStride = kStBlocks * kStLevels;

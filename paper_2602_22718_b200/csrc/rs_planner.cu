@@ -712,15 +712,15 @@ static bool fast_spec_ok(const rs_scenario_spec* sp) {
          sp->plen_min >= 0 && sp->plen_max <= kFastPlenMax;
 }
 
-// Relative round time of the lockstep evaluator at c resident CTAs per SM,
-// measured on B200 with the C4 workload (one round of c x 148 scenarios):
-// 3.05 / 3.19 / 3.44 / 3.82 ms for c = 1..4 (a lone CTA is latency-bound,
-// four share the issue slots) and 5.25 ms for c = 5, the register-capped
-// build (kLsDenseCtas): less throughput per scenario than four deep, but two
-// rounds instead of three for e.g. a rank's 1,250 scenarios at 8 GPUs.
+// Relative round time of the lockstep evaluator (lockstep2_kernel) at c
+// resident CTAs per SM, measured on B200 with the C4 workload (one round of
+// c x 148 scenarios, tools/round_costs.py): 2.05 / 2.19 / 2.43 / 2.80 ms for
+// c = 1..4 (a lone CTA's walk is latency-bound, four share the issue
+// slots). E.g. a rank's 1,250 scenarios at 8 GPUs run as three rounds of 444
+// (three deep) rather than 592 + 592 + a lone 66.
 static double lockstep_round_cost(int c) {
-  static const double rel[6] = {0.0, 1.00, 1.05, 1.13, 1.25, 1.72};
-  return c <= 5 ? rel[c] : rel[5] * c / 5.0;
+  static const double rel[5] = {0.0, 1.00, 1.07, 1.19, 1.37};
+  return c <= 4 ? rel[c] : rel[4] * c / 4.0;
 }
 
 // Modelled time of one lockstep batch of U scenarios and the CTAs per SM
