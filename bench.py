@@ -487,12 +487,14 @@ def run_ours(args, world, rank, local):
             result["c5"] = bench_c5()
         if world == 1 and not args.no_trace:
             result["trace"] = bench_trace(args, ctx, torch, dev)
-        print(json.dumps(result), flush=True)
     if comm is not None:
         comm.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    if rank == 0:  # last, after every communicator log line
+        sys.stderr.flush()
+        print(json.dumps(result), flush=True)
 
 
 def bench_arrays(args, ctx, torch, dev, ps):
@@ -814,9 +816,9 @@ def main(argv=None):
         env = dict(os.environ)
         sys.exit(subprocess.call(relaunch_cmd(raw, args.gpus, free_port()), env=env))
     world, rank, local = init_dist()
-    if world > 1:  # NCCL's communicator log (ranks, NVLS / NVLink paths) on stderr
+    if world > 1:  # NCCL's communicator log (ranks, NVLS / NVLink paths)
         os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
