@@ -49,7 +49,9 @@ clean:
 REF       ?= /root/reference/proj
 NLOHMANN  ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty
 SHIM_OUT  := build/shim
-REF_OBJ   := oracle/_ref/obj
+# the reference's non-hot-path units, compiled for the drop-in under build/shim
+# (apart from the oracle build in oracle/_ref), with the reference's flags
+REF_OBJ   := $(SHIM_OUT)/ref
 REF_KEEP  := workload predictor profile placement simulator training report cli
 SHIM_SRCS := $(wildcard $(PKG)/shim/*.cpp)
 SHIM_OBJS := $(patsubst $(PKG)/shim/%.cpp,$(SHIM_OUT)/%.o,$(SHIM_SRCS))
@@ -90,7 +92,8 @@ $(SHIM_OUT)/training_b200.cpp: $(REF)/src/training.cpp $(PKG)/shim/patches/train
 $(SHIM_OUT)/training_b200.o: $(SHIM_OUT)/training_b200.cpp $(PKG)/shim/rollsim_b200.hpp
 	$(CXXREF) -I$(PKG)/shim -c $< -o $@
 
-$(SHIM_OUT)/librollsim_b200_train.a: $(SHIM_OBJS) $(SHIM_OUT)/training_b200.o ref
+$(SHIM_OUT)/librollsim_b200_train.a: $(SHIM_OBJS) $(SHIM_OUT)/training_b200.o \
+    $(addprefix $(REF_OBJ)/,$(addsuffix .o,$(filter-out training,$(REF_KEEP))))
 	ar rcs $@ $(SHIM_OBJS) $(SHIM_OUT)/training_b200.o \
 	    $(addprefix $(REF_OBJ)/,$(addsuffix .o,$(filter-out training,$(REF_KEEP))))
 
@@ -108,11 +111,15 @@ $(SHIM_OUT)/test_placement_b200: $(PKG)/shim/tests/test_placement_b200.cpp $(SHI
 	$(CXXREF) -I$(PKG)/shim -I$(PKG)/shim/doctest $< -o $@ $(SHIM_OUT)/librollsim_b200.a \
 	    -L$(PKG) -lrs_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -lpthread
 
+$(REF_OBJ)/%.o: $(REF)/src/%.cpp
+	@mkdir -p $(REF_OBJ)
+	$(CXXREF) -c $< -o $@
+
 $(SHIM_OUT)/%.o: $(PKG)/shim/%.cpp $(PKG)/shim/rs_shim.hpp $(PKG)/shim/rollsim_b200.hpp include/rs.h
 	@mkdir -p $(SHIM_OUT)
 	$(CXXREF) -c $< -o $@
 
-$(SHIM_OUT)/librollsim_b200.a: $(SHIM_OBJS) ref
+$(SHIM_OUT)/librollsim_b200.a: $(SHIM_OBJS) $(addprefix $(REF_OBJ)/,$(addsuffix .o,$(REF_KEEP)))
 	ar rcs $@ $(SHIM_OBJS) $(addprefix $(REF_OBJ)/,$(addsuffix .o,$(REF_KEEP)))
 
 $(SHIM_OUT)/%_b200: $(REF)/tests/%.cpp $(SHIM_OUT)/librollsim_b200.a $(LIB)
