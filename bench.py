@@ -770,6 +770,14 @@ def bench_dedup(args, ctx, torch, dev, stream):
     return out
 
 
+def nccl_log_on(env):
+    """NCCL's INIT log (rank count, transports) at INFO, even where the image
+    presets a quieter NCCL_DEBUG (VERSION / WARN)."""
+    if env.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+        env["NCCL_DEBUG"] = "INFO"
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+
+
 def relaunch_cmd(argv, n, port):
     """The torchrun command that runs this bench on n ranks (one per GPU)."""
     return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
@@ -814,11 +822,11 @@ def main(argv=None):
         # `bench.py --gpus N` directly); NCCL's communicator log stays on so
         # the rank count is visible in stderr
         env = dict(os.environ)
+        nccl_log_on(env)
         sys.exit(subprocess.call(relaunch_cmd(raw, args.gpus, free_port()), env=env))
     world, rank, local = init_dist()
     if world > 1:  # NCCL's communicator log (ranks, NVLS / NVLink paths)
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        nccl_log_on(os.environ)
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
