@@ -1395,6 +1395,26 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
                "l"(src) : "memory");
 }
+// Shared-memory loads at explicit 32-bit shared addresses (the walk keeps
+// running addresses in registers instead of re-deriving generic pointers).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ int2 lds_s32x2(uint32_t a) {
+  int2 v;
+  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ int lds_u16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+  return (int)v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -1475,9 +1495,10 @@ __global__ void __launch_bounds__(kLsThreads, kMinB) lockstep2_kernel(LsArgs A) 
     double* gtp = A.gt + gbase;
     const uint4* gtabp = A.gtab + gbase;
     const double* gfp = A.gfirst + gbase;
-    int g = N - 1, a = 0, ka = 0, kb = 0, va = 0, jl = 0, smb = 0, cjr = -1, cbase = 0, bqo = 0;
+    // group state; a finished lane parks on ka = -2, kb = -1 (k >= 0 never
+    // matches either), so the walk needs no separate "done" test
+    int g = N - 1, a = 0, ka = -2, kb = -1, va = 0, jl = 0, smb = 0, cjr = -1, cbase = 0, bqo = 0;
     double total = 0.0;
-    bool done = !on;
     uint4 nxt = make_uint4(0u, 0u, 0u, 0u);
     double nfirst = 0.0;
     auto enter = [&](uint4 e, double first) {  // start group g (entry decoded by group_table)
@@ -1496,33 +1517,37 @@ __global__ void __launch_bounds__(kLsThreads, kMinB) lockstep2_kernel(LsArgs A) 
       }
     };
     if (on) enter(__ldg(gtabp), __ldg(gfp));
+    auto complete = [&](int k) {  // groups completing at segment k
+      while (k == ka) {
+        *gtp = total;
+        if (g == 0) {
+          ka = -2;
+          kb = -1;
+        } else {
+          --g;
+          --gtp;
+          --gtabp;
+          --gfp;
+          enter(nxt, nfirst);
+        }
+      }
+    };
+    const uint32_t u_top = kTopSmem ? smem_addr(s_top) : 0u;
+    const uint32_t u_tail = smem_addr(s_tail) - 8u;  // u_tail + 8 * live = &s_tail[live - 1]
     int fnext = 0;  // finish tick of segment k + 1 (uniform)
     while (k >= 0) {
       const int klo = ch * kChunk;
       const int b = ch & 1;
-      const int2* cs = s_seg + b * kChunk - klo;
-      const uint32_t* cpm = s_pm + b * kChunk - klo;
-      const uint16_t* cbq = s_bq + b * kChunkBq;
-      auto complete = [&]() {  // groups completing at segment k
-        while (!done && k == ka) {
-          *gtp = total;
-          if (g == 0) {
-            done = true;
-          } else {
-            --g;
-            --gtp;
-            --gtabp;
-            --gfp;
-            enter(nxt, nfirst);
-          }
-        }
-      };
+      // running shared addresses of segment k's entry and in-block maxima
+      uint32_t sa = smem_addr(s_seg + b * kChunk) + 8u * (uint32_t)(k - klo);
+      uint32_t pa = smem_addr(s_pm + b * kChunk) + 4u * (uint32_t)(k - klo);
+      const uint32_t u_bq = smem_addr(s_bq + b * kChunkBq);
       // Phase 1 (fnext < tail_from): runs may start inside the context memo.
-      for (; k >= klo && fnext < tail_from; --k) {
-        const int2 sk = cs[k];
+      for (; k >= klo && fnext < tail_from; --k, sa -= 8u, pa -= 4u) {
+        const int2 sk = lds_s32x2(sa);
         const int f = sk.x & 0xffff;
         const int df = f - fnext;  // uniform: ticks of run k
-        if (!done && k < kb) {
+        if (k < kb) {
           const int live = min(sk.y - a, live_top);
           // base = max(va, MX over (ka, k]): the group's first block from its
           // all-pairs row, a later block from cbase and the in-block prefix
@@ -1539,18 +1564,19 @@ __global__ void __launch_bounds__(kLsThreads, kMinB) lockstep2_kernel(LsArgs A) 
                                           __ldg(g_st + lev * kStBlocks + jr - (1 << lev))));
             }
           }
-          const int v = first_blk ? (int)cbq[bqo + (k & (kBlk - 1))] : (int)(cpm[k] & 0xffffu);
+          const int v = lds_u16(first_blk ? u_bq + 2u * (uint32_t)(bqo + (k & (kBlk - 1))) : pa);
           const int base = at_a ? va : max(first_blk ? va : cbase, v);
           const int cc = base + fnext;
           double rs;
           if (df == 1) {  // one context: 1 * (t + t) / 2.0 == t (uniform branch)
             const int ci = min(max(cc, clo), chi) - clo;
             if (kTopSmem)
-              rs = live >= live_top ? s_top[ci] : __ldg(rows_full + ((live - 1) * ncm + ci));
+              rs = live >= live_top ? lds_f64(u_top + 8u * (uint32_t)ci)
+                                    : __ldg(rows_full + ((live - 1) * ncm + ci));
             else
               rs = __ldg(rows_full + ((live - 1) * ncm + ci));  // the last row is the clamped one
           } else if (cc >= tail_from) {
-            rs = dmul((double)df, s_tail[live - 1]);
+            rs = dmul((double)df, lds_f64(u_tail + 8u * (uint32_t)live));
           } else {  // tpot_context_run_sum (planner.cpp:61-84), piece by piece
             const double* rp = rows_full + (live - 1) * ncm;
             const int c1 = base + f - 1;
@@ -1569,16 +1595,17 @@ __global__ void __launch_bounds__(kLsThreads, kMinB) lockstep2_kernel(LsArgs A) 
           }
           total = dadd(total, rs);
         }
-        complete();
+        complete(k);
         fnext = f;
       }
       // Phase 2 (fnext >= tail_from, uniform): every run is one clamped piece.
-      for (; k >= klo; --k) {
-        const int2 sk = cs[k];
+      for (; k >= klo; --k, sa -= 8u) {
+        const int2 sk = lds_s32x2(sa);
         const int f = sk.x & 0xffff;
-        if (!done && k < kb)
-          total = dadd(total, dmul((double)(f - fnext), s_tail[min(sk.y - a, live_top) - 1]));
-        complete();
+        if (k < kb)
+          total = dadd(total, dmul((double)(f - fnext),
+                                   lds_f64(u_tail + 8u * (uint32_t)min(sk.y - a, live_top))));
+        complete(k);
         fnext = f;
       }
       if (ch == 0) break;
