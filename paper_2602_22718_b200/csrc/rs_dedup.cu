@@ -601,7 +601,9 @@ constexpr int kSoloMembers = 1024;
 // Every round after round 0's compare, in one persistent launch, one grid
 // barrier per round: round_phase closes round r and compares round r + 1,
 // while the table set of round r + 2 is cleared.
-__global__ void __launch_bounds__(256)
+constexpr int kRefineT = 256;
+
+__global__ void __launch_bounds__(kRefineT)
 refine_kernel(DedupState st, int* kc, unsigned long long* bar) {
   unsigned long long target = 0;
   int cur = 0;
@@ -645,116 +647,84 @@ refine_kernel(DedupState st, int* kc, unsigned long long* bar) {
 }
 
 // The five PrefixIndex tables from the difference array and the counts
-// (dedup.cpp:73-98), one CTA. With x_m = x on depths 1..maxd and 0 elsewhere:
+// (dedup.cpp:73-98). With x_m = x on depths 1..maxd and 0 elsewhere:
 //   nodes[d] = incl(node_diff_m)[d] (0 at d = 0 and d = maxd + 1)
 //   scb[d]   = incl(end_count_m)[d] - end_count_m[d]
 //   stb[d]   = incl(end_count_m * i)[d] - end_count_m[d] * d
 //   lcf[d]   = total(len_count_m) - incl(len_count_m)[d]
 //   ltf[d]   = total(len_count_m * i) - incl(len_count_m * i)[d]
-// Each thread scans kTabIPT consecutive depths; the five thread totals go
-// through one CTA scan per chunk of kTabT * kTabIPT depths, and the chunk is
-// staged in shared memory and written out coalesced. Every CTA of the grid
-// runs the (cheap) scan; CTA b writes only depths [b n / G, (b + 1) n / G),
-// so the writes into mapped host memory leave from G SMs at once. maxd < 0: the
-// longest prompt from stats; the tables are written (stride maxd + 2) only
-// if maxd <= cap_md. stats_out (nullable) receives {min, max, total, leaves,
+// kTabSlices CTAs per table (five independent scans): each thread scans
+// kTabIPT consecutive depths, one CTA-wide scan of the thread totals per
+// chunk of kTabT * kTabIPT depths; every CTA of a table runs its (cheap)
+// scan and writes one slice, so writes into mapped host memory leave from
+// 5 x kTabSlices SMs at once. maxd < 0: the longest
+// prompt from stats; the tables are written (stride maxd + 2) only if
+// maxd <= cap_md. stats_out (nullable) receives {min, max, total, leaves,
 // flags}.
-constexpr int kTabT = 512;
+constexpr int kTabT = 1024;
 constexpr int kTabIPT = 4;
-constexpr int kTabQ = 5;
-constexpr int kTabChunk = kTabT * kTabIPT;
-// staged as [q][j][thread], rows padded by 8 so a warp's reads of 32
-// consecutive depths (8 threads x 4 j) spread over all banks
-constexpr int kTabRow = kTabT + 8;
-constexpr int kTabStage = kTabIPT * kTabRow;
-constexpr int kTabSmem = (int)sizeof(int64_t) * kTabQ * kTabStage;
-constexpr int kTabCtas = 16;
+constexpr int kTabSlices = 4;
+constexpr int kTabCtas = 5 * kTabSlices;
+constexpr int kTabSmem = 8 * kTabT * kTabIPT;  // one chunk staged for coalesced writes
 
 __global__ void __launch_bounds__(kTabT)
 tables_kernel(DedupState st, int maxd, int cap_md, int64_t* out, int64_t* stats_out) {
-  __shared__ int64_t ws[kTabQ][32];
-  extern __shared__ int64_t stage[];  // [kTabQ][kTabIPT][kTabRow]
+  __shared__ int64_t ws[32];
+  extern __shared__ int64_t stage[];  // [kTabT * kTabIPT]
   if (maxd < 0) maxd = (int)st.stats[1];
-  if (stats_out && blockIdx.x == 0 && threadIdx.x < 5)
+  const int q = blockIdx.x / kTabSlices, slice = blockIdx.x % kTabSlices;  // table, slice
+  if (stats_out && q == 0 && threadIdx.x < 5)
     stats_out[threadIdx.x] = threadIdx.x == 0 ? INT64_MAX - st.stats[0]
                              : threadIdx.x == 4 ? (int64_t)*st.flags : st.stats[threadIdx.x];
   if (maxd > cap_md) return;
   const int n = maxd + 2;  // depths 0 .. maxd + 1
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int64_t* const tab[kTabQ] = {out, out + n, out + 2 * (int64_t)n, out + 3 * (int64_t)n,
-                               out + 4 * (int64_t)n};
+  int64_t* tab = out + (int64_t)q * n;
+  const int s_lo = (int)((int64_t)slice * n / kTabSlices), s_hi = (int)((int64_t)(slice + 1) * n / kTabSlices);
+  const int64_t* src = q == 0 ? st.node_diff : q <= 2 ? st.end_count : st.len_count;
+  const bool weighted = q == 2 || q == 4;  // x * depth
   // totals of the suffix tables: prompts of length >= 1, and all tokens
-  const int64_t tl = st.P - st.len_count[0], tt = st.stats[2];
-  int64_t carry[kTabQ] = {0, 0, 0, 0, 0};
+  const int64_t total = q == 3 ? st.P - st.len_count[0] : q == 4 ? st.stats[2] : 0;
+  int64_t carry = 0;
   for (int d0 = 0; d0 < n; d0 += kTabT * kTabIPT) {
-    int64_t v[kTabIPT][kTabQ];
-    int64_t run[kTabQ] = {0, 0, 0, 0, 0};
+    int64_t x[kTabIPT];
+    int64_t run = 0;
 #pragma unroll
     for (int j = 0; j < kTabIPT; ++j) {
       const int d = d0 + threadIdx.x * kTabIPT + j;
-      const bool in = d >= 1 && d <= maxd;
-      const int64_t nd = in ? st.node_diff[d] : 0;
-      const int64_t ec = in ? st.end_count[d] : 0;
-      const int64_t lc = in ? st.len_count[d] : 0;
-      const int64_t x[kTabQ] = {nd, ec, ec * d, lc, lc * d};
-#pragma unroll
-      for (int q = 0; q < kTabQ; ++q) {
-        run[q] += x[q];
-        v[j][q] = x[q];
-      }
+      const int64_t c = d >= 1 && d <= maxd ? src[d] : 0;
+      x[j] = weighted ? c * d : c;
+      run += x[j];
     }
-    // CTA exclusive scan of the thread totals, all five at once
-    int64_t incl[kTabQ];
-#pragma unroll
-    for (int q = 0; q < kTabQ; ++q) {
-      incl[q] = warp_incl_sum(run[q]);
-      if (lane == 31) ws[q][wid] = incl[q];
-    }
+    const int64_t incl = warp_incl_sum(run);
+    if (lane == 31) ws[wid] = incl;
     __syncthreads();
-    constexpr int kTabW = kTabT / 32;
     if (wid == 0) {
-#pragma unroll
-      for (int q = 0; q < kTabQ; ++q) {
-        const int64_t x = lane < kTabW ? ws[q][lane] : 0;
-        ws[q][lane] = warp_incl_sum(x) - x;
-      }
+      const int64_t t = ws[lane];
+      ws[lane] = warp_incl_sum(t) - t;
     }
     __syncthreads();
-    int64_t pre[kTabQ];
-#pragma unroll
-    for (int q = 0; q < kTabQ; ++q) pre[q] = carry[q] + ws[q][wid] + incl[q] - run[q];
+    int64_t pre = carry + ws[wid] + incl - run;  // exclusive prefix of this thread
 #pragma unroll
     for (int j = 0; j < kTabIPT; ++j) {
       const int d = d0 + threadIdx.x * kTabIPT + j;
-#pragma unroll
-      for (int q = 0; q < kTabQ; ++q) pre[q] += v[j][q];
-      const bool in = d >= 1 && d <= maxd;
-      int64_t* sj = stage + j * kTabRow + threadIdx.x;
-      sj[0 * kTabStage] = in ? pre[0] : 0;
-      sj[1 * kTabStage] = pre[1] - v[j][1];
-      sj[2 * kTabStage] = pre[2] - v[j][1] * d;
-      sj[3 * kTabStage] = tl - pre[3];
-      sj[4 * kTabStage] = tt - pre[4];
+      pre += x[j];  // inclusive at d
+      int64_t v;
+      if (q == 0) v = d >= 1 && d <= maxd ? pre : 0;
+      else if (q <= 2) v = pre - x[j];
+      else v = total - pre;
+      stage[threadIdx.x * kTabIPT + j] = v;
     }
     __syncthreads();
     {  // this CTA's slice of the chunk, consecutive depths per warp
-      const int lo = max(d0, (int)((int64_t)blockIdx.x * n / gridDim.x));
-      const int hi = min(min(d0 + kTabChunk, n), (int)((int64_t)(blockIdx.x + 1) * n / gridDim.x));
-      for (int d = lo + threadIdx.x; d < hi; d += kTabT) {
-        const int i = d - d0, k = (i % kTabIPT) * kTabRow + i / kTabIPT;
-#pragma unroll
-        for (int q = 0; q < kTabQ; ++q) tab[q][d] = stage[q * kTabStage + k];
-      }
+      const int lo = max(d0, s_lo), hi = min(min(d0 + kTabT * kTabIPT, n), s_hi);
+      for (int d = lo + threadIdx.x; d < hi; d += kTabT) tab[d] = stage[d - d0];
     }
-    // carry = chunk total (the last warp's inclusive totals)
+    // the chunk's total (the last thread's inclusive prefix) carries over
     __syncthreads();
-    if (threadIdx.x == kTabT - 1) {
-#pragma unroll
-      for (int q = 0; q < kTabQ; ++q) ws[q][0] = ws[q][kTabW - 1] + incl[q];
-    }
+    if (threadIdx.x == kTabT - 1) ws[0] = ws[31] + incl;
     __syncthreads();
-#pragma unroll
-    for (int q = 0; q < kTabQ; ++q) carry[q] += ws[q][0];
+    carry += ws[0];
     __syncthreads();
   }
 }
@@ -770,14 +740,14 @@ uint32_t pow2_at_least(int64_t v) {
 static int launch_refine(rs_ctx* ctx, DedupState st, int* kc, unsigned long long* bar) {
   int& per_sm = ctx->dev_cache.refine_per_sm;  // per device: the context's
   if (!per_sm) {
-    RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, 256, 0));
+    RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, kRefineT, 0));
     per_sm = std::max(1, std::min(per_sm, 4));
   }
   const int blocks = per_sm * ctx->num_sms;
   void* args[] = {&st, &kc, &bar};
   cudaEvent_t ev = nullptr;
   timer_begin(ctx, "dedup_refine", &ev);
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)refine_kernel, blocks, 256, args, 0, ctx->stream);
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)refine_kernel, blocks, kRefineT, args, 0, ctx->stream);
   ctx->launches++;
   if (e != cudaSuccess) return fail(RS_E_CUDA, std::string("launch dedup_refine: ") + cudaGetErrorString(e));
   timer_end(ctx, "dedup_refine", ev);
@@ -804,7 +774,6 @@ struct RefineTail {
 static int tables_setup(rs_ctx* ctx) {
   bool& done = ctx->dev_cache.tables_ready;
   if (!done) {
-    RS_CUDA_TRY(cudaFuncSetAttribute(tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTabSmem));
     done = true;
   }
   return RS_OK;
