@@ -238,6 +238,11 @@ typedef struct rs_scale_out {
   /* sum_{N=n_min}^{n_max} N entries: every group time of every candidate,
    * candidate-major (for host TimePenaltyFn callbacks). */
   double* group_times;
+  /* LPT extension, C entries each, nullable: the same
+   * predictions as G responses of ceil(pred) tokens, greedy LPT onto N actors
+   * (as rs_lpt): token makespan and intra-function idle N*makespan - sum. */
+  int64_t* lpt_makespan;
+  int64_t* lpt_idle;
 } rs_scale_out;
 
 /* scale(): t_penalty (nullable, C entries) is added to each candidate's

@@ -28,6 +28,7 @@ class RsScaleOut(C.Structure):
         ("t_norm", P_f64), ("c_norm", P_f64), ("score", P_f64),
         ("idle_slot_ticks", P_i64), ("order", P_i32),
         ("actor_times", P_f64), ("group_times", P_f64),
+        ("lpt_makespan", P_i64), ("lpt_idle", P_i64),
     ]
 
 

@@ -1427,6 +1427,40 @@ int rs_sweep_select(const double* sum_t, const double* sum_c, int64_t n_scenario
   return sweep_select_host(sum_t, sum_c, n_scenarios, C, n_min, lambda, n_star);
 }
 
+// LPT over id-ordered predictions already in HBM (pid): the (len desc, id
+// asc, r asc) order by a stable radix sort, then one warp per candidate.
+static int lpt_core(rs_ctx* ctx, const double* pid, int64_t count, int G, int n_min, int n_max,
+                    uint64_t* keys, uint32_t* vals, int64_t* len_r, char* sscr, int64_t* mk,
+                    int64_t* id) {
+  const int C = n_max - n_min + 1;
+  RS_LAUNCH(ctx, "lpt_keys", lpt_keys_kernel, grid_for(ctx, count, 256), 256, 0, pid,
+            count, keys, vals);
+  uint64_t* ko;
+  uint32_t* vo;
+  RS_TRY(radix_sort_pairs(ctx, keys, vals, count, sscr, &ko, &vo));
+  RS_LAUNCH(ctx, "lpt_gather", lpt_gather_kernel, grid_for(ctx, count, 256), 256, 0, pid, vo,
+            count, len_r);
+  int warps_per_block = 4;
+  int blocks = (C + warps_per_block - 1) / warps_per_block;
+  int R = (n_max + 31) / 32;
+#define RS_LPT(RR)                                                                           \
+  RS_LAUNCH(ctx, "lpt", lpt_kernel<RR>, blocks, 32 * warps_per_block, 0, len_r, count, \
+            G, n_min, n_max, mk, id)
+  if (R <= 1) RS_LPT(1);
+  else if (R <= 2) RS_LPT(2);
+  else if (R <= 4) RS_LPT(4);
+  else if (R <= 8) RS_LPT(8);
+  else if (R <= 16) RS_LPT(16);
+  else RS_LPT(32);
+#undef RS_LPT
+  return RS_OK;
+}
+
+static size_t lpt_bytes(int64_t count, int C) {
+  return abytes(count, 8) * 2 + abytes(count, 4) + radix_sort_scratch_bytes64(count) +
+         abytes(C, 8) * 2;
+}
+
 // scale() with either a caller-provided penalty array (t_penalty) or the
 // device placement penalty (pen), or neither.
 static int scale_impl(rs_ctx* ctx, const double* pred, const int32_t* plen,
@@ -1448,6 +1482,14 @@ static int scale_impl(rs_ctx* ctx, const double* pred, const int32_t* plen,
                       " needs " + std::to_string(gpus) + " GPUs on one node per actor, the cluster hosts " +
                       std::to_string(slots.n_placeable) + " such actors");
   }
+  const bool want_lpt = out->lpt_makespan || out->lpt_idle;
+  if (want_lpt) {  // LPT extension on the same predictions
+    if (n_max > 1024) return fail(RS_E_CONFIG, "lpt: n_max <= 1024 supported");
+    double mx = 0;
+    for (int32_t i = 0; i < count; ++i) mx = pred[i] > mx ? pred[i] : mx;
+    if (std::ceil(mx) * (double)count * G >= 0x1.0p52)
+      return fail(RS_E_CONFIG, "lpt: total response tokens must stay below 2^52");
+  }
   DevProfile dp;
   RS_TRY(get_profile(ctx, profile, &dp));
   const int C = n_max - n_min + 1;
@@ -1455,7 +1497,7 @@ static int scale_impl(rs_ctx* ctx, const double* pred, const int32_t* plen,
   std::vector<int64_t> off = {0, count};
   SetRun run;
   size_t extra = abytes(T, 8) + abytes(C, 8) * 7 + abytes(count, 4) + abytes(C, 8) + 4096 +
-                 (pen ? placement_bytes(count, n_max) : 0);
+                 (pen ? placement_bytes(count, n_max) : 0) + (want_lpt ? lpt_bytes(count, C) : 0);
   RS_TRY(prepare_sets(ctx, pred, plen, id_rank, off, 1, &dp, G, extra, &run));
   double* gt = arena_alloc<double>(ctx, T);
   double* tt = arena_alloc<double>(ctx, C);
@@ -1478,6 +1520,18 @@ static int scale_impl(rs_ctx* ctx, const double* pred, const int32_t* plen,
             with_pen ? tp : (const double*)nullptr, cc, tn, cn, sc, ns);
   RS_LAUNCH(ctx, "map_order", map_order_kernel, grid_for(ctx, count, 256), 256, 0,
             run.built.order_r(), run.orig, (int64_t)count, order);
+  if (want_lpt) {
+    uint64_t* keys = arena_alloc<uint64_t>(ctx, count);
+    uint32_t* vals = arena_alloc<uint32_t>(ctx, count);
+    int64_t* len_r = arena_alloc<int64_t>(ctx, count);
+    char* sscr = arena_alloc<char>(ctx, radix_sort_scratch_bytes64(count));
+    int64_t* mk = arena_alloc<int64_t>(ctx, C);
+    int64_t* li = arena_alloc<int64_t>(ctx, C);
+    if (!li) return fail(RS_E_NOMEM, "arena exhausted (lpt)");
+    RS_TRY(lpt_core(ctx, run.pred, count, G, n_min, n_max, keys, vals, len_r, sscr, mk, li));
+    if (out->lpt_makespan) RS_TRY(d2h(ctx, out->lpt_makespan, mk, 8 * C));
+    if (out->lpt_idle) RS_TRY(d2h(ctx, out->lpt_idle, li, 8 * C));
+  }
   RS_TRY(d2h(ctx, &out->n_star, ns, 4));
   if (out->t_total) RS_TRY(d2h(ctx, out->t_total, tt, 8 * C));
   if (out->cost) RS_TRY(d2h(ctx, out->cost, cc, 8 * C));
@@ -1709,26 +1763,7 @@ int rs_lpt(rs_ctx* ctx, const double* pred, const int32_t* id_rank, int32_t coun
   RS_TRY(read_flags(ctx, &fl));
   if (fl & (kFlagBadPerm)) return fail(RS_E_ARG, "id_rank is not a permutation of [0, count)");
   if (fl) return flags_to_status(fl);
-  RS_LAUNCH(ctx, "lpt_keys", lpt_keys_kernel, grid_for(ctx, count, 256), 256, 0, pid,
-            (int64_t)count, keys, vals);
-  uint64_t* ko;
-  uint32_t* vo;
-  RS_TRY(radix_sort_pairs(ctx, keys, vals, count, sscr, &ko, &vo));
-  RS_LAUNCH(ctx, "lpt_gather", lpt_gather_kernel, grid_for(ctx, count, 256), 256, 0, pid, vo,
-            (int64_t)count, len_r);
-  int warps_per_block = 4;
-  int blocks = (C + warps_per_block - 1) / warps_per_block;
-  int R = (n_max + 31) / 32;
-#define RS_LPT(RR)                                                                           \
-  RS_LAUNCH(ctx, "lpt", lpt_kernel<RR>, blocks, 32 * warps_per_block, 0, len_r, (int64_t)count, \
-            G, n_min, n_max, mk, id)
-  if (R <= 1) RS_LPT(1);
-  else if (R <= 2) RS_LPT(2);
-  else if (R <= 4) RS_LPT(4);
-  else if (R <= 8) RS_LPT(8);
-  else if (R <= 16) RS_LPT(16);
-  else RS_LPT(32);
-#undef RS_LPT
+  RS_TRY(lpt_core(ctx, pid, count, G, n_min, n_max, keys, vals, len_r, sscr, mk, id));
   RS_TRY(d2h(ctx, makespan, mk, 8 * C));
   RS_TRY(d2h(ctx, idle, id, 8 * C));
   return sync_and_check(ctx);

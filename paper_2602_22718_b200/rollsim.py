@@ -602,11 +602,13 @@ class PlacementPenalty:
 
 
 def scale(predicted: Sequence[PredictedPrompt], profile: LatencyProfile, responses_per_prompt,
-          n_min, n_max, lambda_, gpus_per_actor, penalty=None):
+          n_min, n_max, lambda_, gpus_per_actor, penalty=None, with_lpt=False):
     """scale (proj/src/planner.cpp:159-218). A Python `penalty` is called per
     candidate in ascending N with that candidate's groups and times, like
     TimePenaltyFn (planner.hpp:80-82); a `PlacementPenalty` is evaluated on
-    the device instead (rs_scale_placed)."""
+    the device instead (rs_scale_placed). with_lpt: also the LPT extension's
+    token makespan and idle per candidate on the same predictions
+    (res.lpt_makespan, res.lpt_idle)."""
     ctx = context()
     P = len(predicted)
     if P:
@@ -621,10 +623,14 @@ def scale(predicted: Sequence[PredictedPrompt], profile: LatencyProfile, respons
     order = np.zeros(max(P, 1), np.int32)
     gt = np.zeros(T, np.float64)
     at = np.zeros(max(n_max, 1), np.float64)
+    lpt_mk = np.zeros(Cn, np.int64)
+    lpt_idle = np.zeros(Cn, np.int64)
     out = _abi.RsScaleOut(0, *[ptr(arr[k], C.c_double) for k in
                                ("t_total", "t_penalty", "cost", "t_norm", "c_norm", "score")],
                           ptr(idle, C.c_int64), ptr(order, C.c_int32), ptr(at, C.c_double),
-                          ptr(gt, C.c_double) if callable(penalty) else None)
+                          ptr(gt, C.c_double) if callable(penalty) else None,
+                          ptr(lpt_mk, C.c_int64) if with_lpt else None,
+                          ptr(lpt_idle, C.c_int64) if with_lpt else None)
     s, keep = profile.struct()
     if isinstance(penalty, PlacementPenalty):
         pp, keep_p = penalty.struct()
@@ -662,6 +668,8 @@ def scale(predicted: Sequence[PredictedPrompt], profile: LatencyProfile, respons
     res.groups = _groups_from_order(predicted, order[:P], n_star, gpus_per_actor)
     res.actor_times = at[:n_star].tolist()
     res.idle_slot_ticks = idle
+    if with_lpt:
+        res.lpt_makespan, res.lpt_idle = lpt_mk, lpt_idle
     return res
 
 

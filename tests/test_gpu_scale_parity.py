@@ -132,3 +132,19 @@ def test_sweep_long_context_profile(S, P):
     assert np.array_equal(got["n_star"], ns)
     print(f"long-context sweep S={S} P={P}: {got['seconds'] * 1e3:.1f} ms "
           f"({S * 64 / got['seconds']:.0f} evals/s)")
+
+
+def test_scale_with_lpt_outputs():
+    """scale() with the LPT extension's outputs (rs_scale_out.lpt_makespan /
+    lpt_idle): per candidate equal to orc_lpt on the same predictions, and
+    the scale() results themselves unchanged (bitwise vs the port)."""
+    pred, plen = port().generate_scenarios(c4_spec(1, count=4096, first=77))
+    ps = [rs.PredictedPrompt(f"p{i:06d}", int(plen[i]), float(pred[i])) for i in range(len(pred))]
+    got = rs.scale(ps, default_profile(), 8, 1, 64, 0.7, 2, with_lpt=True)
+    wmk, widle = port().lpt(pred, None, 8, 1, 64)
+    assert got.lpt_makespan.tolist() == wmk.tolist()
+    assert got.lpt_idle.tolist() == widle.tolist()
+    exp = port().scale(pred, plen, None, default_profile(), 8, 1, 64, 0.7, 2)
+    assert got.n_star == exp["n_star"]
+    t = np.array([c.t_total for c in got.candidates])
+    assert np.array_equal(bits(t), bits(exp["t_total"]))
