@@ -1175,7 +1175,7 @@ __device__ __forceinline__ int ls_range(const LsView& V, int l, int r) {
 // run spans the longest context range (often several knot pieces), so it is
 // evaluated here in parallel rather than inside the lockstep walk.
 __global__ void group_table_kernel(FastSS ss, FastProf fp, CandRange cr, int S, uint4* gtab,
-                                   double* gfirst) {
+                                   double* gfirst, uint16_t* gka) {
   if (*ss.flags & kFastBad) return;
   const int64_t total = (int64_t)S * cr.T;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
@@ -1210,6 +1210,7 @@ __global__ void group_table_kernel(FastSS ss, FastProf fp, CandRange cr, int S, 
     const uint32_t bqo = (uint32_t)((jl & 15) * kBlkPairs + i * (2 * kBlk + 1 - i) / 2 - i);
     gtab[t] = make_uint4((uint32_t)ka | ((uint32_t)kb << 16), (uint32_t)va | ((uint32_t)smb << 16),
                          bqo | ((uint32_t)jl << 16), (uint32_t)a);
+    gka[t] = (uint16_t)ka;  // compact copy for the idle sum of fast_finish
     // run_sum(G * (b - a), top_m, top_m + f - 1) from the halved tables
     // (piece terms and their order as tpot_context_run_sum; 0.0 + x == x)
     const int clo = fp.c_lo, chi = fp.c_hi, clo1 = fp.c_lo - 1;
@@ -1235,7 +1236,7 @@ __global__ void group_table_kernel(FastSS ss, FastProf fp, CandRange cr, int S, 
 // table; n_star comes from block reductions with the reference's min/max and
 // first-strict-minimum semantics (planner.cpp:196-217).
 __global__ void __launch_bounds__(kLsThreads)
-fast_finish_kernel(FastSS ss, CandRange cr, const double* gt_all, const uint4* gtab_all,
+fast_finish_kernel(FastSS ss, CandRange cr, const double* gt_all, const uint16_t* gka_all,
                    LsEpilogue ep) {
   __shared__ double r_d[4][kLsThreads / 32];
   __shared__ int r_i[kLsThreads / 32];
@@ -1274,12 +1275,12 @@ fast_finish_kernel(FastSS ss, CandRange cr, const double* gt_all, const uint4* g
       const int64_t i0 = ss.item_off[s], so = i0 + s;
       const int P = (int)(ss.item_off[s + 1] - i0);
       const int D = ss.nseg[s];
-      const uint4* gtab = gtab_all + gbase;
+      const uint16_t* gka = gka_all + gbase;
       const int q = P / N, rem = P % N;
       int64_t acc = 0;
       for (int h = 0; h < N; ++h) {
         const int size = q + (h < rem ? 1 : 0);
-        if (size > 0) acc += (int64_t)size * (__ldg(&ss.seg[so + (__ldg(&gtab[h].x) & 0xffffu)].x) & 0xffff);
+        if (size > 0) acc += (int64_t)size * (__ldg(&ss.seg[so + __ldg(gka + h)].x) & 0xffff);
       }
       ep.idle[o] = (acc - ss.segCF[so + D]) * cr.G;
     }
@@ -1626,13 +1627,14 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
   if (int st = fast_prof_make(ctx, prof, cr.G, &fp)) return st;
   const int C = cr.n_max - cr.n_min + 1;
   uint4* gtab = arena_alloc<uint4>(ctx, (size_t)S * cr.T);
+  uint16_t* gka = arena_alloc<uint16_t>(ctx, (size_t)S * cr.T);
   double* gfirst = arena_alloc<double>(ctx, (size_t)S * cr.T);
-  if (!gtab || !gfirst) return fail(RS_E_NOMEM, "arena exhausted (group table)");
+  if (!gtab || !gfirst || !gka) return fail(RS_E_NOMEM, "arena exhausted (group table)");
   {
     const int64_t n = (int64_t)S * cr.T;
     RS_LAUNCH(ctx, "group_table", group_table_kernel,
               (int)std::min<int64_t>((n + 255) / 256, 16 * ctx->num_sms), 256, 0, ss, fp, cr, S,
-              gtab, gfirst);
+              gtab, gfirst, gka);
   }
   const int cand_units = (C + kLsThreads - 1) / kLsThreads;
   LsArgs A{ss, fp, cr, S, cand_units, gt, gtab, gfirst};
@@ -1650,7 +1652,7 @@ int lockstep_eval(rs_ctx* ctx, int S, const FastSS& ss, const DevProfile& prof, 
     if (!lockstep_fuses_select(cr)) return fail(RS_E_ARG, "finish kernel needs <= 256 candidates");
     LsEpilogue ep{fuse->tt, fuse->cc, fuse->idle, fuse->n_star, fuse->rho, fuse->lambda,
                   fuse->gpus, fuse->n_star ? 1 : 0};
-    RS_LAUNCH(ctx, "finish", fast_finish_kernel, S, kLsThreads, 0, ss, cr, gt, gtab, ep);
+    RS_LAUNCH(ctx, "finish", fast_finish_kernel, S, kLsThreads, 0, ss, cr, gt, gka, ep);
   }
   return RS_OK;
 }

@@ -820,7 +820,8 @@ static int sweep_pass(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
   const bool host_in = !generated && !device_ptrs;  // caller arrays in host memory
   const size_t in_bytes = abytes(P, 8) + abytes(P, 4);
   const size_t per_scen = in_bytes * (host_in ? 2 : 1) + built_bytes(P, 1, with_generic) +
-                          abytes(T, 8) * 2 + abytes(T, 16) + abytes(C, 8) * 3 + abytes(1, 4) + 2048;
+                          abytes(T, 8) * 2 + abytes(T, 16) + abytes(T, 2) + abytes(C, 8) * 3 +
+                          abytes(1, 4) + 2048;
   // Batches: what an 8 GiB scratch budget holds (<= 2048 scenarios), planned
   // as whole waves of the lockstep evaluator (S = 10,000 on 148 SMs x 4:
   // batches of 1,184) with the remainder merged into the last batch when it
