@@ -273,20 +273,30 @@ def parity_sample(args, world, rank, S_local, s0, t_total, cost, idle, n_star, n
     chunk = 256
     for c0 in range(0, len(idx), chunk):
         sel = idx[c0:c0 + chunk]
-        preds, plens = [], []
-        for s in sel:  # each sampled scenario generated by the port itself
-            p, l = port().generate_scenarios(c4_spec(1, count=args.prompts, first=s0 + int(s)))
-            preds.append(p)
-            plens.append(l)
-        pred, plen = np.concatenate(preds), np.concatenate(plens)
+        if sel[-1] - sel[0] + 1 == len(sel):  # a contiguous block: one generator call
+            pred, plen = port().generate_scenarios(c4_spec(len(sel), count=args.prompts,
+                                                           first=s0 + int(sel[0])))
+            preds = np.split(pred, len(sel))
+        else:
+            preds, plens = [], []
+            for s in sel:  # each sampled scenario generated by the port itself
+                p, l = port().generate_scenarios(c4_spec(1, count=args.prompts, first=s0 + int(s)))
+                preds.append(p)
+                plens.append(l)
+            pred, plen = np.concatenate(preds), np.concatenate(plens)
         tt, cc, ns = port().sweep_arrays(pred, plen, len(sel), args.prompts, prof, args.G,
                                          args.n_min, args.n_max, args.lam, 2, threads=threads)
         ok &= bool(np.array_equal(tt.view(np.uint64), tt_d[sel].view(np.uint64)))
         ok &= bool(np.array_equal(cc.view(np.uint64), cc_d[sel].view(np.uint64)))
         ok &= bool(np.array_equal(ns, ns_d[sel]))
+        # idle slot-ticks per scenario on the host threads (the port's C call
+        # releases the GIL)
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(threads) as ex:
+            idles = list(ex.map(lambda p: port().scale_idle(p, None, args.G, args.n_min, args.n_max),
+                                preds))
         for j, s in enumerate(sel):
-            ok &= bool(np.array_equal(port().scale_idle(preds[j], None, args.G, args.n_min,
-                                                        args.n_max), id_d[s]))
+            ok &= bool(np.array_equal(idles[j], id_d[s]))
     return len(idx), ok
 
 
