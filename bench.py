@@ -252,16 +252,18 @@ def counters(key):
 
 
 def parity_sample(args, world, rank, S_local, s0, t_total, cost, idle, n_star, n_cand):
-    """Bitwise check of sampled scenarios of THIS rank's block (spread over
-    every batch, first and last included) against the C port, outside the
-    timed region; --parity-full checks every scenario (minutes of CPU)."""
+    """Bitwise check against the C port, outside the timed region: at N=1
+    every scenario of the sweep (~1 minute on the host cores), at N>1 (or
+    with --parity-sampled-only) --parity-samples scenarios spread over every
+    batch of every rank's block, first and last included."""
     import torch
     from cases import c4_spec
     from oracle_lib import port
     from paper_2602_22718_b200.rollsim import default_profile
     if S_local == 0:
         return 0, True
-    want = S_local if args.parity_full else max(1, -(-args.parity_samples // world))
+    full = args.parity_full or (world == 1 and not args.parity_sampled_only)
+    want = S_local if full else max(1, -(-args.parity_samples // world))
     idx = np.unique(np.linspace(0, S_local - 1, min(want, S_local)).round().astype(np.int64))
     tt_d = t_total.view(S_local, n_cand).cpu().numpy()
     cc_d = cost.view(S_local, n_cand).cpu().numpy()
@@ -817,7 +819,10 @@ def main(argv=None):
     ap.add_argument("--arrays-scenarios", type=int, default=2368,
                     help="scenarios of the e2e_arrays line (host inputs: 786 KB each)")
     ap.add_argument("--parity-samples", type=int, default=64)
-    ap.add_argument("--parity-full", action="store_true", help="bit-check every scenario")
+    ap.add_argument("--parity-full", action="store_true",
+                    help="bit-check every scenario (the default at N=1)")
+    ap.add_argument("--parity-sampled-only", action="store_true",
+                    help="at N=1 too, check only --parity-samples scenarios")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dedup", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
