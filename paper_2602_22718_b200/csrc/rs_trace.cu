@@ -85,6 +85,41 @@ __device__ __forceinline__ int64_t parse_long_at(const unsigned char* t, int64_t
   return p;
 }
 
+// SWAR classification of 16 bytes: bit j of each mask is byte i + j.
+// Bytes outside [lo, hi) read as whitespace (never digits or signs). i is
+// 16-byte aligned; the text buffer is padded, so the load never faults.
+struct Mask16 {
+  uint32_t ws, dig, sgn;
+};
+
+__device__ __forceinline__ uint32_t pack4(uint32_t m) {  // 0xff / 0x00 bytes -> 4 bits
+  return (((m >> 7) & 0x01010101u) * 0x01020408u) >> 24;
+}
+
+__device__ __forceinline__ Mask16 mask16(const unsigned char* t, int64_t i, int64_t lo, int64_t hi) {
+  const uint4 v = *reinterpret_cast<const uint4*>(t + i);
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  Mask16 m{0u, 0u, 0u};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t x = w[q];
+    // std::isspace in the "C" locale: ' ' and '\t' .. '\r'
+    const uint32_t ws = __vcmpeq4(x, 0x20202020u) | (__vcmpgeu4(x, 0x09090909u) & __vcmpleu4(x, 0x0d0d0d0du));
+    const uint32_t dg = __vcmpgeu4(x, 0x30303030u) & __vcmpleu4(x, 0x39393939u);
+    const uint32_t sg = __vcmpeq4(x, 0x2b2b2b2bu) | __vcmpeq4(x, 0x2d2d2d2du);
+    m.ws |= pack4(ws) << (4 * q);
+    m.dig |= pack4(dg) << (4 * q);
+    m.sgn |= pack4(sg) << (4 * q);
+  }
+  uint32_t valid = 0xffffu;
+  if (i < lo) valid &= lo - i >= 16 ? 0u : 0xffffu << (int)(lo - i);
+  if (i + 16 > hi) valid &= hi > i ? 0xffffu >> (int)(16 - (hi - i)) : 0u;
+  m.ws = (m.ws | ~valid) & 0xffffu;
+  m.dig &= valid;
+  m.sgn &= valid;
+  return m;
+}
+
 __global__ void nl_count_kernel(const char* text, int64_t n, uint32_t* cnt) {
   __shared__ uint32_t part[kNlT / 32];
   const int64_t b0 = blockIdx.x * kChunk, b1 = min(n, b0 + kChunk);
@@ -237,42 +272,69 @@ __global__ void classify_kernel(const char* text_c, const int64_t* line_start, i
     // field that starts with one but goes on with other characters may hold
     // more numbers ("12-3" is 12, -3): such lines are counted serially.
     if (li.type == kPrompt && !li.bad) {
+      // 16 bytes per lane (SWAR masks), 512 per warp step; a 32-bit line
+      // position is enough within a step
       const int64_t ts = li.tok_pos;
       int count = 0;       // complete fields so far (warp-uniform)
       int stop = -1;       // tokens when the list ended (warp-uniform)
-      int run = 0;         // non-space characters ending the previous chunk
-      bool prev_ws = true;
+      int run = 0;         // non-space characters ending the previous step
+      uint32_t prev_ws = 1u;
       if (ts < e && !is_ws(t[ts])) li.serial = 1;  // something glued to gt
-      for (int64_t c0 = ts; c0 < e && stop < 0 && !li.serial; c0 += 32) {
-        const int64_t i = c0 + lane;
-        const bool in = i < e;
-        const unsigned char ch = in ? t[i] : ' ';
-        const bool ws = is_ws(ch);
-        const bool up = __shfl_up_sync(0xffffffffu, ws, 1);  // every lane takes part
-        const bool start = !ws && (lane == 0 ? prev_ws : up);
-        const unsigned char nx = i + 1 < e ? t[i + 1] : ' ';
-        const bool digit = ch >= '0' && ch <= '9';
-        const bool sign_ok = start && (ch == '+' || ch == '-') && nx >= '0' && nx <= '9';
-        const unsigned sm = __ballot_sync(0xffffffffu, start);
-        const unsigned wsm = __ballot_sync(0xffffffffu, ws);
-        const unsigned badm = __ballot_sync(0xffffffffu, !ws && !digit && !sign_ok);
-        // non-space run ending at this lane: fields of 19+ characters may
-        // overflow long, so such lines take the exact path
-        const unsigned wsle = wsm & ((2u << lane) - 1);
-        const int r = wsle ? lane - (31 - __clz(wsle)) : lane + 1 + run;
-        if (__any_sync(0xffffffffu, r >= 19)) {
+      for (int64_t b0 = ts & ~(int64_t)15; b0 < e && stop < 0 && !li.serial; b0 += 512) {
+        const int64_t i = b0 + 16 * lane;
+        const Mask16 m = mask16(t, i, ts, e);
+        const uint32_t nonws = ~m.ws & 0xffffu;
+        const uint32_t up = __shfl_up_sync(0xffffffffu, m.ws >> 15, 1);
+        const uint32_t wsprev = ((m.ws << 1) | (lane == 0 ? prev_ws : up)) & 0xffffu;
+        const uint32_t start = nonws & wsprev;
+        // a sign opens a number only if a digit follows (istream >> long)
+        uint32_t dnext = __shfl_down_sync(0xffffffffu, m.dig & 1u, 1);
+        if (lane == 31) {
+          const int64_t j = i + 16;
+          dnext = j < e && t[j] >= '0' && t[j] <= '9' ? 1u : 0u;
+        }
+        const uint32_t dig_next = ((m.dig >> 1) | (dnext << 15)) & 0xffffu;
+        const uint32_t bad = nonws & ~m.dig & ~(start & m.sgn & dig_next) & 0xffffu;
+        // non-space runs: fields of 19+ characters may overflow long, so
+        // such lines take the exact path. Run ending at this lane's end:
+        // a full lane extends the run from the left.
+        const bool full = nonws == 0xffffu;
+        const int lead = __ffs(~nonws) - 1;          // leading non-spaces (16 if full)
+        const int trail = __clz(~(nonws << 16));     // trailing non-spaces (16 if full)
+        int rend = full ? 16 : trail;                // run ending at this lane's end
+        bool rfull = full;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int or_ = __shfl_up_sync(0xffffffffu, rend, d);
+          const bool of = __shfl_up_sync(0xffffffffu, rfull, d);
+          if (lane >= d && rfull) {
+            rend += or_;
+            rfull = of;
+          }
+        }
+        if (rfull) rend += run;  // the whole prefix of lanes is one run from the previous step
+        int left = __shfl_up_sync(0xffffffffu, rend, 1);  // run ending just before this lane
+        if (lane == 0) left = run;
+        if (__any_sync(0xffffffffu, (!full && left + lead >= 19) || rend >= 19)) {
           li.serial = 1;
           break;
         }
-        run = __shfl_sync(0xffffffffu, r, 31);
-        if (badm) {
-          const int bpos = __ffs(badm) - 1;  // the line's first bad character
-          if ((sm >> bpos) & 1u) stop = count + __popc(sm & ((1u << bpos) - 1));  // field fails
+        run = __shfl_sync(0xffffffffu, rend, 31);
+        const unsigned badl = __ballot_sync(0xffffffffu, bad != 0u);
+        const int pc = __popc(start);
+        const int pre = warp_incl_sum(pc) - pc;
+        if (badl) {
+          const int bl = __ffs(badl) - 1;  // the line's first bad character: lane bl ...
+          const uint32_t bbad = __shfl_sync(0xffffffffu, bad, bl);
+          const uint32_t bstart = __shfl_sync(0xffffffffu, start, bl);
+          const int bpre = __shfl_sync(0xffffffffu, pre, bl);
+          const int bit = __ffs(bbad) - 1;  // ... byte bit
+          if ((bstart >> bit) & 1u) stop = count + bpre + __popc(bstart & ((1u << bit) - 1u));  // field fails
           else li.serial = 1;  // a number with more characters glued on
         } else {
-          count += __popc(sm);
+          count += __shfl_sync(0xffffffffu, pre + pc, 31);
         }
-        prev_ws = __shfl_sync(0xffffffffu, ws, 31);
+        prev_ws = __shfl_sync(0xffffffffu, m.ws >> 15, 31);
       }
       li.ntok = stop >= 0 ? stop : count;
       if (li.serial) li.ntok = lane == 0 ? serial_tokens(t, ts, e, nullptr) : 0;
@@ -291,7 +353,7 @@ __global__ void __launch_bounds__(kTokT)
 tokens_kernel(const char* text_c, const int64_t* line_start, int64_t L, int64_t n,
               const LineInfo* info, const int32_t* pline, int32_t P, const int64_t* tok_off,
               int32_t* tok) {
-  __shared__ uint16_t s_fs[kTokT / 32][kTokWin / 2 + 32];
+  __shared__ uint16_t s_fs[kTokT / 32][kTokWin / 2 + 32];  // fields start after a space: <= 512 per window
   const unsigned char* t = reinterpret_cast<const unsigned char*>(text_c);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint16_t* fs = s_fs[w];
@@ -307,24 +369,34 @@ tokens_kernel(const char* text_c, const int64_t* line_start, int64_t L, int64_t 
       continue;
     }
     int count = 0;
-    bool prev_ws = true;
-    for (int64_t w0 = li.tok_pos; w0 < e && count < li.ntok; w0 += kTokWin) {
+    uint32_t prev_wsm = 1u;
+    for (int64_t w0 = li.tok_pos & ~(int64_t)15; w0 < e && count < li.ntok; w0 += kTokWin) {
       int nf = 0;
-      for (int c = 0; c < kTokWin; c += 32) {
-        const int64_t i = w0 + c + lane;
-        const bool ws = i < e ? is_ws(t[i]) : true;
-        const bool up = __shfl_up_sync(0xffffffffu, ws, 1);
-        const bool start = !ws && (lane == 0 ? prev_ws : up);
-        const unsigned sm = __ballot_sync(0xffffffffu, start);
-        if (start) fs[nf + __popc(sm & ((1u << lane) - 1))] = (uint16_t)(c + lane);
-        nf += __popc(sm);
-        prev_ws = __shfl_sync(0xffffffffu, ws, 31);
+      for (int c = 0; c < kTokWin; c += 512) {  // 16 bytes per lane (SWAR masks)
+        const int64_t i = w0 + c + 16 * lane;
+        const Mask16 m = mask16(t, i, li.tok_pos, e);
+        const uint32_t up = __shfl_up_sync(0xffffffffu, m.ws >> 15, 1);
+        uint32_t start = ~m.ws & ((m.ws << 1) | (lane == 0 ? prev_wsm : up)) & 0xffffu;
+        const int pc = __popc(start);
+        int pos = nf + warp_incl_sum(pc) - pc;
+        while (start) {
+          const int j = __ffs(start) - 1;
+          fs[pos++] = (uint16_t)(c + 16 * lane + j);
+          start &= start - 1;
+        }
+        nf = __shfl_sync(0xffffffffu, pos, 31);  // lane 31's end = every start so far
+        prev_wsm = __shfl_sync(0xffffffffu, m.ws >> 15, 31);
       }
       __syncwarp();
       for (int f = lane; f < nf && count + f < li.ntok; f += 32) {
-        long long v = 0;
-        parse_long_at(t, w0 + fs[f], e, &v);
-        out[count + f] = (int32_t)v;
+        // a fast-path field is an integer of < 19 characters (the classify
+        // pass sends longer runs to the serial path): no overflow check needed
+        int64_t p = w0 + fs[f];
+        const bool neg = t[p] == '-';
+        p += (t[p] == '-' || t[p] == '+') ? 1 : 0;
+        unsigned long long m = 0;
+        for (; p < e && t[p] >= '0' && t[p] <= '9'; ++p) m = m * 10u + (unsigned)(t[p] - '0');
+        out[count + f] = (int32_t)(neg ? 0ULL - m : m);
       }
       __syncwarp();
       count += nf;
