@@ -586,7 +586,9 @@ def bench_trace(args, ctx, torch, dev):
     tests/cases.py c2_trace_text) -> id-sorted token CSR in HBM
     (rs_trace_csr_parse), tokens/s. value: text already in HBM; e2e: from
     pinned host text; cpu_baseline: the reference's trace_from_string on the
-    first 4,096 prompts."""
+    same trace shape cut to 4,096 prompts. The trace carries one step
+    scheduling the whole batch (g = 8 rows per prompt, 524,288 step rows),
+    parsed into the step table in the same call."""
     from cases import c2_trace_text
     from paper_2602_22718_b200.lib import check
     text, tok, off = c2_trace_text()
@@ -610,7 +612,9 @@ def bench_trace(args, ctx, torch, dev):
     ctx.enable_kernel_timing(True)
     ctx.reset_kernel_timing()
     parse(d_text.data_ptr(), 1)
-    kt = {n: ctx.kernel_time(n)[0] for n in ("trace_classify", "trace_tokens", "trace_nl_write")}
+    kt = {n: ctx.kernel_time(n)[0] for n in ("trace_classify", "trace_tokens", "trace_nl_write",
+                                             "trace_steprow", "trace_group", "trace_run_scan",
+                                             "trace_entry_scan")}
     ctx.enable_kernel_timing(False)
     pt = torch.from_numpy(text).pin_memory()
     parse(pt.data_ptr(), 0)
@@ -623,7 +627,8 @@ def bench_trace(args, ctx, torch, dev):
     achieved = text.nbytes / (kt[top] / 1e3) / 1e9  # the dominant pass reads the text once
     out = {"metric": "trace prompt-table parse tokens/sec (CSV -> device CSR)", "value": n_tok / dev_s,
            "unit": "tokens/s", "text_bytes": int(text.nbytes), "ms_per_parse": dev_s * 1e3,
-           "config": {"workload": "C2 batch as CSV trace text: 65536 '# prompt' lines x 2560 tokens"},
+           "config": {"workload": "C2 batch as CSV trace text: 65536 '# prompt' lines x 2560 tokens "
+                                  "+ one step of 65536 x 8 rows"},
            "e2e": {"value": n_tok / host_s, "unit": "tokens/s", "h2d_bytes_per_step": int(text.nbytes),
                    "d2h_bytes_per_step": 0},
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -635,14 +640,13 @@ def bench_trace(args, ctx, torch, dev):
         from oracle_lib import ref
         R = ref()
         if R is not None:
-            sample = text[: 22 + 4096 * (20 + 6 * 2560 + 1)].tobytes() + \
-                b"step_idx,prompt_id,response_idx,actual_len\n"
+            sample = c2_trace_text(n_prompts=4096)[0].tobytes()
             t0 = time.perf_counter()
             R.trace_prompts(sample)
             dt = time.perf_counter() - t0
             out["cpu_baseline"] = {"value": 4096 * 2560 / dt, "unit": "tokens/s", "cores": 1,
                                    "kind": "reference",
-                                   "sample": f"first 4,096 prompts ({len(sample) / 1e6:.0f} MB), "
+                                   "sample": f"4,096 prompts + 32,768 step rows ({len(sample) / 1e6:.0f} MB), "
                                              f"trace_from_string, {dt:.1f} s"}
     return out
 

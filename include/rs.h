@@ -328,13 +328,13 @@ int rs_predict_lengths(rs_ctx* ctx, const double* obs, const int32_t* depth,
 /* ------------------------------------------------------------------ */
 /* (1b) Trace prompt table -> device CSR                */
 /* ------------------------------------------------------------------ */
-/* The '# prompt <id> <ground_truth> <tok>...' metadata of a CSV trace
- * (csv_from_string, workload.cpp:169-263; the step rows are not parsed
- * here), parsed on the device from the file bytes (host, or device memory
+/* A CSV trace (csv_from_string, workload.cpp:169-263): the '# prompt <id>
+ * <ground_truth> <tok>...' metadata and the step rows, parsed on the device from the file bytes (host, or device memory
  * when device_ptr != 0) into an id-sorted token CSR in HBM that
  * rs_prefix_index_build_device takes directly. Errors in the reference's
- * order: RS_E_PARSE (malformed metadata, missing or misplaced column
- * header), then RS_E_VALIDATION (WorkloadTrace::validate's prompt rules). */
+ * order: RS_E_PARSE (malformed metadata or step rows, missing or misplaced
+ * column header, first offending line), then RS_E_VALIDATION
+ * (WorkloadTrace::validate's prompt rules, then its step rules). */
 typedef struct rs_trace_csr rs_trace_csr;
 int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes, int device_ptr,
                        rs_trace_csr** out);
@@ -349,6 +349,20 @@ int rs_trace_csr_device(const rs_trace_csr* trace, const int32_t** d_tokens,
  * id_bytes[id_bytes], id_offsets[count+1], ground_truth[count]. */
 int rs_trace_csr_copy(rs_ctx* ctx, const rs_trace_csr* trace, int32_t* tokens, int64_t* offsets,
                       char* id_bytes, int64_t* id_offsets, int32_t* ground_truth);
+/* The step rows (StepRecord, workload.hpp:29-33) as a step table, built on
+ * the device: n_steps steps, n_entries scheduled (step, prompt) entries.
+ * step_idx[n_steps]; entry_off[n_steps + 1] (entries of step s are
+ * [entry_off[s], entry_off[s+1]), in scheduled_prompts order);
+ * entry_prompt[n_entries] indexes the id-sorted prompt table;
+ * lengths[n_entries * g] holds each entry's actual_lengths in response
+ * order. Device views (valid until rs_trace_csr_free; NULL when there are
+ * no rows) and host copies (any pointer may be NULL). */
+int rs_trace_csr_steps_info(const rs_trace_csr* trace, int32_t* n_steps, int64_t* n_entries);
+int rs_trace_csr_steps_device(const rs_trace_csr* trace, const int32_t** step_idx,
+                              const int32_t** entry_off, const int32_t** entry_prompt,
+                              const int32_t** lengths);
+int rs_trace_csr_steps_copy(rs_ctx* ctx, const rs_trace_csr* trace, int32_t* step_idx,
+                            int32_t* entry_off, int32_t* entry_prompt, int32_t* lengths);
 void rs_trace_csr_free(rs_trace_csr* trace);
 
 /* ------------------------------------------------------------------ */

@@ -96,6 +96,8 @@ ORACLE_API(orc_)
 /* Reference-only: the prompt table of a CSV trace via trace_from_string. */
 int ref_trace_prompts(const char* text, int64_t n_bytes, int64_t* info, int32_t* tokens,
                       int64_t* offsets, char* ids, int64_t* id_offsets, int32_t* gt);
+int ref_trace_steps(const char* text, int64_t n_bytes, int64_t* info, int32_t* step_idx,
+                    int32_t* entry_off, int32_t* entry_prompt, int32_t* lengths);
 
 /* Builder-defined oracles (port only). */
 int orc_generate_scenarios(const rs_scenario_spec* spec, double* pred,

@@ -427,6 +427,35 @@ int ref_trace_prompts(const char* text, int64_t n_bytes, int64_t* info, int32_t*
   });
 }
 
+// The step table of a CSV trace through the reference's own reader: info =
+// {n_steps, n_entries, g}; the arrays (nullable) as rs_trace_csr_steps_copy
+// lays them out — step_idx, entry_off, the id-sorted index of each
+// scheduled prompt in batch order, and its actual_lengths.
+int ref_trace_steps(const char* text, int64_t n_bytes, int64_t* info, int32_t* step_idx,
+                    int32_t* entry_off, int32_t* entry_prompt, int32_t* lengths) {
+  return guarded([&] {
+    rollsim::WorkloadTrace t =
+        rollsim::trace_from_string(std::string(text, text + n_bytes), rollsim::TraceFormat::csv);
+    int64_t e = 0;
+    for (size_t s = 0; s < t.steps.size(); ++s) {
+      const rollsim::StepRecord& st = t.steps[s];
+      if (step_idx) step_idx[s] = st.step_idx;
+      if (entry_off) entry_off[s] = (int32_t)e;
+      for (const std::string& id : st.scheduled_prompts) {
+        const rollsim::Prompt* p = t.find_prompt(id);
+        if (entry_prompt) entry_prompt[e] = (int32_t)(p - t.prompts.data());
+        const std::vector<int>& lens = st.actual_lengths.at(id);
+        if (lengths) std::copy(lens.begin(), lens.end(), lengths + e * t.responses_per_prompt);
+        ++e;
+      }
+    }
+    if (entry_off) entry_off[t.steps.size()] = (int32_t)e;
+    info[0] = (int64_t)t.steps.size();
+    info[1] = e;
+    info[2] = t.responses_per_prompt;
+  });
+}
+
 int ref_sweep_arrays(const double* pred, const int32_t* plen,
                      int32_t n_scenarios, int32_t count, const rs_profile* p,
                      int32_t g, int32_t n_min, int32_t n_max, double lambda,

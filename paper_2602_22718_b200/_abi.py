@@ -115,6 +115,10 @@ PRODUCT_SIGS = {
     "rs_trace_csr_info": ([vp, P_i32, P_i64, P_i64, P_i32, P_i32, P_i32], C.c_int),
     "rs_trace_csr_device": ([vp, C.POINTER(vp), C.POINTER(vp)], C.c_int),
     "rs_trace_csr_copy": ([vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "rs_trace_csr_steps_info": ([vp, P_i32, P_i64], C.c_int),
+    "rs_trace_csr_steps_device": ([vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)],
+                                  C.c_int),
+    "rs_trace_csr_steps_copy": ([vp, vp, vp, vp, vp, vp], C.c_int),
     "rs_trace_csr_free": ([vp], None),
     "rs_scale_select": ([vp, P_f64, P_f64, P_f64, i32, i32, f64, P_f64, P_f64, P_f64, P_i32], C.c_int),
     "rs_generate_scenarios": ([vp, C.POINTER(RsScenarioSpec), vp, vp, C.c_int], C.c_int),
@@ -161,6 +165,7 @@ ORACLE_SIGS = {
 
 REF_ONLY_SIGS = {
     "ref_trace_prompts": ([vp, i64, P_i64, vp, vp, vp, vp, vp], C.c_int),
+    "ref_trace_steps": ([vp, i64, P_i64, vp, vp, vp, vp], C.c_int),
 }
 
 PORT_ONLY_SIGS = {

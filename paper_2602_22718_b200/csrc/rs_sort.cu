@@ -132,9 +132,106 @@ exclusive_scan_u32_kernel(const uint32_t* in, uint32_t* out, int64_t n) {
   }
 }
 
+// ------------------------------------------------------ multi-CTA scan --
+// Three launches: per-tile sums, one CTA scanning the tile sums (and the
+// total), per-tile scans with the tile base. 512 threads x 8 items per tile.
+namespace {
+constexpr int kScanT = 512;
+constexpr int kScanIPT = 8;
+constexpr int64_t kScanTile = kScanT * kScanIPT;
+
+template <class T>
+__device__ __forceinline__ T block_excl_sum(T v, T* wsum, T* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const T incl = warp_incl_sum(v);
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const T x = lane < kScanT / 32 ? wsum[lane] : T(0);
+    const T xi = warp_incl_sum(x);
+    if (lane < kScanT / 32) wsum[lane] = xi - x;
+    if (lane == 31) *total = xi;
+  }
+  __syncthreads();
+  return wsum[w] + incl - v;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kScanT) scan_reduce_kernel(const T* in, int64_t n, T* part) {
+  __shared__ T wsum[kScanT / 32];
+  __shared__ T tot;
+  const int64_t b = blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanIPT;
+  T v = 0;
+#pragma unroll
+  for (int j = 0; j < kScanIPT; ++j)
+    if (b + j < n) v += in[b + j];
+  block_excl_sum(v, wsum, &tot);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kScanT) scan_partials_kernel(T* part, int64_t nt, T* total) {
+  __shared__ T wsum[kScanT / 32];
+  __shared__ T tot;
+  T carry = 0;
+  for (int64_t t0 = 0; t0 < nt; t0 += kScanT) {
+    const int64_t i = t0 + threadIdx.x;
+    const T v = i < nt ? part[i] : T(0);
+    const T ex = block_excl_sum(v, wsum, &tot);
+    if (i < nt) part[i] = carry + ex;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && total) *total = carry;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kScanT) scan_apply_kernel(const T* in, T* out, int64_t n, const T* part) {
+  __shared__ T wsum[kScanT / 32];
+  __shared__ T tot;
+  const int64_t b = blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanIPT;
+  T x[kScanIPT];
+  T v = 0;
+#pragma unroll
+  for (int j = 0; j < kScanIPT; ++j) {
+    x[j] = b + j < n ? in[b + j] : T(0);
+    v += x[j];
+  }
+  T run = part[blockIdx.x] + block_excl_sum(v, wsum, &tot);
+#pragma unroll
+  for (int j = 0; j < kScanIPT; ++j)
+    if (b + j < n) {
+      out[b + j] = run;
+      run += x[j];
+    }
+}
+}  // namespace
+
+size_t scan_scratch_bytes(int64_t n, size_t elem) {
+  return abytes((n + kScanTile - 1) / kScanTile + 1, elem);
+}
+
+template <class T>
+int exclusive_scan(rs_ctx* ctx, const T* in, T* out, int64_t n, T* scratch, T* total) {
+  const int64_t nt = (n + kScanTile - 1) / kScanTile;
+  if (nt == 0) {
+    if (total) RS_CUDA_TRY(cudaMemsetAsync(total, 0, sizeof(T), ctx->stream));
+    return RS_OK;
+  }
+  RS_LAUNCH(ctx, "scan_reduce", scan_reduce_kernel<T>, (int)nt, kScanT, 0, in, n, scratch);
+  RS_LAUNCH(ctx, "scan_partials", scan_partials_kernel<T>, 1, kScanT, 0, scratch, nt, total);
+  RS_LAUNCH(ctx, "scan_apply", scan_apply_kernel<T>, (int)nt, kScanT, 0, in, out, n, scratch);
+  return RS_OK;
+}
+
+template int exclusive_scan<uint32_t>(rs_ctx*, const uint32_t*, uint32_t*, int64_t, uint32_t*, uint32_t*);
+template int exclusive_scan<unsigned long long>(rs_ctx*, const unsigned long long*, unsigned long long*,
+                                                int64_t, unsigned long long*, unsigned long long*);
+
 size_t radix_sort_scratch_bytes64(int64_t n) {
   int64_t ntiles = (n + kTile - 1) / kTile;
-  return abytes(n, 8) + abytes(n, 4) + abytes(256 * ntiles, 4) * 2 + abytes(2, 8);
+  return abytes(n, 8) + abytes(n, 4) + abytes(256 * ntiles, 4) * 2 + abytes(2, 8) +
+         scan_scratch_bytes(256 * ntiles, 4);
 }
 
 int radix_sort_pairs(rs_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t n,
@@ -148,7 +245,8 @@ int radix_sort_pairs(rs_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t n,
   uint32_t* v2 = (uint32_t*)q; q += abytes(n, 4);
   uint32_t* hist = (uint32_t*)q; q += abytes(256 * ntiles, 4);
   uint32_t* offs = (uint32_t*)q; q += abytes(256 * ntiles, 4);
-  unsigned long long* ao = (unsigned long long*)q;
+  unsigned long long* ao = (unsigned long long*)q; q += abytes(2, 8);
+  uint32_t* scan_part = (uint32_t*)q;
   unsigned long long init[2] = {~0ULL, 0ULL};
   RS_CUDA_TRY(cudaMemcpyAsync(ao, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 4 * ctx->num_sms);
@@ -165,8 +263,12 @@ int radix_sort_pairs(rs_ctx* ctx, uint64_t* keys, uint32_t* vals, int64_t n,
     if (((vary >> shift) & 255) == 0) continue;
     RS_LAUNCH(ctx, "radix_hist", radix_hist_kernel, (int)ntiles, kSortThreads, 0,
               kin, n, shift, hist, (int)ntiles);
-    RS_LAUNCH(ctx, "radix_scan", exclusive_scan_u32_kernel, 1, 1024, 0, hist,
-              offs, (int64_t)256 * ntiles);
+    if (ntiles >= 64) {  // one CTA would walk 256 x ntiles counts alone
+      RS_TRY(exclusive_scan<uint32_t>(ctx, hist, offs, 256 * ntiles, scan_part, nullptr));
+    } else {
+      RS_LAUNCH(ctx, "radix_scan", exclusive_scan_u32_kernel, 1, 1024, 0, hist,
+                offs, (int64_t)256 * ntiles);
+    }
     RS_LAUNCH(ctx, "radix_scatter", radix_scatter_kernel, (int)ntiles,
               kSortThreads, 0, kin, vin, kout, vout, n, shift, offs, (int)ntiles);
     std::swap(kin, kout);

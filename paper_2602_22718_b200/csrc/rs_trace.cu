@@ -24,9 +24,20 @@
 //   * prompts are then sorted by id (std::string order) and validated like
 //     WorkloadTrace::validate (workload.cpp:34-60): unique non-empty ids,
 //     1 <= prompt_len <= max_prompt_len, 1 <= gt <= max_response_len.
-// The step rows after the header are not parsed here.
+//   * the step rows after the header (split on ',', 4 trimmed fields, the
+//     integers read by std::stol) are parsed one thread per row and grouped
+//     by (step run, prompt) with a device radix sort, which checks the
+//     reader's response_idx order and the validator's step rules
+//     (workload.cpp:53-91) and yields the step table: step_idx per step,
+//     the scheduled prompts per step in batch order (indices into the
+//     id-sorted table) and their g lengths in response order.
 #include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -260,7 +271,16 @@ __global__ void classify_kernel(const char* text_c, const int64_t* line_start, i
         li.type = klen == 1 ? kG : (klen == 14 ? kMaxPrompt : kMaxResponse);
         while (p < e && is_ws(t[p])) ++p;
         long long v = 0;
-        if (parse_long_at(t, p, e, &v) < 0) li.bad = 1;
+        if (parse_long_at(t, p, e, &v) < 0) {
+          // `ms >> v` failed: "# g" is a ParseError; the max_* keys keep what
+          // num_get stored — LONG_MAX / LONG_MIN when the digits overflow,
+          // else 0 (an empty field leaves v unset in the reference: 0 here)
+          li.bad = 1;
+          int64_t q = p;
+          const bool neg = q < e && t[q] == '-';
+          if (q < e && (t[q] == '+' || t[q] == '-')) ++q;
+          v = q < e && t[q] >= '0' && t[q] <= '9' ? (neg ? LLONG_MIN : LLONG_MAX) : 0;
+        }
         li.val = v;
       } else {
         li.type = kOtherMeta;
@@ -412,6 +432,333 @@ __global__ void ids_gather_kernel(const char* text, const LineInfo* info, const 
   }
 }
 
+// -------------------------------------------------- line bookkeeping --
+// The reader's line loop (workload.cpp:178-225) as reductions and one
+// compaction over the classified lines, so only scalars cross to the host.
+struct LineStat {
+  unsigned int header;      // first body line (~0u: none) = the column header
+  unsigned int first_bad;   // first malformed '# prompt' / '# g' line before it
+  unsigned int meta_after;  // first '#' line after it
+  unsigned int last_g, last_mp, last_mr;  // last '# g' / max_* line before it, + 1 (0: none)
+  unsigned int maxid;       // longest prompt id
+  int bad_type;             // LineType of first_bad
+  int header_ok;            // the header line reads step_idx,prompt_id,response_idx,actual_len
+  int pad;
+  long long g, mp, mr;      // the values of last_g / last_mp / last_mr
+  unsigned long long counts;  // prompt lines << 32 | step rows
+  unsigned long long n_tok, n_idb;
+};
+
+__device__ __forceinline__ void warp_min_u32(unsigned int* addr, unsigned int v) {
+  const unsigned int m = __reduce_min_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0 && m != ~0u) atomicMin(addr, m);
+}
+
+__global__ void line_header_kernel(const LineInfo* info, int64_t L, LineStat* st) {
+  const int64_t L32 = (L + 31) & ~(int64_t)31;  // whole warps for the reductions
+  for (int64_t ln = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ln < L32;
+       ln += (int64_t)gridDim.x * blockDim.x)
+    warp_min_u32(&st->header, ln < L && info[ln].type == kBody ? (unsigned int)ln : ~0u);
+}
+
+// prompt lines before the header and body lines after it, as one u64 flag
+// (prompt << 32 | row) for a single scan; the rare lines by atomics.
+__global__ void line_flags_kernel(const LineInfo* info, int64_t L, LineStat* st,
+                                  unsigned long long* flags) {
+  const unsigned int header = st->header;
+  const int64_t L32 = (L + 31) & ~(int64_t)31;
+  for (int64_t ln = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ln < L32;
+       ln += (int64_t)gridDim.x * blockDim.x) {
+    unsigned int bad = ~0u, after = ~0u;
+    if (ln < L) {
+      const LineInfo li = info[ln];
+      const bool before = (unsigned int)ln < header;
+      unsigned long long f = 0;
+      if (li.type == kBody) {
+        f = (unsigned int)ln > header ? 1ULL : 0ULL;
+      } else if (li.type != kEmpty) {
+        if (!before) after = (unsigned int)ln;
+        else if (li.type == kPrompt) f = 1ULL << 32;
+        if (before && li.bad && (li.type == kPrompt || li.type == kG)) bad = (unsigned int)ln;
+        if (before && li.type == kG) atomicMax(&st->last_g, (unsigned int)ln + 1);
+        if (before && li.type == kMaxPrompt) atomicMax(&st->last_mp, (unsigned int)ln + 1);
+        if (before && li.type == kMaxResponse) atomicMax(&st->last_mr, (unsigned int)ln + 1);
+      }
+      flags[ln] = f;
+    }
+    warp_min_u32(&st->first_bad, bad);
+    warp_min_u32(&st->meta_after, after);
+  }
+}
+
+__global__ void line_compact_kernel(const LineInfo* info, const unsigned long long* flags,
+                                    const unsigned long long* pos, int64_t L, int32_t* pline,
+                                    uint32_t* rline, unsigned long long* pntok,
+                                    unsigned long long* pidlen, int32_t* pgt, LineStat* st) {
+  const int64_t L32 = (L + 31) & ~(int64_t)31;
+  for (int64_t ln = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ln < L32;
+       ln += (int64_t)gridDim.x * blockDim.x) {
+    unsigned int idl = 0, ntok = 0;
+    if (ln < L) {
+      const unsigned long long f = flags[ln];
+      if (f >> 32) {
+        const LineInfo li = info[ln];
+        const unsigned long long i = pos[ln] >> 32;
+        pline[i] = (int32_t)ln;
+        pntok[i] = (unsigned long long)li.ntok;
+        pidlen[i] = (unsigned long long)li.id_len;
+        pgt[i] = (int32_t)li.val;
+        idl = (unsigned int)li.id_len;
+        ntok = (unsigned int)li.ntok;
+      } else if (f) {
+        rline[pos[ln] & 0xffffffffULL] = (uint32_t)ln;
+      }
+    }
+    const unsigned int m = __reduce_max_sync(0xffffffffu, idl);
+    const unsigned int sid = __reduce_add_sync(0xffffffffu, idl);
+    const unsigned int stok = __reduce_add_sync(0xffffffffu, ntok);
+    if ((threadIdx.x & 31) == 0 && (sid | stok)) {
+      atomicMax(&st->maxid, m);
+      atomicAdd(&st->n_idb, (unsigned long long)sid);
+      atomicAdd(&st->n_tok, (unsigned long long)stok);
+    }
+  }
+}
+
+// The metadata values and the column header check (workload.cpp:216-224:
+// the trimmed line with its spaces removed), one thread.
+__global__ void line_meta_kernel(const char* text_c, const int64_t* line_start, const LineInfo* info,
+                                 int64_t L, int64_t n, LineStat* st) {
+  const unsigned char* t = reinterpret_cast<const unsigned char*>(text_c);
+  if (st->last_g) st->g = info[st->last_g - 1].val;
+  if (st->last_mp) st->mp = info[st->last_mp - 1].val;
+  if (st->last_mr) st->mr = info[st->last_mr - 1].val;
+  if (st->first_bad != ~0u) st->bad_type = info[st->first_bad].type;
+  if (st->header == ~0u) return;
+  const int64_t h = st->header;
+  int64_t s = line_start[h], e = h + 1 < L ? line_start[h + 1] - 1 : n;
+  while (s < e && (t[s] == ' ' || t[s] == '\t' || t[s] == '\r')) ++s;
+  while (e > s && (t[e - 1] == ' ' || t[e - 1] == '\t' || t[e - 1] == '\r')) --e;
+  const char* want = "step_idx,prompt_id,response_idx,actual_len";
+  int k = 0;
+  bool ok = true;
+  for (int64_t i = s; i < e && ok; ++i) {
+    if (t[i] == ' ') continue;
+    ok = want[k] != 0 && (unsigned char)want[k] == t[i];
+    ++k;
+  }
+  st->header_ok = ok && want[k] == 0;
+}
+
+// ---------------------------------------------------------- step rows --
+// The body of the CSV trace (csv_from_string, workload.cpp:226-258): after
+// the column header every non-empty line is `step_idx,prompt_id,
+// response_idx,actual_len` — split on ',' into exactly 4 fields, each
+// trimmed of " \t\r", the three integers read by std::stol with nothing
+// left over. One thread per line.
+struct SRow {
+  int64_t id_s;
+  int32_t id_len;
+  int32_t step, ridx, len;
+  int32_t pidx;  // index in the id-sorted prompt table, -1: unknown id
+  int32_t code;  // 0 ok, 1: not 4 fields, 2: field 0 / 2 / 3 not an integer
+  int32_t nf;    // fields found (code 1)
+};
+
+// std::stol(s, &pos) with pos == s.size() on the trimmed field [p, e):
+// leading isspace skipped, optional sign, >= 1 digit, no overflow of long,
+// nothing after the digits.
+__device__ bool stol_exact(const unsigned char* t, int64_t p, int64_t e, long long* v) {
+  while (p < e && is_ws(t[p])) ++p;
+  const int64_t q = parse_long_at(t, p, e, v);
+  return q >= 0 && q == e;
+}
+
+__device__ __forceinline__ int id_cmp(const unsigned char* a, int64_t la, const char* b, int64_t lb) {
+  const int64_t n = la < lb ? la : lb;
+  for (int64_t i = 0; i < n; ++i) {
+    const unsigned char cb = (unsigned char)b[i];
+    if (a[i] != cb) return a[i] < cb ? -1 : 1;
+  }
+  return la < lb ? -1 : (la > lb ? 1 : 0);
+}
+
+__global__ void steprow_kernel(const char* text_c, const int64_t* line_start, const uint32_t* rline,
+                               int64_t R, int64_t L, int64_t n, const char* sids,
+                               const int64_t* sid_off, int32_t P, SRow* rows) {
+  const unsigned char* t = reinterpret_cast<const unsigned char*>(text_c);
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ln = rline[r];
+    int64_t s = line_start[ln];
+    int64_t e = ln + 1 < L ? line_start[ln + 1] - 1 : n;
+    while (s < e && (t[s] == ' ' || t[s] == '\t' || t[s] == '\r')) ++s;
+    while (e > s && (t[e - 1] == ' ' || t[e - 1] == '\t' || t[e - 1] == '\r')) --e;
+    SRow row{};
+    row.pidx = -1;
+    int64_t fs[4], fe[4];
+    int nf = 0;
+    int64_t a = s;
+    for (int64_t i = s; i <= e; ++i)
+      if (i == e || t[i] == ',') {
+        if (nf < 4) {
+          fs[nf] = a;
+          fe[nf] = i;
+        }
+        ++nf;
+        a = i + 1;
+      }
+    row.nf = nf;
+    if (nf != 4) {
+      row.code = 1;
+    } else {
+      for (int f = 0; f < 4; ++f) {  // trim " \t\r"
+        while (fs[f] < fe[f] && (t[fs[f]] == ' ' || t[fs[f]] == '\t' || t[fs[f]] == '\r')) ++fs[f];
+        while (fe[f] > fs[f] && (t[fe[f] - 1] == ' ' || t[fe[f] - 1] == '\t' || t[fe[f] - 1] == '\r')) --fe[f];
+      }
+      long long v0 = 0, v2 = 0, v3 = 0;
+      if (!stol_exact(t, fs[0], fe[0], &v0) || !stol_exact(t, fs[2], fe[2], &v2) ||
+          !stol_exact(t, fs[3], fe[3], &v3)) {
+        row.code = 2;
+      } else {
+        row.step = (int32_t)v0;
+        row.ridx = (int32_t)v2;
+        row.len = (int32_t)v3;
+        row.id_s = fs[1];
+        row.id_len = (int32_t)(fe[1] - fs[1]);
+        int lo = 0, hi = P;  // the id in the sorted prompt table
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          const int c = id_cmp(t + row.id_s, row.id_len, sids + sid_off[mid], sid_off[mid + 1] - sid_off[mid]);
+          if (c == 0) {
+            row.pidx = mid;
+            break;
+          }
+          if (c < 0) hi = mid;
+          else lo = mid + 1;
+        }
+      }
+    }
+    rows[r] = row;
+  }
+}
+
+// Rows in order: step decrease (code 3) and run starts (a new StepRecord,
+// csv_from_string's `cur->step_idx != step`).
+__global__ void row_runs_kernel(SRow* rows, int64_t R, uint32_t* run_head) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t step = rows[r].step;
+    const int32_t prev = r > 0 ? rows[r - 1].step : 0;
+    run_head[r] = r == 0 || prev != step ? 1u : 0u;
+    if (r > 0 && rows[r].code == 0 && rows[r - 1].code == 0 && step < prev) rows[r].code = 3;
+  }
+}
+
+// The (run, prompt) grouping key of each row (run = exclusive scan of the
+// run heads + head - 1); unknown ids get P + row, a group of their own,
+// checked on the host.
+__global__ void row_group_key_kernel(const SRow* rows, const uint32_t* run_head,
+                                     const uint32_t* run_excl, int64_t R, int32_t P,
+                                     uint64_t* key, uint32_t* val) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const SRow row = rows[r];
+    const uint64_t run = run_excl[r] + run_head[r] - 1;
+    const uint64_t pk = row.pidx >= 0 ? (uint64_t)row.pidx : (uint64_t)P + (uint64_t)r;
+    key[r] = (run << 32) | pk;
+    val[r] = (uint32_t)r;
+  }
+}
+
+__device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t n, uint64_t k) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < k) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Sorted by (run, prompt, row): the position inside the group is the
+// response_idx the reader expects (code 4 otherwise, expected kept in nf);
+// group heads flagged in row order.
+__global__ void row_group_kernel(SRow* rows, const uint64_t* skey, const uint32_t* srow, int64_t R,
+                                 int32_t P, uint32_t* head, uint32_t* gstart) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < R;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = skey[p];
+    const int64_t lo = p > 0 && skey[p - 1] == k ? lower_bound_u64(skey, p, k) : p;
+    const uint32_t r = srow[p];
+    head[r] = p == lo ? 1u : 0u;
+    gstart[p] = (uint32_t)lo;
+    const bool known = (k & 0xffffffffULL) < (uint64_t)P;
+    if (known && rows[r].code == 0 && rows[r].ridx != (int32_t)(p - lo)) {
+      rows[r].code = 4;
+      rows[r].nf = (int32_t)(p - lo);
+    }
+  }
+}
+
+// First offending row (rows are in line order) and the rows with an id the
+// prompt table does not hold.
+__global__ void row_err_kernel(const SRow* rows, int64_t R, unsigned long long* stat) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const SRow row = rows[r];
+    if (row.code) atomicMin(&stat[0], (unsigned long long)r);
+    else if (row.pidx < 0) atomicAdd(&stat[1], 1ULL);
+  }
+}
+
+// WorkloadTrace::validate's per-prompt step rules (workload.cpp:72-91) on
+// each known group: exactly g lengths, each in [1, max_response_len]. The
+// first bad group in (step, id) order — the validator's order, the map
+// being id-sorted — is the smallest key.
+__global__ void group_check_kernel(const SRow* rows, const uint64_t* skey, const uint32_t* srow,
+                                   int64_t R, int32_t P, int32_t g, int32_t max_len,
+                                   unsigned long long* bad) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < R;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = skey[p];
+    if ((k & 0xffffffffULL) >= (uint64_t)P || (p > 0 && skey[p - 1] == k)) continue;
+    int64_t e = p + 1;
+    while (e < R && skey[e] == k && e - p <= g) ++e;
+    bool ok = e - p == g && (e == R || skey[e] != k);
+    for (int64_t q = p; ok && q < e; ++q) {
+      const int32_t len = rows[srow[q]].len;
+      ok = len >= 1 && len <= max_len;
+    }
+    if (!ok) atomicMin(bad, (unsigned long long)k);
+  }
+}
+
+// The step table: run heads give step_idx and the first entry of each step;
+// group heads (first appearance of an id in its step) are the entries, in
+// scheduled order; every row lands at lengths[entry * g + response_idx].
+__global__ void step_table_kernel(const SRow* rows, const uint32_t* run_head, const uint32_t* run_excl,
+                                  const uint32_t* head, const uint32_t* epos, int64_t R,
+                                  int32_t* step_idx, int32_t* entry_off, int32_t* entry_prompt) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    if (run_head[r]) {
+      step_idx[run_excl[r]] = rows[r].step;
+      entry_off[run_excl[r]] = (int32_t)epos[r];
+    }
+    if (head[r]) entry_prompt[epos[r]] = rows[r].pidx;
+  }
+}
+
+__global__ void step_lengths_kernel(const SRow* rows, const uint32_t* srow, const uint32_t* gstart,
+                                    const uint32_t* epos, int64_t R, int32_t g, int32_t* lengths) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < R;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t lo = gstart[p];
+    lengths[(int64_t)epos[srow[lo]] * g + (p - lo)] = rows[srow[p]].len;
+  }
+}
+
 // sorted position r takes prompt perm[r]: copy its tokens
 __global__ void csr_gather_kernel(const int32_t* src, const int64_t* src_off, const uint32_t* perm,
                                   int32_t P, const int64_t* dst_off, int32_t* dst) {
@@ -436,17 +783,25 @@ struct rs_trace_csr {
   std::vector<int64_t> id_off;
   std::vector<int32_t> gt;
   std::vector<int64_t> offsets;
+  // the step table (rs_trace_csr_steps_*)
+  int32_t n_steps = 0;
+  int64_t n_entries = 0;
+  int32_t* d_step_idx = nullptr;
+  int32_t* d_entry_off = nullptr;
+  int32_t* d_entry_prompt = nullptr;
+  int32_t* d_lengths = nullptr;
   // The outputs are stream-ordered allocations, complete when the parse
   // returns. The handle may outlive its context (and the context's streams),
   // so it is freed with the synchronous cudaFree on its own device.
   int device = 0;
   ~rs_trace_csr() {
-    if (!d_tokens && !d_offsets) return;
+    void* bufs[6] = {d_tokens, d_offsets, d_step_idx, d_entry_off, d_entry_prompt, d_lengths};
+    if (std::all_of(bufs, bufs + 6, [](void* b) { return b == nullptr; })) return;
     int prev = -1;
     cudaGetDevice(&prev);
     if (prev != device) cudaSetDevice(device);
-    if (d_tokens) cudaFree(d_tokens);
-    if (d_offsets) cudaFree(d_offsets);
+    for (void* b : bufs)
+      if (b) cudaFree(b);
     if (prev >= 0 && prev != device) cudaSetDevice(prev);
     cudaGetLastError();
   }
@@ -471,9 +826,281 @@ struct AsyncBuf {
   }
 };
 
+// RS_TRACE_PHASES=1: host wall time of each parse phase on stderr (tools/prof_trace.py).
+struct PhaseClock {
+  bool on = std::getenv("RS_TRACE_PHASES") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "  [trace phase] %-22s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 static int parse_error(int64_t line, const std::string& what) {
   return fail(RS_E_PARSE, "<trace>:" + std::to_string(line + 1) + ": " + what);
 }
+
+static std::string trim_ws(const std::string& s) {  // trim, workload.cpp:112-117
+  const size_t a = s.find_first_not_of(" \t\r");
+  if (a == std::string::npos) return "";
+  return s.substr(a, s.find_last_not_of(" \t\r") - a + 1);
+}
+
+// The step rows of the CSV body (csv_from_string's loop after the column
+// header, workload.cpp:226-258) on the device, in two stages so the errors
+// come in the reference's order: parse() raises the rows' ParseErrors (the
+// caller has already raised the metadata ones before them in line order),
+// table() runs after the prompt rules of WorkloadTrace::validate with the
+// step rules (workload.cpp:53-91) and writes the step table into the handle.
+struct StepRows {
+  rs_ctx* ctx;
+  rs_trace_csr* tr;
+  const char* d_text;
+  const char* text;  // the caller's bytes (device memory when device_ptr)
+  int device_ptr;
+  int64_t n_bytes, L;
+  const int64_t* line_start;
+  const uint32_t* d_rline = nullptr;  // the R body rows after the header, line order
+  int64_t R = 0;
+  AsyncBuf buf;
+  SRow* rows = nullptr;
+  uint32_t *run_head = nullptr, *run_excl = nullptr, *head = nullptr,
+           *epos = nullptr, *gstart = nullptr, *srow = nullptr;
+  uint64_t* skey = nullptr;
+  uint32_t* scan_part = nullptr;
+  unsigned long long* stat = nullptr;  // first error row, unknown-id rows, first bad group
+  std::vector<SRow> h_rows;            // downloaded only on the error paths
+  int64_t first_unknown = -1;
+
+  int grid(int64_t n) const {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 32 * (int64_t)ctx->num_sms));
+  }
+
+  std::string line_text(int64_t ln) {
+    int64_t a = 0, b = 0;
+    if (d2h(ctx, &a, line_start + ln, 8) || (ln + 1 < L && d2h(ctx, &b, line_start + ln + 1, 8)) ||
+        sync_and_check(ctx))
+      return "";
+    b = ln + 1 < L ? b - 1 : n_bytes;
+    std::string out((size_t)std::max<int64_t>(0, b - a), '\0');
+    if (!out.empty() && (d2h(ctx, &out[0], d_text + a, out.size()) || sync_and_check(ctx))) return "";
+    return out;
+  }
+
+  int rows_to_host() {
+    if ((int64_t)h_rows.size() == R) return RS_OK;
+    h_rows.resize(R);
+    RS_TRY(d2h(ctx, h_rows.data(), rows, sizeof(SRow) * R));
+    return sync_and_check(ctx);
+  }
+
+  std::string id_text(const SRow& row) {
+    std::string id((size_t)row.id_len, '\0');
+    if (row.id_len && d2h(ctx, &id[0], d_text + row.id_s, id.size()) == RS_OK) sync_and_check(ctx);
+    return id;
+  }
+
+  int64_t line_of(int64_t r) {
+    uint32_t ln = 0;
+    if (d2h(ctx, &ln, d_rline + r, 4) || sync_and_check(ctx)) return -1;
+    return ln;
+  }
+
+  // The reader's message for row r (workload.cpp:227-253), rebuilt on the host.
+  int row_error(int64_t r, const SRow& row) {
+    const int64_t ln = line_of(r);
+    if (row.code == 1) return parse_error(ln, "expected 4 fields, got " + std::to_string(row.nf));
+    if (row.code == 3) return parse_error(ln, "step indices must not decrease");
+    if (row.code == 4)
+      return parse_error(ln, "response_idx out of order for prompt '" + id_text(row) + "' (expected " +
+                                 std::to_string(row.nf) + ", got " + std::to_string(row.ridx) + ")");
+    std::vector<std::string> f(1);
+    for (char c : trim_ws(line_text(ln))) {
+      if (c == ',') f.emplace_back();
+      else f.back() += c;
+    }
+    for (int i : {0, 2, 3}) {
+      const std::string v = trim_ws(f[i]);
+      bool ok = true;
+      try {
+        size_t pos = 0;
+        (void)std::stol(v, &pos);
+        ok = pos == v.size();
+      } catch (const std::exception&) {
+        ok = false;
+      }
+      if (!ok) return parse_error(ln, "expected integer, got '" + v + "'");
+    }
+    return parse_error(ln, "malformed step row");
+  }
+
+  int parse(int64_t meta_after) {
+    if (R == 0) return meta_after >= 0 ? parse_error(meta_after, "metadata after the column header") : RS_OK;
+    if (R >= (int64_t)INT32_MAX / 2) return fail(RS_E_ARG, "trace has too many step rows");
+    const int32_t P = tr->count;
+    // device copies of the id-sorted prompt ids for the lookup
+    const size_t scratch = radix_sort_scratch_bytes64(R) + scan_scratch_bytes(R, 4);
+    const size_t bytes = abytes(R, sizeof(SRow)) + abytes(R, 4) * 6 + abytes(R, 8) + abytes(4, 8) +
+                         abytes(tr->ids.size() + 1, 1) + abytes(P + 1, 8) + scratch;
+    char* b = buf.alloc<char>(ctx->stream, bytes);
+    if (!b) return fail(RS_E_NOMEM, "trace step rows: allocation failed");
+    auto carve = [&](size_t n) {
+      char* q = b;
+      b += n;
+      return q;
+    };
+    rows = (SRow*)carve(abytes(R, sizeof(SRow)));
+    run_head = (uint32_t*)carve(abytes(R, 4));
+    run_excl = (uint32_t*)carve(abytes(R, 4));
+    head = (uint32_t*)carve(abytes(R, 4));
+    epos = (uint32_t*)carve(abytes(R, 4));
+    gstart = (uint32_t*)carve(abytes(R, 4));
+    uint32_t* val = (uint32_t*)carve(abytes(R, 4));
+    uint64_t* key = (uint64_t*)carve(abytes(R, 8));
+    stat = (unsigned long long*)carve(abytes(4, 8));
+    char* d_sids = carve(abytes(tr->ids.size() + 1, 1));
+    int64_t* d_sid_off = (int64_t*)carve(abytes(P + 1, 8));
+    scan_part = (uint32_t*)carve(scan_scratch_bytes(R, 4));
+    char* d_scratch = carve(radix_sort_scratch_bytes64(R));
+    if (!tr->ids.empty()) RS_TRY(h2d(ctx, d_sids, tr->ids.data(), tr->ids.size()));
+    RS_TRY(h2d(ctx, d_sid_off, tr->id_off.data(), 8ull * (P + 1)));
+    const unsigned long long init[4] = {~0ULL, 0ULL, ~0ULL, 0ULL};
+    RS_TRY(h2d(ctx, stat, init, sizeof init));
+    const int gr = grid(R);
+    RS_LAUNCH(ctx, "trace_steprow", steprow_kernel, gr, 256, 0, d_text, line_start, d_rline, R, L,
+              n_bytes, d_sids, d_sid_off, P, rows);
+    RS_LAUNCH(ctx, "trace_runs", row_runs_kernel, gr, 256, 0, rows, R, run_head);
+    RS_TRY(exclusive_scan<uint32_t>(ctx, run_head, run_excl, R, scan_part, nullptr));
+    RS_LAUNCH(ctx, "trace_group_key", row_group_key_kernel, gr, 256, 0, rows, run_head, run_excl, R, P,
+              key, val);
+    RS_TRY(radix_sort_pairs(ctx, key, val, R, d_scratch, &skey, &srow));
+    RS_LAUNCH(ctx, "trace_group", row_group_kernel, gr, 256, 0, rows, skey, srow, R, P, head, gstart);
+    RS_LAUNCH(ctx, "trace_row_err", row_err_kernel, gr, 256, 0, rows, R, stat);
+    unsigned long long st[2];
+    RS_TRY(d2h(ctx, st, stat, sizeof st));
+    RS_TRY(sync_and_check(ctx));
+    int64_t err_r = st[0] == ~0ULL ? R : (int64_t)st[0];
+    int64_t host_err = -1;  // an unknown id's response_idx out of order
+    if (st[1] > 0) {
+      RS_TRY(rows_to_host());
+      std::string host_text;
+      const char* t = text;
+      if (device_ptr) {
+        host_text.resize((size_t)n_bytes);
+        if (n_bytes) RS_TRY(d2h(ctx, &host_text[0], d_text, (size_t)n_bytes));
+        RS_TRY(sync_and_check(ctx));
+        t = host_text.data();
+      }
+      std::map<std::pair<int64_t, std::string>, int32_t> seen;
+      int64_t run = -1;
+      for (int64_t r = 0; r < err_r; ++r) {
+        const SRow& row = h_rows[r];
+        if (r == 0 || row.step != h_rows[r - 1].step) ++run;
+        if (row.pidx >= 0) continue;
+        if (first_unknown < 0) first_unknown = r;
+        int32_t& c = seen[{run, std::string(t + row.id_s, t + row.id_s + row.id_len)}];
+        if (row.ridx != c) {
+          h_rows[r].code = 4;
+          h_rows[r].nf = c;
+          host_err = r;
+          break;
+        }
+        ++c;
+      }
+    }
+    if (host_err >= 0) err_r = host_err;
+    if (err_r < R && (meta_after < 0 || line_of(err_r) < meta_after)) {
+      SRow row;
+      if (host_err >= 0) row = h_rows[err_r];
+      else {
+        RS_TRY(d2h(ctx, &row, rows + err_r, sizeof row));
+        RS_TRY(sync_and_check(ctx));
+      }
+      return row_error(err_r, row);
+    }
+    if (meta_after >= 0) return parse_error(meta_after, "metadata after the column header");
+    return RS_OK;
+  }
+
+  int table() {
+    if (R == 0) return RS_OK;
+    const int32_t P = tr->count, g = tr->g;
+    const int gr = grid(R);
+    RS_LAUNCH(ctx, "trace_group_check", group_check_kernel, gr, 256, 0, rows, skey, srow, R, P, g,
+              tr->max_response_len, stat + 2);
+    RS_TRY(exclusive_scan<uint32_t>(ctx, head, epos, R, scan_part, nullptr));
+    uint32_t tail[4];
+    unsigned long long bad = 0;
+    SRow row0;
+    RS_TRY(d2h(ctx, &tail[0], run_excl + R - 1, 4));
+    RS_TRY(d2h(ctx, &tail[1], run_head + R - 1, 4));
+    RS_TRY(d2h(ctx, &tail[2], epos + R - 1, 4));
+    RS_TRY(d2h(ctx, &tail[3], head + R - 1, 4));
+    RS_TRY(d2h(ctx, &bad, stat + 2, 8));
+    RS_TRY(d2h(ctx, &row0, rows, sizeof row0));
+    RS_TRY(sync_and_check(ctx));
+    const int32_t S = (int32_t)(tail[0] + tail[1]);
+    const int64_t E = (int64_t)tail[2] + tail[3];
+    // WorkloadTrace::validate, step by step (workload.cpp:53-91)
+    auto step_err = [&](int32_t step, const std::string& what) {
+      return fail(RS_E_VALIDATION, "step " + std::to_string(step) + what);
+    };
+    if (row0.step <= -1)
+      return fail(RS_E_VALIDATION, "step indices must be strictly increasing at step " +
+                                       std::to_string(row0.step));
+    const int64_t bad_run = bad == ~0ULL ? -1 : (int64_t)(bad >> 32);
+    if (first_unknown >= 0) {
+      int64_t run = 0;
+      for (int64_t r = 1; r <= first_unknown; ++r) run += h_rows[r].step != h_rows[r - 1].step;
+      if (bad_run < 0 || run <= bad_run) {
+        const SRow& u = h_rows[first_unknown];
+        return step_err(u.step, " schedules unknown prompt '" + id_text(u) + "'");
+      }
+    }
+    if (bad_run >= 0) {
+      RS_TRY(rows_to_host());
+      std::vector<uint64_t> hk(R);
+      std::vector<uint32_t> hs(R);
+      RS_TRY(d2h(ctx, hk.data(), skey, 8ull * R));
+      RS_TRY(d2h(ctx, hs.data(), srow, 4ull * R));
+      RS_TRY(sync_and_check(ctx));
+      const int64_t lo = std::lower_bound(hk.begin(), hk.end(), (uint64_t)bad) - hk.begin();
+      const int64_t hi = std::upper_bound(hk.begin(), hk.end(), (uint64_t)bad) - hk.begin();
+      const SRow& first = h_rows[hs[lo]];
+      const int32_t pidx = (int32_t)(bad & 0xffffffffULL);
+      const std::string id(tr->ids.data() + tr->id_off[pidx], tr->ids.data() + tr->id_off[pidx + 1]);
+      if (hi - lo != g)
+        return step_err(first.step, " prompt '" + id + "' needs exactly " + std::to_string(g) +
+                                        " response lengths");
+      for (int64_t q = lo; q < hi; ++q) {
+        const int32_t l = h_rows[hs[q]].len;
+        if (l < 1 || l > tr->max_response_len)
+          return step_err(first.step, " prompt '" + id + "' response length out of range: " +
+                                          std::to_string(l));
+      }
+    }
+    // the step table, owned by the handle
+    tr->n_steps = S;
+    tr->n_entries = E;
+    if (cudaMallocAsync(&tr->d_step_idx, 4ull * S, ctx->stream) != cudaSuccess ||
+        cudaMallocAsync(&tr->d_entry_off, 4ull * (S + 1), ctx->stream) != cudaSuccess ||
+        cudaMallocAsync(&tr->d_entry_prompt, 4ull * std::max<int64_t>(E, 1), ctx->stream) != cudaSuccess ||
+        cudaMallocAsync(&tr->d_lengths, 4ull * std::max<int64_t>(E * g, 1), ctx->stream) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(RS_E_NOMEM, "trace step table allocation failed");
+    }
+    const int32_t e32 = (int32_t)E;
+    RS_TRY(h2d(ctx, tr->d_entry_off + S, &e32, 4));
+    RS_LAUNCH(ctx, "trace_step_table", step_table_kernel, gr, 256, 0, rows, run_head, run_excl, head,
+              epos, R, tr->d_step_idx, tr->d_entry_off, tr->d_entry_prompt);
+    RS_LAUNCH(ctx, "trace_step_lengths", step_lengths_kernel, gr, 256, 0, rows, srow, gstart, epos, R,
+              g, tr->d_lengths);
+    return RS_OK;
+  }
+};
 
 extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes, int device_ptr,
                                   rs_trace_csr** out) {
@@ -482,6 +1109,7 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
   if (n_bytes < 0) return fail(RS_E_ARG, "negative size");
   *out = nullptr;
   try {
+    PhaseClock clk;
     // 1. the bytes, 16-byte aligned and padded, in the context input buffer
     const size_t need = abytes(n_bytes + 64, 1);
     if (need > ctx->in_cap) {
@@ -501,6 +1129,7 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
                                   device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                                   ctx->stream));
     RS_CUDA_TRY(cudaMemsetAsync(d_text + n_bytes, 0, 64, ctx->stream));
+    clk.mark("text");
     // 2. line starts
     const int64_t nblk = std::max<int64_t>(1, (n_bytes + kChunk - 1) / kChunk);
     RS_TRY(arena_reserve(ctx, abytes(nblk, 4) * 2 + 4096));
@@ -513,6 +1142,7 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
     RS_TRY(d2h(ctx, &last[1], cnt + nblk - 1, 4));
     RS_TRY(sync_and_check(ctx));
     const int64_t L = (int64_t)last[0] + last[1] + 1;  // lines (the last may be empty)
+    clk.mark("newline count");
     AsyncBuf b_ls, b_info;
     int64_t* line_start = b_ls.alloc<int64_t>(ctx->stream, L + 1);
     LineInfo* info = b_info.alloc<LineInfo>(ctx->stream, L);
@@ -520,86 +1150,84 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
     RS_LAUNCH(ctx, "trace_nl_write", nl_write_kernel, (int)nblk, kNlT, 0, d_text, n_bytes, base,
               line_start);
     // 3. one warp per line
+    if (L >= (int64_t)UINT32_MAX - 1) return fail(RS_E_ARG, "trace has too many lines");
     const int cgrid = (int)std::min<int64_t>((L * 32 + 255) / 256, 64 * (int64_t)ctx->num_sms);
     RS_LAUNCH(ctx, "trace_classify", classify_kernel, std::max(cgrid, 1), 256, 0, d_text,
               line_start, L, n_bytes, info);
-    std::vector<LineInfo> h(L);
-    RS_TRY(d2h(ctx, h.data(), info, sizeof(LineInfo) * L));
+    // 4. the line loop's bookkeeping on the device: header, metadata, the
+    // prompt lines and the step rows compacted in line order
+    AsyncBuf b_lines;
+    const size_t lbytes = abytes(1, sizeof(LineStat)) + abytes(L, 8) * 4 + abytes(L, 4) * 3 +
+                          scan_scratch_bytes(L, 8);
+    char* lb = b_lines.alloc<char>(ctx->stream, lbytes);
+    if (!lb) return fail(RS_E_NOMEM, "trace line arrays: allocation failed");
+    auto carve = [&](size_t nb) {
+      char* q = lb;
+      lb += nb;
+      return q;
+    };
+    LineStat* d_st = (LineStat*)carve(abytes(1, sizeof(LineStat)));
+    auto* flags = (unsigned long long*)carve(abytes(L, 8));
+    auto* pos = (unsigned long long*)carve(abytes(L, 8));
+    auto* pntok = (unsigned long long*)carve(abytes(L + 1, 8));   // -> token offsets (line order)
+    auto* pidlen = (unsigned long long*)carve(abytes(L + 1, 8));  // -> id offsets
+    int32_t* d_pline = (int32_t*)carve(abytes(L, 4));
+    uint32_t* d_rline = (uint32_t*)carve(abytes(L, 4));
+    int32_t* d_pgt = (int32_t*)carve(abytes(L, 4));
+    auto* scan_part = (unsigned long long*)carve(scan_scratch_bytes(L, 8));
+    LineStat st0{};
+    st0.header = st0.first_bad = st0.meta_after = ~0u;
+    st0.g = 1;
+    st0.mp = 1024;
+    st0.mr = 2048;
+    RS_TRY(h2d(ctx, d_st, &st0, sizeof st0));
+    const int lgrid = (int)std::max<int64_t>(1, std::min<int64_t>((L + 255) / 256, 32 * (int64_t)ctx->num_sms));
+    RS_LAUNCH(ctx, "trace_line_header", line_header_kernel, lgrid, 256, 0, info, L, d_st);
+    RS_LAUNCH(ctx, "trace_line_flags", line_flags_kernel, lgrid, 256, 0, info, L, d_st, flags);
+    RS_TRY(exclusive_scan<unsigned long long>(ctx, flags, pos, L, scan_part, &d_st->counts));
+    RS_LAUNCH(ctx, "trace_line_compact", line_compact_kernel, lgrid, 256, 0, info, flags, pos, L,
+              d_pline, d_rline, pntok, pidlen, d_pgt, d_st);
+    RS_LAUNCH(ctx, "trace_line_meta", line_meta_kernel, 1, 1, 0, d_text, line_start, info, L, n_bytes,
+              d_st);
+    LineStat st;
+    RS_TRY(d2h(ctx, &st, d_st, sizeof st));
     RS_TRY(sync_and_check(ctx));
-    // 4. the metadata region, in line order (errors at the first offending line)
+    clk.mark("classify + lines");
     auto tr = new rs_trace_csr();
     std::unique_ptr<rs_trace_csr> own(tr);
-    std::vector<int32_t> pline;
-    int64_t header = -1;
-    for (int64_t ln = 0; ln < L; ++ln) {
-      const LineInfo& li = h[ln];
-      if (li.type == kEmpty) continue;
-      if (li.type == kBody) {
-        if (header < 0) header = ln;
-        continue;
-      }
-      if (header >= 0) return parse_error(ln, "metadata after the column header");
-      if (li.type == kPrompt) {
-        if (li.bad) return parse_error(ln, "malformed prompt metadata");
-        pline.push_back((int32_t)ln);
-      } else if (li.type == kG) {
-        if (li.bad) return parse_error(ln, "malformed g metadata");
-        tr->g = (int32_t)li.val;
-      } else if (li.type == kMaxPrompt) {
-        if (li.bad) return parse_error(ln, "malformed max_prompt_len metadata");
-        tr->max_prompt_len = (int32_t)li.val;
-      } else if (li.type == kMaxResponse) {
-        if (li.bad) return parse_error(ln, "malformed max_response_len metadata");
-        tr->max_response_len = (int32_t)li.val;
-      }
-    }
-    if (header < 0) return fail(RS_E_PARSE, "<trace>: missing column header");
-    {  // the header line, trimmed, compared with its spaces removed (workload.cpp:216-224)
-      int64_t ls = 0, le = 0;
-      RS_TRY(d2h(ctx, &ls, line_start + header, 8));
-      if (header + 1 < L) RS_TRY(d2h(ctx, &le, line_start + header + 1, 8));
-      RS_TRY(sync_and_check(ctx));
-      if (header + 1 >= L) le = n_bytes + 1;
-      std::string line((size_t)std::max<int64_t>(0, le - 1 - ls), '\0');
-      if (!line.empty()) RS_TRY(d2h(ctx, &line[0], d_text + ls, line.size()));
-      RS_TRY(sync_and_check(ctx));
-      std::string compact;
-      size_t a = line.find_first_not_of(" \t\r"), b = line.find_last_not_of(" \t\r");
-      for (size_t i = a; a != std::string::npos && i <= b; ++i)
-        if (line[i] != ' ') compact += line[i];
-      if (compact != "step_idx,prompt_id,response_idx,actual_len")
-        return parse_error(header, "expected column header 'step_idx,prompt_id,response_idx,actual_len'");
-    }
-    // 5. prompts in line order: token and id offsets
-    const int32_t P = (int32_t)pline.size();
+    // errors in line order: malformed metadata before the header, then the header
+    if (st.first_bad != ~0u)
+      return parse_error(st.first_bad, st.bad_type == kG ? "malformed g metadata" : "malformed prompt metadata");
+    if (st.header == ~0u) return fail(RS_E_PARSE, "<trace>: missing column header");
+    if (!st.header_ok)
+      return parse_error(st.header, "expected column header 'step_idx,prompt_id,response_idx,actual_len'");
+    tr->g = (int32_t)st.g;
+    tr->max_prompt_len = (int32_t)st.mp;
+    tr->max_response_len = (int32_t)st.mr;
+    const int64_t meta_after = st.meta_after == ~0u ? -1 : (int64_t)st.meta_after;
+    StepRows sr{ctx, tr, d_text, text, device_ptr, n_bytes, L, line_start, d_rline,
+                (int64_t)(st.counts & 0xffffffffULL)};
+    // 5. prompts in line order: token and id offsets (scans in place)
+    const int32_t P = (int32_t)(st.counts >> 32);
+    const int64_t T = (int64_t)st.n_tok, IDB = (int64_t)st.n_idb;
+    const int64_t maxid = st.maxid;
     tr->count = P;
-    std::vector<int64_t> tok_off(P + 1, 0), id_off(P + 1, 0);
-    int64_t maxid = 0;
-    for (int32_t i = 0; i < P; ++i) {
-      tok_off[i + 1] = tok_off[i] + h[pline[i]].ntok;
-      id_off[i + 1] = id_off[i] + h[pline[i]].id_len;
-      maxid = std::max<int64_t>(maxid, h[pline[i]].id_len);
-    }
-    const int64_t T = tok_off[P];
     tr->n_tokens = T;
+    RS_TRY(exclusive_scan<unsigned long long>(ctx, pntok, pntok, P, scan_part, pntok + P));
+    RS_TRY(exclusive_scan<unsigned long long>(ctx, pidlen, pidlen, P, scan_part, pidlen + P));
+    const int64_t* d_tok_off = (const int64_t*)pntok;
+    const int64_t* d_id_off = (const int64_t*)pidlen;
     // prompt-level device work: the arena, sized now (the line arrays live
     // outside it)
-    const size_t more = abytes(P, 4) + abytes(P + 1, 8) * 4 + abytes(T + 1, 4) +
-                        abytes(id_off[P] + 1, 1) + abytes(P, 4) +
+    const size_t more = abytes(T + 1, 4) + abytes(IDB + 1, 1) + abytes(P, 4) + abytes(P + 1, 8) +
                         rank_strings_device_bytes(std::max(P, 1), std::max<int64_t>(maxid, 1)) +
                         (1 << 16);
     RS_TRY(arena_reserve(ctx, more));
-    int32_t* d_pline = arena_alloc<int32_t>(ctx, std::max(P, 1));
-    int64_t* d_tok_off = arena_alloc<int64_t>(ctx, P + 1);
-    int64_t* d_id_off = arena_alloc<int64_t>(ctx, P + 1);
     int32_t* d_tok_line = arena_alloc<int32_t>(ctx, T + 1);
-    char* d_ids = arena_alloc<char>(ctx, id_off[P] + 1);
+    char* d_ids = arena_alloc<char>(ctx, IDB + 1);
     uint32_t* d_perm = arena_alloc<uint32_t>(ctx, std::max(P, 1));
     int64_t* d_sorted_off = arena_alloc<int64_t>(ctx, P + 1);
     if (P > 0) {
-      RS_TRY(h2d(ctx, d_pline, pline.data(), 4ull * P));
-      RS_TRY(h2d(ctx, d_tok_off, tok_off.data(), 8ull * (P + 1)));
-      RS_TRY(h2d(ctx, d_id_off, id_off.data(), 8ull * (P + 1)));
       const int pgrid = (int)std::min<int64_t>(((int64_t)P * 32 + kTokT - 1) / kTokT, 64 * (int64_t)ctx->num_sms);
       RS_LAUNCH(ctx, "trace_tokens", tokens_kernel, pgrid, kTokT, 0, d_text, line_start, L, n_bytes,
                 info, d_pline, P, d_tok_off, d_tok_line);
@@ -610,13 +1238,19 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
       RS_TRY(rank_strings_device(ctx, d_ids, d_id_off, P, maxid, d_perm));
     }
     std::vector<uint32_t> perm(P);
-    std::vector<char> ids_line(id_off[P]);
+    std::vector<char> ids_line(IDB);
+    std::vector<int64_t> tok_off(P + 1, 0), id_off(P + 1, 0);
+    std::vector<int32_t> gt_line(P);
     if (P > 0) {
       RS_TRY(d2h(ctx, perm.data(), d_perm, 4ull * P));
+      RS_TRY(d2h(ctx, tok_off.data(), d_tok_off, 8ull * (P + 1)));
+      RS_TRY(d2h(ctx, id_off.data(), d_id_off, 8ull * (P + 1)));
+      RS_TRY(d2h(ctx, gt_line.data(), d_pgt, 4ull * P));
       if (!ids_line.empty()) RS_TRY(d2h(ctx, ids_line.data(), d_ids, ids_line.size()));
       RS_TRY(sync_and_check(ctx));
     }
     // 7. sorted prompt table + WorkloadTrace::validate's prompt rules
+    clk.mark("tokens + id rank");
     tr->offsets.assign(P + 1, 0);
     tr->id_off.assign(P + 1, 0);
     tr->gt.resize(P);
@@ -624,13 +1258,17 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
       const uint32_t i = perm[r];
       tr->offsets[r + 1] = tr->offsets[r] + (tok_off[i + 1] - tok_off[i]);
       tr->id_off[r + 1] = tr->id_off[r] + (id_off[i + 1] - id_off[i]);
-      tr->gt[r] = (int32_t)h[pline[i]].val;
+      tr->gt[r] = gt_line[i];
     }
-    tr->ids.resize(id_off[P]);
+    tr->ids.resize(IDB);
     for (int32_t r = 0; r < P; ++r) {
       const uint32_t i = perm[r];
       std::memcpy(tr->ids.data() + tr->id_off[r], ids_line.data() + id_off[i], id_off[i + 1] - id_off[i]);
     }
+    // 8. the step rows' ParseErrors, then the validator
+    clk.mark("sorted table (host)");
+    RS_TRY(sr.parse(meta_after));
+    clk.mark("step rows parse");
     if (tr->g < 1) return fail(RS_E_VALIDATION, "responses_per_prompt must be >= 1");
     if (tr->max_prompt_len < 1 || tr->max_response_len < 1)
       return fail(RS_E_VALIDATION, "trace limits must be positive");
@@ -653,7 +1291,9 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
       if (tr->gt[r] < 1 || tr->gt[r] > tr->max_response_len)
         return fail(RS_E_VALIDATION, "prompt '" + id_of(r) + "' ground_truth_len out of range");
     }
-    // 8. the id-ordered token CSR, owned by the handle
+    RS_TRY(sr.table());
+    clk.mark("step table");
+    // 9. the id-ordered token CSR, owned by the handle
     tr->device = ctx->device;
     if (cudaMallocAsync(&tr->d_tokens, 4ull * std::max<int64_t>(T, 1), ctx->stream) != cudaSuccess ||
         cudaMallocAsync(&tr->d_offsets, 8ull * (P + 1), ctx->stream) != cudaSuccess) {
@@ -668,6 +1308,7 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
                 d_tok_off, d_perm, P, d_sorted_off, tr->d_tokens);
     }
     RS_TRY(sync_and_check(ctx));
+    clk.mark("CSR gather");
     *out = own.release();
     return RS_OK;
   } catch (const std::bad_alloc&) {
@@ -706,6 +1347,39 @@ extern "C" int rs_trace_csr_copy(rs_ctx* ctx, const rs_trace_csr* tr, int32_t* t
   if (id_bytes && !tr->ids.empty()) std::memcpy(id_bytes, tr->ids.data(), tr->ids.size());
   if (id_offsets) std::memcpy(id_offsets, tr->id_off.data(), 8ull * (tr->count + 1));
   if (ground_truth && tr->count) std::memcpy(ground_truth, tr->gt.data(), 4ull * tr->count);
+  return sync_and_check(ctx);
+}
+
+extern "C" int rs_trace_csr_steps_info(const rs_trace_csr* tr, int32_t* n_steps, int64_t* n_entries) {
+  if (!tr) return fail(RS_E_ARG, "NULL trace");
+  if (n_steps) *n_steps = tr->n_steps;
+  if (n_entries) *n_entries = tr->n_entries;
+  return RS_OK;
+}
+
+extern "C" int rs_trace_csr_steps_device(const rs_trace_csr* tr, const int32_t** step_idx,
+                                         const int32_t** entry_off, const int32_t** entry_prompt,
+                                         const int32_t** lengths) {
+  if (!tr) return fail(RS_E_ARG, "NULL trace");
+  if (step_idx) *step_idx = tr->d_step_idx;
+  if (entry_off) *entry_off = tr->d_entry_off;
+  if (entry_prompt) *entry_prompt = tr->d_entry_prompt;
+  if (lengths) *lengths = tr->d_lengths;
+  return RS_OK;
+}
+
+extern "C" int rs_trace_csr_steps_copy(rs_ctx* ctx, const rs_trace_csr* tr, int32_t* step_idx,
+                                       int32_t* entry_off, int32_t* entry_prompt, int32_t* lengths) {
+  RS_DEVICE_GUARD(ctx);
+  if (!ctx || !tr) return fail(RS_E_ARG, "NULL argument");
+  const int64_t S = tr->n_steps, E = tr->n_entries;
+  if (step_idx && S) RS_TRY(d2h(ctx, step_idx, tr->d_step_idx, 4ull * S));
+  if (entry_off) {
+    if (S) RS_TRY(d2h(ctx, entry_off, tr->d_entry_off, 4ull * (S + 1)));
+    else entry_off[0] = 0;
+  }
+  if (entry_prompt && E) RS_TRY(d2h(ctx, entry_prompt, tr->d_entry_prompt, 4ull * E));
+  if (lengths && E) RS_TRY(d2h(ctx, lengths, tr->d_lengths, 4ull * E * tr->g));
   return sync_and_check(ctx);
 }
 

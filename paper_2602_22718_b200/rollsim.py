@@ -220,6 +220,22 @@ class TraceCSR:
         return {"ids": [raw[ioff[i]:ioff[i + 1]].decode("latin-1") for i in range(self.count)],
                 "gt": gt[:self.count], "tokens": tok[:self.n_tokens], "offsets": off}
 
+    def steps(self):
+        """The step table (rs_trace_csr_steps_copy): step_idx[S], entry_off[S+1],
+        entry_prompt[E] (index into the id-sorted prompts, batch order) and
+        lengths[E, g] (actual_lengths in response order)."""
+        S, E = C.c_int32(), C.c_int64()
+        check(self._ctx.lib.rs_trace_csr_steps_info(self._h, C.byref(S), C.byref(E)))
+        S, E, g = S.value, E.value, self.responses_per_prompt
+        st = np.zeros(max(S, 1), np.int32)
+        eo = np.zeros(S + 1, np.int32)
+        ep = np.zeros(max(E, 1), np.int32)
+        ln = np.zeros(max(E * g, 1), np.int32)
+        check(self._ctx.lib.rs_trace_csr_steps_copy(self._ctx.handle, self._h, st.ctypes.data,
+                                                    eo.ctypes.data, ep.ctypes.data, ln.ctypes.data))
+        return {"step_idx": st[:S], "entry_off": eo, "entry_prompt": ep[:E],
+                "lengths": ln[:E * g].reshape(E, g)}
+
     def prefix_index(self) -> "PrefixIndex":
         t, o = self.device()
         return PrefixIndex.build_device(t, o, self.count)

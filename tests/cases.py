@@ -177,6 +177,29 @@ def trace_csv(prompts, g=1, max_prompt_len=None, max_response_len=None, steps=()
     return ("\n".join(lines) + "\n").encode()
 
 
+def steps_trace(seed, n, n_steps, g=4, max_len=48, interleave=False, max_response_len=2048):
+    """A trace with `n_steps` steps (increasing step_idx with gaps), each
+    scheduling a random subset of the prompts in a random batch order; with
+    `interleave` the rows of a step go response by response across its
+    prompts (still in response order per prompt, the reader accepts it).
+    Returns (text, prompts, steps) — the steps as trace_csv takes them."""
+    rng = np.random.RandomState(seed)
+    prompts = [(f"q{i:05d}", int(rng.randint(1, max_response_len + 1)),
+                rng.randint(0, 32000, rng.randint(1, max_len + 1)).tolist()) for i in rng.permutation(n)]
+    steps, st = [], int(rng.randint(0, 3))
+    for _ in range(n_steps):
+        pick = rng.permutation(n)[: int(rng.randint(1, n + 1))]
+        steps.append((st, [(prompts[i][0], [int(x) for x in rng.randint(1, max_response_len + 1, g)])
+                           for i in pick]))
+        st += int(rng.randint(1, 4))
+    if not interleave:
+        return trace_csv(prompts, g=g, max_prompt_len=max_len, steps=steps), prompts, steps
+    lines = trace_csv(prompts, g=g, max_prompt_len=max_len).decode().splitlines()
+    for st_i, rows in steps:
+        lines += [f"{st_i},{pid},{r},{lens[r]}" for r in range(g) for pid, lens in rows]
+    return ("\n".join(lines) + "\n").encode(), prompts, steps
+
+
 def random_trace(seed, n, max_len=64, g=2, shared=0):
     rng = np.random.RandomState(seed)
     head = rng.randint(0, 32000, shared).tolist()
@@ -188,15 +211,17 @@ def random_trace(seed, n, max_len=64, g=2, shared=0):
     return trace_csv(prompts, g=g, max_prompt_len=max_len + shared, steps=steps)
 
 
-def c2_trace_text(n_prompts=65536, shared=2048, unique=512, vocab=32000, seed=1):
+def c2_trace_text(n_prompts=65536, shared=2048, unique=512, vocab=32000, seed=1, g=8, rows=True):
     """The C2 batch (c2_tokens) as CSV trace text: '# prompt p%06d 100 '
     then the tokens as zero-padded 5-digit decimals (valid istream integers,
     vocab < 100000), so every line has the same width and numpy builds the
-    ~1 GB text directly. Returns (text uint8 array, tokens, offsets)."""
+    ~1 GB text directly; with `rows`, one step (step 0) scheduling the whole
+    batch in a seeded random order, g rows per prompt ('0,p%06d,r,%04d',
+    lengths in [1, 2048]). Returns (text uint8 array, tokens, offsets)."""
     tok, off = c2_tokens(n_prompts, shared, unique, vocab, seed)
     L = shared + unique
-    assert vocab <= 100000 and np.all(np.diff(off) == L)
-    head = np.frombuffer(b"# max_prompt_len 4096\n", np.uint8)
+    assert vocab <= 100000 and np.all(np.diff(off) == L) and g <= 10
+    head = np.frombuffer(f"# g {g}\n# max_prompt_len 4096\n".encode(), np.uint8)
     tail = np.frombuffer(b"step_idx,prompt_id,response_idx,actual_len\n", np.uint8)
     pre = 20  # '# prompt p000000 100'
     width = pre + 6 * L + 1
@@ -211,7 +236,20 @@ def c2_trace_text(n_prompts=65536, shared=2048, unique=512, vocab=32000, seed=1)
     for k in range(5):
         cols[:, :, 5 - k] = ord("0") + (t // 10 ** k) % 10
     body[:, -1] = ord("\n")
-    return np.concatenate([head, body.reshape(-1), tail]), tok, off
+    parts = [head, body.reshape(-1), tail]
+    if rows:
+        rng = np.random.RandomState(seed + 1)
+        order = np.repeat(rng.permutation(n_prompts), g)
+        lens = rng.randint(1, 2049, n_prompts * g)
+        r = np.empty((n_prompts * g, 17), np.uint8)  # '0,p000000,r,llll\n'
+        r[:] = np.frombuffer(b"0,p000000,0,0000\n", np.uint8)
+        for k in range(6):
+            r[:, 8 - k] = ord("0") + (order // 10 ** k) % 10
+        r[:, 10] = ord("0") + np.tile(np.arange(g), n_prompts)
+        for k in range(4):
+            r[:, 15 - k] = ord("0") + (lens // 10 ** k) % 10
+        parts.append(r.reshape(-1))
+    return np.concatenate(parts), tok, off
 
 
 def c2_tokens_multi(n_prompts=65536, n_sys=8, shared=2048, unique=512, vocab=32000, seed=1):

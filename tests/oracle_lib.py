@@ -205,6 +205,22 @@ class Oracle:
                 "gt": gt[:n], "tokens": tok[:nt], "offsets": off, "g": int(info[3]),
                 "max_prompt_len": int(info[4]), "max_response_len": int(info[5])}
 
+    def trace_steps(self, text: bytes):
+        """Reference only: the step table of a CSV trace (ref_trace_steps)."""
+        info = np.zeros(3, np.int64)
+        buf = C.create_string_buffer(text, len(text))
+        self._chk(self.lib.ref_trace_steps(buf, len(text), ptr(info, C.c_int64), None, None, None,
+                                           None))
+        S, E, g = (int(x) for x in info)
+        st = np.zeros(max(S, 1), np.int32)
+        eo = np.zeros(S + 1, np.int32)
+        ep = np.zeros(max(E, 1), np.int32)
+        ln = np.zeros(max(E * g, 1), np.int32)
+        self._chk(self.lib.ref_trace_steps(buf, len(text), ptr(info, C.c_int64), st.ctypes.data,
+                                           eo.ctypes.data, ep.ctypes.data, ln.ctypes.data))
+        return {"step_idx": st[:S], "entry_off": eo, "entry_prompt": ep[:E],
+                "lengths": ln[:E * g].reshape(E, g)}
+
     def sweep_arrays(self, pred, plen, S, P, prof, g, n_min, n_max, lam, gpus, threads=1):
         pred, plen = as_f64(pred), as_i32(plen)
         Cn = n_max - n_min + 1

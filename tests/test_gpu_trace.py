@@ -1,12 +1,16 @@
 """GPU parity for the trace prompt table (rs_trace_csr_parse):
 the '# prompt' metadata of CSV traces parsed on the device, against the
 reference's own reader (trace_from_string via oracle/_ref): ids, ground
-truths, tokens, limits and the error types, on generated traces, the reader's
-edge cases, and a C2-shaped trace whose device CSR feeds the dedup index."""
+truths, tokens, limits, the step table (step rows grouped on the device) and
+the errors (type, and the message for the step rules), on generated traces,
+the reader's edge cases, and a C2-shaped trace whose device CSR feeds the
+dedup index."""
+import re
+
 import numpy as np
 import pytest
 
-from cases import random_trace, trace_csv
+from cases import random_trace, steps_trace, trace_csv
 from oracle_lib import OracleError, ref
 from paper_2602_22718_b200 import rollsim as rs
 from paper_2602_22718_b200.lib import ParseError, ValidationError
@@ -49,6 +53,12 @@ def test_reader_edge_cases_match_reference():
         trace_csv([("x", 3, [1, 2]), ("y", 3, [1])], max_prompt_len=2, max_response_len=3),
         trace_csv([]),                                                          # no prompts
         trace_csv(p).replace(b"\n", b"\r"),                                     # CR only: one line
+        trace_csv([("x", 3, [1])], extra_meta=["# max_prompt_len x"]),          # num_get stores 0
+        trace_csv([("x", 3, [1])], extra_meta=["# max_prompt_len 5000000000"]), # narrowed
+        trace_csv([("x", 3, [1])], extra_meta=["# max_response_len 99999999999999999999"]),
+        trace_csv([("x", 3, [1])], extra_meta=["# max_response_len -99999999999999999999"]),
+        trace_csv([("x", 3, [1])], extra_meta=["# max_prompt_len 7x", "# max_prompt_len 9"]),
+        trace_csv([("x", 3, [1])], extra_meta=["# g 99999999999999999999"]),     # g: ParseError
     ]
     for i, text in enumerate(cases):
         try:
@@ -107,3 +117,127 @@ def test_c2_shaped_trace_to_prefix_index():
     assert all(np.array_equal(a, b) for a, b in zip(idx.tables(), direct.tables()))
     assert idx.unique_prefix_count(2048) == 1
     assert idx.unique_prefix_count(2049) == len(np.unique(arr[:, 0]))
+
+
+# ----------------------------------------------------------------- step rows
+def same_steps(text):
+    want = ref().trace_steps(text)
+    got = rs.TraceCSR(text).steps()
+    for k in ("step_idx", "entry_off", "entry_prompt", "lengths"):
+        assert np.array_equal(got[k], want[k]), k
+    return got
+
+
+def _tail(msg):
+    """The message after the reader's origin ('<string>:12: ...' -> '12: ...')."""
+    m = re.search(r":(\d+: .*)$", msg)
+    return m.group(1) if m else msg.split("] ", 1)[-1]
+
+
+def same_error(text):
+    with pytest.raises(OracleError) as e:
+        ref().trace_steps(text)
+    kind = ParseError if e.value.status == 7 else ValidationError
+    assert e.value.status in (1, 7), e.value
+    with pytest.raises(kind) as got:
+        rs.TraceCSR(text)
+    want_msg = str(e.value).split("] ", 1)[1]
+    if kind is ParseError:
+        assert _tail(str(got.value)) == _tail(want_msg)
+    else:
+        assert str(got.value) == want_msg
+
+
+def test_step_table_matches_reference():
+    for seed in range(8):
+        text, prompts, steps = steps_trace(seed, 30 + 10 * seed, 1 + seed, g=1 + seed % 5,
+                                           interleave=seed % 2 == 1)
+        got = same_steps(text)
+        assert got["step_idx"].tolist() == [st for st, _ in steps]
+
+
+def test_step_table_without_rows():
+    text = trace_csv([("a", 3, [1, 2])], g=2)
+    got = same_steps(text)
+    assert len(got["step_idx"]) == 0 and got["entry_off"].tolist() == [0]
+
+
+def test_step_row_edge_cases_match_reference():
+    p = [("b", 5, [1, 2, 3]), ("a", 9, [4])]
+    base = trace_csv(p, g=2).decode()
+    ok = [
+        base + "0,a,0,5\n0,a,1,7\n",
+        base + " 0 , a , 0 , 5 \r\n\t0,\ta,1,7\r\n",          # trimmed fields, CRLF
+        base + "+3,b,+0,1\n3,b,1,2\n\n\n4,a,0,3\n4,a,1,4\n",   # signs, blank lines
+        base + "0,a,0,5\n0,b,0,6\n0,a,1,7\n0,b,1,8\n",        # interleaved prompts
+        base + "2147483648,a,0,5\n2147483648,a,1,7\n",          # narrowed step: INT_MIN -> negative
+        base + "5,a,0,5\n5,a,1,7\n5,b,0,1\n5,b,1,1\n",
+        base + "0,a,0,5\n0,a,1,7\n1,a,0,2\n1,a,1,2\n1,b,0,3\n1,b,1,3\n",
+    ]
+    for text in ok:
+        text = text.encode()
+        try:
+            same_steps(text)
+        except OracleError:
+            same_error(text)
+
+
+def test_step_row_errors_match_reference():
+    p = [("b", 5, [1, 2, 3]), ("a", 9, [4])]
+    base = trace_csv(p, g=2).decode()
+    bad = [
+        "0,a,0\n",                                   # 3 fields
+        "0,a,0,5,6\n",                               # 5 fields
+        "x,a,0,5\n",                                 # step not an integer
+        "0,a,0,5x\n",                                # trailing characters
+        "0,a,0,\n",                                  # empty field
+        "0,a,0,99999999999999999999\n",              # out of range for long
+        "0,a,1,5\n",                                 # response_idx must start at 0
+        "0,a,0,5\n0,a,0,6\n",                        # repeated response_idx
+        "1,a,0,5\n1,a,1,5\n0,b,0,1\n",               # step decreases
+        "0,a,0,5\n0,zz,0,1\n0,zz,2,1\n",             # unknown id, out of order: ParseError
+        "0,a,0,5\n0,a,1,5\n0,zz,0,1\n0,zz,1,1\n",    # unknown id: ValidationError
+        "0,a,0,5\n",                                 # g = 2: one length missing
+        "0,a,0,5\n0,a,1,5\n0,a,2,5\n",               # three lengths
+        "0,a,0,5\n0,a,1,0\n",                        # length out of range
+        "0,a,0,5\n0,a,1,2049\n",
+        "-1,a,0,5\n-1,a,1,5\n",                      # first step must be >= 0
+        "0,b,0,1\n0,b,1,0\n0,a,0,1\n",               # two bad groups: id order decides
+        "0,a,0,5\n0,a,1,5\n1,zz,0,1\n1,zz,1,1\n1,a,0,9\n",
+        "0,a,0,5\n# g 3\n",                          # metadata after header
+        "0,a,0,5,1\n# g 3\n",                        # a bad row before it wins
+    ]
+    for rows in bad:
+        same_error((base + rows).encode())
+    # a bad prompt table outranks bad steps; a bad row outranks both
+    same_error(trace_csv([("x", 0, [1])], g=1, steps=[(0, [("x", [0])])]))
+    same_error(trace_csv([("x", 0, [1])], g=1).replace(b"actual_len\n", b"actual_len\n0,x\n"))
+
+
+def test_step_table_device_views():
+    import ctypes as C
+
+    import torch
+    from paper_2602_22718_b200.lib import check
+
+    class View:  # a raw device int32 array, for torch.as_tensor
+        def __init__(self, ptr, n):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr, False),
+                                             "version": 3}
+
+    text, _, _ = steps_trace(3, 40, 5, g=3)
+    tr = rs.TraceCSR(text)
+    host = tr.steps()
+    views = [C.c_void_p() for _ in range(4)]
+    check(tr._ctx.lib.rs_trace_csr_steps_device(tr._h, *[C.byref(v) for v in views]))
+    S, E = len(host["step_idx"]), len(host["entry_prompt"])
+    for v, n, k in zip(views, (S, S + 1, E, 3 * E), ("step_idx", "entry_off", "entry_prompt", "lengths")):
+        dev = torch.as_tensor(View(v.value, n), device="cuda").cpu().numpy()
+        assert np.array_equal(dev, host[k].reshape(-1)), k
+
+
+@pytest.mark.slow
+def test_large_step_table_matches_reference():
+    """~200k step rows (50 steps x up to 512 prompts x g = 8)."""
+    text, _, _ = steps_trace(11, 512, 50, g=8, max_len=16)
+    same_steps(text)

@@ -7,6 +7,8 @@ import time
 
 REPO = pathlib.Path(__file__).resolve().parents[1]
 sys.path[:0] = [str(REPO), str(REPO / "tests")]
+import os  # noqa: E402
+os.environ.setdefault("RS_TRACE_PHASES", "1")
 import torch  # noqa: E402
 from cases import c2_trace_text  # noqa: E402
 from paper_2602_22718_b200.lib import check, context  # noqa: E402
@@ -18,7 +20,10 @@ ctx = context(0)
 d = torch.from_numpy(text).cuda()
 h = C.c_void_p()
 names = ["trace_nl_count", "trace_nl_scan", "trace_nl_write", "trace_classify", "trace_tokens",
-         "trace_ids", "string_words", "gather_keys", "trace_gather"]
+         "trace_ids", "string_words", "gather_keys", "trace_gather", "trace_steprow", "trace_runs",
+         "trace_run_scan", "trace_group_key", "radix_hist", "radix_scan", "radix_scatter", "trace_group",
+         "trace_row_err", "trace_group_check", "trace_entry_scan", "trace_step_table",
+         "trace_step_lengths"]
 for rep in range(4):
     timing = rep == 3
     ctx.enable_kernel_timing(timing)
