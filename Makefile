@@ -61,7 +61,7 @@ SUITES    := acceptance_main test_dedup test_planner test_profile test_training
 
 .PHONY: shim
 shim: $(foreach t,$(SUITES),$(SHIM_OUT)/$(t)_b200 $(SHIM_OUT)/$(t)_ref) \
-      $(SHIM_OUT)/test_placement_b200 $(SHIM_OUT)/c5_bench_b200 $(SHIM_OUT)/c5_bench_ref \
+      $(SHIM_OUT)/test_placement_b200 $(SHIM_OUT)/test_trace_b200 $(SHIM_OUT)/c5_bench_b200 $(SHIM_OUT)/c5_bench_ref \
       $(SHIM_OUT)/c5_bench_train $(SHIM_OUT)/test_training_train \
       $(SHIM_OUT)/c3_bench_b200 $(SHIM_OUT)/c3_bench_ref
 
@@ -108,6 +108,10 @@ $(SHIM_OUT)/test_training_train: $(REF)/tests/test_training.cpp $(SHIM_OUT)/libr
 
 # drop-in extension suite (rollsim_b200.hpp) against the stock penalty path
 $(SHIM_OUT)/test_placement_b200: $(PKG)/shim/tests/test_placement_b200.cpp $(SHIM_OUT)/librollsim_b200.a $(LIB)
+	$(CXXREF) -I$(PKG)/shim -I$(PKG)/shim/doctest $< -o $@ $(SHIM_OUT)/librollsim_b200.a \
+	    -L$(PKG) -lrs_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -lpthread
+
+$(SHIM_OUT)/test_trace_b200: $(PKG)/shim/tests/test_trace_b200.cpp $(SHIM_OUT)/librollsim_b200.a $(LIB)
 	$(CXXREF) -I$(PKG)/shim -I$(PKG)/shim/doctest $< -o $@ $(SHIM_OUT)/librollsim_b200.a \
 	    -L$(PKG) -lrs_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -lpthread
 

@@ -94,6 +94,9 @@ ORACLE_API(ref_)
 ORACLE_API(orc_)
 
 /* Reference-only: the prompt table of a CSV trace via trace_from_string. */
+void ref_trace_set_format(int fmt);
+int ref_trace_convert(const char* text, int64_t n_bytes, int fmt_in, int fmt_out, char* out,
+                      int64_t cap, int64_t* out_len);
 int ref_trace_prompts(const char* text, int64_t n_bytes, int64_t* info, int32_t* tokens,
                       int64_t* offsets, char* ids, int64_t* id_offsets, int32_t* gt);
 int ref_trace_steps(const char* text, int64_t n_bytes, int64_t* info, int32_t* step_idx,

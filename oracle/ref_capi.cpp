@@ -391,7 +391,27 @@ int ref_predict_lengths(const double* obs, const int32_t* depth, const int32_t* 
   });
 }
 
-// The prompt table of a CSV trace through the reference's own reader
+// The format ref_trace_prompts / ref_trace_steps read (0 CSV, 1 JSONL).
+static rollsim::TraceFormat g_trace_format = rollsim::TraceFormat::csv;
+void ref_trace_set_format(int fmt) {
+  g_trace_format = fmt == 1 ? rollsim::TraceFormat::jsonl : rollsim::TraceFormat::csv;
+}
+
+// trace_to_string(trace_from_string(text, fmt_in), fmt_out) (workload.cpp):
+// *out_len gets the size; out (nullable) the bytes when cap allows.
+int ref_trace_convert(const char* text, int64_t n_bytes, int fmt_in, int fmt_out, char* out,
+                      int64_t cap, int64_t* out_len) {
+  return guarded([&] {
+    const auto fi = fmt_in == 1 ? rollsim::TraceFormat::jsonl : rollsim::TraceFormat::csv;
+    const auto fo = fmt_out == 1 ? rollsim::TraceFormat::jsonl : rollsim::TraceFormat::csv;
+    const std::string s =
+        rollsim::trace_to_string(rollsim::trace_from_string(std::string(text, text + n_bytes), fi), fo);
+    *out_len = (int64_t)s.size();
+    if (out && cap >= (int64_t)s.size()) std::copy(s.begin(), s.end(), out);
+  });
+}
+
+// The prompt table of a trace through the reference's own reader
 // (trace_from_string, workload.cpp:355-359): info = {count, n_tokens,
 // id_bytes, g, max_prompt_len, max_response_len}; the arrays (nullable) get
 // the id-sorted prompts.
@@ -399,7 +419,7 @@ int ref_trace_prompts(const char* text, int64_t n_bytes, int64_t* info, int32_t*
                       int64_t* offsets, char* ids, int64_t* id_offsets, int32_t* gt) {
   return guarded([&] {
     rollsim::WorkloadTrace t =
-        rollsim::trace_from_string(std::string(text, text + n_bytes), rollsim::TraceFormat::csv);
+        rollsim::trace_from_string(std::string(text, text + n_bytes), g_trace_format);
     int64_t ntok = 0, nid = 0;
     for (const auto& p : t.prompts) {
       ntok += (int64_t)p.token_ids.size();
@@ -435,7 +455,7 @@ int ref_trace_steps(const char* text, int64_t n_bytes, int64_t* info, int32_t* s
                     int32_t* entry_off, int32_t* entry_prompt, int32_t* lengths) {
   return guarded([&] {
     rollsim::WorkloadTrace t =
-        rollsim::trace_from_string(std::string(text, text + n_bytes), rollsim::TraceFormat::csv);
+        rollsim::trace_from_string(std::string(text, text + n_bytes), g_trace_format);
     int64_t e = 0;
     for (size_t s = 0; s < t.steps.size(); ++s) {
       const rollsim::StepRecord& st = t.steps[s];

@@ -112,6 +112,7 @@ PRODUCT_SIGS = {
     "rs_predict_lengths": ([vp, vp, vp, vp, i32, i32, f64, i32, P_noise, vp, vp, C.c_int, vp],
                            C.c_int),
     "rs_trace_csr_parse": ([vp, vp, i64, C.c_int, C.POINTER(vp)], C.c_int),
+    "rs_trace_csr_parse_jsonl": ([vp, vp, i64, C.c_int, C.POINTER(vp)], C.c_int),
     "rs_trace_csr_info": ([vp, P_i32, P_i64, P_i64, P_i32, P_i32, P_i32], C.c_int),
     "rs_trace_csr_device": ([vp, C.POINTER(vp), C.POINTER(vp)], C.c_int),
     "rs_trace_csr_copy": ([vp, vp, vp, vp, vp, vp, vp], C.c_int),
@@ -166,6 +167,8 @@ ORACLE_SIGS = {
 REF_ONLY_SIGS = {
     "ref_trace_prompts": ([vp, i64, P_i64, vp, vp, vp, vp, vp], C.c_int),
     "ref_trace_steps": ([vp, i64, P_i64, vp, vp, vp, vp], C.c_int),
+    "ref_trace_set_format": ([C.c_int], None),
+    "ref_trace_convert": ([vp, i64, C.c_int, C.c_int, vp, i64, P_i64], C.c_int),
 }
 
 PORT_ONLY_SIGS = {

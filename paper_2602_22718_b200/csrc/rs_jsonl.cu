@@ -1,0 +1,1400 @@
+// rs_jsonl.cu — a JSONL workload trace parsed on the device:
+// jsonl_from_string (proj/src/workload.cpp:294-352), one JSON document per
+// line read by nlohmann::json, into the same handle as the CSV reader
+// (rs_trace.cu): the id-sorted token CSR in HBM and the step table.
+//
+// Work split.
+//   1. Structural index over the whole text, 64 bytes per thread: backslash
+//      runs -> escaped characters -> unescaped quotes -> in-string masks (a
+//      scan of quote parities) -> bracket depth outside strings (a scan of
+//      depth deltas). Two lists come out: every structural character at
+//      level <= 1 (the top-level value and its direct members), and every
+//      comma at level 2 (the separators of the members' own containers).
+//      The states run across lines without a reset: a valid line ends
+//      outside strings at depth 0, so a wrong state can only follow a line
+//      that is itself an error, which is reported first.
+//   2. One thread per line walks the top-level object sequentially: keys,
+//      scalars, and each member container jumped over through the level-1
+//      list (its matching closer).
+//   3. One thread per container child (the spans between the level-2
+//      commas): each child is validated as a complete JSON value (array
+//      members) or "key": value member (object members) and the schema's
+//      fields are extracted — prompt objects, scheduled ids, length lists.
+//      A line is valid iff its skeleton and all its children are, whatever
+//      the split, so the reader accepts exactly what nlohmann accepts (up to
+//      the constructs listed below).
+//   4. Prompts: counts -> scans -> writes -> the shared id-order tail
+//      (rs_trace.cuh). Steps: the extracted records go to the host, which
+//      applies std::map / scheduled-list semantics and WorkloadTrace::validate
+//      (workload.cpp:53-91), and the step table is uploaded.
+//
+// nlohmann semantics kept: whitespace (space, \t, \n, \r); strings with every
+// escape, \u surrogate pairs, UTF-8 validation and no raw control
+// characters; number grammar; duplicate keys (the last wins); get<int> from
+// integers (int64 / uint64 truncation), booleans and floats (truncation,
+// INT_MIN out of range); "prompts": null; "lengths": null; "scheduled"
+// absent (the lengths keys in map order).
+// Rejected as RS_E_PARSE "unsupported" although nlohmann reads them:
+// "prompts" given as an object, "lengths" given as an array, nesting deeper
+// than 256, and floats converted to int that lie within 1e-6 below an
+// integer (where the double rounding decides the result) or have more than
+// 18 significant digits or an exponent beyond +-60.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "rs_sort.cuh"
+#include "rs_trace.cuh"
+
+namespace rs {
+namespace {
+
+constexpr int kJErr = 1;     // a ParseError of the reference reader
+constexpr int kJUnsup = 2;   // valid for nlohmann, not read here
+
+// ------------------------------------------------------------ stage 1 ----
+// 64-byte words: bitmasks of one character class, bit j = byte 64 w + j.
+__device__ __forceinline__ void word_masks(const unsigned char* t, int64_t w, int64_t n,
+                                           uint64_t* bs, uint64_t* q, uint64_t* op, uint64_t* cl,
+                                           uint64_t* cm, uint64_t* co) {
+  const uint4* p = reinterpret_cast<const uint4*>(t + 64 * w);
+  uint64_t mbs = 0, mq = 0, mop = 0, mcl = 0, mcm = 0, mco = 0;
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const uint4 x = p[v];
+    const uint32_t wd[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int j = 16 * v + 4 * k + b;
+        const unsigned c = (wd[k] >> (8 * b)) & 0xffu;
+        const uint64_t bit = 64 * w + j < n ? 1ULL << j : 0ULL;
+        mbs |= c == '\\' ? bit : 0;
+        mq |= c == '"' ? bit : 0;
+        mop |= (c == '{' || c == '[') ? bit : 0;
+        mcl |= (c == '}' || c == ']') ? bit : 0;
+        mcm |= c == ',' ? bit : 0;
+        mco |= c == ':' ? bit : 0;
+      }
+  }
+  *bs = mbs;
+  *q = mq;
+  *op = mop;
+  *cl = mcl;
+  *cm = mcm;
+  *co = mco;
+}
+
+// Escaped characters of a word given the parity of the backslash run that
+// ends right before it: a character is escaped iff an odd run precedes it.
+// Runs are rare, so the loop walks runs, not bytes.
+__device__ __forceinline__ uint64_t escaped_of(uint64_t bs, int carry) {
+  if (bs == ~0ULL) return 0;  // a word of backslashes: its run goes on into the next word
+  uint64_t esc = (carry && !(bs & 1ULL)) ? 1ULL : 0ULL;
+  uint64_t m = bs;
+  while (m) {
+    const int s = __ffsll((long long)m) - 1;   // run start
+    const int len = __ffsll((long long)~(m >> s)) - 1;
+    const int e = s + len;                      // the character after the run
+    if (e < 64 && ((len + (s == 0 ? carry : 0)) & 1)) esc |= 1ULL << e;
+    m = e >= 64 ? 0ULL : m & (~0ULL << e);
+  }
+  return esc;
+}
+
+__device__ __forceinline__ uint64_t prefix_xor(uint64_t x) {
+  x ^= x << 1;
+  x ^= x << 2;
+  x ^= x << 4;
+  x ^= x << 8;
+  x ^= x << 16;
+  x ^= x << 32;
+  return x;
+}
+
+// Word state: trailing backslash run parity, all-backslash flag.
+__global__ void js_bs_kernel(const char* text, int64_t n, int64_t W, uint8_t* tail) {
+  const unsigned char* t = reinterpret_cast<const unsigned char*>(text);
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t bs, q, op, cl, cm, co;
+    word_masks(t, w, n, &bs, &q, &op, &cl, &cm, &co);
+    const int lead = __clzll((long long)~bs);  // backslashes at the top of the word
+    tail[w] = (uint8_t)((bs == ~0ULL ? 2 : 0) | (lead & 1));
+  }
+}
+
+// The run parity before word w (words of 64 backslashes pass it through).
+__device__ __forceinline__ int esc_carry(const uint8_t* tail, int64_t w) {
+  int64_t v = w - 1;
+  while (v >= 0 && (tail[v] & 2)) --v;
+  return v >= 0 ? (tail[v] & 1) : 0;
+}
+
+// Unescaped quotes per word (their parity, for the in-string scan).
+__global__ void js_quote_kernel(const char* text, int64_t n, int64_t W, const uint8_t* tail,
+                                uint32_t* qpar) {
+  const unsigned char* t = reinterpret_cast<const unsigned char*>(text);
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t bs, q, op, cl, cm, co;
+    word_masks(t, w, n, &bs, &q, &op, &cl, &cm, &co);
+    const uint64_t uq = q & ~escaped_of(bs, esc_carry(tail, w));
+    qpar[w] = __popcll((long long)uq) & 1;
+  }
+}
+
+// Structural characters outside strings; depth delta per word.
+__device__ __forceinline__ void outside(const unsigned char* t, int64_t n, int64_t w, const uint8_t* tail,
+                                        const uint32_t* qscan, uint64_t* op, uint64_t* cl, uint64_t* cm,
+                                        uint64_t* co) {
+  uint64_t bs, q;
+  word_masks(t, w, n, &bs, &q, op, cl, cm, co);
+  const uint64_t uq = q & ~escaped_of(bs, esc_carry(tail, w));
+  uint64_t ins = prefix_xor(uq);  // 1 from an opening quote up to (not incl.) its closing one
+  if (qscan[w] & 1) ins = ~ins;
+  const uint64_t out = ~ins & ~uq;
+  *op &= out;
+  *cl &= out;
+  *cm &= out;
+  *co &= out;
+}
+
+__global__ void js_depth_kernel(const char* text, int64_t n, int64_t W, const uint8_t* tail,
+                                const uint32_t* qscan, unsigned long long* dd) {
+  const unsigned char* t = reinterpret_cast<const unsigned char*>(text);
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t op, cl, cm, co;
+    outside(t, n, w, tail, qscan, &op, &cl, &cm, &co);
+    dd[w] = (unsigned long long)(long long)(__popcll((long long)op) - __popcll((long long)cl));
+  }
+}
+
+// Tokens at level <= 1 (list A) and commas at level 2 (list B): counted
+// (write = false) or written at their scanned offsets. Level: an opener's
+// depth before it, a closer's depth after it, a comma's / colon's depth.
+template <bool kWrite>
+__global__ void js_tokens_kernel(const char* text, int64_t n, int64_t W, const uint8_t* tail,
+                                 const uint32_t* qscan, const unsigned long long* dscan,
+                                 uint32_t* ca, uint32_t* cb, const uint32_t* oa, const uint32_t* ob,
+                                 uint64_t* la, int64_t* lb) {
+  const unsigned char* t = reinterpret_cast<const unsigned char*>(text);
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t op, cl, cm, co;
+    outside(t, n, w, tail, qscan, &op, &cl, &cm, &co);
+    long long d = (long long)dscan[w];
+    uint64_t all = op | cl | cm | co;
+    uint32_t na = 0, nb = 0;
+    const uint32_t a0 = kWrite ? oa[w] : 0, b0 = kWrite ? ob[w] : 0;
+    while (all) {
+      const int j = __ffsll((long long)all) - 1;
+      all &= all - 1;
+      const uint64_t bit = 1ULL << j;
+      long long lev;
+      if (op & bit) {
+        lev = d;
+        ++d;
+      } else if (cl & bit) {
+        --d;
+        lev = d;
+      } else {
+        lev = d;
+      }
+      const int64_t pos = 64 * w + j;
+      if (lev >= 0 && lev <= 1) {
+        if (kWrite) la[a0 + na] = ((uint64_t)pos << 8) | t[pos];
+        ++na;
+      } else if (lev == 2 && (cm & bit)) {
+        if (kWrite) lb[b0 + nb] = pos;
+        ++nb;
+      }
+    }
+    if (!kWrite) {
+      ca[w] = na;
+      cb[w] = nb;
+    }
+  }
+}
+
+// ------------------------------------------------------ JSON scanning ----
+struct JIn {
+  const unsigned char* t;
+  int64_t p, e;
+};
+
+__device__ __forceinline__ bool jws(unsigned char c) {
+  return c == ' ' || c == '\t' || c == '\n' || c == '\r';
+}
+__device__ __forceinline__ void skip_ws(JIn& in) {
+  while (in.p < in.e && jws(in.t[in.p])) ++in.p;
+}
+__device__ __forceinline__ int hexv(unsigned char c) {
+  if (c >= '0' && c <= '9') return c - '0';
+  if (c >= 'a' && c <= 'f') return c - 'a' + 10;
+  if (c >= 'A' && c <= 'F') return c - 'A' + 10;
+  return -1;
+}
+
+// A string at in.p (the opening quote): validated like nlohmann's lexer;
+// *len = its unescaped bytes, written to out (nullable, out_cap bytes kept).
+// Returns 0 or kJErr.
+__device__ int jstring(JIn& in, char* out, int64_t out_cap, int64_t* len) {
+  const unsigned char* t = in.t;
+  int64_t p = in.p + 1, k = 0;
+  auto put = [&](unsigned c) {
+    if (out && k < out_cap) out[k] = (char)c;
+    ++k;
+  };
+  for (;;) {
+    if (p >= in.e) return kJErr;
+    const unsigned c = t[p];
+    if (c == '"') {
+      ++p;
+      break;
+    }
+    if (c < 0x20) return kJErr;
+    if (c == '\\') {
+      if (p + 1 >= in.e) return kJErr;
+      const unsigned x = t[p + 1];
+      p += 2;
+      switch (x) {
+        case '"': put('"'); break;
+        case '\\': put('\\'); break;
+        case '/': put('/'); break;
+        case 'b': put('\b'); break;
+        case 'f': put('\f'); break;
+        case 'n': put('\n'); break;
+        case 'r': put('\r'); break;
+        case 't': put('\t'); break;
+        case 'u': {
+          auto hex4 = [&](int64_t at, unsigned* v) {
+            if (at + 4 > in.e) return false;
+            unsigned r = 0;
+            for (int i = 0; i < 4; ++i) {
+              const int h = hexv(t[at + i]);
+              if (h < 0) return false;
+              r = r * 16 + (unsigned)h;
+            }
+            *v = r;
+            return true;
+          };
+          unsigned cp;
+          if (!hex4(p, &cp)) return kJErr;
+          p += 4;
+          if (cp >= 0xD800 && cp <= 0xDBFF) {
+            unsigned lo;
+            if (p + 2 > in.e || t[p] != '\\' || t[p + 1] != 'u' || !hex4(p + 2, &lo) ||
+                lo < 0xDC00 || lo > 0xDFFF)
+              return kJErr;
+            p += 6;
+            cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
+          } else if (cp >= 0xDC00 && cp <= 0xDFFF) {
+            return kJErr;
+          }
+          if (cp < 0x80) {
+            put(cp);
+          } else if (cp < 0x800) {
+            put(0xC0 | (cp >> 6));
+            put(0x80 | (cp & 0x3F));
+          } else if (cp < 0x10000) {
+            put(0xE0 | (cp >> 12));
+            put(0x80 | ((cp >> 6) & 0x3F));
+            put(0x80 | (cp & 0x3F));
+          } else {
+            put(0xF0 | (cp >> 18));
+            put(0x80 | ((cp >> 12) & 0x3F));
+            put(0x80 | ((cp >> 6) & 0x3F));
+            put(0x80 | (cp & 0x3F));
+          }
+          break;
+        }
+        default:
+          return kJErr;
+      }
+      continue;
+    }
+    if (c < 0x80) {
+      put(c);
+      ++p;
+      continue;
+    }
+    // UTF-8 (RFC 3629, as nlohmann's lexer checks it)
+    int need;
+    unsigned lo = 0x80, hi = 0xBF;
+    if (c >= 0xC2 && c <= 0xDF) need = 1;
+    else if (c == 0xE0) { need = 2; lo = 0xA0; }
+    else if ((c >= 0xE1 && c <= 0xEC) || c == 0xEE || c == 0xEF) need = 2;
+    else if (c == 0xED) { need = 2; hi = 0x9F; }
+    else if (c == 0xF0) { need = 3; lo = 0x90; }
+    else if (c >= 0xF1 && c <= 0xF3) need = 3;
+    else if (c == 0xF4) { need = 3; hi = 0x8F; }
+    else return kJErr;
+    if (p + need >= in.e) return kJErr;
+    put(c);
+    for (int i = 1; i <= need; ++i) {
+      const unsigned d = t[p + i];
+      const unsigned l = i == 1 ? lo : 0x80, h = i == 1 ? hi : 0xBF;
+      if (d < l || d > h) return kJErr;
+      put(d);
+    }
+    p += need + 1;
+  }
+  in.p = p;
+  *len = k;
+  return 0;
+}
+
+// A number at in.p: the JSON grammar, and its value as nlohmann's get<int>
+// gives it (*v). Returns 0, kJErr (grammar) or kJUnsup.
+__device__ int jnumber(JIn& in, int32_t* v) {
+  const unsigned char* t = in.t;
+  int64_t p = in.p;
+  const bool neg = p < in.e && t[p] == '-';
+  if (neg) ++p;
+  if (p >= in.e || t[p] < '0' || t[p] > '9') return kJErr;
+  const int64_t i0 = p;
+  if (t[p] == '0') ++p;
+  else
+    while (p < in.e && t[p] >= '0' && t[p] <= '9') ++p;
+  const int64_t i1 = p;
+  int64_t f0 = p, f1 = p;
+  bool is_float = false;
+  if (p < in.e && t[p] == '.') {
+    ++p;
+    f0 = p;
+    if (p >= in.e || t[p] < '0' || t[p] > '9') return kJErr;
+    while (p < in.e && t[p] >= '0' && t[p] <= '9') ++p;
+    f1 = p;
+    is_float = true;
+  }
+  long long ex = 0;
+  if (p < in.e && (t[p] == 'e' || t[p] == 'E')) {
+    ++p;
+    bool eneg = false;
+    if (p < in.e && (t[p] == '+' || t[p] == '-')) {
+      eneg = t[p] == '-';
+      ++p;
+    }
+    if (p >= in.e || t[p] < '0' || t[p] > '9') return kJErr;
+    while (p < in.e && t[p] >= '0' && t[p] <= '9') {
+      if (ex < 100000) ex = ex * 10 + (t[p] - '0');
+      ++p;
+    }
+    if (eneg) ex = -ex;
+    is_float = true;
+  }
+  in.p = p;
+  if (!is_float) {
+    unsigned long long m = 0;
+    bool over = false;
+    for (int64_t i = i0; i < i1; ++i) {
+      const unsigned d = t[i] - '0';
+      if (m > (0xFFFFFFFFFFFFFFFFULL - d) / 10) over = true;
+      else m = m * 10 + d;
+    }
+    if (neg) {
+      if (over || m > 0x8000000000000000ULL) *v = INT32_MIN;  // a float far out of range
+      else *v = (int32_t)(long long)(0ULL - m);                // int64, narrowed
+    } else {
+      *v = over ? INT32_MIN : (int32_t)m;                       // int64 / uint64, narrowed
+    }
+    return 0;
+  }
+  // a float: the truncation of the nearest double. value = m * 10^e10 with
+  // m the first 18 significant digits (sticky: a nonzero digit dropped)
+  unsigned long long m = 0;
+  int digits = 0;
+  long long e10 = ex;
+  bool sticky = false;
+  auto digit = [&](unsigned d, bool frac) {
+    if (m == 0 && d == 0) {
+      if (frac) --e10;
+      return;
+    }
+    if (digits < 18) {
+      m = m * 10 + d;
+      ++digits;
+      if (frac) --e10;
+    } else {
+      sticky |= d != 0;
+      if (!frac) ++e10;
+    }
+  };
+  for (int64_t i = i0; i < i1; ++i) digit(t[i] - '0', false);
+  for (int64_t i = f0; i < f1; ++i) digit(t[i] - '0', true);
+  if (m == 0) {
+    *v = 0;
+    return 0;
+  }
+  if (e10 > 60 || e10 < -60) return kJUnsup;
+  if (e10 >= 0) {  // an integer (sticky digits only below it): its range decides
+    unsigned long long x = m;
+    bool big = false;
+    for (long long i = 0; i < e10 && !big; ++i) {
+      if (x > 3000000000ULL) big = true;
+      else x *= 10;
+    }
+    if (big || (neg ? x > 2147483648ULL : x >= 2147483648ULL)) *v = INT32_MIN;
+    else *v = neg ? (int32_t)(0 - (long long)x) : (int32_t)x;
+    return 0;
+  }
+  const long long k = -e10;
+  if (k >= 19) {  // |value| < 0.1
+    *v = 0;
+    return 0;
+  }
+  unsigned long long pw = 1;
+  for (long long i = 0; i < k; ++i) pw *= 10;
+  const unsigned long long ip = m / pw, fr = m % pw;
+  // within 1e-6 below the next integer the double rounding decides
+  if ((double)(pw - fr) <= 1e-6 * (double)pw || (sticky && fr == pw - 1)) return kJUnsup;
+  if (neg ? ip > 2147483648ULL : ip >= 2147483648ULL) *v = INT32_MIN;
+  else *v = neg ? (int32_t)(0 - (long long)ip) : (int32_t)ip;
+  return 0;
+}
+
+__device__ __forceinline__ bool jlit(JIn& in, const char* w, int n) {
+  if (in.p + n > in.e) return false;
+  for (int i = 0; i < n; ++i)
+    if (in.t[in.p + i] != (unsigned char)w[i]) return false;
+  in.p += n;
+  return true;
+}
+
+// Any JSON value at in.p (after whitespace): validated, skipped. An explicit
+// 256-level stack (bit = object).
+__device__ int jskip(JIn& in) {
+  uint64_t stk[4] = {0, 0, 0, 0};
+  int depth = 0;
+  enum { kValue, kAfter } st = kValue;
+  for (;;) {
+    skip_ws(in);
+    if (st == kValue) {
+      if (in.p >= in.e) return kJErr;
+      const unsigned char c = in.t[in.p];
+      if (c == '{' || c == '[') {
+        if (depth >= 256) return kJUnsup;
+        const bool obj = c == '{';
+        if (obj) stk[depth >> 6] |= 1ULL << (depth & 63);
+        else stk[depth >> 6] &= ~(1ULL << (depth & 63));
+        ++depth;
+        ++in.p;
+        skip_ws(in);
+        if (in.p < in.e && in.t[in.p] == (obj ? '}' : ']')) {
+          ++in.p;
+          --depth;
+          st = kAfter;
+          continue;
+        }
+        if (obj) {  // first key
+          int64_t l;
+          if (in.p >= in.e || in.t[in.p] != '"' || jstring(in, nullptr, 0, &l)) return kJErr;
+          skip_ws(in);
+          if (in.p >= in.e || in.t[in.p] != ':') return kJErr;
+          ++in.p;
+        }
+        continue;  // a value
+      }
+      if (c == '"') {
+        int64_t l;
+        if (jstring(in, nullptr, 0, &l)) return kJErr;
+      } else if (c == '-' || (c >= '0' && c <= '9')) {
+        int32_t v;
+        const int r = jnumber(in, &v);
+        if (r == kJErr) return kJErr;  // a float outside the int conversion is still a number
+      } else if (!(jlit(in, "true", 4) || jlit(in, "false", 5) || jlit(in, "null", 4))) {
+        return kJErr;
+      }
+      st = kAfter;
+      continue;
+    }
+    // after a value
+    if (depth == 0) return 0;
+    const bool obj = (stk[(depth - 1) >> 6] >> ((depth - 1) & 63)) & 1;
+    if (in.p >= in.e) return kJErr;
+    const unsigned char c = in.t[in.p];
+    if (c == ',') {
+      ++in.p;
+      if (obj) {
+        skip_ws(in);
+        int64_t l;
+        if (in.p >= in.e || in.t[in.p] != '"' || jstring(in, nullptr, 0, &l)) return kJErr;
+        skip_ws(in);
+        if (in.p >= in.e || in.t[in.p] != ':') return kJErr;
+        ++in.p;
+      }
+      st = kValue;
+    } else if (c == (obj ? '}' : ']')) {
+      ++in.p;
+      --depth;
+    } else {
+      return kJErr;
+    }
+  }
+}
+
+// get<int> of the value at in.p: numbers and booleans; kJErr for the rest.
+__device__ int jint(JIn& in, int32_t* v) {
+  skip_ws(in);
+  if (in.p >= in.e) return kJErr;
+  const unsigned char c = in.t[in.p];
+  if (c == '-' || (c >= '0' && c <= '9')) return jnumber(in, v);
+  if (jlit(in, "true", 4)) {
+    *v = 1;
+    return 0;
+  }
+  if (jlit(in, "false", 5)) {
+    *v = 0;
+    return 0;
+  }
+  return kJErr;  // a string / null / container: type_error (or a syntax error)
+}
+
+// get<std::vector<int>> of the value at in.p: count, and write when out.
+__device__ int jint_array(JIn& in, int32_t* out, int64_t* count) {
+  skip_ws(in);
+  if (in.p >= in.e || in.t[in.p] != '[') return kJErr;
+  ++in.p;
+  int64_t k = 0;
+  skip_ws(in);
+  if (in.p < in.e && in.t[in.p] == ']') {
+    ++in.p;
+    *count = 0;
+    return 0;
+  }
+  for (;;) {
+    int32_t v;
+    const int r = jint(in, &v);
+    if (r) return r;
+    if (out) out[k] = v;
+    ++k;
+    skip_ws(in);
+    if (in.p >= in.e) return kJErr;
+    if (in.t[in.p] == ',') {
+      ++in.p;
+      continue;
+    }
+    if (in.t[in.p] == ']') {
+      ++in.p;
+      break;
+    }
+    return kJErr;
+  }
+  *count = k;
+  return 0;
+}
+
+// A key at in.p (the opening quote), matched against the schema's names:
+// returns the index in names (or -1), after the ':' and its whitespace.
+__device__ int jkey(JIn& in, const char* const* names, int nn, int* err) {
+  char buf[24];
+  int64_t len;
+  if (in.p >= in.e || in.t[in.p] != '"' || jstring(in, buf, sizeof buf, &len)) {
+    *err = kJErr;
+    return -1;
+  }
+  skip_ws(in);
+  if (in.p >= in.e || in.t[in.p] != ':') {
+    *err = kJErr;
+    return -1;
+  }
+  ++in.p;
+  skip_ws(in);
+  for (int i = 0; i < nn; ++i) {
+    int l = 0;
+    while (names[i][l]) ++l;
+    if (l != len) continue;
+    bool eq = true;
+    for (int j = 0; j < l; ++j) eq &= buf[j] == names[i][j];
+    if (eq) return i;
+  }
+  return -1;
+}
+
+// ------------------------------------------------------- stage 2: lines --
+enum LineKind : int32_t { kLEmpty = 0, kLHeader, kLStep };
+enum Role : int32_t { kRValidate = 0, kRPrompts, kRSched, kRLengths };
+
+struct JLine {
+  int32_t kind, err;
+  int32_t g, mp, mr;  // header values
+  int32_t step;       // step line: "step"
+  int32_t has_sched;
+  int32_t prompts_null;  // header: "prompts": null
+  int32_t lengths_null;  // step: "lengths": null
+};
+
+struct JCont {
+  int64_t open, close;  // the container's brackets
+  int32_t line, role, is_obj, pad;
+};
+
+__device__ __forceinline__ int64_t lower_a(const uint64_t* a, int64_t n, int64_t pos) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)(a[mid] >> 8) < pos) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void js_first_line_kernel(const char* text, const int64_t* line_start, int64_t L, int64_t n,
+                                     unsigned int* first) {
+  const unsigned char* t = reinterpret_cast<const unsigned char*>(text);
+  for (int64_t ln = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ln < L;
+       ln += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s = line_start[ln], e = ln + 1 < L ? line_start[ln + 1] - 1 : n;
+    bool any = false;
+    for (int64_t i = s; i < e && !any; ++i) any = !(t[i] == ' ' || t[i] == '\t' || t[i] == '\r');
+    if (any) atomicMin(first, (unsigned int)ln);
+  }
+}
+
+// One thread per line: the top-level object, member containers jumped over
+// (their closer: the next level-1 token). Containers go to a list (count
+// via atomicAdd; cont_cap entries at most).
+__global__ void js_line_kernel(const char* text, const int64_t* line_start, int64_t L, int64_t n,
+                               const unsigned int* first, const uint64_t* la, int64_t na,
+                               JLine* lines, JCont* conts, unsigned int* ncont, int64_t cont_cap) {
+  const unsigned char* t = reinterpret_cast<const unsigned char*>(text);
+  for (int64_t ln = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ln < L;
+       ln += (int64_t)gridDim.x * blockDim.x) {
+    JLine out{};
+    out.g = 0;
+    out.mp = 1024;
+    out.mr = 2048;
+    int64_t s = line_start[ln], e = ln + 1 < L ? line_start[ln + 1] - 1 : n;
+    while (s < e && (t[s] == ' ' || t[s] == '\t' || t[s] == '\r')) ++s;
+    while (e > s && (t[e - 1] == ' ' || t[e - 1] == '\t' || t[e - 1] == '\r')) --e;
+    if (s == e || ln < (int64_t)*first) {
+      lines[ln] = out;
+      continue;
+    }
+    const bool header = ln == (int64_t)*first;
+    out.kind = header ? kLHeader : kLStep;
+    JIn in{t, s, e};
+    int err = 0;
+    // members seen (last wins): type ok?, g, max_*, prompts / step, scheduled, lengths
+    bool has_type = false, type_ok = false, has_g = false, has_prompts = false, has_step = false,
+         has_lengths = false;
+    int last_role_cont[4] = {-1, -1, -1, -1};  // container index per role (prompts / sched / lengths)
+    auto demote = [&](int role) {  // an earlier container of a repeated key: validate only
+      if (last_role_cont[role] >= 0) conts[last_role_cont[role]].role = kRValidate;
+      last_role_cont[role] = -1;
+    };
+    auto add_cont = [&](int64_t open, int role) -> int64_t {  // jump to the matching closer
+      const int64_t i = lower_a(la, na, open);
+      if (i + 1 >= na || (int64_t)(la[i] >> 8) != open) return -1;
+      const uint64_t c = la[i + 1];
+      const unsigned char oc = t[open], cc = (unsigned char)(c & 0xff);
+      if (!((oc == '{' && cc == '}') || (oc == '[' && cc == ']'))) return -1;
+      const int64_t close = (int64_t)(c >> 8);
+      const unsigned int k = atomicAdd(ncont, 1u);
+      if ((int64_t)k < cont_cap) {
+        JCont jc{open, close, (int32_t)ln, role, oc == '{' ? 1 : 0, 0};
+        conts[k] = jc;
+        if (role != kRValidate) last_role_cont[role] = (int)k;
+      }
+      return close + 1;
+    };
+    skip_ws(in);
+    if (in.p >= in.e || t[in.p] != '{') {
+      err = kJErr;  // contains("type") / at("step") need an object
+    } else {
+      ++in.p;
+      skip_ws(in);
+      bool first_m = true;
+      while (!err) {
+        if (in.p < in.e && t[in.p] == '}' && first_m) {
+          ++in.p;
+          break;
+        }
+        static const char* const kHdr[] = {"type", "g", "max_prompt_len", "max_response_len", "prompts"};
+        static const char* const kStp[] = {"step", "scheduled", "lengths"};
+        const int key = header ? jkey(in, kHdr, 5, &err) : jkey(in, kStp, 3, &err);
+        if (err) break;
+        const unsigned char c = in.p < in.e ? t[in.p] : 0;
+        const bool cont = c == '{' || c == '[';
+        int role = kRValidate;
+        if (header && key == 4) role = kRPrompts;
+        if (!header && key == 1) role = kRSched;
+        if (!header && key == 2) role = kRLengths;
+        if (role != kRValidate) demote(role);
+        if (cont) {
+          int r2 = role;
+          if (role == kRPrompts && c == '{') r2 = -kJUnsup;   // "prompts" as an object
+          if (role == kRLengths && c == '[') r2 = -kJUnsup;   // "lengths" as an array
+          if (role == kRSched && c == '{') r2 = -kJErr;       // get<vector<string>> of an object
+          const int64_t np = add_cont(in.p, r2 < 0 ? kRValidate : r2);
+          if (np < 0) {
+            err = kJErr;
+            break;
+          }
+          if (r2 < 0) err = -r2;
+          in.p = np;
+          if (header && key == 4) has_prompts = true;
+          if (!header && key == 2) has_lengths = true;
+          if (!header && key == 1) out.has_sched = 1;
+          if (header && key == 0) type_ok = false, has_type = true;
+          if ((header && (key == 1 || key == 2 || key == 3)) || (!header && key == 0)) err = kJErr;
+        } else {
+          // a scalar member
+          if (header && key == 0) {
+            has_type = true;
+            type_ok = false;
+            if (c == '"') {
+              char buf[8];
+              int64_t l;
+              JIn tmp = in;
+              if (jstring(tmp, buf, sizeof buf, &l)) err = kJErr;
+              else type_ok = l == 6 && buf[0] == 'h' && buf[1] == 'e' && buf[2] == 'a' && buf[3] == 'd' &&
+                             buf[4] == 'e' && buf[5] == 'r';
+            }
+            if (!err) err = jskip(in);
+          } else if ((header && key >= 1 && key <= 3) || (!header && key == 0)) {
+            int32_t v = 0;
+            err = jint(in, &v);
+            if (!err) {
+              if (header && key == 1) {
+                out.g = v;
+                has_g = true;
+              } else if (header && key == 2) {
+                out.mp = v;
+              } else if (header && key == 3) {
+                out.mr = v;
+              } else {
+                out.step = v;
+                has_step = true;
+              }
+            }
+          } else if (role == kRPrompts || role == kRLengths || role == kRSched) {
+            // null: no items / prompts; "scheduled": null is a type_error;
+            // other scalars: a type_error on the first element
+            if (jlit(in, "null", 4)) {
+              if (role == kRSched) err = kJErr;
+              if (role == kRPrompts) {
+                has_prompts = true;
+                out.prompts_null = 1;
+              }
+              if (role == kRLengths) {
+                has_lengths = true;
+                out.lengths_null = 1;
+              }
+            } else {
+              err = jskip(in);
+              if (!err) err = kJErr;
+            }
+          } else {
+            err = jskip(in);
+          }
+        }
+        if (err) break;
+        skip_ws(in);
+        first_m = false;
+        if (in.p < in.e && t[in.p] == ',') {
+          ++in.p;
+          skip_ws(in);
+          continue;
+        }
+        if (in.p < in.e && t[in.p] == '}') {
+          ++in.p;
+          break;
+        }
+        err = kJErr;
+      }
+      if (!err) {
+        skip_ws(in);
+        if (in.p != in.e) err = kJErr;  // trailing content
+      }
+      if (!err && header && !(has_type && type_ok)) err = kJErr;  // "first line must be the header object"
+      if (!err && header && (!has_g || !has_prompts)) err = kJErr;  // at("g") / at("prompts")
+      if (!err && !header && (!has_step || !has_lengths)) err = kJErr;  // at("step") / at("lengths")
+    }
+    if (header) out.prompts_null = out.prompts_null && last_role_cont[kRPrompts] < 0;
+    else out.lengths_null = out.lengths_null && last_role_cont[kRLengths] < 0;
+    out.err = err;
+    lines[ln] = out;
+  }
+}
+
+// ----------------------------------------------------- stage 3: children --
+// Children of container ci: the spans between its level-2 commas.
+__device__ __forceinline__ int64_t lower_b(const int64_t* b, int64_t n, int64_t pos) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (b[mid] < pos) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void js_child_count_kernel(const char* text, const JCont* conts, int64_t nc, const int64_t* lb,
+                                      int64_t nb, unsigned long long* nchild) {
+  const unsigned char* t = reinterpret_cast<const unsigned char*>(text);
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const JCont jc = conts[c];
+    const int64_t b0 = lower_b(lb, nb, jc.open), b1 = lower_b(lb, nb, jc.close);
+    int64_t k = b1 - b0 + 1;
+    if (b1 == b0) {  // no separator: empty if only whitespace inside
+      bool any = false;
+      for (int64_t i = jc.open + 1; i < jc.close && !any; ++i) any = !jws(t[i]);
+      if (!any) k = 0;
+    }
+    nchild[c] = (unsigned long long)k;
+  }
+}
+
+struct JChild {   // pass-1 results of one child
+  int64_t a, e;        // span
+  int64_t id_len;      // prompt id / scheduled id / lengths key: unescaped bytes
+  int64_t n_int;       // prompt tokens / length values
+  int64_t id_at, ints_at;  // where the id string and the int array start (pass 2)
+  int32_t gt, err;
+  int32_t cont, line;
+};
+
+// Pass 1 (write = false): validate, measure. Pass 2: write ids and ints at
+// their scanned offsets.
+template <bool kWrite>
+__global__ void js_child_kernel(const char* text, const JCont* conts, const unsigned long long* cscan,
+                                int64_t nc, const int64_t* lb, int64_t nb, int64_t total, JChild* ch,
+                                const int64_t* id_off, const int64_t* int_off, char* ids, int32_t* ints,
+                                unsigned int* first_err, int wrole) {
+  const unsigned char* t = reinterpret_cast<const unsigned char*>(text);
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    JChild r{};
+    int64_t ci;
+    if (kWrite) {
+      r = ch[u];
+      ci = r.cont;
+      if (r.err || conts[ci].role != wrole) continue;  // another role's pass writes it
+    } else {  // container of unit u, index inside it
+      int64_t lo = 0, hi = nc;  // last container with cscan <= u
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)cscan[mid] <= u) lo = mid;
+        else hi = mid;
+      }
+      ci = lo;
+      while (ci + 1 < nc && (int64_t)cscan[ci + 1] <= u) ++ci;
+      const JCont jc = conts[ci];
+      const int64_t idx = u - (int64_t)cscan[ci];
+      const int64_t b0 = lower_b(lb, nb, jc.open), b1 = lower_b(lb, nb, jc.close);
+      r.a = idx == 0 ? jc.open + 1 : lb[b0 + idx - 1] + 1;
+      r.e = b0 + idx < b1 ? lb[b0 + idx] : jc.close;
+      r.cont = (int32_t)ci;
+      r.line = jc.line;
+    }
+    const JCont jc = conts[ci];
+    JIn in{t, r.a, r.e};
+    int err = 0;
+    skip_ws(in);
+    if (jc.is_obj) {  // a member: "key": value
+      if (jc.role == kRLengths) {
+        if (in.p >= in.e || t[in.p] != '"') err = kJErr;
+        else {
+          r.id_at = in.p;
+          int64_t l;
+          err = jstring(in, kWrite ? ids + id_off[u] : nullptr, kWrite ? r.id_len : 0, &l);
+          r.id_len = l;
+        }
+        if (!err) {
+          skip_ws(in);
+          if (in.p >= in.e || t[in.p] != ':') err = kJErr;
+          else ++in.p;
+        }
+        if (!err) {
+          skip_ws(in);
+          r.ints_at = in.p;
+          int64_t k;
+          err = jint_array(in, kWrite ? ints + int_off[u] : nullptr, &k);
+          if (err == kJErr && !kWrite) {  // a syntax error is still an error; keep kJErr
+          }
+          r.n_int = k;
+        }
+      } else {
+        int64_t l;
+        if (in.p >= in.e || t[in.p] != '"' || jstring(in, nullptr, 0, &l)) err = kJErr;
+        if (!err) {
+          skip_ws(in);
+          if (in.p >= in.e || t[in.p] != ':') err = kJErr;
+          else ++in.p;
+        }
+        if (!err) err = jskip(in);
+      }
+    } else if (jc.role == kRSched) {
+      if (in.p >= in.e || t[in.p] != '"') {
+        err = jskip(in);  // get<std::string> of a non-string: type_error
+        if (!err) err = kJErr;
+      } else {
+        r.id_at = in.p;
+        int64_t l;
+        err = jstring(in, kWrite ? ids + id_off[u] : nullptr, kWrite ? r.id_len : 0, &l);
+        r.id_len = l;
+      }
+    } else if (jc.role == kRPrompts) {
+      if (kWrite) {  // the id and the tokens, from the recorded positions
+        JIn is{t, r.id_at, r.e};
+        int64_t l;
+        jstring(is, ids + id_off[u], r.id_len, &l);
+        JIn it{t, r.ints_at, r.e};
+        int64_t k;
+        jint_array(it, ints + int_off[u], &k);
+        continue;
+      }
+      // a prompt object: id / ground_truth_len / token_ids (the last of each)
+      bool has_id = false, has_gt = false, has_tok = false;
+      if (in.p >= in.e || t[in.p] != '{') {
+        err = jskip(in);  // at() on a non-object: type_error
+        if (!err) err = kJErr;
+      } else {
+        ++in.p;
+        skip_ws(in);
+        if (in.p < in.e && t[in.p] == '}') ++in.p;
+        else
+          while (!err) {
+            static const char* const kP[] = {"id", "ground_truth_len", "token_ids"};
+            const int key = jkey(in, kP, 3, &err);
+            if (err) break;
+            if (key == 0) {
+              if (in.p >= in.e || t[in.p] != '"') {
+                err = jskip(in);
+                if (!err) err = kJErr;
+              } else {
+                r.id_at = in.p;
+                err = jstring(in, nullptr, 0, &r.id_len);
+                has_id = true;
+              }
+            } else if (key == 1) {
+              err = jint(in, &r.gt);
+              has_gt = true;
+            } else if (key == 2) {
+              r.ints_at = in.p;
+              const unsigned char c0 = in.p < in.e ? t[in.p] : 0;
+              err = jint_array(in, nullptr, &r.n_int);
+              if (err == kJErr && c0 != '[') {  // a type_error, but the value must still parse
+                JIn tmp{t, r.ints_at, r.e};
+                err = jskip(tmp) ? kJErr : kJErr;
+              }
+              has_tok = true;
+            } else {
+              err = jskip(in);
+            }
+            if (err) break;
+            skip_ws(in);
+            if (in.p < in.e && t[in.p] == ',') {
+              ++in.p;
+              skip_ws(in);
+              continue;
+            }
+            if (in.p < in.e && t[in.p] == '}') {
+              ++in.p;
+              break;
+            }
+            err = kJErr;
+          }
+        if (!err && !(has_id && has_gt && has_tok)) err = kJErr;
+      }
+    } else {
+      err = jskip(in);
+    }
+    if (!err) {
+      skip_ws(in);
+      if (in.p != in.e) err = kJErr;
+    }
+    if (!kWrite) {
+      r.err = err;
+      ch[u] = r;
+      if (err) atomicMin(first_err, ((unsigned int)r.line << 1) | (err == kJUnsup ? 1u : 0u));
+    }
+  }
+}
+
+// Children with no error keep their pass-1 sizes; others count 0.
+__global__ void js_sizes_kernel(const JChild* ch, const JCont* conts, int64_t total, int role,
+                                unsigned long long* idl, unsigned long long* nint) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const JChild r = ch[u];
+    const bool mine = !r.err && conts[r.cont].role == role;
+    idl[u] = mine ? (unsigned long long)r.id_len : 0ULL;
+    nint[u] = mine ? (unsigned long long)r.n_int : 0ULL;
+  }
+}
+
+// The header's prompts, in child order: their line-order tables for the
+// shared tail (token offsets, id offsets, ground truths).
+__global__ void js_prompt_tables_kernel(const JChild* ch, int64_t c0, int32_t P, const int64_t* id_off,
+                                        const int64_t* int_off, int64_t* p_id_off, int64_t* p_tok_off,
+                                        int32_t* p_gt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= P;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    p_id_off[i] = id_off[c0 + i] - id_off[c0];
+    p_tok_off[i] = int_off[c0 + i] - int_off[c0];
+    if (i < P) p_gt[i] = ch[c0 + i].gt;
+  }
+}
+
+}  // namespace
+}  // namespace rs
+
+using namespace rs;
+
+extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n_bytes, int device_ptr,
+                                        rs_trace_csr** out) {
+  RS_DEVICE_GUARD(ctx);
+  if (!ctx || !out || (!text && n_bytes > 0)) return fail(RS_E_ARG, "NULL argument");
+  if (n_bytes < 0) return fail(RS_E_ARG, "negative size");
+  *out = nullptr;
+  try {
+    PhaseClock clk;
+    char* d_text = nullptr;
+    RS_TRY(trace_stage_text(ctx, text, n_bytes, device_ptr, &d_text));
+    AsyncBuf b_ls;
+    int64_t* line_start = nullptr;
+    int64_t L = 0;
+    RS_TRY(trace_line_starts(ctx, d_text, n_bytes, &b_ls, &line_start, &L));
+    clk.mark("line starts");
+    auto grid = [&](int64_t n) {
+      return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 32 * (int64_t)ctx->num_sms));
+    };
+    // 1. structural index
+    const int64_t W = std::max<int64_t>(1, (n_bytes + 63) / 64);
+    AsyncBuf b_w;
+    const size_t wbytes = abytes(W, 1) + abytes(W + 1, 4) * 6 + abytes(W + 1, 8) * 2 +
+                          scan_scratch_bytes(W + 1, 8) + abytes(8, 8);
+    char* wb = b_w.alloc<char>(ctx->stream, wbytes);
+    if (!wb) return fail(RS_E_NOMEM, "jsonl structural index: allocation failed");
+    auto carve = [&](char*& base, size_t nb) {
+      char* q = base;
+      base += nb;
+      return q;
+    };
+    uint8_t* tail = (uint8_t*)carve(wb, abytes(W, 1));
+    uint32_t* qpar = (uint32_t*)carve(wb, abytes(W + 1, 4));
+    uint32_t* qscan = (uint32_t*)carve(wb, abytes(W + 1, 4));
+    uint32_t* ca = (uint32_t*)carve(wb, abytes(W + 1, 4));
+    uint32_t* cb = (uint32_t*)carve(wb, abytes(W + 1, 4));
+    uint32_t* oa = (uint32_t*)carve(wb, abytes(W + 1, 4));
+    uint32_t* ob = (uint32_t*)carve(wb, abytes(W + 1, 4));
+    auto* dd = (unsigned long long*)carve(wb, abytes(W + 1, 8));
+    auto* dscan = (unsigned long long*)carve(wb, abytes(W + 1, 8));
+    auto* part64 = (unsigned long long*)carve(wb, scan_scratch_bytes(W + 1, 8));
+    auto* small = (unsigned int*)carve(wb, abytes(8, 8));  // first line, #containers, first error, totals
+    uint32_t* part32 = (uint32_t*)part64;
+    const int gw = grid(W);
+    RS_LAUNCH(ctx, "jsonl_bs", js_bs_kernel, gw, 256, 0, d_text, n_bytes, W, tail);
+    RS_LAUNCH(ctx, "jsonl_quote", js_quote_kernel, gw, 256, 0, d_text, n_bytes, W, tail, qpar);
+    RS_TRY(exclusive_scan<uint32_t>(ctx, qpar, qscan, W, part32, nullptr));
+    RS_LAUNCH(ctx, "jsonl_depth", js_depth_kernel, gw, 256, 0, d_text, n_bytes, W, tail, qscan, dd);
+    RS_TRY(exclusive_scan<unsigned long long>(ctx, dd, dscan, W, part64, nullptr));
+    RS_LAUNCH(ctx, "jsonl_tok_count", js_tokens_kernel<false>, gw, 256, 0, d_text, n_bytes, W, tail,
+              qscan, dscan, ca, cb, (const uint32_t*)nullptr, (const uint32_t*)nullptr, (uint64_t*)nullptr,
+              (int64_t*)nullptr);
+    RS_TRY(exclusive_scan<uint32_t>(ctx, ca, oa, W, part32, oa + W));
+    RS_TRY(exclusive_scan<uint32_t>(ctx, cb, ob, W, part32, ob + W));
+    uint32_t tot[2];
+    RS_TRY(d2h(ctx, &tot[0], oa + W, 4));
+    RS_TRY(d2h(ctx, &tot[1], ob + W, 4));
+    RS_TRY(sync_and_check(ctx));
+    const int64_t NA = tot[0], NB = tot[1];
+    AsyncBuf b_lists;
+    char* lbuf = b_lists.alloc<char>(ctx->stream, abytes(NA + 1, 8) + abytes(NB + 1, 8));
+    if (!lbuf) return fail(RS_E_NOMEM, "jsonl token lists: allocation failed");
+    uint64_t* la = (uint64_t*)carve(lbuf, abytes(NA + 1, 8));
+    int64_t* lbv = (int64_t*)carve(lbuf, abytes(NB + 1, 8));
+    RS_LAUNCH(ctx, "jsonl_tok_write", js_tokens_kernel<true>, gw, 256, 0, d_text, n_bytes, W, tail,
+              qscan, dscan, ca, cb, (const uint32_t*)oa, (const uint32_t*)ob, la, lbv);
+    clk.mark("structural index");
+    // 2. lines
+    const int64_t cont_cap = NA / 2 + 1;
+    AsyncBuf b_lines;
+    char* lnb = b_lines.alloc<char>(ctx->stream, abytes(L, sizeof(JLine)) + abytes(cont_cap, sizeof(JCont)) +
+                                                     abytes(cont_cap + 1, 8) * 2 + scan_scratch_bytes(cont_cap + 1, 8));
+    if (!lnb) return fail(RS_E_NOMEM, "jsonl line records: allocation failed");
+    JLine* d_lines = (JLine*)carve(lnb, abytes(L, sizeof(JLine)));
+    JCont* d_conts = (JCont*)carve(lnb, abytes(cont_cap, sizeof(JCont)));
+    auto* nchild = (unsigned long long*)carve(lnb, abytes(cont_cap + 1, 8));
+    auto* cscan = (unsigned long long*)carve(lnb, abytes(cont_cap + 1, 8));
+    auto* cpart = (unsigned long long*)carve(lnb, scan_scratch_bytes(cont_cap + 1, 8));
+    const unsigned int init[4] = {~0u, 0u, ~0u, 0u};
+    RS_TRY(h2d(ctx, small, init, sizeof init));
+    RS_LAUNCH(ctx, "jsonl_first_line", js_first_line_kernel, grid(L), 256, 0, d_text, line_start, L, n_bytes,
+              small);
+    RS_LAUNCH(ctx, "jsonl_lines", js_line_kernel, grid(L), 128, 0, d_text, line_start, L, n_bytes, small,
+              la, NA, d_lines, d_conts, small + 1, cont_cap);
+    unsigned int hs[2];
+    RS_TRY(d2h(ctx, hs, small, 8));
+    RS_TRY(sync_and_check(ctx));
+    const int64_t first = hs[0] == ~0u ? -1 : (int64_t)hs[0];
+    const int64_t NC = std::min<int64_t>(hs[1], cont_cap);
+    // 3. children of every member container
+    RS_LAUNCH(ctx, "jsonl_child_count", js_child_count_kernel, grid(NC), 256, 0, d_text, d_conts, NC, lbv, NB,
+              nchild);
+    RS_TRY(exclusive_scan<unsigned long long>(ctx, nchild, cscan, NC, cpart, cscan + NC));
+    unsigned long long nch = 0;
+    RS_TRY(d2h(ctx, &nch, cscan + NC, 8));
+    RS_TRY(sync_and_check(ctx));
+    const int64_t NCH = (int64_t)nch;
+    AsyncBuf b_ch;
+    char* chb = b_ch.alloc<char>(ctx->stream, abytes(NCH + 1, sizeof(JChild)) + abytes(NCH + 1, 8) * 4 +
+                                                  scan_scratch_bytes(NCH + 1, 8));
+    if (!chb) return fail(RS_E_NOMEM, "jsonl children: allocation failed");
+    JChild* d_ch = (JChild*)carve(chb, abytes(NCH + 1, sizeof(JChild)));
+    auto* idl = (unsigned long long*)carve(chb, abytes(NCH + 1, 8));
+    auto* nint = (unsigned long long*)carve(chb, abytes(NCH + 1, 8));
+    auto* id_off = (unsigned long long*)carve(chb, abytes(NCH + 1, 8));
+    auto* int_off = (unsigned long long*)carve(chb, abytes(NCH + 1, 8));
+    auto* chpart = (unsigned long long*)carve(chb, scan_scratch_bytes(NCH + 1, 8));
+    if (NCH > 0)
+      RS_LAUNCH(ctx, "jsonl_child_check", js_child_kernel<false>, grid(NCH), 128, 0, d_text, d_conts, cscan, NC,
+                lbv, NB, NCH, d_ch, (const int64_t*)nullptr, (const int64_t*)nullptr, (char*)nullptr,
+                (int32_t*)nullptr, small + 2, 0);
+    // the first error line over the lines and the children
+    std::vector<JLine> hl(L);
+    unsigned int cerr = ~0u;
+    RS_TRY(d2h(ctx, hl.data(), d_lines, sizeof(JLine) * L));
+    RS_TRY(d2h(ctx, &cerr, small + 2, 4));
+    RS_TRY(sync_and_check(ctx));
+    clk.mark("lines + children");
+    int64_t err_line = -1;
+    int err_kind = 0;
+    for (int64_t ln = 0; ln < L; ++ln)
+      if (hl[ln].err) {
+        err_line = ln;
+        err_kind = hl[ln].err;
+        break;
+      }
+    if (cerr != ~0u && (err_line < 0 || (int64_t)(cerr >> 1) < err_line)) {
+      err_line = cerr >> 1;
+      err_kind = (cerr & 1) ? kJUnsup : kJErr;
+    } else if (cerr != ~0u && (int64_t)(cerr >> 1) == err_line && err_kind == kJUnsup && !(cerr & 1)) {
+      err_kind = kJErr;
+    }
+    if (err_line >= 0)
+      return trace_parse_error(err_line, err_kind == kJUnsup ? "JSON construct the device reader does not support"
+                                                             : "malformed JSON trace line");
+    if (first < 0) return fail(RS_E_PARSE, "<trace>: missing header line");
+    // 4. the header's prompts (the container with the prompts role, if any)
+    std::vector<JCont> hc(NC);
+    std::vector<unsigned long long> hcs(NC + 1);
+    if (NC) {
+      RS_TRY(d2h(ctx, hc.data(), d_conts, sizeof(JCont) * NC));
+      RS_TRY(d2h(ctx, hcs.data(), cscan, 8ull * (NC + 1)));
+      RS_TRY(sync_and_check(ctx));
+    } else {
+      hcs[0] = 0;
+    }
+    auto tr = new rs_trace_csr();
+    std::unique_ptr<rs_trace_csr> own(tr);
+    const JLine& H = hl[first];
+    tr->g = H.g;
+    tr->max_prompt_len = H.mp;
+    tr->max_response_len = H.mr;
+    int64_t pc = -1;  // the prompts container
+    for (int64_t c = 0; c < NC; ++c)
+      if (hc[c].role == kRPrompts) pc = c;
+    int32_t P = 0;
+    int64_t c0 = 0;
+    if (pc >= 0) {
+      c0 = (int64_t)hcs[pc];
+      P = (int32_t)(hcs[pc + 1] - hcs[pc]);
+    }
+    // sizes of every extracted child (per role), scanned, then written
+    auto sizes = [&](int role) -> int {
+      if (NCH == 0) return RS_OK;
+      RS_LAUNCH(ctx, "jsonl_sizes", js_sizes_kernel, grid(NCH), 256, 0, d_ch, d_conts, NCH, role, idl, nint);
+      RS_TRY(exclusive_scan<unsigned long long>(ctx, idl, id_off, NCH, chpart, id_off + NCH));
+      RS_TRY(exclusive_scan<unsigned long long>(ctx, nint, int_off, NCH, chpart, int_off + NCH));
+      return RS_OK;
+    };
+    RS_TRY(sizes(kRPrompts));
+    unsigned long long ptot[2] = {0, 0};
+    if (NCH) {
+      RS_TRY(d2h(ctx, &ptot[0], id_off + NCH, 8));
+      RS_TRY(d2h(ctx, &ptot[1], int_off + NCH, 8));
+      RS_TRY(sync_and_check(ctx));
+    }
+    const int64_t IDB = (int64_t)ptot[0], T = (int64_t)ptot[1];
+    AsyncBuf b_p;
+    char* pb = b_p.alloc<char>(ctx->stream, abytes(IDB + 1, 1) + abytes(T + 1, 4) + abytes(P + 1, 8) * 2 +
+                                                abytes(P + 1, 4) * 2);
+    if (!pb) return fail(RS_E_NOMEM, "jsonl prompts: allocation failed");
+    char* d_ids = carve(pb, abytes(IDB + 1, 1));
+    int32_t* d_tok = (int32_t*)carve(pb, abytes(T + 1, 4));
+    int64_t* p_id_off = (int64_t*)carve(pb, abytes(P + 1, 8));
+    int64_t* p_tok_off = (int64_t*)carve(pb, abytes(P + 1, 8));
+    int32_t* p_gt = (int32_t*)carve(pb, abytes(P + 1, 4));
+    uint32_t* d_perm = (uint32_t*)carve(pb, abytes(P + 1, 4));
+    int64_t maxid = 1;
+    if (P > 0) {
+      RS_LAUNCH(ctx, "jsonl_prompt_write", js_child_kernel<true>, grid(NCH), 128, 0, d_text, d_conts, cscan, NC,
+                lbv, NB, NCH, d_ch, (const int64_t*)id_off, (const int64_t*)int_off, d_ids, d_tok, small + 2,
+                (int)kRPrompts);
+      RS_LAUNCH(ctx, "jsonl_prompt_tables", js_prompt_tables_kernel, grid(P + 1), 256, 0, d_ch, c0, P,
+                (const int64_t*)id_off, (const int64_t*)int_off, p_id_off, p_tok_off, p_gt);
+      std::vector<int64_t> ioff(P + 1);
+      RS_TRY(d2h(ctx, ioff.data(), p_id_off, 8ull * (P + 1)));
+      RS_TRY(sync_and_check(ctx));
+      for (int32_t i = 0; i < P; ++i) maxid = std::max<int64_t>(maxid, ioff[i + 1] - ioff[i]);
+    }
+    RS_TRY(trace_sorted_table(ctx, tr, P, maxid, d_ids, p_id_off, p_tok_off, p_gt, d_perm));
+    clk.mark("prompts");
+    // 5. steps, on the host: scheduled ids and length lists per step line
+    std::vector<JChild> hch(NCH);
+    std::vector<unsigned long long> h_id_off, h_int_off;
+    std::vector<char> h_ids;
+    std::vector<int32_t> h_ints;
+    bool any_steps = false;
+    for (int64_t ln = 0; ln < L; ++ln) any_steps |= hl[ln].kind == kLStep;
+    if (any_steps && NCH > 0) {
+      auto gather = [&](int role) -> int {  // sizes + writes of one role's children, to the host
+        RS_TRY(sizes(role));
+        unsigned long long tt[2];
+        RS_TRY(d2h(ctx, &tt[0], id_off + NCH, 8));
+        RS_TRY(d2h(ctx, &tt[1], int_off + NCH, 8));
+        RS_TRY(sync_and_check(ctx));
+        AsyncBuf b;
+        char* q = b.alloc<char>(ctx->stream, abytes(tt[0] + 1, 1) + abytes(tt[1] + 1, 4));
+        if (!q) return fail(RS_E_NOMEM, "jsonl steps: allocation failed");
+        char* d_i = q;
+        int32_t* d_n = (int32_t*)(q + abytes(tt[0] + 1, 1));
+        RS_LAUNCH(ctx, "jsonl_step_write", js_child_kernel<true>, grid(NCH), 128, 0, d_text, d_conts, cscan, NC,
+                  lbv, NB, NCH, d_ch, (const int64_t*)id_off, (const int64_t*)int_off, d_i, d_n, small + 2,
+                  role);
+        const size_t o_i = h_ids.size(), o_n = h_ints.size();
+        h_ids.resize(o_i + tt[0]);
+        h_ints.resize(o_n + tt[1]);
+        std::vector<unsigned long long> a(NCH + 1), c(NCH + 1);
+        RS_TRY(d2h(ctx, a.data(), id_off, 8ull * (NCH + 1)));
+        RS_TRY(d2h(ctx, c.data(), int_off, 8ull * (NCH + 1)));
+        if (tt[0]) RS_TRY(d2h(ctx, h_ids.data() + o_i, d_i, tt[0]));
+        if (tt[1]) RS_TRY(d2h(ctx, h_ints.data() + o_n, d_n, 4ull * tt[1]));
+        RS_TRY(sync_and_check(ctx));
+        if (h_id_off.empty()) {
+          h_id_off.assign(NCH + 1, 0);
+          h_int_off.assign(NCH + 1, 0);
+        }
+        for (int64_t u = 0; u < NCH; ++u)
+          if (hc[hch[u].cont].role == role) {
+            h_id_off[u] = o_i + a[u];
+            h_int_off[u] = o_n + c[u];
+          }
+        return RS_OK;
+      };
+      RS_TRY(d2h(ctx, hch.data(), d_ch, sizeof(JChild) * NCH));
+      RS_TRY(sync_and_check(ctx));
+      RS_TRY(gather(kRSched));
+      RS_TRY(gather(kRLengths));
+    }
+    // WorkloadTrace::validate: the prompt rules, then step by step
+    RS_TRY(trace_validate_prompts(tr));
+    // per step line: its containers (the last of each role) and children
+    std::vector<int64_t> sched_c(L, -1), len_c(L, -1);
+    for (int64_t c = 0; c < NC; ++c) {
+      if (hc[c].role == kRSched) sched_c[hc[c].line] = c;
+      if (hc[c].role == kRLengths) len_c[hc[c].line] = c;
+    }
+    auto id_index = [&](const std::string& id) -> int32_t {  // in the id-sorted table
+      int32_t lo = 0, hi = tr->count;
+      while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        const std::string m(tr->ids.data() + tr->id_off[mid], tr->ids.data() + tr->id_off[mid + 1]);
+        if (m < id) lo = mid + 1;
+        else if (id < m) hi = mid;
+        else return mid;
+      }
+      return -1;
+    };
+    std::vector<int32_t> st_idx, e_off{0}, e_prompt, lens;
+    int prev_step = -1;
+    const int32_t G = tr->g;
+    for (int64_t ln = 0; ln < L; ++ln) {
+      if (hl[ln].kind != kLStep) continue;
+      const int step = hl[ln].step;
+      const std::string sn = std::to_string(step);
+      std::vector<std::string> sched;
+      std::map<std::string, std::vector<int>> lmap;
+      if (len_c[ln] >= 0) {
+        const int64_t c = len_c[ln];
+        for (unsigned long long u = hcs[c]; u < hcs[c + 1]; ++u) {
+          std::string key(h_ids.data() + h_id_off[u], h_ids.data() + h_id_off[u] + hch[u].id_len);
+          lmap[key] = std::vector<int>(h_ints.begin() + h_int_off[u], h_ints.begin() + h_int_off[u] + hch[u].n_int);
+        }
+      }
+      if (hl[ln].has_sched && sched_c[ln] >= 0) {
+        const int64_t c = sched_c[ln];
+        for (unsigned long long u = hcs[c]; u < hcs[c + 1]; ++u)
+          sched.emplace_back(h_ids.data() + h_id_off[u], h_ids.data() + h_id_off[u] + hch[u].id_len);
+      } else if (!hl[ln].has_sched) {
+        for (const auto& kv : lmap) sched.push_back(kv.first);
+      }
+      if (step <= prev_step)
+        return fail(RS_E_VALIDATION, "step indices must be strictly increasing at step " + sn);
+      prev_step = step;
+      if (sched.empty()) return fail(RS_E_VALIDATION, "step " + sn + " schedules no prompts");
+      std::set<std::string> seen;
+      for (const std::string& id : sched) {
+        if (id_index(id) < 0) return fail(RS_E_VALIDATION, "step " + sn + " schedules unknown prompt '" + id + "'");
+        if (!seen.insert(id).second)
+          return fail(RS_E_VALIDATION, "step " + sn + " schedules prompt '" + id + "' twice");
+      }
+      if (lmap.size() != sched.size())
+        return fail(RS_E_VALIDATION, "step " + sn + " lengths do not cover the scheduled batch");
+      for (const auto& kv : lmap) {
+        if (!seen.count(kv.first))
+          return fail(RS_E_VALIDATION, "step " + sn + " has lengths for unscheduled prompt '" + kv.first + "'");
+        if ((int)kv.second.size() != G)
+          return fail(RS_E_VALIDATION, "step " + sn + " prompt '" + kv.first + "' needs exactly " +
+                                           std::to_string(G) + " response lengths");
+        for (int l : kv.second)
+          if (l < 1 || l > tr->max_response_len)
+            return fail(RS_E_VALIDATION, "step " + sn + " prompt '" + kv.first +
+                                             "' response length out of range: " + std::to_string(l));
+      }
+      st_idx.push_back(step);
+      for (const std::string& id : sched) {
+        e_prompt.push_back(id_index(id));
+        const std::vector<int>& v = lmap[id];
+        lens.insert(lens.end(), v.begin(), v.end());
+      }
+      e_off.push_back((int32_t)e_prompt.size());
+    }
+    clk.mark("steps (host)");
+    // the step table, owned by the handle
+    tr->n_steps = (int32_t)st_idx.size();
+    tr->n_entries = (int64_t)e_prompt.size();
+    tr->device = ctx->device;
+    if (tr->n_steps > 0) {
+      if (cudaMallocAsync(&tr->d_step_idx, 4ull * st_idx.size(), ctx->stream) != cudaSuccess ||
+          cudaMallocAsync(&tr->d_entry_off, 4ull * e_off.size(), ctx->stream) != cudaSuccess ||
+          cudaMallocAsync(&tr->d_entry_prompt, 4ull * std::max<size_t>(e_prompt.size(), 1), ctx->stream) != cudaSuccess ||
+          cudaMallocAsync(&tr->d_lengths, 4ull * std::max<size_t>(lens.size(), 1), ctx->stream) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(RS_E_NOMEM, "trace step table allocation failed");
+      }
+      RS_TRY(h2d(ctx, tr->d_step_idx, st_idx.data(), 4ull * st_idx.size()));
+      RS_TRY(h2d(ctx, tr->d_entry_off, e_off.data(), 4ull * e_off.size()));
+      RS_TRY(h2d(ctx, tr->d_entry_prompt, e_prompt.data(), 4ull * e_prompt.size()));
+      RS_TRY(h2d(ctx, tr->d_lengths, lens.data(), 4ull * lens.size()));
+    }
+    // the id-ordered token CSR
+    RS_TRY(trace_gather_csr(ctx, tr, d_tok, p_tok_off, d_perm));
+    clk.mark("CSR gather");
+    *out = own.release();
+    return RS_OK;
+  } catch (const std::bad_alloc&) {
+    return fail(RS_E_NOMEM, "host allocation failed");
+  }
+}

@@ -42,8 +42,8 @@
 #include <string>
 #include <vector>
 
-#include "rs_internal.cuh"
 #include "rs_sort.cuh"
+#include "rs_trace.cuh"
 
 namespace rs {
 
@@ -773,75 +773,13 @@ __global__ void csr_gather_kernel(const int32_t* src, const int64_t* src_off, co
 
 using namespace rs;
 
-struct rs_trace_csr {
-  int32_t count = 0;
-  int64_t n_tokens = 0;
-  int32_t g = 1, max_prompt_len = 1024, max_response_len = 2048;
-  int32_t* d_tokens = nullptr;
-  int64_t* d_offsets = nullptr;
-  std::vector<char> ids;
-  std::vector<int64_t> id_off;
-  std::vector<int32_t> gt;
-  std::vector<int64_t> offsets;
-  // the step table (rs_trace_csr_steps_*)
-  int32_t n_steps = 0;
-  int64_t n_entries = 0;
-  int32_t* d_step_idx = nullptr;
-  int32_t* d_entry_off = nullptr;
-  int32_t* d_entry_prompt = nullptr;
-  int32_t* d_lengths = nullptr;
-  // The outputs are stream-ordered allocations, complete when the parse
-  // returns. The handle may outlive its context (and the context's streams),
-  // so it is freed with the synchronous cudaFree on its own device.
-  int device = 0;
-  ~rs_trace_csr() {
-    void* bufs[6] = {d_tokens, d_offsets, d_step_idx, d_entry_off, d_entry_prompt, d_lengths};
-    if (std::all_of(bufs, bufs + 6, [](void* b) { return b == nullptr; })) return;
-    int prev = -1;
-    cudaGetDevice(&prev);
-    if (prev != device) cudaSetDevice(device);
-    for (void* b : bufs)
-      if (b) cudaFree(b);
-    if (prev >= 0 && prev != device) cudaSetDevice(prev);
-    cudaGetLastError();
-  }
-};
-
-// Stream-ordered temporary (outside the arena, which is re-reserved once the
-// prompt table's size is known).
-struct AsyncBuf {
-  void* p = nullptr;
-  cudaStream_t s = nullptr;
-  ~AsyncBuf() {
-    if (p) cudaFreeAsync(p, s);
-  }
-  template <class T>
-  T* alloc(cudaStream_t st, size_t count) {
-    s = st;
-    if (cudaMallocAsync(&p, std::max<size_t>(count * sizeof(T), 16), st) != cudaSuccess) {
-      cudaGetLastError();
-      p = nullptr;
-    }
-    return static_cast<T*>(p);
-  }
-};
-
-// RS_TRACE_PHASES=1: host wall time of each parse phase on stderr (tools/prof_trace.py).
-struct PhaseClock {
-  bool on = std::getenv("RS_TRACE_PHASES") != nullptr;
-  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-  void mark(const char* what) {
-    if (!on) return;
-    const auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "  [trace phase] %-22s %8.3f ms\n", what,
-                 std::chrono::duration<double, std::milli>(now - t).count());
-    t = now;
-  }
-};
-
-static int parse_error(int64_t line, const std::string& what) {
+namespace rs {
+int trace_parse_error(int64_t line, const std::string& what) {
   return fail(RS_E_PARSE, "<trace>:" + std::to_string(line + 1) + ": " + what);
 }
+}  // namespace rs
+
+static int parse_error(int64_t line, const std::string& what) { return trace_parse_error(line, what); }
 
 static std::string trim_ws(const std::string& s) {  // trim, workload.cpp:112-117
   const size_t a = s.find_first_not_of(" \t\r");
@@ -1110,45 +1048,17 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
   *out = nullptr;
   try {
     PhaseClock clk;
-    // 1. the bytes, 16-byte aligned and padded, in the context input buffer
-    const size_t need = abytes(n_bytes + 64, 1);
-    if (need > ctx->in_cap) {
-      RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-      if (ctx->in_buf) cudaFree(ctx->in_buf);
-      ctx->in_buf = nullptr;
-      ctx->in_cap = 0;
-      if (cudaMalloc(&ctx->in_buf, need) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(RS_E_NOMEM, "trace text allocation failed");
-      }
-      ctx->in_cap = need;
-    }
-    char* d_text = ctx->in_buf;
-    if (n_bytes)
-      RS_CUDA_TRY(cudaMemcpyAsync(d_text, text, n_bytes,
-                                  device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                                  ctx->stream));
-    RS_CUDA_TRY(cudaMemsetAsync(d_text + n_bytes, 0, 64, ctx->stream));
+    // 1. the bytes; 2. line starts
+    char* d_text = nullptr;
+    RS_TRY(trace_stage_text(ctx, text, n_bytes, device_ptr, &d_text));
     clk.mark("text");
-    // 2. line starts
-    const int64_t nblk = std::max<int64_t>(1, (n_bytes + kChunk - 1) / kChunk);
-    RS_TRY(arena_reserve(ctx, abytes(nblk, 4) * 2 + 4096));
-    uint32_t* cnt = arena_alloc<uint32_t>(ctx, nblk);
-    uint32_t* base = arena_alloc<uint32_t>(ctx, nblk);
-    RS_LAUNCH(ctx, "trace_nl_count", nl_count_kernel, (int)nblk, kNlT, 0, d_text, n_bytes, cnt);
-    RS_LAUNCH(ctx, "trace_nl_scan", exclusive_scan_u32_kernel, 1, 1024, 0, cnt, base, nblk);
-    uint32_t last[2] = {0, 0};
-    RS_TRY(d2h(ctx, &last[0], base + nblk - 1, 4));
-    RS_TRY(d2h(ctx, &last[1], cnt + nblk - 1, 4));
-    RS_TRY(sync_and_check(ctx));
-    const int64_t L = (int64_t)last[0] + last[1] + 1;  // lines (the last may be empty)
-    clk.mark("newline count");
     AsyncBuf b_ls, b_info;
-    int64_t* line_start = b_ls.alloc<int64_t>(ctx->stream, L + 1);
+    int64_t* line_start = nullptr;
+    int64_t L = 0;
+    RS_TRY(trace_line_starts(ctx, d_text, n_bytes, &b_ls, &line_start, &L));
+    clk.mark("line starts");
     LineInfo* info = b_info.alloc<LineInfo>(ctx->stream, L);
-    if (!line_start || !info) return fail(RS_E_NOMEM, "trace line arrays: allocation failed");
-    RS_LAUNCH(ctx, "trace_nl_write", nl_write_kernel, (int)nblk, kNlT, 0, d_text, n_bytes, base,
-              line_start);
+    if (!info) return fail(RS_E_NOMEM, "trace line arrays: allocation failed");
     // 3. one warp per line
     if (L >= (int64_t)UINT32_MAX - 1) return fail(RS_E_ARG, "trace has too many lines");
     const int cgrid = (int)std::min<int64_t>((L * 32 + 255) / 256, 64 * (int64_t)ctx->num_sms);
@@ -1219,14 +1129,13 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
     const int64_t* d_id_off = (const int64_t*)pidlen;
     // prompt-level device work: the arena, sized now (the line arrays live
     // outside it)
-    const size_t more = abytes(T + 1, 4) + abytes(IDB + 1, 1) + abytes(P, 4) + abytes(P + 1, 8) +
+    const size_t more = abytes(T + 1, 4) + abytes(IDB + 1, 1) + abytes(P, 4) +
                         rank_strings_device_bytes(std::max(P, 1), std::max<int64_t>(maxid, 1)) +
                         (1 << 16);
     RS_TRY(arena_reserve(ctx, more));
     int32_t* d_tok_line = arena_alloc<int32_t>(ctx, T + 1);
     char* d_ids = arena_alloc<char>(ctx, IDB + 1);
     uint32_t* d_perm = arena_alloc<uint32_t>(ctx, std::max(P, 1));
-    int64_t* d_sorted_off = arena_alloc<int64_t>(ctx, P + 1);
     if (P > 0) {
       const int pgrid = (int)std::min<int64_t>(((int64_t)P * 32 + kTokT - 1) / kTokT, 64 * (int64_t)ctx->num_sms);
       RS_LAUNCH(ctx, "trace_tokens", tokens_kernel, pgrid, kTokT, 0, d_text, line_start, L, n_bytes,
@@ -1234,80 +1143,18 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
       RS_LAUNCH(ctx, "trace_ids", ids_gather_kernel,
                 (int)std::min<int64_t>(P, 16 * (int64_t)ctx->num_sms), 32, 0, d_text, info, d_pline,
                 P, d_id_off, d_ids);
-      // 6. id order (std::string <) on the device
-      RS_TRY(rank_strings_device(ctx, d_ids, d_id_off, P, maxid, d_perm));
     }
-    std::vector<uint32_t> perm(P);
-    std::vector<char> ids_line(IDB);
-    std::vector<int64_t> tok_off(P + 1, 0), id_off(P + 1, 0);
-    std::vector<int32_t> gt_line(P);
-    if (P > 0) {
-      RS_TRY(d2h(ctx, perm.data(), d_perm, 4ull * P));
-      RS_TRY(d2h(ctx, tok_off.data(), d_tok_off, 8ull * (P + 1)));
-      RS_TRY(d2h(ctx, id_off.data(), d_id_off, 8ull * (P + 1)));
-      RS_TRY(d2h(ctx, gt_line.data(), d_pgt, 4ull * P));
-      if (!ids_line.empty()) RS_TRY(d2h(ctx, ids_line.data(), d_ids, ids_line.size()));
-      RS_TRY(sync_and_check(ctx));
-    }
-    // 7. sorted prompt table + WorkloadTrace::validate's prompt rules
-    clk.mark("tokens + id rank");
-    tr->offsets.assign(P + 1, 0);
-    tr->id_off.assign(P + 1, 0);
-    tr->gt.resize(P);
-    for (int32_t r = 0; r < P; ++r) {
-      const uint32_t i = perm[r];
-      tr->offsets[r + 1] = tr->offsets[r] + (tok_off[i + 1] - tok_off[i]);
-      tr->id_off[r + 1] = tr->id_off[r] + (id_off[i + 1] - id_off[i]);
-      tr->gt[r] = gt_line[i];
-    }
-    tr->ids.resize(IDB);
-    for (int32_t r = 0; r < P; ++r) {
-      const uint32_t i = perm[r];
-      std::memcpy(tr->ids.data() + tr->id_off[r], ids_line.data() + id_off[i], id_off[i + 1] - id_off[i]);
-    }
+    // 6. id order (std::string <) on the device; 7. the sorted host table
+    RS_TRY(trace_sorted_table(ctx, tr, P, maxid, d_ids, d_id_off, d_tok_off, d_pgt, d_perm));
+    clk.mark("id rank + sorted table");
     // 8. the step rows' ParseErrors, then the validator
-    clk.mark("sorted table (host)");
     RS_TRY(sr.parse(meta_after));
     clk.mark("step rows parse");
-    if (tr->g < 1) return fail(RS_E_VALIDATION, "responses_per_prompt must be >= 1");
-    if (tr->max_prompt_len < 1 || tr->max_response_len < 1)
-      return fail(RS_E_VALIDATION, "trace limits must be positive");
-    auto id_of = [&](int32_t r) {
-      return std::string(tr->ids.data() + tr->id_off[r], tr->ids.data() + tr->id_off[r + 1]);
-    };
-    for (int32_t r = 0; r < P; ++r) {
-      if (r > 0) {  // std::string order: bytes, then length
-        const char* pa = tr->ids.data() + tr->id_off[r - 1];
-        const char* pb = tr->ids.data() + tr->id_off[r];
-        const int64_t la = tr->id_off[r] - tr->id_off[r - 1], lb = tr->id_off[r + 1] - tr->id_off[r];
-        const int c = std::memcmp(pa, pb, (size_t)std::min(la, lb));
-        if (!(c < 0 || (c == 0 && la < lb)))
-          return fail(RS_E_VALIDATION, "prompts not sorted by unique id near '" + id_of(r) + "'");
-      }
-      const int64_t len = tr->offsets[r + 1] - tr->offsets[r];
-      if (len < 1) return fail(RS_E_VALIDATION, "prompt '" + id_of(r) + "' has no tokens");
-      if (len > tr->max_prompt_len)
-        return fail(RS_E_VALIDATION, "prompt '" + id_of(r) + "' longer than max_prompt_len");
-      if (tr->gt[r] < 1 || tr->gt[r] > tr->max_response_len)
-        return fail(RS_E_VALIDATION, "prompt '" + id_of(r) + "' ground_truth_len out of range");
-    }
+    RS_TRY(trace_validate_prompts(tr));
     RS_TRY(sr.table());
     clk.mark("step table");
     // 9. the id-ordered token CSR, owned by the handle
-    tr->device = ctx->device;
-    if (cudaMallocAsync(&tr->d_tokens, 4ull * std::max<int64_t>(T, 1), ctx->stream) != cudaSuccess ||
-        cudaMallocAsync(&tr->d_offsets, 8ull * (P + 1), ctx->stream) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(RS_E_NOMEM, "trace CSR allocation failed");
-    }
-    RS_TRY(h2d(ctx, tr->d_offsets, tr->offsets.data(), 8ull * (P + 1)));
-    if (P > 0) {
-      RS_TRY(h2d(ctx, d_sorted_off, tr->offsets.data(), 8ull * (P + 1)));
-      RS_LAUNCH(ctx, "trace_gather", csr_gather_kernel,
-                (int)std::min<int64_t>(P, 16 * (int64_t)ctx->num_sms), 256, 0, d_tok_line,
-                d_tok_off, d_perm, P, d_sorted_off, tr->d_tokens);
-    }
-    RS_TRY(sync_and_check(ctx));
+    RS_TRY(trace_gather_csr(ctx, tr, d_tok_line, d_tok_off, d_perm));
     clk.mark("CSR gather");
     *out = own.release();
     return RS_OK;
@@ -1315,6 +1162,137 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
     return fail(RS_E_NOMEM, "host allocation failed");
   }
 }
+
+namespace rs {
+
+int trace_stage_text(rs_ctx* ctx, const char* text, int64_t n_bytes, int device_ptr, char** d_text) {
+  const size_t need = abytes(n_bytes + 64, 1);
+  if (need > ctx->in_cap) {
+    RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (ctx->in_buf) cudaFree(ctx->in_buf);
+    ctx->in_buf = nullptr;
+    ctx->in_cap = 0;
+    if (cudaMalloc(&ctx->in_buf, need) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(RS_E_NOMEM, "trace text allocation failed");
+    }
+    ctx->in_cap = need;
+  }
+  *d_text = ctx->in_buf;
+  if (n_bytes)
+    RS_CUDA_TRY(cudaMemcpyAsync(*d_text, text, n_bytes,
+                                device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                ctx->stream));
+  RS_CUDA_TRY(cudaMemsetAsync(*d_text + n_bytes, 0, 64, ctx->stream));
+  return RS_OK;
+}
+
+int trace_line_starts(rs_ctx* ctx, const char* d_text, int64_t n_bytes, AsyncBuf* buf,
+                      int64_t** line_start, int64_t* L_out) {
+  const int64_t nblk = std::max<int64_t>(1, (n_bytes + kChunk - 1) / kChunk);
+  RS_TRY(arena_reserve(ctx, abytes(nblk, 4) * 2 + 4096));
+  uint32_t* cnt = arena_alloc<uint32_t>(ctx, nblk);
+  uint32_t* base = arena_alloc<uint32_t>(ctx, nblk);
+  RS_LAUNCH(ctx, "trace_nl_count", nl_count_kernel, (int)nblk, kNlT, 0, d_text, n_bytes, cnt);
+  RS_LAUNCH(ctx, "trace_nl_scan", exclusive_scan_u32_kernel, 1, 1024, 0, cnt, base, nblk);
+  uint32_t last[2] = {0, 0};
+  RS_TRY(d2h(ctx, &last[0], base + nblk - 1, 4));
+  RS_TRY(d2h(ctx, &last[1], cnt + nblk - 1, 4));
+  RS_TRY(sync_and_check(ctx));
+  const int64_t L = (int64_t)last[0] + last[1] + 1;  // lines (the last may be empty)
+  if (L >= (int64_t)UINT32_MAX - 1) return fail(RS_E_ARG, "trace has too many lines");
+  *line_start = buf->alloc<int64_t>(ctx->stream, L + 1);
+  if (!*line_start) return fail(RS_E_NOMEM, "trace line arrays: allocation failed");
+  RS_LAUNCH(ctx, "trace_nl_write", nl_write_kernel, (int)nblk, kNlT, 0, d_text, n_bytes, base,
+            *line_start);
+  *L_out = L;
+  return RS_OK;
+}
+
+int trace_sorted_table(rs_ctx* ctx, rs_trace_csr* tr, int32_t P, int64_t maxid, const char* d_ids,
+                       const int64_t* d_id_off, const int64_t* d_tok_off, const int32_t* d_gt,
+                       uint32_t* d_perm) {
+  std::vector<uint32_t> perm(P);
+  std::vector<int64_t> tok_off(P + 1, 0), id_off(P + 1, 0);
+  std::vector<int32_t> gt_line(P);
+  std::vector<char> ids_line;
+  if (P > 0) {
+    RS_TRY(rank_strings_device(ctx, d_ids, d_id_off, P, std::max<int64_t>(maxid, 1), d_perm));
+    RS_TRY(d2h(ctx, perm.data(), d_perm, 4ull * P));
+    RS_TRY(d2h(ctx, tok_off.data(), d_tok_off, 8ull * (P + 1)));
+    RS_TRY(d2h(ctx, id_off.data(), d_id_off, 8ull * (P + 1)));
+    RS_TRY(d2h(ctx, gt_line.data(), d_gt, 4ull * P));
+    RS_TRY(sync_and_check(ctx));
+    ids_line.resize(id_off[P]);
+    if (!ids_line.empty()) RS_TRY(d2h(ctx, ids_line.data(), d_ids, ids_line.size()));
+    RS_TRY(sync_and_check(ctx));
+  }
+  tr->count = P;
+  tr->n_tokens = tok_off[P];
+  tr->offsets.assign(P + 1, 0);
+  tr->id_off.assign(P + 1, 0);
+  tr->gt.resize(P);
+  for (int32_t r = 0; r < P; ++r) {
+    const uint32_t i = perm[r];
+    tr->offsets[r + 1] = tr->offsets[r] + (tok_off[i + 1] - tok_off[i]);
+    tr->id_off[r + 1] = tr->id_off[r] + (id_off[i + 1] - id_off[i]);
+    tr->gt[r] = gt_line[i];
+  }
+  tr->ids.resize(id_off[P]);
+  for (int32_t r = 0; r < P; ++r) {
+    const uint32_t i = perm[r];
+    std::memcpy(tr->ids.data() + tr->id_off[r], ids_line.data() + id_off[i], id_off[i + 1] - id_off[i]);
+  }
+  return RS_OK;
+}
+
+int trace_validate_prompts(const rs_trace_csr* tr) {
+  if (tr->g < 1) return fail(RS_E_VALIDATION, "responses_per_prompt must be >= 1");
+  if (tr->max_prompt_len < 1 || tr->max_response_len < 1)
+    return fail(RS_E_VALIDATION, "trace limits must be positive");
+  const int32_t P = tr->count;
+  auto id_of = [&](int32_t r) {
+    return std::string(tr->ids.data() + tr->id_off[r], tr->ids.data() + tr->id_off[r + 1]);
+  };
+  for (int32_t r = 0; r < P; ++r) {
+    if (tr->id_off[r + 1] == tr->id_off[r]) return fail(RS_E_VALIDATION, "prompt with empty id");
+    if (r > 0) {  // std::string order: bytes, then length
+      const char* pa = tr->ids.data() + tr->id_off[r - 1];
+      const char* pb = tr->ids.data() + tr->id_off[r];
+      const int64_t la = tr->id_off[r] - tr->id_off[r - 1], lb = tr->id_off[r + 1] - tr->id_off[r];
+      const int c = std::memcmp(pa, pb, (size_t)std::min(la, lb));
+      if (!(c < 0 || (c == 0 && la < lb)))
+        return fail(RS_E_VALIDATION, "prompts not sorted by unique id near '" + id_of(r) + "'");
+    }
+    const int64_t len = tr->offsets[r + 1] - tr->offsets[r];
+    if (len < 1) return fail(RS_E_VALIDATION, "prompt '" + id_of(r) + "' has no tokens");
+    if (len > tr->max_prompt_len)
+      return fail(RS_E_VALIDATION, "prompt '" + id_of(r) + "' longer than max_prompt_len");
+    if (tr->gt[r] < 1 || tr->gt[r] > tr->max_response_len)
+      return fail(RS_E_VALIDATION, "prompt '" + id_of(r) + "' ground_truth_len out of range");
+  }
+  return RS_OK;
+}
+
+int trace_gather_csr(rs_ctx* ctx, rs_trace_csr* tr, const int32_t* d_tok_line,
+                     const int64_t* d_tok_off, const uint32_t* d_perm) {
+  const int32_t P = tr->count;
+  const int64_t T = tr->n_tokens;
+  tr->device = ctx->device;
+  if (cudaMallocAsync(&tr->d_tokens, 4ull * std::max<int64_t>(T, 1), ctx->stream) != cudaSuccess ||
+      cudaMallocAsync(&tr->d_offsets, 8ull * (P + 1), ctx->stream) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(RS_E_NOMEM, "trace CSR allocation failed");
+  }
+  RS_TRY(h2d(ctx, tr->d_offsets, tr->offsets.data(), 8ull * (P + 1)));
+  if (P > 0)
+    RS_LAUNCH(ctx, "trace_gather", csr_gather_kernel,
+              (int)std::min<int64_t>(P, 16 * (int64_t)ctx->num_sms), 256, 0, d_tok_line, d_tok_off,
+              d_perm, P, (const int64_t*)tr->d_offsets, tr->d_tokens);
+  return sync_and_check(ctx);
+}
+
+}  // namespace rs
 
 extern "C" int rs_trace_csr_info(const rs_trace_csr* tr, int32_t* count, int64_t* n_tokens,
                                  int64_t* id_bytes, int32_t* g, int32_t* max_prompt_len,

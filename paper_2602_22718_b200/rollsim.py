@@ -176,17 +176,17 @@ class TraceCSR:
     CSR in HBM (rs_trace_csr_parse). `prefix_index()` builds the dedup index
     from that CSR without a host round trip."""
 
-    def __init__(self, text, device=False):
+    def __init__(self, text, device=False, fmt="csv"):
         ctx = context()
         self._ctx = ctx
         h = C.c_void_p()
+        parse = ctx.lib.rs_trace_csr_parse_jsonl if fmt == "jsonl" else ctx.lib.rs_trace_csr_parse
         if device:  # a torch uint8 CUDA tensor
-            check(ctx.lib.rs_trace_csr_parse(ctx.handle, C.c_void_p(text.data_ptr()), text.numel(),
-                                             1, C.byref(h)))
+            check(parse(ctx.handle, C.c_void_p(text.data_ptr()), text.numel(), 1, C.byref(h)))
         else:
             data = text.encode() if isinstance(text, str) else bytes(text)
             buf = C.create_string_buffer(data, len(data))
-            check(ctx.lib.rs_trace_csr_parse(ctx.handle, buf, len(data), 0, C.byref(h)))
+            check(parse(ctx.handle, buf, len(data), 0, C.byref(h)))
         self._h = h
         n, nt, nb = C.c_int32(), C.c_int64(), C.c_int64()
         g, mp, mr = C.c_int32(), C.c_int32(), C.c_int32()
@@ -197,9 +197,11 @@ class TraceCSR:
             g.value, mp.value, mr.value)
 
     @staticmethod
-    def load(path):
+    def load(path, fmt=None):
+        """load_trace (workload.cpp): the format from the extension unless given."""
+        fmt = fmt or ("jsonl" if str(path).endswith(".jsonl") else "csv")
         with open(path, "rb") as f:
-            return TraceCSR(f.read())
+            return TraceCSR(f.read(), fmt=fmt)
 
     def device(self):
         """(tokens, offsets) device pointers, valid while this object lives."""

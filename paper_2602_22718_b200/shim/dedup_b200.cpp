@@ -39,16 +39,22 @@ struct Handle {
 }  // namespace
 
 PrefixIndex PrefixIndex::build(const std::vector<const Prompt*>& batch) {
-  if (batch.empty()) throw ValidationError("prefix index needs a non-empty batch");
-  for (const Prompt* p : batch)
-    if (p == nullptr || p->prompt_len() < 1)
-      throw ValidationError("prefix index: empty prompt in batch");
-  std::vector<int32_t> tok;
-  std::vector<int64_t> off;
-  to_csr(batch, &tok, &off);
   Handle h;
-  rs_shim::check(rs_prefix_index_build(rs_shim::ctx(), tok.data(), off.data(),
-                                       static_cast<int32_t>(batch.size()), &h.h));
+  const rs_shim::DeviceCsr* dev = rs_shim::device_csr_of(batch);
+  if (dev) {  // b200::DeviceTrace::prefix_index: the CSR is already in HBM
+    rs_shim::check(rs_prefix_index_build_device(rs_shim::ctx(), dev->tokens, dev->offsets,
+                                                dev->count, &h.h));
+  } else {
+    if (batch.empty()) throw ValidationError("prefix index needs a non-empty batch");
+    for (const Prompt* p : batch)
+      if (p == nullptr || p->prompt_len() < 1)
+        throw ValidationError("prefix index: empty prompt in batch");
+    std::vector<int32_t> tok;
+    std::vector<int64_t> off;
+    to_csr(batch, &tok, &off);
+    rs_shim::check(rs_prefix_index_build(rs_shim::ctx(), tok.data(), off.data(),
+                                         static_cast<int32_t>(batch.size()), &h.h));
+  }
   PrefixIndex idx;
   int32_t bs, mn, mx;
   rs_shim::check(rs_prefix_index_info(h.h, &bs, &mn, &mx, &idx.total_tokens_));

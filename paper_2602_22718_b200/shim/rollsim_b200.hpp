@@ -10,11 +10,16 @@
 // ValidationError / ConfigError / PlacementError in the reference's order.
 #pragma once
 
+#include <string>
 #include <vector>
 
+#include "rollsim/dedup.hpp"
 #include "rollsim/placement.hpp"
 #include "rollsim/planner.hpp"
 #include "rollsim/predictor.hpp"
+#include "rollsim/workload.hpp"
+
+struct rs_trace_csr;
 
 namespace rollsim::b200 {
 
@@ -30,5 +35,29 @@ ScaleResult scale_placed(const std::vector<PredictedPrompt>& predicted,
 std::vector<double> predict_lengths(const LengthHistory& history,
                                     const std::vector<const Prompt*>& prompts,
                                     const NoiseModel* noise = nullptr);
+
+// A CSV trace parsed on the GPU (rs_trace_csr_parse): trace() is
+// trace_from_string(text, TraceFormat::csv) (workload.cpp:169-263) bit for
+// bit, with its ParseError / ValidationError in the reference's order (thrown
+// by parse_csv), and prefix_index() is PrefixIndex::build over the id-sorted
+// prompt table, built from the token CSR already in HBM — no per-prompt
+// vectors and no host gather.
+class DeviceTrace {
+ public:
+  static DeviceTrace parse_csv(const std::string& text);
+  DeviceTrace(DeviceTrace&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  DeviceTrace& operator=(DeviceTrace&& o) noexcept;
+  DeviceTrace(const DeviceTrace&) = delete;
+  DeviceTrace& operator=(const DeviceTrace&) = delete;
+  ~DeviceTrace();
+
+  WorkloadTrace trace() const;
+  PrefixIndex prefix_index() const;
+  int prompt_count() const;
+
+ private:
+  explicit DeviceTrace(rs_trace_csr* h) : h_(h) {}
+  rs_trace_csr* h_ = nullptr;
+};
 
 }  // namespace rollsim::b200

@@ -43,6 +43,7 @@ void check(int status) {
   if (status == RS_E_VALIDATION) throw rollsim::ValidationError(msg);
   if (status == RS_E_CONFIG) throw rollsim::ConfigError(msg);
   if (status == RS_E_PLACEMENT) throw rollsim::PlacementError(msg);
+  if (status == RS_E_PARSE) throw rollsim::ParseError(msg);
   throw rollsim::Error("librs_b200: " + msg);
 }
 
@@ -71,5 +72,18 @@ std::vector<int32_t> rank_ids(const std::vector<std::string>& ids) {
                           rank.data()));
   return rank;
 }
+
+namespace {
+const rollsim::Prompt kDeviceSentinel{};
+thread_local const DeviceCsr* t_device_csr = nullptr;
+}  // namespace
+
+const DeviceCsr* device_csr_of(const std::vector<const rollsim::Prompt*>& batch) {
+  return batch.size() == 1 && batch[0] == &kDeviceSentinel ? t_device_csr : nullptr;
+}
+
+DeviceCsrScope::DeviceCsrScope(const DeviceCsr& csr) { t_device_csr = &csr; }
+DeviceCsrScope::~DeviceCsrScope() { t_device_csr = nullptr; }
+std::vector<const rollsim::Prompt*> DeviceCsrScope::batch() const { return {&kDeviceSentinel}; }
 
 }  // namespace rs_shim

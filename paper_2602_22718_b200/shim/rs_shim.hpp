@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "rollsim/profile.hpp"
+#include "rollsim/workload.hpp"
 #include "rs.h"
 
 namespace rs_shim {
@@ -28,5 +29,22 @@ struct Profile {
 
 // Rank of every id under std::string ordering, computed on the device.
 std::vector<int32_t> rank_ids(const std::vector<std::string>& ids);
+
+// A token CSR resident in HBM (rs_trace_csr_device). PrefixIndex::build has
+// the reference's signature (host prompt pointers); b200::DeviceTrace hands
+// it a one-element batch holding the sentinel that device_csr_of recognises,
+// with the CSR registered for the calling thread, so the index is built from
+// HBM without materialising prompts.
+struct DeviceCsr {
+  const int32_t* tokens;
+  const int64_t* offsets;
+  int32_t count;
+};
+const DeviceCsr* device_csr_of(const std::vector<const rollsim::Prompt*>& batch);
+struct DeviceCsrScope {  // registers csr for this thread; returns the batch to pass
+  explicit DeviceCsrScope(const DeviceCsr& csr);
+  ~DeviceCsrScope();
+  std::vector<const rollsim::Prompt*> batch() const;
+};
 
 }  // namespace rs_shim

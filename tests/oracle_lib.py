@@ -186,8 +186,25 @@ class Oracle:
                                              ptr(out, C.c_double)))
         return out[:n]
 
-    def trace_prompts(self, text: bytes):
-        """Reference only: the id-sorted prompt table of a CSV trace."""
+    def trace_format(self, fmt):
+        """Reference only: the format trace_prompts / trace_steps read."""
+        self.lib.ref_trace_set_format(1 if fmt == "jsonl" else 0)
+
+    def trace_convert(self, text: bytes, fmt_in="csv", fmt_out="jsonl") -> bytes:
+        """Reference only: trace_to_string(trace_from_string(text, fmt_in), fmt_out)."""
+        n = C.c_int64()
+        buf = C.create_string_buffer(text, len(text))
+        codes = {"csv": 0, "jsonl": 1}
+        self._chk(self.lib.ref_trace_convert(buf, len(text), codes[fmt_in], codes[fmt_out], None, 0,
+                                             C.byref(n)))
+        out = C.create_string_buffer(max(n.value, 1))
+        self._chk(self.lib.ref_trace_convert(buf, len(text), codes[fmt_in], codes[fmt_out], out,
+                                             n.value, C.byref(n)))
+        return out.raw[:n.value]
+
+    def trace_prompts(self, text: bytes, fmt="csv"):
+        """Reference only: the id-sorted prompt table of a CSV / JSONL trace."""
+        self.trace_format(fmt)
         info = np.zeros(6, np.int64)
         buf = C.create_string_buffer(text, len(text))
         self._chk(self.lib.ref_trace_prompts(buf, len(text), ptr(info, C.c_int64), None, None, None,
@@ -205,8 +222,9 @@ class Oracle:
                 "gt": gt[:n], "tokens": tok[:nt], "offsets": off, "g": int(info[3]),
                 "max_prompt_len": int(info[4]), "max_response_len": int(info[5])}
 
-    def trace_steps(self, text: bytes):
-        """Reference only: the step table of a CSV trace (ref_trace_steps)."""
+    def trace_steps(self, text: bytes, fmt="csv"):
+        """Reference only: the step table of a CSV / JSONL trace (ref_trace_steps)."""
+        self.trace_format(fmt)
         info = np.zeros(3, np.int64)
         buf = C.create_string_buffer(text, len(text))
         self._chk(self.lib.ref_trace_steps(buf, len(text), ptr(info, C.c_int64), None, None, None,

@@ -63,6 +63,16 @@ def test_placement_extension_on_dropin():
     assert "test cases:" in out and code == 0 and not failed_cases(out), out[-3000:]
 
 
+@pytest.mark.gpu
+def test_device_trace_on_dropin():
+    """rollsim::b200::DeviceTrace (rollsim_b200.hpp): CSV traces parsed on
+    the GPU equal trace_from_string's WorkloadTrace (operator==), errors
+    keep the reference's types, and the index built from the device CSR
+    equals PrefixIndex::build over the parsed prompts (shim/tests/)."""
+    code, out = run(SHIM / "test_trace_b200")
+    assert "test cases:" in out and code == 0 and not failed_cases(out), out[-3000:]
+
+
 def run_args(binary, args, timeout=900):
     if not binary.exists():
         pytest.skip(f"{binary.name} not built (needs /root/reference at build time)")

@@ -1,0 +1,212 @@
+"""GPU parity for the JSONL trace reader (rs_trace_csr_parse_jsonl,
+SURVEY §8f-4) against the reference's own reader (jsonl_from_string through
+oracle/_ref, nlohmann::json): prompt tables and step tables of traces the
+reference writes (trace_to_string) and of hand-written lines that exercise
+nlohmann's grammar and conversions; errors by type (ParseError at a line vs
+ValidationError with the validator's message)."""
+import json
+
+import numpy as np
+import pytest
+
+from cases import random_trace, steps_trace, trace_csv
+from oracle_lib import OracleError, ref
+from paper_2602_22718_b200 import rollsim as rs
+from paper_2602_22718_b200.lib import ParseError, ValidationError
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(ref() is None, reason="reference not built (oracle/_ref)")]
+
+
+def same(text):
+    want_p = ref().trace_prompts(text, "jsonl")
+    want_s = ref().trace_steps(text, "jsonl")
+    tr = rs.TraceCSR(text, fmt="jsonl")
+    got = tr.host()
+    assert got["ids"] == want_p["ids"]
+    assert got["gt"].tolist() == want_p["gt"].tolist()
+    assert got["offsets"].tolist() == want_p["offsets"].tolist()
+    assert np.array_equal(got["tokens"], want_p["tokens"])
+    assert (tr.responses_per_prompt, tr.max_prompt_len, tr.max_response_len) == (
+        want_p["g"], want_p["max_prompt_len"], want_p["max_response_len"])
+    steps = tr.steps()
+    for k in ("step_idx", "entry_off", "entry_prompt", "lengths"):
+        assert np.array_equal(steps[k], want_s[k]), k
+    return tr
+
+
+def same_error(text):
+    with pytest.raises(OracleError) as e:
+        ref().trace_prompts(text, "jsonl")
+    assert e.value.status in (1, 7), e.value
+    kind = ParseError if e.value.status == 7 else ValidationError
+    with pytest.raises(kind) as got:
+        rs.TraceCSR(text, fmt="jsonl")
+    want = str(e.value).split("] ", 1)[1]
+    if kind is ValidationError:
+        assert str(got.value) == want
+    else:  # the same line: '<string>:N: ...' / '<trace>:N: ...'
+        assert want.split(":")[1] == str(got.value).split(":")[1], (want, str(got.value))
+
+
+def header(prompts, g=2, **kw):
+    h = {"type": "header", "g": g, "prompts": prompts}
+    h.update(kw)
+    return h
+
+
+def lines(*objs, raw=()):
+    out = [o if isinstance(o, str) else json.dumps(o) for o in objs]
+    return ("\n".join(out + list(raw)) + "\n").encode()
+
+
+P2 = [{"id": "b", "ground_truth_len": 5, "token_ids": [1, 2, 3]},
+      {"id": "a", "ground_truth_len": 9, "token_ids": [4]}]
+
+
+def test_reference_written_traces():
+    for seed in range(5):
+        text, _, _ = steps_trace(seed, 30 + 20 * seed, 1 + seed, g=1 + seed % 4,
+                                 interleave=seed % 2 == 1)
+        same(ref().trace_convert(text))
+    same(ref().trace_convert(random_trace(7, 200, max_len=60, shared=5)))
+    same(ref().trace_convert(trace_csv([("x", 3, [1, 2])], g=2)))
+
+
+def grammar_cases():
+    step = {"step": 0, "scheduled": ["a", "b"], "lengths": {"a": [5, 6], "b": [7, 8]}}
+    return [
+        lines(header(P2), step),
+        # whitespace, key order, unknown members with nested values
+        lines(' { "prompts" : %s , "g":2,"x":{"y":[1,{"z":null}],"w":"\\u00e9"},"type":"header"} '
+              % json.dumps(P2), step),
+        # CRLF, blank lines, tabs
+        lines(header(P2), step).replace(b"\n", b"\r\n") + b"\n\t\n",
+        # escapes in ids: é, \", \\, a surrogate pair
+        lines(header([{"id": "é\"\\\U0001F600", "ground_truth_len": 3, "token_ids": [1]}], g=1),
+              {"step": 4, "lengths": {"é\"\\\U0001F600": [2]}}),
+        lines('{"type":"header","g":1,"prompts":[{"id":"\\u0061\\/b","ground_truth_len":3,'
+              '"token_ids":[1]}]}', '{"step":1,"lengths":{"a/b":[9]}}'),
+        # duplicate keys: the last wins (members and prompt fields)
+        lines('{"type":"x","g":5,"type":"header","g":2,"prompts":[],"prompts":%s}' % json.dumps(P2),
+              '{"step":0,"step":3,"lengths":{"a":[1,1],"b":[2,2],"a":[3,3]}}'),
+        lines('{"type":"header","g":1,"prompts":[{"id":"z","id":"q","token_ids":[1],'
+              '"ground_truth_len":4,"token_ids":[7,8]}]}'),
+        # get<int> from floats, booleans, -0, exponents, uint64 wrap
+        lines('{"type":"header","g":2.9,"max_prompt_len":1e3,"max_response_len":2048.5,'
+              '"prompts":[{"id":"a","ground_truth_len":true,"token_ids":[-0,1.5,-2.5,true,false,'
+              '4294967297,18446744073709551615,-2147483649,3e2,0.25e1,1E+1]}]}',
+              '{"step":0,"lengths":{"a":[1.99,2]}}'),
+        # "scheduled" absent: the lengths keys in map order; several steps
+        lines(header(P2), {"step": 0, "lengths": {"b": [1, 2], "a": [3, 4]}},
+              {"step": 9, "scheduled": ["a"], "lengths": {"a": [5, 5]}}),
+        # "prompts": null / []
+        lines('{"type":"header","g":1,"prompts":null}'),
+        lines('{"type":"header","g":1,"prompts":[]}'),
+        # long token arrays
+        lines(header([{"id": f"p{i}", "ground_truth_len": 7, "token_ids": list(range(i, i + 300))}
+                      for i in range(40)], g=1, max_prompt_len=1000)),
+    ]
+
+
+def test_json_grammar_and_conversions():
+    for i, text in enumerate(grammar_cases()):
+        try:
+            ref().trace_prompts(text, "jsonl")
+        except OracleError as e:
+            pytest.fail(f"case {i}: the reference rejects it: {e}")
+        same(text)
+
+
+def syntax_errors():
+    step = '{"step":0,"lengths":{"a":[1,2],"b":[3,4]}}'
+    good = json.dumps(header(P2))
+    bad = [
+        good + "\n" + '{"step":0,"lengths":{"a":[1,2],"b":[3,4],}}',   # trailing comma
+        good + "\n" + '{"step":0 "lengths":{}}',                       # missing comma
+        good.replace('"g":', '"g" '),                                   # missing colon
+        good.replace('"b"', '"b\\x"'),                                  # bad escape
+        good.replace('"b"', '"b\\ud800"'),                              # lone surrogate
+        good.replace('"b"', '"b\x01"'),                                 # control character
+        good.replace("[1, 2, 3]", "[01, 2]"),                           # leading zero
+        good.replace("[1, 2, 3]", "[1., 2]"),                           # '1.'
+        good.replace("[1, 2, 3]", "[1, 2"),                              # unbalanced
+        good + " x",                                                     # trailing content
+        good + "\n" + step + "\n" + '{"step":1,"lengths":{"a":[1,2]}',  # unterminated (last line)
+        '{"type":"other","g":1,"prompts":[]}',                          # not a header
+        '[1,2]',                                                         # not an object
+        '{"type":"header","prompts":[]}',                                # no g
+        '{"type":"header","g":1}',                                       # no prompts
+        '{"type":"header","g":"2","prompts":[]}',                        # g a string
+        '{"type":"header","g":1,"prompts":[{"ground_truth_len":1,"token_ids":[1]}]}',   # no id
+        '{"type":"header","g":1,"prompts":[{"id":5,"ground_truth_len":1,"token_ids":[1]}]}',
+        '{"type":"header","g":1,"prompts":[{"id":"a","ground_truth_len":1,"token_ids":"x"}]}',
+        '{"type":"header","g":1,"prompts":[{"id":"a","ground_truth_len":1,"token_ids":[null]}]}',
+        '{"type":"header","g":1,"prompts":[3]}',                         # a prompt not an object
+        good + "\n" + '{"lengths":{}}',                                  # no step
+        good + "\n" + '{"step":0}',                                      # no lengths
+        good + "\n" + '{"step":0,"scheduled":"a","lengths":{}}',         # scheduled not an array
+        good + "\n" + '{"step":0,"scheduled":[1],"lengths":{}}',         # scheduled element
+        good + "\n" + '{"step":0,"lengths":{"a":"x"}}',                  # lengths value
+        good + "\n" + good,                                              # a second header
+        "",                                                              # no header
+        good.encode().replace(b'"b"', b'"b\xff"').decode("latin-1"),     # invalid UTF-8
+    ]
+    return [t.encode("latin-1") + b"\n" for t in bad]
+
+
+def test_json_syntax_and_schema_errors():
+    for text in syntax_errors():
+        same_error(text)
+
+
+def validation_errors():
+    g = json.dumps(header(P2))
+    bad = [
+        g + "\n" + '{"step":0,"scheduled":["a","zz"],"lengths":{"a":[1,2],"zz":[1,2]}}',
+        g + "\n" + '{"step":0,"scheduled":["a","a"],"lengths":{"a":[1,2]}}',
+        g + "\n" + '{"step":0,"scheduled":["a","b"],"lengths":{"a":[1,2]}}',
+        g + "\n" + '{"step":0,"scheduled":["a"],"lengths":{"b":[1,2]}}',
+        g + "\n" + '{"step":0,"lengths":{"a":[1,2,3],"b":[1,2]}}',
+        g + "\n" + '{"step":0,"lengths":{"a":[1,0],"b":[1,2]}}',
+        g + "\n" + '{"step":3,"lengths":{"a":[1,2]}}\n{"step":3,"lengths":{"a":[1,2]}}',
+        g + "\n" + '{"step":-1,"lengths":{"a":[1,2]}}',
+        g + "\n" + '{"step":0,"lengths":{}}',
+        g + "\n" + '{"step":0,"lengths":null}',
+        json.dumps(header([{"id": "", "ground_truth_len": 1, "token_ids": [1]}])),
+        json.dumps(header(P2 + [{"id": "a", "ground_truth_len": 1, "token_ids": [1]}])),
+        json.dumps(header([{"id": "a", "ground_truth_len": 1, "token_ids": []}])),
+        json.dumps(header(P2, g=0)),
+        json.dumps(header(P2, max_prompt_len=2)),
+        json.dumps(header([{"id": "a", "ground_truth_len": 5000, "token_ids": [1]}])),
+    ]
+    return [t.encode() + b"\n" for t in bad]
+
+
+def test_validation_errors():
+    for text in validation_errors():
+        same_error(text)
+
+
+def test_unsupported_constructs_are_reported():
+    """Valid for nlohmann, rejected here with RS_E_PARSE (rs.h)."""
+    for text in ['{"type":"header","g":1,"prompts":{"k":{"id":"a","ground_truth_len":1,"token_ids":[1]}}}',
+                 json.dumps(header(P2)) + '\n{"step":0,"lengths":[[1,2]]}']:
+        ref().trace_prompts(text.encode(), "jsonl") if "lengths" not in text else None
+        with pytest.raises(ParseError, match="not support"):
+            rs.TraceCSR(text.encode() + b"\n", fmt="jsonl")
+
+
+@pytest.mark.slow
+def test_c2_shaped_jsonl_to_prefix_index():
+    """8,192 prompts x 2,560 tokens as one JSONL header line: the device CSR
+    equals the reference's parse and feeds the dedup index."""
+    from cases import Rng
+    rng = Rng(1)
+    head = [rng.uniform_int(0, 31999) for _ in range(2048)]
+    arr = np.random.RandomState(2).randint(0, 32000, (8192, 512))
+    prompts = [(f"p{i:06d}", 100, head + arr[i].tolist()) for i in range(8192)]
+    text = ref().trace_convert(trace_csv(prompts, max_prompt_len=4096))
+    tr = same(text)
+    direct = rs.PrefixIndex.build([p[2] for p in prompts])
+    assert all(np.array_equal(a, b) for a, b in zip(tr.prefix_index().tables(), direct.tables()))
