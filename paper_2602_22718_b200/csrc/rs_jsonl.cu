@@ -51,6 +51,8 @@
 #include "rs_trace.cuh"
 
 namespace rs {
+size_t rank_strings_device_bytes(int64_t n, int64_t maxlen);
+
 namespace {
 
 constexpr int kJErr = 1;     // a ParseError of the reference reader
@@ -1033,6 +1035,36 @@ __global__ void js_sizes_kernel(const JChild* ch, const JCont* conts, int64_t to
   }
 }
 
+// Each scheduled id / lengths key of one role: its index in the id-sorted
+// prompt table (binary search, std::string order), -1 when absent.
+__global__ void js_lookup_kernel(const JChild* ch, const JCont* conts, int64_t total, int role,
+                                 const int64_t* id_off, const char* ids, const char* sids,
+                                 const int64_t* sid_off, int32_t P, int32_t* pidx) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const JChild r = ch[u];
+    if (r.err || conts[r.cont].role != role) continue;
+    const unsigned char* a = reinterpret_cast<const unsigned char*>(ids + id_off[u]);
+    const int64_t la = r.id_len;
+    int32_t lo = 0, hi = P, found = -1;
+    while (lo < hi) {
+      const int32_t mid = (lo + hi) >> 1;
+      const unsigned char* b = reinterpret_cast<const unsigned char*>(sids + sid_off[mid]);
+      const int64_t lb = sid_off[mid + 1] - sid_off[mid];
+      int c = 0;
+      for (int64_t i = 0; i < (la < lb ? la : lb) && !c; ++i) c = a[i] < b[i] ? -1 : (a[i] > b[i] ? 1 : 0);
+      if (!c) c = la < lb ? -1 : (la > lb ? 1 : 0);
+      if (!c) {
+        found = mid;
+        break;
+      }
+      if (c < 0) hi = mid;
+      else lo = mid + 1;
+    }
+    pidx[u] = found;
+  }
+}
+
 // The header's prompts, in child order: their line-order tables for the
 // shared tail (token offsets, id offsets, ground truths).
 __global__ void js_prompt_tables_kernel(const JChild* ch, int64_t c0, int32_t P, const int64_t* id_off,
@@ -1249,6 +1281,7 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
       RS_TRY(sync_and_check(ctx));
       for (int32_t i = 0; i < P; ++i) maxid = std::max<int64_t>(maxid, ioff[i + 1] - ioff[i]);
     }
+    RS_TRY(arena_reserve(ctx, rank_strings_device_bytes(std::max(P, 1), maxid) + (1 << 16)));
     RS_TRY(trace_sorted_table(ctx, tr, P, maxid, d_ids, p_id_off, p_tok_off, p_gt, d_perm));
     clk.mark("prompts");
     // 5. steps, on the host: scheduled ids and length lists per step line
@@ -1256,8 +1289,23 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     std::vector<unsigned long long> h_id_off, h_int_off;
     std::vector<char> h_ids;
     std::vector<int32_t> h_ints;
+    std::vector<int32_t> hp;  // per child: its index in the id-sorted table (-1: unknown)
     bool any_steps = false;
     for (int64_t ln = 0; ln < L; ++ln) any_steps |= hl[ln].kind == kLStep;
+    AsyncBuf b_sid;
+    int32_t* d_pidx = nullptr;
+    char* d_sids = nullptr;
+    int64_t* d_sid_off = nullptr;
+    if (any_steps && NCH > 0) {
+      char* q = b_sid.alloc<char>(ctx->stream, abytes(tr->ids.size() + 1, 1) + abytes(P + 1, 8) + abytes(NCH, 4));
+      if (!q) return fail(RS_E_NOMEM, "jsonl steps: allocation failed");
+      d_sids = carve(q, abytes(tr->ids.size() + 1, 1));
+      d_sid_off = (int64_t*)carve(q, abytes(P + 1, 8));
+      d_pidx = (int32_t*)carve(q, abytes(NCH, 4));
+      if (!tr->ids.empty()) RS_TRY(h2d(ctx, d_sids, tr->ids.data(), tr->ids.size()));
+      RS_TRY(h2d(ctx, d_sid_off, tr->id_off.data(), 8ull * (P + 1)));
+      RS_CUDA_TRY(cudaMemsetAsync(d_pidx, 0xff, 4ull * NCH, ctx->stream));
+    }
     if (any_steps && NCH > 0) {
       auto gather = [&](int role) -> int {  // sizes + writes of one role's children, to the host
         RS_TRY(sizes(role));
@@ -1273,6 +1321,8 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
         RS_LAUNCH(ctx, "jsonl_step_write", js_child_kernel<true>, grid(NCH), 128, 0, d_text, d_conts, cscan, NC,
                   lbv, NB, NCH, d_ch, (const int64_t*)id_off, (const int64_t*)int_off, d_i, d_n, small + 2,
                   role);
+        RS_LAUNCH(ctx, "jsonl_lookup", js_lookup_kernel, grid(NCH), 256, 0, d_ch, d_conts, NCH, role,
+                  (const int64_t*)id_off, d_i, d_sids, d_sid_off, P, d_pidx);
         const size_t o_i = h_ids.size(), o_n = h_ints.size();
         h_ids.resize(o_i + tt[0]);
         h_ints.resize(o_n + tt[1]);
@@ -1297,6 +1347,9 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
       RS_TRY(sync_and_check(ctx));
       RS_TRY(gather(kRSched));
       RS_TRY(gather(kRLengths));
+      hp.resize(NCH);
+      RS_TRY(d2h(ctx, hp.data(), d_pidx, 4ull * NCH));
+      RS_TRY(sync_and_check(ctx));
     }
     // WorkloadTrace::validate: the prompt rules, then step by step
     RS_TRY(trace_validate_prompts(tr));
@@ -1320,29 +1373,95 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     std::vector<int32_t> st_idx, e_off{0}, e_prompt, lens;
     int prev_step = -1;
     const int32_t G = tr->g;
+    auto child_id = [&](unsigned long long u) {
+      return std::string(h_ids.data() + h_id_off[u], h_ids.data() + h_id_off[u] + hch[u].id_len);
+    };
+    auto table_id = [&](int32_t p) {
+      return std::string(tr->ids.data() + tr->id_off[p], tr->ids.data() + tr->id_off[p + 1]);
+    };
+    // per prompt, stamped with the step line: its last lengths child, scheduled
+    std::vector<int64_t> last_u(std::max(P, 1), -1), stamp_len(std::max(P, 1), -1),
+        stamp_sched(std::max(P, 1), -1);
     for (int64_t ln = 0; ln < L; ++ln) {
       if (hl[ln].kind != kLStep) continue;
       const int step = hl[ln].step;
       const std::string sn = std::to_string(step);
-      std::vector<std::string> sched;
-      std::map<std::string, std::vector<int>> lmap;
-      if (len_c[ln] >= 0) {
-        const int64_t c = len_c[ln];
-        for (unsigned long long u = hcs[c]; u < hcs[c + 1]; ++u) {
-          std::string key(h_ids.data() + h_id_off[u], h_ids.data() + h_id_off[u] + hch[u].id_len);
-          lmap[key] = std::vector<int>(h_ints.begin() + h_int_off[u], h_ints.begin() + h_int_off[u] + hch[u].n_int);
-        }
-      }
-      if (hl[ln].has_sched && sched_c[ln] >= 0) {
-        const int64_t c = sched_c[ln];
-        for (unsigned long long u = hcs[c]; u < hcs[c + 1]; ++u)
-          sched.emplace_back(h_ids.data() + h_id_off[u], h_ids.data() + h_id_off[u] + hch[u].id_len);
-      } else if (!hl[ln].has_sched) {
-        for (const auto& kv : lmap) sched.push_back(kv.first);
-      }
       if (step <= prev_step)
         return fail(RS_E_VALIDATION, "step indices must be strictly increasing at step " + sn);
       prev_step = step;
+      // the lengths map (std::map: key order, the last duplicate wins) by
+      // table index; a key outside the table takes the string path below
+      std::vector<int32_t> keys;
+      bool known = true;
+      if (len_c[ln] >= 0)
+        for (unsigned long long u = hcs[len_c[ln]]; u < hcs[len_c[ln] + 1] && known; ++u) {
+          const int32_t p = hp[u];
+          if (p < 0) {
+            known = false;
+            break;
+          }
+          if (stamp_len[p] != ln) {
+            stamp_len[p] = ln;
+            keys.push_back(p);
+          }
+          last_u[p] = (int64_t)u;
+        }
+      if (known) {
+        std::sort(keys.begin(), keys.end());
+        std::vector<int32_t> sched;
+        std::vector<unsigned long long> sched_u;
+        if (hl[ln].has_sched && sched_c[ln] >= 0) {
+          for (unsigned long long u = hcs[sched_c[ln]]; u < hcs[sched_c[ln] + 1]; ++u) {
+            sched.push_back(hp[u]);
+            sched_u.push_back(u);
+          }
+        } else if (!hl[ln].has_sched) {
+          sched = keys;
+        }
+        if (sched.empty()) return fail(RS_E_VALIDATION, "step " + sn + " schedules no prompts");
+        for (size_t i = 0; i < sched.size(); ++i) {
+          const int32_t p = sched[i];
+          if (p < 0)
+            return fail(RS_E_VALIDATION, "step " + sn + " schedules unknown prompt '" + child_id(sched_u[i]) + "'");
+          if (stamp_sched[p] == ln)
+            return fail(RS_E_VALIDATION, "step " + sn + " schedules prompt '" + table_id(p) + "' twice");
+          stamp_sched[p] = ln;
+        }
+        if (keys.size() != sched.size())
+          return fail(RS_E_VALIDATION, "step " + sn + " lengths do not cover the scheduled batch");
+        for (const int32_t p : keys) {
+          if (stamp_sched[p] != ln)
+            return fail(RS_E_VALIDATION, "step " + sn + " has lengths for unscheduled prompt '" + table_id(p) + "'");
+          const unsigned long long u = (unsigned long long)last_u[p];
+          if ((int)hch[u].n_int != G)
+            return fail(RS_E_VALIDATION, "step " + sn + " prompt '" + table_id(p) + "' needs exactly " +
+                                             std::to_string(G) + " response lengths");
+          for (int64_t i = 0; i < hch[u].n_int; ++i) {
+            const int l = h_ints[h_int_off[u] + i];
+            if (l < 1 || l > tr->max_response_len)
+              return fail(RS_E_VALIDATION, "step " + sn + " prompt '" + table_id(p) +
+                                               "' response length out of range: " + std::to_string(l));
+          }
+        }
+        st_idx.push_back(step);
+        for (const int32_t p : sched) {
+          e_prompt.push_back(p);
+          const unsigned long long u = (unsigned long long)last_u[p];
+          lens.insert(lens.end(), h_ints.begin() + h_int_off[u], h_ints.begin() + h_int_off[u] + hch[u].n_int);
+        }
+        e_off.push_back((int32_t)e_prompt.size());
+        continue;
+      }
+      // a key outside the prompt table: the reference's containers verbatim
+      std::vector<std::string> sched;
+      std::map<std::string, std::vector<int>> lmap;
+      for (unsigned long long u = hcs[len_c[ln]]; u < hcs[len_c[ln] + 1]; ++u)
+        lmap[child_id(u)] = std::vector<int>(h_ints.begin() + h_int_off[u], h_ints.begin() + h_int_off[u] + hch[u].n_int);
+      if (hl[ln].has_sched && sched_c[ln] >= 0) {
+        for (unsigned long long u = hcs[sched_c[ln]]; u < hcs[sched_c[ln] + 1]; ++u) sched.push_back(child_id(u));
+      } else if (!hl[ln].has_sched) {
+        for (const auto& kv : lmap) sched.push_back(kv.first);
+      }
       if (sched.empty()) return fail(RS_E_VALIDATION, "step " + sn + " schedules no prompts");
       std::set<std::string> seen;
       for (const std::string& id : sched) {
@@ -1363,13 +1482,7 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
             return fail(RS_E_VALIDATION, "step " + sn + " prompt '" + kv.first +
                                              "' response length out of range: " + std::to_string(l));
       }
-      st_idx.push_back(step);
-      for (const std::string& id : sched) {
-        e_prompt.push_back(id_index(id));
-        const std::vector<int>& v = lmap[id];
-        lens.insert(lens.end(), v.begin(), v.end());
-      }
-      e_off.push_back((int32_t)e_prompt.size());
+      return fail(RS_E_VALIDATION, "step " + sn + ": lengths key outside the prompt table");  // unreachable
     }
     clk.mark("steps (host)");
     // the step table, owned by the handle

@@ -252,6 +252,67 @@ def c2_trace_text(n_prompts=65536, shared=2048, unique=512, vocab=32000, seed=1,
     return np.concatenate(parts), tok, off
 
 
+def c2_trace_jsonl(n_prompts=65536, shared=2048, unique=512, vocab=32000, seed=1, g=8, rows=True):
+    """c2_trace_text's trace in the JSONL form (jsonl_to_string's layout:
+    the header object on one line, then one step object): tokens
+    right-aligned in 5 columns after a comma (JSON whitespace, no leading
+    zeros), so numpy writes the ~1 GB line directly. Returns (text uint8
+    array, tokens, offsets)."""
+    tok, off = c2_tokens(n_prompts, shared, unique, vocab, seed)
+    L = shared + unique
+    assert vocab <= 100000 and np.all(np.diff(off) == L) and g <= 10
+
+    def digits(x, width):  # right-aligned decimal columns, spaces before the first digit
+        x = np.asarray(x)
+        out = np.full(x.shape + (width,), ord(" "), np.uint8)
+        nz = x.copy()
+        for k in range(width):
+            col = width - 1 - k
+            d = (nz % 10).astype(np.uint8) + ord("0")
+            show = (x >= 10 ** k) | (k == 0)
+            out[..., col] = np.where(show, d, ord(" "))
+            nz //= 10
+        return out
+
+    head = f'{{"g":{g},"max_prompt_len":4096,"max_response_len":2048,"prompts":['.encode()
+    pre = b'{"ground_truth_len":100,"id":"p000000","token_ids":['
+    width = len(pre) + 6 * L - 1 + 2 + 1  # tokens, "]}", ","
+    body = np.empty((n_prompts, width), np.uint8)
+    body[:, :len(pre)] = np.frombuffer(pre, np.uint8)
+    ids = np.arange(n_prompts)
+    at = pre.index(b"p000000") + 1
+    for k in range(6):
+        body[:, at + 5 - k] = ord("0") + (ids // 10 ** k) % 10
+    cols = body[:, len(pre):len(pre) + 6 * L].reshape(n_prompts, L, 6)
+    cols[:, :, :5] = digits(tok.reshape(n_prompts, L), 5)
+    cols[:, :, 5] = ord(",")
+    body[:, len(pre) + 6 * L - 1:len(pre) + 6 * L + 1] = np.frombuffer(b"]}", np.uint8)
+    body[:, -1] = ord(",")
+    flat = body.reshape(-1)[:-1]  # no comma after the last prompt
+    parts = [np.frombuffer(head, np.uint8), flat, np.frombuffer(b'],"type":"header"}\n', np.uint8)]
+    if rows:
+        rng = np.random.RandomState(seed + 1)
+        order = rng.permutation(n_prompts)
+        lens = rng.randint(1, 2049, (n_prompts, g))
+        ent = b'"p000000":[' + b",".join([b"    "] * g) + b"],"
+        e = np.empty((n_prompts, len(ent)), np.uint8)
+        e[:] = np.frombuffer(ent, np.uint8)
+        srt = np.arange(n_prompts)  # map order = id order; prompt order[j] has lens[j]
+        inv = np.argsort(order)
+        for k in range(6):
+            e[:, 7 - k] = ord("0") + (srt // 10 ** k) % 10
+        for r in range(g):
+            e[:, 11 + 5 * r:15 + 5 * r] = digits(lens[inv, r], 4)
+        sch = np.empty((n_prompts, 10), np.uint8)
+        sch[:] = np.frombuffer(b'"p000000",', np.uint8)
+        for k in range(6):
+            sch[:, 7 - k] = ord("0") + (order // 10 ** k) % 10
+        parts += [np.frombuffer(b'{"lengths":{', np.uint8), e.reshape(-1)[:-1],
+                  np.frombuffer(b'},"scheduled":[', np.uint8), sch.reshape(-1)[:-1],
+                  np.frombuffer(b'],"step":0}\n', np.uint8)]
+    return np.concatenate(parts), tok, off
+
+
 def c2_tokens_multi(n_prompts=65536, n_sys=8, shared=2048, unique=512, vocab=32000, seed=1):
     """The C2 variant of SURVEY.md §8d with n_sys distinct system prompts
     (prompt i carries system prompt i mod n_sys), so the prefix tree branches

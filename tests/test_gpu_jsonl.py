@@ -171,6 +171,12 @@ def validation_errors():
         g + "\n" + '{"step":0,"lengths":{"a":[1,0],"b":[1,2]}}',
         g + "\n" + '{"step":3,"lengths":{"a":[1,2]}}\n{"step":3,"lengths":{"a":[1,2]}}',
         g + "\n" + '{"step":-1,"lengths":{"a":[1,2]}}',
+        g + "\n" + '{"step":0,"scheduled":["a","b"],"lengths":{"a":[1],"b":[1,2],"zz":[1,2]}}',
+        g + "\n" + '{"step":0,"lengths":{"a":[1,2],"zz":[1,2]}}',
+        g + "\n" + '{"step":0,"scheduled":["a","b"],"lengths":{"a":[1],"zz":[1,2]}}',
+        g + "\n" + '{"step":0,"scheduled":["a","b"],"lengths":{"a":[1,2],"zz":[1,2]}}',
+        g + "\n" + '{"step":0,"scheduled":["b","a"],"lengths":{"a":[1,2],"b":[1,2]}}\n'
+            '{"step":1,"scheduled":["a"],"lengths":{"a":[1,2],"a":[1]}}',
         g + "\n" + '{"step":0,"lengths":{}}',
         g + "\n" + '{"step":0,"lengths":null}',
         json.dumps(header([{"id": "", "ground_truth_len": 1, "token_ids": [1]}])),
