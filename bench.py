@@ -648,6 +648,59 @@ def bench_trace(args, ctx, torch, dev):
                                    "kind": "reference",
                                    "sample": f"4,096 prompts + 32,768 step rows ({len(sample) / 1e6:.0f} MB), "
                                              f"trace_from_string, {dt:.1f} s"}
+    out["jsonl"] = bench_trace_jsonl(args, ctx, torch, dev)
+    return out
+
+
+def bench_trace_jsonl(args, ctx, torch, dev):
+    """The same trace in the JSONL form (tests/cases.py c2_trace_jsonl: the
+    whole prompt table on one ~1 GB header line, one step object) through
+    rs_trace_csr_parse_jsonl; cpu_baseline: the reference's nlohmann reader
+    on the same shape cut to 1,024 prompts."""
+    from cases import c2_trace_jsonl
+    from paper_2602_22718_b200.lib import check
+    text, tok, _ = c2_trace_jsonl()
+    n_tok = int(tok.size)
+    d_text = torch.from_numpy(text).to(dev)
+    h = C.c_void_p()
+    lib = ctx.lib
+
+    def parse(ptr, device):
+        check(lib.rs_trace_csr_parse_jsonl(ctx.handle, C.c_void_p(ptr), text.nbytes, device, C.byref(h)))
+        lib.rs_trace_csr_free(h)
+
+    for _ in range(2):
+        parse(d_text.data_ptr(), 1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        parse(d_text.data_ptr(), 1)
+    dev_s = (time.perf_counter() - t0) / 5
+    pt = torch.from_numpy(text).pin_memory()
+    parse(pt.data_ptr(), 0)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        parse(pt.data_ptr(), 0)
+    host_s = (time.perf_counter() - t0) / 3
+    out = {"metric": "trace JSONL parse tokens/sec (JSONL -> device CSR + step table)",
+           "value": n_tok / dev_s, "unit": "tokens/s", "text_bytes": int(text.nbytes),
+           "ms_per_parse": dev_s * 1e3,
+           "config": {"workload": "C2 batch as a JSONL trace: one 65536-prompt header line x 2560 tokens "
+                                  "+ one step of 65536 x 8 lengths"},
+           "e2e": {"value": n_tok / host_s, "unit": "tokens/s", "h2d_bytes_per_step": int(text.nbytes),
+                   "d2h_bytes_per_step": 0}}
+    if not args.no_cpu:
+        from oracle_lib import ref
+        R = ref()
+        if R is not None:
+            sample = c2_trace_jsonl(n_prompts=1024)[0].tobytes()
+            t0 = time.perf_counter()
+            R.trace_prompts(sample, "jsonl")
+            dt = time.perf_counter() - t0
+            out["cpu_baseline"] = {"value": 1024 * 2560 / dt, "unit": "tokens/s", "cores": 1,
+                                   "kind": "reference",
+                                   "sample": f"1,024 prompts + 8,192 lengths ({len(sample) / 1e6:.0f} MB), "
+                                             f"trace_from_string(jsonl), {dt:.1f} s"}
     return out
 
 

@@ -36,7 +36,7 @@ std::vector<double> predict_lengths(const LengthHistory& history,
                                     const std::vector<const Prompt*>& prompts,
                                     const NoiseModel* noise = nullptr);
 
-// A CSV trace parsed on the GPU (rs_trace_csr_parse): trace() is
+// A CSV (or JSONL) trace parsed on the GPU (rs_trace_csr_parse): trace() is
 // trace_from_string(text, TraceFormat::csv) (workload.cpp:169-263) bit for
 // bit, with its ParseError / ValidationError in the reference's order (thrown
 // by parse_csv), and prefix_index() is PrefixIndex::build over the id-sorted
@@ -45,6 +45,9 @@ std::vector<double> predict_lengths(const LengthHistory& history,
 class DeviceTrace {
  public:
   static DeviceTrace parse_csv(const std::string& text);
+  // trace_from_string(text, TraceFormat::jsonl) (workload.cpp:294-352); the
+  // constructs rs.h lists as unsupported throw ParseError.
+  static DeviceTrace parse_jsonl(const std::string& text);
   DeviceTrace(DeviceTrace&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
   DeviceTrace& operator=(DeviceTrace&& o) noexcept;
   DeviceTrace(const DeviceTrace&) = delete;

@@ -51,7 +51,23 @@ TEST_CASE("device CSV trace equals the reference reader") {
 
 TEST_CASE("the C5 trace (512 prompts x 1,000 steps, G = 8)") {
   const std::string text = synthetic_csv(512, 1000, 8, 11);
-  CHECK(b200::DeviceTrace::parse_csv(text).trace() == trace_from_string(text, TraceFormat::csv));
+  const WorkloadTrace want = trace_from_string(text, TraceFormat::csv);
+  CHECK(b200::DeviceTrace::parse_csv(text).trace() == want);
+  const std::string jsonl = trace_to_string(want, TraceFormat::jsonl);
+  CHECK(b200::DeviceTrace::parse_jsonl(jsonl).trace() == trace_from_string(jsonl, TraceFormat::jsonl));
+}
+
+TEST_CASE("device JSONL trace equals the reference reader") {
+  for (uint64_t seed : {2ull, 5ull}) {
+    const std::string text =
+        trace_to_string(trace_from_string(synthetic_csv(100, 6, 4, seed), TraceFormat::csv), TraceFormat::jsonl);
+    const b200::DeviceTrace dev = b200::DeviceTrace::parse_jsonl(text);
+    CHECK(dev.trace() == trace_from_string(text, TraceFormat::jsonl));
+    std::vector<const Prompt*> ptrs;
+    const WorkloadTrace want = trace_from_string(text, TraceFormat::jsonl);
+    for (const Prompt& p : want.prompts) ptrs.push_back(&p);
+    same_index(dev.prefix_index(), PrefixIndex::build(ptrs));
+  }
 }
 
 TEST_CASE("errors come with the reference's types") {

@@ -17,6 +17,13 @@ DeviceTrace DeviceTrace::parse_csv(const std::string& text) {
   return DeviceTrace(h);
 }
 
+DeviceTrace DeviceTrace::parse_jsonl(const std::string& text) {
+  rs_trace_csr* h = nullptr;
+  rs_shim::check(rs_trace_csr_parse_jsonl(rs_shim::ctx(), text.data(),
+                                          static_cast<int64_t>(text.size()), 0, &h));
+  return DeviceTrace(h);
+}
+
 DeviceTrace& DeviceTrace::operator=(DeviceTrace&& o) noexcept {
   if (this != &o) {
     rs_trace_csr_free(h_);
