@@ -613,8 +613,8 @@ def bench_trace(args, ctx, torch, dev):
     ctx.reset_kernel_timing()
     parse(d_text.data_ptr(), 1)
     kt = {n: ctx.kernel_time(n)[0] for n in ("trace_classify", "trace_tokens", "trace_nl_write",
-                                             "trace_steprow", "trace_group", "trace_run_scan",
-                                             "trace_entry_scan")}
+                                             "trace_steprow", "trace_group", "trace_line_flags",
+                                             "trace_line_compact", "scan_apply")}
     ctx.enable_kernel_timing(False)
     pt = torch.from_numpy(text).pin_memory()
     parse(pt.data_ptr(), 0)

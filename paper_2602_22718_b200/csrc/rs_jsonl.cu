@@ -1230,6 +1230,7 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     }
     auto tr = new rs_trace_csr();
     std::unique_ptr<rs_trace_csr> own(tr);
+    tr->device = ctx->device;
     const JLine& H = hl[first];
     tr->g = H.g;
     tr->max_prompt_len = H.mp;

@@ -1105,6 +1105,7 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
     clk.mark("classify + lines");
     auto tr = new rs_trace_csr();
     std::unique_ptr<rs_trace_csr> own(tr);
+    tr->device = ctx->device;
     // errors in line order: malformed metadata before the header, then the header
     if (st.first_bad != ~0u)
       return parse_error(st.first_bad, st.bad_type == kG ? "malformed g metadata" : "malformed prompt metadata");
