@@ -59,7 +59,11 @@ constexpr int kJErr = 1;     // a ParseError of the reference reader
 constexpr int kJUnsup = 2;   // valid for nlohmann, not read here
 
 // ------------------------------------------------------------ stage 1 ----
-// 64-byte words: bitmasks of one character class, bit j = byte 64 w + j.
+// 64-byte words: bitmasks of one character class, bit j = byte 64 w + j,
+// four bytes at a time (SWAR byte compares packed to bits).
+__device__ __forceinline__ uint32_t pk4(uint32_t m) {  // 0xff / 0x00 bytes -> 4 bits
+  return (((m & 0x01010101u) * 0x01020408u) >> 24) & 0xfu;
+}
 __device__ __forceinline__ void word_masks(const unsigned char* t, int64_t w, int64_t n,
                                            uint64_t* bs, uint64_t* q, uint64_t* op, uint64_t* cl,
                                            uint64_t* cm, uint64_t* co) {
@@ -70,26 +74,25 @@ __device__ __forceinline__ void word_masks(const unsigned char* t, int64_t w, in
     const uint4 x = p[v];
     const uint32_t wd[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int j = 16 * v + 4 * k + b;
-        const unsigned c = (wd[k] >> (8 * b)) & 0xffu;
-        const uint64_t bit = 64 * w + j < n ? 1ULL << j : 0ULL;
-        mbs |= c == '\\' ? bit : 0;
-        mq |= c == '"' ? bit : 0;
-        mop |= (c == '{' || c == '[') ? bit : 0;
-        mcl |= (c == '}' || c == ']') ? bit : 0;
-        mcm |= c == ',' ? bit : 0;
-        mco |= c == ':' ? bit : 0;
-      }
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t y = wd[k];
+      const int sh = 16 * v + 4 * k;
+      mbs |= (uint64_t)pk4(__vcmpeq4(y, 0x5c5c5c5cu)) << sh;                                  // '\\'
+      mq |= (uint64_t)pk4(__vcmpeq4(y, 0x22222222u)) << sh;                                   // '"'
+      mop |= (uint64_t)pk4(__vcmpeq4(y, 0x7b7b7b7bu) | __vcmpeq4(y, 0x5b5b5b5bu)) << sh;      // '{' '['
+      mcl |= (uint64_t)pk4(__vcmpeq4(y, 0x7d7d7d7du) | __vcmpeq4(y, 0x5d5d5d5du)) << sh;      // '}' ']'
+      mcm |= (uint64_t)pk4(__vcmpeq4(y, 0x2c2c2c2cu)) << sh;                                  // ','
+      mco |= (uint64_t)pk4(__vcmpeq4(y, 0x3a3a3a3au)) << sh;                                  // ':'
+    }
   }
-  *bs = mbs;
-  *q = mq;
-  *op = mop;
-  *cl = mcl;
-  *cm = mcm;
-  *co = mco;
+  const int64_t left = n - 64 * w;  // bytes of the word inside the text
+  const uint64_t in = left >= 64 ? ~0ULL : (left <= 0 ? 0ULL : ((1ULL << left) - 1));
+  *bs = mbs & in;
+  *q = mq & in;
+  *op = mop & in;
+  *cl = mcl & in;
+  *cm = mcm & in;
+  *co = mco & in;
 }
 
 // Escaped characters of a word given the parity of the backslash run that
@@ -193,6 +196,9 @@ __global__ void js_tokens_kernel(const char* text, int64_t n, int64_t W, const u
     outside(t, n, w, tail, qscan, &op, &cl, &cm, &co);
     long long d = (long long)dscan[w];
     uint64_t all = op | cl | cm | co;
+    // no token of this word can come back to level 2 (the bulk of the text:
+    // the insides of token arrays at depth 4)
+    if (d - __popcll((long long)cl) > 2) all = 0;
     uint32_t na = 0, nb = 0;
     const uint32_t a0 = kWrite ? oa[w] : 0, b0 = kWrite ? ob[w] : 0;
     while (all) {
