@@ -886,7 +886,7 @@ __global__ void js_child_kernel(const char* text, const JCont* conts, const unsi
     if (kWrite) {
       r = ch[u];
       ci = r.cont;
-      if (r.err || conts[ci].role != wrole) continue;  // another role's pass writes it
+      if (r.err || !((wrole >> conts[ci].role) & 1)) continue;  // another pass writes it
     } else {  // container of unit u, index inside it
       int64_t lo = 0, hi = nc;  // last container with cscan <= u
       while (hi - lo > 1) {
@@ -1030,12 +1030,12 @@ __global__ void js_child_kernel(const char* text, const JCont* conts, const unsi
 }
 
 // Children with no error keep their pass-1 sizes; others count 0.
-__global__ void js_sizes_kernel(const JChild* ch, const JCont* conts, int64_t total, int role,
+__global__ void js_sizes_kernel(const JChild* ch, const JCont* conts, int64_t total, int rmask,
                                 unsigned long long* idl, unsigned long long* nint) {
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
        u += (int64_t)gridDim.x * blockDim.x) {
     const JChild r = ch[u];
-    const bool mine = !r.err && conts[r.cont].role == role;
+    const bool mine = !r.err && ((rmask >> conts[r.cont].role) & 1);
     idl[u] = mine ? (unsigned long long)r.id_len : 0ULL;
     nint[u] = mine ? (unsigned long long)r.n_int : 0ULL;
   }
@@ -1043,13 +1043,13 @@ __global__ void js_sizes_kernel(const JChild* ch, const JCont* conts, int64_t to
 
 // Each scheduled id / lengths key of one role: its index in the id-sorted
 // prompt table (binary search, std::string order), -1 when absent.
-__global__ void js_lookup_kernel(const JChild* ch, const JCont* conts, int64_t total, int role,
+__global__ void js_lookup_kernel(const JChild* ch, const JCont* conts, int64_t total, int rmask,
                                  const int64_t* id_off, const char* ids, const char* sids,
                                  const int64_t* sid_off, int32_t P, int32_t* pidx) {
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
        u += (int64_t)gridDim.x * blockDim.x) {
     const JChild r = ch[u];
-    if (r.err || conts[r.cont].role != role) continue;
+    if (r.err || !((rmask >> conts[r.cont].role) & 1)) continue;
     const unsigned char* a = reinterpret_cast<const unsigned char*>(ids + id_off[u]);
     const int64_t la = r.id_len;
     int32_t lo = 0, hi = P, found = -1;
@@ -1251,14 +1251,14 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
       P = (int32_t)(hcs[pc + 1] - hcs[pc]);
     }
     // sizes of every extracted child (per role), scanned, then written
-    auto sizes = [&](int role) -> int {
+    auto sizes = [&](int rmask) -> int {
       if (NCH == 0) return RS_OK;
-      RS_LAUNCH(ctx, "jsonl_sizes", js_sizes_kernel, grid(NCH), 256, 0, d_ch, d_conts, NCH, role, idl, nint);
+      RS_LAUNCH(ctx, "jsonl_sizes", js_sizes_kernel, grid(NCH), 256, 0, d_ch, d_conts, NCH, rmask, idl, nint);
       RS_TRY(exclusive_scan<unsigned long long>(ctx, idl, id_off, NCH, chpart, id_off + NCH));
       RS_TRY(exclusive_scan<unsigned long long>(ctx, nint, int_off, NCH, chpart, int_off + NCH));
       return RS_OK;
     };
-    RS_TRY(sizes(kRPrompts));
+    RS_TRY(sizes(1 << kRPrompts));
     unsigned long long ptot[2] = {0, 0};
     if (NCH) {
       RS_TRY(d2h(ctx, &ptot[0], id_off + NCH, 8));
@@ -1280,7 +1280,7 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     if (P > 0) {
       RS_LAUNCH(ctx, "jsonl_prompt_write", js_child_kernel<true>, grid(NCH), 128, 0, d_text, d_conts, cscan, NC,
                 lbv, NB, NCH, d_ch, (const int64_t*)id_off, (const int64_t*)int_off, d_ids, d_tok, small + 2,
-                (int)kRPrompts);
+                1 << kRPrompts);
       RS_LAUNCH(ctx, "jsonl_prompt_tables", js_prompt_tables_kernel, grid(P + 1), 256, 0, d_ch, c0, P,
                 (const int64_t*)id_off, (const int64_t*)int_off, p_id_off, p_tok_off, p_gt);
       std::vector<int64_t> ioff(P + 1);
@@ -1291,75 +1291,68 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     RS_TRY(arena_reserve(ctx, rank_strings_device_bytes(std::max(P, 1), maxid) + (1 << 16)));
     RS_TRY(trace_sorted_table(ctx, tr, P, maxid, d_ids, p_id_off, p_tok_off, p_gt, d_perm));
     clk.mark("prompts");
-    // 5. steps, on the host: scheduled ids and length lists per step line
-    std::vector<JChild> hch(NCH);
-    std::vector<unsigned long long> h_id_off, h_int_off;
+    // 5. steps: the scheduled ids and lengths keys / lists of every step line
+    // written on the device (one pass for both roles), the keys resolved
+    // against the id-sorted table there, and the records copied to the host
+    // through pinned memory in one go
+    std::vector<unsigned long long> h_id_off, h_int_off, h_il, h_ni;
     std::vector<char> h_ids;
     std::vector<int32_t> h_ints;
     std::vector<int32_t> hp;  // per child: its index in the id-sorted table (-1: unknown)
     bool any_steps = false;
     for (int64_t ln = 0; ln < L; ++ln) any_steps |= hl[ln].kind == kLStep;
-    AsyncBuf b_sid;
-    int32_t* d_pidx = nullptr;
-    char* d_sids = nullptr;
-    int64_t* d_sid_off = nullptr;
     if (any_steps && NCH > 0) {
-      char* q = b_sid.alloc<char>(ctx->stream, abytes(tr->ids.size() + 1, 1) + abytes(P + 1, 8) + abytes(NCH, 4));
+      const int smask = (1 << kRSched) | (1 << kRLengths);
+      RS_TRY(sizes(smask));
+      unsigned long long tt[2];
+      RS_TRY(d2h(ctx, &tt[0], id_off + NCH, 8));
+      RS_TRY(d2h(ctx, &tt[1], int_off + NCH, 8));
+      RS_TRY(sync_and_check(ctx));
+      AsyncBuf b_st;
+      char* q = b_st.alloc<char>(ctx->stream, abytes(tr->ids.size() + 1, 1) + abytes(P + 1, 8) + abytes(NCH, 4) +
+                                                  abytes(tt[0] + 1, 1) + abytes(tt[1] + 1, 4));
       if (!q) return fail(RS_E_NOMEM, "jsonl steps: allocation failed");
-      d_sids = carve(q, abytes(tr->ids.size() + 1, 1));
-      d_sid_off = (int64_t*)carve(q, abytes(P + 1, 8));
-      d_pidx = (int32_t*)carve(q, abytes(NCH, 4));
+      char* d_sids = carve(q, abytes(tr->ids.size() + 1, 1));
+      int64_t* d_sid_off = (int64_t*)carve(q, abytes(P + 1, 8));
+      int32_t* d_pidx = (int32_t*)carve(q, abytes(NCH, 4));
+      char* d_i = carve(q, abytes(tt[0] + 1, 1));
+      int32_t* d_n = (int32_t*)carve(q, abytes(tt[1] + 1, 4));
       if (!tr->ids.empty()) RS_TRY(h2d(ctx, d_sids, tr->ids.data(), tr->ids.size()));
       RS_TRY(h2d(ctx, d_sid_off, tr->id_off.data(), 8ull * (P + 1)));
       RS_CUDA_TRY(cudaMemsetAsync(d_pidx, 0xff, 4ull * NCH, ctx->stream));
-    }
-    if (any_steps && NCH > 0) {
-      auto gather = [&](int role) -> int {  // sizes + writes of one role's children, to the host
-        RS_TRY(sizes(role));
-        unsigned long long tt[2];
-        RS_TRY(d2h(ctx, &tt[0], id_off + NCH, 8));
-        RS_TRY(d2h(ctx, &tt[1], int_off + NCH, 8));
-        RS_TRY(sync_and_check(ctx));
-        AsyncBuf b;
-        char* q = b.alloc<char>(ctx->stream, abytes(tt[0] + 1, 1) + abytes(tt[1] + 1, 4));
-        if (!q) return fail(RS_E_NOMEM, "jsonl steps: allocation failed");
-        char* d_i = q;
-        int32_t* d_n = (int32_t*)(q + abytes(tt[0] + 1, 1));
-        RS_LAUNCH(ctx, "jsonl_step_write", js_child_kernel<true>, grid(NCH), 128, 0, d_text, d_conts, cscan, NC,
-                  lbv, NB, NCH, d_ch, (const int64_t*)id_off, (const int64_t*)int_off, d_i, d_n, small + 2,
-                  role);
-        RS_LAUNCH(ctx, "jsonl_lookup", js_lookup_kernel, grid(NCH), 256, 0, d_ch, d_conts, NCH, role,
-                  (const int64_t*)id_off, d_i, d_sids, d_sid_off, P, d_pidx);
-        const size_t o_i = h_ids.size(), o_n = h_ints.size();
-        h_ids.resize(o_i + tt[0]);
-        h_ints.resize(o_n + tt[1]);
-        std::vector<unsigned long long> a(NCH + 1), c(NCH + 1);
-        RS_TRY(d2h(ctx, a.data(), id_off, 8ull * (NCH + 1)));
-        RS_TRY(d2h(ctx, c.data(), int_off, 8ull * (NCH + 1)));
-        if (tt[0]) RS_TRY(d2h(ctx, h_ids.data() + o_i, d_i, tt[0]));
-        if (tt[1]) RS_TRY(d2h(ctx, h_ints.data() + o_n, d_n, 4ull * tt[1]));
-        RS_TRY(sync_and_check(ctx));
-        if (h_id_off.empty()) {
-          h_id_off.assign(NCH + 1, 0);
-          h_int_off.assign(NCH + 1, 0);
-        }
-        for (int64_t u = 0; u < NCH; ++u)
-          if (hc[hch[u].cont].role == role) {
-            h_id_off[u] = o_i + a[u];
-            h_int_off[u] = o_n + c[u];
-          }
-        return RS_OK;
-      };
-      RS_TRY(d2h(ctx, hch.data(), d_ch, sizeof(JChild) * NCH));
+      RS_LAUNCH(ctx, "jsonl_step_write", js_child_kernel<true>, grid(NCH), 128, 0, d_text, d_conts, cscan, NC,
+                lbv, NB, NCH, d_ch, (const int64_t*)id_off, (const int64_t*)int_off, d_i, d_n, small + 2, smask);
+      RS_LAUNCH(ctx, "jsonl_lookup", js_lookup_kernel, grid(NCH), 256, 0, d_ch, d_conts, NCH, smask,
+                (const int64_t*)id_off, d_i, d_sids, d_sid_off, P, d_pidx);
+      // one pinned staging area: sizes, table indices, id bytes, lengths
+      const size_t o_il = 0, o_ni = abytes(NCH, 8), o_p = 2 * abytes(NCH, 8), o_i = o_p + abytes(NCH, 4),
+                   o_n = o_i + abytes(tt[0] + 1, 1), total_b = o_n + abytes(tt[1] + 1, 4);
+      RS_TRY(pinned_reserve(ctx, total_b));
+      char* hb = static_cast<char*>(ctx->pinned);
+      RS_TRY(d2h(ctx, hb + o_il, idl, 8ull * NCH));
+      RS_TRY(d2h(ctx, hb + o_ni, nint, 8ull * NCH));
+      RS_TRY(d2h(ctx, hb + o_p, d_pidx, 4ull * NCH));
+      if (tt[0]) RS_TRY(d2h(ctx, hb + o_i, d_i, tt[0]));
+      if (tt[1]) RS_TRY(d2h(ctx, hb + o_n, d_n, 4ull * tt[1]));
       RS_TRY(sync_and_check(ctx));
-      RS_TRY(gather(kRSched));
-      RS_TRY(gather(kRLengths));
-      hp.resize(NCH);
-      RS_TRY(d2h(ctx, hp.data(), d_pidx, 4ull * NCH));
-      RS_TRY(sync_and_check(ctx));
+      const auto* il = reinterpret_cast<const unsigned long long*>(hb + o_il);
+      const auto* ni = reinterpret_cast<const unsigned long long*>(hb + o_ni);
+      h_il.assign(il, il + NCH);
+      h_ni.assign(ni, ni + NCH);
+      hp.assign(reinterpret_cast<const int32_t*>(hb + o_p), reinterpret_cast<const int32_t*>(hb + o_p) + NCH);
+      h_ids.assign(hb + o_i, hb + o_i + tt[0]);
+      h_ints.assign(reinterpret_cast<const int32_t*>(hb + o_n), reinterpret_cast<const int32_t*>(hb + o_n) + tt[1]);
+      h_id_off.assign(NCH + 1, 0);
+      h_int_off.assign(NCH + 1, 0);
+      for (int64_t u = 0; u < NCH; ++u) {
+        h_id_off[u + 1] = h_id_off[u] + h_il[u];
+        h_int_off[u + 1] = h_int_off[u] + h_ni[u];
+      }
+      clk.mark("steps: device records");
     }
     // WorkloadTrace::validate: the prompt rules, then step by step
     RS_TRY(trace_validate_prompts(tr));
+    clk.mark("prompt rules");
     // per step line: its containers (the last of each role) and children
     std::vector<int64_t> sched_c(L, -1), len_c(L, -1);
     for (int64_t c = 0; c < NC; ++c) {
@@ -1381,7 +1374,7 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     int prev_step = -1;
     const int32_t G = tr->g;
     auto child_id = [&](unsigned long long u) {
-      return std::string(h_ids.data() + h_id_off[u], h_ids.data() + h_id_off[u] + hch[u].id_len);
+      return std::string(h_ids.data() + h_id_off[u], h_ids.data() + h_id_off[u] + h_il[u]);
     };
     auto table_id = [&](int32_t p) {
       return std::string(tr->ids.data() + tr->id_off[p], tr->ids.data() + tr->id_off[p + 1]);
@@ -1414,7 +1407,13 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
           last_u[p] = (int64_t)u;
         }
       if (known) {
-        std::sort(keys.begin(), keys.end());
+        if ((int64_t)keys.size() * 16 > (int64_t)P) {  // dense: the stamps in table order
+          keys.clear();
+          for (int32_t p = 0; p < P; ++p)
+            if (stamp_len[p] == ln) keys.push_back(p);
+        } else {
+          std::sort(keys.begin(), keys.end());
+        }
         std::vector<int32_t> sched;
         std::vector<unsigned long long> sched_u;
         if (hl[ln].has_sched && sched_c[ln] >= 0) {
@@ -1440,10 +1439,10 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
           if (stamp_sched[p] != ln)
             return fail(RS_E_VALIDATION, "step " + sn + " has lengths for unscheduled prompt '" + table_id(p) + "'");
           const unsigned long long u = (unsigned long long)last_u[p];
-          if ((int)hch[u].n_int != G)
+          if ((int)h_ni[u] != G)
             return fail(RS_E_VALIDATION, "step " + sn + " prompt '" + table_id(p) + "' needs exactly " +
                                              std::to_string(G) + " response lengths");
-          for (int64_t i = 0; i < hch[u].n_int; ++i) {
+          for (int64_t i = 0; i < (int64_t)h_ni[u]; ++i) {
             const int l = h_ints[h_int_off[u] + i];
             if (l < 1 || l > tr->max_response_len)
               return fail(RS_E_VALIDATION, "step " + sn + " prompt '" + table_id(p) +
@@ -1454,7 +1453,7 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
         for (const int32_t p : sched) {
           e_prompt.push_back(p);
           const unsigned long long u = (unsigned long long)last_u[p];
-          lens.insert(lens.end(), h_ints.begin() + h_int_off[u], h_ints.begin() + h_int_off[u] + hch[u].n_int);
+          lens.insert(lens.end(), h_ints.begin() + h_int_off[u], h_ints.begin() + h_int_off[u] + h_ni[u]);
         }
         e_off.push_back((int32_t)e_prompt.size());
         continue;
@@ -1463,7 +1462,7 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
       std::vector<std::string> sched;
       std::map<std::string, std::vector<int>> lmap;
       for (unsigned long long u = hcs[len_c[ln]]; u < hcs[len_c[ln] + 1]; ++u)
-        lmap[child_id(u)] = std::vector<int>(h_ints.begin() + h_int_off[u], h_ints.begin() + h_int_off[u] + hch[u].n_int);
+        lmap[child_id(u)] = std::vector<int>(h_ints.begin() + h_int_off[u], h_ints.begin() + h_int_off[u] + h_ni[u]);
       if (hl[ln].has_sched && sched_c[ln] >= 0) {
         for (unsigned long long u = hcs[sched_c[ln]]; u < hcs[sched_c[ln] + 1]; ++u) sched.push_back(child_id(u));
       } else if (!hl[ln].has_sched) {
