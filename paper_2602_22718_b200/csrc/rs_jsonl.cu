@@ -905,6 +905,7 @@ __global__ void js_child_kernel(const char* text, const JCont* conts, const unsi
       r.line = jc.line;
     }
     const JCont jc = conts[ci];
+    if (!kWrite && jc.role == kRPrompts) continue;  // js_prompt_kernel: a warp per prompt
     JIn in{t, r.a, r.e};
     int err = 0;
     skip_ws(in);
@@ -1022,6 +1023,295 @@ __global__ void js_child_kernel(const char* text, const JCont* conts, const unsi
       if (in.p != in.e) err = kJErr;
     }
     if (!kWrite) {
+      r.err = err;
+      ch[u] = r;
+      if (err) atomicMin(first_err, ((unsigned int)r.line << 1) | (err == kJUnsup ? 1u : 0u));
+    }
+  }
+}
+
+// ------------------------------------------- warp-cooperative prompts --
+// An int array of plain integers at p (just after its '['), 16 bytes per
+// lane, 512 per step: byte classes as masks, every item checked against the
+// previous non-blank one (a number after ',' or the '[', a ',' after a
+// number, the ']' after a number or the '['), no '-' except at a number's
+// start, no leading zero, at most 18 digits. Counts (out == nullptr) or
+// writes the values. Returns 0 (with *count and *end, the position after
+// the ']') or 1 when the array is not of that form — a float, a boolean, a
+// longer number, or a syntax error: the caller's serial path then decides.
+__device__ int warp_int_array(const unsigned char* t, int64_t p, int64_t e, int32_t* out, int64_t* count,
+                              int64_t* end) {
+  const int lane = threadIdx.x & 31;
+  enum : int { kNone = 0, kStart = 1, kNum = 2, kComma = 3 };  // class of the last non-blank byte
+  int carry = kStart;    // the '['
+  uint32_t prevX = 0, prevM = 0;  // the byte before the step: part of a number / a '-'
+  int64_t k = 0;
+  for (int64_t b0 = p & ~(int64_t)15;; b0 += 512) {
+    if (b0 >= e) return 1;  // no ']' before the end of the span
+    const int64_t i = b0 + 16 * lane;
+    uint32_t D = 0, M = 0, Z = 0, C = 0, W = 0, E = 0, O = 0;
+    {
+      const uint4 v = *reinterpret_cast<const uint4*>(t + i);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t x = w[q];
+        const uint32_t dg = __vcmpgeu4(x, 0x30303030u) & __vcmpleu4(x, 0x39393939u);
+        const uint32_t mi = __vcmpeq4(x, 0x2d2d2d2du), ze = __vcmpeq4(x, 0x30303030u);
+        const uint32_t cm = __vcmpeq4(x, 0x2c2c2c2cu), cl = __vcmpeq4(x, 0x5d5d5d5du);
+        const uint32_t ws = __vcmpeq4(x, 0x20202020u) | __vcmpeq4(x, 0x09090909u) |
+                            __vcmpeq4(x, 0x0a0a0a0au) | __vcmpeq4(x, 0x0d0d0d0du);
+        D |= pk4(dg) << (4 * q);
+        M |= pk4(mi) << (4 * q);
+        Z |= pk4(ze) << (4 * q);
+        C |= pk4(cm) << (4 * q);
+        E |= pk4(cl) << (4 * q);
+        W |= pk4(ws) << (4 * q);
+      }
+      uint32_t valid = 0xffffu;
+      if (i < p) valid &= p - i >= 16 ? 0u : 0xffffu << (int)(p - i);
+      if (i + 16 > e) valid &= e > i ? 0xffffu >> (int)(16 - (e - i)) : 0u;
+      D &= valid;
+      M &= valid;
+      Z &= valid;
+      C &= valid;
+      E &= valid;
+      W = (W & valid) | (~valid & 0xffffu & (i < p ? (p - i >= 16 ? 0xffffu : ((1u << (p - i)) - 1)) : 0u));
+      O = ~(D | M | C | E | W) & 0xffffu;  // bytes past e count as other
+    }
+    // the array ends at the first ']': later bytes do not matter
+    const unsigned eb = __ballot_sync(0xffffffffu, E != 0);
+    int close_lane = eb ? __ffs(eb) - 1 : 32;
+    if (lane > close_lane) D = M = Z = C = E = O = 0, W = 0xffffu;
+    if (lane == close_lane) {
+      const int j = __ffs(E) - 1;
+      const uint32_t keep = (2u << j) - 1;  // up to and with the ']'
+      D &= keep;
+      M &= keep;
+      Z &= keep;
+      C &= keep;
+      E &= keep;
+      O &= keep;
+      W = (W & keep) | (~keep & 0xffffu);
+    }
+    const uint32_t X = D | M;
+    const uint32_t up = __shfl_up_sync(0xffffffffu, X >> 15, 1);
+    const uint32_t S = X & ~((X << 1) | (lane == 0 ? prevX : up)) & 0xffffu;
+    const uint32_t dn = __shfl_down_sync(0xffffffffu, D & 1u, 1);
+    const uint32_t d_after = i + 16 < e && t[i + 16] >= '0' && t[i + 16] <= '9' ? 1u : 0u;
+    const uint32_t Dn = ((D >> 1) | ((lane == 31 ? d_after : dn) << 15)) & 0xffffu;  // next byte a digit
+    const uint32_t mup = __shfl_up_sync(0xffffffffu, M >> 15, 1);
+    const uint32_t Mp = ((M << 1) & 0xffffu) | (lane == 0 ? prevM : mup);
+    bool bad = O != 0;
+    bad |= (M & ~S) != 0;                // '-' inside a number
+    bad |= (M & ~Dn) != 0;               // '-' not followed by a digit
+    bad |= (Z & (S | Mp) & Dn) != 0;     // leading zero
+    // the class of the last non-blank byte before each lane (a "last
+    // non-none" scan over the lanes, from the previous step's carry)
+    const uint32_t NW = ~W & 0xffffu;
+    int last = kNone;
+    if (NW) {
+      const int j = 31 - __clz(NW);
+      last = ((C >> j) & 1) ? kComma : (((E >> j) & 1) ? kNone : kNum);
+    }
+    int before = last;  // inclusive scan of "the last defined" across the lanes
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, before, d);
+      if (lane >= d && before == kNone) before = o;
+    }
+    // exclusive: the lane before's inclusive value (or the carry)
+    int prev = __shfl_up_sync(0xffffffffu, before, 1);
+    if (lane == 0) prev = kNone;
+    if (prev == kNone) prev = carry;
+    // walk this lane's items: starts, commas, the ']'
+    uint32_t items = S | C | E;
+    int pc = prev;
+    uint32_t nw = NW;
+    while (items && !bad) {
+      const int j = __ffs(items) - 1;
+      items &= items - 1;
+      // the last non-blank byte below j in this lane, else the carried class
+      const uint32_t below = nw & ((1u << j) - 1);
+      int cls = pc;
+      if (below) {
+        const int jb = 31 - __clz(below);
+        cls = ((C >> jb) & 1) ? kComma : kNum;
+      }
+      if ((S >> j) & 1) bad |= !(cls == kComma || cls == kStart);
+      else if ((C >> j) & 1) bad |= cls != kNum;
+      else bad |= !(cls == kNum || cls == kStart);
+    }
+    // numbers: each lane parses the ones starting in its bytes
+    const int ns = __popc(S);
+    const int before_n = warp_incl_sum(ns) - ns;
+    if (!bad && ns) {
+      uint32_t m = S;
+      int idx = 0;
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        int64_t q = i + j;
+        const bool neg = t[q] == '-';
+        if (neg) ++q;
+        unsigned long long v = 0;
+        int nd = 0;
+        for (; q < e && t[q] >= '0' && t[q] <= '9'; ++q, ++nd) v = v * 10u + (unsigned)(t[q] - '0');
+        if (nd > 18) bad = true;
+        if (out && !bad) out[k + before_n + idx] = (int32_t)(neg ? 0ULL - v : v);
+        ++idx;
+      }
+    }
+    if (__any_sync(0xffffffffu, bad)) return 1;
+    k += __shfl_sync(0xffffffffu, before_n + ns, 31);
+    // the carry: the class of the last non-blank byte of this step
+    const int lastcls = __shfl_sync(0xffffffffu, before, 31);
+    if (lastcls != kNone) carry = lastcls;
+    prevX = __shfl_sync(0xffffffffu, (X >> 15) & 1u, 31);
+    prevM = __shfl_sync(0xffffffffu, (M >> 15) & 1u, 31);
+    if (close_lane < 32) {
+      const uint32_t ej = (uint32_t)__shfl_sync(0xffffffffu, (uint32_t)(__ffs(E) - 1), close_lane);
+      *count = k;
+      *end = b0 + 16 * close_lane + ej + 1;
+      return 0;
+    }
+  }
+}
+
+// One warp per prompt object (the children [c0, c0 + P) of the prompts
+// container): lane 0 reads the members, the warp reads "token_ids" (serial
+// fallback on lane 0 for arrays outside the fast form). Pass 1 records the
+// child like js_child_kernel; pass 2 writes the id and the tokens.
+template <bool kWrite>
+__global__ void js_prompt_kernel(const char* text, const JCont* conts, const unsigned long long* cscan,
+                                 int64_t c0, int64_t P, const int64_t* lb, int64_t nb, int64_t pc,
+                                 JChild* ch, const int64_t* id_off, const int64_t* int_off, char* ids,
+                                 int32_t* ints, unsigned int* first_err) {
+  const unsigned char* t = reinterpret_cast<const unsigned char*>(text);
+  const int lane = threadIdx.x & 31;
+  for (int64_t pi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; pi < P;
+       pi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t u = c0 + pi;
+    JChild r{};
+    const JCont jc = conts[pc];
+    if (kWrite) {
+      r = ch[u];
+      if (r.err) continue;
+      if (lane == 0) {
+        JIn is{t, r.id_at, r.e};
+        int64_t l;
+        jstring(is, ids + id_off[u], r.id_len, &l);
+      }
+      int64_t cnt, endp;
+      const int st = warp_int_array(t, r.ints_at + 1, r.e, ints + int_off[u], &cnt, &endp);
+      if (st && lane == 0) {
+        JIn it{t, r.ints_at, r.e};
+        jint_array(it, ints + int_off[u], &cnt);
+      }
+      continue;
+    }
+    const int64_t b0 = lower_b(lb, nb, jc.open), b1 = lower_b(lb, nb, jc.close);
+    r.a = pi == 0 ? jc.open + 1 : lb[b0 + pi - 1] + 1;
+    r.e = b0 + pi < b1 ? lb[b0 + pi] : jc.close;
+    r.cont = (int32_t)pc;
+    r.line = jc.line;
+    // lane 0 walks the members; at "token_ids" the warp reads the array
+    JIn in{t, r.a, r.e};
+    int err = 0;
+    bool has_id = false, has_gt = false, has_tok = false, open_ok = false;
+    if (lane == 0) {
+      skip_ws(in);
+      if (in.p >= in.e || t[in.p] != '{') {
+        err = jskip(in);
+        if (!err) err = kJErr;
+      } else {
+        ++in.p;
+        skip_ws(in);
+        open_ok = true;
+      }
+    }
+    bool done = !__shfl_sync(0xffffffffu, open_ok, 0);
+    bool first_m = true;
+    while (!done) {
+      int key = -1, want_arr = 0;
+      int64_t arr_at = 0;
+      if (lane == 0) {
+        if (first_m && in.p < in.e && t[in.p] == '}') {
+          ++in.p;
+          done = true;
+        } else {
+          static const char* const kP[] = {"id", "ground_truth_len", "token_ids"};
+          key = jkey(in, kP, 3, &err);
+          if (err) {
+            done = true;
+          } else if (key == 0) {
+            if (in.p >= in.e || t[in.p] != '"') {
+              err = jskip(in);
+              if (!err) err = kJErr;
+            } else {
+              r.id_at = in.p;
+              err = jstring(in, nullptr, 0, &r.id_len);
+              has_id = true;
+            }
+          } else if (key == 1) {
+            err = jint(in, &r.gt);
+            has_gt = true;
+          } else if (key == 2) {
+            r.ints_at = in.p;
+            has_tok = true;
+            if (in.p < in.e && t[in.p] == '[') {
+              want_arr = 1;
+              arr_at = in.p;
+            } else {
+              err = jskip(in);
+              if (!err) err = kJErr;
+            }
+          } else {
+            err = jskip(in);
+          }
+        }
+      }
+      want_arr = __shfl_sync(0xffffffffu, want_arr, 0);
+      if (want_arr) {
+        arr_at = __shfl_sync(0xffffffffu, arr_at, 0);
+        int64_t cnt = 0, endp = 0;
+        const int st = warp_int_array(t, arr_at + 1, r.e, nullptr, &cnt, &endp);
+        if (lane == 0) {
+          if (st) {
+            JIn it{t, arr_at, in.e};
+            err = jint_array(it, nullptr, &cnt);
+            endp = it.p;
+          }
+          r.n_int = cnt;
+          in.p = endp;
+        }
+      }
+      if (lane == 0 && !done) {
+        if (err) {
+          done = true;
+        } else {
+          skip_ws(in);
+          if (in.p < in.e && t[in.p] == ',') {
+            ++in.p;
+            skip_ws(in);
+          } else if (in.p < in.e && t[in.p] == '}') {
+            ++in.p;
+            done = true;
+          } else {
+            err = kJErr;
+            done = true;
+          }
+        }
+      }
+      first_m = false;
+      done = __shfl_sync(0xffffffffu, done, 0);
+    }
+    if (lane == 0) {
+      if (!err && open_ok && !(has_id && has_gt && has_tok)) err = kJErr;
+      if (!err) {
+        skip_ws(in);
+        if (in.p != in.e) err = kJErr;
+      }
       r.err = err;
       ch[u] = r;
       if (err) atomicMin(first_err, ((unsigned int)r.line << 1) | (err == kJUnsup ? 1u : 0u));
@@ -1195,10 +1485,30 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     auto* id_off = (unsigned long long*)carve(chb, abytes(NCH + 1, 8));
     auto* int_off = (unsigned long long*)carve(chb, abytes(NCH + 1, 8));
     auto* chpart = (unsigned long long*)carve(chb, scan_scratch_bytes(NCH + 1, 8));
+    // the containers (the prompts one gets a warp per prompt object)
+    std::vector<JCont> hc(NC);
+    std::vector<unsigned long long> hcs(NC + 1, 0);
+    if (NC) {
+      RS_TRY(d2h(ctx, hc.data(), d_conts, sizeof(JCont) * NC));
+      RS_TRY(d2h(ctx, hcs.data(), cscan, 8ull * (NC + 1)));
+      RS_TRY(sync_and_check(ctx));
+    }
+    int64_t pc = -1;  // the prompts container
+    for (int64_t c = 0; c < NC; ++c)
+      if (hc[c].role == kRPrompts) pc = c;
+    const int64_t c0 = pc >= 0 ? (int64_t)hcs[pc] : 0;
+    const int32_t P = pc >= 0 ? (int32_t)(hcs[pc + 1] - hcs[pc]) : 0;
+    auto wgrid = [&](int64_t n) {  // a warp per item, 128-thread blocks
+      return (int)std::max<int64_t>(1, std::min<int64_t>((n + 3) / 4, 64 * (int64_t)ctx->num_sms));
+    };
     if (NCH > 0)
       RS_LAUNCH(ctx, "jsonl_child_check", js_child_kernel<false>, grid(NCH), 128, 0, d_text, d_conts, cscan, NC,
                 lbv, NB, NCH, d_ch, (const int64_t*)nullptr, (const int64_t*)nullptr, (char*)nullptr,
                 (int32_t*)nullptr, small + 2, 0);
+    if (P > 0)
+      RS_LAUNCH(ctx, "jsonl_prompt_check", js_prompt_kernel<false>, wgrid(P), 128, 0, d_text, d_conts, cscan, c0,
+                (int64_t)P, lbv, NB, pc, d_ch, (const int64_t*)nullptr, (const int64_t*)nullptr, (char*)nullptr,
+                (int32_t*)nullptr, small + 2);
     // the first error line over the lines and the children
     std::vector<JLine> hl(L);
     unsigned int cerr = ~0u;
@@ -1225,15 +1535,6 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
                                                              : "malformed JSON trace line");
     if (first < 0) return fail(RS_E_PARSE, "<trace>: missing header line");
     // 4. the header's prompts (the container with the prompts role, if any)
-    std::vector<JCont> hc(NC);
-    std::vector<unsigned long long> hcs(NC + 1);
-    if (NC) {
-      RS_TRY(d2h(ctx, hc.data(), d_conts, sizeof(JCont) * NC));
-      RS_TRY(d2h(ctx, hcs.data(), cscan, 8ull * (NC + 1)));
-      RS_TRY(sync_and_check(ctx));
-    } else {
-      hcs[0] = 0;
-    }
     auto tr = new rs_trace_csr();
     std::unique_ptr<rs_trace_csr> own(tr);
     tr->device = ctx->device;
@@ -1241,15 +1542,6 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     tr->g = H.g;
     tr->max_prompt_len = H.mp;
     tr->max_response_len = H.mr;
-    int64_t pc = -1;  // the prompts container
-    for (int64_t c = 0; c < NC; ++c)
-      if (hc[c].role == kRPrompts) pc = c;
-    int32_t P = 0;
-    int64_t c0 = 0;
-    if (pc >= 0) {
-      c0 = (int64_t)hcs[pc];
-      P = (int32_t)(hcs[pc + 1] - hcs[pc]);
-    }
     // sizes of every extracted child (per role), scanned, then written
     auto sizes = [&](int rmask) -> int {
       if (NCH == 0) return RS_OK;
@@ -1278,9 +1570,9 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     uint32_t* d_perm = (uint32_t*)carve(pb, abytes(P + 1, 4));
     int64_t maxid = 1;
     if (P > 0) {
-      RS_LAUNCH(ctx, "jsonl_prompt_write", js_child_kernel<true>, grid(NCH), 128, 0, d_text, d_conts, cscan, NC,
-                lbv, NB, NCH, d_ch, (const int64_t*)id_off, (const int64_t*)int_off, d_ids, d_tok, small + 2,
-                1 << kRPrompts);
+      RS_LAUNCH(ctx, "jsonl_prompt_write", js_prompt_kernel<true>, wgrid(P), 128, 0, d_text, d_conts, cscan, c0,
+                (int64_t)P, lbv, NB, pc, d_ch, (const int64_t*)id_off, (const int64_t*)int_off, d_ids, d_tok,
+                small + 2);
       RS_LAUNCH(ctx, "jsonl_prompt_tables", js_prompt_tables_kernel, grid(P + 1), 256, 0, d_ch, c0, P,
                 (const int64_t*)id_off, (const int64_t*)int_off, p_id_off, p_tok_off, p_gt);
       std::vector<int64_t> ioff(P + 1);

@@ -216,3 +216,61 @@ def test_c2_shaped_jsonl_to_prefix_index():
     tr = same(text)
     direct = rs.PrefixIndex.build([p[2] for p in prompts])
     assert all(np.array_equal(a, b) for a, b in zip(tr.prefix_index().tables(), direct.tables()))
+
+
+def fuzz_arrays(seed, n=300):
+    """Prompt token arrays in random JSON layouts (blanks around every comma,
+    signs, zeros, 18-digit and longer numbers), long enough to cross the
+    warp reader's 512-byte steps anywhere."""
+    rng = np.random.RandomState(seed)
+    prompts = []
+    for i in range(n):
+        k = int(rng.randint(1, 400))
+        toks = []
+        for _ in range(k):
+            r = rng.rand()
+            if r < 0.05:
+                v = "0"
+            elif r < 0.1:
+                v = "-" + str(rng.randint(0, 10 ** 9))
+            elif r < 0.12:
+                v = str(rng.randint(10 ** 17, 10 ** 18 - 1))        # 18 digits
+            elif r < 0.13:
+                v = str(rng.randint(10 ** 18, 2 ** 63 - 1))         # 19: the serial path
+            else:
+                v = str(rng.randint(0, 40000))
+            toks.append(v)
+        seps = [" " * int(rng.randint(0, 3)) + "," + "\t" * int(rng.randint(0, 2)) + " " * int(rng.randint(0, 2))
+                for _ in range(k - 1)]
+        body = toks[0] + "".join(s + t for s, t in zip(seps, toks[1:]))
+        arr = "[" + " " * int(rng.randint(0, 3)) + body + " " * int(rng.randint(0, 3)) + "]"
+        prompts.append('{"id":"q%05d","ground_truth_len":5,"token_ids":%s}' % (i, arr))
+    return prompts
+
+
+def test_token_arrays_fuzz():
+    for seed in range(4):
+        prompts = fuzz_arrays(seed)
+        text = ('{"type":"header","g":1,"max_prompt_len":400,"prompts":[' + ",".join(prompts) + ']}\n').encode()
+        same(text)
+
+
+def test_token_array_defects_fuzz():
+    rng = np.random.RandomState(9)
+    defects = ["01", "1 2", "1,,2", "-", "--1", "1-", "0x", "- 1", "1.", ".5", "+1", "00"]
+    for trial in range(24):
+        prompts = fuzz_arrays(100 + trial, n=40)
+        i = int(rng.randint(0, len(prompts)))
+        p = prompts[i]
+        lo = p.index("[") + 1
+        hi = p.index("]")
+        cut = [j for j in range(lo, hi) if p[j] == ","]
+        at = cut[int(rng.randint(0, len(cut)))] + 1 if cut else lo
+        d = defects[trial % len(defects)]
+        prompts[i] = p[:at] + d + "," + p[at:] if cut else p[:lo] + d + p[hi:]
+        text = ('{"type":"header","g":1,"max_prompt_len":500,"prompts":[' + ",".join(prompts) + ']}\n').encode()
+        try:
+            ref().trace_prompts(text, "jsonl")
+            same(text)  # still valid JSON for the reference (e.g. a float)
+        except OracleError:
+            same_error(text)

@@ -24,7 +24,7 @@ d = torch.from_numpy(text).cuda()
 h = C.c_void_p()
 names = ["jsonl_bs", "jsonl_quote", "jsonl_depth", "jsonl_tok_count", "jsonl_tok_write",
          "jsonl_first_line", "jsonl_lines", "jsonl_child_count", "jsonl_child_check", "jsonl_sizes",
-         "jsonl_prompt_write", "jsonl_prompt_tables", "jsonl_step_write", "scan_reduce", "scan_apply"] if JSONL else [
+         "jsonl_prompt_check", "jsonl_prompt_write", "jsonl_prompt_tables", "jsonl_step_write", "jsonl_lookup", "scan_reduce", "scan_apply"] if JSONL else [
          "trace_nl_count", "trace_nl_scan", "trace_nl_write", "trace_classify", "trace_tokens",
          "trace_ids", "string_words", "gather_keys", "trace_gather", "trace_steprow", "trace_runs",
          "trace_run_scan", "trace_group_key", "radix_hist", "radix_scan", "radix_scatter", "trace_group",
