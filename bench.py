@@ -505,6 +505,8 @@ def run_ours(args, world, rank, local):
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0:  # last, after every communicator log line
+        if world > 1:
+            nccl_log_summary()
         sys.stderr.flush()
         print(json.dumps(result), flush=True)
 
@@ -839,12 +841,36 @@ def bench_dedup(args, ctx, torch, dev, stream):
     return out
 
 
+NCCL_LOG = "/tmp/rs_bench_nccl.%h.%p.log"
+
+
 def nccl_log_on(env):
     """NCCL's INIT log (rank count, transports) at INFO, even where the image
-    presets a quieter NCCL_DEBUG (VERSION / WARN)."""
+    presets a quieter NCCL_DEBUG (VERSION / WARN), written to per-process
+    files (NCCL's default is stdout, where only the JSON line may go); rank 0
+    echoes its key lines to stderr at the end (nccl_log_summary)."""
     if env.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
         env["NCCL_DEBUG"] = "INFO"
         env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    if env.get("NCCL_DEBUG_FILE", "") in ("", "/dev/stdout"):
+        env["NCCL_DEBUG_FILE"] = NCCL_LOG
+
+
+def nccl_log_summary():
+    """The communicator lines of the NCCL logs (ranks, NVLS / NVLink paths) on stderr."""
+    import glob
+    keys = ("NVLS", "nRanks", "Init COMPLETE", "P2P/CUMEM", "via P2P", "NCCL version", "comm 0x")
+    shown = 0
+    for path in sorted(glob.glob("/tmp/rs_bench_nccl.*.log")):
+        try:
+            with open(path, errors="replace") as f:
+                for line in f:
+                    if any(k in line for k in keys) and shown < 40:
+                        sys.stderr.write(line)
+                        shown += 1
+            os.remove(path)
+        except OSError:
+            pass
 
 
 def relaunch_cmd(argv, n, port):
