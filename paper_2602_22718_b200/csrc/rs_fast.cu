@@ -280,10 +280,14 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
   int32_t* segend = cur;  // cur is dead after the scatter
   for (int k = tid; k < D; k += kBuildT) segend[k] = ss.seg[so + k].y;
   __syncthreads();
-  if (tid == 0) {  // greedy windows of whole buckets (<= kWin records; a wider bucket alone)
-    int nw = 0, k0 = 0, ws = 0;
-    while (k0 < D && nw < kMaxWin) {
-      wb[nw++] = k0;
+  // Greedy windows of whole buckets (<= kWin records; a wider bucket alone).
+  // Where the next window would start if one started at bucket k0 is a
+  // binary search per bucket, done by all threads (in the window region,
+  // free until the windows); thread 0 then only follows the chain.
+  {
+    uint16_t* nxt = reinterpret_cast<uint16_t*>(cur + kBuildCur);
+    for (int k0 = tid; k0 < D; k0 += kBuildT) {
+      const int ws = k0 == 0 ? 0 : segend[k0 - 1];
       int k1 = k0 + 1;
       if (segend[k0] - ws <= kWin) {  // largest k1 with segend[k1 - 1] <= ws + kWin
         int lo = k0 + 1, hi = D;
@@ -294,15 +298,26 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
         }
         k1 = lo;
       } else if (segend[k0] - ws > kWide) {
-        nw = -1;
-        break;
+        k1 = 0xffff;  // too wide for the fast path
       }
-      ws = segend[k1 - 1];
-      k0 = k1;
+      nxt[k0] = (uint16_t)k1;
     }
-    if (nw >= 0 && k0 < D) nw = -1;  // more windows than kMaxWin
-    if (nw >= 0) wb[nw] = D;
-    s_nw = nw;
+    __syncthreads();
+    if (tid == 0) {
+      int nw = 0, k0 = 0;
+      while (k0 < D && nw < kMaxWin) {
+        wb[nw++] = k0;
+        const int k1 = nxt[k0];
+        if (k1 == 0xffff) {
+          nw = -1;
+          break;
+        }
+        k0 = k1;
+      }
+      if (nw >= 0 && k0 < D) nw = -1;  // more windows than kMaxWin
+      if (nw >= 0) wb[nw] = D;
+      s_nw = nw;
+    }
   }
   __syncthreads();
   RS_PH(3);
