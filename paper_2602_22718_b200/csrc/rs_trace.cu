@@ -1167,7 +1167,10 @@ extern "C" int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes
 namespace rs {
 
 int trace_stage_text(rs_ctx* ctx, const char* text, int64_t n_bytes, int device_ptr, char** d_text) {
-  const size_t need = abytes(n_bytes + 64, 1);
+  // 4 KB of slack: the warp scans load whole 512-byte steps (two 1 KB
+  // windows in the token scan) past the end of the last line; the bytes
+  // beyond the text are masked out, they only have to be readable
+  const size_t need = abytes(n_bytes + 4096, 1);
   if (need > ctx->in_cap) {
     RS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     if (ctx->in_buf) cudaFree(ctx->in_buf);

@@ -84,7 +84,7 @@ namespace rs {
 // "<trace>:<line + 1>: what" as RS_E_PARSE (the reader's origin:lineno form).
 int trace_parse_error(int64_t line, const std::string& what);
 
-// The text, 16-byte aligned and padded with 64 zero bytes, in the context's
+// The text, 16-byte aligned, padded (4 KB: 64 zero bytes, then readable slack), in the context's
 // input buffer (host bytes copied, device bytes copied on the device).
 int trace_stage_text(rs_ctx* ctx, const char* text, int64_t n_bytes, int device_ptr, char** d_text);
 
