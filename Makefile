@@ -92,10 +92,20 @@ $(SHIM_OUT)/training_b200.cpp: $(REF)/src/training.cpp $(PKG)/shim/patches/train
 $(SHIM_OUT)/training_b200.o: $(SHIM_OUT)/training_b200.cpp $(PKG)/shim/rollsim_b200.hpp
 	$(CXXREF) -I$(PKG)/shim -c $< -o $@
 
-$(SHIM_OUT)/librollsim_b200_train.a: $(SHIM_OBJS) $(SHIM_OUT)/training_b200.o \
-    $(addprefix $(REF_OBJ)/,$(addsuffix .o,$(filter-out training,$(REF_KEEP))))
-	ar rcs $@ $(SHIM_OBJS) $(SHIM_OUT)/training_b200.o \
-	    $(addprefix $(REF_OBJ)/,$(addsuffix .o,$(filter-out training,$(REF_KEEP))))
+# and the simulator's dispatch pass skipped while no actor holds a queued cut
+# (shim/patches/simulator_b200.patch; run_step's results are unchanged)
+$(SHIM_OUT)/simulator_b200.cpp: $(REF)/src/simulator.cpp $(PKG)/shim/patches/simulator_b200.patch
+	@mkdir -p $(SHIM_OUT)
+	patch -s -o $@ $(REF)/src/simulator.cpp $(PKG)/shim/patches/simulator_b200.patch
+
+$(SHIM_OUT)/simulator_b200.o: $(SHIM_OUT)/simulator_b200.cpp
+	$(CXXREF) -c $< -o $@
+
+$(SHIM_OUT)/librollsim_b200_train.a: $(SHIM_OBJS) $(SHIM_OUT)/training_b200.o $(SHIM_OUT)/simulator_b200.o \
+    $(addprefix $(REF_OBJ)/,$(addsuffix .o,$(filter-out training simulator,$(REF_KEEP))))
+	rm -f $@
+	ar rcs $@ $(SHIM_OBJS) $(SHIM_OUT)/training_b200.o $(SHIM_OUT)/simulator_b200.o \
+	    $(addprefix $(REF_OBJ)/,$(addsuffix .o,$(filter-out training simulator,$(REF_KEEP))))
 
 $(SHIM_OUT)/c5_bench_train: $(PKG)/shim/tools/c5_bench.cpp $(SHIM_OUT)/librollsim_b200_train.a $(LIB)
 	$(CXXREF) $< -o $@ $(SHIM_OUT)/librollsim_b200_train.a -L$(PKG) -lrs_b200 \
@@ -124,6 +134,7 @@ $(SHIM_OUT)/%.o: $(PKG)/shim/%.cpp $(PKG)/shim/rs_shim.hpp $(PKG)/shim/rollsim_b
 	$(CXXREF) -c $< -o $@
 
 $(SHIM_OUT)/librollsim_b200.a: $(SHIM_OBJS) $(addprefix $(REF_OBJ)/,$(addsuffix .o,$(REF_KEEP)))
+	rm -f $@
 	ar rcs $@ $(SHIM_OBJS) $(addprefix $(REF_OBJ)/,$(addsuffix .o,$(REF_KEEP)))
 
 $(SHIM_OUT)/%_b200: $(REF)/tests/%.cpp $(SHIM_OUT)/librollsim_b200.a $(LIB)
