@@ -1183,7 +1183,7 @@ __device__ int warp_int_array(const unsigned char* t, int64_t p, int64_t e, int3
 // fallback on lane 0 for arrays outside the fast form). Pass 1 records the
 // child like js_child_kernel; pass 2 writes the id and the tokens.
 template <bool kWrite>
-__global__ void js_prompt_kernel(const char* text, const JCont* conts, const unsigned long long* cscan,
+__global__ void __launch_bounds__(128, 8) js_prompt_kernel(const char* text, const JCont* conts, const unsigned long long* cscan,
                                  int64_t c0, int64_t P, const int64_t* lb, int64_t nb, int64_t pc,
                                  JChild* ch, const int64_t* id_off, const int64_t* int_off, char* ids,
                                  int32_t* ints, unsigned int* first_err) {
