@@ -32,11 +32,12 @@
 // escape, \u surrogate pairs, UTF-8 validation and no raw control
 // characters; number grammar; duplicate keys (the last wins); get<int> from
 // integers (int64 / uint64 truncation), booleans and floats (truncation,
-// INT_MIN out of range); "prompts": null; "lengths": null; "scheduled"
-// absent (the lengths keys in map order).
+// INT_MIN out of range); "prompts": null; "lengths": null or an array
+// (items() keys "0", "1", ...); "scheduled" absent (the lengths keys in map
+// order).
 // Rejected as RS_E_PARSE "unsupported" although nlohmann reads them:
-// "prompts" given as an object, "lengths" given as an array, nesting deeper
-// than 256, and floats converted to int that lie within 1e-6 below an
+// "prompts" given as an object, nesting deeper than 256, and floats
+// converted to int that lie within 1e-6 below an
 // integer (where the double rounding decides the result) or have more than
 // 18 significant digits or an exponent beyond +-60.
 #include <algorithm>
@@ -739,7 +740,6 @@ __global__ void js_line_kernel(const char* text, const int64_t* line_start, int6
         if (cont) {
           int r2 = role;
           if (role == kRPrompts && c == '{') r2 = -kJUnsup;   // "prompts" as an object
-          if (role == kRLengths && c == '[') r2 = -kJUnsup;   // "lengths" as an array
           if (role == kRSched && c == '{') r2 = -kJErr;       // get<vector<string>> of an object
           const int64_t np = add_cont(in.p, r2 < 0 ? kRValidate : r2);
           if (np < 0) {
@@ -942,6 +942,12 @@ __global__ void js_child_kernel(const char* text, const JCont* conts, const unsi
         }
         if (!err) err = jskip(in);
       }
+    } else if (jc.role == kRLengths) {  // "lengths" as an array: items() keys "0", "1", ...
+      r.id_len = 0;                      // (the host names them)
+      r.ints_at = in.p;
+      int64_t k;
+      err = jint_array(in, kWrite ? ints + int_off[u] : nullptr, &k);
+      r.n_int = k;
     } else if (jc.role == kRSched) {
       if (in.p >= in.e || t[in.p] != '"') {
         err = jskip(in);  // get<std::string> of a non-string: type_error
@@ -1665,7 +1671,17 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     std::vector<int32_t> st_idx, e_off{0}, e_prompt, lens;
     int prev_step = -1;
     const int32_t G = tr->g;
+    // "lengths" given as an array: nlohmann's items() names the elements
+    // "0", "1", ...; their table indices are looked up here
+    std::vector<std::string> idx_key(any_steps ? NCH : 0);
+    for (int64_t c = 0; c < NC && any_steps; ++c)
+      if (hc[c].role == kRLengths && !hc[c].is_obj)
+        for (unsigned long long u = hcs[c]; u < hcs[c + 1]; ++u) {
+          idx_key[u] = std::to_string(u - hcs[c]);
+          hp[u] = id_index(idx_key[u]);
+        }
     auto child_id = [&](unsigned long long u) {
+      if (!idx_key[u].empty()) return idx_key[u];
       return std::string(h_ids.data() + h_id_off[u], h_ids.data() + h_id_off[u] + h_il[u]);
     };
     auto table_id = [&](int32_t p) {
@@ -1698,7 +1714,10 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
           }
           last_u[p] = (int64_t)u;
         }
+      // items() of an array runs in element order (an object's, in key order)
+      const bool arr = len_c[ln] >= 0 && !hc[len_c[ln]].is_obj;
       if (known) {
+        const std::vector<int32_t> keys_items = arr ? keys : std::vector<int32_t>();
         if ((int64_t)keys.size() * 16 > (int64_t)P) {  // dense: the stamps in table order
           keys.clear();
           for (int32_t p = 0; p < P; ++p)
@@ -1714,7 +1733,7 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
             sched_u.push_back(u);
           }
         } else if (!hl[ln].has_sched) {
-          sched = keys;
+          sched = arr ? keys_items : keys;
         }
         if (sched.empty()) return fail(RS_E_VALIDATION, "step " + sn + " schedules no prompts");
         for (size_t i = 0; i < sched.size(); ++i) {
@@ -1758,7 +1777,10 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
       if (hl[ln].has_sched && sched_c[ln] >= 0) {
         for (unsigned long long u = hcs[sched_c[ln]]; u < hcs[sched_c[ln] + 1]; ++u) sched.push_back(child_id(u));
       } else if (!hl[ln].has_sched) {
-        for (const auto& kv : lmap) sched.push_back(kv.first);
+        if (arr)
+          for (unsigned long long u = hcs[len_c[ln]]; u < hcs[len_c[ln] + 1]; ++u) sched.push_back(child_id(u));
+        else
+          for (const auto& kv : lmap) sched.push_back(kv.first);
       }
       if (sched.empty()) return fail(RS_E_VALIDATION, "step " + sn + " schedules no prompts");
       std::set<std::string> seen;

@@ -196,11 +196,22 @@ def test_validation_errors():
 
 def test_unsupported_constructs_are_reported():
     """Valid for nlohmann, rejected here with RS_E_PARSE (rs.h)."""
-    for text in ['{"type":"header","g":1,"prompts":{"k":{"id":"a","ground_truth_len":1,"token_ids":[1]}}}',
-                 json.dumps(header(P2)) + '\n{"step":0,"lengths":[[1,2]]}']:
-        ref().trace_prompts(text.encode(), "jsonl") if "lengths" not in text else None
-        with pytest.raises(ParseError, match="not support"):
-            rs.TraceCSR(text.encode() + b"\n", fmt="jsonl")
+    text = '{"type":"header","g":1,"prompts":{"k":{"id":"a","ground_truth_len":1,"token_ids":[1]}}}'
+    ref().trace_prompts(text.encode(), "jsonl")  # the reference reads it
+    with pytest.raises(ParseError, match="not support"):
+        rs.TraceCSR(text.encode() + b"\n", fmt="jsonl")
+
+
+def test_lengths_as_an_array():
+    """items() of an array: keys "0", "1", ... in map (string) order."""
+    ids = [{"id": str(i), "ground_truth_len": 3, "token_ids": [i + 1]} for i in range(12)]
+    arr = [[i + 1, i + 2] for i in range(12)]
+    same(lines(header(ids), {"step": 0, "lengths": arr}))
+    same(lines(header(ids), {"step": 0, "scheduled": ["3", "0", "11"], "lengths": {"3": [1, 1], "0": [2, 2], "11": [3, 3]}},
+               {"step": 1, "scheduled": [str(i) for i in range(12)], "lengths": arr}))
+    same_error(lines(header(P2), {"step": 0, "lengths": [[1, 2], [3, 4]]}))   # "0" is not a prompt
+    same_error(lines(header(ids), {"step": 0, "lengths": [[1, 2], [3]]}))     # "1" needs 2 lengths
+    same_error(lines(header(ids), {"step": 0, "lengths": [[1, 2], "x"]}))     # an element not an array
 
 
 @pytest.mark.slow
