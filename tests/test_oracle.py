@@ -275,3 +275,27 @@ def test_reference_trace_reader_wrapper():
     with pytest.raises(OracleError) as e:
         ref().trace_prompts(trace_csv([("a", 1, [1])], header=False))
     assert e.value.status == 7
+
+
+@needs_ref
+def test_reference_trace_steps_and_jsonl_wrappers():
+    """ref_trace_steps lays the step table out as rs_trace_csr_steps_copy
+    does (batch order, indices into the id-sorted table, g lengths per
+    entry), for both formats; ref_trace_convert round-trips CSV <-> JSONL."""
+    from cases import trace_csv
+    text = trace_csv([("b", 5, [1, 2, 3]), ("a", 9, [4])], g=2,
+                     steps=[(0, [("b", [7, 8]), ("a", [5, 6])]), (3, [("a", [1, 2])])])
+    s = ref().trace_steps(text)
+    assert s["step_idx"].tolist() == [0, 3] and s["entry_off"].tolist() == [0, 2, 3]
+    assert s["entry_prompt"].tolist() == [1, 0, 0]
+    assert s["lengths"].tolist() == [[7, 8], [5, 6], [1, 2]]
+    jsonl = ref().trace_convert(text, "csv", "jsonl")
+    assert jsonl.startswith(b'{"g":2') and b'"type":"header"' in jsonl
+    j = ref().trace_steps(jsonl, "jsonl")
+    # JSONL keeps the batch order in "scheduled" next to the id-keyed lengths
+    assert j["step_idx"].tolist() == [0, 3] and j["entry_prompt"].tolist() == [1, 0, 0]
+    assert j["lengths"].tolist() == [[7, 8], [5, 6], [1, 2]]
+    assert ref().trace_convert(jsonl, "jsonl", "csv") == ref().trace_convert(text, "csv", "csv")
+    with pytest.raises(OracleError) as e:
+        ref().trace_steps(b'{"type":"header","g":1,"prompts":[]}\n{"step":0}\n', "jsonl")
+    assert e.value.status == 7
