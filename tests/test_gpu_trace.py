@@ -241,3 +241,62 @@ def test_large_step_table_matches_reference():
     """~200k step rows (50 steps x up to 512 prompts x g = 8)."""
     text, _, _ = steps_trace(11, 512, 50, g=8, max_len=16)
     same_steps(text)
+
+
+def fuzz_csv(seed, n=120, steps=4, g=3, defect=None):
+    """A CSV trace in random layouts: blanks and tabs around fields and
+    tokens, CRLF, blank lines, signs, glued and overlong numbers in the
+    prompt lists; optionally one defect in the step rows."""
+    rng = np.random.RandomState(seed)
+    sp = lambda: " " * int(rng.randint(0, 3)) + ("\t" if rng.rand() < 0.2 else "")
+    lines = [f"# g {g}", "# max_prompt_len 600"]
+    ids = [f"id{i:04d}" for i in rng.permutation(n)]
+    for pid in ids:
+        toks = []
+        for _ in range(int(rng.randint(1, 400))):
+            r = rng.rand()
+            toks.append(str(rng.randint(0, 32000)) if r < 0.9 else
+                        ("-" + str(rng.randint(0, 99)) if r < 0.95 else
+                         ("+" + str(rng.randint(0, 99)) if r < 0.98 else "12-3")))
+        lines.append(sp() + f"# prompt {pid} {int(rng.randint(1, 2048))} " + " ".join(toks) + sp())
+        if rng.rand() < 0.05:
+            lines.append(sp())
+    lines.append(" step_idx , prompt_id,response_idx , actual_len ")
+    rows = []
+    st = 0
+    for _ in range(steps):
+        for pid in rng.permutation(ids)[: int(rng.randint(1, n))]:
+            for r in range(g):
+                rows.append(f"{sp()}{st}{sp()},{sp()}{pid}{sp()},{sp()}{r}{sp()},{sp()}{int(rng.randint(1, 2048))}{sp()}")
+        st += int(rng.randint(1, 5))
+    if defect is not None and rows:
+        i = int(rng.randint(0, len(rows)))
+        rows[i] = {"fields": rows[i] + ",9", "int": rows[i].replace(",", ",x", 1),
+                   "order": rows[i].replace(",0,", ",1,", 1) if ",0," in rows[i] else rows[i] + ",",
+                   "long": rows[i].split(",")[0] + ",idzz,0,1", "len": rows[i].rsplit(",", 1)[0] + ",0"}[defect]
+    lines += rows
+    text = "\n".join(lines) + "\n"
+    if rng.rand() < 0.5:
+        text = text.replace("\n", "\r\n")
+    return text.encode()
+
+
+def test_csv_fuzz_layouts():
+    for seed in range(6):
+        text = fuzz_csv(seed)
+        try:
+            ref().trace_prompts(text)
+        except OracleError as e:
+            pytest.fail(f"seed {seed}: the reference rejects it: {e}")
+        same_as_reference(text)
+        same_steps(text)
+
+
+def test_csv_fuzz_defects():
+    for seed, d in enumerate(["fields", "int", "order", "long", "len"] * 3):
+        text = fuzz_csv(100 + seed, n=40, steps=3, defect=d)
+        try:
+            ref().trace_steps(text)
+            same_steps(text)
+        except OracleError:
+            same_error(text)
