@@ -871,8 +871,9 @@ struct JChild {   // pass-1 results of one child
   int32_t cont, line;
 };
 
-// Pass 1 (write = false): validate, measure. Pass 2: write ids and ints at
-// their scanned offsets.
+// Every child but the prompt objects (js_prompt_kernel), a thread each.
+// Pass 1 (write = false): validate, measure. Pass 2: write the ids and ints
+// of the roles in wrole (a bit mask) at their scanned offsets.
 template <bool kWrite>
 __global__ void js_child_kernel(const char* text, const JCont* conts, const unsigned long long* cscan,
                                 int64_t nc, const int64_t* lb, int64_t nb, int64_t total, JChild* ch,
@@ -905,7 +906,7 @@ __global__ void js_child_kernel(const char* text, const JCont* conts, const unsi
       r.line = jc.line;
     }
     const JCont jc = conts[ci];
-    if (!kWrite && jc.role == kRPrompts) continue;  // js_prompt_kernel: a warp per prompt
+    if (jc.role == kRPrompts) continue;  // js_prompt_kernel: a warp per prompt object
     JIn in{t, r.a, r.e};
     int err = 0;
     skip_ws(in);
@@ -928,8 +929,6 @@ __global__ void js_child_kernel(const char* text, const JCont* conts, const unsi
           r.ints_at = in.p;
           int64_t k;
           err = jint_array(in, kWrite ? ints + int_off[u] : nullptr, &k);
-          if (err == kJErr && !kWrite) {  // a syntax error is still an error; keep kJErr
-          }
           r.n_int = k;
         }
       } else {
@@ -957,69 +956,6 @@ __global__ void js_child_kernel(const char* text, const JCont* conts, const unsi
         int64_t l;
         err = jstring(in, kWrite ? ids + id_off[u] : nullptr, kWrite ? r.id_len : 0, &l);
         r.id_len = l;
-      }
-    } else if (jc.role == kRPrompts) {
-      if (kWrite) {  // the id and the tokens, from the recorded positions
-        JIn is{t, r.id_at, r.e};
-        int64_t l;
-        jstring(is, ids + id_off[u], r.id_len, &l);
-        JIn it{t, r.ints_at, r.e};
-        int64_t k;
-        jint_array(it, ints + int_off[u], &k);
-        continue;
-      }
-      // a prompt object: id / ground_truth_len / token_ids (the last of each)
-      bool has_id = false, has_gt = false, has_tok = false;
-      if (in.p >= in.e || t[in.p] != '{') {
-        err = jskip(in);  // at() on a non-object: type_error
-        if (!err) err = kJErr;
-      } else {
-        ++in.p;
-        skip_ws(in);
-        if (in.p < in.e && t[in.p] == '}') ++in.p;
-        else
-          while (!err) {
-            static const char* const kP[] = {"id", "ground_truth_len", "token_ids"};
-            const int key = jkey(in, kP, 3, &err);
-            if (err) break;
-            if (key == 0) {
-              if (in.p >= in.e || t[in.p] != '"') {
-                err = jskip(in);
-                if (!err) err = kJErr;
-              } else {
-                r.id_at = in.p;
-                err = jstring(in, nullptr, 0, &r.id_len);
-                has_id = true;
-              }
-            } else if (key == 1) {
-              err = jint(in, &r.gt);
-              has_gt = true;
-            } else if (key == 2) {
-              r.ints_at = in.p;
-              const unsigned char c0 = in.p < in.e ? t[in.p] : 0;
-              err = jint_array(in, nullptr, &r.n_int);
-              if (err == kJErr && c0 != '[') {  // a type_error, but the value must still parse
-                JIn tmp{t, r.ints_at, r.e};
-                err = jskip(tmp) ? kJErr : kJErr;
-              }
-              has_tok = true;
-            } else {
-              err = jskip(in);
-            }
-            if (err) break;
-            skip_ws(in);
-            if (in.p < in.e && t[in.p] == ',') {
-              ++in.p;
-              skip_ws(in);
-              continue;
-            }
-            if (in.p < in.e && t[in.p] == '}') {
-              ++in.p;
-              break;
-            }
-            err = kJErr;
-          }
-        if (!err && !(has_id && has_gt && has_tok)) err = kJErr;
       }
     } else {
       err = jskip(in);
