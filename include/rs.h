@@ -343,9 +343,8 @@ int rs_trace_csr_parse(rs_ctx* ctx, const char* text, int64_t n_bytes, int devic
  * then one {"step","scheduled","lengths"} object per line, each read by
  * nlohmann::json) into the same handle. RS_E_PARSE at the first malformed
  * line (JSON syntax or the schema's types), then RS_E_VALIDATION. Not read
- * (RS_E_PARSE "not support"): "prompts" as an object, nesting deeper than
- * 256, floats converted to int within 1e-6 below an integer or with an
- * exponent beyond +-60. */
+ * (RS_E_PARSE "not support"): nesting deeper than 256, floats converted to
+ * int within 1e-6 below an integer or with an exponent beyond +-60. */
 int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n_bytes, int device_ptr,
                              rs_trace_csr** out);
 int rs_trace_csr_info(const rs_trace_csr* trace, int32_t* count, int64_t* n_tokens,

@@ -35,9 +35,10 @@
 // INT_MIN out of range); "prompts": null; "lengths": null or an array
 // (items() keys "0", "1", ...); "scheduled" absent (the lengths keys in map
 // order).
-// Rejected as RS_E_PARSE "unsupported" although nlohmann reads them:
-// "prompts" given as an object, nesting deeper than 256, and floats
-// converted to int that lie within 1e-6 below an
+// "prompts" given as an object (its values in key order, the last member
+// of a repeated key). Rejected as RS_E_PARSE "unsupported" although nlohmann
+// reads them: nesting deeper than 256, and floats converted to int that lie
+// within 1e-6 below an
 // integer (where the double rounding decides the result) or have more than
 // 18 significant digits or an exponent beyond +-60.
 #include <algorithm>
@@ -53,6 +54,8 @@
 
 namespace rs {
 size_t rank_strings_device_bytes(int64_t n, int64_t maxlen);
+int rank_strings_device(rs_ctx* ctx, const char* d_bytes, const int64_t* d_off, int64_t n,
+                        int64_t maxlen, uint32_t* d_perm);
 
 namespace {
 
@@ -739,7 +742,6 @@ __global__ void js_line_kernel(const char* text, const int64_t* line_start, int6
         if (role != kRValidate) demote(role);
         if (cont) {
           int r2 = role;
-          if (role == kRPrompts && c == '{') r2 = -kJUnsup;   // "prompts" as an object
           if (role == kRSched && c == '{') r2 = -kJErr;       // get<vector<string>> of an object
           const int64_t np = add_cont(in.p, r2 < 0 ? kRValidate : r2);
           if (np < 0) {
@@ -867,6 +869,9 @@ struct JChild {   // pass-1 results of one child
   int64_t id_len;      // prompt id / scheduled id / lengths key: unescaped bytes
   int64_t n_int;       // prompt tokens / length values
   int64_t id_at, ints_at;  // where the id string and the int array start (pass 2)
+  int64_t key_at;      // "prompts" given as an object: the member's key
+  int32_t key_len;     // its unescaped bytes
+  int32_t serr;        // its schema error (counts only if no later member repeats the key)
   int32_t gt, err;
   int32_t cont, line;
 };
@@ -1159,9 +1164,40 @@ __global__ void __launch_bounds__(128, 8) js_prompt_kernel(const char* text, con
     r.line = jc.line;
     // lane 0 walks the members; at "token_ids" the warp reads the array
     JIn in{t, r.a, r.e};
-    int err = 0;
+    int err = 0, syn = 0;
+    int64_t val_end = -1;  // object members: where the value ends (syntax checked first)
     bool has_id = false, has_gt = false, has_tok = false, open_ok = false;
-    if (lane == 0) {
+    if (lane == 0 && jc.is_obj) {
+      // "key": value — the key kept for the duplicate rule, the value's JSON
+      // checked on its own: a syntax error always counts, a schema error only
+      // for the last member with this key (nlohmann keeps the last one)
+      skip_ws(in);
+      int64_t kl = 0;
+      if (in.p >= in.e || t[in.p] != '"') syn = kJErr;
+      else {
+        r.key_at = in.p;
+        syn = jstring(in, nullptr, 0, &kl);
+        r.key_len = (int32_t)kl;
+      }
+      if (!syn) {
+        skip_ws(in);
+        if (in.p >= in.e || t[in.p] != ':') syn = kJErr;
+        else ++in.p;
+      }
+      if (!syn) {
+        skip_ws(in);
+        JIn v = in;
+        syn = jskip(v);
+        if (!syn) {
+          skip_ws(v);
+          if (v.p != v.e) syn = kJErr;
+          val_end = v.p;
+        }
+      }
+      if (syn) in.p = in.e;  // nothing more to read
+    }
+    syn = __shfl_sync(0xffffffffu, syn, 0);
+    if (lane == 0 && !syn) {
       skip_ws(in);
       if (in.p >= in.e || t[in.p] != '{') {
         err = jskip(in);
@@ -1172,7 +1208,7 @@ __global__ void __launch_bounds__(128, 8) js_prompt_kernel(const char* text, con
         open_ok = true;
       }
     }
-    bool done = !__shfl_sync(0xffffffffu, open_ok, 0);
+    bool done = syn || !__shfl_sync(0xffffffffu, open_ok, 0);
     bool first_m = true;
     while (!done) {
       int key = -1, want_arr = 0;
@@ -1250,13 +1286,72 @@ __global__ void __launch_bounds__(128, 8) js_prompt_kernel(const char* text, con
     }
     if (lane == 0) {
       if (!err && open_ok && !(has_id && has_gt && has_tok)) err = kJErr;
-      if (!err) {
+      if (!err && !jc.is_obj) {
         skip_ws(in);
         if (in.p != in.e) err = kJErr;
+      }
+      if (jc.is_obj) {  // the schema error waits for the duplicate rule
+        r.serr = syn ? 0 : err;
+        err = syn;
+        (void)val_end;
       }
       r.err = err;
       ch[u] = r;
       if (err) atomicMin(first_err, ((unsigned int)r.line << 1) | (err == kJUnsup ? 1u : 0u));
+    }
+  }
+}
+
+// "prompts" given as an object: the members' keys written out (for the
+// string ranking), then the duplicate rule — of the members sharing a key,
+// the last one is the prompt; the others are dropped (err = -1, after their
+// schema errors are ignored) and the survivors' schema errors reported.
+__global__ void js_key_write_kernel(const char* text, const JChild* ch, int64_t c0, int64_t n,
+                                    const int64_t* koff, char* keys) {
+  const unsigned char* t = reinterpret_cast<const unsigned char*>(text);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const JChild r = ch[c0 + i];
+    if (r.err) continue;
+    JIn in{t, r.key_at, r.e};
+    int64_t l;
+    jstring(in, keys + koff[i], r.key_len, &l);
+  }
+}
+
+__global__ void js_key_sizes_kernel(const JChild* ch, int64_t c0, int64_t n, unsigned long long* kl) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    kl[i] = ch[c0 + i].err ? 0ULL : (unsigned long long)ch[c0 + i].key_len;
+}
+
+__global__ void js_key_dedup_kernel(JChild* ch, int64_t c0, int64_t n, const uint32_t* perm,
+                                    const char* keys, const int64_t* koff, unsigned int* first_err,
+                                    uint32_t* kept) {
+  auto same = [&](uint32_t x, uint32_t y) {
+    const int64_t lx = koff[x + 1] - koff[x], ly = koff[y + 1] - koff[y];
+    if (lx != ly) return false;
+    for (int64_t j = 0; j < lx; ++j)
+      if (keys[koff[x] + j] != keys[koff[y] + j]) return false;
+    return true;
+  };
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = perm[r];
+    JChild& c = ch[c0 + i];
+    if (c.err) {  // a syntax error: already reported
+      kept[i] = 0;
+      continue;
+    }
+    bool last = true;  // no later member (higher index) with the same key
+    for (int64_t q = r - 1; q >= 0 && same(perm[q], i); --q) last &= perm[q] < i || ch[c0 + perm[q]].err;
+    for (int64_t q = r + 1; q < n && same(perm[q], i); ++q) last &= perm[q] < i || ch[c0 + perm[q]].err;
+    kept[i] = last ? 1u : 0u;
+    if (!last) {
+      c.err = -1;  // dropped: no prompt, no error
+    } else if (c.serr) {
+      c.err = c.serr;
+      atomicMin(first_err, ((unsigned int)c.line << 1) | (c.serr == kJUnsup ? 1u : 0u));
     }
   }
 }
@@ -1305,14 +1400,17 @@ __global__ void js_lookup_kernel(const JChild* ch, const JCont* conts, int64_t t
 
 // The header's prompts, in child order: their line-order tables for the
 // shared tail (token offsets, id offsets, ground truths).
-__global__ void js_prompt_tables_kernel(const JChild* ch, int64_t c0, int32_t P, const int64_t* id_off,
-                                        const int64_t* int_off, int64_t* p_id_off, int64_t* p_tok_off,
-                                        int32_t* p_gt) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= P;
+// (kidx: the prompt index of each member, nullptr when every child is one.)
+__global__ void js_prompt_tables_kernel(const JChild* ch, int64_t c0, int64_t nkids, const uint32_t* kidx,
+                                        const int64_t* id_off, const int64_t* int_off, int64_t* p_id_off,
+                                        int64_t* p_tok_off, int32_t* p_gt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= nkids;
        i += (int64_t)gridDim.x * blockDim.x) {
-    p_id_off[i] = id_off[c0 + i] - id_off[c0];
-    p_tok_off[i] = int_off[c0 + i] - int_off[c0];
-    if (i < P) p_gt[i] = ch[c0 + i].gt;
+    if (i < nkids && ch[c0 + i].err) continue;  // a dropped member
+    const int64_t k = kidx ? kidx[i] : i;
+    p_id_off[k] = id_off[c0 + i] - id_off[c0];
+    p_tok_off[k] = int_off[c0 + i] - int_off[c0];
+    if (i < nkids) p_gt[k] = ch[c0 + i].gt;
   }
 }
 
@@ -1439,7 +1537,9 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     for (int64_t c = 0; c < NC; ++c)
       if (hc[c].role == kRPrompts) pc = c;
     const int64_t c0 = pc >= 0 ? (int64_t)hcs[pc] : 0;
-    const int32_t P = pc >= 0 ? (int32_t)(hcs[pc + 1] - hcs[pc]) : 0;
+    const int64_t nkids = pc >= 0 ? (int64_t)(hcs[pc + 1] - hcs[pc]) : 0;  // prompt objects / members
+    const bool pobj = pc >= 0 && hc[pc].is_obj;  // "prompts" given as an object
+    int32_t P = (int32_t)nkids;                  // prompts (object: after the duplicate rule)
     auto wgrid = [&](int64_t n) {  // a warp per item, 128-thread blocks
       return (int)std::max<int64_t>(1, std::min<int64_t>((n + 3) / 4, 64 * (int64_t)ctx->num_sms));
     };
@@ -1447,10 +1547,48 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
       RS_LAUNCH(ctx, "jsonl_child_check", js_child_kernel<false>, grid(NCH), 128, 0, d_text, d_conts, cscan, NC,
                 lbv, NB, NCH, d_ch, (const int64_t*)nullptr, (const int64_t*)nullptr, (char*)nullptr,
                 (int32_t*)nullptr, small + 2, 0);
-    if (P > 0)
-      RS_LAUNCH(ctx, "jsonl_prompt_check", js_prompt_kernel<false>, wgrid(P), 128, 0, d_text, d_conts, cscan, c0,
-                (int64_t)P, lbv, NB, pc, d_ch, (const int64_t*)nullptr, (const int64_t*)nullptr, (char*)nullptr,
+    if (nkids > 0)
+      RS_LAUNCH(ctx, "jsonl_prompt_check", js_prompt_kernel<false>, wgrid(nkids), 128, 0, d_text, d_conts, cscan,
+                c0, nkids, lbv, NB, pc, d_ch, (const int64_t*)nullptr, (const int64_t*)nullptr, (char*)nullptr,
                 (int32_t*)nullptr, small + 2);
+    // "prompts" as an object: nlohmann keeps the last member of each key; the
+    // others are neither prompts nor schema errors
+    AsyncBuf b_keys;
+    uint32_t* kidx = nullptr;  // prompt index of each member (exclusive scan of the survivors)
+    if (pobj && nkids > 0) {
+      char* q = b_keys.alloc<char>(ctx->stream, abytes(nkids + 1, 8) * 3 + abytes(nkids + 1, 4) * 3 +
+                                                    scan_scratch_bytes(nkids + 1, 8));
+      if (!q) return fail(RS_E_NOMEM, "jsonl prompt keys: allocation failed");
+      auto* kl = (unsigned long long*)carve(q, abytes(nkids + 1, 8));
+      auto* koff = (unsigned long long*)carve(q, abytes(nkids + 1, 8));
+      auto* kpart = (unsigned long long*)carve(q, scan_scratch_bytes(nkids + 1, 8));
+      uint32_t* kperm = (uint32_t*)carve(q, abytes(nkids + 1, 4));
+      uint32_t* kept = (uint32_t*)carve(q, abytes(nkids + 1, 4));
+      kidx = (uint32_t*)carve(q, abytes(nkids + 1, 4));
+      RS_LAUNCH(ctx, "jsonl_key_sizes", js_key_sizes_kernel, grid(nkids), 256, 0, d_ch, c0, nkids, kl);
+      RS_TRY(exclusive_scan<unsigned long long>(ctx, kl, koff, nkids, kpart, koff + nkids));
+      std::vector<unsigned long long> hkl(nkids);
+      unsigned long long kbytes = 0;
+      RS_TRY(d2h(ctx, hkl.data(), kl, 8ull * nkids));
+      RS_TRY(d2h(ctx, &kbytes, koff + nkids, 8));
+      RS_TRY(sync_and_check(ctx));
+      int64_t maxk = 1;
+      for (unsigned long long v : hkl) maxk = std::max<int64_t>(maxk, (int64_t)v);
+      AsyncBuf b_kb;
+      char* keys = b_kb.alloc<char>(ctx->stream, kbytes + 1);
+      if (!keys) return fail(RS_E_NOMEM, "jsonl prompt keys: allocation failed");
+      RS_LAUNCH(ctx, "jsonl_key_write", js_key_write_kernel, grid(nkids), 256, 0, d_text, d_ch, c0, nkids,
+                (const int64_t*)koff, keys);
+      RS_TRY(arena_reserve(ctx, rank_strings_device_bytes(nkids, maxk) + (1 << 16)));
+      RS_TRY(rank_strings_device(ctx, keys, (const int64_t*)koff, nkids, maxk, kperm));
+      RS_LAUNCH(ctx, "jsonl_key_dedup", js_key_dedup_kernel, grid(nkids), 256, 0, d_ch, c0, nkids, kperm, keys,
+                (const int64_t*)koff, small + 2, kept);
+      RS_TRY(exclusive_scan<uint32_t>(ctx, kept, kidx, nkids, (uint32_t*)kpart, kidx + nkids));
+      uint32_t np = 0;
+      RS_TRY(d2h(ctx, &np, kidx + nkids, 4));
+      RS_TRY(sync_and_check(ctx));
+      P = (int32_t)np;
+    }
     // the first error line over the lines and the children
     std::vector<JLine> hl(L);
     unsigned int cerr = ~0u;
@@ -1512,11 +1650,11 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     uint32_t* d_perm = (uint32_t*)carve(pb, abytes(P + 1, 4));
     int64_t maxid = 1;
     if (P > 0) {
-      RS_LAUNCH(ctx, "jsonl_prompt_write", js_prompt_kernel<true>, wgrid(P), 128, 0, d_text, d_conts, cscan, c0,
-                (int64_t)P, lbv, NB, pc, d_ch, (const int64_t*)id_off, (const int64_t*)int_off, d_ids, d_tok,
+      RS_LAUNCH(ctx, "jsonl_prompt_write", js_prompt_kernel<true>, wgrid(nkids), 128, 0, d_text, d_conts, cscan,
+                c0, nkids, lbv, NB, pc, d_ch, (const int64_t*)id_off, (const int64_t*)int_off, d_ids, d_tok,
                 small + 2);
-      RS_LAUNCH(ctx, "jsonl_prompt_tables", js_prompt_tables_kernel, grid(P + 1), 256, 0, d_ch, c0, P,
-                (const int64_t*)id_off, (const int64_t*)int_off, p_id_off, p_tok_off, p_gt);
+      RS_LAUNCH(ctx, "jsonl_prompt_tables", js_prompt_tables_kernel, grid(nkids + 1), 256, 0, d_ch, c0, nkids,
+                (const uint32_t*)kidx, (const int64_t*)id_off, (const int64_t*)int_off, p_id_off, p_tok_off, p_gt);
       std::vector<int64_t> ioff(P + 1);
       RS_TRY(d2h(ctx, ioff.data(), p_id_off, 8ull * (P + 1)));
       RS_TRY(sync_and_check(ctx));

@@ -194,12 +194,30 @@ def test_validation_errors():
         same_error(text)
 
 
-def test_unsupported_constructs_are_reported():
-    """Valid for nlohmann, rejected here with RS_E_PARSE (rs.h)."""
-    text = '{"type":"header","g":1,"prompts":{"k":{"id":"a","ground_truth_len":1,"token_ids":[1]}}}'
-    ref().trace_prompts(text.encode(), "jsonl")  # the reference reads it
-    with pytest.raises(ParseError, match="not support"):
-        rs.TraceCSR(text.encode() + b"\n", fmt="jsonl")
+def test_prompts_as_an_object():
+    """Range-for over an object visits its values in key order; of members
+    with the same key only the last exists (its schema decides, the earlier
+    ones' types do not matter, their syntax does)."""
+    pa = '{"id":"a","ground_truth_len":1,"token_ids":[1,2]}'
+    pb = '{"id":"b","ground_truth_len":2,"token_ids":[3]}'
+    ok = [
+        '{"type":"header","g":1,"prompts":{"k":%s,"j":%s}}' % (pa, pb),
+        '{"type":"header","g":1,"prompts":{"k":{"id":5},"j":%s,"k":%s}}' % (pb, pa),   # bad, then replaced
+        '{"type":"header","g":1,"prompts":{"\\u006b":[1],"k":%s}}' % pa,                # escaped key duplicate
+        '{"type":"header","g":1,"prompts":{}}',
+        '{"type":"header","g":1,"prompts":{"x":%s,"y":%s,"z":%s}}\n{"step":0,"lengths":{"a":[4],"b":[5]}}'
+        % (pa, pb, pb.replace('"b"', '"c"')),
+    ]
+    for text in ok:
+        same(text.encode() + b"\n")
+    bad = [
+        '{"type":"header","g":1,"prompts":{"k":%s,"k":{"id":5}}}' % pa,     # the last one is bad
+        '{"type":"header","g":1,"prompts":{"k":{"id":5,},"k":%s}}' % pa,    # syntax of a dropped one
+        '{"type":"header","g":1,"prompts":{"k":%s,"j":3}}' % pa,            # a member not an object
+        '{"type":"header","g":1,"prompts":{"k":%s,"j":%s}}' % (pa, pa),     # duplicate prompt ids
+    ]
+    for text in bad:
+        same_error(text.encode() + b"\n")
 
 
 def test_lengths_as_an_array():
