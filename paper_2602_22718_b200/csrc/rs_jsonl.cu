@@ -38,9 +38,8 @@
 // "prompts" given as an object (its values in key order, the last member
 // of a repeated key). Rejected as RS_E_PARSE "unsupported" although nlohmann
 // reads them: nesting deeper than 256, and floats converted to int that lie
-// within 1e-6 below an
-// integer (where the double rounding decides the result) or have more than
-// 18 significant digits or an exponent beyond +-60.
+// within 1e-6 below an integer (where the double rounding decides the result)
+// or have a decimal exponent beyond +-60.
 #include <algorithm>
 #include <cstring>
 #include <map>
