@@ -982,11 +982,11 @@ __global__ void js_child_kernel(const char* text, const JCont* conts, const unsi
 // previous non-blank one (a number after ',' or the '[', a ',' after a
 // number, the ']' after a number or the '['), no '-' except at a number's
 // start, no leading zero, at most 18 digits. Counts (out == nullptr) or
-// writes the values. Returns 0 (with *count and *end, the position after
+// writes the first cap values. Returns 0 (with *count and *end, the position after
 // the ']') or 1 when the array is not of that form — a float, a boolean, a
 // longer number, or a syntax error: the caller's serial path then decides.
-__device__ int warp_int_array(const unsigned char* t, int64_t p, int64_t e, int32_t* out, int64_t* count,
-                              int64_t* end) {
+__device__ int warp_int_array(const unsigned char* t, int64_t p, int64_t e, int32_t* out, int64_t cap,
+                              int64_t* count, int64_t* end) {
   const int lane = threadIdx.x & 31;
   enum : int { kNone = 0, kStart = 1, kNum = 2, kComma = 3 };  // class of the last non-blank byte
   int carry = kStart;    // the '['
@@ -1104,7 +1104,7 @@ __device__ int warp_int_array(const unsigned char* t, int64_t p, int64_t e, int3
         int nd = 0;
         for (; q < e && t[q] >= '0' && t[q] <= '9'; ++q, ++nd) v = v * 10u + (unsigned)(t[q] - '0');
         if (nd > 18) bad = true;
-        if (out && !bad) out[k + before_n + idx] = (int32_t)(neg ? 0ULL - v : v);
+        if (out && !bad && k + before_n + idx < cap) out[k + before_n + idx] = (int32_t)(neg ? 0ULL - v : v);
         ++idx;
       }
     }
@@ -1124,11 +1124,67 @@ __device__ int warp_int_array(const unsigned char* t, int64_t p, int64_t e, int3
   }
 }
 
+// The count-only form of warp_int_array for the first pass: the array ends at
+// its first ']', holds (commas + 1) items, or none when only blanks precede
+// the ']'. Values and the grammar are not checked here — pass 2 reads the
+// same bytes with warp_int_array and reports what it rejects. Returns 1 (the
+// caller's serial path decides) when a '[', '{' or '"' comes before the ']'
+// or there is no ']' before e: there the first ']' need not be the array's.
+__device__ int warp_count_array(const unsigned char* t, int64_t p, int64_t e, int64_t* count, int64_t* end) {
+  const int lane = threadIdx.x & 31;
+  int64_t commas = 0;
+  bool nonblank = false;
+  for (int64_t b0 = p & ~(int64_t)15;; b0 += 512) {
+    if (b0 >= e) return 1;
+    const int64_t i = b0 + 16 * lane;
+    uint32_t C = 0, E = 0, W = 0, Q = 0;
+    {
+      const uint4 v = *reinterpret_cast<const uint4*>(t + i);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t x = w[q];
+        const uint32_t ws = __vcmpeq4(x, 0x20202020u) | __vcmpeq4(x, 0x09090909u) |
+                            __vcmpeq4(x, 0x0a0a0a0au) | __vcmpeq4(x, 0x0d0d0d0du);
+        const uint32_t nest = __vcmpeq4(x, 0x5b5b5b5bu) | __vcmpeq4(x, 0x7b7b7b7bu) | __vcmpeq4(x, 0x22222222u);
+        C |= pk4(__vcmpeq4(x, 0x2c2c2c2cu)) << (4 * q);
+        E |= pk4(__vcmpeq4(x, 0x5d5d5d5du)) << (4 * q);
+        W |= pk4(ws) << (4 * q);
+        Q |= pk4(nest) << (4 * q);
+      }
+      uint32_t valid = 0xffffu;
+      if (i < p) valid &= p - i >= 16 ? 0u : 0xffffu << (int)(p - i);
+      if (i + 16 > e) valid &= e > i ? 0xffffu >> (int)(16 - (e - i)) : 0u;
+      C &= valid;
+      E &= valid;
+      Q &= valid;
+      W = ~W & valid;  // from here: the non-blank bytes
+    }
+    const unsigned eb = __ballot_sync(0xffffffffu, E != 0);
+    const int close_lane = eb ? __ffs(eb) - 1 : 32;
+    uint32_t keep = lane < close_lane ? 0xffffu : 0u;  // the bytes before the ']'
+    if (lane == close_lane) keep = (1u << (__ffs(E) - 1)) - 1;
+    if (__any_sync(0xffffffffu, (Q & keep) != 0)) return 1;
+    commas += __reduce_add_sync(0xffffffffu, (unsigned)__popc(C & keep));
+    nonblank |= __any_sync(0xffffffffu, (W & keep) != 0);
+    if (close_lane < 32) {
+      const uint32_t ej = (uint32_t)__shfl_sync(0xffffffffu, (uint32_t)(__ffs(E) - 1), close_lane);
+      *count = nonblank ? commas + 1 : 0;
+      *end = b0 + 16 * close_lane + ej + 1;
+      return 0;
+    }
+  }
+}
+
 // One warp per prompt object (the children [c0, c0 + P) of the prompts
 // container): lane 0 reads the members, the warp reads "token_ids" (serial
-// fallback on lane 0 for arrays outside the fast form). Pass 1 records the
-// child like js_child_kernel; pass 2 writes the id and the tokens.
-template <bool kWrite>
+// fallback on lane 0 for arrays outside the fast form). kMode 0 (pass 1)
+// records the child like js_child_kernel, sizing "token_ids" by its commas
+// (warp_count_array); kMode 2 (pass 2) writes the id and the tokens,
+// checking the arrays as it goes, and kMode 1 only checks them — the error
+// path's pass, so a bad array is reported before an error on a later line.
+// Modes 1 and 2 report through first_err like pass 1.
+template <int kMode>
 __global__ void __launch_bounds__(128, 8) js_prompt_kernel(const char* text, const JCont* conts, const unsigned long long* cscan,
                                  int64_t c0, int64_t P, const int64_t* lb, int64_t nb, int64_t pc,
                                  JChild* ch, const int64_t* id_off, const int64_t* int_off, char* ids,
@@ -1140,19 +1196,25 @@ __global__ void __launch_bounds__(128, 8) js_prompt_kernel(const char* text, con
     const int64_t u = c0 + pi;
     JChild r{};
     const JCont jc = conts[pc];
-    if (kWrite) {
+    if (kMode != 0) {
       r = ch[u];
       if (r.err) continue;
-      if (lane == 0) {
+      if (kMode == 2 && lane == 0) {
         JIn is{t, r.id_at, r.e};
         int64_t l;
         jstring(is, ids + id_off[u], r.id_len, &l);
       }
-      int64_t cnt, endp;
-      const int st = warp_int_array(t, r.ints_at + 1, r.e, ints + int_off[u], &cnt, &endp);
-      if (st && lane == 0) {
-        JIn it{t, r.ints_at, r.e};
-        jint_array(it, ints + int_off[u], &cnt);
+      int32_t* out = kMode == 2 ? ints + int_off[u] : nullptr;
+      int64_t cnt = 0, endp;
+      const int st = warp_int_array(t, r.ints_at + 1, r.e, out, r.n_int, &cnt, &endp);
+      if (lane == 0) {
+        int err = 0;
+        if (st) {  // pass 1's count bounds the writes: items <= commas + 1
+          JIn it{t, r.ints_at, r.e};
+          err = jint_array(it, out, &cnt);
+        }
+        if (!err && cnt != r.n_int) err = kJErr;
+        if (err) atomicMin(first_err, ((unsigned int)r.line << 1) | (err == kJUnsup ? 1u : 0u));
       }
       continue;
     }
@@ -1252,7 +1314,7 @@ __global__ void __launch_bounds__(128, 8) js_prompt_kernel(const char* text, con
       if (want_arr) {
         arr_at = __shfl_sync(0xffffffffu, arr_at, 0);
         int64_t cnt = 0, endp = 0;
-        const int st = warp_int_array(t, arr_at + 1, r.e, nullptr, &cnt, &endp);
+        const int st = warp_count_array(t, arr_at + 1, r.e, &cnt, &endp);
         if (lane == 0) {
           if (st) {
             JIn it{t, arr_at, in.e};
@@ -1547,7 +1609,7 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
                 lbv, NB, NCH, d_ch, (const int64_t*)nullptr, (const int64_t*)nullptr, (char*)nullptr,
                 (int32_t*)nullptr, small + 2, 0);
     if (nkids > 0)
-      RS_LAUNCH(ctx, "jsonl_prompt_check", js_prompt_kernel<false>, wgrid(nkids), 128, 0, d_text, d_conts, cscan,
+      RS_LAUNCH(ctx, "jsonl_prompt_check", js_prompt_kernel<0>, wgrid(nkids), 128, 0, d_text, d_conts, cscan,
                 c0, nkids, lbv, NB, pc, d_ch, (const int64_t*)nullptr, (const int64_t*)nullptr, (char*)nullptr,
                 (int32_t*)nullptr, small + 2);
     // "prompts" as an object: nlohmann keeps the last member of each key; the
@@ -1597,17 +1659,32 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     clk.mark("lines + children");
     int64_t err_line = -1;
     int err_kind = 0;
-    for (int64_t ln = 0; ln < L; ++ln)
-      if (hl[ln].err) {
-        err_line = ln;
-        err_kind = hl[ln].err;
-        break;
+    auto first_error = [&]() {
+      err_line = -1;
+      err_kind = 0;
+      for (int64_t ln = 0; ln < L; ++ln)
+        if (hl[ln].err) {
+          err_line = ln;
+          err_kind = hl[ln].err;
+          break;
+        }
+      if (cerr != ~0u && (err_line < 0 || (int64_t)(cerr >> 1) < err_line)) {
+        err_line = cerr >> 1;
+        err_kind = (cerr & 1) ? kJUnsup : kJErr;
+      } else if (cerr != ~0u && (int64_t)(cerr >> 1) == err_line && err_kind == kJUnsup && !(cerr & 1)) {
+        err_kind = kJErr;
       }
-    if (cerr != ~0u && (err_line < 0 || (int64_t)(cerr >> 1) < err_line)) {
-      err_line = cerr >> 1;
-      err_kind = (cerr & 1) ? kJUnsup : kJErr;
-    } else if (cerr != ~0u && (int64_t)(cerr >> 1) == err_line && err_kind == kJUnsup && !(cerr & 1)) {
-      err_kind = kJErr;
+    };
+    first_error();
+    // pass 1 only sized the "token_ids" arrays: an error at or after the
+    // prompts' line waits for their check, which may report an earlier one
+    if (err_line >= 0 && nkids > 0 && err_line >= (int64_t)hc[pc].line) {
+      RS_LAUNCH(ctx, "jsonl_prompt_verify", js_prompt_kernel<1>, wgrid(nkids), 128, 0, d_text, d_conts, cscan,
+                c0, nkids, lbv, NB, pc, d_ch, (const int64_t*)nullptr, (const int64_t*)nullptr, (char*)nullptr,
+                (int32_t*)nullptr, small + 2);
+      RS_TRY(d2h(ctx, &cerr, small + 2, 4));
+      RS_TRY(sync_and_check(ctx));
+      first_error();
     }
     if (err_line >= 0)
       return trace_parse_error(err_line, err_kind == kJUnsup ? "JSON construct the device reader does not support"
@@ -1649,14 +1726,18 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     uint32_t* d_perm = (uint32_t*)carve(pb, abytes(P + 1, 4));
     int64_t maxid = 1;
     if (P > 0) {
-      RS_LAUNCH(ctx, "jsonl_prompt_write", js_prompt_kernel<true>, wgrid(nkids), 128, 0, d_text, d_conts, cscan,
+      RS_LAUNCH(ctx, "jsonl_prompt_write", js_prompt_kernel<2>, wgrid(nkids), 128, 0, d_text, d_conts, cscan,
                 c0, nkids, lbv, NB, pc, d_ch, (const int64_t*)id_off, (const int64_t*)int_off, d_ids, d_tok,
                 small + 2);
       RS_LAUNCH(ctx, "jsonl_prompt_tables", js_prompt_tables_kernel, grid(nkids + 1), 256, 0, d_ch, c0, nkids,
                 (const uint32_t*)kidx, (const int64_t*)id_off, (const int64_t*)int_off, p_id_off, p_tok_off, p_gt);
       std::vector<int64_t> ioff(P + 1);
       RS_TRY(d2h(ctx, ioff.data(), p_id_off, 8ull * (P + 1)));
+      RS_TRY(d2h(ctx, &cerr, small + 2, 4));
       RS_TRY(sync_and_check(ctx));
+      if (cerr != ~0u)  // a "token_ids" array pass 1 only sized (no other error is left)
+        return trace_parse_error(cerr >> 1, (cerr & 1) ? "JSON construct the device reader does not support"
+                                                       : "malformed JSON trace line");
       for (int32_t i = 0; i < P; ++i) maxid = std::max<int64_t>(maxid, ioff[i + 1] - ioff[i]);
     }
     RS_TRY(arena_reserve(ctx, rank_strings_device_bytes(std::max(P, 1), maxid) + (1 << 16)));

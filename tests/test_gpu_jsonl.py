@@ -303,3 +303,32 @@ def test_token_array_defects_fuzz():
             same(text)  # still valid JSON for the reference (e.g. a float)
         except OracleError:
             same_error(text)
+
+
+def test_token_array_defects_before_later_errors():
+    """The first pass only sizes "token_ids" (commas before the ']'); the
+    arrays are read in full later. A defect in the header's arrays must still
+    win over an error on a later line, and in "prompts" given as an object
+    only the surviving member's array counts."""
+    later = ['{"step":0 "lengths":{}}', '{"step":0,"lengths":{"zz":[1,2]}}', '{"step":0}']
+    defects = ["[1 2 3 4 5]", "[1,,2]", "[01]", "[1,2,]", "[,]", "[-]", "[1.]", "[ 1 2 ]"]
+    for d in defects:
+        for last in (False, True):
+            ps = [dict(p) for p in P2]
+            head = json.dumps(header(ps))
+            which = '[4]' if last else '[1, 2, 3]'
+            head = head.replace(which, d)
+            same_error((head + "\n").encode())
+            for step in later:
+                same_error((head + "\n" + step + "\n").encode())
+    pa = '{"id":"a","ground_truth_len":1,"token_ids":[1,2]}'
+    for d in defects:
+        bad = pa.replace("[1,2]", d)
+        same_error(('{"type":"header","g":1,"prompts":{"k":%s,"k":%s}}\n' % (pa, bad)).encode())
+        same_error(('{"type":"header","g":1,"prompts":{"k":%s,"k":%s}}\n' % (bad, pa)).encode())  # syntax
+        same_error(('{"type":"header","g":1,"prompts":{"k":%s,"j":%s}}\n{"step":0}\n' % (pa, bad)).encode())
+    # a dropped member's array with a type defect (valid JSON) is ignored
+    for d in ['["x"]', "[[1]]", "[null]", "[1,[2]]", "[{}]"]:
+        same(('{"type":"header","g":1,"prompts":{"k":%s,"k":%s}}\n' % (pa.replace("[1,2]", d), pa)).encode())
+        same_error(('{"type":"header","g":1,"prompts":{"k":%s,"k":%s}}\n{"step":0}\n'
+                    % (pa, pa.replace("[1,2]", d))).encode())
