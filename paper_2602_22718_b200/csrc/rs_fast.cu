@@ -122,7 +122,7 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
   // the sorting window afterwards
   extern __shared__ __align__(16) int32_t cur[];  // [kFastFmax + 2]
   uint16_t* skf = reinterpret_cast<uint16_t*>(cur + kBuildCur);
-  __shared__ int32_t wsum[32];
+  __shared__ int32_t wsum[32], wsum2[32];
   __shared__ long long wsum64[32];
   __shared__ int bad, s_nw;
   __shared__ int wb[kMaxWin + 1];  // window w = buckets [wb[w], wb[w + 1])
@@ -177,62 +177,67 @@ fast_build_kernel(GenSpec gs, const double* nz, const double* lnz, double* pred_
     if (tid == 0) atomicOr(flags, bad);
     return;
   }
-  // Descending exclusive scan over bins f = Fmax..1; thread t owns 16 bins.
-  constexpr int kPer = kFastFmax / kBuildT;
-  int cnt[kPer];
-  int csum = 0, nzc = 0;
-  long long cf = 0;
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    int f = kFastFmax - tid * kPer - j;
-    cnt[j] = cur[f];
-    csum += cnt[j];
-    nzc += cnt[j] ? 1 : 0;
-    cf += (long long)cnt[j] * f;
-  }
-  auto excl32 = [&](int v) -> int {
-    int incl = warp_incl_sum(v);
-    if (lane == 31) wsum[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-      int x = wsum[lane];
-      wsum[lane] = warp_incl_sum(x) - x;
-    }
-    __syncthreads();
-    int r = wsum[wid] + incl - v;
-    __syncthreads();
-    return r;
-  };
-  int start = excl32(csum);
-  int kbase = excl32(nzc);
-  long long cfb;
+  // Descending exclusive scans (records, non-empty buckets, count * f) over
+  // f = Fmax .. 1: warp w owns f in (Fmax - 512 (w + 1), Fmax - 512 w], round
+  // r lane l the bin Fmax - 512 w - 32 r - l (one bin per lane: the reads
+  // are conflict-free, where a thread owning 16 consecutive bins made them
+  // 16-way bank conflicts).
+  constexpr int kW = kBuildT / 32;
+  constexpr int kRounds = kFastFmax / kBuildT;
+  static_assert(kFastFmax % kBuildT == 0, "whole scan rounds per warp");
+  const int fw = kFastFmax - wid * (kFastFmax / kW) - lane;
   {
-    long long incl = warp_incl_sum(cf);
-    if (lane == 31) wsum64[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-      long long x = wsum64[lane];
-      wsum64[lane] = warp_incl_sum(x) - x;
+    int cs = 0, nzc = 0;
+    long long cf = 0;
+#pragma unroll 4
+    for (int r = 0; r < kRounds; ++r) {
+      const int f = fw - 32 * r;
+      const int c = cur[f];
+      cs += c;
+      nzc += c ? 1 : 0;
+      cf += (long long)c * f;
     }
-    __syncthreads();
-    cfb = wsum64[wid] + incl - cf;
+    cs = warp_sum(cs);
+    nzc = warp_sum(nzc);
+    cf = warp_sum(cf);
+    if (lane == 0) {
+      wsum[wid] = cs;
+      wsum2[wid] = nzc;
+      wsum64[wid] = cf;
+    }
+  }
+  __syncthreads();
+  int start = 0, kbase = 0;
+  long long cfb = 0;
+  {  // warp w's offsets: lanes < w of the warp totals
+    const int a = lane < wid ? wsum[lane] : 0, b = lane < wid ? wsum2[lane] : 0;
+    const long long c = lane < wid ? wsum64[lane] : 0;
+    start = warp_sum(a);
+    kbase = warp_sum(b);
+    cfb = warp_sum(c);
   }
   if (tid == kBuildT - 1) {
-    ss.nseg[s] = kbase + nzc;
-    ss.segCF[so + kbase + nzc] = cfb + cf;
+    const int D = kbase + wsum2[kW - 1];
+    ss.nseg[s] = D;
+    ss.segCF[so + D] = cfb + wsum64[kW - 1];
   }
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    int f = kFastFmax - tid * kPer - j;
-    cur[f] = start;
-    skf[f] = (uint16_t)kbase;
-    if (cnt[j]) {
-      ss.seg[so + kbase] = make_int2(f, start + cnt[j]);
-      ss.segCF[so + kbase] = cfb;
-      ++kbase;
+#pragma unroll 2
+  for (int r = 0; r < kRounds; ++r) {
+    const int f = fw - 32 * r;
+    const int c = cur[f];
+    const int nz1 = c ? 1 : 0;
+    const int ic = warp_incl_sum(c), in = warp_incl_sum(nz1);
+    const long long icf = warp_incl_sum((long long)c * f);
+    const int st = start + ic - c, kb = kbase + in - nz1;
+    cur[f] = st;
+    skf[f] = (uint16_t)kb;
+    if (c) {
+      ss.seg[so + kb] = make_int2(f, st + c);
+      ss.segCF[so + kb] = cfb + icf - (long long)c * f;
     }
-    start += cnt[j];
-    cfb += (long long)cnt[j] * f;
+    start += __shfl_sync(0xffffffffu, ic, 31);
+    kbase += __shfl_sync(0xffffffffu, in, 31);
+    cfb += __shfl_sync(0xffffffffu, icf, 31);
   }
   __syncthreads();
   RS_PH(1);
