@@ -1599,19 +1599,20 @@ __global__ void __launch_bounds__(kLsThreads, kMinB) lockstep2_kernel(LsArgs A) 
           } else if (cc >= tail_from) {
             rs = dmul((double)df, lds_f64(u_tail + 8u * (uint32_t)live));
           } else {  // tpot_context_run_sum (planner.cpp:61-84), piece by piece
+            // the clamped row (live == live_top, most runs) from shared memory
+            const bool top = kTopSmem && live >= live_top;
             const double* rp = rows_full + (live - 1) * ncm;
+            auto tv = [&](int x) -> double {
+              const int i = min(max(x, clo), chi) - clo;
+              return top ? lds_f64(u_top + 8u * (uint32_t)i) : __ldg(rp + i);
+            };
             const int c1 = base + f - 1;
             int x = cc;
             int pe = piece_end(s_pex, x, c1, clo1, chi);
-            rs = dmul(dmul((double)(pe - x + 1),
-                           dadd(__ldg(rp + min(max(x, clo), chi) - clo), __ldg(rp + min(max(pe, clo), chi) - clo))),
-                      0.5);
+            rs = dmul(dmul((double)(pe - x + 1), dadd(tv(x), tv(pe))), 0.5);
             for (x = pe + 1; x <= c1; x = pe + 1) {
               pe = piece_end(s_pex, x, c1, clo1, chi);
-              rs = dadd(rs, dmul(dmul((double)(pe - x + 1),
-                                      dadd(__ldg(rp + min(max(x, clo), chi) - clo),
-                                           __ldg(rp + min(max(pe, clo), chi) - clo))),
-                                 0.5));
+              rs = dadd(rs, dmul(dmul((double)(pe - x + 1), dadd(tv(x), tv(pe))), 0.5));
             }
           }
           total = dadd(total, rs);
