@@ -1459,6 +1459,107 @@ __global__ void js_lookup_kernel(const JChild* ch, const JCont* conts, int64_t t
   }
 }
 
+// ------------------------------------------------ steps on the device --
+// The step table without the host (WorkloadTrace::validate's step rules,
+// workload.cpp:53-91, over the reader's containers, :304-349): every step
+// line's "lengths" children and "scheduled" children become sort keys
+// (step line << 32 | prompt table index). Sorted (stable), the last lengths
+// child of each key is the one std::map keeps; the distinct keys of a line
+// are its lengths map in key order (= id order = table order). A valid step
+// has a scheduled list without repeats equal to that key set, g lengths per
+// key, each in [1, max_response_len]. Any deviation sets *bad and the host
+// path (which reproduces the reference's first error) runs instead.
+struct JStepLine {   // per step line, device copy
+  int32_t e_off;     // its first entry in the step table
+  int32_t sk_start;  // its first scheduled key in the sorted scheduled keys (-1: no "scheduled")
+  int32_t dk_start;  // its first distinct lengths key
+  int32_t pad;
+};
+
+__global__ void js_step_keys_kernel(const JChild* ch, const JCont* conts, const unsigned long long* cscan,
+                                    int64_t n, const int64_t* cbase, const int32_t* cstep, const int32_t* pidx,
+                                    uint64_t* lk, uint32_t* lv, uint64_t* sk, uint32_t* sv, int* bad) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+    const int c = ch[u].cont;
+    const int64_t b = cbase[c];
+    if (b < 0) continue;  // not the last "lengths" / "scheduled" of a step line
+    const int64_t i = b + (u - (int64_t)cscan[c]);
+    const int32_t p = pidx[u];
+    if (p < 0) atomicOr(bad, 1);  // an id outside the prompt table
+    const uint64_t key = ((uint64_t)cstep[c] << 32) | (uint32_t)max(p, 0);
+    if (conts[c].role == kRLengths) {
+      lk[i] = key;
+      lv[i] = (uint32_t)u;
+    } else {
+      sk[i] = key;
+      sv[i] = (uint32_t)(u - (int64_t)cscan[c]);
+    }
+  }
+}
+
+// flag the last child of each (line, key) run of the sorted lengths keys
+__global__ void js_step_ends_kernel(const uint64_t* k, int64_t n, uint32_t* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = (i == n - 1 || k[i + 1] != k[i]) ? 1u : 0u;
+}
+
+__global__ void js_step_distinct_kernel(const uint64_t* k, const uint32_t* v, const uint32_t* flag,
+                                        const uint32_t* pos, int64_t n, uint64_t* dk, uint32_t* dw,
+                                        int32_t* dcnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!flag[i]) continue;
+    dk[pos[i]] = k[i];
+    dw[pos[i]] = v[i];
+    atomicAdd(&dcnt[k[i] >> 32], 1);
+  }
+}
+
+// scheduled lines: no repeats, the same sorted keys as the line's lengths,
+// entries in batch order; lines without "scheduled": the keys in map order
+__global__ void js_step_entries_kernel(const uint64_t* sk, const uint32_t* sv, int64_t nsk, const uint64_t* dk,
+                                       const uint32_t* dw, int64_t nd, const JStepLine* sl, int32_t* e_prompt,
+                                       uint32_t* e_win, int* bad) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nsk + nd;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    if (j < nsk) {
+      const int s = (int)(sk[j] >> 32);
+      const JStepLine L = sl[s];
+      if (j > 0 && sk[j - 1] == sk[j]) atomicOr(bad, 2);  // scheduled twice
+      const int64_t d = L.dk_start + (j - L.sk_start);
+      if (dk[d] != sk[j]) atomicOr(bad, 4);  // lengths and scheduled differ
+      const int64_t e = L.e_off + sv[j];
+      e_prompt[e] = (int32_t)(sk[j] & 0xffffffffu);
+      e_win[e] = dw[d];
+    } else {
+      const int64_t d = j - nsk;
+      const int s = (int)(dk[d] >> 32);
+      const JStepLine L = sl[s];
+      if (L.sk_start >= 0) continue;
+      const int64_t e = L.e_off + (d - L.dk_start);
+      e_prompt[e] = (int32_t)(dk[d] & 0xffffffffu);
+      e_win[e] = dw[d];
+    }
+  }
+}
+
+__global__ void js_step_lengths_kernel(const uint32_t* e_win, int64_t ne, const unsigned long long* nint,
+                                       const unsigned long long* int_off, const int32_t* vals, int G, int max_r,
+                                       int32_t* lengths, int* bad) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = e_win[e];
+    if ((int64_t)nint[u] != G) {
+      atomicOr(bad, 8);
+      continue;
+    }
+    const int32_t* src = vals + int_off[u];
+    for (int i = 0; i < G; ++i) {
+      const int32_t l = src[i];
+      if (l < 1 || l > max_r) atomicOr(bad, 16);
+      lengths[e * G + i] = l;
+    }
+  }
+}
+
 // The header's prompts, in child order: their line-order tables for the
 // shared tail (token offsets, id offsets, ground truths).
 // (kidx: the prompt index of each member, nullptr when every child is one.)
@@ -1753,6 +1854,148 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     std::vector<int32_t> hp;  // per child: its index in the id-sorted table (-1: unknown)
     bool any_steps = false;
     for (int64_t ln = 0; ln < L; ++ln) any_steps |= hl[ln].kind == kLStep;
+    // The step table on the device (js_step_*_kernel). Sets steps_done when
+    // every step is of the valid form; otherwise the host path below runs
+    // (it reports the reference's first error). Errors returned here are
+    // CUDA / allocation failures only.
+    bool steps_done = false;
+    auto steps_device = [&](const int32_t* d_pidx, const int32_t* d_vals) -> int {
+      const int32_t G = tr->g;
+      if (G < 1) return RS_OK;
+      std::vector<int64_t> sc_of(L, -1), lc_of(L, -1);  // the last container of each role
+      for (int64_t c = 0; c < NC; ++c) {
+        if (hc[c].role == kRSched) sc_of[hc[c].line] = c;
+        if (hc[c].role == kRLengths) lc_of[hc[c].line] = c;
+      }
+      std::vector<int64_t> lines;
+      std::vector<int64_t> cbase(NC, -1);
+      std::vector<int32_t> cstep(NC, 0);
+      std::vector<JStepLine> sl;
+      int64_t nlk = 0, nsk = 0;
+      int prev = -1;
+      for (int64_t ln = 0; ln < L; ++ln) {
+        if (hl[ln].kind != kLStep) continue;
+        if (hl[ln].step <= prev) return RS_OK;  // not strictly increasing
+        prev = hl[ln].step;
+        const int64_t lc = lc_of[ln], sc = sc_of[ln];
+        if (lc < 0 || !hc[lc].is_obj || hcs[lc + 1] == hcs[lc]) return RS_OK;
+        const int32_t s = (int32_t)lines.size();
+        JStepLine x{0, -1, 0, 0};
+        if (hl[ln].has_sched) {
+          if (sc < 0 || hcs[sc + 1] == hcs[sc]) return RS_OK;
+          x.sk_start = (int32_t)nsk;
+          cbase[sc] = nsk;
+          cstep[sc] = s;
+          nsk += (int64_t)(hcs[sc + 1] - hcs[sc]);
+        }
+        cbase[lc] = nlk;
+        cstep[lc] = s;
+        nlk += (int64_t)(hcs[lc + 1] - hcs[lc]);
+        lines.push_back(ln);
+        sl.push_back(x);
+      }
+      const int64_t nsl = (int64_t)lines.size();
+      if (nsl == 0 || nlk >= INT32_MAX || nsk >= INT32_MAX) return RS_OK;
+      const int64_t nmax = std::max<int64_t>(nlk, nsk);
+      AsyncBuf b;
+      char* q = b.alloc<char>(ctx->stream, abytes(NC, 8) + abytes(NC, 4) + abytes(nlk, 8) * 2 + abytes(nlk, 4) * 4 +
+                                               abytes(nlk + 1, 4) + abytes(nsk + 1, 8) + abytes(nsk + 1, 4) +
+                                               2 * radix_sort_scratch_bytes64(nmax) + scan_scratch_bytes(nlk + 1, 4) +
+                                               abytes(nsl, 4) + abytes(nsl, sizeof(JStepLine)) + 64);
+      if (!q) return fail(RS_E_NOMEM, "jsonl steps: allocation failed");
+      int64_t* d_cbase = (int64_t*)carve(q, abytes(NC, 8));
+      int32_t* d_cstep = (int32_t*)carve(q, abytes(NC, 4));
+      uint64_t* lk = (uint64_t*)carve(q, abytes(nlk, 8));
+      uint64_t* dk = (uint64_t*)carve(q, abytes(nlk, 8));
+      uint32_t* lv = (uint32_t*)carve(q, abytes(nlk, 4));
+      uint32_t* dw = (uint32_t*)carve(q, abytes(nlk, 4));
+      uint32_t* flag = (uint32_t*)carve(q, abytes(nlk, 4));
+      uint32_t* e_win = (uint32_t*)carve(q, abytes(nlk, 4));  // entries <= distinct keys (checked below)
+      uint32_t* pos = (uint32_t*)carve(q, abytes(nlk + 1, 4));
+      uint64_t* sk = (uint64_t*)carve(q, abytes(nsk + 1, 8));
+      uint32_t* sv = (uint32_t*)carve(q, abytes(nsk + 1, 4));
+      char* sort1 = carve(q, radix_sort_scratch_bytes64(nmax));
+      char* sort2 = carve(q, radix_sort_scratch_bytes64(nmax));
+      uint32_t* spart = (uint32_t*)carve(q, scan_scratch_bytes(nlk + 1, 4));
+      int32_t* dcnt = (int32_t*)carve(q, abytes(nsl, 4));
+      JStepLine* d_sl = (JStepLine*)carve(q, abytes(nsl, sizeof(JStepLine)));
+      int* d_bad = (int*)carve(q, 64);
+      RS_TRY(h2d(ctx, d_cbase, cbase.data(), 8ull * NC));
+      RS_TRY(h2d(ctx, d_cstep, cstep.data(), 4ull * NC));
+      RS_CUDA_TRY(cudaMemsetAsync(dcnt, 0, 4ull * nsl, ctx->stream));
+      RS_CUDA_TRY(cudaMemsetAsync(d_bad, 0, 64, ctx->stream));
+      RS_LAUNCH(ctx, "jsonl_step_keys", js_step_keys_kernel, grid(NCH), 256, 0, d_ch, d_conts, cscan, NCH,
+                d_cbase, d_cstep, d_pidx, lk, lv, sk, sv, d_bad);
+      uint64_t *lks, *sks;
+      uint32_t *lvs, *svs;
+      RS_TRY(radix_sort_pairs(ctx, lk, lv, nlk, sort1, &lks, &lvs));
+      RS_TRY(radix_sort_pairs(ctx, sk, sv, nsk, sort2, &sks, &svs));
+      RS_LAUNCH(ctx, "jsonl_step_ends", js_step_ends_kernel, grid(nlk), 256, 0, lks, nlk, flag);
+      RS_TRY(exclusive_scan<uint32_t>(ctx, flag, pos, nlk, spart, pos + nlk));
+      RS_LAUNCH(ctx, "jsonl_step_distinct", js_step_distinct_kernel, grid(nlk), 256, 0, lks, lvs, flag, pos, nlk,
+                dk, dw, dcnt);
+      std::vector<int32_t> hcnt(nsl);
+      uint32_t nd = 0;
+      int bad = 0;
+      RS_TRY(d2h(ctx, hcnt.data(), dcnt, 4ull * nsl));
+      RS_TRY(d2h(ctx, &nd, pos + nlk, 4));
+      RS_TRY(d2h(ctx, &bad, d_bad, 4));
+      RS_TRY(sync_and_check(ctx));
+      if (bad) return RS_OK;
+      // entries per step: the scheduled list, or the keys
+      std::vector<int32_t> st_idx(nsl), e_off(nsl + 1, 0);
+      int64_t dks = 0;
+      for (int64_t s = 0; s < nsl; ++s) {
+        const int64_t ln = lines[s];
+        int64_t ne = hcnt[s];
+        if (hl[ln].has_sched) {
+          const int64_t sc = sc_of[ln];
+          if ((int64_t)(hcs[sc + 1] - hcs[sc]) != ne) return RS_OK;  // lengths do not cover the batch
+        }
+        sl[s].dk_start = (int32_t)dks;
+        sl[s].e_off = e_off[s];
+        dks += hcnt[s];
+        if ((int64_t)e_off[s] + ne >= INT32_MAX) return RS_OK;
+        e_off[s + 1] = (int32_t)(e_off[s] + ne);
+        st_idx[s] = hl[ln].step;
+      }
+      const int64_t ne = e_off[nsl];
+      if (dks != (int64_t)nd || ne > nlk) return RS_OK;
+      RS_TRY(h2d(ctx, d_sl, sl.data(), sizeof(JStepLine) * nsl));
+      int32_t *d_step_idx = nullptr, *d_entry_off = nullptr, *d_entry_prompt = nullptr, *d_lengths = nullptr;
+      auto release = [&]() {
+        for (int32_t* p : {d_step_idx, d_entry_off, d_entry_prompt, d_lengths})
+          if (p) cudaFreeAsync(p, ctx->stream);
+      };
+      if (cudaMallocAsync(&d_step_idx, 4ull * nsl, ctx->stream) != cudaSuccess ||
+          cudaMallocAsync(&d_entry_off, 4ull * (nsl + 1), ctx->stream) != cudaSuccess ||
+          cudaMallocAsync(&d_entry_prompt, 4ull * std::max<int64_t>(ne, 1), ctx->stream) != cudaSuccess ||
+          cudaMallocAsync(&d_lengths, 4ull * std::max<int64_t>(ne * G, 1), ctx->stream) != cudaSuccess) {
+        cudaGetLastError();
+        release();
+        return fail(RS_E_NOMEM, "trace step table allocation failed");
+      }
+      RS_LAUNCH(ctx, "jsonl_step_entries", js_step_entries_kernel, grid(nsk + nd), 256, 0, sks, svs, nsk, dk, dw,
+                (int64_t)nd, d_sl, d_entry_prompt, e_win, d_bad);
+      RS_LAUNCH(ctx, "jsonl_step_lengths", js_step_lengths_kernel, grid(ne), 256, 0, e_win, ne, nint, int_off,
+                d_vals, G, tr->max_response_len, d_lengths, d_bad);
+      RS_TRY(h2d(ctx, d_step_idx, st_idx.data(), 4ull * nsl));
+      RS_TRY(h2d(ctx, d_entry_off, e_off.data(), 4ull * (nsl + 1)));
+      RS_TRY(d2h(ctx, &bad, d_bad, 4));
+      RS_TRY(sync_and_check(ctx));
+      if (bad) {
+        release();
+        return RS_OK;
+      }
+      tr->n_steps = (int32_t)nsl;
+      tr->n_entries = ne;
+      tr->d_step_idx = d_step_idx;
+      tr->d_entry_off = d_entry_off;
+      tr->d_entry_prompt = d_entry_prompt;
+      tr->d_lengths = d_lengths;
+      steps_done = true;
+      return RS_OK;
+    };
     if (any_steps && NCH > 0) {
       const int smask = (1 << kRSched) | (1 << kRLengths);
       RS_TRY(sizes(smask));
@@ -1776,7 +2019,9 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
                 lbv, NB, NCH, d_ch, (const int64_t*)id_off, (const int64_t*)int_off, d_i, d_n, small + 2, smask);
       RS_LAUNCH(ctx, "jsonl_lookup", js_lookup_kernel, grid(NCH), 256, 0, d_ch, d_conts, NCH, smask,
                 (const int64_t*)id_off, d_i, d_sids, d_sid_off, P, d_pidx);
-      // one pinned staging area: sizes, table indices, id bytes, lengths
+      RS_TRY(steps_device(d_pidx, d_n));
+      if (steps_done) clk.mark("steps: device table");
+      if (!steps_done) {  // the host path: the records through one pinned staging area
       const size_t o_il = 0, o_ni = abytes(NCH, 8), o_p = 2 * abytes(NCH, 8), o_i = o_p + abytes(NCH, 4),
                    o_n = o_i + abytes(tt[0] + 1, 1), total_b = o_n + abytes(tt[1] + 1, 4);
       RS_TRY(pinned_reserve(ctx, total_b));
@@ -1800,181 +2045,184 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
         h_id_off[u + 1] = h_id_off[u] + h_il[u];
         h_int_off[u + 1] = h_int_off[u] + h_ni[u];
       }
+      }
       clk.mark("steps: device records");
     }
     // WorkloadTrace::validate: the prompt rules, then step by step
     RS_TRY(trace_validate_prompts(tr));
     clk.mark("prompt rules");
-    // per step line: its containers (the last of each role) and children
-    std::vector<int64_t> sched_c(L, -1), len_c(L, -1);
-    for (int64_t c = 0; c < NC; ++c) {
-      if (hc[c].role == kRSched) sched_c[hc[c].line] = c;
-      if (hc[c].role == kRLengths) len_c[hc[c].line] = c;
-    }
-    auto id_index = [&](const std::string& id) -> int32_t {  // in the id-sorted table
-      int32_t lo = 0, hi = tr->count;
-      while (lo < hi) {
-        const int32_t mid = (lo + hi) >> 1;
-        const std::string m(tr->ids.data() + tr->id_off[mid], tr->ids.data() + tr->id_off[mid + 1]);
-        if (m < id) lo = mid + 1;
-        else if (id < m) hi = mid;
-        else return mid;
+    if (!steps_done) {  // the host path (a deviation from the device path's valid form)
+      // per step line: its containers (the last of each role) and children
+      std::vector<int64_t> sched_c(L, -1), len_c(L, -1);
+      for (int64_t c = 0; c < NC; ++c) {
+        if (hc[c].role == kRSched) sched_c[hc[c].line] = c;
+        if (hc[c].role == kRLengths) len_c[hc[c].line] = c;
       }
-      return -1;
-    };
-    std::vector<int32_t> st_idx, e_off{0}, e_prompt, lens;
-    int prev_step = -1;
-    const int32_t G = tr->g;
-    // "lengths" given as an array: nlohmann's items() names the elements
-    // "0", "1", ...; their table indices are looked up here
-    std::vector<std::string> idx_key(any_steps ? NCH : 0);
-    for (int64_t c = 0; c < NC && any_steps; ++c)
-      if (hc[c].role == kRLengths && !hc[c].is_obj)
-        for (unsigned long long u = hcs[c]; u < hcs[c + 1]; ++u) {
-          idx_key[u] = std::to_string(u - hcs[c]);
-          hp[u] = id_index(idx_key[u]);
+      auto id_index = [&](const std::string& id) -> int32_t {  // in the id-sorted table
+        int32_t lo = 0, hi = tr->count;
+        while (lo < hi) {
+          const int32_t mid = (lo + hi) >> 1;
+          const std::string m(tr->ids.data() + tr->id_off[mid], tr->ids.data() + tr->id_off[mid + 1]);
+          if (m < id) lo = mid + 1;
+          else if (id < m) hi = mid;
+          else return mid;
         }
-    auto child_id = [&](unsigned long long u) {
-      if (!idx_key[u].empty()) return idx_key[u];
-      return std::string(h_ids.data() + h_id_off[u], h_ids.data() + h_id_off[u] + h_il[u]);
-    };
-    auto table_id = [&](int32_t p) {
-      return std::string(tr->ids.data() + tr->id_off[p], tr->ids.data() + tr->id_off[p + 1]);
-    };
-    // per prompt, stamped with the step line: its last lengths child, scheduled
-    std::vector<int64_t> last_u(std::max(P, 1), -1), stamp_len(std::max(P, 1), -1),
-        stamp_sched(std::max(P, 1), -1);
-    for (int64_t ln = 0; ln < L; ++ln) {
-      if (hl[ln].kind != kLStep) continue;
-      const int step = hl[ln].step;
-      const std::string sn = std::to_string(step);
-      if (step <= prev_step)
-        return fail(RS_E_VALIDATION, "step indices must be strictly increasing at step " + sn);
-      prev_step = step;
-      // the lengths map (std::map: key order, the last duplicate wins) by
-      // table index; a key outside the table takes the string path below
-      std::vector<int32_t> keys;
-      bool known = true;
-      if (len_c[ln] >= 0)
-        for (unsigned long long u = hcs[len_c[ln]]; u < hcs[len_c[ln] + 1] && known; ++u) {
-          const int32_t p = hp[u];
-          if (p < 0) {
-            known = false;
-            break;
+        return -1;
+      };
+      std::vector<int32_t> st_idx, e_off{0}, e_prompt, lens;
+      int prev_step = -1;
+      const int32_t G = tr->g;
+      // "lengths" given as an array: nlohmann's items() names the elements
+      // "0", "1", ...; their table indices are looked up here
+      std::vector<std::string> idx_key(any_steps ? NCH : 0);
+      for (int64_t c = 0; c < NC && any_steps; ++c)
+        if (hc[c].role == kRLengths && !hc[c].is_obj)
+          for (unsigned long long u = hcs[c]; u < hcs[c + 1]; ++u) {
+            idx_key[u] = std::to_string(u - hcs[c]);
+            hp[u] = id_index(idx_key[u]);
           }
-          if (stamp_len[p] != ln) {
-            stamp_len[p] = ln;
-            keys.push_back(p);
+      auto child_id = [&](unsigned long long u) {
+        if (!idx_key[u].empty()) return idx_key[u];
+        return std::string(h_ids.data() + h_id_off[u], h_ids.data() + h_id_off[u] + h_il[u]);
+      };
+      auto table_id = [&](int32_t p) {
+        return std::string(tr->ids.data() + tr->id_off[p], tr->ids.data() + tr->id_off[p + 1]);
+      };
+      // per prompt, stamped with the step line: its last lengths child, scheduled
+      std::vector<int64_t> last_u(std::max(P, 1), -1), stamp_len(std::max(P, 1), -1),
+          stamp_sched(std::max(P, 1), -1);
+      for (int64_t ln = 0; ln < L; ++ln) {
+        if (hl[ln].kind != kLStep) continue;
+        const int step = hl[ln].step;
+        const std::string sn = std::to_string(step);
+        if (step <= prev_step)
+          return fail(RS_E_VALIDATION, "step indices must be strictly increasing at step " + sn);
+        prev_step = step;
+        // the lengths map (std::map: key order, the last duplicate wins) by
+        // table index; a key outside the table takes the string path below
+        std::vector<int32_t> keys;
+        bool known = true;
+        if (len_c[ln] >= 0)
+          for (unsigned long long u = hcs[len_c[ln]]; u < hcs[len_c[ln] + 1] && known; ++u) {
+            const int32_t p = hp[u];
+            if (p < 0) {
+              known = false;
+              break;
+            }
+            if (stamp_len[p] != ln) {
+              stamp_len[p] = ln;
+              keys.push_back(p);
+            }
+            last_u[p] = (int64_t)u;
           }
-          last_u[p] = (int64_t)u;
+        // items() of an array runs in element order (an object's, in key order)
+        const bool arr = len_c[ln] >= 0 && !hc[len_c[ln]].is_obj;
+        if (known) {
+          const std::vector<int32_t> keys_items = arr ? keys : std::vector<int32_t>();
+          if ((int64_t)keys.size() * 16 > (int64_t)P) {  // dense: the stamps in table order
+            keys.clear();
+            for (int32_t p = 0; p < P; ++p)
+              if (stamp_len[p] == ln) keys.push_back(p);
+          } else {
+            std::sort(keys.begin(), keys.end());
+          }
+          std::vector<int32_t> sched;
+          std::vector<unsigned long long> sched_u;
+          if (hl[ln].has_sched && sched_c[ln] >= 0) {
+            for (unsigned long long u = hcs[sched_c[ln]]; u < hcs[sched_c[ln] + 1]; ++u) {
+              sched.push_back(hp[u]);
+              sched_u.push_back(u);
+            }
+          } else if (!hl[ln].has_sched) {
+            sched = arr ? keys_items : keys;
+          }
+          if (sched.empty()) return fail(RS_E_VALIDATION, "step " + sn + " schedules no prompts");
+          for (size_t i = 0; i < sched.size(); ++i) {
+            const int32_t p = sched[i];
+            if (p < 0)
+              return fail(RS_E_VALIDATION, "step " + sn + " schedules unknown prompt '" + child_id(sched_u[i]) + "'");
+            if (stamp_sched[p] == ln)
+              return fail(RS_E_VALIDATION, "step " + sn + " schedules prompt '" + table_id(p) + "' twice");
+            stamp_sched[p] = ln;
+          }
+          if (keys.size() != sched.size())
+            return fail(RS_E_VALIDATION, "step " + sn + " lengths do not cover the scheduled batch");
+          for (const int32_t p : keys) {
+            if (stamp_sched[p] != ln)
+              return fail(RS_E_VALIDATION, "step " + sn + " has lengths for unscheduled prompt '" + table_id(p) + "'");
+            const unsigned long long u = (unsigned long long)last_u[p];
+            if ((int)h_ni[u] != G)
+              return fail(RS_E_VALIDATION, "step " + sn + " prompt '" + table_id(p) + "' needs exactly " +
+                                               std::to_string(G) + " response lengths");
+            for (int64_t i = 0; i < (int64_t)h_ni[u]; ++i) {
+              const int l = h_ints[h_int_off[u] + i];
+              if (l < 1 || l > tr->max_response_len)
+                return fail(RS_E_VALIDATION, "step " + sn + " prompt '" + table_id(p) +
+                                                 "' response length out of range: " + std::to_string(l));
+            }
+          }
+          st_idx.push_back(step);
+          for (const int32_t p : sched) {
+            e_prompt.push_back(p);
+            const unsigned long long u = (unsigned long long)last_u[p];
+            lens.insert(lens.end(), h_ints.begin() + h_int_off[u], h_ints.begin() + h_int_off[u] + h_ni[u]);
+          }
+          e_off.push_back((int32_t)e_prompt.size());
+          continue;
         }
-      // items() of an array runs in element order (an object's, in key order)
-      const bool arr = len_c[ln] >= 0 && !hc[len_c[ln]].is_obj;
-      if (known) {
-        const std::vector<int32_t> keys_items = arr ? keys : std::vector<int32_t>();
-        if ((int64_t)keys.size() * 16 > (int64_t)P) {  // dense: the stamps in table order
-          keys.clear();
-          for (int32_t p = 0; p < P; ++p)
-            if (stamp_len[p] == ln) keys.push_back(p);
-        } else {
-          std::sort(keys.begin(), keys.end());
-        }
-        std::vector<int32_t> sched;
-        std::vector<unsigned long long> sched_u;
+        // a key outside the prompt table: the reference's containers verbatim
+        std::vector<std::string> sched;
+        std::map<std::string, std::vector<int>> lmap;
+        for (unsigned long long u = hcs[len_c[ln]]; u < hcs[len_c[ln] + 1]; ++u)
+          lmap[child_id(u)] = std::vector<int>(h_ints.begin() + h_int_off[u], h_ints.begin() + h_int_off[u] + h_ni[u]);
         if (hl[ln].has_sched && sched_c[ln] >= 0) {
-          for (unsigned long long u = hcs[sched_c[ln]]; u < hcs[sched_c[ln] + 1]; ++u) {
-            sched.push_back(hp[u]);
-            sched_u.push_back(u);
-          }
+          for (unsigned long long u = hcs[sched_c[ln]]; u < hcs[sched_c[ln] + 1]; ++u) sched.push_back(child_id(u));
         } else if (!hl[ln].has_sched) {
-          sched = arr ? keys_items : keys;
+          if (arr)
+            for (unsigned long long u = hcs[len_c[ln]]; u < hcs[len_c[ln] + 1]; ++u) sched.push_back(child_id(u));
+          else
+            for (const auto& kv : lmap) sched.push_back(kv.first);
         }
         if (sched.empty()) return fail(RS_E_VALIDATION, "step " + sn + " schedules no prompts");
-        for (size_t i = 0; i < sched.size(); ++i) {
-          const int32_t p = sched[i];
-          if (p < 0)
-            return fail(RS_E_VALIDATION, "step " + sn + " schedules unknown prompt '" + child_id(sched_u[i]) + "'");
-          if (stamp_sched[p] == ln)
-            return fail(RS_E_VALIDATION, "step " + sn + " schedules prompt '" + table_id(p) + "' twice");
-          stamp_sched[p] = ln;
+        std::set<std::string> seen;
+        for (const std::string& id : sched) {
+          if (id_index(id) < 0) return fail(RS_E_VALIDATION, "step " + sn + " schedules unknown prompt '" + id + "'");
+          if (!seen.insert(id).second)
+            return fail(RS_E_VALIDATION, "step " + sn + " schedules prompt '" + id + "' twice");
         }
-        if (keys.size() != sched.size())
+        if (lmap.size() != sched.size())
           return fail(RS_E_VALIDATION, "step " + sn + " lengths do not cover the scheduled batch");
-        for (const int32_t p : keys) {
-          if (stamp_sched[p] != ln)
-            return fail(RS_E_VALIDATION, "step " + sn + " has lengths for unscheduled prompt '" + table_id(p) + "'");
-          const unsigned long long u = (unsigned long long)last_u[p];
-          if ((int)h_ni[u] != G)
-            return fail(RS_E_VALIDATION, "step " + sn + " prompt '" + table_id(p) + "' needs exactly " +
+        for (const auto& kv : lmap) {
+          if (!seen.count(kv.first))
+            return fail(RS_E_VALIDATION, "step " + sn + " has lengths for unscheduled prompt '" + kv.first + "'");
+          if ((int)kv.second.size() != G)
+            return fail(RS_E_VALIDATION, "step " + sn + " prompt '" + kv.first + "' needs exactly " +
                                              std::to_string(G) + " response lengths");
-          for (int64_t i = 0; i < (int64_t)h_ni[u]; ++i) {
-            const int l = h_ints[h_int_off[u] + i];
+          for (int l : kv.second)
             if (l < 1 || l > tr->max_response_len)
-              return fail(RS_E_VALIDATION, "step " + sn + " prompt '" + table_id(p) +
+              return fail(RS_E_VALIDATION, "step " + sn + " prompt '" + kv.first +
                                                "' response length out of range: " + std::to_string(l));
-          }
         }
-        st_idx.push_back(step);
-        for (const int32_t p : sched) {
-          e_prompt.push_back(p);
-          const unsigned long long u = (unsigned long long)last_u[p];
-          lens.insert(lens.end(), h_ints.begin() + h_int_off[u], h_ints.begin() + h_int_off[u] + h_ni[u]);
+        return fail(RS_E_VALIDATION, "step " + sn + ": lengths key outside the prompt table");  // unreachable
+      }
+      clk.mark("steps (host)");
+      // the step table, owned by the handle
+      tr->n_steps = (int32_t)st_idx.size();
+      tr->n_entries = (int64_t)e_prompt.size();
+      tr->device = ctx->device;
+      if (tr->n_steps > 0) {
+        if (cudaMallocAsync(&tr->d_step_idx, 4ull * st_idx.size(), ctx->stream) != cudaSuccess ||
+            cudaMallocAsync(&tr->d_entry_off, 4ull * e_off.size(), ctx->stream) != cudaSuccess ||
+            cudaMallocAsync(&tr->d_entry_prompt, 4ull * std::max<size_t>(e_prompt.size(), 1), ctx->stream) != cudaSuccess ||
+            cudaMallocAsync(&tr->d_lengths, 4ull * std::max<size_t>(lens.size(), 1), ctx->stream) != cudaSuccess) {
+          cudaGetLastError();
+          return fail(RS_E_NOMEM, "trace step table allocation failed");
         }
-        e_off.push_back((int32_t)e_prompt.size());
-        continue;
+        RS_TRY(h2d(ctx, tr->d_step_idx, st_idx.data(), 4ull * st_idx.size()));
+        RS_TRY(h2d(ctx, tr->d_entry_off, e_off.data(), 4ull * e_off.size()));
+        RS_TRY(h2d(ctx, tr->d_entry_prompt, e_prompt.data(), 4ull * e_prompt.size()));
+        RS_TRY(h2d(ctx, tr->d_lengths, lens.data(), 4ull * lens.size()));
       }
-      // a key outside the prompt table: the reference's containers verbatim
-      std::vector<std::string> sched;
-      std::map<std::string, std::vector<int>> lmap;
-      for (unsigned long long u = hcs[len_c[ln]]; u < hcs[len_c[ln] + 1]; ++u)
-        lmap[child_id(u)] = std::vector<int>(h_ints.begin() + h_int_off[u], h_ints.begin() + h_int_off[u] + h_ni[u]);
-      if (hl[ln].has_sched && sched_c[ln] >= 0) {
-        for (unsigned long long u = hcs[sched_c[ln]]; u < hcs[sched_c[ln] + 1]; ++u) sched.push_back(child_id(u));
-      } else if (!hl[ln].has_sched) {
-        if (arr)
-          for (unsigned long long u = hcs[len_c[ln]]; u < hcs[len_c[ln] + 1]; ++u) sched.push_back(child_id(u));
-        else
-          for (const auto& kv : lmap) sched.push_back(kv.first);
-      }
-      if (sched.empty()) return fail(RS_E_VALIDATION, "step " + sn + " schedules no prompts");
-      std::set<std::string> seen;
-      for (const std::string& id : sched) {
-        if (id_index(id) < 0) return fail(RS_E_VALIDATION, "step " + sn + " schedules unknown prompt '" + id + "'");
-        if (!seen.insert(id).second)
-          return fail(RS_E_VALIDATION, "step " + sn + " schedules prompt '" + id + "' twice");
-      }
-      if (lmap.size() != sched.size())
-        return fail(RS_E_VALIDATION, "step " + sn + " lengths do not cover the scheduled batch");
-      for (const auto& kv : lmap) {
-        if (!seen.count(kv.first))
-          return fail(RS_E_VALIDATION, "step " + sn + " has lengths for unscheduled prompt '" + kv.first + "'");
-        if ((int)kv.second.size() != G)
-          return fail(RS_E_VALIDATION, "step " + sn + " prompt '" + kv.first + "' needs exactly " +
-                                           std::to_string(G) + " response lengths");
-        for (int l : kv.second)
-          if (l < 1 || l > tr->max_response_len)
-            return fail(RS_E_VALIDATION, "step " + sn + " prompt '" + kv.first +
-                                             "' response length out of range: " + std::to_string(l));
-      }
-      return fail(RS_E_VALIDATION, "step " + sn + ": lengths key outside the prompt table");  // unreachable
-    }
-    clk.mark("steps (host)");
-    // the step table, owned by the handle
-    tr->n_steps = (int32_t)st_idx.size();
-    tr->n_entries = (int64_t)e_prompt.size();
-    tr->device = ctx->device;
-    if (tr->n_steps > 0) {
-      if (cudaMallocAsync(&tr->d_step_idx, 4ull * st_idx.size(), ctx->stream) != cudaSuccess ||
-          cudaMallocAsync(&tr->d_entry_off, 4ull * e_off.size(), ctx->stream) != cudaSuccess ||
-          cudaMallocAsync(&tr->d_entry_prompt, 4ull * std::max<size_t>(e_prompt.size(), 1), ctx->stream) != cudaSuccess ||
-          cudaMallocAsync(&tr->d_lengths, 4ull * std::max<size_t>(lens.size(), 1), ctx->stream) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(RS_E_NOMEM, "trace step table allocation failed");
-      }
-      RS_TRY(h2d(ctx, tr->d_step_idx, st_idx.data(), 4ull * st_idx.size()));
-      RS_TRY(h2d(ctx, tr->d_entry_off, e_off.data(), 4ull * e_off.size()));
-      RS_TRY(h2d(ctx, tr->d_entry_prompt, e_prompt.data(), 4ull * e_prompt.size()));
-      RS_TRY(h2d(ctx, tr->d_lengths, lens.data(), 4ull * lens.size()));
     }
     // the id-ordered token CSR
     RS_TRY(trace_gather_csr(ctx, tr, d_tok, p_tok_off, d_perm));

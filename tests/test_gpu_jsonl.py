@@ -332,3 +332,23 @@ def test_token_array_defects_before_later_errors():
         same(('{"type":"header","g":1,"prompts":{"k":%s,"k":%s}}\n' % (pa.replace("[1,2]", d), pa)).encode())
         same_error(('{"type":"header","g":1,"prompts":{"k":%s,"k":%s}}\n{"step":0}\n'
                     % (pa, pa.replace("[1,2]", d))).encode())
+
+
+def test_step_table_built_on_the_device(monkeypatch, capfd):
+    """Valid steps (scheduled lists, key order, duplicate keys, several
+    steps) take the device step table; a deviation falls back to the host
+    path, which reports the reference's error."""
+    monkeypatch.setenv("RS_TRACE_PHASES", "1")
+    ok = [
+        ref().trace_convert(steps_trace(3, 60, 4, g=3)[0]),
+        lines(header(P2), {"step": 0, "lengths": {"b": [1, 2], "a": [3, 4], "b": [5, 6]}},
+              {"step": 7, "scheduled": ["b", "a"], "lengths": {"a": [1, 1], "b": [2, 2]}}),
+    ]
+    for text in ok:
+        capfd.readouterr()
+        same(text)
+        assert "steps: device table" in capfd.readouterr().err
+    for text in validation_errors()[:6]:
+        capfd.readouterr()
+        same_error(text)
+        assert "steps: device table" not in capfd.readouterr().err
