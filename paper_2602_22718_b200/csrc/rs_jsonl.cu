@@ -1895,7 +1895,7 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
         sl.push_back(x);
       }
       const int64_t nsl = (int64_t)lines.size();
-      if (nsl == 0 || nlk >= INT32_MAX || nsk >= INT32_MAX) return RS_OK;
+      if (nsl == 0 || nlk >= INT32_MAX || nsk >= INT32_MAX || NCH >= (int64_t)UINT32_MAX) return RS_OK;
       const int64_t nmax = std::max<int64_t>(nlk, nsk);
       AsyncBuf b;
       char* q = b.alloc<char>(ctx->stream, abytes(NC, 8) + abytes(NC, 4) + abytes(nlk, 8) * 2 + abytes(nlk, 4) * 4 +

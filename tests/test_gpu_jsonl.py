@@ -352,3 +352,67 @@ def test_step_table_built_on_the_device(monkeypatch, capfd):
         capfd.readouterr()
         same_error(text)
         assert "steps: device table" not in capfd.readouterr().err
+
+
+def fuzz_steps(seed, n_prompts=40, n_steps=12, g=3):
+    """A header of n_prompts and n_steps step lines, each a random batch
+    with a random perturbation (or none): a repeated, missing, extra or
+    unknown id, a wrong length count, a length out of range, duplicate
+    lengths keys (the last wins), "scheduled" absent or permuted, a step
+    index that does not increase."""
+    rng = np.random.RandomState(seed)
+    ids = [f"q{i:03d}" for i in range(n_prompts)]
+    prompts = [{"id": x, "ground_truth_len": 5, "token_ids": [1 + i, 2]} for i, x in enumerate(ids)]
+    out = [json.dumps(header(prompts, g=g, max_response_len=100))]
+    step = 0
+    for _ in range(n_steps):
+        step += int(rng.randint(1, 4))
+        k = int(rng.randint(1, 9))
+        batch = [ids[j] for j in rng.choice(n_prompts, k, replace=False)]
+        lens = {x: [int(v) for v in rng.randint(1, 101, g)] for x in batch}
+        sched = list(batch)
+        items = list(lens.items())
+        kind = int(rng.randint(0, 12)) if rng.rand() < 0.35 else -1
+        st = step
+        if kind == 0:
+            sched.append(sched[0])                       # scheduled twice
+        elif kind == 1 and len(sched) > 1:
+            sched.pop()                                  # lengths not scheduled
+        elif kind == 2:
+            sched.append("zz")                           # unknown id
+        elif kind == 3:
+            items[0] = (items[0][0], items[0][1][:-1])   # too few lengths
+        elif kind == 4:
+            items[-1] = (items[-1][0], [0] * g)          # out of range
+        elif kind == 5:
+            items[0] = (items[0][0], [101] * g)
+        elif kind == 6:
+            st = step - 3                                # not increasing
+        elif kind == 7:
+            items.append(("zz", [1] * g))                # unknown lengths key
+        elif kind == 8 and len(items) > 1:
+            items = items[:-1]                           # scheduled without lengths
+        body_items = ",".join(f'"{x}":{json.dumps(v)}' for x, v in items)
+        if kind == 9:                                    # duplicate key, the last one valid
+            body_items = f'"{items[0][0]}":[1],' + body_items
+        if kind == 10:                                   # duplicate key, the last one invalid
+            body_items = body_items + f',"{items[0][0]}":[0]'
+        s = '{"step":%d,' % st
+        if kind == 11:                                   # "scheduled" permuted or absent
+            rng.shuffle(sched)
+        if kind != 11 or rng.rand() < 0.5:
+            s += '"scheduled":%s,' % json.dumps(sched)
+        s += '"lengths":{%s}}' % body_items
+        out.append(s)
+    return ("\n".join(out) + "\n").encode()
+
+
+def test_step_table_fuzz():
+    for seed in range(40):
+        text = fuzz_steps(seed)
+        try:
+            ref().trace_steps(text, "jsonl")
+        except OracleError:
+            same_error(text)
+            continue
+        same(text)
