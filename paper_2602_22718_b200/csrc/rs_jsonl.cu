@@ -1088,21 +1088,42 @@ __device__ int warp_int_array(const unsigned char* t, int64_t p, int64_t e, int3
       else if ((C >> j) & 1) bad |= cls != kNum;
       else bad |= !(cls == kNum || cls == kStart);
     }
-    // numbers: each lane parses the ones starting in its bytes
+    // numbers: each lane parses the ones starting in its bytes. The digit
+    // run's length comes from the digit masks (this lane's and the next
+    // one's); up to 8 digits are read as one 8-byte window (three aligned
+    // words) and converted by SWAR multiply-adds, longer or unbounded runs
+    // (past the next lane, or past the step) byte by byte.
     const int ns = __popc(S);
     const int before_n = warp_incl_sum(ns) - ns;
+    const uint32_t Dnx = __shfl_down_sync(0xffffffffu, D, 1);
     if (!bad && ns) {
+      const uint32_t Dx = D | ((lane == 31 ? d_after : Dnx) << 16);
+      const int wend = lane == 31 ? 17 : 32;  // bits of Dx the masks cover
       uint32_t m = S;
       int idx = 0;
       while (m) {
         const int j = __ffs(m) - 1;
         m &= m - 1;
-        int64_t q = i + j;
-        const bool neg = t[q] == '-';
-        if (neg) ++q;
+        const int neg = (M >> j) & 1;
+        const int p0 = j + neg;
+        int nd = __ffs(~(Dx >> p0)) - 1;  // -1: the run fills the window
         unsigned long long v = 0;
-        int nd = 0;
-        for (; q < e && t[q] >= '0' && t[q] <= '9'; ++q, ++nd) v = v * 10u + (unsigned)(t[q] - '0');
+        if (nd >= 1 && nd <= 8 && p0 + nd < wend) {
+          const int64_t a = i + p0;
+          const uint32_t* wp = reinterpret_cast<const uint32_t*>(t + (a & ~(int64_t)3));
+          const uint32_t w0 = wp[0], w1 = wp[1], w2 = wp[2];
+          const int sh = (int)(a & 3) * 8;
+          unsigned long long x = ((unsigned long long)__funnelshift_r(w1, w2, sh) << 32) | __funnelshift_r(w0, w1, sh);
+          const int pad = 8 - nd;  // leading '0' bytes: the digits end at byte 7
+          if (pad) x = (x << (8 * pad)) | (0x3030303030303030ULL >> (8 * nd));
+          x = ((x & 0x0F0F0F0F0F0F0F0FULL) * 2561ULL) >> 8;
+          x = ((x & 0x00FF00FF00FF00FFULL) * 6553601ULL) >> 16;
+          v = ((x & 0x0000FFFF0000FFFFULL) * 42949672960001ULL) >> 32;
+        } else {
+          int64_t q = i + p0;
+          nd = 0;
+          for (; q < e && t[q] >= '0' && t[q] <= '9'; ++q, ++nd) v = v * 10u + (unsigned)(t[q] - '0');
+        }
         if (nd > 18) bad = true;
         if (out && !bad && k + before_n + idx < cap) out[k + before_n + idx] = (int32_t)(neg ? 0ULL - v : v);
         ++idx;
