@@ -173,37 +173,43 @@ __device__ __forceinline__ void outside(const unsigned char* t, int64_t n, int64
   *co &= out;
 }
 
+// (ncl: the word's closers outside strings, so the token pass can skip a
+// word that cannot come back to level 2 without reading it)
 __global__ void js_depth_kernel(const char* text, int64_t n, int64_t W, const uint8_t* tail,
-                                const uint32_t* qscan, unsigned long long* dd) {
+                                const uint32_t* qscan, unsigned long long* dd, uint8_t* ncl) {
   const unsigned char* t = reinterpret_cast<const unsigned char*>(text);
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
        w += (int64_t)gridDim.x * blockDim.x) {
     uint64_t op, cl, cm, co;
     outside(t, n, w, tail, qscan, &op, &cl, &cm, &co);
-    dd[w] = (unsigned long long)(long long)(__popcll((long long)op) - __popcll((long long)cl));
+    const int c = __popcll((long long)cl);
+    dd[w] = (unsigned long long)(long long)(__popcll((long long)op) - c);
+    ncl[w] = (uint8_t)c;
   }
 }
 
-// Tokens at level <= 1 (list A) and commas at level 2 (list B): counted
-// (write = false) or written at their scanned offsets. Level: an opener's
-// depth before it, a closer's depth after it, a comma's / colon's depth.
-template <bool kWrite>
+// Tokens at level <= 1 (list A) and commas at level 2 (list B), counted per
+// word; a word that holds any keeps them as two bit masks (ma / mb), which
+// js_tokens_expand_kernel turns into the lists at the scanned offsets (the
+// byte classes are computed once). Level: an opener's depth before it, a
+// closer's depth after it, a comma's / colon's depth.
 __global__ void js_tokens_kernel(const char* text, int64_t n, int64_t W, const uint8_t* tail,
-                                 const uint32_t* qscan, const unsigned long long* dscan,
-                                 uint32_t* ca, uint32_t* cb, const uint32_t* oa, const uint32_t* ob,
-                                 uint64_t* la, int64_t* lb) {
+                                 const uint32_t* qscan, const unsigned long long* dscan, const uint8_t* ncl,
+                                 uint32_t* ca, uint32_t* cb, uint64_t* ma, uint64_t* mb) {
   const unsigned char* t = reinterpret_cast<const unsigned char*>(text);
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
        w += (int64_t)gridDim.x * blockDim.x) {
+    long long d = (long long)dscan[w];
+    // no token of this word can come back to level 2 (the bulk of the text:
+    // the insides of token arrays at depth 4): not read at all
+    if (d - ncl[w] > 2) {
+      ca[w] = cb[w] = 0;
+      continue;
+    }
     uint64_t op, cl, cm, co;
     outside(t, n, w, tail, qscan, &op, &cl, &cm, &co);
-    long long d = (long long)dscan[w];
     uint64_t all = op | cl | cm | co;
-    // no token of this word can come back to level 2 (the bulk of the text:
-    // the insides of token arrays at depth 4)
-    if (d - __popcll((long long)cl) > 2) all = 0;
-    uint32_t na = 0, nb = 0;
-    const uint32_t a0 = kWrite ? oa[w] : 0, b0 = kWrite ? ob[w] : 0;
+    uint64_t a = 0, b = 0;
     while (all) {
       const int j = __ffsll((long long)all) - 1;
       all &= all - 1;
@@ -218,18 +224,35 @@ __global__ void js_tokens_kernel(const char* text, int64_t n, int64_t W, const u
       } else {
         lev = d;
       }
-      const int64_t pos = 64 * w + j;
-      if (lev >= 0 && lev <= 1) {
-        if (kWrite) la[a0 + na] = ((uint64_t)pos << 8) | t[pos];
-        ++na;
-      } else if (lev == 2 && (cm & bit)) {
-        if (kWrite) lb[b0 + nb] = pos;
-        ++nb;
-      }
+      if (lev >= 0 && lev <= 1) a |= bit;
+      else if (lev == 2 && (cm & bit)) b |= bit;
     }
-    if (!kWrite) {
-      ca[w] = na;
-      cb[w] = nb;
+    ca[w] = (uint32_t)__popcll((long long)a);
+    cb[w] = (uint32_t)__popcll((long long)b);
+    if (a | b) {
+      ma[w] = a;
+      mb[w] = b;
+    }
+  }
+}
+
+__global__ void js_tokens_expand_kernel(const char* text, int64_t W, const uint32_t* ca, const uint32_t* cb,
+                                        const uint64_t* ma, const uint64_t* mb, const uint32_t* oa,
+                                        const uint32_t* ob, uint64_t* la, int64_t* lb) {
+  const unsigned char* t = reinterpret_cast<const unsigned char*>(text);
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    if (!(ca[w] | cb[w])) continue;
+    uint64_t a = ma[w], b = mb[w];
+    uint32_t ia = oa[w], ib = ob[w];
+    while (a) {
+      const int64_t pos = 64 * w + __ffsll((long long)a) - 1;
+      a &= a - 1;
+      la[ia++] = ((uint64_t)pos << 8) | t[pos];
+    }
+    while (b) {
+      lb[ib++] = 64 * w + __ffsll((long long)b) - 1;
+      b &= b - 1;
     }
   }
 }
@@ -1623,7 +1646,7 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     // 1. structural index
     const int64_t W = std::max<int64_t>(1, (n_bytes + 63) / 64);
     AsyncBuf b_w;
-    const size_t wbytes = abytes(W, 1) + abytes(W + 1, 4) * 6 + abytes(W + 1, 8) * 2 +
+    const size_t wbytes = abytes(W, 1) * 2 + abytes(W + 1, 4) * 6 + abytes(W + 1, 8) * 4 +
                           scan_scratch_bytes(W + 1, 8) + abytes(8, 8);
     char* wb = b_w.alloc<char>(ctx->stream, wbytes);
     if (!wb) return fail(RS_E_NOMEM, "jsonl structural index: allocation failed");
@@ -1633,6 +1656,7 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
       return q;
     };
     uint8_t* tail = (uint8_t*)carve(wb, abytes(W, 1));
+    uint8_t* ncl = (uint8_t*)carve(wb, abytes(W, 1));
     uint32_t* qpar = (uint32_t*)carve(wb, abytes(W + 1, 4));
     uint32_t* qscan = (uint32_t*)carve(wb, abytes(W + 1, 4));
     uint32_t* ca = (uint32_t*)carve(wb, abytes(W + 1, 4));
@@ -1641,6 +1665,8 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     uint32_t* ob = (uint32_t*)carve(wb, abytes(W + 1, 4));
     auto* dd = (unsigned long long*)carve(wb, abytes(W + 1, 8));
     auto* dscan = (unsigned long long*)carve(wb, abytes(W + 1, 8));
+    uint64_t* ma = (uint64_t*)carve(wb, abytes(W + 1, 8));  // per word: list A / list B token masks
+    uint64_t* mb = (uint64_t*)carve(wb, abytes(W + 1, 8));
     auto* part64 = (unsigned long long*)carve(wb, scan_scratch_bytes(W + 1, 8));
     auto* small = (unsigned int*)carve(wb, abytes(8, 8));  // first line, #containers, first error, totals
     uint32_t* part32 = (uint32_t*)part64;
@@ -1648,11 +1674,10 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     RS_LAUNCH(ctx, "jsonl_bs", js_bs_kernel, gw, 256, 0, d_text, n_bytes, W, tail);
     RS_LAUNCH(ctx, "jsonl_quote", js_quote_kernel, gw, 256, 0, d_text, n_bytes, W, tail, qpar);
     RS_TRY(exclusive_scan<uint32_t>(ctx, qpar, qscan, W, part32, nullptr));
-    RS_LAUNCH(ctx, "jsonl_depth", js_depth_kernel, gw, 256, 0, d_text, n_bytes, W, tail, qscan, dd);
+    RS_LAUNCH(ctx, "jsonl_depth", js_depth_kernel, gw, 256, 0, d_text, n_bytes, W, tail, qscan, dd, ncl);
     RS_TRY(exclusive_scan<unsigned long long>(ctx, dd, dscan, W, part64, nullptr));
-    RS_LAUNCH(ctx, "jsonl_tok_count", js_tokens_kernel<false>, gw, 256, 0, d_text, n_bytes, W, tail,
-              qscan, dscan, ca, cb, (const uint32_t*)nullptr, (const uint32_t*)nullptr, (uint64_t*)nullptr,
-              (int64_t*)nullptr);
+    RS_LAUNCH(ctx, "jsonl_tok_count", js_tokens_kernel, gw, 256, 0, d_text, n_bytes, W, tail, qscan, dscan, ncl,
+              ca, cb, ma, mb);
     RS_TRY(exclusive_scan<uint32_t>(ctx, ca, oa, W, part32, oa + W));
     RS_TRY(exclusive_scan<uint32_t>(ctx, cb, ob, W, part32, ob + W));
     uint32_t tot[2];
@@ -1665,8 +1690,9 @@ extern "C" int rs_trace_csr_parse_jsonl(rs_ctx* ctx, const char* text, int64_t n
     if (!lbuf) return fail(RS_E_NOMEM, "jsonl token lists: allocation failed");
     uint64_t* la = (uint64_t*)carve(lbuf, abytes(NA + 1, 8));
     int64_t* lbv = (int64_t*)carve(lbuf, abytes(NB + 1, 8));
-    RS_LAUNCH(ctx, "jsonl_tok_write", js_tokens_kernel<true>, gw, 256, 0, d_text, n_bytes, W, tail,
-              qscan, dscan, ca, cb, (const uint32_t*)oa, (const uint32_t*)ob, la, lbv);
+    RS_LAUNCH(ctx, "jsonl_tok_write", js_tokens_expand_kernel, gw, 256, 0, d_text, W, (const uint32_t*)ca,
+              (const uint32_t*)cb, (const uint64_t*)ma, (const uint64_t*)mb, (const uint32_t*)oa, (const uint32_t*)ob,
+              la, lbv);
     clk.mark("structural index");
     // 2. lines
     const int64_t cont_cap = NA / 2 + 1;
