@@ -583,6 +583,25 @@ def bench_c3(args):
                              "kind": "reference", "sample": "one scale() call, 1 thread"}}
 
 
+def trace_parity(d_text, tok, off, fmt, n=65536, g=8, seed=1):
+    """One parse (outside the timed region) checked against what the text
+    encodes (tests/cases.py's generator): the id-sorted token CSR (ids
+    p000000.. sort in prompt order), and the step table — one step, the batch
+    in the generator's order with its g lengths per prompt."""
+    from paper_2602_22718_b200.rollsim import TraceCSR
+    tr = TraceCSR(d_text, device=True, fmt=fmt)
+    got, st = tr.host(), tr.steps()
+    rng = np.random.RandomState(seed + 1)
+    order = rng.permutation(n)
+    lens = rng.randint(1, 2049, (n, g))
+    ok = (np.array_equal(got["tokens"], tok) and np.array_equal(got["offsets"], off)
+          and st["step_idx"].tolist() == [0] and np.array_equal(st["entry_prompt"], order)
+          and np.array_equal(st["lengths"], lens))
+    del tr
+    return {"ok": bool(ok), "fields": "tokens, offsets, step entries and lengths bitwise",
+            "vs": "the generator of the text (tests/cases.py)"}
+
+
 def bench_trace(args, ctx, torch, dev):
     """the C2 batch written as a CSV trace (~1 GB of text,
     tests/cases.py c2_trace_text) -> id-sorted token CSR in HBM
@@ -627,6 +646,7 @@ def bench_trace(args, ctx, torch, dev):
     peak, _ = peaks()
     top = max(kt, key=kt.get)
     achieved = text.nbytes / (kt[top] / 1e3) / 1e9  # the dominant pass reads the text once
+    parity = trace_parity(d_text, tok, off, "csv")
     out = {"metric": "trace prompt-table parse tokens/sec (CSV -> device CSR)", "value": n_tok / dev_s,
            "unit": "tokens/s", "text_bytes": int(text.nbytes), "ms_per_parse": dev_s * 1e3,
            "config": {"workload": "C2 batch as CSV trace text: 65536 '# prompt' lines x 2560 tokens "
@@ -637,7 +657,8 @@ def bench_trace(args, ctx, torch, dev):
                         "frac": achieved / peak, "kernel": top,
                         "traffic": (_profile_traffic("trace_tokens_dram_bytes_per_launch")
                                     if top == "trace_tokens" else None),
-                        "launch_ms": kt[top], "kernel_ms": kt}}
+                        "launch_ms": kt[top], "kernel_ms": kt},
+           "parity": parity}
     if not args.no_cpu:
         from oracle_lib import ref
         R = ref()
@@ -661,7 +682,7 @@ def bench_trace_jsonl(args, ctx, torch, dev):
     on the same shape cut to 1,024 prompts."""
     from cases import c2_trace_jsonl
     from paper_2602_22718_b200.lib import check
-    text, tok, _ = c2_trace_jsonl()
+    text, tok, off = c2_trace_jsonl()
     n_tok = int(tok.size)
     d_text = torch.from_numpy(text).to(dev)
     h = C.c_void_p()
@@ -684,13 +705,15 @@ def bench_trace_jsonl(args, ctx, torch, dev):
     for _ in range(3):
         parse(pt.data_ptr(), 0)
     host_s = (time.perf_counter() - t0) / 3
+    parity = trace_parity(d_text, tok, off, "jsonl")
     out = {"metric": "trace JSONL parse tokens/sec (JSONL -> device CSR + step table)",
            "value": n_tok / dev_s, "unit": "tokens/s", "text_bytes": int(text.nbytes),
            "ms_per_parse": dev_s * 1e3,
            "config": {"workload": "C2 batch as a JSONL trace: one 65536-prompt header line x 2560 tokens "
                                   "+ one step of 65536 x 8 lengths"},
            "e2e": {"value": n_tok / host_s, "unit": "tokens/s", "h2d_bytes_per_step": int(text.nbytes),
-                   "d2h_bytes_per_step": 0}}
+                   "d2h_bytes_per_step": 0},
+           "parity": parity}
     if not args.no_cpu:
         from oracle_lib import ref
         R = ref()

@@ -14,5 +14,6 @@ import json, sys
 d = json.loads(open(sys.argv[1]).read())
 print({"value": d["value"], "e2e": d["e2e"]["value"], "frac": d["roofline"]["frac"],
        "parity": d["parity_sampled"], "c5": d["c5"]["value"], "trace": d["trace"]["value"],
-       "jsonl": d["trace"]["jsonl"]["value"], "clocks": d["clocks"]})
+       "jsonl": d["trace"]["jsonl"]["value"], "trace_parity": [d["trace"].get("parity"), d["trace"]["jsonl"].get("parity")],
+       "clocks": d["clocks"]})
 PY
