@@ -37,7 +37,6 @@ static_assert(kBlkPairs % 4 == 0, "bq rows are written as 64-bit words");
 __host__ __device__ constexpr int blk_pair(int i, int j) { return i * (2 * kBlk + 1 - i) / 2 + (j - i); }
 constexpr int kMaxSeg = kFastFmax; // D <= Fmax
 constexpr int kTopCap = 4096;      // smem tpot row entries
-constexpr int kCoopN = 4;         // N < kCoopN: warp-cooperative groups
 constexpr int kStBlocks = kMaxSeg / kBlk;  // 1024
 constexpr int kStLevels = 11;              // floor(log2(1024)) + 1
 constexpr int kStStride = kStBlocks * kStLevels;

@@ -654,7 +654,11 @@ static int build_batch(rs_ctx* ctx, int S, const int64_t* d_off, int64_t n, doub
   return RS_OK;
 }
 
-constexpr int kLockstepMinScenarios = 32;
+// Batches of fewer scenarios evaluate one group per lane / warp
+// (fast_eval): with its per-batch warp-cooperative threshold it beats the
+// lockstep walk (+ group table) up to ~50 C4-shaped scenarios (32: 1.55 vs
+// 1.93 ms, 48: 1.89 vs 2.02, 64: 2.24 vs 2.11, kernels of one batch).
+constexpr int kLockstepMinScenarios = 56;
 
 static int units_for(rs_ctx* ctx, int S, int C) {
   int want = (2 * ctx->num_sms + S - 1) / S;
@@ -675,7 +679,7 @@ static int eval_batch(rs_ctx* ctx, const Built& b, int S, const DevProfile& dp, 
     // Few scenarios: one group per lane, candidates split over CTAs.
     // the lockstep evaluator runs one CTA per scenario: even a partial wave
     // (a sweep's last batch) beats splitting candidates over CTAs from about
-    // 32 scenarios on
+    // 56 scenarios on (kLockstepMinScenarios)
     if (S >= kLockstepMinScenarios && lockstep_ok(dp, G)) {
       const bool f = fuse && fused && lockstep_fuses_select(cr);
       if (f) {
