@@ -1714,26 +1714,40 @@ int lockstep_slots(rs_ctx* ctx, const DevProfile& prof, int G) {
 bool lockstep_fuses_select(CandRange cr) { return cr.n_max - cr.n_min + 1 <= kLsThreads; }
 
 // ----------------------------------------------------------------- reduce --
+// One warp per (scenario, candidate): the group times are read 32 at a time;
+// the maximum (std::max over finite times) and the idle slot-ticks (int64)
+// are order-free warp reductions, the cost sum runs in group order on every
+// lane from shuffles (planner.cpp:148-157, 190-195).
 __global__ void fast_reduce_kernel(FastSS ss, int S, CandRange cr, double rho, int gpus,
                                    const double* gt, double* t_total, double* cost,
                                    int64_t* idle) {
   if (*ss.flags & kFastBad) return;
+  const int lane = threadIdx.x & 31;
   const int C = cr.n_max - cr.n_min + 1;
   const int64_t total = (int64_t)S * C;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
+  const double gd = (double)gpus;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < total;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int s = (int)(t / C), ci = (int)(t % C);
     const int N = cr.n_min + ci;
     const double* g = gt + (int64_t)s * cr.T + (tri64(N) - tri64(cr.n_min));
     double tt = 0.0, dollars = 0.0;
-    const double gd = (double)gpus;
-    for (int k = 0; k < N; ++k) {
-      const double v = g[k];
-      tt = tt < v ? v : tt;                             // std::max(t_total, t)
-      dollars = dadd(dollars, dmul(dmul(rho, v), gd));  // rho * t * gpu_count
+    for (int k0 = 0; k0 < N; k0 += 32) {
+      const double v = k0 + lane < N ? g[k0 + lane] : 0.0;
+      tt = tt < v ? v : tt;
+      const int n = min(32, N - k0);
+      for (int j = 0; j < n; ++j)
+        dollars = dadd(dollars, dmul(dmul(rho, __shfl_sync(0xffffffffu, v, j)), gd));  // rho * t * gpu_count
     }
-    t_total[t] = tt;
-    cost[t] = dollars;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double w = __shfl_xor_sync(0xffffffffu, tt, o);
+      tt = tt < w ? w : tt;
+    }
+    if (lane == 0) {
+      t_total[t] = tt;
+      cost[t] = dollars;
+    }
     if (idle) {
       const int64_t i0 = ss.item_off[s], so = i0 + s;
       const int P = (int)(ss.item_off[s + 1] - i0);
@@ -1745,22 +1759,23 @@ __global__ void fast_reduce_kernel(FastSS ss, int S, CandRange cr, double rho, i
         return ss.segCF[so + k] + (int64_t)(p - sk) * (ss.seg[so + k].x & 0xffff);
       };
       const int q = P / N, r = P % N;
-      int64_t acc = 0;
-      for (int k = 0; k < N; ++k) {
+      long long acc = 0;
+      for (int k = lane; k < N; k += 32) {
         const int a = k * q + min(k, r), b = a + q + (k < r ? 1 : 0);
         if (b <= a) continue;
         const int64_t fa = ss.seg[so + ss.rinfo[i0 + a].x].x & 0xffff;
         acc += (int64_t)(b - a) * fa - (cfpos(b) - cfpos(a));
       }
-      idle[t] = acc * cr.G;
+      acc = warp_sum(acc);
+      if (lane == 0) idle[t] = acc * cr.G;
     }
   }
 }
 
 int fast_reduce(rs_ctx* ctx, int S, const FastSS& ss, CandRange cr, double rho, int gpus,
                 const double* gt, double* t_total, double* cost, int64_t* idle) {
-  const int64_t n = (int64_t)S * (cr.n_max - cr.n_min + 1);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 127) / 128, 8 * ctx->num_sms));
+  const int64_t n = (int64_t)S * (cr.n_max - cr.n_min + 1);  // warps
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 3) / 4, 16 * ctx->num_sms));
   RS_LAUNCH(ctx, "candidate_reduce", fast_reduce_kernel, grid, 128, 0, ss, S, cr, rho, gpus, gt,
             t_total, cost, idle);
   return RS_OK;

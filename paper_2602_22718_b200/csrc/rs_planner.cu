@@ -347,41 +347,62 @@ __global__ void candidate_reduce_kernel(SSView ss, CandSpec cs, double rho,
 
 // Normalise + first strict argmin (planner.cpp:196-217), one thread per
 // scenario, sequential exactly like the reference.
+// One warp per scenario: the minima and maxima of t (t_total + penalty) and
+// cost are order-free over finite values; the first strict minimum of the
+// score (planner.cpp:210-214) is the lexicographic (score, index) minimum.
 __global__ void select_kernel(int S, int C, int n_min, double lambda,
                               const double* t_total, const double* t_pen,
                               const double* cost, double* t_norm,
                               double* c_norm, double* score, int32_t* n_star) {
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S;
-       s += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < S;
+       s += (gridDim.x * blockDim.x) >> 5) {
     const double* tt = t_total + (int64_t)s * C;
     const double* cc = cost + (int64_t)s * C;
     const double* tp = t_pen ? t_pen + (int64_t)s * C : nullptr;
-    double t_min = dadd(tt[0], tp ? tp[0] : 0.0);
+    double t_min = dadd(tt[0], tp ? tp[0] : 0.0);  // planner.cpp:196-205
     double t_max = t_min, c_min = cc[0], c_max = c_min;
-    for (int i = 0; i < C; ++i) {
-      double t = dadd(tt[i], tp ? tp[i] : 0.0);
+    for (int i = lane; i < C; i += 32) {
+      const double t = dadd(tt[i], tp ? tp[i] : 0.0);
       t_min = t < t_min ? t : t_min;
       t_max = t_max < t ? t : t_max;
       c_min = cc[i] < c_min ? cc[i] : c_min;
       c_max = c_max < cc[i] ? cc[i] : c_max;
     }
-    int best = 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double a = __shfl_xor_sync(0xffffffffu, t_min, o), b = __shfl_xor_sync(0xffffffffu, t_max, o);
+      const double c = __shfl_xor_sync(0xffffffffu, c_min, o), d = __shfl_xor_sync(0xffffffffu, c_max, o);
+      t_min = a < t_min ? a : t_min;
+      t_max = t_max < b ? b : t_max;
+      c_min = c < c_min ? c : c_min;
+      c_max = c_max < d ? d : c_max;
+    }
+    int best = INT32_MAX;
     double best_score = 0.0;
-    for (int i = 0; i < C; ++i) {
-      double t = dadd(tt[i], tp ? tp[i] : 0.0);
-      double tn = t_max > t_min ? ddiv(dsub(t, t_min), dsub(t_max, t_min)) : 0.0;
-      double cn = c_max > c_min ? ddiv(dsub(cc[i], c_min), dsub(c_max, c_min)) : 0.0;
-      double sc = dadd(dmul(lambda, tn), dmul(dsub(1.0, lambda), cn));
+    for (int i = lane; i < C; i += 32) {
+      const double t = dadd(tt[i], tp ? tp[i] : 0.0);
+      const double tn = t_max > t_min ? ddiv(dsub(t, t_min), dsub(t_max, t_min)) : 0.0;
+      const double cn = c_max > c_min ? ddiv(dsub(cc[i], c_min), dsub(c_max, c_min)) : 0.0;
+      const double sc = dadd(dmul(lambda, tn), dmul(dsub(1.0, lambda), cn));
       if (t_norm) t_norm[(int64_t)s * C + i] = tn;
       if (c_norm) c_norm[(int64_t)s * C + i] = cn;
       if (score) score[(int64_t)s * C + i] = sc;
-      if (i == 0) best_score = sc;
-      if (sc < best_score) {
+      if (best == INT32_MAX || sc < best_score) {  // ascending i per lane: first strict minimum
         best = i;
         best_score = sc;
       }
     }
-    n_star[s] = n_min + best;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double w = __shfl_xor_sync(0xffffffffu, best_score, o);
+      const int wi = __shfl_xor_sync(0xffffffffu, best, o);
+      if (wi != INT32_MAX && (best == INT32_MAX || w < best_score || (!(best_score < w) && wi < best))) {
+        best_score = w;
+        best = wi;
+      }
+    }
+    if (lane == 0) n_star[s] = n_min + best;
   }
 }
 
@@ -1004,7 +1025,7 @@ static int sweep_pass(rs_ctx* ctx, const rs_scenario_spec* spec, const double* h
       RS_TRY(reduce_batch(ctx, built, Sb, n_min, n_max, G, dp.rho, gpus, gt, o_tt, o_cc,
                           out->idle_slot_ticks ? o_idle : (int64_t*)nullptr));
     if (!fused_select)
-      RS_LAUNCH(ctx, "select", select_kernel, grid_for(ctx, Sb, 128), 128, 0, Sb, C, n_min,
+      RS_LAUNCH(ctx, "select", select_kernel, grid_for(ctx, (int64_t)Sb * 32, 128), 128, 0, Sb, C, n_min,
                 lambda, o_tt, (const double*)nullptr, o_cc, (double*)nullptr, (double*)nullptr,
                 (double*)nullptr, o_ns);
     RS_LAUNCH(ctx, "aggregate", aggregate_kernel, grid_for(ctx, (int64_t)C * 32, 256), 256, 0, Sb, C, n_min,
