@@ -28,16 +28,13 @@ struct SoA {
 
 SoA to_soa(const std::vector<PredictedPrompt>& predicted) {
   SoA s;
-  std::vector<std::string> ids;
   s.pred.reserve(predicted.size());
   s.plen.reserve(predicted.size());
-  ids.reserve(predicted.size());
   for (const PredictedPrompt& p : predicted) {
     s.pred.push_back(p.predicted_len);
     s.plen.push_back(p.prompt_len);
-    ids.push_back(p.id);
   }
-  s.rank = rs_shim::rank_ids(ids);
+  s.rank = rs_shim::rank_ids_by(predicted.size(), [&](size_t i) -> const std::string& { return predicted[i].id; });
   return s;
 }
 

@@ -59,18 +59,15 @@ Profile::Profile(const rollsim::LatencyProfile& lp) {
   p.rho = lp.rho;
 }
 
-std::vector<int32_t> rank_ids(const std::vector<std::string>& ids) {
-  std::vector<int64_t> off(ids.size() + 1, 0);
-  std::string bytes;
-  for (size_t i = 0; i < ids.size(); ++i) {
-    bytes += ids[i];
-    off[i + 1] = static_cast<int64_t>(bytes.size());
-  }
-  std::vector<int32_t> rank(ids.size());
-  if (!ids.empty())
-    check(rs_rank_strings(ctx(), bytes.data(), off.data(), static_cast<int32_t>(ids.size()),
-                          rank.data()));
+std::vector<int32_t> rank_ids_flat(const std::string& bytes, const std::vector<int64_t>& off) {
+  const size_t n = off.empty() ? 0 : off.size() - 1;
+  std::vector<int32_t> rank(n);
+  if (n) check(rs_rank_strings(ctx(), bytes.data(), off.data(), static_cast<int32_t>(n), rank.data()));
   return rank;
+}
+
+std::vector<int32_t> rank_ids(const std::vector<std::string>& ids) {
+  return rank_ids_by(ids.size(), [&](size_t i) -> const std::string& { return ids[i]; });
 }
 
 namespace {

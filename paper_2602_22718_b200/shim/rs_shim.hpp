@@ -29,6 +29,22 @@ struct Profile {
 
 // Rank of every id under std::string ordering, computed on the device.
 std::vector<int32_t> rank_ids(const std::vector<std::string>& ids);
+// The same for n ids given by id_of(i) (a const std::string&), without
+// copying them into a vector first.
+std::vector<int32_t> rank_ids_flat(const std::string& bytes, const std::vector<int64_t>& off);
+template <class F>
+std::vector<int32_t> rank_ids_by(size_t n, F id_of) {
+  size_t total = 0;
+  for (size_t i = 0; i < n; ++i) total += id_of(i).size();
+  std::string bytes;
+  bytes.reserve(total);
+  std::vector<int64_t> off(n + 1, 0);
+  for (size_t i = 0; i < n; ++i) {
+    bytes += id_of(i);
+    off[i + 1] = static_cast<int64_t>(bytes.size());
+  }
+  return rank_ids_flat(bytes, off);
+}
 
 // A token CSR resident in HBM (rs_trace_csr_device). PrefixIndex::build has
 // the reference's signature (host prompt pointers); b200::DeviceTrace hands
