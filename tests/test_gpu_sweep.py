@@ -247,3 +247,11 @@ def test_sweep_multi_batch_pinned_outputs():
     assert np.array_equal(bits(t["t_total"].numpy().reshape(S, Cn)), bits(tt))
     assert np.array_equal(bits(t["cost"].numpy().reshape(S, Cn)), bits(cc))
     assert np.array_equal(t["n_star"].numpy(), ns)
+
+
+def test_sweep_evaluator_thresholds_bitwise():
+    """Both sides of the small-batch evaluator's thresholds (fast_eval with
+    every group per warp up to 8 scenarios, N < 128 per warp above, the
+    lockstep walk from 56): same bits as the oracle, candidates past 128."""
+    for S in (8, 9, 55, 56):
+        check_sweep(c4_spec(S, count=4096, first=300 + S), 1, 160)
