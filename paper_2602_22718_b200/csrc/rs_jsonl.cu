@@ -1174,6 +1174,12 @@ __device__ int warp_int_array(const unsigned char* t, int64_t p, int64_t e, int3
 // same bytes with warp_int_array and reports what it rejects. Returns 1 (the
 // caller's serial path decides) when a '[', '{' or '"' comes before the ']'
 // or there is no ']' before e: there the first ']' need not be the array's.
+// 0x80 in every byte of x equal to the matching byte of c (exact per byte)
+__device__ __forceinline__ uint32_t byte_eq(uint32_t x, uint32_t c) {
+  const uint32_t y = x ^ c;
+  return ~(((y & 0x7f7f7f7fu) + 0x7f7f7f7fu) | y | 0x7f7f7f7fu);
+}
+
 __device__ int warp_count_array(const unsigned char* t, int64_t p, int64_t e, int64_t* count, int64_t* end) {
   const int lane = threadIdx.x & 31;
   int64_t commas = 0;
@@ -1181,6 +1187,29 @@ __device__ int warp_count_array(const unsigned char* t, int64_t p, int64_t e, in
   for (int64_t b0 = p & ~(int64_t)15;; b0 += 512) {
     if (b0 >= e) return 1;
     const int64_t i = b0 + 16 * lane;
+    if (b0 >= p && b0 + 512 <= e) {
+      // a whole step inside the span: byte flags (the high bit of each
+      // matching byte), no bit packing; a step holding the ']' is redone
+      // below with positions
+      const uint4 v = *reinterpret_cast<const uint4*>(t + i);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      uint32_t fe = 0, fq = 0, fnb = 0;
+      int nc = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t x = w[q];
+        fe |= byte_eq(x, 0x5d5d5d5du);
+        fq |= byte_eq(x, 0x5b5b5b5bu) | byte_eq(x, 0x7b7b7b7bu) | byte_eq(x, 0x22222222u);
+        nc += __popc(byte_eq(x, 0x2c2c2c2cu));
+        fnb |= __vcmpgtu4(x, 0x20202020u);  // above ' ': not blank (blank bytes are <= ' ')
+      }
+      if (!__any_sync(0xffffffffu, fe != 0)) {
+        if (__any_sync(0xffffffffu, fq != 0)) return 1;
+        commas += __reduce_add_sync(0xffffffffu, (unsigned)nc);
+        nonblank |= __any_sync(0xffffffffu, fnb != 0);
+        continue;
+      }
+    }
     uint32_t C = 0, E = 0, W = 0, Q = 0;
     {
       const uint4 v = *reinterpret_cast<const uint4*>(t + i);
