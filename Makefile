@@ -62,7 +62,7 @@ SUITES    := acceptance_main test_dedup test_planner test_profile test_training
 .PHONY: shim
 shim: $(foreach t,$(SUITES),$(SHIM_OUT)/$(t)_b200 $(SHIM_OUT)/$(t)_ref) \
       $(SHIM_OUT)/test_placement_b200 $(SHIM_OUT)/test_trace_b200 $(SHIM_OUT)/c5_bench_b200 $(SHIM_OUT)/c5_bench_ref \
-      $(SHIM_OUT)/c5_bench_train $(SHIM_OUT)/test_training_train \
+      $(SHIM_OUT)/c5_bench_train $(SHIM_OUT)/test_training_train $(SHIM_OUT)/test_simulator_train \
       $(SHIM_OUT)/c3_bench_b200 $(SHIM_OUT)/c3_bench_ref
 
 # C3 driver (shim/tools/c3_bench.cpp): scale() at 64K x G=8, N in [1, 512]
@@ -110,6 +110,11 @@ $(SHIM_OUT)/librollsim_b200_train.a: $(SHIM_OBJS) $(SHIM_OUT)/training_b200.o $(
 $(SHIM_OUT)/c5_bench_train: $(PKG)/shim/tools/c5_bench.cpp $(SHIM_OUT)/librollsim_b200_train.a $(LIB)
 	$(CXXREF) $< -o $@ $(SHIM_OUT)/librollsim_b200_train.a -L$(PKG) -lrs_b200 \
 	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -lpthread
+
+# the reference's own simulator suite against the patched simulator.cpp
+$(SHIM_OUT)/test_simulator_train: $(REF)/tests/test_simulator.cpp $(SHIM_OUT)/librollsim_b200_train.a $(LIB)
+	$(CXXREF) -I$(PKG)/shim/doctest $< -o $@ $(SHIM_OUT)/librollsim_b200_train.a \
+	    -L$(PKG) -lrs_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -lpthread
 
 # the reference's own training suite against the patched training.cpp
 $(SHIM_OUT)/test_training_train: $(REF)/tests/test_training.cpp $(SHIM_OUT)/librollsim_b200_train.a $(LIB)

@@ -106,3 +106,12 @@ def test_reference_training_suite_on_patched_training():
     code, out = run(SHIM / "test_training_train")
     assert "test cases:" in out, out[-3000:]
     assert failed_cases(out) == KNOWN_REF_FAILURES.get("test_training", set()), out[-3000:]
+
+
+@pytest.mark.gpu
+def test_reference_simulator_suite_on_patched_simulator():
+    """The reference's test_simulator.cpp against the patched simulator.cpp
+    (lazy ticks, skipped dispatch passes): every case passes."""
+    code, out = run(SHIM / "test_simulator_train")
+    assert "test cases:" in out, out[-3000:]
+    assert failed_cases(out) == KNOWN_REF_FAILURES.get("test_simulator", set()), out[-3000:]
