@@ -26,5 +26,5 @@ ncu --set full --clock-control none --import-source on \
     -o $out/${tag}_trace python tools/prof_trace.py > $out/${tag}_ncu_trace.log 2>&1
 python tools/prof_trace.py jsonl > $out/${tag}_jsonl_plain.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k "regex:js_prompt_kernel|js_tokens_kernel|js_depth_kernel|js_child_kernel" -c 5 \
+    -k "regex:js_prompt_kernel|js_tokens_kernel|js_depth_kernel|js_child_kernel|js_step" -c 7 \
     -o $out/${tag}_jsonl python tools/prof_trace.py jsonl > $out/${tag}_ncu_jsonl.log 2>&1 || true
