@@ -15,11 +15,12 @@
 // eval   (persistent CTAs, one scenario's segment table staged in shared
 //        memory, 16-segment block maxima + sparse table for prefix-max
 //        queries, the clamped-batch tpot row and piece ends in shared
-//        memory): candidate groups with N >= 8 run one group per LANE, the
-//        lane walking its runs in ascending finish order and accumulating
-//        the FP64 total sequentially (exactly the reference order); the few
-//        huge groups (N < 8) run warp-cooperatively, 32 runs per step, the
-//        lane sums added in lane order by one lane.
+//        memory): candidate groups with N >= coop_n run one group per LANE,
+//        the lane walking its runs in ascending finish order and accumulating
+//        the FP64 total sequentially (exactly the reference order); groups
+//        with N < coop_n (per batch size: fast_eval_coop_n) run
+//        warp-cooperatively, 32 runs per step, the lane sums added in lane
+//        order by one lane.
 // reduce per (scenario, candidate): max / sequential cost sum / idle.
 #include <algorithm>
 #include <cmath>
